@@ -1,0 +1,161 @@
+"""Seeded synthetic input generators shared by the oracle tests, the GPU tests and bench.py.
+
+This module holds NO arithmetic of the MoE method (no gating, routing, FFN,
+combine or placement).  It only draws random tensors with the shapes and value
+distributions of the paper's workloads and holds the
+config table from BASELINE.json.  Both ``oracle/`` and the CUDA path receive
+the same arrays from here; neither imports the other.
+
+Families
+--------
+grid      : every value on {k/64 : |k| <= 31} (expert weights additionally /8).
+            Exact in bf16, and every fp32 gate logit is exact under any
+            summation order, so routing parity is bit-exact.
+balanced  : X ~ N(0,1), Wg ~ N(0,1/d), W1 ~ N(0,1/d), W2 ~ N(0,1/f): near-uniform
+            routing, as in training ("nearly the same across all experts",
+            PAPER.md:243 §2.2).
+zipf      : z_t ~ Zipf(s) over experts, X_t = 6 u_{z_t} + N(0, I), Wg[:, e] = u_e.
+            Reproduces the skewed inference popularity of PAPER.md:243 (§2.2).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+# ----------------------------------------------------------------------------
+# Config table (BASELINE.json "configs"; SURVEY.md §8 glossary).  Values marked
+# "proposed" in SURVEY.md §8 are the readings recorded in DESIGN.md.
+# ----------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class LayerConfig:
+    name: str
+    num_experts: int      # E (global)
+    k: int                # top-k
+    d_model: int          # d
+    d_ffn: int            # f
+    tokens_per_rank: int  # T
+    cf: float | None      # capacity factor; None => dropless (C = T)
+    dtype: str            # "f32" | "bf16"
+
+    def capacity(self) -> int:
+        """C = ceil(cf * k * T / E) slots per expert per source rank (R5)."""
+        if self.cf is None:
+            return self.tokens_per_rank
+        return int(math.ceil(self.cf * self.k * self.tokens_per_rank / self.num_experts))
+
+
+CONFIGS = {
+    # configs[0]: tiny, fp32, CPU oracle in seconds.  cf=1.0 gives drops.
+    "C1": LayerConfig("C1-tiny", 4, 1, 64, 256, 512, 1.0, "f32"),
+    # configs[1]: GPT-2-small-shaped, 8 experts (1/GPU at 8 GPUs), top-2, d=768, 8K tok/GPU, bf16.
+    "C2": LayerConfig("C2-gpt2s", 8, 2, 768, 3072, 8192, 1.25, "bf16"),
+    # configs[2]: BERT-large-shaped, 16 experts, top-2, d=1024, capacity 1.25.
+    "C3": LayerConfig("C3-bertl", 16, 2, 1024, 4096, 8192, 1.25, "bf16"),
+    # configs[3]: Transformer-XL-shaped inference, 32 experts, top-1, dropless.
+    "C4": LayerConfig("C4-txl-inf", 32, 1, 1024, 4096, 4096, None, "bf16"),
+    # configs[4]: scale sweep.
+    "C5": LayerConfig("C5-scale", 64, 2, 2048, 8192, 32768, 1.25, "bf16"),
+}
+
+
+# ----------------------------------------------------------------------------
+# Random draws
+# ----------------------------------------------------------------------------
+
+
+def _rng(seed: int, *stream: int) -> np.random.Generator:
+    return np.random.default_rng(np.random.SeedSequence([int(seed), *[int(s) for s in stream]]))
+
+
+def bf16_representable(a: np.ndarray) -> np.ndarray:
+    """Round float32 data to the nearest bf16 value (RNE), returned as float32.
+
+    Data preparation only: makes a random draw storable in bf16 without loss, so
+    both sides start from identical values.
+    """
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    u = (u + 0x7FFF + lsb) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+def grid(rng: np.random.Generator, shape, scale: float = 1.0) -> np.ndarray:
+    """Uniform on {k/64 : |k| <= 31} * scale (scale a power of two keeps bf16 exactness)."""
+    k = rng.integers(-31, 32, size=shape, dtype=np.int64)
+    return (k.astype(np.float64) / 64.0 * scale).astype(np.float32)
+
+
+TENSOR_IDS = {"X": 1, "Wg": 2, "W1": 3, "W2": 4, "dY": 5, "zipf": 6}
+
+
+def layer_weights(cfg: LayerConfig, seed: int, family: str = "grid"):
+    """Global weights, identical on every rank: Wg [d,E] fp32, W1 [E,f,d], W2 [E,d,f]."""
+    d, f, E = cfg.d_model, cfg.d_ffn, cfg.num_experts
+    if family == "grid":
+        Wg = grid(_rng(seed, TENSOR_IDS["Wg"]), (d, E))
+        W1 = grid(_rng(seed, TENSOR_IDS["W1"]), (E, f, d), 1.0 / 8)
+        W2 = grid(_rng(seed, TENSOR_IDS["W2"]), (E, d, f), 1.0 / 8)
+    elif family == "balanced":
+        Wg = (_rng(seed, TENSOR_IDS["Wg"]).standard_normal((d, E)) / math.sqrt(d)).astype(np.float32)
+        W1 = (_rng(seed, TENSOR_IDS["W1"]).standard_normal((E, f, d), dtype=np.float32) / np.float32(math.sqrt(d)))
+        W2 = (_rng(seed, TENSOR_IDS["W2"]).standard_normal((E, d, f), dtype=np.float32) / np.float32(math.sqrt(f)))
+    elif family == "zipf":
+        U = _zipf_directions(cfg, seed)
+        Wg = np.ascontiguousarray(U.T).astype(np.float32)
+        W1 = (_rng(seed, TENSOR_IDS["W1"]).standard_normal((E, f, d), dtype=np.float32) / np.float32(math.sqrt(d)))
+        W2 = (_rng(seed, TENSOR_IDS["W2"]).standard_normal((E, d, f), dtype=np.float32) / np.float32(math.sqrt(f)))
+    else:
+        raise ValueError(f"unknown family {family!r}")
+    if cfg.dtype == "bf16":
+        W1 = bf16_representable(W1)
+        W2 = bf16_representable(W2)
+    return Wg, W1, W2
+
+
+def _zipf_directions(cfg: LayerConfig, seed: int) -> np.ndarray:
+    U = _rng(seed, TENSOR_IDS["zipf"], 0).standard_normal((cfg.num_experts, cfg.d_model))
+    U /= np.linalg.norm(U, axis=1, keepdims=True)
+    return U
+
+
+def zipf_probs(E: int, s: float) -> np.ndarray:
+    w = 1.0 / np.arange(1, E + 1, dtype=np.float64) ** s
+    return w / w.sum()
+
+
+def layer_tokens(cfg: LayerConfig, seed: int, rank: int, family: str = "grid",
+                 zipf_s: float = 1.0, num_tokens: int | None = None):
+    """Per-rank tokens X [T,d] and upstream gradient dY [T,d] (bf16-representable when dtype=bf16)."""
+    T = cfg.tokens_per_rank if num_tokens is None else num_tokens
+    d = cfg.d_model
+    if family == "grid":
+        X = grid(_rng(seed, TENSOR_IDS["X"], rank), (T, d))
+        dY = grid(_rng(seed, TENSOR_IDS["dY"], rank), (T, d))
+    elif family == "balanced":
+        X = _rng(seed, TENSOR_IDS["X"], rank).standard_normal((T, d), dtype=np.float32)
+        dY = _rng(seed, TENSOR_IDS["dY"], rank).standard_normal((T, d), dtype=np.float32)
+    elif family == "zipf":
+        rng = _rng(seed, TENSOR_IDS["X"], rank)
+        U = _zipf_directions(cfg, seed)
+        z = rng.choice(cfg.num_experts, size=T, p=zipf_probs(cfg.num_experts, zipf_s))
+        X = (6.0 * U[z] + rng.standard_normal((T, d))).astype(np.float32)
+        dY = _rng(seed, TENSOR_IDS["dY"], rank).standard_normal((T, d), dtype=np.float32)
+    else:
+        raise ValueError(f"unknown family {family!r}")
+    if cfg.dtype == "bf16":
+        X = bf16_representable(X)
+        dY = bf16_representable(dY)
+    return X, dY
+
+
+def with_tokens(cfg: LayerConfig, tokens: int, **changes) -> LayerConfig:
+    """A reduced copy of a config (parity cases at sizes the oracle finishes in seconds)."""
+    fields = dict(cfg.__dict__)
+    fields["tokens_per_rank"] = tokens
+    fields.update(changes)
+    return LayerConfig(**fields)
