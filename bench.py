@@ -1,0 +1,342 @@
+"""Benchmark of the Lina B200 MoE layer: one step = forward + backward of the whole hot
+path (gate, route, permute, dispatch all-to-all, expert FFN, combine all-to-all,
+un-permute, and their backward) on synthetic tokens shaped like BASELINE.json's
+configs[1] (GPT-2-small-shaped MoE layer: 8 experts, top-2, d_model 768, 8K
+tokens per GPU, bf16).  Metric: MoE layer tokens/s fwd+bwd, whole job.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config C2] [--n-chunks n]
+    python bench.py --impl reference ...      # the CPU oracle on a bounded sample
+
+Multi-GPU: launched by torch.distributed.run, one rank per GPU (weak scaling: each
+rank keeps T tokens; experts are partitioned E/N per rank).  Timing: CUDA events
+on the launching stream around each step, L2 flushed (256 MB write) between
+steps outside the events, barrier + synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+import lina_inputs as li  # noqa: E402
+
+METRIC = "MoE layer tokens/s fwd+bwd"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="lina", choices=["lina", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(li.CONFIGS))
+    ap.add_argument("--n-chunks", type=int, default=0, help="0 = 1 at N=1, 4 otherwise")
+    ap.add_argument("--family", default="balanced", choices=["balanced", "grid"])
+    ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=256, help="tokens in the oracle sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        p = json.load(open(path))
+        return {"bf16_sustained": float(p["bf16_tflops_sustained"]), "bf16_burst": float(p["bf16_tflops"]),
+                "hbm": float(p["hbm_gbs"]), "src": "measured"}
+    except Exception:
+        return {"bf16_sustained": 1400.0, "bf16_burst": 1590.0, "hbm": 6650.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU oracle timing
+
+
+def oracle_step_sample(cfg, seed, family, sample_tokens, world):
+    """One oracle fwd+bwd over a bounded sample: `sample_tokens` tokens of one rank, all experts.
+    Returns (seconds, tokens)."""
+    from oracle import moe
+    sub = li.with_tokens(cfg, sample_tokens)
+    Wg, W1, W2 = li.layer_weights(sub, seed, family)
+    X, dY = li.layer_tokens(sub, seed, 0, family)
+    C = li.with_tokens(cfg, sample_tokens).capacity()
+    t0 = time.perf_counter()
+    fw = moe.moe_forward([X], Wg, W1, W2, cfg.k, C, cfg.dtype)
+    moe.moe_backward(fw, [X], [dY], Wg, W1, W2, cfg.k, cfg.dtype)
+    return time.perf_counter() - t0, sample_tokens
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+        return int(n)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = li.CONFIGS[args.config]
+    for _ in range(args.warmup):
+        oracle_step_sample(cfg, args.seed, args.family, args.cpu_sample, world)
+    tot, toks = 0.0, 0
+    for _ in range(args.steps):
+        s, n = oracle_step_sample(cfg, args.seed, args.family, args.cpu_sample, world)
+        tot += s
+        toks += n
+    value = toks / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: E={cfg.num_experts} top-{cfg.k} d={cfg.d_model} f={cfg.d_ffn} "
+                               f"T/rank={cfg.tokens_per_rank} cf={cfg.cf} {cfg.dtype}",
+                   "sample_tokens": args.cpu_sample},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+                         "sample": f"{args.cpu_sample} tokens of one rank's {cfg.name} batch, fwd+bwd, all experts, "
+                                   "fp64 numpy oracle (per step)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.gpus != world and world == 1 and args.gpus > 1:
+        print(f"--gpus {args.gpus} needs torch.distributed.run with {args.gpus} processes", file=sys.stderr)
+        sys.exit(2)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import paper_2210_17223_b200 as lina
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+        uid = [lina.lina_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = lina.Comm(world, rank, local, uid[0])
+    else:
+        comm = lina.Comm(1, 0, local)
+
+    cfg = li.CONFIGS[args.config]
+    T, d, f, E, k = cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, cfg.num_experts, cfg.k
+    C = cfg.capacity()
+    El = E // world
+    n_chunks = args.n_chunks or (1 if world == 1 else 4)
+    tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    Wg_np, W1_np, W2_np = li.layer_weights(cfg, args.seed, args.family, experts=range(rank * El, (rank + 1) * El))
+    X_np, dY_np = li.layer_tokens(cfg, args.seed, rank, args.family)
+    wg = torch.from_numpy(Wg_np).to(dev)
+    w1 = torch.from_numpy(W1_np).to(tdt).to(dev)
+    w2 = torch.from_numpy(W2_np).to(tdt).to(dev)
+    x = torch.from_numpy(X_np).to(tdt).to(dev)
+    dy = torch.from_numpy(dY_np).to(tdt).to(dev)
+    del W1_np, W2_np
+    layer = lina.MoELayer(comm, T, d, f, E, k, C, n_chunks, tdt, dev)
+    outs = {"y": torch.empty((T, d), dtype=tdt, device=dev), "dx": torch.empty((T, d), dtype=tdt, device=dev),
+            "dwg": torch.empty_like(wg), "dw1": torch.empty_like(w1), "dw2": torch.empty_like(w2)}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(xx, dyy):
+        layer.forward(xx, wg, w1, w2, out=outs["y"])
+        layer.backward(dyy, xx, wg, w1, w2, outs["dx"], outs["dwg"], outs["dw1"], outs["dw2"])
+
+    # routing of this batch (identical every step): kept assignments for the algorithmic flop count
+    layer.forward(x, wg, w1, w2, out=outs["y"], want_route=True)
+    counts = layer.route_t["counts"].cpu().numpy()
+    kept_local = int(np.minimum(counts, C).sum())
+    for _ in range(args.warmup):
+        step(x, dy)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---------------- timed region (device time, per-step events, L2 flushed between steps)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    lina.lina_profile_read(comm)
+    lina.lina_profile_enable(comm, True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step(x, dy)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    lina.lina_profile_enable(comm, False)
+    prof = lina.lina_profile_read(comm)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(step_ms))
+    gemm_ms = prof["gemm_ms"]
+    t_all = torch.tensor([total_ms, gemm_ms, float(kept_local)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = t_all.clone()
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        sm = t_all.clone()
+        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+        total_ms_max, kept_total = float(mx[0]), float(sm[2])
+    else:
+        total_ms_max, kept_total = total_ms, float(kept_local)
+    value = world * T * args.steps / (total_ms_max / 1e3)
+
+    # ---------------- end to end through the public API, host buffers (pinned), copies timed
+    e2e = None
+    if not args.no_e2e:
+        xp = torch.from_numpy(X_np).to(tdt).pin_memory()
+        dyp = torch.from_numpy(dY_np).to(tdt).pin_memory()
+        yp = torch.empty((T, d), dtype=tdt).pin_memory()
+        dxp = torch.empty((T, d), dtype=tdt).pin_memory()
+        xd, dyd = torch.empty_like(x), torch.empty_like(dy)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            xd.copy_(xp, non_blocking=True)
+            dyd.copy_(dyp, non_blocking=True)
+            step(xd, dyd)
+            yp.copy_(outs["y"], non_blocking=True)
+            dxp.copy_(outs["dx"], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX)
+        elt = 2 if tdt == torch.bfloat16 else 4
+        e2e = {"value": world * T * args.steps / (float(e2e_ms[0]) / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": 2 * T * d * elt, "d2h_bytes_per_step": 2 * T * d * elt}
+
+    # ---------------- roofline of the dominant kernel family (expert GEMMs, tensor-bound)
+    pk = peaks()
+    flops_per_step_local = 12.0 * kept_local * d * f          # fwd 4df + bwd 8df per kept assignment
+    gemm_ms_per_step = gemm_ms / max(args.steps, 1)
+    achieved = flops_per_step_local / (gemm_ms_per_step / 1e3) / 1e12 if gemm_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config)
+        except Exception:
+            traffic = None
+    roof = {"bound": "tensor", "kernel": "expert grouped GEMMs (fwd GEMM1+ReLU, GEMM2; bwd dgrad x2, wgrad x2)",
+            "achieved": achieved, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
+            "frac": (achieved / pk["bf16_sustained"]) if achieved else None, "traffic": traffic,
+            "peak_src": f"{pk['src']} bf16 sustained (MEASURED_PEAKS.json)",
+            "gemm_ms_per_step": gemm_ms_per_step,
+            "gemm_share_of_step": gemm_ms_per_step / (total_ms / args.steps) if total_ms > 0 else None,
+            "algorithmic_flops_per_step": flops_per_step_local}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s, n = oracle_step_sample(cfg, args.seed, args.family, args.cpu_sample, world)
+        cpu = {"value": n / s, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": f"{n} tokens of the {cfg.name} batch, fwd+bwd, all {E} experts, fp64 numpy oracle "
+                         f"({s:.2f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if tdt == torch.bfloat16 else "f32",
+            "data": f"synthetic ({args.family} family, seeded random-init weights)",
+            "config": {"workload": f"{cfg.name}: E={E} top-{k} d={d} f={f} T/rank={T} cf={cfg.cf} C={C} "
+                                   f"n_chunks={n_chunks} {cfg.dtype}",
+                       "global_batch": world * T, "parallelism": f"ep{world}",
+                       "l2": "flushed between timed steps (256 MB write, outside the step events)",
+                       "kept_assignments": int(kept_total)},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(prof["kernel_launches"]),
+            "clocks": clocks.summary(),
+            "step_ms": {"min": min(step_ms), "median": float(np.median(step_ms)), "max": max(step_ms)},
+        }
+        print(json.dumps(line), flush=True)
+    comm.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

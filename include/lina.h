@@ -1,0 +1,266 @@
+/*
+ * lina.h — C ABI of the B200-native Lina expert-parallel MoE layer.
+ *
+ * What is computed (PAPER.md = arXiv 2210.17223, "Accelerating Distributed MoE
+ * Training and Inference with Lina"; P:n = PAPER.md line n):
+ *   An MoE layer "consists of multiple FFNs each serving as an expert, and a
+ *   gating network ... Every expert is a fully-connected two-layer network using
+ *   ReLU ... The gating network takes in the embedding vector of each token and
+ *   multiplies them with its trainable matrix. Based on the results, it
+ *   dispatches the token to a small number of experts ... The final output of
+ *   the MoE layer is the weighted sum of outputs from the selected expert(s)"
+ *   (§2.1).  With expert parallelism "an all-to-all communication is then
+ *   needed to send tokens to their experts selected by the gating network, and
+ *   another all-to-all is needed to send tokens back".
+ *   Lina partitions the all-to-all into micro-ops along the token dimension and
+ *   pipelines the expert FFN behind them (§4.2; §6.1),
+ *   gives all-to-all strict priority over the gradient allreduce, whose tensors
+ *   are split into equal micro-ops (§3, §4.2, §6.1),
+ *   and in inference replicates popular experts by Eq. (1) with first-fit-
+ *   decreasing packing (§5.2) and an unequal-split all-to-all.
+ *   Readings where the paper is silent (capacity, drop order, gate
+ *   normalisation, tie-breaks, rounding points) are R1-R16 in DESIGN.md §3.
+ *
+ * Conventions for every entry point:
+ *   - Every function returns lina_status; nothing throws across the ABI.  On a
+ *     non-OK status, lina_last_error() returns a thread-local message; for
+ *     LINA_ERR_INVALID_ARGUMENT it lists EVERY violated invariant.
+ *   - Pointers named *device* / all tensor arguments of lina_moe_* are CUDA
+ *     device pointers on the communicator's device, caller-owned, row-major,
+ *     contiguous, 16-byte aligned.  Host arrays are named host_* or documented.
+ *   - All device work is enqueued on the caller's `stream` (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream).  Internal streams fork
+ *     from and join back to `stream` with events; results are valid when
+ *     `stream` reaches that point.  Pointers must stay live until then.  The
+ *     calls never synchronise the host, except lina_moe_infer_forward (the
+ *     unequal all-to-all needs host-visible counts).
+ *   - The library never allocates caller-visible memory in forward/backward:
+ *     scratch and saved state are caller-allocated, sized by
+ *     lina_moe_workspace_size().
+ *   - One lina_comm per rank (process/GPU).  Calls on one lina_comm are not
+ *     reentrant.  There is NO CPU fallback: on a machine without an sm_100 GPU
+ *     lina_comm_init fails with LINA_ERR_UNSUPPORTED.
+ */
+#ifndef LINA_H_
+#define LINA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LINA_OK = 0,
+  LINA_ERR_INVALID_ARGUMENT = 1, /* descriptor / pointer invariant violated (all listed)      */
+  LINA_ERR_UNSUPPORTED = 2,      /* valid but not implemented here (e.g. no sm_100 device)     */
+  LINA_ERR_INFEASIBLE_PLAN = 3,  /* E > N * max_per_device, or a replica cannot be placed      */
+  LINA_ERR_CUDA = 4,             /* a CUDA runtime/driver call failed (message has the name)   */
+  LINA_ERR_NCCL = 5,             /* an NCCL call failed or the communicator reported an error  */
+  LINA_ERR_WORKSPACE = 6         /* workspace/saved buffer smaller than lina_moe_workspace_size */
+} lina_status;
+
+typedef enum {
+  LINA_F32 = 0,  /* fp32 tokens/weights/outputs; expert GEMMs on CUDA cores (no TF32)        */
+  LINA_BF16 = 1  /* bf16 tokens/weights/outputs; expert GEMMs on tcgen05 tensor cores, fp32 acc */
+} lina_dtype;
+
+typedef enum {
+  /* Non-expert allreduce micro-ops are issued as soon as their gradient is
+   * ready, whole tensors, on the low-priority stream — concurrent with the
+   * all-to-all and fair-sharing the links (the paper's DeepSpeed baseline,
+   * P:64, fig:schedule_baseline P:283). */
+  LINA_SCHED_BASELINE = 0,
+  /* Lina: each gradient is split into equal partition_bytes micro-ops (never
+   * mixing gradients); a micro-op is launched only while no
+   * all-to-all micro-op is queued or in flight; launching stops
+   * once the combine backward starts, "since this implies all-to-all is
+   * imminent". */
+  LINA_SCHED_LINA = 1
+} lina_policy;
+
+typedef void* lina_stream; /* cudaStream_t */
+typedef struct lina_comm lina_comm;
+
+/* ------------------------------------------------------------------------ */
+/* Errors, version                                                           */
+/* ------------------------------------------------------------------------ */
+
+/* Thread-local message for the last non-OK status on this thread ("" if none). */
+const char* lina_last_error(void);
+/* Library version and build arch string, e.g. "lina 0.1 sm_100a". */
+const char* lina_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* Communicator: one per rank.  Expert-parallel (EP) and data-parallel (DP)   */
+/* NCCL communicators over the same world (the paper's separate EP and DP    */
+/* process groups, each on its own CUDA stream), a high-priority stream */
+/* for all-to-all micro-ops and a low-priority stream for allreduce micro-ops.*/
+/* ------------------------------------------------------------------------ */
+
+/* Rank 0 creates an NCCL unique id (128 bytes, host memory) that the caller
+ * broadcasts to the other ranks (e.g. through its torch process group). */
+lina_status lina_get_unique_id(unsigned char host_id[128]);
+
+/* world >= 1, 0 <= rank < world, cuda_device = local GPU index.  host_id may
+ * be NULL only when world == 1 (no NCCL is created: the P=1 layer needs no
+ * collective).  nccl_max_ctas > 0 caps the SMs each NCCL kernel may take
+ * (ncclConfig_t.maxCTAs) so the expert GEMM keeps the rest; 0 = NCCL default.
+ * Errors: INVALID_ARGUMENT, UNSUPPORTED (device is not sm_100), CUDA, NCCL. */
+lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned char* host_id,
+                           int nccl_max_ctas, lina_comm** out);
+/* Waits for the scheduler thread, destroys comms/streams/events.  NULL is a no-op. */
+lina_status lina_comm_destroy(lina_comm* comm);
+/* Surfaces asynchronous NCCL/CUDA errors (ncclCommGetAsyncError, cudaPeekAtLastError). */
+lina_status lina_comm_check(lina_comm* comm);
+/* rank / world of a communicator. */
+lina_status lina_comm_info(const lina_comm* comm, int* rank, int* world);
+
+/* ------------------------------------------------------------------------ */
+/* Placement / replication tables (paper D3: expert -> device mapping,        */
+/* replica list and per-replica token split; Eq. (1)).  */
+/* All arrays are HOST memory owned by the caller.                            */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t num_experts;    /* E                                                        */
+  int32_t num_devices;    /* N (= world)                                              */
+  int32_t max_per_device; /* at most this many experts hosted per device (4)   */
+  int32_t max_replicas;   /* row pitch of replica_device; >= max r_e (N is always enough) */
+  int32_t* replicas;      /* [E]                 r_e >= 1                              */
+  int32_t* replica_device;/* [E][max_replicas]   device ids ascending, -1 padded       */
+  int32_t* hosted;        /* [N][max_per_device] expert ids ascending, -1 padded       */
+} lina_placement;
+
+/* Eq. (1) n_e = N * popularity[e]; r_e = max(1, round-half-up(n_e)) capped at N,
+ * trimmed largest-first while sum r_e > N*max_per_device; replicas (size n_e/r_e
+ * device-loads) packed first-fit-decreasing into devices of capacity 1.0
+ * (P:478); an item that fits nowhere goes to the least-loaded eligible device
+ * (lowest id), the deterministic stand-in for "randomly assigned".
+ * popularity: host [E], >= 0 (need not sum to 1).  `out` arrays caller-allocated
+ * with the pitches above.  Errors: INVALID_ARGUMENT, INFEASIBLE_PLAN
+ * (E > N*max_per_device).  Pure host function, no device needed. */
+lina_status lina_placement_compute(const double* host_popularity, int32_t num_experts,
+                                   int32_t num_devices, int32_t max_per_device,
+                                   lina_placement* out);
+
+/* Tokens a source rank sends to each replica of one expert (R14: contiguous
+ * blocks in slot order whose sizes differ by <= 1; block q goes to replica
+ * (q + source_rank) mod r_e).  host_out[r_e]. */
+lina_status lina_replica_split(int32_t count, int32_t replicas, int32_t source_rank,
+                               int32_t* host_out);
+
+/* ------------------------------------------------------------------------ */
+/* MoE layer                                                                 */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t num_tokens;  /* T tokens on this rank (>= 0)                                  */
+  int32_t d_model;     /* d  (d*elt % 16 == 0; bf16 also d % 128 == 0)                  */
+  int32_t d_ffn;       /* f  (f*elt % 16 == 0; bf16 also f % 128 == 0)                  */
+  int32_t num_experts; /* E global; static placement needs E % world == 0 (E_l = E/world) */
+  int32_t k;           /* top-k, 1 <= k <= min(E, 8)  (k=2 training, k=1 inference) */
+  int32_t capacity;    /* C >= 1 slots per expert per SOURCE rank (R5); C >= T => dropless */
+  int32_t n_chunks;    /* all-to-all micro-ops per direction, 1 <= n <= C (R10) */
+  lina_dtype dtype;    /* tokens, expert weights, outputs and their gradients            */
+} lina_moe_desc;
+
+/* Optional routing tensors (device, caller-owned; NULL fields are skipped).
+ * Forward writes them; with override_routing = 1, idx and gate are INPUTS
+ * (caller-chosen routing: the paper's Ideal forced-balanced mode). */
+typedef struct {
+  int32_t* idx;     /* [T,k] selected experts, (logit desc, id asc) order (R3)   */
+  float* gate;      /* [T,k] gate weights (R4)                                    */
+  int32_t* slot;    /* [T,k] capacity slot, -1 = dropped (R5, R6)                 */
+  int32_t* counts;  /* [E]   pre-drop assignments per expert from this rank       */
+  float* probs;     /* [T,E] softmax probabilities                               */
+  int32_t override_routing;
+} lina_route;
+
+/* Bytes of scratch (`workspace`) and of state kept from forward to backward
+ * (`saved`) for this descriptor on this communicator.  saved may be 0-sized
+ * pointer-wise for inference-only forward (pass saved = NULL). */
+lina_status lina_moe_workspace_size(const lina_comm* comm, const lina_moe_desc* desc,
+                                    size_t* workspace_bytes, size_t* saved_bytes);
+
+/* Training/inference forward with the static placement e -> rank floor(e/E_l):
+ *   tokens [T,d] dtype; gate_w [d,E] fp32 (replicated); w1 [E_l,f,d], w2 [E_l,d,f]
+ *   dtype (this rank's experts, nn.Linear layout); out [T,d] dtype = the MoE
+ *   term only (the residual belongs to the caller, R7).  saved: NULL or
+ *   saved_bytes (needed for backward).  n_chunks micro-ops per all-to-all,
+ *   pipelined against the expert GEMMs.  Errors: INVALID_ARGUMENT,
+ *   WORKSPACE, CUDA, NCCL. */
+lina_status lina_moe_forward(lina_comm* comm, const lina_moe_desc* desc, const void* tokens,
+                             const float* gate_w, const void* w1, const void* w2, void* out,
+                             void* saved, void* workspace, size_t workspace_bytes,
+                             lina_route* route, lina_stream stream);
+
+/* Backward of lina_moe_forward (same desc, saved from that forward):
+ *   dout [T,d] dtype -> dtokens [T,d] dtype; dgate_w [d,E] fp32 (this rank's
+ *   sum over its tokens; the DP allreduce is lina_allreduce_submit's job, R12);
+ *   dw1 [E_l,f,d], dw2 [E_l,d,f] dtype (sum over every source rank's tokens
+ *   routed to this rank's experts).  No gradient flows through the top-k
+ *   selection; dropped assignments get none (R13). */
+lina_status lina_moe_backward(lina_comm* comm, const lina_moe_desc* desc, const void* saved,
+                              const void* dout, const void* tokens, const float* gate_w,
+                              const void* w1, const void* w2, void* dtokens, float* dgate_w,
+                              void* dw1, void* dw2, void* workspace, size_t workspace_bytes,
+                              lina_stream stream);
+
+/* Inference forward with popularity-driven replication:
+ *   w1_all [E,f,d], w2_all [E,d,f]: ALL experts on every rank (the paper keeps
+ *   all experts in host DRAM; here in HBM so a placement change moves no
+ *   weights).  placement: NULL => computed from this batch's global histogram
+ *   (allreduce of per-expert counts; the paper's "w/o estimation" variant,
+ *   P:905) with max_per_device; else used as given (e.g. an estimate-based
+ *   plan, phase one).  plan_out (nullable, host arrays caller-allocated) gets the
+ *   plan used.  Dropless top-k (capacity ignored, R5).  Synchronises the host
+ *   once (H9).  Output equals lina_moe_forward's with a static placement (P9). */
+lina_status lina_moe_infer_forward(lina_comm* comm, const lina_moe_desc* desc, const void* tokens,
+                                   const float* gate_w, const void* w1_all, const void* w2_all,
+                                   void* out, const lina_placement* placement,
+                                   int32_t max_per_device, lina_placement* plan_out,
+                                   void* workspace, size_t workspace_bytes, lina_stream stream);
+/* Workspace for lina_moe_infer_forward. */
+lina_status lina_moe_infer_workspace_size(const lina_comm* comm, const lina_moe_desc* desc,
+                                          size_t* workspace_bytes);
+
+/* ------------------------------------------------------------------------ */
+/* Micro-op allreduce scheduler (§4; §6.1)             */
+/* ------------------------------------------------------------------------ */
+
+/* policy and micro-op size (default LINA, 30 MB = the paper's partition). */
+lina_status lina_sched_config(lina_comm* comm, lina_policy policy, size_t partition_bytes);
+/* Queue one gradient (device, fp32 or bf16, `count` elements) for a SUM
+ * allreduce over the DP communicator, in place.  It becomes ready when
+ * `ready_stream` reaches this call.  Gradients are never mixed in one
+ * micro-op.  Non-blocking. */
+lina_status lina_allreduce_submit(lina_comm* comm, void* grad, size_t count, lina_dtype dtype,
+                                  lina_stream ready_stream);
+/* Make `stream` wait until every submitted allreduce has completed. */
+lina_status lina_allreduce_wait(lina_comm* comm, lina_stream stream);
+/* Scheduler statistics since the last call: micro-ops issued, micro-ops that
+ * were deferred because an all-to-all was queued/in flight. */
+lina_status lina_sched_stats(lina_comm* comm, int64_t* issued, int64_t* deferred);
+
+
+/* ------------------------------------------------------------------------ */
+/* Instrumentation (bench.py / tests): counters since the last read.          */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int64_t kernel_launches; /* this library's CUDA kernel launches (all communicators, process-wide) */
+  int64_t gemm_launches;   /* expert GEMM launches on this communicator while profiling   */
+  double gemm_ms;          /* device time of the expert-GEMM phases (CUDA events recorded on the
+                              compute stream around each phase, after its all-to-all waits) */
+  int64_t gemm_phases;     /* number of timed phases summed into gemm_ms                  */
+} lina_profile;
+
+/* on != 0: record timing events around the expert-GEMM phases of every forward /
+ * backward on this communicator (cheap; off by default). */
+lina_status lina_profile_enable(lina_comm* comm, int on);
+/* Synchronises the recorded events, fills *out, and resets the counters. */
+lina_status lina_profile_read(lina_comm* comm, lina_profile* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LINA_H_ */

@@ -93,28 +93,44 @@ def grid(rng: np.random.Generator, shape, scale: float = 1.0) -> np.ndarray:
 TENSOR_IDS = {"X": 1, "Wg": 2, "W1": 3, "W2": 4, "dY": 5, "zipf": 6}
 
 
-def layer_weights(cfg: LayerConfig, seed: int, family: str = "grid"):
-    """Global weights, identical on every rank: Wg [d,E] fp32, W1 [E,f,d], W2 [E,d,f]."""
-    d, f, E = cfg.d_model, cfg.d_ffn, cfg.num_experts
+def gate_weight(cfg: LayerConfig, seed: int, family: str = "grid") -> np.ndarray:
+    """Wg [d,E] fp32, identical on every rank."""
+    d, E = cfg.d_model, cfg.num_experts
     if family == "grid":
-        Wg = grid(_rng(seed, TENSOR_IDS["Wg"]), (d, E))
-        W1 = grid(_rng(seed, TENSOR_IDS["W1"]), (E, f, d), 1.0 / 8)
-        W2 = grid(_rng(seed, TENSOR_IDS["W2"]), (E, d, f), 1.0 / 8)
-    elif family == "balanced":
-        Wg = (_rng(seed, TENSOR_IDS["Wg"]).standard_normal((d, E)) / math.sqrt(d)).astype(np.float32)
-        W1 = (_rng(seed, TENSOR_IDS["W1"]).standard_normal((E, f, d), dtype=np.float32) / np.float32(math.sqrt(d)))
-        W2 = (_rng(seed, TENSOR_IDS["W2"]).standard_normal((E, d, f), dtype=np.float32) / np.float32(math.sqrt(f)))
-    elif family == "zipf":
-        U = _zipf_directions(cfg, seed)
-        Wg = np.ascontiguousarray(U.T).astype(np.float32)
-        W1 = (_rng(seed, TENSOR_IDS["W1"]).standard_normal((E, f, d), dtype=np.float32) / np.float32(math.sqrt(d)))
-        W2 = (_rng(seed, TENSOR_IDS["W2"]).standard_normal((E, d, f), dtype=np.float32) / np.float32(math.sqrt(f)))
+        return grid(_rng(seed, TENSOR_IDS["Wg"]), (d, E))
+    if family == "balanced":
+        return (_rng(seed, TENSOR_IDS["Wg"]).standard_normal((d, E)) / math.sqrt(d)).astype(np.float32)
+    if family == "zipf":
+        return np.ascontiguousarray(_zipf_directions(cfg, seed).T).astype(np.float32)
+    raise ValueError(f"unknown family {family!r}")
+
+
+def expert_weights(cfg: LayerConfig, seed: int, e: int, family: str = "grid"):
+    """Expert e's W1 [f,d] and W2 [d,f] (each expert drawn from its own stream, so a rank
+    can generate just the experts it hosts)."""
+    d, f = cfg.d_model, cfg.d_ffn
+    r1, r2 = _rng(seed, TENSOR_IDS["W1"], e), _rng(seed, TENSOR_IDS["W2"], e)
+    if family == "grid":
+        W1 = grid(r1, (f, d), 1.0 / 8)
+        W2 = grid(r2, (d, f), 1.0 / 8)
+    elif family in ("balanced", "zipf"):
+        W1 = r1.standard_normal((f, d), dtype=np.float32) / np.float32(math.sqrt(d))
+        W2 = r2.standard_normal((d, f), dtype=np.float32) / np.float32(math.sqrt(f))
     else:
         raise ValueError(f"unknown family {family!r}")
     if cfg.dtype == "bf16":
         W1 = bf16_representable(W1)
         W2 = bf16_representable(W2)
-    return Wg, W1, W2
+    return W1, W2
+
+
+def layer_weights(cfg: LayerConfig, seed: int, family: str = "grid", experts=None):
+    """Wg [d,E] fp32 and the stacked W1 [n,f,d], W2 [n,d,f] of `experts` (default: all E)."""
+    experts = range(cfg.num_experts) if experts is None else experts
+    ws = [expert_weights(cfg, seed, e, family) for e in experts]
+    W1 = np.stack([w[0] for w in ws])
+    W2 = np.stack([w[1] for w in ws])
+    return gate_weight(cfg, seed, family), W1, W2
 
 
 def _zipf_directions(cfg: LayerConfig, seed: int) -> np.ndarray:

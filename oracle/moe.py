@@ -170,17 +170,22 @@ def moe_forward(Xs, Wg, W1, W2, k: int, capacity: int, dtype: str):
         for n, (r, t, j) in enumerate(rows):
             outs[r].h[(int(t), int(j))] = h[n]
             outs[r].o[(int(t), int(j))] = o[n]
-    # Combine (the return all-to-all + "computing the weighted output"):
-    # y_t = sum over kept j, ascending, of g[t,j] * o[t,j]; fp64, one final rounding (R9).
     for fw in outs:
-        T = fw.y.shape[0]
-        acc = np.zeros_like(fw.y)
-        for t in range(T):
-            for j in range(k):
-                if fw.slot[t, j] >= 0:
-                    acc[t] += fw.gate[t, j] * fw.o[(t, j)]
-        fw.y = round_to(acc, dtype)
+        fw.y = combine(fw, k, dtype)
     return outs
+
+
+def combine(fw: "RankForward", k: int, dtype: str) -> np.ndarray:
+    """The return all-to-all + "computing the weighted output" (P:133, P:172-173):
+    y_t = sum over kept j, ascending, of g[t,j] * o[t,j]; fp64, one final rounding (R9).
+    A token whose k assignments were all dropped gets y_t = 0 (R7)."""
+    T, d = fw.y.shape
+    acc = np.zeros((T, d))
+    for t in range(T):
+        for j in range(k):
+            if fw.slot[t, j] >= 0:
+                acc[t] += fw.gate[t, j] * fw.o[(t, j)]
+    return round_to(acc, dtype)
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,474 @@
+// C ABI of include/lina.h: argument validation (every violated invariant is
+// listed), status codes, communicator lifetime, and dispatch into layer.cpp /
+// infer.cpp / sched.cpp / placement.cpp.  Nothing throws across the ABI.
+#include <cstring>
+#include <sstream>
+#include <vector>
+
+#include "internal.h"
+#include "layer.h"
+
+#include <atomic>
+
+namespace lina {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static cudaEvent_t prof_event(lina_comm* cm) {
+  if (!cm->prof_pool.empty()) {
+    cudaEvent_t e = cm->prof_pool.back();
+    cm->prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  LINA_CUDA_CHECK(cudaEventCreate(&e));
+  return e;
+}
+void prof_begin(lina_comm* cm, cudaStream_t s) {
+  if (!cm->prof) return;
+  cudaEvent_t a = prof_event(cm);
+  LINA_CUDA_CHECK(cudaEventRecord(a, s));
+  cm->prof_gemm.push_back({a, nullptr});
+}
+void prof_end(lina_comm* cm, cudaStream_t s, int gemm_launches) {
+  if (!cm->prof || cm->prof_gemm.empty() || cm->prof_gemm.back().second) return;
+  cudaEvent_t b = prof_event(cm);
+  LINA_CUDA_CHECK(cudaEventRecord(b, s));
+  cm->prof_gemm.back().second = b;
+  cm->prof_gemm_launches += gemm_launches;
+}
+
+void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
+                   const float* gate_w, const void* w1_all, const void* w2_all, void* out,
+                   const lina_placement* placement, int mpd, lina_placement* plan_out, void* ws,
+                   size_t ws_bytes, cudaStream_t s);
+size_t infer_workspace_bytes(const lina_moe_desc& desc, int world);
+}  // namespace lina
+
+using namespace lina;
+
+namespace {
+
+template <typename F>
+lina_status guarded(F&& f) {
+  try {
+    g_err.clear();
+    return f();
+  } catch (const ArgError& e) {
+    g_err = e.what;
+    return LINA_ERR_INVALID_ARGUMENT;
+  } catch (const StatusError& e) {
+    g_err = e.what;
+    return e.status;
+  } catch (const CudaError& e) {
+    g_err = e.what;
+    return LINA_ERR_CUDA;
+  } catch (const NcclError& e) {
+    g_err = e.what;
+    return LINA_ERR_NCCL;
+  } catch (const std::exception& e) {
+    g_err = std::string("internal error: ") + e.what();
+    return LINA_ERR_CUDA;
+  }
+}
+
+// Lists every violated invariant of a descriptor (lina.h, lina_moe_desc).
+void validate_desc(const lina_moe_desc* d, int world, bool static_placement) {
+  if (!d) throw ArgError{"desc is NULL"};
+  std::vector<std::string> v;
+  const int elt = d->dtype == LINA_BF16 ? 2 : 4;
+  if (d->dtype != LINA_F32 && d->dtype != LINA_BF16) v.push_back("dtype not LINA_F32/LINA_BF16");
+  if (d->num_tokens < 0) v.push_back("num_tokens < 0");
+  if (d->d_model <= 0) v.push_back("d_model <= 0");
+  if (d->d_ffn <= 0) v.push_back("d_ffn <= 0");
+  if (d->num_experts < 1 || d->num_experts > 64) v.push_back("num_experts not in [1, 64]");
+  if (d->k < 1 || d->k > 8 || d->k > d->num_experts) v.push_back("k not in [1, min(E, 8)]");
+  if (d->capacity < 1) v.push_back("capacity < 1");
+  if (d->n_chunks < 1 || d->n_chunks > 32 || (d->capacity >= 1 && d->n_chunks > d->capacity))
+    v.push_back("n_chunks not in [1, min(C, 32)]");
+  if (d->d_model > 0 && (d->d_model * elt) % 16 != 0) v.push_back("d_model*elt % 16 != 0");
+  if (d->d_ffn > 0 && (d->d_ffn * elt) % 16 != 0) v.push_back("d_ffn*elt % 16 != 0");
+  if (d->d_model > 0 && d->d_model % 16 != 0) v.push_back("d_model % 16 != 0");
+  if (static_placement && d->num_experts >= 1 && d->num_experts % world != 0)
+    v.push_back("num_experts % world != 0 (static placement needs E_l = E/world experts per rank)");
+  if (!v.empty()) {
+    std::ostringstream os;
+    os << "invalid lina_moe_desc:";
+    for (auto& s : v) os << " [" << s << "]";
+    throw ArgError{os.str()};
+  }
+}
+
+void need(std::vector<std::string>& v, const void* p, const char* name) {
+  if (!p) v.push_back(std::string(name) + " is NULL");
+}
+void raise_if(const std::vector<std::string>& v, const char* what) {
+  if (v.empty()) return;
+  std::ostringstream os;
+  os << what << ":";
+  for (auto& s : v) os << " [" << s << "]";
+  throw ArgError{os.str()};
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lina_last_error(void) { return g_err.c_str(); }
+const char* lina_version(void) { return "lina 0.1 sm_100a"; }
+
+lina_status lina_get_unique_id(unsigned char host_id[128]) {
+  return guarded([&] {
+    if (!host_id) throw ArgError{"host_id is NULL"};
+    ncclUniqueId id;
+    LINA_NCCL_CHECK(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(host_id, &id, 128);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned char* host_id,
+                           int nccl_max_ctas, lina_comm** out) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    if (!out) v.push_back("out is NULL");
+    if (world < 1) v.push_back("world < 1");
+    if (rank < 0 || rank >= world) v.push_back("rank not in [0, world)");
+    if (world > 1 && !host_id) v.push_back("host_id is NULL with world > 1");
+    if (nccl_max_ctas < 0) v.push_back("nccl_max_ctas < 0");
+    raise_if(v, "lina_comm_init");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw StatusError{LINA_ERR_UNSUPPORTED, "no CUDA device visible (there is no CPU fallback)"};
+    if (cuda_device < 0 || cuda_device >= ndev) throw ArgError{"cuda_device out of range"};
+    LINA_CUDA_CHECK(cudaSetDevice(cuda_device));
+    cudaDeviceProp prop;
+    LINA_CUDA_CHECK(cudaGetDeviceProperties(&prop, cuda_device));
+    if (prop.major != 10)
+      throw StatusError{LINA_ERR_UNSUPPORTED, "device is sm_" + std::to_string(prop.major) +
+                                                  std::to_string(prop.minor) +
+                                                  "; this library is built for sm_100a only"};
+    auto* cm = new lina_comm();
+    cm->rank = rank;
+    cm->world = world;
+    cm->device = cuda_device;
+    cm->num_sms = prop.multiProcessorCount;
+    int lo_prio = 0, hi_prio = 0;
+    LINA_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->hi, cudaStreamNonBlocking, hi_prio));
+    LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->hi2, cudaStreamNonBlocking, hi_prio));
+    LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->lo, cudaStreamNonBlocking, lo_prio));
+    cm->ev.resize(128);
+    for (auto& e : cm->ev) LINA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (world > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, host_id, 128);
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      if (nccl_max_ctas > 0) cfg.maxCTAs = nccl_max_ctas;
+      LINA_NCCL_CHECK(ncclCommInitRankConfig(&cm->ep_disp, world, id, rank, &cfg));
+      ncclConfig_t cfg2 = NCCL_CONFIG_INITIALIZER;
+      if (nccl_max_ctas > 0) cfg2.maxCTAs = nccl_max_ctas;
+      LINA_NCCL_CHECK(ncclCommSplit(cm->ep_disp, 0, rank, &cm->ep_comb, &cfg2));
+      ncclConfig_t cfg3 = NCCL_CONFIG_INITIALIZER;
+      if (nccl_max_ctas > 0) cfg3.maxCTAs = nccl_max_ctas;
+      LINA_NCCL_CHECK(ncclCommSplit(cm->ep_disp, 0, rank, &cm->dp, &cfg3));
+      cm->sched = sched_create(cm);
+    }
+    *out = cm;
+    return LINA_OK;
+  });
+}
+
+lina_status lina_comm_destroy(lina_comm* cm) {
+  return guarded([&] {
+    if (!cm) return LINA_OK;
+    cudaSetDevice(cm->device);
+    if (cm->sched) sched_destroy(cm->sched);
+    cm->sched = nullptr;
+    if (cm->dp) ncclCommDestroy(cm->dp);
+    if (cm->ep_comb) ncclCommDestroy(cm->ep_comb);
+    if (cm->ep_disp) ncclCommDestroy(cm->ep_disp);
+    for (auto e : cm->ev) cudaEventDestroy(e);
+    if (cm->hi) cudaStreamDestroy(cm->hi);
+    if (cm->hi2) cudaStreamDestroy(cm->hi2);
+    if (cm->lo) cudaStreamDestroy(cm->lo);
+    delete cm;
+    return LINA_OK;
+  });
+}
+
+lina_status lina_comm_check(lina_comm* cm) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    LINA_CUDA_CHECK(cudaPeekAtLastError());
+    for (ncclComm_t c : {cm->ep_disp, cm->ep_comb, cm->dp}) {
+      if (!c) continue;
+      ncclResult_t r = ncclSuccess;
+      LINA_NCCL_CHECK(ncclCommGetAsyncError(c, &r));
+      if (r != ncclSuccess && r != ncclInProgress)
+        throw NcclError{std::string("async NCCL error: ") + ncclGetErrorString(r)};
+    }
+    return LINA_OK;
+  });
+}
+
+lina_status lina_comm_info(const lina_comm* cm, int* rank, int* world) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    if (rank) *rank = cm->rank;
+    if (world) *world = cm->world;
+    return LINA_OK;
+  });
+}
+
+lina_status lina_placement_compute(const double* pop, int32_t E, int32_t N, int32_t mpd,
+                                   lina_placement* out) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    need(v, pop, "host_popularity");
+    need(v, out, "out");
+    if (E < 1) v.push_back("num_experts < 1");
+    if (N < 1) v.push_back("num_devices < 1");
+    if (mpd < 1) v.push_back("max_per_device < 1");
+    if (out) {
+      need(v, out->replicas, "out->replicas");
+      need(v, out->replica_device, "out->replica_device");
+      need(v, out->hosted, "out->hosted");
+      if (out->max_replicas < std::min(N, 1 << 30) && out->max_replicas < N)
+        v.push_back("out->max_replicas < num_devices");
+    }
+    if (pop)
+      for (int e = 0; e < E; ++e)
+        if (!(pop[e] >= 0.0)) {
+          v.push_back("popularity[" + std::to_string(e) + "] < 0 or NaN");
+          break;
+        }
+    raise_if(v, "lina_placement_compute");
+    std::string err;
+    lina_status st = placement_compute(pop, E, N, mpd, out, &err);
+    if (st != LINA_OK) throw StatusError{st, err};
+    return LINA_OK;
+  });
+}
+
+lina_status lina_replica_split(int32_t count, int32_t replicas, int32_t source_rank,
+                               int32_t* host_out) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    if (count < 0) v.push_back("count < 0");
+    if (replicas < 1) v.push_back("replicas < 1");
+    if (source_rank < 0) v.push_back("source_rank < 0");
+    need(v, host_out, "host_out");
+    raise_if(v, "lina_replica_split");
+    replica_split(count, replicas, source_rank, host_out);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_moe_workspace_size(const lina_comm* cm, const lina_moe_desc* desc,
+                                    size_t* workspace_bytes, size_t* saved_bytes) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    validate_desc(desc, cm->world, true);
+    Plan p = make_plan(*desc, cm->world);
+    if (workspace_bytes) *workspace_bytes = p.ws_bytes;
+    if (saved_bytes) *saved_bytes = p.saved_bytes;
+    return LINA_OK;
+  });
+}
+
+lina_status lina_moe_forward(lina_comm* cm, const lina_moe_desc* desc, const void* tokens,
+                             const float* gate_w, const void* w1, const void* w2, void* out,
+                             void* saved, void* workspace, size_t workspace_bytes,
+                             lina_route* route, lina_stream stream) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    validate_desc(desc, cm->world, true);
+    std::vector<std::string> v;
+    const bool any = desc->num_tokens > 0;
+    if (any) need(v, tokens, "tokens");
+    need(v, gate_w, "gate_w");
+    need(v, w1, "w1");
+    need(v, w2, "w2");
+    if (any) need(v, out, "out");
+    need(v, saved, "saved (forward keeps routing and expert activations there)");
+    need(v, workspace, "workspace");
+    if (route && route->override_routing) {
+      need(v, route->idx, "route->idx (override_routing)");
+      need(v, route->gate, "route->gate (override_routing)");
+    }
+    raise_if(v, "lina_moe_forward");
+    Plan p = make_plan(*desc, cm->world);
+    if (workspace_bytes < p.ws_bytes)
+      throw StatusError{LINA_ERR_WORKSPACE, "workspace_bytes " + std::to_string(workspace_bytes) +
+                                                " < required " + std::to_string(p.ws_bytes)};
+    LINA_CUDA_CHECK(cudaSetDevice(cm->device));
+    moe_forward(cm, p, tokens, gate_w, w1, w2, out, saved, workspace, route, (cudaStream_t)stream);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_moe_backward(lina_comm* cm, const lina_moe_desc* desc, const void* saved,
+                              const void* dout, const void* tokens, const float* gate_w,
+                              const void* w1, const void* w2, void* dtokens, float* dgate_w,
+                              void* dw1, void* dw2, void* workspace, size_t workspace_bytes,
+                              lina_stream stream) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    validate_desc(desc, cm->world, true);
+    std::vector<std::string> v;
+    const bool any = desc->num_tokens > 0;
+    need(v, saved, "saved");
+    if (any) {
+      need(v, dout, "dout");
+      need(v, tokens, "tokens");
+      need(v, dtokens, "dtokens");
+    }
+    need(v, gate_w, "gate_w");
+    need(v, w1, "w1");
+    need(v, w2, "w2");
+    need(v, dgate_w, "dgate_w");
+    need(v, dw1, "dw1");
+    need(v, dw2, "dw2");
+    need(v, workspace, "workspace");
+    raise_if(v, "lina_moe_backward");
+    Plan p = make_plan(*desc, cm->world);
+    if (workspace_bytes < p.ws_bytes)
+      throw StatusError{LINA_ERR_WORKSPACE, "workspace_bytes " + std::to_string(workspace_bytes) +
+                                                " < required " + std::to_string(p.ws_bytes)};
+    LINA_CUDA_CHECK(cudaSetDevice(cm->device));
+    moe_backward(cm, p, saved, dout, tokens, gate_w, w1, w2, dtokens, dgate_w, dw1, dw2, workspace,
+                 (cudaStream_t)stream);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_moe_infer_workspace_size(const lina_comm* cm, const lina_moe_desc* desc,
+                                          size_t* workspace_bytes) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    validate_desc(desc, cm->world, false);
+    if (workspace_bytes) *workspace_bytes = infer_workspace_bytes(*desc, cm->world);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_moe_infer_forward(lina_comm* cm, const lina_moe_desc* desc, const void* tokens,
+                                   const float* gate_w, const void* w1_all, const void* w2_all,
+                                   void* out, const lina_placement* placement,
+                                   int32_t max_per_device, lina_placement* plan_out,
+                                   void* workspace, size_t workspace_bytes, lina_stream stream) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    validate_desc(desc, cm->world, false);
+    std::vector<std::string> v;
+    if (desc->num_tokens > 0) {
+      need(v, tokens, "tokens");
+      need(v, out, "out");
+    }
+    need(v, gate_w, "gate_w");
+    need(v, w1_all, "w1_all");
+    need(v, w2_all, "w2_all");
+    need(v, workspace, "workspace");
+    if (!placement && max_per_device < 1) v.push_back("max_per_device < 1 with placement == NULL");
+    if (placement) {
+      if (placement->num_experts != desc->num_experts) v.push_back("placement->num_experts != E");
+      if (placement->num_devices != cm->world) v.push_back("placement->num_devices != world");
+      need(v, placement->replicas, "placement->replicas");
+      need(v, placement->replica_device, "placement->replica_device");
+      need(v, placement->hosted, "placement->hosted");
+    }
+    raise_if(v, "lina_moe_infer_forward");
+    if (workspace_bytes < infer_workspace_bytes(*desc, cm->world))
+      throw StatusError{LINA_ERR_WORKSPACE, "workspace too small"};
+    LINA_CUDA_CHECK(cudaSetDevice(cm->device));
+    infer_forward(cm, *desc, tokens, gate_w, w1_all, w2_all, out, placement, max_per_device,
+                  plan_out, workspace, workspace_bytes, (cudaStream_t)stream);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_sched_config(lina_comm* cm, lina_policy policy, size_t partition_bytes) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    if (policy != LINA_SCHED_BASELINE && policy != LINA_SCHED_LINA)
+      throw ArgError{"policy not LINA_SCHED_BASELINE/LINA_SCHED_LINA"};
+    if (cm->sched) sched_config(cm->sched, policy, partition_bytes);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_allreduce_submit(lina_comm* cm, void* grad, size_t count, lina_dtype dtype,
+                                  lina_stream ready_stream) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    if (!cm) v.push_back("comm is NULL");
+    need(v, grad, "grad");
+    if (dtype != LINA_F32 && dtype != LINA_BF16) v.push_back("dtype not LINA_F32/LINA_BF16");
+    raise_if(v, "lina_allreduce_submit");
+    if (count == 0 || !cm->sched) return LINA_OK;  // world == 1: the sum over one rank is itself
+    LINA_CUDA_CHECK(cudaSetDevice(cm->device));
+    sched_submit(cm->sched, grad, count, dtype, (cudaStream_t)ready_stream);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_allreduce_wait(lina_comm* cm, lina_stream stream) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    if (cm->sched) sched_wait(cm->sched, (cudaStream_t)stream);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_profile_enable(lina_comm* cm, int on) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    cm->prof = on != 0;
+    return LINA_OK;
+  });
+}
+
+lina_status lina_profile_read(lina_comm* cm, lina_profile* out) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    if (!out) throw ArgError{"out is NULL"};
+    double ms = 0.0;
+    int64_t phases = 0;
+    for (auto& pr : cm->prof_gemm) {
+      if (pr.second) {
+        LINA_CUDA_CHECK(cudaEventSynchronize(pr.second));
+        float t = 0.f;
+        LINA_CUDA_CHECK(cudaEventElapsedTime(&t, pr.first, pr.second));
+        ms += t;
+        ++phases;
+        cm->prof_pool.push_back(pr.second);
+      }
+      cm->prof_pool.push_back(pr.first);
+    }
+    cm->prof_gemm.clear();
+    out->kernel_launches = g_launches.exchange(0);
+    out->gemm_launches = cm->prof_gemm_launches;
+    out->gemm_ms = ms;
+    out->gemm_phases = phases;
+    cm->prof_gemm_launches = 0;
+    return LINA_OK;
+  });
+}
+
+lina_status lina_sched_stats(lina_comm* cm, int64_t* issued, int64_t* deferred) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    int64_t a = 0, b = 0;
+    if (cm->sched) sched_stats(cm->sched, &a, &b);
+    if (issued) *issued = a;
+    if (deferred) *deferred = b;
+    return LINA_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// Shared device/host helpers for the Lina B200 library (internal header).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace lina {
+
+// ---------------------------------------------------------------- error plumbing
+void set_error(const std::string& msg);           // thread-local message (api.cpp)
+
+struct CudaError {
+  std::string what;
+};
+
+#define LINA_CUDA_CHECK(expr)                                                              \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      throw ::lina::CudaError{std::string(#expr) + " -> " + cudaGetErrorString(_e) + " (" + \
+                              __FILE__ + ":" + std::to_string(__LINE__) + ")"};            \
+  } while (0)
+
+// Process-wide count of this library's kernel launches (lina_profile_read).
+void count_launch();
+#define LINA_LAUNCH_CHECK()                   \
+  do {                                        \
+    ::lina::count_launch();                   \
+    LINA_CUDA_CHECK(cudaGetLastError());      \
+  } while (0)
+
+// ---------------------------------------------------------------- dtype traits
+template <typename T> struct Elt;
+template <> struct Elt<float> {
+  __device__ __forceinline__ static float to_f(float x) { return x; }
+  __device__ __forceinline__ static float from_f(float x) { return x; }
+};
+template <> struct Elt<__nv_bfloat16> {
+  __device__ __forceinline__ static float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+  __device__ __forceinline__ static __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
+};
+
+// 16-byte vector of T (8 bf16 or 4 fp32)
+template <typename T> struct Vec16 {
+  static constexpr int N = 16 / sizeof(T);
+};
+
+__device__ __forceinline__ void load16(const void* p, float* out, const float*) {
+  float4 v = *reinterpret_cast<const float4*>(p);
+  out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+}
+__device__ __forceinline__ void load16(const void* p, float* out, const __nv_bfloat16*) {
+  uint4 v = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    out[2 * i] = f.x; out[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void store16(void* p, const float* in, float*) {
+  *reinterpret_cast<float4*>(p) = make_float4(in[0], in[1], in[2], in[3]);
+}
+__device__ __forceinline__ void store16(void* p, const float* in, __nv_bfloat16*) {
+  uint4 v;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(in[2 * i], in[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = v;
+}
+
+// ---------------------------------------------------------------- chunk geometry (R10)
+// Chunk c of n covers capacity slots [floor(c*C/n), floor((c+1)*C/n)).
+__host__ __device__ __forceinline__ int chunk_begin(int c, int C, int n) {
+  return (int)(((long long)c * C) / n);
+}
+// The chunk holding slot s: largest c with chunk_begin(c) <= s.
+__host__ __device__ __forceinline__ int chunk_of(int s, int C, int n) {
+  return (int)((((long long)s + 1) * n + C - 1) / C) - 1;
+}
+__host__ __device__ __forceinline__ int chunk_rows_max(int C, int n) { return (C + n - 1) / n; }
+
+}  // namespace lina

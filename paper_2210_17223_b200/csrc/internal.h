@@ -1,0 +1,80 @@
+// Internal host-side types of the Lina B200 library.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/lina.h"
+#include "common.h"
+
+namespace lina {
+
+struct NcclError {
+  std::string what;
+};
+struct ArgError {
+  std::string what;
+};
+struct StatusError {
+  lina_status status;
+  std::string what;
+};
+
+#define LINA_NCCL_CHECK(expr)                                                                  \
+  do {                                                                                         \
+    ncclResult_t _r = (expr);                                                                  \
+    if (_r != ncclSuccess)                                                                     \
+      throw ::lina::NcclError{std::string(#expr) + " -> " + ncclGetErrorString(_r) + " (" +    \
+                              __FILE__ + ":" + std::to_string(__LINE__) + ")"};                \
+  } while (0)
+
+class Scheduler;  // sched.cpp
+
+// Buffer plan for one descriptor on one communicator (layer.cpp).
+struct Plan {
+  int T, d, f, E, k, C, n, P, El, Cm, dt;  // dt = element bytes
+  bool bf16;
+  // offsets (bytes) into `saved`
+  size_t s_probs, s_idx, s_gate, s_slot, s_kept, s_tokof, s_recvkept, s_vcount, s_R, s_H, s_C;
+  size_t saved_bytes;
+  // offsets into `workspace`
+  size_t w_route, w_D, w_O, w_dg, w_dL, w_dwg, w_dS, w_dO, w_dH, w_dXe, w_dXs;
+  size_t ws_bytes;
+  size_t rows_send() const { return (size_t)n * E * Cm; }
+  size_t rows_recv() const { return (size_t)n * P * El * Cm; }
+};
+
+Plan make_plan(const lina_moe_desc& desc, int world);
+
+}  // namespace lina
+
+struct lina_comm {
+  int rank = 0, world = 1, device = 0, num_sms = 148;
+  ncclComm_t ep_disp = nullptr;  // dispatch-direction all-to-all micro-ops
+  ncclComm_t ep_comb = nullptr;  // combine-direction all-to-all micro-ops (full-duplex, H8)
+  ncclComm_t dp = nullptr;       // non-expert gradient allreduce micro-ops
+  cudaStream_t hi = nullptr;     // dispatch a2a (greatest priority)
+  cudaStream_t hi2 = nullptr;    // combine a2a (greatest priority)
+  cudaStream_t lo = nullptr;     // allreduce micro-ops (least priority)
+  std::vector<cudaEvent_t> ev;   // event pool (timing disabled)
+  lina::Scheduler* sched = nullptr;
+  // profiling (lina_profile_enable / lina_profile_read)
+  bool prof = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_gemm;  // recorded (start, end) pairs
+  std::vector<cudaEvent_t> prof_pool;                          // free timing events
+  int64_t prof_gemm_launches = 0;
+};
+
+namespace lina {
+// Profiling helpers (api.cpp): open/close one timed expert-GEMM phase on stream s.
+void prof_begin(lina_comm* cm, cudaStream_t s);
+void prof_end(lina_comm* cm, cudaStream_t s, int gemm_launches);
+}  // namespace lina

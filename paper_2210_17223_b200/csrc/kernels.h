@@ -1,0 +1,58 @@
+// Internal kernel launchers of the Lina B200 library.  All launches are
+// asynchronous on the given stream; they throw lina::CudaError on launch failure.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace lina {
+
+enum { kEpiNone = 0, kEpiRelu = 1, kEpiMask = 2 };
+
+// Row-grouped expert GEMM over the segments of one chunk (see gemm_simt.cu).
+struct RowGemm {
+  const void* A;       // [nseg_total][Cm][K]
+  const void* B;       // [El][N][K] (K-major) or [El][K][N] (MN-major)
+  void* D;             // [nseg_total][Cm][N]
+  const void* aux;     // [nseg_total][Cm][N] (kEpiMask: keep where aux > 0)
+  const int* vcount;   // [nseg_total] valid rows per segment
+  int seg0, nseg, El, Cm, N, K;
+};
+
+// Weight-gradient GEMM: D[El][M][N] = Σ_{c,s} Σ_{r < v} A[seg][r][:]ᵀ B[seg][r][:].
+struct WGrad {
+  const void* A;       // [nseg_total][Cm][M]
+  const void* B;       // [nseg_total][Cm][N]
+  void* D;             // [El][M][N]
+  const int* vcount;
+  int nchunks, P, El, Cm, M, N;
+};
+
+void launch_gate_topk(int dtype, const void* X, const float* Wg, int T, int d, int E, int k,
+                      int write_routing, float* probs, int* idx, float* gate, cudaStream_t s);
+
+size_t route_scratch_ints(int T, int k, int E);
+void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int* slot, int* counts,
+                  int* kept, int* tok_of, cudaStream_t s);
+// vcount[(c*P + s)*El + el] = clamp(recv_kept[s*El + el] - b_c, 0, Cc)
+void launch_vcount(const int* recv_kept, int P, int El, int C, int n, int* vcount, cudaStream_t s);
+
+void launch_permute(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
+                    int Cm, void* Send, cudaStream_t s);
+void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot, const float* gate,
+                    int T, int k, int d, int E, int C, int n, int Cm, void* Y, cudaStream_t s);
+void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* tok_of,
+                        const float* gate, int T, int k, int d, int E, int C, int n, int Cm,
+                        void* dSend, float* dg, cudaStream_t s);
+void launch_gate_bwd(const float* probs, const int* idx, const float* gate, const float* dg, int T,
+                     int k, int E, float* dL, cudaStream_t s);
+void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* dL,
+               const float* Wg, int T, int k, int d, int E, int C, int n, int Cm, void* dX,
+               cudaStream_t s);
+size_t dwg_scratch_floats(int T, int d, int E);
+void launch_dwg(int dtype, const void* X, const float* dL, int T, int d, int E, float* scratch,
+                float* dWg, cudaStream_t s);
+
+void launch_row_gemm_simt(int dtype, const RowGemm& p, bool b_kmajor, int epi, cudaStream_t s);
+void launch_wgrad_simt(int dtype, const WGrad& p, cudaStream_t s);
+
+}  // namespace lina

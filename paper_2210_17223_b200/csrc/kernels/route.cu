@@ -1,0 +1,130 @@
+// S2 (K2): capacity slot assignment — deterministic histogram + scan + in-warp ranks.
+//
+// Reading R5/R6 (the paper never states capacity):
+// per source rank, assignments are visited in priority order a = j*T + t (all
+// first choices in token order, then all second choices, ...); slot = number of
+// earlier assignments to the same expert; kept iff slot < C.
+//
+// Three tiny launches, all order-deterministic (atomics only count, never order):
+//   count : CTA b (1024 assignments) builds a shared-memory histogram  -> blockcnt[b][E]
+//   scan  : one thread per expert prefix-sums blockcnt over b            -> blockbase, counts, kept
+//   assign: CTA b re-ranks its assignments with __match_any_sync (rank among
+//           same-expert lanes below it) + per-warp counts prefix     -> slot[T,k], tok_of[E][C]
+// tok_of[e][s] = t*k + j of the assignment holding slot s (or -1): the inverse
+// map the row-parallel permute / combine-backward kernels gather through.
+#include "../common.h"
+#include "../kernels.h"
+
+namespace lina {
+namespace {
+
+constexpr int kRouteBlock = 1024;
+
+__global__ void __launch_bounds__(kRouteBlock) route_count_kernel(const int* __restrict__ idx, int T,
+                                                                 int k, int E,
+                                                                 int* __restrict__ blockcnt) {
+  __shared__ int h[64];
+  for (int i = threadIdx.x; i < E; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const long long a = (long long)blockIdx.x * kRouteBlock + threadIdx.x;
+  if (a < (long long)T * k) {
+    const int j = (int)(a / T), t = (int)(a % T);
+    atomicAdd(&h[idx[(size_t)t * k + j]], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) blockcnt[(size_t)blockIdx.x * E + i] = h[i];
+}
+
+__global__ void route_scan_kernel(const int* __restrict__ blockcnt, int nb, int E, int C,
+                                  int* __restrict__ blockbase, int* __restrict__ counts,
+                                  int* __restrict__ kept) {
+  const int e = threadIdx.x;
+  if (e >= E) return;
+  int run = 0;
+  for (int b = 0; b < nb; ++b) {
+    blockbase[(size_t)b * E + e] = run;
+    run += blockcnt[(size_t)b * E + e];
+  }
+  if (counts) counts[e] = run;
+  kept[e] = run < C ? run : C;
+}
+
+__global__ void __launch_bounds__(kRouteBlock) route_assign_kernel(
+    const int* __restrict__ idx, int T, int k, int E, int C, const int* __restrict__ blockbase,
+    int* __restrict__ slot, int* __restrict__ tok_of) {
+  __shared__ int wc[32][65];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 32 * 65; i += kRouteBlock) (&wc[0][0])[i] = 0;
+  __syncthreads();
+  const long long a = (long long)blockIdx.x * kRouteBlock + tid;
+  const bool valid = a < (long long)T * k;
+  int j = 0, t = 0, e = -1 - lane;  // distinct negative keys never match
+  if (valid) {
+    j = (int)(a / T);
+    t = (int)(a % T);
+    e = idx[(size_t)t * k + j];
+  }
+  const unsigned mask = __match_any_sync(0xffffffffu, e);
+  const unsigned lt = (1u << lane) - 1u;
+  const int rank = __popc(mask & lt);
+  if (valid && lane == __ffs(mask) - 1) wc[warp][e] = __popc(mask);
+  __syncthreads();
+  if (valid) {
+    int pre = 0;
+    for (int w = 0; w < warp; ++w) pre += wc[w][e];
+    const int s = blockbase[(size_t)blockIdx.x * E + e] + pre + rank;
+    const int code = t * k + j;
+    if (s < C) {
+      slot[code] = s;
+      tok_of[(size_t)e * C + s] = code;
+    } else {
+      slot[code] = -1;
+    }
+  }
+}
+
+__global__ void vcount_kernel(const int* __restrict__ recv_kept, int P, int El, int C, int n,
+                              int* __restrict__ vcount) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * P * El) return;
+  const int se = i % (P * El);  // s*El + el
+  const int c = i / (P * El);
+  const int b = chunk_begin(c, C, n), Cc = chunk_begin(c + 1, C, n) - b;
+  int v = recv_kept[se] - b;
+  vcount[i] = v < 0 ? 0 : (v > Cc ? Cc : v);
+}
+
+}  // namespace
+
+void launch_vcount(const int* recv_kept, int P, int El, int C, int n, int* vcount, cudaStream_t s) {
+  const int tot = n * P * El;
+  if (tot <= 0) return;
+  vcount_kernel<<<(tot + 255) / 256, 256, 0, s>>>(recv_kept, P, El, C, n, vcount);
+  LINA_LAUNCH_CHECK();
+}
+
+size_t route_scratch_ints(int T, int k, int E) {
+  const long long nb = ((long long)T * k + kRouteBlock - 1) / kRouteBlock;
+  return (size_t)(2 * nb * E);
+}
+
+void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int* slot, int* counts,
+                  int* kept, int* tok_of, cudaStream_t s) {
+  LINA_CUDA_CHECK(cudaMemsetAsync(tok_of, 0xff, sizeof(int) * (size_t)E * C, s));
+  if (T <= 0) {
+    LINA_CUDA_CHECK(cudaMemsetAsync(kept, 0, sizeof(int) * E, s));
+    if (counts) LINA_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(int) * E, s));
+    return;
+  }
+  const int nb = (int)(((long long)T * k + kRouteBlock - 1) / kRouteBlock);
+  int* blockcnt = scratch;
+  int* blockbase = scratch + (size_t)nb * E;
+  route_count_kernel<<<nb, kRouteBlock, 0, s>>>(idx, T, k, E, blockcnt);
+  LINA_LAUNCH_CHECK();
+  route_scan_kernel<<<1, 64, 0, s>>>(blockcnt, nb, E, C, blockbase, counts, kept);
+  LINA_LAUNCH_CHECK();
+  route_assign_kernel<<<nb, kRouteBlock, 0, s>>>(idx, T, k, E, C, blockbase, slot, tok_of);
+  LINA_LAUNCH_CHECK();
+}
+
+}  // namespace lina

@@ -1,0 +1,299 @@
+// The MoE layer pipeline: forward (S1-S7) and backward (S8) with the Lina
+// micro-op pipelining of the all-to-all against the expert GEMMs.
+//
+// Forward, per rank ("the expert can start computing with a
+// subset of the tokens after one all-to-all micro-op"; "FFN is ready to
+// start right after each all-to-all micro-op"):
+//   s  : gate+softmax+top-k -> route (slot, tok_of) -> permute into Send[n][E][Cm][d]
+//   hi : count all-to-all (kept[E] -> recv_kept[P][E_l])
+//   for c: hi : all-to-all Send[c] -> Recv[c]                     (dispatch micro-op)
+//   for c: s  : wait dispatch c; GEMM1+ReLU, GEMM2 on Recv[c]      (expert micro-op)
+//   for c: hi2: wait GEMM c; all-to-all Out[c] -> Back[c]          (combine micro-op)
+//   s  : wait combine n-1; weighted un-permute -> y
+// Host enqueue order is all dispatches, then GEMMs, then combines (H8 in
+// SURVEY.md): NCCL runs one communicator's operations in issue order, so an
+// interleaved order would make dispatch c+1 wait behind combine c.  Dispatch and
+// combine use separate communicators/streams so both link directions overlap.
+// The host only enqueues: no host<->device synchronisation anywhere, so the
+// whole sequence is CUDA-graph capturable.  At P = 1 there is no collective and
+// Recv/Back alias Send/Out.
+#include <cstring>
+
+#include "internal.h"
+#include "kernels.h"
+#include "layer.h"
+
+namespace lina {
+
+static size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+Plan make_plan(const lina_moe_desc& dsc, int world) {
+  Plan p{};
+  p.T = dsc.num_tokens;
+  p.d = dsc.d_model;
+  p.f = dsc.d_ffn;
+  p.E = dsc.num_experts;
+  p.k = dsc.k;
+  p.C = dsc.capacity;
+  p.n = dsc.n_chunks;
+  p.P = world;
+  p.El = dsc.num_experts / world;
+  p.Cm = chunk_rows_max(p.C, p.n);
+  p.bf16 = dsc.dtype == LINA_BF16;
+  p.dt = p.bf16 ? 2 : 4;
+  const size_t T = p.T, k = p.k, E = p.E;
+  const size_t send_rows = p.rows_send(), recv_rows = p.rows_recv();
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align_up(o + bytes);
+    return at;
+  };
+  // ---- saved (forward -> backward)
+  p.s_probs = take(4 * T * E);
+  p.s_idx = take(4 * T * k);
+  p.s_gate = take(4 * T * k);
+  p.s_slot = take(4 * T * k);
+  p.s_kept = take(4 * E);
+  p.s_tokof = take(4 * E * (size_t)p.C);
+  p.s_recvkept = take(4 * (size_t)p.P * p.El);
+  p.s_vcount = take(4 * (size_t)p.n * p.P * p.El);
+  p.s_R = take(recv_rows * p.d * p.dt);                       // routed tokens (X rows)
+  p.s_H = take(recv_rows * (size_t)p.f * p.dt);               // relu(X W1ᵀ)
+  p.s_C = take(send_rows * p.d * p.dt);                       // returned expert outputs
+  p.saved_bytes = o;
+  // ---- workspace
+  o = 0;
+  p.w_route = take(4 * route_scratch_ints(p.T, p.k, p.E));
+  p.w_D = (p.P > 1) ? take(send_rows * p.d * p.dt) : 0;       // send buffer (P=1: = R)
+  p.w_O = (p.P > 1) ? take(recv_rows * p.d * p.dt) : 0;       // expert outputs (P=1: = C)
+  p.w_dg = take(4 * T * k);
+  p.w_dL = take(4 * T * E);
+  p.w_dwg = take(4 * dwg_scratch_floats(p.T, p.d, p.E));
+  p.w_dS = take(send_rows * p.d * p.dt);                      // g·dY rows, send layout
+  p.w_dO = (p.P > 1) ? take(recv_rows * p.d * p.dt) : 0;      // (P=1: = dS)
+  p.w_dH = take(recv_rows * (size_t)p.f * p.dt);
+  p.w_dXe = take(recv_rows * p.d * p.dt);
+  p.w_dXs = (p.P > 1) ? take(send_rows * p.d * p.dt) : 0;     // (P=1: = dXe)
+  p.ws_bytes = o;
+  return p;
+}
+
+namespace {
+
+struct Ptrs {
+  float* probs; int* idx; float* gate; int* slot; int* kept; int* tok_of; int* recv_kept;
+  int* vcount; char* R; char* H; char* Cb;
+  int* route; char* D; char* O; float* dg; float* dL; float* dwg; char* dS; char* dO; char* dH;
+  char* dXe; char* dXs;
+};
+
+Ptrs carve(const Plan& p, void* saved, void* ws) {
+  char* sv = (char*)saved;
+  char* w = (char*)ws;
+  Ptrs q{};
+  if (sv) {
+    q.probs = (float*)(sv + p.s_probs);
+    q.idx = (int*)(sv + p.s_idx);
+    q.gate = (float*)(sv + p.s_gate);
+    q.slot = (int*)(sv + p.s_slot);
+    q.kept = (int*)(sv + p.s_kept);
+    q.tok_of = (int*)(sv + p.s_tokof);
+    q.recv_kept = (int*)(sv + p.s_recvkept);
+    q.vcount = (int*)(sv + p.s_vcount);
+    q.R = sv + p.s_R;
+    q.H = sv + p.s_H;
+    q.Cb = sv + p.s_C;
+  }
+  if (w) {
+    q.route = (int*)(w + p.w_route);
+    q.D = p.P > 1 ? w + p.w_D : q.R;
+    q.O = p.P > 1 ? w + p.w_O : q.Cb;
+    q.dg = (float*)(w + p.w_dg);
+    q.dL = (float*)(w + p.w_dL);
+    q.dwg = (float*)(w + p.w_dwg);
+    q.dS = w + p.w_dS;
+    q.dO = p.P > 1 ? w + p.w_dO : q.dS;
+    q.dH = w + p.w_dH;
+    q.dXe = w + p.w_dXe;
+    q.dXs = p.P > 1 ? w + p.w_dXs : q.dXe;
+  }
+  return q;
+}
+
+ncclDataType_t nccl_dt(const Plan& p) { return p.bf16 ? ncclBfloat16 : ncclFloat32; }
+
+// Equal-split all-to-all of chunk c of a send-layout buffer ([n][E][Cm][w]) into a
+// receive-layout buffer ([n][P][E_l][Cm][w]).  Per peer: E_l*Cm*w elements.
+void a2a_send_to_recv(const Plan& p, const char* send, char* recv, int w, int c, ncclComm_t comm,
+                      cudaStream_t st) {
+  const size_t per_peer = (size_t)p.El * p.Cm * w;
+  const size_t chunk = per_peer * p.P;  // = E*Cm*w = P*El*Cm*w
+  LINA_NCCL_CHECK(ncclAlltoAll(send + c * chunk * p.dt, recv + c * chunk * p.dt, per_peer,
+                               nccl_dt(p), comm, st));
+}
+// Reverse: receive layout chunk c -> send layout chunk c (same sizes).
+void a2a_recv_to_send(const Plan& p, const char* recv, char* send, int w, int c, ncclComm_t comm,
+                      cudaStream_t st) {
+  a2a_send_to_recv(p, recv, send, w, c, comm, st);
+}
+
+void row_gemm(const Plan& p, const void* A, const void* B, void* D, const void* aux,
+              const int* vcount, int c, int N, int K, bool b_kmajor, int epi, cudaStream_t st) {
+  RowGemm g{};
+  g.A = A;
+  g.B = B;
+  g.D = D;
+  g.aux = aux;
+  g.vcount = vcount;
+  g.seg0 = c * p.P * p.El;
+  g.nseg = p.P * p.El;
+  g.El = p.El;
+  g.Cm = p.Cm;
+  g.N = N;
+  g.K = K;
+  launch_expert_row_gemm(p.bf16 ? 1 : 0, g, b_kmajor, epi, st);
+}
+
+}  // namespace
+
+void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* gate_w,
+                 const void* w1, const void* w2, void* out, void* saved, void* ws,
+                 lina_route* route, cudaStream_t s) {
+  Ptrs q = carve(p, saved, ws);
+  const int dtype = p.bf16 ? 1 : 0;
+  const bool override_r = route && route->override_routing;
+  if (override_r) {
+    LINA_CUDA_CHECK(cudaMemcpyAsync(q.idx, route->idx, 4 * (size_t)p.T * p.k,
+                                    cudaMemcpyDeviceToDevice, s));
+    LINA_CUDA_CHECK(cudaMemcpyAsync(q.gate, route->gate, 4 * (size_t)p.T * p.k,
+                                    cudaMemcpyDeviceToDevice, s));
+  }
+  // S1 gate, S2 route, S3 permute
+  launch_gate_topk(dtype, tokens, gate_w, p.T, p.d, p.E, p.k, override_r ? 0 : 1, q.probs, q.idx,
+                   q.gate, s);
+  launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr,
+               q.kept, q.tok_of, s);
+  launch_permute(dtype, tokens, q.tok_of, p.k, p.d, p.E, p.C, p.n, p.Cm, q.D, s);
+  if (route) {
+    if (route->idx && !override_r)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->idx, q.idx, 4 * (size_t)p.T * p.k,
+                                      cudaMemcpyDeviceToDevice, s));
+    if (route->gate && !override_r)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->gate, q.gate, 4 * (size_t)p.T * p.k,
+                                      cudaMemcpyDeviceToDevice, s));
+    if (route->slot)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->slot, q.slot, 4 * (size_t)p.T * p.k,
+                                      cudaMemcpyDeviceToDevice, s));
+    if (route->probs)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->probs, q.probs, 4 * (size_t)p.T * p.E,
+                                      cudaMemcpyDeviceToDevice, s));
+  }
+  if (p.P == 1) {
+    // All experts local: the "all-to-all" is the identity and chunks only re-slice the GEMMs.
+    launch_vcount(q.kept, 1, p.E, p.C, p.n, q.vcount, s);
+    prof_begin(cm, s);
+    for (int c = 0; c < p.n; ++c) {
+      row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, c, p.f, p.d, true, kEpiRelu, s);
+      row_gemm(p, q.H, w2, q.O, nullptr, q.vcount, c, p.d, p.f, true, kEpiNone, s);
+    }
+    prof_end(cm, s, 2 * p.n);
+    launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, p.n, p.Cm, out, s);
+    return;
+  }
+  // ---- P > 1: pipelined micro-ops
+  cudaEvent_t* ev = cm->ev.data();
+  const int n = p.n;
+  cudaEvent_t e_perm = ev[0], e_cnt = ev[1], e_end = ev[2];
+  cudaEvent_t* e_disp = ev + 3;
+  cudaEvent_t* e_gemm = ev + 3 + n;
+  LINA_CUDA_CHECK(cudaEventRecord(e_perm, s));
+  LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi, e_perm, 0));
+  LINA_NCCL_CHECK(ncclAlltoAll(q.kept, q.recv_kept, (size_t)p.El, ncclInt32, cm->ep_disp, cm->hi));
+  LINA_CUDA_CHECK(cudaEventRecord(e_cnt, cm->hi));
+  for (int c = 0; c < n; ++c) {
+    a2a_send_to_recv(p, q.D, q.R, p.d, c, cm->ep_disp, cm->hi);
+    LINA_CUDA_CHECK(cudaEventRecord(e_disp[c], cm->hi));
+  }
+  LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_cnt, 0));
+  launch_vcount(q.recv_kept, p.P, p.El, p.C, n, q.vcount, s);
+  for (int c = 0; c < n; ++c) {
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_disp[c], 0));
+    prof_begin(cm, s);
+    row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, c, p.f, p.d, true, kEpiRelu, s);
+    row_gemm(p, q.H, w2, q.O, nullptr, q.vcount, c, p.d, p.f, true, kEpiNone, s);
+    prof_end(cm, s, 2);
+    LINA_CUDA_CHECK(cudaEventRecord(e_gemm[c], s));
+  }
+  for (int c = 0; c < n; ++c) {
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi2, e_gemm[c], 0));
+    a2a_recv_to_send(p, q.O, q.Cb, p.d, c, cm->ep_comb, cm->hi2);
+  }
+  LINA_CUDA_CHECK(cudaEventRecord(e_end, cm->hi2));
+  LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_end, 0));
+  launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, p.n, p.Cm, out, s);
+}
+
+void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* dout,
+                  const void* tokens, const float* gate_w, const void* w1, const void* w2,
+                  void* dtokens, float* dgate_w, void* dw1, void* dw2, void* ws, cudaStream_t s) {
+  Ptrs q = carve(p, const_cast<void*>(saved), ws);
+  const int dtype = p.bf16 ? 1 : 0;
+  const int n = p.n;
+  // (a) combine backward: dg and g·dY rows into the send layout
+  launch_combine_bwd(dtype, dout, q.Cb, q.tok_of, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, q.dS,
+                     q.dg, s);
+  // the scheduler stops admitting allreduce micro-ops: all-to-all is imminent
+  if (cm->sched) sched_a2a_imminent(cm);
+  WGrad wg2{q.dO, q.H, dw2, q.vcount, n, p.P, p.El, p.Cm, p.d, p.f};
+  WGrad wg1{q.dH, q.R, dw1, q.vcount, n, p.P, p.El, p.Cm, p.f, p.d};
+  if (p.P == 1) {
+    prof_begin(cm, s);
+    for (int c = 0; c < n; ++c) {
+      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, c, p.f, p.d, false, kEpiMask, s);
+      row_gemm(p, q.dH, w1, q.dXe, nullptr, q.vcount, c, p.d, p.f, false, kEpiNone, s);
+    }
+    launch_expert_wgrad(dtype, wg2, s);
+    launch_expert_wgrad(dtype, wg1, s);
+    prof_end(cm, s, 2 * n + 2);
+  } else {
+    cudaEvent_t* ev = cm->ev.data();
+    cudaEvent_t e_cb = ev[0], e_end = ev[1], e_wg = ev[2];
+    cudaEvent_t* e_disp = ev + 3;
+    cudaEvent_t* e_gemm = ev + 3 + n;
+    LINA_CUDA_CHECK(cudaEventRecord(e_cb, s));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi, e_cb, 0));
+    if (cm->sched) sched_a2a_begin(cm, cm->hi);
+    for (int c = 0; c < n; ++c) {
+      a2a_send_to_recv(p, q.dS, q.dO, p.d, c, cm->ep_disp, cm->hi);
+      LINA_CUDA_CHECK(cudaEventRecord(e_disp[c], cm->hi));
+    }
+    for (int c = 0; c < n; ++c) {
+      LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_disp[c], 0));
+      prof_begin(cm, s);
+      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, c, p.f, p.d, false, kEpiMask, s);
+      row_gemm(p, q.dH, w1, q.dXe, nullptr, q.vcount, c, p.d, p.f, false, kEpiNone, s);
+      prof_end(cm, s, 2);
+      LINA_CUDA_CHECK(cudaEventRecord(e_gemm[c], s));
+    }
+    for (int c = 0; c < n; ++c) {
+      LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi2, e_gemm[c], 0));
+      a2a_recv_to_send(p, q.dXe, q.dXs, p.d, c, cm->ep_comb, cm->hi2);
+    }
+    LINA_CUDA_CHECK(cudaEventRecord(e_end, cm->hi2));
+    if (cm->sched) sched_a2a_end(cm, cm->hi2);
+    // weight gradients after every chunk: off the critical path, overlap the last combine a2a
+    prof_begin(cm, s);
+    launch_expert_wgrad(dtype, wg2, s);
+    launch_expert_wgrad(dtype, wg1, s);
+    prof_end(cm, s, 2);
+    LINA_CUDA_CHECK(cudaEventRecord(e_wg, s));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_end, 0));
+  }
+  // (e)+(f): gate backward, gather-sum dX, dWg
+  launch_gate_bwd(q.probs, q.idx, q.gate, q.dg, p.T, p.k, p.E, q.dL, s);
+  launch_dx(dtype, q.dXs, q.idx, q.slot, q.dL, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm, dtokens, s);
+  launch_dwg(dtype, tokens, q.dL, p.T, p.d, p.E, q.dwg, dgate_w, s);
+}
+
+}  // namespace lina

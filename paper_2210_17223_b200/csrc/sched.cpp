@@ -1,0 +1,199 @@
+// S9: the micro-op communication scheduler (§3-§4; §6.1).
+//
+// "Lina's communication scheduler for training is deployed on all devices and runs
+// a single thread ... no coordination is needed across the scheduler instances"
+// (P:495-496).  "Each scheduler instance maintains a priority queue to schedule the
+// micro-ops.  The micro-op size is passed in as a hyperparameter".
+// "Lina partitions each gradient tensor into equal-sized small chunks and executes
+// individual allreduce micro-ops independently"; "We avoid putting chunks
+// from different gradients into the same micro-op".  Priority: an
+// allreduce micro-op is launched only while no all-to-all is waiting or ongoing
+// (P:249), and "the scheduler stops launching allreduce micro-ops if the
+// combining computation in backward pass [starts], since this implies all-to-all is
+// imminent".
+//
+// B200 design: the all-to-all micro-ops are enqueued by the layer on the
+// high-priority streams (the "a2a > allreduce" queue order is structural: the
+// layer never waits on the scheduler).  This thread owns the DP communicator and
+// the low-priority stream.  Micro-ops are pointer offsets into the caller's
+// gradient (no chunk/cat copies).  It polls CUDA events (never
+// blocks the device) for (a) gradient readiness and (b) completion of the
+// registered all-to-all phase, and issues ncclAllReduce micro-ops only when the
+// LINA admission rule holds.  BASELINE issues whole gradients immediately, gated
+// on readiness only on the device (fair-sharing the links).
+#include <chrono>
+
+#include "layer.h"
+
+namespace lina {
+
+struct ArJob {
+  char* ptr;
+  size_t count;      // elements
+  size_t elt;        // bytes per element
+  ncclDataType_t dt;
+  cudaEvent_t ready;
+  size_t next = 0;   // next element offset to issue
+};
+
+class Scheduler {
+ public:
+  explicit Scheduler(lina_comm* cm) : cm_(cm) { thread_ = std::thread([this] { run(); }); }
+  ~Scheduler() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    thread_.join();
+    for (auto& j : jobs_) cudaEventDestroy(j.ready);
+    for (auto e : a2a_events_) cudaEventDestroy(e);
+  }
+  void config(lina_policy pol, size_t bytes) {
+    std::lock_guard<std::mutex> g(mu_);
+    policy_ = pol;
+    partition_bytes_ = bytes ? bytes : (size_t)30 << 20;
+  }
+  void submit(void* grad, size_t count, lina_dtype dt, cudaStream_t ready_stream) {
+    ArJob j{};
+    j.ptr = (char*)grad;
+    j.count = count;
+    j.elt = dt == LINA_BF16 ? 2 : 4;
+    j.dt = dt == LINA_BF16 ? ncclBfloat16 : ncclFloat32;
+    LINA_CUDA_CHECK(cudaEventCreateWithFlags(&j.ready, cudaEventDisableTiming));
+    LINA_CUDA_CHECK(cudaEventRecord(j.ready, ready_stream));
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      jobs_.push_back(j);
+      ++outstanding_;
+    }
+    cv_.notify_all();
+  }
+  void a2a_imminent() {
+    std::lock_guard<std::mutex> g(mu_);
+    imminent_ = true;
+  }
+  // The all-to-all phase ends when `a2a_stream` reaches this point.
+  void a2a_end(cudaStream_t a2a_stream) {
+    cudaEvent_t e;
+    LINA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    LINA_CUDA_CHECK(cudaEventRecord(e, a2a_stream));
+    std::lock_guard<std::mutex> g(mu_);
+    a2a_events_.push_back(e);
+    cv_.notify_all();
+  }
+  // Block the host until every submitted job is fully issued, then make `s` wait.
+  void wait(cudaStream_t s) {
+    std::unique_lock<std::mutex> g(mu_);
+    cv_.wait(g, [&] { return outstanding_ == 0 || !err_.empty(); });
+    if (!err_.empty()) {
+      std::string e = err_;
+      err_.clear();
+      throw NcclError{e};
+    }
+    g.unlock();
+    cudaEvent_t e;
+    LINA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    LINA_CUDA_CHECK(cudaEventRecord(e, cm_->lo));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e, 0));
+    LINA_CUDA_CHECK(cudaEventDestroy(e));
+  }
+  void stats(int64_t* issued, int64_t* deferred) {
+    std::lock_guard<std::mutex> g(mu_);
+    *issued = issued_;
+    *deferred = deferred_;
+    issued_ = deferred_ = 0;
+  }
+
+ private:
+  // true while an all-to-all is queued or in flight (LINA admission rule)
+  bool a2a_busy_locked() {
+    while (!a2a_events_.empty()) {
+      cudaError_t q = cudaEventQuery(a2a_events_.front());
+      if (q == cudaErrorNotReady) return true;
+      cudaEventDestroy(a2a_events_.front());
+      a2a_events_.erase(a2a_events_.begin());
+      if (a2a_events_.empty()) imminent_ = false;  // the a2a phase has drained
+    }
+    return imminent_;
+  }
+  void run() {
+    std::unique_lock<std::mutex> g(mu_);
+    while (true) {
+      if (stop_) return;
+      if (jobs_.empty()) {
+        cv_.wait(g);
+        continue;
+      }
+      ArJob& j = jobs_.front();
+      const bool lina = policy_ == LINA_SCHED_LINA;
+      bool can_issue = true;
+      if (lina) {
+        if (cudaEventQuery(j.ready) == cudaErrorNotReady) can_issue = false;
+        else if (a2a_busy_locked()) {
+          can_issue = false;
+          ++deferred_;
+        }
+      }
+      if (!can_issue) {
+        g.unlock();
+        std::this_thread::sleep_for(std::chrono::microseconds(10));
+        g.lock();
+        continue;
+      }
+      size_t cnt = j.count - j.next;
+      if (lina) cnt = std::min(cnt, std::max<size_t>(1, partition_bytes_ / j.elt));
+      try {
+        if (j.next == 0) LINA_CUDA_CHECK(cudaStreamWaitEvent(cm_->lo, j.ready, 0));
+        char* p = j.ptr + j.next * j.elt;
+        LINA_NCCL_CHECK(ncclAllReduce(p, p, cnt, j.dt, ncclSum, cm_->dp, cm_->lo));
+      } catch (NcclError& e) {
+        err_ = e.what;
+      } catch (CudaError& e) {
+        err_ = e.what;
+      }
+      ++issued_;
+      j.next += cnt;
+      if (j.next >= j.count || !err_.empty()) {
+        cudaEventDestroy(j.ready);
+        jobs_.pop_front();
+        --outstanding_;
+        cv_.notify_all();
+      }
+    }
+  }
+
+  lina_comm* cm_;
+  std::thread thread_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<ArJob> jobs_;
+  std::vector<cudaEvent_t> a2a_events_;
+  lina_policy policy_ = LINA_SCHED_LINA;
+  size_t partition_bytes_ = (size_t)30 << 20;
+  bool imminent_ = false, stop_ = false;
+  int outstanding_ = 0;
+  int64_t issued_ = 0, deferred_ = 0;
+  std::string err_;
+};
+
+Scheduler* sched_create(lina_comm* cm) { return new Scheduler(cm); }
+void sched_destroy(Scheduler* s) { delete s; }
+void sched_config(Scheduler* s, lina_policy p, size_t b) { s->config(p, b); }
+void sched_submit(Scheduler* s, void* g, size_t c, lina_dtype dt, cudaStream_t rs) {
+  s->submit(g, c, dt, rs);
+}
+void sched_wait(Scheduler* s, cudaStream_t st) { s->wait(st); }
+void sched_stats(Scheduler* s, int64_t* i, int64_t* d) { s->stats(i, d); }
+
+void sched_a2a_imminent(lina_comm* cm) {
+  if (cm->sched) cm->sched->a2a_imminent();
+}
+void sched_a2a_begin(lina_comm* cm, cudaStream_t) {
+  if (cm->sched) cm->sched->a2a_imminent();
+}
+void sched_a2a_end(lina_comm* cm, cudaStream_t a2a_stream) {
+  if (cm->sched) cm->sched->a2a_end(a2a_stream);
+}
+
+}  // namespace lina

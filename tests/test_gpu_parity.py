@@ -1,0 +1,166 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Routing (idx, slot, counts) must match bit-exactly; outputs and
+gradients within the north_star tolerances (fp32 1e-5, bf16 2e-2, normwise)."""
+import numpy as np
+import pytest
+import torch
+
+import lina_inputs as li
+from oracle import moe
+from tests.parity_util import TOL, compare, gpu_layer, oracle_layer, to_dev, tdtype
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(name, tokens=None, seed=1234, family="grid", **changes):
+    cfg = li.CONFIGS[name]
+    if tokens is not None or changes:
+        cfg = li.with_tokens(cfg, tokens or cfg.tokens_per_rank, **changes)
+    Wg, W1, W2 = li.layer_weights(cfg, seed, family)
+    X, dY = li.layer_tokens(cfg, seed, 0, family)
+    return cfg, X, Wg, W1, W2, dY
+
+
+@pytest.mark.parametrize("n_chunks", [1, 4])
+def test_c1_full_fwd_bwd(n_chunks):
+    """configs[0] at full size: fp32, 4 experts, top-1, capacity factor 1.0 (drops occur)."""
+    cfg, X, Wg, W1, W2, dY = _case("C1")
+    g = gpu_layer(cfg, n_chunks, X, Wg, W1, W2, dY)
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY)
+    assert (o["fw"].slot < 0).any()
+    compare(cfg, g, o)
+
+
+def test_c1_chunk_invariance_bitwise():
+    """P8: n_chunks only re-slices the GEMMs; outputs and gradients are bitwise equal."""
+    cfg, X, Wg, W1, W2, dY = _case("C1")
+    a = gpu_layer(cfg, 1, X, Wg, W1, W2, dY)
+    for n in (2, 4, 7):
+        b = gpu_layer(cfg, n, X, Wg, W1, W2, dY)
+        for key in ("y", "dx", "dwg", "dw1", "dw2", "idx", "slot"):
+            assert np.array_equal(a[key], b[key]), (n, key)
+
+
+@pytest.mark.parametrize("k,capacity", [(1, 512), (2, 128), (2, 1), (3, 300)])
+def test_c1_variants(k, capacity):
+    cfg, X, Wg, W1, W2, dY = _case("C1", k=k)
+    g = gpu_layer(cfg, 2 if capacity > 1 else 1, X, Wg, W1, W2, dY, capacity=capacity)
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY, capacity=capacity)
+    compare(cfg, g, o)
+
+
+@pytest.mark.parametrize("tokens", [1, 63, 333])
+def test_ragged_token_counts(tokens):
+    cfg, X, Wg, W1, W2, dY = _case("C1", tokens=tokens, k=2)
+    g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY)
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY)
+    compare(cfg, g, o)
+
+
+@pytest.mark.parametrize("n_chunks", [1, 3])
+def test_c2_reduced_bf16(n_chunks):
+    """configs[1] shapes (E=8, top-2, d=768, f=3072, bf16) at 512 tokens."""
+    cfg, X, Wg, W1, W2, dY = _case("C2", tokens=512)
+    g = gpu_layer(cfg, n_chunks, X, Wg, W1, W2, dY)
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY)
+    compare(cfg, g, o)
+
+
+def test_c3_reduced_bf16():
+    """configs[2] shapes (E=16, top-2, d=1024, f=4096, capacity 1.25) at 256 tokens."""
+    cfg, X, Wg, W1, W2, dY = _case("C3", tokens=256)
+    g = gpu_layer(cfg, 2, X, Wg, W1, W2, dY)
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY)
+    compare(cfg, g, o)
+
+
+def test_c5_reduced_bf16_forward():
+    """configs[4] shapes (E=64, top-2, d=2048, f=8192) at 128 tokens: forward parity."""
+    cfg, X, Wg, W1, W2, dY = _case("C5", tokens=128)
+    g = gpu_layer(cfg, 1, X, Wg, W1, W2)
+    o = oracle_layer(cfg, X, Wg, W1, W2)
+    compare(cfg, g, o, check_bwd=False)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_identity_experts_roundtrip(dtype):
+    """P5 on the GPU: combine(dispatch(x)) = x · Σ_kept g within one ulp of dtype."""
+    cfg, X, Wg, _, _, _ = _case("C1", tokens=300, k=2, dtype=dtype)
+    d, f, E = cfg.d_model, cfg.d_ffn, cfg.num_experts
+    W1 = np.zeros((E, f, d), np.float32); W2 = np.zeros((E, d, f), np.float32)
+    for e in range(E):
+        W1[e, :d] = np.eye(d); W1[e, d:2 * d] = -np.eye(d)
+        W2[e, :, :d] = np.eye(d); W2[e, :, d:2 * d] = -np.eye(d)
+    g = gpu_layer(cfg, 2, X, Wg, W1, W2)
+    gsum = (g["gate"] * (g["slot"] >= 0)).sum(1, keepdims=True).astype(np.float64)
+    ref = X.astype(np.float64) * gsum
+    ulp = 2.0 ** -8 if dtype == "bf16" else 2.0 ** -23
+    assert np.all(np.abs(g["y"] - ref) <= ulp * np.abs(ref) + 1e-30)
+    assert (g["slot"] < 0).any()
+
+
+def test_override_routing_non_grid_inputs():
+    """Non-grid (balanced) inputs: routing is fed from the oracle so the FFN/combine/backward
+    arithmetic is compared on identical assignments."""
+    cfg, X, Wg, W1, W2, dY = _case("C2", tokens=256, family="balanced")
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY)
+    g = gpu_layer(cfg, 2, X, Wg, W1, W2, dY, override=(o["fw"].idx, o["fw"].gate))
+    tol = TOL["bf16"]
+    from tests.parity_util import assert_close
+    assert np.array_equal(g["slot"], o["fw"].slot)
+    assert_close(g["y"], o["fw"].y, tol, "y")
+    assert_close(g["dw1"], o["bw"].dW1, tol, "dW1")
+    assert_close(g["dw2"], o["bw"].dW2, tol, "dW2")
+
+
+def test_c2_full_size_sampled():
+    """configs[1] at full size (8192 tokens, the bench launch configuration, n_chunks=1):
+    routing bit-exact on every token; y and dX on a sample of tokens computed one by one."""
+    cfg, X, Wg, W1, W2, dY = _case("C2")
+    g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY)
+    L = moe.gate_logits(X, Wg)
+    p = moe.softmax(L)
+    idx = moe.top_k(L, cfg.k)
+    gate = moe.gate_weights(p, idx)
+    slot, counts = moe.capacity_slots(idx, cfg.num_experts, cfg.capacity())
+    assert np.array_equal(g["idx"], idx)
+    assert np.array_equal(g["slot"], slot)
+    assert np.array_equal(g["counts"], counts)
+    rng = np.random.default_rng(0)
+    sample = np.concatenate([[0, cfg.tokens_per_rank - 1], rng.choice(cfg.tokens_per_rank - 1, 62, replace=False) + 1])
+    Xs, dYs = X[sample], dY[sample]
+    rf = moe.RankForward(L=L[sample], p=p[sample], idx=idx[sample], gate=gate[sample], slot=slot[sample],
+                         counts=counts, y=np.zeros((len(sample), cfg.d_model)))
+    for n, t in enumerate(sample):
+        for j in range(cfg.k):
+            if slot[t, j] >= 0:
+                e = idx[t, j]
+                h, o = moe.expert_ffn(X[t:t + 1], W1[e], W2[e], "bf16")
+                rf.h[(n, j)] = h[0]
+                rf.o[(n, j)] = o[0]
+    rf.y = moe.combine(rf, cfg.k, "bf16")
+    bw = moe.moe_backward([rf], [Xs], [dYs], Wg, W1, W2, cfg.k, "bf16")   # dX rows are per-token exact
+    from tests.parity_util import assert_close
+    assert_close(g["y"][sample], rf.y, TOL["bf16"], "y (sampled)")
+    assert_close(g["dx"][sample], bw.dXs[0], TOL["bf16"], "dX (sampled)")
+
+
+def test_comm_and_errors():
+    import paper_2210_17223_b200 as lina
+    comm = lina.Comm(1, 0, 0)
+    bad = lina.make_desc(10, 30, 64, 5, 9, 0, 4, "bf16")
+    with pytest.raises(lina.LinaError) as ei:
+        lina.lina_moe_workspace_size(comm, bad)
+    msg = str(ei.value)
+    for frag in ["k not in", "capacity < 1", "n_chunks", "d_model % 16"]:
+        assert frag in msg, msg
+    good = lina.make_desc(64, 64, 256, 4, 1, 16, 1, "f32")
+    ws, sv = lina.lina_moe_workspace_size(comm, good)
+    small = torch.empty(8, dtype=torch.uint8, device="cuda")
+    x = torch.zeros(64, 64, device="cuda")
+    with pytest.raises(lina.LinaError) as ei:
+        lina.lina_moe_forward(comm, good, x, torch.zeros(64, 4, device="cuda"), torch.zeros(4, 256, 64, device="cuda"),
+                              torch.zeros(4, 64, 256, device="cuda"), torch.empty_like(x),
+                              torch.empty(sv, dtype=torch.uint8, device="cuda"), small)
+    assert ei.value.status == 6
+    comm.close()
