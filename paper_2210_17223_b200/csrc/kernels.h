@@ -15,6 +15,7 @@ struct RowGemm {
   void* D;             // [nseg_total][Cm][N]
   const void* aux;     // [nseg_total][Cm][N] (kEpiMask: keep where aux > 0)
   const int* vcount;   // [nseg_total] valid rows per segment
+  const int* mtp;      // [nseg+1] prefix of valid 128-row blocks over this launch's segments
   int seg0, nseg, El, Cm, N, K;
 };
 
@@ -51,6 +52,13 @@ void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, cons
 size_t dwg_scratch_floats(int T, int d, int E);
 void launch_dwg(int dtype, const void* X, const float* dL, int T, int d, int E, float* scratch,
                 float* dWg, cudaStream_t s);
+
+// mtp[c][i] = Σ_{i' < i} ceil(vcount[c*nseg + i'] / 128), i in [0, nseg]  (tcgen05 tile lists)
+void launch_mtile_prefix(const int* vcount, int n, int nseg, int* mtp, cudaStream_t s);
+bool tc_row_supported(const RowGemm& g);
+bool tc_wgrad_supported(const WGrad& g);
+void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s);
+void launch_wgrad_tc(const WGrad& g, cudaStream_t s);
 
 void launch_row_gemm_simt(int dtype, const RowGemm& p, bool b_kmajor, int epi, cudaStream_t s);
 void launch_wgrad_simt(int dtype, const WGrad& p, cudaStream_t s);

@@ -1,0 +1,536 @@
+// S5 / S8c expert FFN GEMMs on the 5th-generation tensor cores (bf16 in, fp32 accumulate).
+//
+// "Every expert is a fully-connected two-layer network using ReLU"; the
+// expert GEMMs are the only dense contraction on the path.
+//
+// One persistent, warp-specialised kernel per (A-major, B-major, epilogue):
+//   warp 0      : TMA producer (one elected lane) — A and B tiles into a 4-stage
+//                 128B-swizzled shared-memory ring, completion on mbarriers;
+//   warp 1      : TMEM allocator + MMA issuer (one elected lane) —
+//                 tcgen05.mma.cta_group::1.kind::f16, M=128 N=256 K=16, fp32
+//                 accumulators in TMEM, double-buffered (2 x 256 columns) so the
+//                 epilogue of tile i overlaps the MMAs of tile i+1;
+//   warps 2..5  : epilogue — tcgen05.ld 32x32b (one TMEM lane = one row per
+//                 thread), ReLU / ReLU'-mask, bf16 rounding, 16-byte stores.
+// Two problem shapes share the kernel:
+//   ROW   (forward GEMM1/GEMM2, backward dgrad): D[seg rows] = epi(A[seg rows] · B_eᵀ)
+//         over the (segment, 128-row block) tiles that hold valid rows, A viewed
+//         by a 3-D tensor map [segments][Cm rows][K] so a tile never reads past its
+//         segment (TMA zero-fills); B_e K-major (W as stored) or MN-major (the
+//         transposed use of the other weight in dgrad).
+//   WGRAD (backward weight gradients): D_e[M][N] = Σ_segments Σ_rows A_rᵀ B_r with
+//         both operands MN-major views of row buffers; the K loop walks the valid
+//         rows of every (chunk, source) segment of expert e in 64-row blocks.
+// Tiles are handed out statically (tile = blockIdx.x + i*gridDim.x) over a grid of
+// #SMs CTAs; ROW tiles are enumerated from a per-chunk prefix of valid m-blocks
+// (launch_mtile_prefix) so no CTA spins on empty tiles.
+#include <cuda.h>
+
+#include "../common.h"
+#include "../kernels.h"
+
+namespace lina {
+namespace tc {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;                 // 16 KB
+constexpr int B_BYTES = BN * BK * 2;                 // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int NUM_THREADS = 192;
+constexpr int TMEM_COLS = 512;                       // 2 accumulators x BN
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tm) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tm) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, 128B swizzle, sm_100 version bits.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: D fp32, A/B bf16, majors, N>>3 at [17,23), M>>4 at [24,29).
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+struct TcParams {
+  // ROW mode
+  const int* vcount;   // valid rows per segment (global segment index)
+  const int* mtp;      // [nseg+1] prefix of valid 128-row blocks of this launch's segments
+  int seg0, nseg, El, Cm;
+  // both
+  int M, N, K;         // WGRAD: M x N output per expert, K unused; ROW: N, K used
+  int epi;
+  __nv_bfloat16* D;
+  const __nv_bfloat16* aux;
+  // WGRAD mode
+  int nchunks, P;
+};
+
+template <bool WGRAD, bool B_MN, int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_base_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr bool A_MN = WGRAD;  // wgrad: A = (dO or dH) rows viewed MN-major
+
+  // ---- tile space
+  int total_tiles, n_nblk;
+  if (WGRAD) {
+    n_nblk = p.N / BN;
+    total_tiles = p.El * (p.M / BM) * n_nblk;
+  } else {
+    n_nblk = p.N / BN;
+    total_tiles = p.mtp[p.nseg] * n_nblk;
+  }
+  if ((int)blockIdx.x >= total_tiles) return;  // uniform for the whole CTA
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_base_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  // decode a tile into (expert/segment info, m0, n0)
+  auto decode = [&](int t, int& seg_or_el, int& m0, int& n0) {
+    const int nb = t % n_nblk;
+    const int ml = t / n_nblk;
+    n0 = nb * BN;
+    if (WGRAD) {
+      const int mblks = p.M / BM;
+      seg_or_el = ml / mblks;
+      m0 = (ml % mblks) * BM;
+    } else {
+      int i = 0;
+      while (i + 1 < p.nseg && p.mtp[i + 1] <= ml) ++i;
+      seg_or_el = i;  // local segment index within this launch
+      m0 = (ml - p.mtp[i]) * BM;
+    }
+  };
+  auto kblocks_of = [&](int seg_or_el) {
+    if (!WGRAD) return p.K / BK;
+    int kb = 0;
+    for (int c = 0; c < p.nchunks; ++c)
+      for (int s = 0; s < p.P; ++s) kb += (p.vcount[(c * p.P + s) * p.El + seg_or_el] + BK - 1) / BK;
+    return kb;
+  };
+
+  if (warp == 0) {
+    // ================= TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        int se, m0, n0;
+        decode(t, se, m0, n0);
+        auto issue = [&](int a0, int a1, int a2, int b0, int b1, int b2) {
+          mbar_wait(&empty[stage], ph ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          if (!A_MN) {
+            tma_load_3d(sa, &tmA, &full[stage], a0, a1, a2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_3d(sa + j * 8192, &tmA, &full[stage], a0 + j * 64, a1, a2);
+          }
+          if (!B_MN) {
+            tma_load_2d(sb, &tmB, &full[stage], b0, b1);
+          } else if (!WGRAD) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, &full[stage], b0 + j * 64, b1);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_3d(sb + j * 8192, &tmB, &full[stage], b0 + j * 64, b1, b2);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            ph ^= 1;
+          }
+        };
+        if (!WGRAD) {
+          const int seg = p.seg0 + se;
+          const int el = se % p.El;
+          for (int kb = 0; kb < p.K / BK; ++kb) {
+            const int k0 = kb * BK;
+            if (!B_MN) issue(k0, m0, seg, k0, el * p.N + n0, 0);
+            else issue(k0, m0, seg, n0, el * p.K + k0, 0);
+          }
+        } else {
+          const int el = se;
+          for (int c = 0; c < p.nchunks; ++c)
+            for (int s = 0; s < p.P; ++s) {
+              const int seg = (c * p.P + s) * p.El + el;
+              const int v = p.vcount[seg];
+              for (int r0 = 0; r0 < v; r0 += BK) issue(m0, r0, seg, n0, r0, seg);
+            }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        int se, m0, n0;
+        decode(t, se, m0, n0);
+        const int nkb = kblocks_of(se);
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            // K-major SW128: +32 B per K=16 step inside the 128 B atom; SBO = 8 rows * 128 B.
+            // MN-major SW128: +2 x (8 K-rows * 128 B) per K=16 step; LBO = 64-element MN block.
+            const uint64_t ad = A_MN ? sdesc(sa + kk * 2048, 8192, 1024) : sdesc(sa + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc(sb + kk * 2048, 8192, 1024) : sdesc(sb + kk * 32, 16, 1024);
+            mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);  // frees the smem slot once these MMAs have read it
+          if (++stage == STAGES) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);  // accumulator ready (arrives at once if nkb == 0)
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ================= epilogue (warps 2..5): TMEM lane quarter = warp % 4
+    const int quarter = warp & 3;
+    const int row_in_tile = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int se, m0, n0;
+      decode(t, se, m0, n0);
+      const int nkb = kblocks_of(se);
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int r = m0 + row_in_tile;
+      __nv_bfloat16* drow;
+      const __nv_bfloat16* arow = nullptr;
+      bool valid;
+      if (WGRAD) {
+        valid = r < p.M;
+        drow = p.D + ((size_t)se * p.M + r) * p.N + n0;
+      } else {
+        const int seg = p.seg0 + se;
+        valid = r < p.Cm;
+        drow = p.D + ((size_t)seg * p.Cm + r) * p.N + n0;
+        if (EPI == kEpiMask) arow = p.aux + ((size_t)seg * p.Cm + r) * p.N + n0;
+      }
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        if (nkb > 0) {
+          tmem_ld32(tbase + c0, v);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0u;
+        }
+        if (valid) {
+          float x[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
+          if (EPI == kEpiRelu) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = fmaxf(x[i], 0.f);
+          }
+          if (EPI == kEpiMask) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float h[8];
+              load16(arow + c0 + q * 8, h, (const __nv_bfloat16*)nullptr);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) x[q * 8 + i] = h[i] > 0.f ? x[q * 8 + i] : 0.f;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) store16(drow + c0 + q * 8, x + q * 8, (__nv_bfloat16*)nullptr);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
+      }
+    }
+  }
+  __syncwarp();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, TMEM_COLS);
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    LINA_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess)
+      throw CudaError{"cuTensorMapEncodeTiled entry point not found"};
+    fn = (EncodeTiledFn)f;
+  }
+  return fn;
+}
+
+// bf16 tensor map with 128B swizzle; dims/box innermost first; strides in bytes (rank-1 entries).
+static CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                            const uint32_t* box) {
+  CUtensorMap m;
+  cuuint64_t d[3], s[2];
+  cuuint32_t b[3], e[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+  }
+  for (int i = 0; i < rank - 1; ++i) s[i] = strides[i];
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, b,
+                           e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError{"cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
+  return m;
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    LINA_CUDA_CHECK(cudaGetDevice(&dev));
+    LINA_CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return g_num_sms;
+}
+
+template <bool WGRAD, bool B_MN, int EPI>
+static void launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int grid,
+                   cudaStream_t s) {
+  auto kern = tc_gemm_kernel<WGRAD, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    LINA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr_set = true;
+  }
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(a, b, p);
+}
+
+}  // namespace tc
+
+bool tc_row_supported(const RowGemm& g) { return g.N % tc::BN == 0 && g.K % tc::BK == 0 && g.mtp; }
+bool tc_wgrad_supported(const WGrad& g) { return g.M % tc::BM == 0 && g.N % tc::BN == 0; }
+
+void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s) {
+  using namespace tc;
+  const int nseg_total = g.seg0 + g.nseg;  // the map spans every segment up to this launch's last
+  const uint64_t adims[3] = {(uint64_t)g.K, (uint64_t)g.Cm, (uint64_t)nseg_total};
+  const uint64_t astr[2] = {(uint64_t)g.K * 2, (uint64_t)g.Cm * g.K * 2};
+  const uint32_t abox[3] = {BK, BM, 1};
+  CUtensorMap ma = make_map(g.A, 3, adims, astr, abox);
+  CUtensorMap mb;
+  if (b_kmajor) {  // W [El][N][K]
+    const uint64_t bd[2] = {(uint64_t)g.K, (uint64_t)g.El * g.N};
+    const uint64_t bs[1] = {(uint64_t)g.K * 2};
+    const uint32_t bb[2] = {BK, BN};
+    mb = make_map(g.B, 2, bd, bs, bb);
+  } else {  // W [El][K][N]
+    const uint64_t bd[2] = {(uint64_t)g.N, (uint64_t)g.El * g.K};
+    const uint64_t bs[1] = {(uint64_t)g.N * 2};
+    const uint32_t bb[2] = {64, BK};
+    mb = make_map(g.B, 2, bd, bs, bb);
+  }
+  TcParams p{};
+  p.vcount = g.vcount;
+  p.mtp = g.mtp;
+  p.seg0 = g.seg0;
+  p.nseg = g.nseg;
+  p.El = g.El;
+  p.Cm = g.Cm;
+  p.N = g.N;
+  p.K = g.K;
+  p.epi = epi;
+  p.D = (__nv_bfloat16*)g.D;
+  p.aux = (const __nv_bfloat16*)g.aux;
+  const int grid = num_sms();
+  if (b_kmajor) {
+    if (epi == kEpiRelu) launch<false, false, kEpiRelu>(ma, mb, p, grid, s);
+    else if (epi == kEpiMask) launch<false, false, kEpiMask>(ma, mb, p, grid, s);
+    else launch<false, false, kEpiNone>(ma, mb, p, grid, s);
+  } else {
+    if (epi == kEpiRelu) launch<false, true, kEpiRelu>(ma, mb, p, grid, s);
+    else if (epi == kEpiMask) launch<false, true, kEpiMask>(ma, mb, p, grid, s);
+    else launch<false, true, kEpiNone>(ma, mb, p, grid, s);
+  }
+  LINA_LAUNCH_CHECK();
+}
+
+void launch_wgrad_tc(const WGrad& g, cudaStream_t s) {
+  using namespace tc;
+  const uint64_t nseg_total = (uint64_t)g.nchunks * g.P * g.El;
+  const uint64_t ad[3] = {(uint64_t)g.M, (uint64_t)g.Cm, nseg_total};
+  const uint64_t as[2] = {(uint64_t)g.M * 2, (uint64_t)g.Cm * g.M * 2};
+  const uint32_t ab[3] = {64, BK, 1};
+  CUtensorMap ma = make_map(g.A, 3, ad, as, ab);
+  const uint64_t bd[3] = {(uint64_t)g.N, (uint64_t)g.Cm, nseg_total};
+  const uint64_t bs[2] = {(uint64_t)g.N * 2, (uint64_t)g.Cm * g.N * 2};
+  const uint32_t bb[3] = {64, BK, 1};
+  CUtensorMap mb = make_map(g.B, 3, bd, bs, bb);
+  TcParams p{};
+  p.vcount = g.vcount;
+  p.El = g.El;
+  p.Cm = g.Cm;
+  p.M = g.M;
+  p.N = g.N;
+  p.nchunks = g.nchunks;
+  p.P = g.P;
+  p.D = (__nv_bfloat16*)g.D;
+  const int tiles = g.El * (g.M / BM) * (g.N / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  launch<true, true, kEpiNone>(ma, mb, p, grid, s);
+  LINA_LAUNCH_CHECK();
+}
+
+}  // namespace lina

@@ -58,6 +58,7 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
   p.s_tokof = take(4 * E * (size_t)p.C);
   p.s_recvkept = take(4 * (size_t)p.P * p.El);
   p.s_vcount = take(4 * (size_t)p.n * p.P * p.El);
+  p.s_mtp = take(4 * (size_t)p.n * (p.P * p.El + 1));
   p.s_R = take(recv_rows * p.d * p.dt);                       // routed tokens (X rows)
   p.s_H = take(recv_rows * (size_t)p.f * p.dt);               // relu(X W1ᵀ)
   p.s_C = take(send_rows * p.d * p.dt);                       // returned expert outputs
@@ -83,7 +84,7 @@ namespace {
 
 struct Ptrs {
   float* probs; int* idx; float* gate; int* slot; int* kept; int* tok_of; int* recv_kept;
-  int* vcount; char* R; char* H; char* Cb;
+  int* vcount; int* mtp; char* R; char* H; char* Cb;
   int* route; char* D; char* O; float* dg; float* dL; float* dwg; char* dS; char* dO; char* dH;
   char* dXe; char* dXs;
 };
@@ -101,6 +102,7 @@ Ptrs carve(const Plan& p, void* saved, void* ws) {
     q.tok_of = (int*)(sv + p.s_tokof);
     q.recv_kept = (int*)(sv + p.s_recvkept);
     q.vcount = (int*)(sv + p.s_vcount);
+    q.mtp = (int*)(sv + p.s_mtp);
     q.R = sv + p.s_R;
     q.H = sv + p.s_H;
     q.Cb = sv + p.s_C;
@@ -139,8 +141,10 @@ void a2a_recv_to_send(const Plan& p, const char* recv, char* send, int w, int c,
 }
 
 void row_gemm(const Plan& p, const void* A, const void* B, void* D, const void* aux,
-              const int* vcount, int c, int N, int K, bool b_kmajor, int epi, cudaStream_t st) {
+              const int* vcount, const int* mtp, int c, int N, int K, bool b_kmajor, int epi,
+              cudaStream_t st) {
   RowGemm g{};
+  g.mtp = mtp + (size_t)c * (p.P * p.El + 1);
   g.A = A;
   g.B = B;
   g.D = D;
@@ -192,10 +196,11 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   if (p.P == 1) {
     // All experts local: the "all-to-all" is the identity and chunks only re-slice the GEMMs.
     launch_vcount(q.kept, 1, p.E, p.C, p.n, q.vcount, s);
+    launch_mtile_prefix(q.vcount, p.n, p.P * p.El, q.mtp, s);
     prof_begin(cm, s);
     for (int c = 0; c < p.n; ++c) {
-      row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, c, p.f, p.d, true, kEpiRelu, s);
-      row_gemm(p, q.H, w2, q.O, nullptr, q.vcount, c, p.d, p.f, true, kEpiNone, s);
+      row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s);
+      row_gemm(p, q.H, w2, q.O, nullptr, q.vcount, q.mtp, c, p.d, p.f, true, kEpiNone, s);
     }
     prof_end(cm, s, 2 * p.n);
     launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, p.n, p.Cm, out, s);
@@ -217,11 +222,12 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   }
   LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_cnt, 0));
   launch_vcount(q.recv_kept, p.P, p.El, p.C, n, q.vcount, s);
+  launch_mtile_prefix(q.vcount, n, p.P * p.El, q.mtp, s);
   for (int c = 0; c < n; ++c) {
     LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_disp[c], 0));
     prof_begin(cm, s);
-    row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, c, p.f, p.d, true, kEpiRelu, s);
-    row_gemm(p, q.H, w2, q.O, nullptr, q.vcount, c, p.d, p.f, true, kEpiNone, s);
+    row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s);
+    row_gemm(p, q.H, w2, q.O, nullptr, q.vcount, q.mtp, c, p.d, p.f, true, kEpiNone, s);
     prof_end(cm, s, 2);
     LINA_CUDA_CHECK(cudaEventRecord(e_gemm[c], s));
   }
@@ -250,8 +256,8 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
   if (p.P == 1) {
     prof_begin(cm, s);
     for (int c = 0; c < n; ++c) {
-      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, c, p.f, p.d, false, kEpiMask, s);
-      row_gemm(p, q.dH, w1, q.dXe, nullptr, q.vcount, c, p.d, p.f, false, kEpiNone, s);
+      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s);
+      row_gemm(p, q.dH, w1, q.dXe, nullptr, q.vcount, q.mtp, c, p.d, p.f, false, kEpiNone, s);
     }
     launch_expert_wgrad(dtype, wg2, s);
     launch_expert_wgrad(dtype, wg1, s);
@@ -271,8 +277,8 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
     for (int c = 0; c < n; ++c) {
       LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_disp[c], 0));
       prof_begin(cm, s);
-      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, c, p.f, p.d, false, kEpiMask, s);
-      row_gemm(p, q.dH, w1, q.dXe, nullptr, q.vcount, c, p.d, p.f, false, kEpiNone, s);
+      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s);
+      row_gemm(p, q.dH, w1, q.dXe, nullptr, q.vcount, q.mtp, c, p.d, p.f, false, kEpiNone, s);
       prof_end(cm, s, 2);
       LINA_CUDA_CHECK(cudaEventRecord(e_gemm[c], s));
     }

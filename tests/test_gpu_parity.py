@@ -148,7 +148,7 @@ def test_c2_full_size_sampled():
 def test_comm_and_errors():
     import paper_2210_17223_b200 as lina
     comm = lina.Comm(1, 0, 0)
-    bad = lina.make_desc(10, 30, 64, 5, 9, 0, 4, "bf16")
+    bad = lina.make_desc(10, 30, 64, 5, 9, 0, 40, "bf16")
     with pytest.raises(lina.LinaError) as ei:
         lina.lina_moe_workspace_size(comm, bad)
     msg = str(ei.value)
