@@ -81,5 +81,10 @@ __host__ __device__ __forceinline__ int chunk_of(int s, int C, int n) {
   return (int)((((long long)s + 1) * n + C - 1) / C) - 1;
 }
 __host__ __device__ __forceinline__ int chunk_rows_max(int C, int n) { return (C + n - 1) / n; }
+// Row of (expert e, capacity slot s) in the chunk-major send layout [n][E][Cm][w].
+__host__ __device__ __forceinline__ size_t send_row(int e, int s, int E, int C, int n, int Cm) {
+  const int c = chunk_of(s, C, n);
+  return ((size_t)c * E + e) * Cm + (s - chunk_begin(c, C, n));
+}
 
 }  // namespace lina

@@ -8,9 +8,9 @@
 // the raw probability, k>=2 renormalised over the k selected (R4).
 //
 // Layout: X [T,d] (bf16|fp32) row-major, Wg [d,E] fp32 row-major.  One CTA of 256
-// threads owns BT=64 tokens x all E experts; the d reduction runs in DK=32 slabs
-// staged in shared memory (X transposed to fp32, Wg slab), each thread keeping a
-// TM x TE register micro-tile.  Each logit is one fp32 FMA chain in ascending d
+// threads owns BT=32 tokens x all E experts; the d reduction runs in 64/128-column
+// slabs staged in shared memory (X transposed to fp32, Wg slab), each thread
+// keeping one token x E/8 experts in registers.  Each logit is one fp32 FMA chain in ascending d
 // order: deterministic, and exact for the grid inputs of DESIGN.md §4.  The
 // epilogue keeps logits in shared memory and gives one warp per token for the
 // softmax (warp-shuffle max/sum) and k rounds of warp arg-max.
@@ -22,13 +22,16 @@
 namespace lina {
 namespace {
 
-constexpr int kGateBT = 64;
-constexpr int kGateDK = 32;
+constexpr int kGateBT = 32;
 
 __device__ __forceinline__ bool key_better(float la, int ia, float lb, int ib) {
   return la > lb || (la == lb && ia < ib);
 }
 
+// EP = padded expert count (8/16/32/64).  Threads: 8 along experts (TE = EP/8 each) x
+// 32 along tokens (one token each).  DK-column slabs of X (transposed to fp32) and Wg
+// are double-buffered through registers: the global loads of slab i+1 are issued
+// before the FMAs of slab i, so each CTA keeps its next 4 KB-8 KB in flight.
 template <typename TIn, int EP>
 __global__ void __launch_bounds__(256) gate_topk_kernel(const TIn* __restrict__ X,
                                                         const float* __restrict__ Wg, int T, int d,
@@ -36,73 +39,79 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const TIn* __restrict__ 
                                                         float* __restrict__ probs,
                                                         int* __restrict__ idx,
                                                         float* __restrict__ gate) {
-  constexpr int BT = kGateBT, DK = kGateDK;
-  constexpr int TE = (EP >= 16) ? 4 : 2;
-  constexpr int TX = EP / TE;
-  constexpr int TY = 256 / TX;
-  constexpr int TM = BT / TY;
-  static_assert(TM >= 1 && TM * TY == BT, "tile");
-  __shared__ float xs[DK][BT + 4];
+  constexpr int BT = kGateBT;
+  constexpr int DK = (EP <= 16) ? 128 : 64;
+  constexpr int TE = EP / 8;
+  constexpr int XV = BT * DK / 256;        // X elements per thread per slab (16 or 8)
+  constexpr int WV = DK * EP / 256;        // Wg floats per thread per slab
+  __shared__ float xs[DK][BT + 1];
   __shared__ float ws[DK][EP];
   __shared__ float lt[BT][EP + 1];
 
   const int tid = threadIdx.x;
-  const int tx = tid % TX, ty = tid / TX;
+  const int tx = tid & 7, ty = tid >> 3;   // expert group, token
   const int t0 = blockIdx.x * BT;
-  float acc[TM][TE];
+  // slab loaders: X row r = tid / (DK/XV), columns cs..cs+XV; Wg flat index tid*WV..
+  constexpr int XT = DK / XV;              // threads per X row
+  const int xr = tid / XT, xc = (tid % XT) * XV;
+  float xreg[XV], wreg[WV];
+  auto load_slab = [&](int k0) {
+    const int t = t0 + xr;
 #pragma unroll
-  for (int m = 0; m < TM; ++m)
-#pragma unroll
-    for (int e = 0; e < TE; ++e) acc[m][e] = 0.f;
-
-  for (int k0 = 0; k0 < d; k0 += DK) {
-    {  // X slab: 64 rows x 32 cols, 8 consecutive elements per thread
-      const int r = tid >> 2, cs = (tid & 3) * 8;
-      const int t = t0 + r;
-      float v[8];
-      if (t < T && k0 + cs + 8 <= d && ((d * sizeof(TIn)) % 16 == 0)) {
-        const TIn* src = X + (size_t)t * d + k0 + cs;
+    for (int i = 0; i < XV; i += 8) {
+      const int c = k0 + xc + i;
+      if (t < T && c + 8 <= d && ((d * (int)sizeof(TIn)) % 16 == 0)) {
+        const TIn* src = X + (size_t)t * d + c;
         if constexpr (sizeof(TIn) == 2) {
-          load16(src, v, (const __nv_bfloat16*)nullptr);
+          load16(src, xreg + i, (const __nv_bfloat16*)nullptr);
         } else {
-          load16(src, v, (const float*)nullptr);
-          load16(src + 4, v + 4, (const float*)nullptr);
+          load16(src, xreg + i, (const float*)nullptr);
+          load16(src + 4, xreg + i + 4, (const float*)nullptr);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          v[i] = (t < T && k0 + cs + i < d) ? Elt<TIn>::to_f(X[(size_t)t * d + k0 + cs + i]) : 0.f;
+        for (int q = 0; q < 8; ++q)
+          xreg[i + q] = (t < T && c + q < d) ? Elt<TIn>::to_f(X[(size_t)t * d + c + q]) : 0.f;
       }
+    }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) xs[cs + i][r] = v[i];
+    for (int i = 0; i < WV; ++i) {
+      const int f = tid * WV + i;
+      const int kk = f / EP, e = f % EP;
+      wreg[i] = (e < E && k0 + kk < d) ? __ldg(Wg + (size_t)(k0 + kk) * E + e) : 0.f;
     }
-    for (int i = tid; i < DK * EP; i += 256) {
-      const int kk = i / EP, e = i % EP;
-      ws[kk][e] = (e < E && k0 + kk < d) ? Wg[(size_t)(k0 + kk) * E + e] : 0.f;
+  };
+  auto store_slab = [&]() {
+#pragma unroll
+    for (int i = 0; i < XV; ++i) xs[xc + i][xr] = xreg[i];
+#pragma unroll
+    for (int i = 0; i < WV; ++i) {
+      const int f = tid * WV + i;
+      ws[f / EP][f % EP] = wreg[i];
     }
+  };
+  float acc[TE];
+#pragma unroll
+  for (int e = 0; e < TE; ++e) acc[e] = 0.f;
+  load_slab(0);
+  for (int k0 = 0; k0 < d; k0 += DK) {
+    store_slab();
     __syncthreads();
+    if (k0 + DK < d) load_slab(k0 + DK);   // in flight during the FMAs below
 #pragma unroll 8
     for (int kk = 0; kk < DK; ++kk) {
-      float a[TM], b[TE];
+      const float a = xs[kk][ty];
 #pragma unroll
-      for (int m = 0; m < TM; ++m) a[m] = xs[kk][ty * TM + m];
-#pragma unroll
-      for (int e = 0; e < TE; ++e) b[e] = ws[kk][tx * TE + e];
-#pragma unroll
-      for (int m = 0; m < TM; ++m)
-#pragma unroll
-        for (int e = 0; e < TE; ++e) acc[m][e] = fmaf(a[m], b[e], acc[m][e]);
+      for (int e = 0; e < TE; ++e) acc[e] = fmaf(a, ws[kk][tx * TE + e], acc[e]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int m = 0; m < TM; ++m)
-#pragma unroll
-    for (int e = 0; e < TE; ++e) lt[ty * TM + m][tx * TE + e] = acc[m][e];
+  for (int e = 0; e < TE; ++e) lt[ty][tx * TE + e] = acc[e];
   __syncthreads();
 
   const int warp = tid >> 5, lane = tid & 31;
-  for (int r = warp; r < BT; r += 8) {
+  for (int r = warp; r < kGateBT; r += 8) {
     const int t = t0 + r;
     if (t >= T) break;
     const bool v0 = lane < E, v1 = lane + 32 < E;
