@@ -53,8 +53,11 @@ size_t dwg_scratch_floats(int T, int d, int E);
 void launch_dwg(int dtype, const void* X, const float* dL, int T, int d, int E, float* scratch,
                 float* dWg, cudaStream_t s);
 
-// mtp[c][i] = Σ_{i' < i} ceil(vcount[c*nseg + i'] / 128), i in [0, nseg]  (tcgen05 tile lists)
-void launch_mtile_prefix(const int* vcount, int n, int nseg, int* mtp, cudaStream_t s);
+// CTAs per tensor-core tile (cta_group::2 pairs -> 256-row tiles).
+constexpr int kTcCtaGroup = 2;
+int tc_tile_rows();
+// mtp[c][i] = Σ_{i' < i} ceil(vcount[c*nseg + i'] / rows), i in [0, nseg]  (tcgen05 tile lists)
+void launch_mtile_prefix(const int* vcount, int n, int nseg, int rows, int* mtp, cudaStream_t s);
 bool tc_row_supported(const RowGemm& g);
 bool tc_wgrad_supported(const WGrad& g);
 void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s);

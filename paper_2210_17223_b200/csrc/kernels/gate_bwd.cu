@@ -13,9 +13,9 @@
 //       FMAs for 6 shared loads.  The expert-gradient rows are gathered with one
 //       16-byte load per (token, kept j).
 // dwg : CTA = 256 columns x 8 experts over a token range, thread = 8 columns x 8
-//       experts, 8 token lanes (one per warp) each walking every 8th token; each
-//       (split, lane) writes its own partial, reduced afterwards in a fixed order
-//       (deterministic, no float atomics).
+//       experts, 8 token lanes (one per warp) each walking every 8th token, folded
+//       in shared memory in a fixed tree order; each split writes one partial,
+//       reduced afterwards in a fixed order (deterministic, no float atomics).
 #include "../common.h"
 #include "../kernels.h"
 
@@ -36,18 +36,9 @@ __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * kDxCols;
   const int t0 = blockIdx.y * kDxTok;
-  for (int i = tid; i < E * kDxCols; i += 256) {
-    const int col = i / E, e = i % E;  // coalesced read of Wg rows
-    sW[e * kDxCols + col] = (c0 + col < d) ? Wg[(size_t)(c0 + col) * E + e] : 0.f;
-  }
-  for (int i = tid; i < kDxTok * E; i += 256) {
-    const int r = i / E, e = i % E;
-    sL[i] = (t0 + r < Tn) ? dL[(size_t)(t0 + r) * E + e] : 0.f;
-  }
-  __syncthreads();
+  // the gathers do not depend on shared memory: issue them before staging
   const int cg = tid & 31, tg = tid >> 5;  // 32 column groups x 8 token groups
   const int col = c0 + cg * 8;
-  if (col >= d) return;
   float acc[4][8];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -57,7 +48,7 @@ __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int t = t0 + tg * 4 + i;
-    if (t >= Tn) continue;
+    if (t >= Tn || col >= d) continue;
     for (int j = 0; j < k; ++j) {
       const int s = slot[(size_t)t * k + j];
       if (s < 0) continue;
@@ -73,6 +64,16 @@ __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe
       for (int c = 0; c < 8; ++c) acc[i][c] += x[c];
     }
   }
+  for (int i = tid; i < E * kDxCols; i += 256) {
+    const int col = i / E, e = i % E;  // coalesced read of Wg rows
+    sW[e * kDxCols + col] = (c0 + col < d) ? Wg[(size_t)(c0 + col) * E + e] : 0.f;
+  }
+  for (int i = tid; i < kDxTok * E; i += 256) {
+    const int r = i / E, e = i % E;
+    sL[i] = (t0 + r < Tn) ? dL[(size_t)(t0 + r) * E + e] : 0.f;
+  }
+  __syncthreads();
+  if (col >= d) return;
   // + dL · Wgᵀ
   for (int e = 0; e < E; ++e) {
     const float4 w0 = *reinterpret_cast<const float4*>(sW + e * kDxCols + cg * 8);
@@ -99,11 +100,13 @@ __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe
   }
 }
 
-// part[(split*8 + lane)][col][e] over tokens t = split*tps + lane + 8*i.
+// part[split][col][e] over tokens t = split*tps + lane + 8*i (8 token lanes = 8 warps,
+// combined in shared memory in a fixed order).
 template <typename T>
 __global__ void __launch_bounds__(256) dwg_tiled_kernel(const T* __restrict__ X, const float* __restrict__ dL,
                                                         int Tn, int d, int E, int tps,
                                                         float* __restrict__ part) {
+  __shared__ float red[4][256 * 8];
   const int tid = threadIdx.x;
   const int cg = tid & 31, lane_t = tid >> 5;
   const int col = blockIdx.x * 256 + cg * 8;
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(256) dwg_tiled_kernel(const T* __restrict__ X,
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[c][q] = 0.f;
   if (col < d) {
-#pragma unroll 2
+#pragma unroll 4
     for (int t = ta + lane_t; t < tb; t += 8) {
       float x[8];
       const T* src = X + (size_t)t * d + col;
@@ -136,7 +139,26 @@ __global__ void __launch_bounds__(256) dwg_tiled_kernel(const T* __restrict__ X,
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[c][q] = fmaf(x[c], l[q], acc[c][q]);
     }
-    float* dst = part + ((size_t)(split * 8 + lane_t) * d + col) * E + e0;
+  }
+  // fixed-order tree over the 8 token lanes: (0+4,1+5,2+6,3+7), (0+2,1+3), (0+1)
+  for (int half = 4; half >= 1; half >>= 1) {
+    if (lane_t >= half && lane_t < 2 * half) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) red[lane_t - half][(c * 8 + q) * 32 + cg] = acc[c][q];
+    }
+    __syncthreads();
+    if (lane_t < half) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[c][q] += red[lane_t][(c * 8 + q) * 32 + cg];
+    }
+    __syncthreads();
+  }
+  if (lane_t == 0 && col < d) {
+    float* dst = part + ((size_t)split * d + col) * E + e0;
 #pragma unroll
     for (int c = 0; c < 8; ++c)
 #pragma unroll
@@ -150,14 +172,22 @@ __global__ void dwg_reduce_kernel(const float* __restrict__ part, int nparts, in
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= dE) return;
   float s = 0.f;
-  for (int q = 0; q < nparts; ++q) s += part[(size_t)q * dE + i];
+  int q = 0;
+  for (; q + 8 <= nparts; q += 8) {  // 8 independent loads in flight, summed in order
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(part + (size_t)(q + u) * dE + i);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; q < nparts; ++q) s += part[(size_t)q * dE + i];
   dWg[i] = s;
 }
 
 int dwg_splits(int T, int d, int E) {
   const int dblk = (d + 255) / 256, eblk = (E + 7) / 8;
-  int want = (600 + dblk * eblk - 1) / (dblk * eblk);  // ~4 waves of CTAs
-  const int maxs = (T + 255) / 256;                     // >= 32 tokens per token lane
+  int want = (1200 + dblk * eblk - 1) / (dblk * eblk);  // ~8 waves of CTAs
+  const int maxs = (T + 127) / 128;                      // >= 16 tokens per token lane
   if (want > maxs) want = maxs;
   return want < 1 ? 1 : want;
 }
@@ -165,7 +195,7 @@ int dwg_splits(int T, int d, int E) {
 }  // namespace
 
 size_t dwg_scratch_floats(int T, int d, int E) {
-  return (size_t)dwg_splits(T, d, E) * 8 * d * E;
+  return (size_t)dwg_splits(T, d, E) * d * E;
 }
 
 void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* dL,
@@ -213,7 +243,7 @@ void launch_dwg(int dtype, const void* X, const float* dL, int T, int d, int E, 
                                                          scratch);
   LINA_LAUNCH_CHECK();
   const int dE = d * E;
-  dwg_reduce_kernel<<<(dE + 255) / 256, 256, 0, s>>>(scratch, nsplit * 8, dE, dWg);
+  dwg_reduce_kernel<<<(dE + 255) / 256, 256, 0, s>>>(scratch, nsplit, dE, dWg);
   LINA_LAUNCH_CHECK();
 }
 

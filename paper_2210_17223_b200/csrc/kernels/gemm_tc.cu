@@ -3,27 +3,33 @@
 // "Every expert is a fully-connected two-layer network using ReLU"; the
 // expert GEMMs are the only dense contraction on the path.
 //
-// One persistent, warp-specialised kernel per (A-major, B-major, epilogue):
-//   warp 0      : TMA producer (one elected lane) — A and B tiles into a 4-stage
+// One persistent, warp-specialised kernel per (CTA-group, problem, B-major, epilogue):
+//   warp 0      : TMA producer (one elected lane) — A and B tiles into a
 //                 128B-swizzled shared-memory ring, completion on mbarriers;
-//   warp 1      : TMEM allocator + MMA issuer (one elected lane) —
-//                 tcgen05.mma.cta_group::1.kind::f16, M=128 N=256 K=16, fp32
-//                 accumulators in TMEM, double-buffered (2 x 256 columns) so the
-//                 epilogue of tile i overlaps the MMAs of tile i+1;
+//   warp 1      : TMEM allocator + MMA issuer (one elected lane of the leader CTA) —
+//                 tcgen05.mma.kind::f16, K=16 per instruction, fp32 accumulators
+//                 in TMEM, double-buffered (2 x 256 columns) so the epilogue of
+//                 tile i overlaps the MMAs of tile i+1;
 //   warps 2..5  : epilogue — tcgen05.ld 32x32b (one TMEM lane = one row per
 //                 thread), ReLU / ReLU'-mask, bf16 rounding, 16-byte stores.
+// CG = 2 (default): a CTA pair (cluster 2x1) computes a 256 x 256 tile with
+//   tcgen05.mma.cta_group::2 (UMMA M=256): each CTA stages its 128 rows of A and
+//   its half (128 columns) of B, so every SM streams 32 KB per 64-deep K block
+//   instead of 48 KB — the L2->SM feed, not the tensor pipe, bounded the 1-CTA
+//   version at ~66% tensor activity (profiles/r01_*).  TMA completions of both CTAs
+//   land on the leader's mbarrier; MMA completion is multicast to both CTAs.
+// CG = 1: single-CTA M=128 N=256 (kept for shapes whose row count is small).
 // Two problem shapes share the kernel:
 //   ROW   (forward GEMM1/GEMM2, backward dgrad): D[seg rows] = epi(A[seg rows] · B_eᵀ)
-//         over the (segment, 128-row block) tiles that hold valid rows, A viewed
-//         by a 3-D tensor map [segments][Cm rows][K] so a tile never reads past its
+//         over the (segment, row-block) tiles that hold valid rows, A viewed by a
+//         3-D tensor map [segments][Cm rows][K] so a tile never reads past its
 //         segment (TMA zero-fills); B_e K-major (W as stored) or MN-major (the
 //         transposed use of the other weight in dgrad).
 //   WGRAD (backward weight gradients): D_e[M][N] = Σ_segments Σ_rows A_rᵀ B_r with
 //         both operands MN-major views of row buffers; the K loop walks the valid
 //         rows of every (chunk, source) segment of expert e in 64-row blocks.
-// Tiles are handed out statically (tile = blockIdx.x + i*gridDim.x) over a grid of
-// #SMs CTAs; ROW tiles are enumerated from a per-chunk prefix of valid m-blocks
-// (launch_mtile_prefix) so no CTA spins on empty tiles.
+// Tiles are handed out statically per cluster over a grid of #SMs CTAs; ROW tiles
+// are enumerated from a per-chunk prefix of valid row blocks (launch_mtile_prefix).
 #include <cuda.h>
 
 #include "../common.h"
@@ -32,17 +38,32 @@
 namespace lina {
 namespace tc {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;                 // 16 KB
-constexpr int B_BYTES = BN * BK * 2;                 // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int BN = 256, BK = 64;
 constexpr int NUM_THREADS = 192;
-constexpr int TMEM_COLS = 512;                       // 2 accumulators x BN
+constexpr int TMEM_COLS = 512;  // 2 accumulators x BN
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the pair leader
+
+template <int CG> struct Geo {
+  static constexpr int ROWS = 128 * CG;                  // tile rows per cluster
+  static constexpr int A_BYTES = 128 * BK * 2;           // 16 KB per CTA
+  static constexpr int B_ROWS = BN / CG;                 // B rows (N) staged per CTA
+  static constexpr int B_BYTES = B_ROWS * BK * 2;        // 32 KB (CG=1) / 16 KB (CG=2)
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+};
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -52,8 +73,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+// Arrive on the barrier at the same offset in CTA `rank` of the cluster.
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -66,21 +95,39 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+template <int CG>
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0,
                                             int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+        "[%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
+        : "memory");
+  }
 }
+template <int CG>
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0,
                                             int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+        "[%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tm) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tm) : "memory");
@@ -91,32 +138,60 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
+template <int CG>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
-               "r"(ncols)
-               : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  if constexpr (CG == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  } else {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
 }
+template <int CG>
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
-               : "memory");
+  if constexpr (CG == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+  else
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
+template <int CG>
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
 }
+// Signal `bar` once every previously issued MMA of this thread has completed
+// (in both CTAs of the pair for CG = 2).
+template <int CG>
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+  } else {
+    const uint16_t mask = 0x3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+        "%1;" ::"r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -151,26 +226,24 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
 }
 
 struct TcParams {
-  // ROW mode
   const int* vcount;   // valid rows per segment (global segment index)
-  const int* mtp;      // [nseg+1] prefix of valid 128-row blocks of this launch's segments
+  const int* mtp;      // ROW: [nseg+1] prefix of valid row blocks of this launch's segments
   int seg0, nseg, El, Cm;
-  // both
-  int M, N, K;         // WGRAD: M x N output per expert, K unused; ROW: N, K used
-  int epi;
+  int M, N, K;         // WGRAD: M x N output per expert; ROW: N, K
   __nv_bfloat16* D;
   const __nv_bfloat16* aux;
-  // WGRAD mode
-  int nchunks, P;
+  int nchunks, P;      // WGRAD
 };
 
-template <bool WGRAD, bool B_MN, int EPI>
+template <int CG, bool WGRAD, bool B_MN, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    TcParams p) {
+  using G = Geo<CG>;
+  constexpr int STAGES = G::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = (uint64_t*)(smem + STAGES * G::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -178,17 +251,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr bool A_MN = WGRAD;  // wgrad: A = (dO or dH) rows viewed MN-major
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / CG, num_clusters = gridDim.x / CG;
 
-  // ---- tile space
-  int total_tiles, n_nblk;
-  if (WGRAD) {
-    n_nblk = p.N / BN;
-    total_tiles = p.El * (p.M / BM) * n_nblk;
-  } else {
-    n_nblk = p.N / BN;
-    total_tiles = p.mtp[p.nseg] * n_nblk;
-  }
-  if ((int)blockIdx.x >= total_tiles) return;  // uniform for the whole CTA
+  // ---- tile space (per cluster)
+  const int n_nblk = p.N / BN;
+  const int total_tiles = WGRAD ? p.El * (p.M / G::ROWS) * n_nblk : p.mtp[p.nseg] * n_nblk;
+  if (cluster_id >= total_tiles) return;  // uniform for the whole cluster
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -199,30 +269,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(tmem_base_slot, TMEM_COLS);
+  if (warp == 1) tmem_alloc<CG>(tmem_base_slot, TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
 
-  // decode a tile into (expert/segment info, m0, n0)
   auto decode = [&](int t, int& seg_or_el, int& m0, int& n0) {
     const int nb = t % n_nblk;
     const int ml = t / n_nblk;
     n0 = nb * BN;
     if (WGRAD) {
-      const int mblks = p.M / BM;
+      const int mblks = p.M / G::ROWS;
       seg_or_el = ml / mblks;
-      m0 = (ml % mblks) * BM;
+      m0 = (ml % mblks) * G::ROWS;
     } else {
       int i = 0;
       while (i + 1 < p.nseg && p.mtp[i + 1] <= ml) ++i;
       seg_or_el = i;  // local segment index within this launch
-      m0 = (ml - p.mtp[i]) * BM;
+      m0 = (ml - p.mtp[i]) * G::ROWS;
     }
   };
   auto kblocks_of = [&](int seg_or_el) {
@@ -234,34 +304,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   };
 
   if (warp == 0) {
-    // ================= TMA producer
+    // ================= TMA producer (both CTAs load their own halves)
     if (lane == 0) {
       int stage = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const int arow = 128 * rank;          // this CTA's rows within the tile
+      const int brow = G::B_ROWS * rank;    // this CTA's B (N) rows within the tile
+      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         int se, m0, n0;
         decode(t, se, m0, n0);
         auto issue = [&](int a0, int a1, int a2, int b0, int b1, int b2) {
           mbar_wait(&empty[stage], ph ^ 1);
-          uint8_t* sa = smem + stage * STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          uint8_t* sa = smem + stage * G::STAGE_BYTES;
+          uint8_t* sb = sa + G::A_BYTES;
+          if (leader) mbar_expect_tx(&full[stage], CG * G::STAGE_BYTES);
           if (!A_MN) {
-            tma_load_3d(sa, &tmA, &full[stage], a0, a1, a2);
+            tma_load_3d<CG>(sa, &tmA, &full[stage], a0, a1, a2);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_3d(sa + j * 8192, &tmA, &full[stage], a0 + j * 64, a1, a2);
+            for (int j = 0; j < 2; ++j) tma_load_3d<CG>(sa + j * 8192, &tmA, &full[stage], a0 + j * 64, a1, a2);
           }
           if (!B_MN) {
-            tma_load_2d(sb, &tmB, &full[stage], b0, b1);
+            tma_load_2d<CG>(sb, &tmB, &full[stage], b0, b1);
           } else if (!WGRAD) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, &full[stage], b0 + j * 64, b1);
+            for (int j = 0; j < G::B_ROWS / 64; ++j)
+              tma_load_2d<CG>(sb + j * 8192, &tmB, &full[stage], b0 + j * 64, b1);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_3d(sb + j * 8192, &tmB, &full[stage], b0 + j * 64, b1, b2);
+            for (int j = 0; j < G::B_ROWS / 64; ++j)
+              tma_load_3d<CG>(sb + j * 8192, &tmB, &full[stage], b0 + j * 64, b1, b2);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -273,8 +345,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int el = se % p.El;
           for (int kb = 0; kb < p.K / BK; ++kb) {
             const int k0 = kb * BK;
-            if (!B_MN) issue(k0, m0, seg, k0, el * p.N + n0, 0);
-            else issue(k0, m0, seg, n0, el * p.K + k0, 0);
+            if (!B_MN) issue(k0, m0 + arow, seg, k0, el * p.N + n0 + brow, 0);
+            else issue(k0, m0 + arow, seg, n0 + brow, el * p.K + k0, 0);
           }
         } else {
           const int el = se;
@@ -282,20 +354,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int s = 0; s < p.P; ++s) {
               const int seg = (c * p.P + s) * p.El + el;
               const int v = p.vcount[seg];
-              for (int r0 = 0; r0 < v; r0 += BK) issue(m0, r0, seg, n0, r0, seg);
+              for (int r0 = 0; r0 < v; r0 += BK) issue(m0 + arow, r0, seg, n0 + brow, r0, seg);
             }
         }
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+    // ================= MMA issuer (leader CTA only)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(G::ROWS, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         int se, m0, n0;
         decode(t, se, m0, n0);
         const int nkb = kblocks_of(se);
@@ -305,23 +377,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], ph);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t sa = smem_u32(smem + stage * G::STAGE_BYTES);
+          const uint32_t sb = sa + G::A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             // K-major SW128: +32 B per K=16 step inside the 128 B atom; SBO = 8 rows * 128 B.
             // MN-major SW128: +2 x (8 K-rows * 128 B) per K=16 step; LBO = 64-element MN block.
             const uint64_t ad = A_MN ? sdesc(sa + kk * 2048, 8192, 1024) : sdesc(sa + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? sdesc(sb + kk * 2048, 8192, 1024) : sdesc(sb + kk * 32, 16, 1024);
-            mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+            mma_bf16<CG>(d_tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
           }
-          mma_commit(&empty[stage]);  // frees the smem slot once these MMAs have read it
+          mma_commit<CG>(&empty[stage]);  // frees the smem slot (in both CTAs) once read
           if (++stage == STAGES) {
             stage = 0;
             ph ^= 1;
           }
         }
-        mma_commit(&tfull[acc]);  // accumulator ready (arrives at once if nkb == 0)
+        mma_commit<CG>(&tfull[acc]);  // accumulator ready (arrives at once if nkb == 0)
         if (++acc == 2) {
           acc = 0;
           aph ^= 1;
@@ -331,10 +403,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {
     // ================= epilogue (warps 2..5): TMEM lane quarter = warp % 4
     const int quarter = warp & 3;
-    const int row_in_tile = quarter * 32 + lane;
+    const int row_in_tile = 128 * rank + quarter * 32 + lane;
     int acc = 0;
     uint32_t aph = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       int se, m0, n0;
       decode(t, se, m0, n0);
       const int nkb = kblocks_of(se);
@@ -357,6 +429,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t v[32];
+        float h[32];
+        if (EPI == kEpiMask && valid) {  // issue the aux loads before waiting on TMEM
+#pragma unroll
+          for (int q = 0; q < 4; ++q) load16(arow + c0 + q * 8, h + q * 8, (const __nv_bfloat16*)nullptr);
+        }
         if (nkb > 0) {
           tmem_ld32(tbase + c0, v);
           tmem_wait_ld();
@@ -374,12 +451,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if (EPI == kEpiMask) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float h[8];
-              load16(arow + c0 + q * 8, h, (const __nv_bfloat16*)nullptr);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) x[q * 8 + i] = h[i] > 0.f ? x[q * 8 + i] : 0.f;
-            }
+            for (int i = 0; i < 32; ++i) x[i] = h[i] > 0.f ? x[i] : 0.f;
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) store16(drow + c0 + q * 8, x + q * 8, (__nv_bfloat16*)nullptr);
@@ -387,7 +459,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(&tempty[acc], 0);
+        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
+      }
       if (++acc == 2) {
         acc = 0;
         aph ^= 1;
@@ -395,8 +470,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   __syncwarp();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem_base, TMEM_COLS);
+  tc_fence_before();
+  if (CG == 2) cluster_sync();
+  else __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<CG>(tmem_base, TMEM_COLS);
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -436,45 +516,76 @@ static CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, co
   return m;
 }
 
-static int g_num_sms = 0;
 static int num_sms() {
-  if (!g_num_sms) {
+  static int n = 0;
+  if (!n) {
     int dev = 0;
     LINA_CUDA_CHECK(cudaGetDevice(&dev));
-    LINA_CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    LINA_CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
   }
-  return g_num_sms;
+  return n;
 }
 
-template <bool WGRAD, bool B_MN, int EPI>
+template <int CG, bool WGRAD, bool B_MN, int EPI>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int grid,
                    cudaStream_t s) {
-  auto kern = tc_gemm_kernel<WGRAD, B_MN, EPI>;
+  auto kern = tc_gemm_kernel<CG, WGRAD, B_MN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
-    LINA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    LINA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Geo<CG>::SMEM_BYTES));
     attr_set = true;
   }
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(a, b, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = Geo<CG>::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LINA_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, b, p));
+}
+
+template <int CG>
+static void row_dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p, bool b_kmajor,
+                         int epi, int grid, cudaStream_t s) {
+  if (b_kmajor) {
+    if (epi == kEpiRelu) launch<CG, false, false, kEpiRelu>(ma, mb, p, grid, s);
+    else if (epi == kEpiMask) launch<CG, false, false, kEpiMask>(ma, mb, p, grid, s);
+    else launch<CG, false, false, kEpiNone>(ma, mb, p, grid, s);
+  } else {
+    if (epi == kEpiRelu) launch<CG, false, true, kEpiRelu>(ma, mb, p, grid, s);
+    else if (epi == kEpiMask) launch<CG, false, true, kEpiMask>(ma, mb, p, grid, s);
+    else launch<CG, false, true, kEpiNone>(ma, mb, p, grid, s);
+  }
 }
 
 }  // namespace tc
 
+// Rows per tensor-core tile (the m-block granularity launch_mtile_prefix must use).
+int tc_tile_rows() { return 128 * kTcCtaGroup; }
+
 bool tc_row_supported(const RowGemm& g) { return g.N % tc::BN == 0 && g.K % tc::BK == 0 && g.mtp; }
-bool tc_wgrad_supported(const WGrad& g) { return g.M % tc::BM == 0 && g.N % tc::BN == 0; }
+bool tc_wgrad_supported(const WGrad& g) { return g.M % tc_tile_rows() == 0 && g.N % tc::BN == 0; }
 
 void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s) {
   using namespace tc;
+  constexpr int CG = kTcCtaGroup;
   const int nseg_total = g.seg0 + g.nseg;  // the map spans every segment up to this launch's last
   const uint64_t adims[3] = {(uint64_t)g.K, (uint64_t)g.Cm, (uint64_t)nseg_total};
   const uint64_t astr[2] = {(uint64_t)g.K * 2, (uint64_t)g.Cm * g.K * 2};
-  const uint32_t abox[3] = {BK, BM, 1};
+  const uint32_t abox[3] = {BK, 128, 1};
   CUtensorMap ma = make_map(g.A, 3, adims, astr, abox);
   CUtensorMap mb;
   if (b_kmajor) {  // W [El][N][K]
     const uint64_t bd[2] = {(uint64_t)g.K, (uint64_t)g.El * g.N};
     const uint64_t bs[1] = {(uint64_t)g.K * 2};
-    const uint32_t bb[2] = {BK, BN};
+    const uint32_t bb[2] = {BK, (uint32_t)Geo<CG>::B_ROWS};
     mb = make_map(g.B, 2, bd, bs, bb);
   } else {  // W [El][K][N]
     const uint64_t bd[2] = {(uint64_t)g.N, (uint64_t)g.El * g.K};
@@ -491,24 +602,16 @@ void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s
   p.Cm = g.Cm;
   p.N = g.N;
   p.K = g.K;
-  p.epi = epi;
   p.D = (__nv_bfloat16*)g.D;
   p.aux = (const __nv_bfloat16*)g.aux;
-  const int grid = num_sms();
-  if (b_kmajor) {
-    if (epi == kEpiRelu) launch<false, false, kEpiRelu>(ma, mb, p, grid, s);
-    else if (epi == kEpiMask) launch<false, false, kEpiMask>(ma, mb, p, grid, s);
-    else launch<false, false, kEpiNone>(ma, mb, p, grid, s);
-  } else {
-    if (epi == kEpiRelu) launch<false, true, kEpiRelu>(ma, mb, p, grid, s);
-    else if (epi == kEpiMask) launch<false, true, kEpiMask>(ma, mb, p, grid, s);
-    else launch<false, true, kEpiNone>(ma, mb, p, grid, s);
-  }
+  const int grid = num_sms() / CG * CG;
+  row_dispatch<CG>(ma, mb, p, b_kmajor, epi, grid, s);
   LINA_LAUNCH_CHECK();
 }
 
 void launch_wgrad_tc(const WGrad& g, cudaStream_t s) {
   using namespace tc;
+  constexpr int CG = kTcCtaGroup;
   const uint64_t nseg_total = (uint64_t)g.nchunks * g.P * g.El;
   const uint64_t ad[3] = {(uint64_t)g.M, (uint64_t)g.Cm, nseg_total};
   const uint64_t as[2] = {(uint64_t)g.M * 2, (uint64_t)g.Cm * g.M * 2};
@@ -527,9 +630,10 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s) {
   p.nchunks = g.nchunks;
   p.P = g.P;
   p.D = (__nv_bfloat16*)g.D;
-  const int tiles = g.El * (g.M / BM) * (g.N / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  launch<true, true, kEpiNone>(ma, mb, p, grid, s);
+  const int tiles = g.El * (g.M / Geo<CG>::ROWS) * (g.N / BN);
+  const int maxc = num_sms() / CG;
+  const int grid = (tiles < maxc ? tiles : maxc) * CG;
+  launch<CG, true, true, kEpiNone>(ma, mb, p, grid, s);
   LINA_LAUNCH_CHECK();
 }
 

@@ -94,23 +94,23 @@ __global__ void vcount_kernel(const int* __restrict__ recv_kept, int P, int El, 
   vcount[i] = v < 0 ? 0 : (v > Cc ? Cc : v);
 }
 
-__global__ void mtile_prefix_kernel(const int* __restrict__ vcount, int n, int nseg,
+__global__ void mtile_prefix_kernel(const int* __restrict__ vcount, int n, int nseg, int rows,
                                     int* __restrict__ mtp) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   int run = 0;
   for (int i = 0; i < nseg; ++i) {
     mtp[c * (nseg + 1) + i] = run;
-    run += (vcount[c * nseg + i] + 127) / 128;
+    run += (vcount[c * nseg + i] + rows - 1) / rows;
   }
   mtp[c * (nseg + 1) + nseg] = run;
 }
 
 }  // namespace
 
-void launch_mtile_prefix(const int* vcount, int n, int nseg, int* mtp, cudaStream_t s) {
+void launch_mtile_prefix(const int* vcount, int n, int nseg, int rows, int* mtp, cudaStream_t s) {
   if (n <= 0) return;
-  mtile_prefix_kernel<<<(n + 63) / 64, 64, 0, s>>>(vcount, n, nseg, mtp);
+  mtile_prefix_kernel<<<(n + 63) / 64, 64, 0, s>>>(vcount, n, nseg, rows, mtp);
   LINA_LAUNCH_CHECK();
 }
 

@@ -196,7 +196,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   if (p.P == 1) {
     // All experts local: the "all-to-all" is the identity and chunks only re-slice the GEMMs.
     launch_vcount(q.kept, 1, p.E, p.C, p.n, q.vcount, s);
-    launch_mtile_prefix(q.vcount, p.n, p.P * p.El, q.mtp, s);
+    launch_mtile_prefix(q.vcount, p.n, p.P * p.El, tc_tile_rows(), q.mtp, s);
     prof_begin(cm, s);
     for (int c = 0; c < p.n; ++c) {
       row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s);
@@ -222,7 +222,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   }
   LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_cnt, 0));
   launch_vcount(q.recv_kept, p.P, p.El, p.C, n, q.vcount, s);
-  launch_mtile_prefix(q.vcount, n, p.P * p.El, q.mtp, s);
+  launch_mtile_prefix(q.vcount, n, p.P * p.El, tc_tile_rows(), q.mtp, s);
   for (int c = 0; c < n; ++c) {
     LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_disp[c], 0));
     prof_begin(cm, s);
