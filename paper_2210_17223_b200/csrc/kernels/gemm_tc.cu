@@ -50,7 +50,8 @@ template <int CG> struct Geo {
   static constexpr int B_BYTES = B_ROWS * BK * 2;        // 32 KB (CG=1) / 16 KB (CG=2)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = CG == 2 ? 6 : 4;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int EPI_BYTES = 4 * 2 * 4096;           // 4 epilogue warps x 2 x (32 rows x 128 B)
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -128,6 +129,26 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, ui
         "l"(tm), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
   }
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const void* src, int c0, int c1,
+                                             int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(tm),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void st_shared16(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tm) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tm) : "memory");
@@ -238,12 +259,13 @@ struct TcParams {
 template <int CG, bool WGRAD, bool B_MN, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   TcParams p) {
+                   const __grid_constant__ CUtensorMap tmD, TcParams p) {
   using G = Geo<CG>;
   constexpr int STAGES = G::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + STAGES * G::STAGE_BYTES);
+  uint8_t* epi_smem = smem + STAGES * G::STAGE_BYTES;   // [4 warps][2 buffers][32 rows][128 B]
+  uint64_t* full = (uint64_t*)(epi_smem + G::EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -263,6 +285,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    prefetch_tmap(&tmD);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -402,10 +425,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // ================= epilogue (warps 2..5): TMEM lane quarter = warp % 4
+    // Each warp owns 32 rows: TMEM -> registers -> epi -> bf16 -> a 128B-swizzled
+    // 32 x 64 smem box -> TMA store (rows past the segment end are clipped by the
+    // tensor map).  Two boxes per warp alternate so the store of one overlaps the
+    // fill of the next.
     const int quarter = warp & 3;
     const int row_in_tile = 128 * rank + quarter * 32 + lane;
+    uint8_t* my_epi = epi_smem + quarter * 8192;
     int acc = 0;
     uint32_t aph = 0;
+    int sub = 0;  // sub-tile counter (buffer = sub & 1)
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       int se, m0, n0;
       decode(t, se, m0, n0);
@@ -413,48 +442,67 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const int r = m0 + row_in_tile;
-      __nv_bfloat16* drow;
+      const int box_row = m0 + 128 * rank + quarter * 32;  // first row of this warp's box
+      int c2;
       const __nv_bfloat16* arow = nullptr;
       bool valid;
       if (WGRAD) {
         valid = r < p.M;
-        drow = p.D + ((size_t)se * p.M + r) * p.N + n0;
+        c2 = se;
       } else {
         const int seg = p.seg0 + se;
         valid = r < p.Cm;
-        drow = p.D + ((size_t)seg * p.Cm + r) * p.N + n0;
+        c2 = seg;
         if (EPI == kEpiMask) arow = p.aux + ((size_t)seg * p.Cm + r) * p.N + n0;
       }
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t v[32];
-        float h[32];
-        if (EPI == kEpiMask && valid) {  // issue the aux loads before waiting on TMEM
+      for (int c0 = 0; c0 < BN; c0 += 64, ++sub) {
+        uint8_t* buf = my_epi + (sub & 1) * 4096;
+        float h[64];
+        if (EPI == kEpiMask) {  // issue the aux loads before waiting on TMEM
 #pragma unroll
-          for (int q = 0; q < 4; ++q) load16(arow + c0 + q * 8, h + q * 8, (const __nv_bfloat16*)nullptr);
+          for (int q = 0; q < 8; ++q) {
+            if (valid) load16(arow + c0 + q * 8, h + q * 8, (const __nv_bfloat16*)nullptr);
+            else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) h[q * 8 + i] = 0.f;
+            }
+          }
         }
+        uint32_t v[64];
         if (nkb > 0) {
-          tmem_ld32(tbase + c0, v);
+          tmem_ld32(tbase + c0, *reinterpret_cast<uint32_t(*)[32]>(v));
+          tmem_ld32(tbase + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
           tmem_wait_ld();
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0u;
+          for (int i = 0; i < 64; ++i) v[i] = 0u;
         }
-        if (valid) {
-          float x[32];
+        if (lane == 0 && sub >= 2) bulk_wait_read1();  // the store that last used `buf` has read it
+        __syncwarp();
+        const uint32_t rowaddr = smem_u32(buf) + lane * 128;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
-          if (EPI == kEpiRelu) {
+        for (int q = 0; q < 8; ++q) {
+          float x[8];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = fmaxf(x[i], 0.f);
+          for (int i = 0; i < 8; ++i) {
+            float y = __uint_as_float(v[q * 8 + i]);
+            if (EPI == kEpiRelu) y = fmaxf(y, 0.f);
+            if (EPI == kEpiMask) y = h[q * 8 + i] > 0.f ? y : 0.f;
+            x[i] = y;
           }
-          if (EPI == kEpiMask) {
+          uint4 pk;
+          __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&pk);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = h[i] > 0.f ? x[i] : 0.f;
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) store16(drow + c0 + q * 8, x + q * 8, (__nv_bfloat16*)nullptr);
+          for (int i = 0; i < 4; ++i) hp[i] = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+          st_shared16(rowaddr + ((q ^ (lane & 7)) << 4), pk);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tmD, buf, n0 + c0, box_row, c2);
+          bulk_commit();
         }
       }
       tc_fence_before();
@@ -468,6 +516,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         aph ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
   __syncwarp();
   tc_fence_before();
@@ -527,8 +576,8 @@ static int num_sms() {
 }
 
 template <int CG, bool WGRAD, bool B_MN, int EPI>
-static void launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int grid,
-                   cudaStream_t s) {
+static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const TcParams& p,
+                   int grid, cudaStream_t s) {
   auto kern = tc_gemm_kernel<CG, WGRAD, B_MN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -548,20 +597,20 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  LINA_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, b, p));
+  LINA_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, b, d, p));
 }
 
 template <int CG>
-static void row_dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p, bool b_kmajor,
-                         int epi, int grid, cudaStream_t s) {
+static void row_dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
+                         const TcParams& p, bool b_kmajor, int epi, int grid, cudaStream_t s) {
   if (b_kmajor) {
-    if (epi == kEpiRelu) launch<CG, false, false, kEpiRelu>(ma, mb, p, grid, s);
-    else if (epi == kEpiMask) launch<CG, false, false, kEpiMask>(ma, mb, p, grid, s);
-    else launch<CG, false, false, kEpiNone>(ma, mb, p, grid, s);
+    if (epi == kEpiRelu) launch<CG, false, false, kEpiRelu>(ma, mb, md, p, grid, s);
+    else if (epi == kEpiMask) launch<CG, false, false, kEpiMask>(ma, mb, md, p, grid, s);
+    else launch<CG, false, false, kEpiNone>(ma, mb, md, p, grid, s);
   } else {
-    if (epi == kEpiRelu) launch<CG, false, true, kEpiRelu>(ma, mb, p, grid, s);
-    else if (epi == kEpiMask) launch<CG, false, true, kEpiMask>(ma, mb, p, grid, s);
-    else launch<CG, false, true, kEpiNone>(ma, mb, p, grid, s);
+    if (epi == kEpiRelu) launch<CG, false, true, kEpiRelu>(ma, mb, md, p, grid, s);
+    else if (epi == kEpiMask) launch<CG, false, true, kEpiMask>(ma, mb, md, p, grid, s);
+    else launch<CG, false, true, kEpiNone>(ma, mb, md, p, grid, s);
   }
 }
 
@@ -604,8 +653,12 @@ void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s
   p.K = g.K;
   p.D = (__nv_bfloat16*)g.D;
   p.aux = (const __nv_bfloat16*)g.aux;
+  const uint64_t ddims[3] = {(uint64_t)g.N, (uint64_t)g.Cm, (uint64_t)nseg_total};
+  const uint64_t dstr[2] = {(uint64_t)g.N * 2, (uint64_t)g.Cm * g.N * 2};
+  const uint32_t dbox[3] = {64, 32, 1};
+  CUtensorMap md = make_map(g.D, 3, ddims, dstr, dbox);
   const int grid = num_sms() / CG * CG;
-  row_dispatch<CG>(ma, mb, p, b_kmajor, epi, grid, s);
+  row_dispatch<CG>(ma, mb, md, p, b_kmajor, epi, grid, s);
   LINA_LAUNCH_CHECK();
 }
 
@@ -633,7 +686,11 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s) {
   const int tiles = g.El * (g.M / Geo<CG>::ROWS) * (g.N / BN);
   const int maxc = num_sms() / CG;
   const int grid = (tiles < maxc ? tiles : maxc) * CG;
-  launch<CG, true, true, kEpiNone>(ma, mb, p, grid, s);
+  const uint64_t dd[3] = {(uint64_t)g.N, (uint64_t)g.M, (uint64_t)g.El};
+  const uint64_t ds[2] = {(uint64_t)g.N * 2, (uint64_t)g.M * g.N * 2};
+  const uint32_t db[3] = {64, 32, 1};
+  CUtensorMap md = make_map(g.D, 3, dd, ds, db);
+  launch<CG, true, true, kEpiNone>(ma, mb, md, p, grid, s);
   LINA_LAUNCH_CHECK();
 }
 

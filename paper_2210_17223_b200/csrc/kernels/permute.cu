@@ -65,6 +65,7 @@ __global__ void combine_kernel(const T* __restrict__ Recv, const int* __restrict
       ++kk;
     }
   }
+#pragma unroll 4
   for (int v = lane; v < d / V; v += 32) {
     float acc[V];
 #pragma unroll
