@@ -7,13 +7,20 @@
 // (R2); top-k keyed on the logits, ties to the lower expert id (R3); k=1 gate is
 // the raw probability, k>=2 renormalised over the k selected (R4).
 //
-// Layout: X [T,d] (bf16|fp32) row-major, Wg [d,E] fp32 row-major.  One CTA of 256
-// threads owns BT=32 tokens x all E experts; the d reduction runs in 64/128-column
-// slabs staged in shared memory (X transposed to fp32, Wg slab), each thread
-// keeping one token x E/8 experts in registers.  Each logit is one fp32 FMA chain in ascending d
-// order: deterministic, and exact for the grid inputs of DESIGN.md §4.  The
-// epilogue keeps logits in shared memory and gives one warp per token for the
-// softmax (warp-shuffle max/sum) and k rounds of warp arg-max.
+// Layout: X [T,d] (bf16|fp32) row-major, Wg [d,E] fp32 row-major.
+//
+// bf16 tokens (gate_mma_kernel): the logits X·Wg are an N = E <= 64 GEMM.  Each warp
+// owns 16 tokens and runs mma.sync m16n8k16 (bf16 in, fp32 accumulate) with the
+// fp32 gate weight split exactly into three bf16 terms (w = hi + mid + lo, 24 =
+// 3 x 8 significand bits), so the product is the fp32 logit up to accumulation
+// order — exact for the grid inputs of DESIGN.md §4.  Tokens are read straight from
+// global memory as 16-byte vectors (16 loads in flight per lane per 256-column
+// slab); K is permuted consistently in A and B so each 16-byte vector feeds two
+// k-steps.  Wg slabs are staged transposed in shared memory (row pitch padded to
+// avoid bank conflicts) and split on the fly.
+// fp32 tokens (gate_simt_kernel, the C1 path): a register-tiled FMA version.
+// Both end in the same epilogue: logits in shared memory, one warp per token for
+// the softmax (warp-shuffle max/sum) and k rounds of warp arg-max.
 #include <math.h>
 
 #include "../common.h"
@@ -22,18 +29,166 @@
 namespace lina {
 namespace {
 
-constexpr int kGateBT = 32;
-
 __device__ __forceinline__ bool key_better(float la, int ia, float lb, int ib) {
   return la > lb || (la == lb && ia < ib);
 }
 
+// Softmax, top-k and gate weights for one token whose E logits are in `lrow`
+// (shared memory).  Called by one full warp.
+__device__ __forceinline__ void gate_epilogue_token(const float* lrow, int t, int E, int k,
+                                                    int write_routing, float* __restrict__ probs,
+                                                    int* __restrict__ idx,
+                                                    float* __restrict__ gate) {
+  const int lane = threadIdx.x & 31;
+  const bool v0 = lane < E, v1 = lane + 32 < E;
+  const float l0 = v0 ? lrow[lane] : -INFINITY;
+  const float l1 = v1 ? lrow[lane + 32] : -INFINITY;
+  float mx = fmaxf(l0, l1);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float z0 = v0 ? expf(l0 - mx) : 0.f;
+  const float z1 = v1 ? expf(l1 - mx) : 0.f;
+  float s = z0 + z1;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float p0 = z0 / s, p1 = z1 / s;
+  if (v0) probs[(size_t)t * E + lane] = p0;
+  if (v1) probs[(size_t)t * E + lane + 32] = p1;
+  if (!write_routing) return;
+  bool sel0 = !v0, sel1 = !v1;
+  float psel[8];
+  float psum = 0.f;
+  for (int j = 0; j < k; ++j) {
+    float bl = -INFINITY;
+    int bi = 0x7fffffff;
+    if (!sel0) { bl = l0; bi = lane; }
+    if (!sel1 && key_better(l1, lane + 32, bl, bi)) { bl = l1; bi = lane + 32; }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (key_better(ol, oi, bl, bi)) { bl = ol; bi = oi; }
+    }
+    float pw = 0.f;
+    if (bi == lane) { sel0 = true; pw = p0; }
+    if (bi == lane + 32) { sel1 = true; pw = p1; }
+    pw = __shfl_sync(0xffffffffu, pw, bi & 31);
+    psel[j] = pw;
+    psum += pw;
+    if (lane == 0) idx[(size_t)t * k + j] = bi;
+  }
+  if (lane == 0)
+    for (int j = 0; j < k; ++j) gate[(size_t)t * k + j] = (k == 1) ? psel[0] : psel[j] / psum;
+}
+
+// ------------------------------------------------------------------ tensor-core gate (bf16 X)
+constexpr int kMmaTok = 64;     // tokens per CTA (4 warps x 16)
+constexpr int kSlab = 256;      // d columns per staged Wg slab
+constexpr int kPitch = kSlab + 4;
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void split3(float w, float& hi, float& mid, float& lo) {
+  hi = __bfloat162float(__float2bfloat16_rn(w));
+  const float r1 = w - hi;
+  mid = __bfloat162float(__float2bfloat16_rn(r1));
+  lo = r1 - mid;  // <= 8 significant bits: exact in bf16
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int NT>  // NT = ceil(E/8) n-tiles of 8 experts
+__global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __restrict__ X,
+                                                       const float* __restrict__ Wg, int T, int d,
+                                                       int E, int k, int write_routing,
+                                                       float* __restrict__ probs,
+                                                       int* __restrict__ idx,
+                                                       float* __restrict__ gate) {
+  extern __shared__ float gsm[];
+  float* wt = gsm;                          // [NT*8][kPitch]  transposed Wg slab
+  float* lt = gsm + NT * 8 * kPitch;        // [kMmaTok][NT*8 + 1] logits
+  constexpr int LP = NT * 8 + 1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int t0 = blockIdx.x * kMmaTok + warp * 16;
+  const int ra = t0 + g, rb = t0 + g + 8;
+  float c[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[n][i] = 0.f;
+
+  for (int s0 = 0; s0 < d; s0 += kSlab) {
+    // X: 8 x 32-column blocks, rows g and g+8, 16 bytes each — all issued before use
+    uint4 xa[8], xb[8];
+#pragma unroll
+    for (int kb = 0; kb < 8; ++kb) {
+      const int col = s0 + kb * 32 + tq * 8;
+      const bool in = col < d;
+      xa[kb] = (in && ra < T) ? *reinterpret_cast<const uint4*>(X + (size_t)ra * d + col) : make_uint4(0, 0, 0, 0);
+      xb[kb] = (in && rb < T) ? *reinterpret_cast<const uint4*>(X + (size_t)rb * d + col) : make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();  // previous slab's B reads are done
+    for (int i = tid; i < NT * 8 * kSlab; i += 128) {
+      const int col = i % kSlab, e = i / kSlab;
+      wt[e * kPitch + col] = (e < E && s0 + col < d) ? __ldg(Wg + (size_t)(s0 + col) * E + e) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kb = 0; kb < 8; ++kb) {
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        // logical k (2tq, 2tq+1 | 2tq+8, 2tq+9) <-> physical columns kb*32 + 8tq + 4s + (0,1 | 2,3)
+        const uint32_t a[4] = {s ? xa[kb].z : xa[kb].x, s ? xb[kb].z : xb[kb].x,
+                               s ? xa[kb].w : xa[kb].y, s ? xb[kb].w : xb[kb].y};
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const float4 w = *reinterpret_cast<const float4*>(wt + (n * 8 + g) * kPitch + kb * 32 + tq * 8 + s * 4);
+          float h0, m0, l0, h1, m1, l1, h2, m2, l2, h3, m3, l3;
+          split3(w.x, h0, m0, l0);
+          split3(w.y, h1, m1, l1);
+          split3(w.z, h2, m2, l2);
+          split3(w.w, h3, m3, l3);
+          mma16816(c[n], a, pack_bf16(h0, h1), pack_bf16(h2, h3));
+          mma16816(c[n], a, pack_bf16(m0, m1), pack_bf16(m2, m3));
+          mma16816(c[n], a, pack_bf16(l0, l1), pack_bf16(l2, l3));
+        }
+      }
+    }
+  }
+  // fragments -> shared logits: c0,c1 = (row g, cols 2tq, 2tq+1); c2,c3 = (row g+8, ...)
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    float* r0 = lt + (warp * 16 + g) * LP + n * 8 + 2 * tq;
+    float* r1 = lt + (warp * 16 + g + 8) * LP + n * 8 + 2 * tq;
+    r0[0] = c[n][0];
+    r0[1] = c[n][1];
+    r1[0] = c[n][2];
+    r1[1] = c[n][3];
+  }
+  __syncwarp();
+  for (int r = 0; r < 16; ++r) {
+    const int t = t0 + r;
+    if (t >= T) break;
+    gate_epilogue_token(lt + (warp * 16 + r) * LP, t, E, k, write_routing, probs, idx, gate);
+  }
+}
+
+// ------------------------------------------------------------------ SIMT gate (fp32 X)
+constexpr int kGateBT = 32;
+
 // EP = padded expert count (8/16/32/64).  Threads: 8 along experts (TE = EP/8 each) x
-// 32 along tokens (one token each).  DK-column slabs of X (transposed to fp32) and Wg
-// are double-buffered through registers: the global loads of slab i+1 are issued
-// before the FMAs of slab i, so each CTA keeps its next 4 KB-8 KB in flight.
+// 32 along tokens.  DK-column slabs of X (transposed to fp32) and Wg are
+// double-buffered through registers.
 template <typename TIn, int EP>
-__global__ void __launch_bounds__(256) gate_topk_kernel(const TIn* __restrict__ X,
+__global__ void __launch_bounds__(256) gate_simt_kernel(const TIn* __restrict__ X,
                                                         const float* __restrict__ Wg, int T, int d,
                                                         int E, int k, int write_routing,
                                                         float* __restrict__ probs,
@@ -42,26 +197,25 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const TIn* __restrict__ 
   constexpr int BT = kGateBT;
   constexpr int DK = (EP <= 16) ? 128 : 64;
   constexpr int TE = EP / 8;
-  constexpr int XV = BT * DK / 256;        // X elements per thread per slab (16 or 8)
-  constexpr int WV = DK * EP / 256;        // Wg floats per thread per slab
+  constexpr int XV = BT * DK / 256;
+  constexpr int WV = DK * EP / 256;
   __shared__ float xs[DK][BT + 1];
   __shared__ float ws[DK][EP];
   __shared__ float lt[BT][EP + 1];
 
   const int tid = threadIdx.x;
-  const int tx = tid & 7, ty = tid >> 3;   // expert group, token
+  const int tx = tid & 7, ty = tid >> 3;
   const int t0 = blockIdx.x * BT;
-  // slab loaders: X row r = tid / (DK/XV), columns cs..cs+XV; Wg flat index tid*WV..
-  constexpr int XT = DK / XV;              // threads per X row
+  constexpr int XT = DK / XV;
   const int xr = tid / XT, xc = (tid % XT) * XV;
   float xreg[XV], wreg[WV];
   auto load_slab = [&](int k0) {
     const int t = t0 + xr;
 #pragma unroll
     for (int i = 0; i < XV; i += 8) {
-      const int c = k0 + xc + i;
-      if (t < T && c + 8 <= d && ((d * (int)sizeof(TIn)) % 16 == 0)) {
-        const TIn* src = X + (size_t)t * d + c;
+      const int cc = k0 + xc + i;
+      if (t < T && cc + 8 <= d && ((d * (int)sizeof(TIn)) % 16 == 0)) {
+        const TIn* src = X + (size_t)t * d + cc;
         if constexpr (sizeof(TIn) == 2) {
           load16(src, xreg + i, (const __nv_bfloat16*)nullptr);
         } else {
@@ -71,7 +225,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const TIn* __restrict__ 
       } else {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          xreg[i + q] = (t < T && c + q < d) ? Elt<TIn>::to_f(X[(size_t)t * d + c + q]) : 0.f;
+          xreg[i + q] = (t < T && cc + q < d) ? Elt<TIn>::to_f(X[(size_t)t * d + cc + q]) : 0.f;
       }
     }
 #pragma unroll
@@ -97,7 +251,7 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const TIn* __restrict__ 
   for (int k0 = 0; k0 < d; k0 += DK) {
     store_slab();
     __syncthreads();
-    if (k0 + DK < d) load_slab(k0 + DK);   // in flight during the FMAs below
+    if (k0 + DK < d) load_slab(k0 + DK);  // in flight during the FMAs below
 #pragma unroll 8
     for (int kk = 0; kk < DK; ++kk) {
       const float a = xs[kk][ty];
@@ -109,63 +263,35 @@ __global__ void __launch_bounds__(256) gate_topk_kernel(const TIn* __restrict__ 
 #pragma unroll
   for (int e = 0; e < TE; ++e) lt[ty][tx * TE + e] = acc[e];
   __syncthreads();
-
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int r = warp; r < kGateBT; r += 8) {
+  const int warp = tid >> 5;
+  for (int r = warp; r < BT; r += 8) {
     const int t = t0 + r;
     if (t >= T) break;
-    const bool v0 = lane < E, v1 = lane + 32 < E;
-    const float l0 = v0 ? lt[r][lane] : -INFINITY;
-    const float l1 = v1 ? lt[r][lane + 32] : -INFINITY;
-    float mx = fmaxf(l0, l1);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float z0 = v0 ? expf(l0 - mx) : 0.f;
-    const float z1 = v1 ? expf(l1 - mx) : 0.f;
-    float s = z0 + z1;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const float p0 = z0 / s, p1 = z1 / s;
-    if (v0) probs[(size_t)t * E + lane] = p0;
-    if (v1) probs[(size_t)t * E + lane + 32] = p1;
-    if (!write_routing) continue;
-    // k rounds of warp arg-max on (logit desc, id asc)
-    bool sel0 = !v0, sel1 = !v1;
-    float psel[8];
-    float psum = 0.f;
-    for (int j = 0; j < k; ++j) {
-      float bl = -INFINITY;
-      int bi = 0x7fffffff;
-      if (!sel0) { bl = l0; bi = lane; }
-      if (!sel1 && key_better(l1, lane + 32, bl, bi)) { bl = l1; bi = lane + 32; }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const float ol = __shfl_xor_sync(0xffffffffu, bl, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (key_better(ol, oi, bl, bi)) { bl = ol; bi = oi; }
-      }
-      // owner lane marks it; broadcast its probability
-      float pw = 0.f;
-      if (bi == lane) { sel0 = true; pw = p0; }
-      if (bi == lane + 32) { sel1 = true; pw = p1; }
-      const int owner = bi & 31;
-      pw = __shfl_sync(0xffffffffu, pw, owner);
-      psel[j] = pw;
-      psum += pw;
-      if (lane == 0) idx[(size_t)t * k + j] = bi;
-    }
-    if (lane == 0) {
-      for (int j = 0; j < k; ++j) gate[(size_t)t * k + j] = (k == 1) ? psel[0] : psel[j] / psum;
-    }
+    gate_epilogue_token(lt[r], t, E, k, write_routing, probs, idx, gate);
   }
 }
 
 template <typename TIn, int EP>
-void launch_gate_ep(const void* X, const float* Wg, int T, int d, int E, int k, int write_routing,
-                    float* probs, int* idx, float* gate, cudaStream_t s) {
+void launch_gate_simt(const void* X, const float* Wg, int T, int d, int E, int k, int write_routing,
+                      float* probs, int* idx, float* gate, cudaStream_t s) {
   const int blocks = (T + kGateBT - 1) / kGateBT;
-  gate_topk_kernel<TIn, EP><<<blocks, 256, 0, s>>>((const TIn*)X, Wg, T, d, E, k, write_routing,
-                                                    probs, idx, gate);
+  gate_simt_kernel<TIn, EP><<<blocks, 256, 0, s>>>((const TIn*)X, Wg, T, d, E, k, write_routing, probs,
+                                                    idx, gate);
+}
+
+template <int NT>
+void launch_gate_mma(const void* X, const float* Wg, int T, int d, int E, int k, int write_routing,
+                     float* probs, int* idx, float* gate, cudaStream_t s) {
+  const size_t smem = sizeof(float) * ((size_t)NT * 8 * kPitch + kMmaTok * (NT * 8 + 1));
+  static bool set = false;
+  if (!set) {
+    LINA_CUDA_CHECK(cudaFuncSetAttribute(gate_mma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+    set = true;
+  }
+  const int blocks = (T + kMmaTok - 1) / kMmaTok;
+  gate_mma_kernel<NT><<<blocks, 128, smem, s>>>((const __nv_bfloat16*)X, Wg, T, d, E, k, write_routing,
+                                                probs, idx, gate);
 }
 
 }  // namespace
@@ -173,15 +299,23 @@ void launch_gate_ep(const void* X, const float* Wg, int T, int d, int E, int k, 
 void launch_gate_topk(int dtype, const void* X, const float* Wg, int T, int d, int E, int k,
                       int write_routing, float* probs, int* idx, float* gate, cudaStream_t s) {
   if (T <= 0) return;
-  auto go = [&](auto tag) {
-    using TIn = decltype(tag);
-    if (E <= 8) launch_gate_ep<TIn, 8>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
-    else if (E <= 16) launch_gate_ep<TIn, 16>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
-    else if (E <= 32) launch_gate_ep<TIn, 32>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
-    else launch_gate_ep<TIn, 64>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
-  };
-  if (dtype == 0) go(float{});
-  else go(__nv_bfloat16{});
+  if (dtype == 1 && d % 32 == 0) {
+    const int nt = (E + 7) / 8;
+    if (nt <= 1) launch_gate_mma<1>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
+    else if (nt <= 2) launch_gate_mma<2>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
+    else if (nt <= 4) launch_gate_mma<4>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
+    else launch_gate_mma<8>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
+  } else {
+    auto go = [&](auto tag) {
+      using TIn = decltype(tag);
+      if (E <= 8) launch_gate_simt<TIn, 8>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
+      else if (E <= 16) launch_gate_simt<TIn, 16>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
+      else if (E <= 32) launch_gate_simt<TIn, 32>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
+      else launch_gate_simt<TIn, 64>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
+    };
+    if (dtype == 0) go(float{});
+    else go(__nv_bfloat16{});
+  }
   LINA_LAUNCH_CHECK();
 }
 

@@ -259,7 +259,8 @@ struct TcParams {
 template <int CG, bool WGRAD, bool B_MN, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmD, TcParams p) {
+                   const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
+                   TcParams p) {
   using G = Geo<CG>;
   constexpr int STAGES = G::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     prefetch_tmap(&tmD);
+    if (EPI == kEpiMask) prefetch_tmap(&tmX);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -294,6 +296,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);
     }
+    for (int a = 0; a < 8; ++a) mbar_init(tempty + 3 + a, 1);  // epilogue aux-box barriers
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc<CG>(tmem_base_slot, TMEM_COLS);
@@ -428,48 +431,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // Each warp owns 32 rows: TMEM -> registers -> epi -> bf16 -> a 128B-swizzled
     // 32 x 64 smem box -> TMA store (rows past the segment end are clipped by the
     // tensor map).  Two boxes per warp alternate so the store of one overlaps the
-    // fill of the next.
+    // fill of the next.  The ReLU'-mask epilogue (dgrad) TMA-loads the matching
+    // 32 x 64 box of H into the same buffer one sub-tile ahead.
     const int quarter = warp & 3;
-    const int row_in_tile = 128 * rank + quarter * 32 + lane;
     uint8_t* my_epi = epi_smem + quarter * 8192;
+    uint64_t* abar = tempty + 2 + 1 + quarter * 2;   // 2 aux barriers per warp (after the TMEM slot)
+    uint32_t abph = 0;                               // bit b = phase of abar[b]
     int acc = 0;
     uint32_t aph = 0;
     int sub = 0;  // sub-tile counter (buffer = sub & 1)
+    auto box_of = [&](int t, int c0, int& x0, int& x1, int& x2) {
+      int se, m0, n0;
+      decode(t, se, m0, n0);
+      x0 = n0 + c0;
+      x1 = m0 + 128 * rank + quarter * 32;
+      x2 = WGRAD ? se : p.seg0 + se;
+    };
+    if (EPI == kEpiMask && lane == 0 && cluster_id < total_tiles) {  // first aux box
+      int x0, x1, x2;
+      box_of(cluster_id, 0, x0, x1, x2);
+      mbar_expect_tx(&abar[0], 4096);
+      tma_load_3d<1>(my_epi, &tmX, &abar[0], x0, x1, x2);
+    }
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       int se, m0, n0;
       decode(t, se, m0, n0);
       const int nkb = kblocks_of(se);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int r = m0 + row_in_tile;
-      const int box_row = m0 + 128 * rank + quarter * 32;  // first row of this warp's box
-      int c2;
-      const __nv_bfloat16* arow = nullptr;
-      bool valid;
-      if (WGRAD) {
-        valid = r < p.M;
-        c2 = se;
-      } else {
-        const int seg = p.seg0 + se;
-        valid = r < p.Cm;
-        c2 = seg;
-        if (EPI == kEpiMask) arow = p.aux + ((size_t)seg * p.Cm + r) * p.N + n0;
-      }
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 64, ++sub) {
-        uint8_t* buf = my_epi + (sub & 1) * 4096;
-        float h[64];
-        if (EPI == kEpiMask) {  // issue the aux loads before waiting on TMEM
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            if (valid) load16(arow + c0 + q * 8, h + q * 8, (const __nv_bfloat16*)nullptr);
-            else {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) h[q * 8 + i] = 0.f;
-            }
-          }
-        }
+        const int b = sub & 1;
+        uint8_t* buf = my_epi + b * 4096;
+        const uint32_t rowaddr = smem_u32(buf) + lane * 128;
         uint32_t v[64];
         if (nkb > 0) {
           tmem_ld32(tbase + c0, *reinterpret_cast<uint32_t(*)[32]>(v));
@@ -479,31 +474,66 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 64; ++i) v[i] = 0u;
         }
-        if (lane == 0 && sub >= 2) bulk_wait_read1();  // the store that last used `buf` has read it
-        __syncwarp();
-        const uint32_t rowaddr = smem_u32(buf) + lane * 128;
+        if (EPI == kEpiMask) {
+          mbar_wait(&abar[b], (abph >> b) & 1);
+          abph ^= 1u << b;
+        } else {
+          if (lane == 0 && sub >= 2) bulk_wait_read1();  // the store that last used `buf` has read it
+          __syncwarp();
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
+          const uint32_t qa = rowaddr + ((q ^ (lane & 7)) << 4);
+          float hx[8];
+          if (EPI == kEpiMask) {
+            uint4 hv;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(hv.x), "=r"(hv.y), "=r"(hv.z), "=r"(hv.w)
+                         : "r"(qa));
+            const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&hv);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __bfloat1622float2(hh[i]);
+              hx[2 * i] = f.x;
+              hx[2 * i + 1] = f.y;
+            }
+          }
           float x[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             float y = __uint_as_float(v[q * 8 + i]);
             if (EPI == kEpiRelu) y = fmaxf(y, 0.f);
-            if (EPI == kEpiMask) y = h[q * 8 + i] > 0.f ? y : 0.f;
+            if (EPI == kEpiMask) y = hx[i] > 0.f ? y : 0.f;
             x[i] = y;
           }
           uint4 pk;
           __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&pk);
 #pragma unroll
           for (int i = 0; i < 4; ++i) hp[i] = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
-          st_shared16(rowaddr + ((q ^ (lane & 7)) << 4), pk);
+          st_shared16(qa, pk);
         }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_3d(&tmD, buf, n0 + c0, box_row, c2);
+          int x0, x1, x2;
+          box_of(t, c0, x0, x1, x2);
+          tma_store_3d(&tmD, buf, x0, x1, x2);
           bulk_commit();
+          if (EPI == kEpiMask) {  // prefetch the next sub-tile's H box into the other buffer
+            int nt = t, nc = c0 + 64;
+            if (nc == BN) {
+              nc = 0;
+              nt = t + num_clusters;
+            }
+            if (nt < total_tiles) {
+              bulk_wait_read1();  // the store that last used the other buffer has read it
+              box_of(nt, nc, x0, x1, x2);
+              mbar_expect_tx(&abar[b ^ 1], 4096);
+              tma_load_3d<1>(my_epi + (b ^ 1) * 4096, &tmX, &abar[b ^ 1], x0, x1, x2);
+            }
+          }
         }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
@@ -576,8 +606,8 @@ static int num_sms() {
 }
 
 template <int CG, bool WGRAD, bool B_MN, int EPI>
-static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const TcParams& p,
-                   int grid, cudaStream_t s) {
+static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const CUtensorMap& x,
+                   const TcParams& p, int grid, cudaStream_t s) {
   auto kern = tc_gemm_kernel<CG, WGRAD, B_MN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -597,20 +627,21 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  LINA_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, b, d, p));
+  LINA_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, b, d, x, p));
 }
 
 template <int CG>
 static void row_dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
-                         const TcParams& p, bool b_kmajor, int epi, int grid, cudaStream_t s) {
+                         const CUtensorMap& mx, const TcParams& p, bool b_kmajor, int epi, int grid,
+                         cudaStream_t s) {
   if (b_kmajor) {
-    if (epi == kEpiRelu) launch<CG, false, false, kEpiRelu>(ma, mb, md, p, grid, s);
-    else if (epi == kEpiMask) launch<CG, false, false, kEpiMask>(ma, mb, md, p, grid, s);
-    else launch<CG, false, false, kEpiNone>(ma, mb, md, p, grid, s);
+    if (epi == kEpiRelu) launch<CG, false, false, kEpiRelu>(ma, mb, md, mx, p, grid, s);
+    else if (epi == kEpiMask) launch<CG, false, false, kEpiMask>(ma, mb, md, mx, p, grid, s);
+    else launch<CG, false, false, kEpiNone>(ma, mb, md, mx, p, grid, s);
   } else {
-    if (epi == kEpiRelu) launch<CG, false, true, kEpiRelu>(ma, mb, md, p, grid, s);
-    else if (epi == kEpiMask) launch<CG, false, true, kEpiMask>(ma, mb, md, p, grid, s);
-    else launch<CG, false, true, kEpiNone>(ma, mb, md, p, grid, s);
+    if (epi == kEpiRelu) launch<CG, false, true, kEpiRelu>(ma, mb, md, mx, p, grid, s);
+    else if (epi == kEpiMask) launch<CG, false, true, kEpiMask>(ma, mb, md, mx, p, grid, s);
+    else launch<CG, false, true, kEpiNone>(ma, mb, md, mx, p, grid, s);
   }
 }
 
@@ -657,8 +688,9 @@ void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s
   const uint64_t dstr[2] = {(uint64_t)g.N * 2, (uint64_t)g.Cm * g.N * 2};
   const uint32_t dbox[3] = {64, 32, 1};
   CUtensorMap md = make_map(g.D, 3, ddims, dstr, dbox);
+  CUtensorMap mx = (epi == kEpiMask) ? make_map(g.aux, 3, ddims, dstr, dbox) : md;
   const int grid = num_sms() / CG * CG;
-  row_dispatch<CG>(ma, mb, md, p, b_kmajor, epi, grid, s);
+  row_dispatch<CG>(ma, mb, md, mx, p, b_kmajor, epi, grid, s);
   LINA_LAUNCH_CHECK();
 }
 
@@ -690,7 +722,7 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s) {
   const uint64_t ds[2] = {(uint64_t)g.N * 2, (uint64_t)g.M * g.N * 2};
   const uint32_t db[3] = {64, 32, 1};
   CUtensorMap md = make_map(g.D, 3, dd, ds, db);
-  launch<CG, true, true, kEpiNone>(ma, mb, md, p, grid, s);
+  launch<CG, true, true, kEpiNone>(ma, mb, md, md, p, grid, s);
   LINA_LAUNCH_CHECK();
 }
 
