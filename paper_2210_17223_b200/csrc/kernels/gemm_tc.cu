@@ -369,6 +369,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (!WGRAD) {
           const int seg = p.seg0 + se;
           const int el = se % p.El;
+          if (EPI == kEpiMask) {
+            // Warm L2 with this CTA's 128 x 256 box of the mask operand H about one
+            // tile before the epilogue TMA-loads it into shared memory.
+            for (int yb = 0; yb < 128; yb += 32)
+              for (int xb = 0; xb < BN; xb += 64)
+                asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(&tmX),
+                             "r"(n0 + xb), "r"(m0 + arow + yb), "r"(seg)
+                             : "memory");
+          }
           for (int kb = 0; kb < p.K / BK; ++kb) {
             const int k0 = kb * BK;
             if (!B_MN) issue(k0, m0 + arow, seg, k0, el * p.N + n0 + brow, 0);
