@@ -33,52 +33,62 @@ __device__ __forceinline__ bool key_better(float la, int ia, float lb, int ib) {
   return la > lb || (la == lb && ia < ib);
 }
 
-// Softmax, top-k and gate weights for one token whose E logits are in `lrow`
-// (shared memory).  Called by one full warp.
-__device__ __forceinline__ void gate_epilogue_token(const float* lrow, int t, int E, int k,
-                                                    int write_routing, float* __restrict__ probs,
-                                                    int* __restrict__ idx,
-                                                    float* __restrict__ gate) {
+// Softmax, top-k and gate weights for `nrows` tokens whose E logits are rows of `lt`
+// (shared memory, pitch `ldl`), row r <-> token t0 + r.  Called by one full warp.
+// The warp is cut into 32/W segments of W = pow2ceil(E) lanes (W = 32 and two
+// logits per lane when E > 32), so 4 tokens are reduced at once when E <= 8:
+// every shuffle stays inside its segment (xor offsets < W).
+__device__ __forceinline__ void gate_epilogue_rows(const float* lt, int ldl, int nrows, int t0, int T,
+                                                   int E, int k, int write_routing,
+                                                   float* __restrict__ probs, int* __restrict__ idx,
+                                                   float* __restrict__ gate) {
   const int lane = threadIdx.x & 31;
-  const bool v0 = lane < E, v1 = lane + 32 < E;
-  const float l0 = v0 ? lrow[lane] : -INFINITY;
-  const float l1 = v1 ? lrow[lane + 32] : -INFINITY;
-  float mx = fmaxf(l0, l1);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  const float z0 = v0 ? expf(l0 - mx) : 0.f;
-  const float z1 = v1 ? expf(l1 - mx) : 0.f;
-  float s = z0 + z1;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const float p0 = z0 / s, p1 = z1 / s;
-  if (v0) probs[(size_t)t * E + lane] = p0;
-  if (v1) probs[(size_t)t * E + lane + 32] = p1;
-  if (!write_routing) return;
-  bool sel0 = !v0, sel1 = !v1;
-  float psel[8];
-  float psum = 0.f;
-  for (int j = 0; j < k; ++j) {
-    float bl = -INFINITY;
-    int bi = 0x7fffffff;
-    if (!sel0) { bl = l0; bi = lane; }
-    if (!sel1 && key_better(l1, lane + 32, bl, bi)) { bl = l1; bi = lane + 32; }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const float ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (key_better(ol, oi, bl, bi)) { bl = ol; bi = oi; }
+  int W = 1;
+  while (W < E && W < 32) W <<= 1;
+  const int TP = 32 / W;
+  const int seg = lane / W, sl = lane % W;
+  for (int r0 = 0; r0 < nrows; r0 += TP) {
+    const int r = r0 + seg;
+    const int t = t0 + r;
+    const bool live = r < nrows && t < T;
+    const float* lrow = lt + (size_t)(live ? r : 0) * ldl;
+    const bool v0 = live && sl < E, v1 = live && sl + 32 < E;
+    const float l0 = v0 ? lrow[sl] : -INFINITY;
+    const float l1 = v1 ? lrow[sl + 32] : -INFINITY;
+    float mx = fmaxf(l0, l1);
+    for (int o = W >> 1; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float z0 = v0 ? expf(l0 - mx) : 0.f;
+    const float z1 = v1 ? expf(l1 - mx) : 0.f;
+    float sum = z0 + z1;
+    for (int o = W >> 1; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float p0 = v0 ? z0 / sum : 0.f, p1 = v1 ? z1 / sum : 0.f;
+    if (v0) probs[(size_t)t * E + sl] = p0;
+    if (v1) probs[(size_t)t * E + sl + 32] = p1;
+    if (!write_routing) continue;
+    bool sel0 = !v0, sel1 = !v1;
+    float psel[8];
+    float psum = 0.f;
+    for (int j = 0; j < k; ++j) {
+      float bl = -INFINITY;
+      int bi = 0x7fffffff;
+      if (!sel0) { bl = l0; bi = sl; }
+      if (!sel1 && key_better(l1, sl + 32, bl, bi)) { bl = l1; bi = sl + 32; }
+      for (int o = W >> 1; o; o >>= 1) {
+        const float ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (key_better(ol, oi, bl, bi)) { bl = ol; bi = oi; }
+      }
+      float pw = 0.f;
+      if (bi == sl) { sel0 = true; pw = p0; }
+      if (bi == sl + 32) { sel1 = true; pw = p1; }
+      pw = __shfl_sync(0xffffffffu, pw, seg * W + ((bi & 0x7fffffff) % W));
+      psel[j] = pw;
+      psum += pw;
+      if (live && sl == 0) idx[(size_t)t * k + j] = bi;
     }
-    float pw = 0.f;
-    if (bi == lane) { sel0 = true; pw = p0; }
-    if (bi == lane + 32) { sel1 = true; pw = p1; }
-    pw = __shfl_sync(0xffffffffu, pw, bi & 31);
-    psel[j] = pw;
-    psum += pw;
-    if (lane == 0) idx[(size_t)t * k + j] = bi;
+    if (live && sl == 0)
+      for (int j = 0; j < k; ++j) gate[(size_t)t * k + j] = (k == 1) ? psel[0] : psel[j] / psum;
   }
-  if (lane == 0)
-    for (int j = 0; j < k; ++j) gate[(size_t)t * k + j] = (k == 1) ? psel[0] : psel[j] / psum;
 }
 
 // ------------------------------------------------------------------ tensor-core gate (bf16 X)
@@ -119,11 +129,11 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
   const int g = lane >> 2, tq = lane & 3;
   const int t0 = blockIdx.x * kMmaTok + warp * 16;
   const int ra = t0 + g, rb = t0 + g + 8;
-  float c[NT][4];
+  float c[NT][4], cm[NT][4], cl[NT][4];  // hi / mid / lo partial products: three independent chains
 #pragma unroll
   for (int n = 0; n < NT; ++n)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) c[n][i] = 0.f;
+    for (int i = 0; i < 4; ++i) c[n][i] = cm[n][i] = cl[n][i] = 0.f;
 
   for (int s0 = 0; s0 < d; s0 += kSlab) {
     // X: 8 x 32-column blocks, rows g and g+8, 16 bytes each — all issued before use
@@ -157,13 +167,17 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
           split3(w.z, h2, m2, l2);
           split3(w.w, h3, m3, l3);
           mma16816(c[n], a, pack_bf16(h0, h1), pack_bf16(h2, h3));
-          mma16816(c[n], a, pack_bf16(m0, m1), pack_bf16(m2, m3));
-          mma16816(c[n], a, pack_bf16(l0, l1), pack_bf16(l2, l3));
+          mma16816(cm[n], a, pack_bf16(m0, m1), pack_bf16(m2, m3));
+          mma16816(cl[n], a, pack_bf16(l0, l1), pack_bf16(l2, l3));
         }
       }
     }
   }
   // fragments -> shared logits: c0,c1 = (row g, cols 2tq, 2tq+1); c2,c3 = (row g+8, ...)
+#pragma unroll
+  for (int n = 0; n < NT; ++n)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[n][i] = (c[n][i] + cm[n][i]) + cl[n][i];
 #pragma unroll
   for (int n = 0; n < NT; ++n) {
     float* r0 = lt + (warp * 16 + g) * LP + n * 8 + 2 * tq;
@@ -174,11 +188,7 @@ __global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __re
     r1[1] = c[n][3];
   }
   __syncwarp();
-  for (int r = 0; r < 16; ++r) {
-    const int t = t0 + r;
-    if (t >= T) break;
-    gate_epilogue_token(lt + (warp * 16 + r) * LP, t, E, k, write_routing, probs, idx, gate);
-  }
+  gate_epilogue_rows(lt + warp * 16 * LP, LP, 16, t0, T, E, k, write_routing, probs, idx, gate);
 }
 
 // ------------------------------------------------------------------ SIMT gate (fp32 X)
@@ -264,11 +274,7 @@ __global__ void __launch_bounds__(256) gate_simt_kernel(const TIn* __restrict__ 
   for (int e = 0; e < TE; ++e) lt[ty][tx * TE + e] = acc[e];
   __syncthreads();
   const int warp = tid >> 5;
-  for (int r = warp; r < BT; r += 8) {
-    const int t = t0 + r;
-    if (t >= T) break;
-    gate_epilogue_token(lt[r], t, E, k, write_routing, probs, idx, gate);
-  }
+  gate_epilogue_rows(&lt[warp * 4][0], EP + 1, 4, t0 + warp * 4, T, E, k, write_routing, probs, idx, gate);
 }
 
 template <typename TIn, int EP>

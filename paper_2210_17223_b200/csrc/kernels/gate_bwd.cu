@@ -24,7 +24,7 @@ namespace {
 
 constexpr int kDxTok = 32, kDxCols = 256;
 
-template <typename T>
+template <typename T, int KT>  // KT = k when 1 or 2, 0 = generic k <= 8
 __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe, const int* __restrict__ idx,
                                                        const int* __restrict__ slot,
                                                        const float* __restrict__ dL,
@@ -44,15 +44,26 @@ __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
-  // gather-sum of the returned expert input-gradients
+  // gather-sum of the returned expert input-gradients: all (slot, idx) pairs of the
+  // thread's 4 tokens first, then every 16-byte row load, so they are all in flight
+  constexpr int KM = KT > 0 ? KT : 8;
+  int sl[4][KM], ex[4][KM];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int t = t0 + tg * 4 + i;
-    if (t >= Tn || col >= d) continue;
-    for (int j = 0; j < k; ++j) {
-      const int s = slot[(size_t)t * k + j];
-      if (s < 0) continue;
-      const T* src = dXe + send_row(idx[(size_t)t * k + j], s, E, C, n, Cm) * d + col;
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+      const bool ok = t < Tn && j < k && col < d;
+      sl[i][j] = ok ? slot[(size_t)t * k + j] : -1;
+      ex[i][j] = ok ? idx[(size_t)t * k + j] : 0;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+      if (sl[i][j] < 0) continue;
+      const T* src = dXe + send_row(ex[i][j], sl[i][j], E, C, n, Cm) * d + col;
       float x[8];
       if constexpr (sizeof(T) == 2) {
         load16(src, x, (const __nv_bfloat16*)nullptr);
@@ -132,8 +143,14 @@ __global__ void __launch_bounds__(256) dwg_tiled_kernel(const T* __restrict__ X,
       }
       float l[8];
       const float* lp = dL + (size_t)t * E + e0;
+      if (ne == 8 && (E & 3) == 0) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(lp));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(lp + 4));
+        l[0] = a.x; l[1] = a.y; l[2] = a.z; l[3] = a.w; l[4] = b.x; l[5] = b.y; l[6] = b.z; l[7] = b.w;
+      } else {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) l[q] = q < ne ? __ldg(lp + q) : 0.f;
+        for (int q = 0; q < 8; ++q) l[q] = q < ne ? __ldg(lp + q) : 0.f;
+      }
 #pragma unroll
       for (int c = 0; c < 8; ++c)
 #pragma unroll
@@ -198,32 +215,34 @@ size_t dwg_scratch_floats(int T, int d, int E) {
   return (size_t)dwg_splits(T, d, E) * d * E;
 }
 
+template <typename T, int KT>
+static void launch_dx_t(const void* dXe, const int* idx, const int* slot, const float* dL,
+                        const float* Wg, int Tn, int k, int d, int E, int C, int n, int Cm, void* dX,
+                        cudaStream_t s) {
+  dim3 grid((d + kDxCols - 1) / kDxCols, (Tn + kDxTok - 1) / kDxTok);
+  const size_t smem = sizeof(float) * ((size_t)E * kDxCols + kDxTok * E);
+  static bool set = false;
+  if (!set) {
+    LINA_CUDA_CHECK(cudaFuncSetAttribute(dx_tiled_kernel<T, KT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    set = true;
+  }
+  dx_tiled_kernel<T, KT><<<grid, 256, smem, s>>>((const T*)dXe, idx, slot, dL, Wg, Tn, k, d, E, C, n, Cm,
+                                                (T*)dX);
+}
+
 void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* dL,
                const float* Wg, int T, int k, int d, int E, int C, int n, int Cm, void* dX,
                cudaStream_t s) {
   if (T <= 0) return;
-  dim3 grid((d + kDxCols - 1) / kDxCols, (T + kDxTok - 1) / kDxTok);
-  const size_t smem = sizeof(float) * ((size_t)E * kDxCols + kDxTok * E);
-  if (dtype == 0) {
-    static bool set = false;
-    if (!set) {
-      LINA_CUDA_CHECK(cudaFuncSetAttribute(dx_tiled_kernel<float>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-      set = true;
-    }
-    dx_tiled_kernel<float><<<grid, 256, smem, s>>>((const float*)dXe, idx, slot, dL, Wg, T, k, d, E,
-                                                   C, n, Cm, (float*)dX);
-  } else {
-    static bool set = false;
-    if (!set) {
-      LINA_CUDA_CHECK(cudaFuncSetAttribute(dx_tiled_kernel<__nv_bfloat16>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-      set = true;
-    }
-    dx_tiled_kernel<__nv_bfloat16><<<grid, 256, smem, s>>>((const __nv_bfloat16*)dXe, idx, slot, dL,
-                                                           Wg, T, k, d, E, C, n, Cm,
-                                                           (__nv_bfloat16*)dX);
-  }
+  auto go = [&](auto tag) {
+    using ET = decltype(tag);
+    if (k == 1) launch_dx_t<ET, 1>(dXe, idx, slot, dL, Wg, T, k, d, E, C, n, Cm, dX, s);
+    else if (k == 2) launch_dx_t<ET, 2>(dXe, idx, slot, dL, Wg, T, k, d, E, C, n, Cm, dX, s);
+    else launch_dx_t<ET, 0>(dXe, idx, slot, dL, Wg, T, k, d, E, C, n, Cm, dX, s);
+  };
+  if (dtype == 0) go(float{});
+  else go(__nv_bfloat16{});
   LINA_LAUNCH_CHECK();
 }
 
