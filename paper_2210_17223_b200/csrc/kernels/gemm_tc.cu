@@ -43,15 +43,18 @@ constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;  // 2 accumulators x BN
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the pair leader
 
-template <int CG> struct Geo {
+// MASK: the dgrad epilogue stages the whole 32 x 256 H box of each warp (4 boxes)
+// and gives up one pipeline stage for it.
+template <int CG, bool MASK = false> struct Geo {
   static constexpr int ROWS = 128 * CG;                  // tile rows per cluster
   static constexpr int A_BYTES = 128 * BK * 2;           // 16 KB per CTA
   static constexpr int B_ROWS = BN / CG;                 // B rows (N) staged per CTA
   static constexpr int B_BYTES = B_ROWS * BK * 2;        // 32 KB (CG=1) / 16 KB (CG=2)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = CG == 2 ? 6 : 4;
-  static constexpr int EPI_BYTES = 4 * 2 * 4096;           // 4 epilogue warps x 2 x (32 rows x 128 B)
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
+  static constexpr int STAGES = (CG == 2 ? 6 : 4) - (MASK ? 1 : 0);
+  static constexpr int EPI_BUFS = MASK ? 4 : 2;          // 32 rows x 128 B boxes per epilogue warp
+  static constexpr int EPI_BYTES = 4 * EPI_BUFS * 4096;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
                    TcParams p) {
-  using G = Geo<CG>;
+  using G = Geo<CG, EPI == kEpiMask>;
   constexpr int STAGES = G::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);
     }
-    for (int a = 0; a < 8; ++a) mbar_init(tempty + 3 + a, 1);  // epilogue aux-box barriers
+    for (int a = 0; a < 16; ++a) mbar_init(tempty + 3 + a, 1);  // epilogue aux-box barriers
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc<CG>(tmem_base_slot, TMEM_COLS);
@@ -440,15 +443,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // Each warp owns 32 rows: TMEM -> registers -> epi -> bf16 -> a 128B-swizzled
     // 32 x 64 smem box -> TMA store (rows past the segment end are clipped by the
     // tensor map).  Two boxes per warp alternate so the store of one overlaps the
-    // fill of the next.  The ReLU'-mask epilogue (dgrad) TMA-loads the matching
-    // 32 x 64 box of H into the same buffer one sub-tile ahead.
+    // fill of the next.  The ReLU'-mask epilogue (dgrad) instead owns four boxes:
+    // before waiting for the accumulator it TMA-loads the warp's whole 32 x 256 box
+    // of H (the loads overlap the tile's MMAs), then overwrites each box in place
+    // with the output and stores it.
     const int quarter = warp & 3;
-    uint8_t* my_epi = epi_smem + quarter * 8192;
-    uint64_t* abar = tempty + 2 + 1 + quarter * 2;   // 2 aux barriers per warp (after the TMEM slot)
-    uint32_t abph = 0;                               // bit b = phase of abar[b]
+    uint8_t* my_epi = epi_smem + quarter * G::EPI_BUFS * 4096;
+    uint64_t* abar = tempty + 2 + 1 + quarter * 4;   // 4 aux barriers per warp (after the TMEM slot)
+    uint32_t abph = 0;                               // phase of this tile's aux boxes
     int acc = 0;
     uint32_t aph = 0;
-    int sub = 0;  // sub-tile counter (buffer = sub & 1)
+    int sub = 0;  // sub-tile counter (buffer = sub & 1 without mask)
     auto box_of = [&](int t, int c0, int& x0, int& x1, int& x2) {
       int se, m0, n0;
       decode(t, se, m0, n0);
@@ -456,22 +461,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       x1 = m0 + 128 * rank + quarter * 32;
       x2 = WGRAD ? se : p.seg0 + se;
     };
-    if (EPI == kEpiMask && lane == 0 && cluster_id < total_tiles) {  // first aux box
-      int x0, x1, x2;
-      box_of(cluster_id, 0, x0, x1, x2);
-      mbar_expect_tx(&abar[0], 4096);
-      tma_load_3d<1>(my_epi, &tmX, &abar[0], x0, x1, x2);
-    }
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       int se, m0, n0;
       decode(t, se, m0, n0);
       const int nkb = kblocks_of(se);
+      if (EPI == kEpiMask && lane == 0) {
+        bulk_wait_all();  // the previous tile's stores have left the boxes
+        for (int j = 0; j < 4; ++j) {
+          int x0, x1, x2;
+          box_of(t, j * 64, x0, x1, x2);
+          mbar_expect_tx(&abar[j], 4096);
+          tma_load_3d<1>(my_epi + j * 4096, &tmX, &abar[j], x0, x1, x2);
+        }
+      }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 64, ++sub) {
-        const int b = sub & 1;
+        const int b = EPI == kEpiMask ? (c0 >> 6) : (sub & 1);
         uint8_t* buf = my_epi + b * 4096;
         const uint32_t rowaddr = smem_u32(buf) + lane * 128;
         uint32_t v[64];
@@ -484,8 +492,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int i = 0; i < 64; ++i) v[i] = 0u;
         }
         if (EPI == kEpiMask) {
-          mbar_wait(&abar[b], (abph >> b) & 1);
-          abph ^= 1u << b;
+          mbar_wait(&abar[b], abph);
         } else {
           if (lane == 0 && sub >= 2) bulk_wait_read1();  // the store that last used `buf` has read it
           __syncwarp();
@@ -528,22 +535,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           box_of(t, c0, x0, x1, x2);
           tma_store_3d(&tmD, buf, x0, x1, x2);
           bulk_commit();
-          if (EPI == kEpiMask) {  // prefetch the next sub-tile's H box into the other buffer
-            int nt = t, nc = c0 + 64;
-            if (nc == BN) {
-              nc = 0;
-              nt = t + num_clusters;
-            }
-            if (nt < total_tiles) {
-              bulk_wait_read1();  // the store that last used the other buffer has read it
-              box_of(nt, nc, x0, x1, x2);
-              mbar_expect_tx(&abar[b ^ 1], 4096);
-              tma_load_3d<1>(my_epi + (b ^ 1) * 4096, &tmX, &abar[b ^ 1], x0, x1, x2);
-            }
-          }
         }
         __syncwarp();
       }
+      abph ^= 1;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -621,13 +616,13 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   static bool attr_set = false;
   if (!attr_set) {
     LINA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Geo<CG>::SMEM_BYTES));
+                                         Geo<CG, EPI == kEpiMask>::SMEM_BYTES));
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = Geo<CG>::SMEM_BYTES;
+  cfg.dynamicSmemBytes = Geo<CG, EPI == kEpiMask>::SMEM_BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
