@@ -1,0 +1,108 @@
+"""Multi-rank parity of the expert-parallel layer (run under torch.distributed.run, one
+rank per GPU).  Every rank runs forward+backward through lina_comm (NCCL all-to-all
+micro-ops); rank 0 gathers every rank's outputs and gradients and compares them with
+the oracle, which simulates all ranks in one process.
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
+        --master-port 29511 tests/mp_parity.py --config C2 --tokens 512 --n-chunks 2
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import lina_inputs as li  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--tokens", type=int, default=512)
+    ap.add_argument("--n-chunks", type=int, default=2)
+    ap.add_argument("--experts", type=int, default=0)
+    ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--seed", type=int, default=77)
+    ap.add_argument("--check-chunks", type=int, default=0, help="also run with this n_chunks and compare bitwise")
+    a = ap.parse_args()
+    world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    import paper_2210_17223_b200 as lina
+
+    changes = {}
+    if a.experts:
+        changes["num_experts"] = a.experts
+    if a.k:
+        changes["k"] = a.k
+    cfg = li.with_tokens(li.CONFIGS[a.config], a.tokens, **changes)
+    E, El = cfg.num_experts, cfg.num_experts // world
+    uid = [lina.lina_get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = lina.Comm(world, rank, local, uid[0])
+    Wg, W1, W2 = li.layer_weights(cfg, a.seed, experts=range(rank * El, (rank + 1) * El))
+    X, dY = li.layer_tokens(cfg, a.seed, rank)
+    tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+
+    def run(n_chunks):
+        layer = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, cfg.capacity(),
+                              n_chunks, tdt, dev)
+        x = torch.from_numpy(X).to(tdt).to(dev)
+        wg = torch.from_numpy(Wg).to(dev)
+        w1 = torch.from_numpy(W1).to(tdt).to(dev)
+        w2 = torch.from_numpy(W2).to(tdt).to(dev)
+        y = layer.forward(x, wg, w1, w2, want_route=True)
+        dx, dwg, dw1, dw2 = layer.backward(torch.from_numpy(dY).to(tdt).to(dev), x, wg, w1, w2)
+        torch.cuda.synchronize()
+        comm.check()
+        return {"y": y.float().cpu().numpy(), "dx": dx.float().cpu().numpy(), "dwg": dwg.cpu().numpy(),
+                "dw1": dw1.float().cpu().numpy(), "dw2": dw2.float().cpu().numpy(),
+                "idx": layer.route_t["idx"].cpu().numpy(), "slot": layer.route_t["slot"].cpu().numpy()}
+
+    res = run(a.n_chunks)
+    gathered = [None] * world
+    dist.gather_object(res, gathered if rank == 0 else None, dst=0)
+    ok = True
+    if a.check_chunks:
+        res2 = run(a.check_chunks)
+        same = all(np.array_equal(res[k], res2[k]) for k in res)
+        flags = [None] * world
+        dist.gather_object(same, flags if rank == 0 else None, dst=0)
+        if rank == 0 and not all(flags):
+            print(f"chunk invariance FAILED: n={a.n_chunks} vs n={a.check_chunks}", flush=True)
+            ok = False
+    if rank == 0:
+        from oracle import moe
+        Wg_all, W1_all, W2_all = li.layer_weights(cfg, a.seed)
+        Xs = [li.layer_tokens(cfg, a.seed, r)[0] for r in range(world)]
+        dYs = [li.layer_tokens(cfg, a.seed, r)[1] for r in range(world)]
+        fw = moe.moe_forward(Xs, Wg_all, W1_all, W2_all, cfg.k, cfg.capacity(), cfg.dtype)
+        bw = moe.moe_backward(fw, Xs, dYs, Wg_all, W1_all, W2_all, cfg.k, cfg.dtype)
+        tol = 1e-5 if cfg.dtype == "f32" else 2e-2
+        dwg_sum = sum(g["dwg"] for g in gathered)   # the DP allreduce of R12
+        errs = {}
+        for r in range(world):
+            g = gathered[r]
+            ok &= np.array_equal(g["idx"], fw[r].idx) and np.array_equal(g["slot"], fw[r].slot)
+            errs[f"y{r}"] = moe.normwise_error(g["y"], fw[r].y)
+            errs[f"dx{r}"] = moe.normwise_error(g["dx"], bw.dXs[r])
+            errs[f"dw1_{r}"] = moe.normwise_error(g["dw1"], bw.dW1[r * El:(r + 1) * El])
+            errs[f"dw2_{r}"] = moe.normwise_error(g["dw2"], bw.dW2[r * El:(r + 1) * El])
+        errs["dwg"] = moe.normwise_error(dwg_sum, bw.dWg)
+        ok &= all(v <= tol for v in errs.values())
+        print("MP_PARITY", "OK" if ok else "FAIL", f"world={world} cfg={cfg.name} T={cfg.tokens_per_rank} "
+              f"n={a.n_chunks}", " ".join(f"{k}={v:.2e}" for k, v in errs.items()), flush=True)
+    flag = torch.tensor([1 if ok else 0], device=dev)
+    dist.broadcast(flag, 0)
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,39 @@
+"""Multi-GPU parity (needs >= 2 GPUs on one box; skipped otherwise): the NCCL
+all-to-all micro-op pipeline against the oracle simulating all ranks."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpu():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _run(nproc, *args, port=29611):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "mp_parity.py"), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "MP_PARITY OK" in out, out[-4000:]
+    return out
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("cfg,tokens,n,extra", [
+    ("C1", 256, 2, ["--experts", "4"]),
+    ("C2", 512, 2, ["--check-chunks", "1"]),
+    ("C3", 256, 3, []),
+])
+def test_two_ranks(cfg, tokens, n, extra):
+    _run(2, "--config", cfg, "--tokens", str(tokens), "--n-chunks", str(n), *extra)
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
+def test_four_ranks():
+    _run(4, "--config", "C2", "--tokens", "384", "--n-chunks", "4", "--check-chunks", "1", port=29612)
