@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--impl", default="lina", choices=["lina", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(li.CONFIGS))
     ap.add_argument("--n-chunks", type=int, default=0, help="0 = 1 at N=1, 4 otherwise")
+    ap.add_argument("--nccl-ctas", type=int, default=8, help="ncclConfig_t.maxCTAs per communicator (N>1)")
     ap.add_argument("--family", default="balanced", choices=["balanced", "grid"])
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -190,7 +191,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         uid = [lina.lina_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        comm = lina.Comm(world, rank, local, uid[0])
+        comm = lina.Comm(world, rank, local, uid[0], args.nccl_ctas)
     else:
         comm = lina.Comm(1, 0, local)
 

@@ -177,6 +177,8 @@ lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned 
       if (nccl_max_ctas > 0) cfg3.maxCTAs = nccl_max_ctas;
       LINA_NCCL_CHECK(ncclCommSplit(cm->ep_disp, 0, rank, &cm->dp, &cfg3));
       cm->sched = sched_create(cm);
+      // dispatch + combine all-to-all kernels may run beside the expert GEMM at once
+      tc_set_reserved_sms(nccl_max_ctas > 0 ? 2 * nccl_max_ctas : 16);
     }
     *out = cm;
     return LINA_OK;

@@ -72,15 +72,28 @@ __device__ __forceinline__ void store16(void* p, const float* in, __nv_bfloat16*
 }
 
 // ---------------------------------------------------------------- chunk geometry (R10)
-// Chunk c of n covers capacity slots [floor(c*C/n), floor((c+1)*C/n)).
+// The n all-to-all micro-ops split the capacity slots of every expert along the token
+// dimension ("partition the data in the token dimension"): chunk c covers slots
+// [c*Cm, min((c+1)*Cm, C)) with pitch Cm = ceil(C/n) rounded up to a multiple of the
+// tensor-core tile height (256, else 128, else 64 rows) whenever all n chunks stay
+// non-empty, so chunk boundaries do not cut expert GEMM tiles.  Results do not depend
+// on n (the oracle has no chunks); only the last chunk can be shorter.
+__host__ __device__ __forceinline__ int chunk_pitch(int C, int n) {
+  if (n <= 1) return C;
+  const int base = (C + n - 1) / n;
+  for (int a = 256; a >= 64; a >>= 1) {
+    const int cm = (base + a - 1) / a * a;
+    if ((long long)(n - 1) * cm < C) return cm;
+  }
+  return base;
+}
 __host__ __device__ __forceinline__ int chunk_begin(int c, int C, int n) {
-  return (int)(((long long)c * C) / n);
+  const long long b = (long long)c * chunk_pitch(C, n);
+  return b < C ? (int)b : C;
 }
-// The chunk holding slot s: largest c with chunk_begin(c) <= s.
-__host__ __device__ __forceinline__ int chunk_of(int s, int C, int n) {
-  return (int)((((long long)s + 1) * n + C - 1) / C) - 1;
-}
-__host__ __device__ __forceinline__ int chunk_rows_max(int C, int n) { return (C + n - 1) / n; }
+// The chunk holding slot s.
+__host__ __device__ __forceinline__ int chunk_of(int s, int C, int n) { return s / chunk_pitch(C, n); }
+__host__ __device__ __forceinline__ int chunk_rows_max(int C, int n) { return chunk_pitch(C, n); }
 // Row of (expert e, capacity slot s) in the chunk-major send layout [n][E][Cm][w].
 __host__ __device__ __forceinline__ size_t send_row(int e, int s, int E, int C, int n, int Cm) {
   const int c = chunk_of(s, C, n);

@@ -56,6 +56,8 @@ void launch_dwg(int dtype, const void* X, const float* dL, int T, int d, int E, 
 // CTAs per tensor-core tile (cta_group::2 pairs -> 256-row tiles).
 constexpr int kTcCtaGroup = 2;
 int tc_tile_rows();
+// SMs the persistent GEMM grid leaves free for concurrently running NCCL kernels.
+void tc_set_reserved_sms(int n);
 // mtp[c][i] = Σ_{i' < i} ceil(vcount[c*nseg + i'] / rows), i in [0, nseg]  (tcgen05 tile lists)
 void launch_mtile_prefix(const int* vcount, int n, int nseg, int rows, int* mtp, cudaStream_t s);
 bool tc_row_supported(const RowGemm& g);

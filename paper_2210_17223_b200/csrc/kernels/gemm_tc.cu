@@ -599,6 +599,11 @@ static CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, co
   return m;
 }
 
+static int g_reserved_sms = 0;  // SMs left to concurrent NCCL kernels (H2 in SURVEY.md)
+
+// SMs the persistent GEMM grid may occupy.  A persistent grid that takes every SM
+// would leave the all-to-all kernels nothing to run on (they would serialise after
+// it) or push a second wave of GEMM CTAs behind them.
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -606,7 +611,8 @@ static int num_sms() {
     LINA_CUDA_CHECK(cudaGetDevice(&dev));
     LINA_CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
   }
-  return n;
+  const int m = n - g_reserved_sms;
+  return m < 2 ? 2 : m;
 }
 
 template <int CG, bool WGRAD, bool B_MN, int EPI>
@@ -650,6 +656,8 @@ static void row_dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
 }
 
 }  // namespace tc
+
+void tc_set_reserved_sms(int n) { tc::g_reserved_sms = n < 0 ? 0 : n; }
 
 // Rows per tensor-core tile (the m-block granularity launch_mtile_prefix must use).
 int tc_tile_rows() { return 128 * kTcCtaGroup; }

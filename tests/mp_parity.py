@@ -70,7 +70,12 @@ def main():
     ok = True
     if a.check_chunks:
         res2 = run(a.check_chunks)
-        same = all(np.array_equal(res[k], res2[k]) for k in res)
+        # outputs and token gradients are bitwise chunk-invariant (each row's arithmetic is
+        # fixed); the weight gradients reduce over rows in chunk-dependent 64-row K blocks on
+        # the tensor cores, so they agree to accumulation rounding only
+        from oracle import moe as _m
+        same = all(np.array_equal(res[k], res2[k]) for k in ("y", "dx", "idx", "slot")) and \
+            all(_m.normwise_error(res2[k], res[k]) <= 1e-2 for k in ("dw1", "dw2", "dwg"))
         flags = [None] * world
         dist.gather_object(same, flags if rank == 0 else None, dst=0)
         if rank == 0 and not all(flags):
