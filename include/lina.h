@@ -220,9 +220,10 @@ lina_status lina_moe_infer_forward(lina_comm* comm, const lina_moe_desc* desc, c
                                    void* out, const lina_placement* placement,
                                    int32_t max_per_device, lina_placement* plan_out,
                                    void* workspace, size_t workspace_bytes, lina_stream stream);
-/* Workspace for lina_moe_infer_forward. */
+/* Workspace for lina_moe_infer_forward with at most max_per_device hosted experts per
+ * device (sized for the worst case: all of a source's tokens routed to one replica). */
 lina_status lina_moe_infer_workspace_size(const lina_comm* comm, const lina_moe_desc* desc,
-                                          size_t* workspace_bytes);
+                                          int32_t max_per_device, size_t* workspace_bytes);
 
 /* ------------------------------------------------------------------------ */
 /* Micro-op allreduce scheduler (§4; §6.1)             */

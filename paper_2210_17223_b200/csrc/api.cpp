@@ -45,7 +45,7 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
                    const float* gate_w, const void* w1_all, const void* w2_all, void* out,
                    const lina_placement* placement, int mpd, lina_placement* plan_out, void* ws,
                    size_t ws_bytes, cudaStream_t s);
-size_t infer_workspace_bytes(const lina_moe_desc& desc, int world);
+size_t infer_workspace_bytes(const lina_moe_desc& desc, int world, int mpd);
 }  // namespace lina
 
 using namespace lina;
@@ -198,6 +198,8 @@ lina_status lina_comm_destroy(lina_comm* cm) {
     if (cm->hi) cudaStreamDestroy(cm->hi);
     if (cm->hi2) cudaStreamDestroy(cm->hi2);
     if (cm->lo) cudaStreamDestroy(cm->lo);
+    for (auto e : cm->prof_pool) cudaEventDestroy(e);
+    if (cm->pinned) cudaFreeHost(cm->pinned);
     delete cm;
     return LINA_OK;
   });
@@ -350,11 +352,12 @@ lina_status lina_moe_backward(lina_comm* cm, const lina_moe_desc* desc, const vo
 }
 
 lina_status lina_moe_infer_workspace_size(const lina_comm* cm, const lina_moe_desc* desc,
-                                          size_t* workspace_bytes) {
+                                          int32_t max_per_device, size_t* workspace_bytes) {
   return guarded([&] {
     if (!cm) throw ArgError{"comm is NULL"};
     validate_desc(desc, cm->world, false);
-    if (workspace_bytes) *workspace_bytes = infer_workspace_bytes(*desc, cm->world);
+    if (max_per_device < 1) throw ArgError{"max_per_device < 1"};
+    if (workspace_bytes) *workspace_bytes = infer_workspace_bytes(*desc, cm->world, max_per_device);
     return LINA_OK;
   });
 }
@@ -380,13 +383,22 @@ lina_status lina_moe_infer_forward(lina_comm* cm, const lina_moe_desc* desc, con
     if (placement) {
       if (placement->num_experts != desc->num_experts) v.push_back("placement->num_experts != E");
       if (placement->num_devices != cm->world) v.push_back("placement->num_devices != world");
+      if (placement->max_per_device < 1) v.push_back("placement->max_per_device < 1");
+      if (placement->max_replicas < 1) v.push_back("placement->max_replicas < 1");
       need(v, placement->replicas, "placement->replicas");
       need(v, placement->replica_device, "placement->replica_device");
       need(v, placement->hosted, "placement->hosted");
     }
+    if (plan_out) {
+      need(v, plan_out->replicas, "plan_out->replicas");
+      need(v, plan_out->replica_device, "plan_out->replica_device");
+      need(v, plan_out->hosted, "plan_out->hosted");
+      if (plan_out->max_replicas < cm->world) v.push_back("plan_out->max_replicas < world");
+    }
     raise_if(v, "lina_moe_infer_forward");
-    if (workspace_bytes < infer_workspace_bytes(*desc, cm->world))
-      throw StatusError{LINA_ERR_WORKSPACE, "workspace too small"};
+    const int mpd = placement ? placement->max_per_device : max_per_device;
+    if (workspace_bytes < infer_workspace_bytes(*desc, cm->world, mpd))
+      throw StatusError{LINA_ERR_WORKSPACE, "workspace_bytes < lina_moe_infer_workspace_size"};
     LINA_CUDA_CHECK(cudaSetDevice(cm->device));
     infer_forward(cm, *desc, tokens, gate_w, w1_all, w2_all, out, placement, max_per_device,
                   plan_out, workspace, workspace_bytes, (cudaStream_t)stream);

@@ -1,19 +1,331 @@
-// S10 inference path with popularity-driven replication (filled in below).
+// S10: inference forward with popularity-driven expert replication.
+//
+// PAPER.md §5.2: replica counts n_e = N·Σ_t P(e)/N_t (Eq. 1), first-fit-
+// decreasing packing; §6.2: the plan carries "how many tokens
+// each replica should handle", the all-to-all uses an unequal split with no
+// transfer to peers that get no tokens, hosted experts run on their device
+// and the second all-to-all follows them.
+//
+// B200 design: every rank holds all E experts in HBM (the paper's
+// host-DRAM copy, moved on-device), so a placement change moves no weights.
+// The plan is computed identically on every rank from the allgathered per-source
+// counts (no device-0 scheduler, no send/broadcast control plane); the default
+// popularity is this batch's histogram (the paper's "w/o estimation" variant, P:905,
+// reading R17).  One host synchronisation per call reads the counts (the unequal
+// all-to-all needs host-visible sizes; H9).  Per call:
+//   s : gate+softmax+top-k -> dropless slots (C = T) -> per-expert counts
+//   s : allgather counts [P][E] -> D2H -> host plan (Eq. 1 + FFD, replica splits,
+//       send/recv sizes) -> H2D of the routing tables
+//   s : replica-routed permute -> grouped ncclSend/ncclRecv -> grouped expert GEMMs
+//       over the hosted experts (tcgen05, weight index per segment) -> grouped
+//       send/recv back -> row-indexed combine.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
 #include "internal.h"
+#include "kernels.h"
 #include "layer.h"
 
 namespace lina {
 
-size_t infer_workspace_bytes(const lina_moe_desc& desc, int world) {
-  (void)desc;
-  (void)world;
-  return 256;
+static size_t al(size_t x) { return (x + 255) / 256 * 256; }
+
+struct InferPlan {
+  int T, d, f, E, k, P, mpd, dt;
+  size_t Cmax;
+  size_t o_probs, o_idx, o_gate, o_slot, o_counts, o_kept, o_tokof, o_route, o_all, o_tab, o_vc,
+      o_mtp, o_segx, o_arow, o_send, o_recv, o_h, o_o, o_back, total;
+  size_t tab_ints() const { return (size_t)E + (size_t)E * P + (size_t)P * E + E; }
+};
+
+static InferPlan infer_plan(const lina_moe_desc& dsc, int P, int mpd) {
+  InferPlan q{};
+  q.T = dsc.num_tokens;
+  q.d = dsc.d_model;
+  q.f = dsc.d_ffn;
+  q.E = dsc.num_experts;
+  q.k = dsc.k;
+  q.P = P;
+  q.mpd = mpd;
+  q.dt = dsc.dtype == LINA_BF16 ? 2 : 4;
+  const size_t Tk = (size_t)q.T * q.k;
+  q.Cmax = std::max<size_t>(128, (Tk + 127) / 128 * 128);  // worst case: a source's tokens to one expert
+  const size_t segs = (size_t)P * mpd;
+  size_t o = 0;
+  auto take = [&](size_t b) {
+    size_t at = o;
+    o = al(o + b);
+    return at;
+  };
+  q.o_probs = take(4 * (size_t)q.T * q.E);
+  q.o_idx = take(4 * Tk);
+  q.o_gate = take(4 * Tk);
+  q.o_slot = take(4 * Tk);
+  q.o_counts = take(4 * (size_t)q.E);
+  q.o_kept = take(4 * (size_t)q.E);
+  q.o_tokof = take(4 * (size_t)q.E * std::max(q.T, 1));
+  q.o_route = take(4 * route_scratch_ints(q.T, q.k, q.E));
+  q.o_all = take(4 * (size_t)P * q.E);
+  q.o_tab = take(4 * q.tab_ints());
+  q.o_vc = take(4 * segs);
+  q.o_mtp = take(4 * (segs + 1));
+  q.o_segx = take(4 * (size_t)mpd);
+  q.o_arow = take(4 * Tk);
+  q.o_send = take(Tk * q.d * q.dt);
+  q.o_recv = take(segs * q.Cmax * q.d * q.dt);
+  q.o_h = take(segs * q.Cmax * q.f * q.dt);
+  q.o_o = take(segs * q.Cmax * q.d * q.dt);
+  q.o_back = take(Tk * q.d * q.dt);
+  q.total = o;
+  return q;
 }
 
-void infer_forward(lina_comm*, const lina_moe_desc&, const void*, const float*, const void*,
-                   const void*, void*, const lina_placement*, int, lina_placement*, void*, size_t,
-                   cudaStream_t) {
-  throw StatusError{LINA_ERR_UNSUPPORTED, "lina_moe_infer_forward: not built yet"};
+size_t infer_workspace_bytes(const lina_moe_desc& desc, int world, int mpd) {
+  return infer_plan(desc, world, std::max(1, mpd)).total;
+}
+
+static int* pinned(lina_comm* cm, size_t ints) {
+  if (cm->pinned_bytes < ints * 4) {
+    if (cm->pinned) cudaFreeHost(cm->pinned);
+    cm->pinned = nullptr;
+    cm->pinned_bytes = 0;
+    LINA_CUDA_CHECK(cudaHostAlloc((void**)&cm->pinned, ints * 4, cudaHostAllocDefault));
+    cm->pinned_bytes = ints * 4;
+  }
+  return cm->pinned;
+}
+
+void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens, const float* gate_w,
+                   const void* w1_all, const void* w2_all, void* out, const lina_placement* placement,
+                   int mpd_arg, lina_placement* plan_out, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int P = cm->world, rank = cm->rank;
+  const int mpd = placement ? placement->max_per_device : mpd_arg;
+  InferPlan q = infer_plan(desc, P, mpd);
+  if (ws_bytes < q.total)
+    throw StatusError{LINA_ERR_WORKSPACE, "workspace_bytes " + std::to_string(ws_bytes) + " < required " +
+                                              std::to_string(q.total)};
+  char* w = (char*)ws;
+  float* probs = (float*)(w + q.o_probs);
+  int* idx = (int*)(w + q.o_idx);
+  float* gate = (float*)(w + q.o_gate);
+  int* slot = (int*)(w + q.o_slot);
+  int* counts = (int*)(w + q.o_counts);
+  int* kept = (int*)(w + q.o_kept);
+  int* tokof = (int*)(w + q.o_tokof);
+  int* allc = (int*)(w + q.o_all);
+  int* tab = (int*)(w + q.o_tab);
+  int* vc = (int*)(w + q.o_vc);
+  int* mtp = (int*)(w + q.o_mtp);
+  int* segx = (int*)(w + q.o_segx);
+  int* arow = (int*)(w + q.o_arow);
+  char* send = w + q.o_send;
+  char* recv = w + q.o_recv;
+  char* hbuf = w + q.o_h;
+  char* obuf = w + q.o_o;
+  char* back = w + q.o_back;
+  const int T = q.T, E = q.E, k = q.k, d = q.d, f = q.f, dt = q.dt;
+  const int dtype = desc.dtype == LINA_BF16 ? 1 : 0;
+  const ncclDataType_t ndt = dtype ? ncclBfloat16 : ncclFloat32;
+
+  // ---- gate, dropless slots, counts (S1, S2 with C = T)
+  launch_gate_topk(dtype, tokens, gate_w, T, d, E, k, 1, probs, idx, gate, s);
+  launch_route(idx, T, k, E, std::max(T, 1), (int*)(w + q.o_route), slot, counts, kept, tokof, s);
+  if (P > 1) {
+    LINA_NCCL_CHECK(ncclAllGather(counts, allc, (size_t)E, ncclInt32, cm->ep_disp, s));
+  } else {
+    LINA_CUDA_CHECK(cudaMemcpyAsync(allc, counts, 4 * (size_t)E, cudaMemcpyDeviceToDevice, s));
+  }
+  const size_t ctrl_ints = (size_t)P * E + q.tab_ints() + (size_t)P * mpd + (P * mpd + 1) + mpd;
+  int* host = pinned(cm, ctrl_ints);
+  LINA_CUDA_CHECK(cudaMemcpyAsync(host, allc, 4 * (size_t)P * E, cudaMemcpyDeviceToHost, s));
+  LINA_CUDA_CHECK(cudaStreamSynchronize(s));
+  std::vector<int> cnt(host, host + (size_t)P * E);  // cnt[src*E + e]
+
+  // ---- the plan (identical on every rank)
+  std::vector<int> r(E), rdev((size_t)E * P, -1), hosted((size_t)P * mpd, -1);
+  if (placement) {
+    const int mr = placement->max_replicas;
+    for (int e = 0; e < E; ++e) {
+      r[e] = placement->replicas[e];
+      for (int i = 0; i < r[e]; ++i) rdev[(size_t)e * P + i] = placement->replica_device[(size_t)e * mr + i];
+    }
+    for (int dv = 0; dv < P; ++dv)
+      for (int i = 0; i < mpd; ++i) hosted[(size_t)dv * mpd + i] = placement->hosted[(size_t)dv * mpd + i];
+  } else {
+    std::vector<double> pop(E, 0.0);
+    double tot = 0.0;
+    for (int src = 0; src < P; ++src)
+      for (int e = 0; e < E; ++e) tot += cnt[(size_t)src * E + e];
+    for (int e = 0; e < E; ++e) {
+      double c = 0.0;
+      for (int src = 0; src < P; ++src) c += cnt[(size_t)src * E + e];
+      pop[e] = tot > 0 ? c / tot : 1.0 / E;
+    }
+    std::vector<int32_t> rr(E), rd((size_t)E * P), hs((size_t)P * mpd);
+    lina_placement pl{E, P, mpd, P, rr.data(), rd.data(), hs.data()};
+    std::string err;
+    lina_status st = placement_compute(pop.data(), E, P, mpd, &pl, &err);
+    if (st != LINA_OK) throw StatusError{st, err};
+    for (int e = 0; e < E; ++e) {
+      r[e] = rr[e];
+      for (int i = 0; i < P; ++i) rdev[(size_t)e * P + i] = rd[(size_t)e * P + i];
+    }
+    hosted.assign(hs.begin(), hs.end());
+  }
+  // replica of e on device dv (-1 if none)
+  auto replica_on = [&](int e, int dv) {
+    for (int i = 0; i < r[e]; ++i)
+      if (rdev[(size_t)e * P + i] == dv) return i;
+    return -1;
+  };
+  std::vector<int> split(P);
+  auto tokens_to = [&](int src, int e, int dv) {  // tokens src sends to dv for expert e (R14)
+    const int i = replica_on(e, dv);
+    if (i < 0) return 0;
+    replica_split(cnt[(size_t)src * E + e], r[e], src, split.data());
+    return split[i];
+  };
+  std::vector<int> nsend((size_t)P * E, 0), soff((size_t)P * E, 0), nrecv((size_t)P * mpd, 0);
+  int off = 0;
+  for (int dv = 0; dv < P; ++dv)
+    for (int i = 0; i < mpd; ++i) {
+      const int e = hosted[(size_t)dv * mpd + i];
+      if (e < 0) continue;
+      soff[(size_t)dv * E + e] = off;
+      nsend[(size_t)dv * E + e] = tokens_to(rank, e, dv);
+      off += nsend[(size_t)dv * E + e];
+    }
+  int maxrows = 0;
+  for (int src = 0; src < P; ++src)
+    for (int h = 0; h < mpd; ++h) {
+      const int e = hosted[(size_t)rank * mpd + h];
+      const int n = e < 0 ? 0 : tokens_to(src, e, rank);
+      nrecv[(size_t)src * mpd + h] = n;
+      maxrows = std::max(maxrows, n);
+    }
+  const int Cm = std::max(128, (maxrows + 127) / 128 * 128);
+  if ((size_t)Cm > q.Cmax) throw StatusError{LINA_ERR_WORKSPACE, "receive segment exceeds workspace"};
+
+  // ---- routing tables to the device (one H2D copy)
+  int* h = host;
+  int* h_tab = h;
+  for (int e = 0; e < E; ++e) h_tab[e] = r[e];
+  for (size_t i = 0; i < (size_t)E * P; ++i) h_tab[E + i] = rdev[i];
+  for (size_t i = 0; i < (size_t)P * E; ++i) h_tab[E + (size_t)E * P + i] = soff[i];
+  for (int e = 0; e < E; ++e) h_tab[E + 2 * (size_t)E * P + e] = cnt[(size_t)rank * E + e];
+  int* h_vc = h_tab + q.tab_ints();
+  int* h_mtp = h_vc + (size_t)P * mpd;
+  int* h_segx = h_mtp + (P * mpd + 1);
+  const int rows = tc_tile_rows();
+  int run = 0;
+  for (int i = 0; i < P * mpd; ++i) {
+    h_vc[i] = nrecv[i];
+    h_mtp[i] = run;
+    run += (nrecv[i] + rows - 1) / rows;
+  }
+  h_mtp[P * mpd] = run;
+  for (int i = 0; i < mpd; ++i) h_segx[i] = std::max(0, hosted[(size_t)rank * mpd + i]);
+  // tab, vc, mtp, segx are adjacent in the workspace in the same order
+  LINA_CUDA_CHECK(cudaMemcpyAsync(tab, h_tab, 4 * q.tab_ints(), cudaMemcpyHostToDevice, s));
+  LINA_CUDA_CHECK(cudaMemcpyAsync(vc, h_vc, 4 * (size_t)P * mpd, cudaMemcpyHostToDevice, s));
+  LINA_CUDA_CHECK(cudaMemcpyAsync(mtp, h_mtp, 4 * (size_t)(P * mpd + 1), cudaMemcpyHostToDevice, s));
+  LINA_CUDA_CHECK(cudaMemcpyAsync(segx, h_segx, 4 * (size_t)mpd, cudaMemcpyHostToDevice, s));
+
+  // ---- replica-routed permute and the unequal-split all-to-all
+  launch_infer_permute(dtype, tokens, idx, slot, tab, T, k, d, E, P, rank, send, arow, s);
+  auto seg_ptr = [&](char* base, int src, int hh, int width) {
+    return base + ((size_t)(src * mpd + hh) * Cm) * width * dt;
+  };
+  if (P > 1) {
+    LINA_NCCL_CHECK(ncclGroupStart());
+    for (int dv = 0; dv < P; ++dv)
+      for (int i = 0; i < mpd; ++i) {
+        const int e = hosted[(size_t)dv * mpd + i];
+        if (e < 0 || nsend[(size_t)dv * E + e] == 0) continue;
+        LINA_NCCL_CHECK(ncclSend(send + (size_t)soff[(size_t)dv * E + e] * d * dt,
+                                 (size_t)nsend[(size_t)dv * E + e] * d, ndt, dv, cm->ep_disp, s));
+      }
+    for (int src = 0; src < P; ++src)
+      for (int hh = 0; hh < mpd; ++hh) {
+        const int n = nrecv[(size_t)src * mpd + hh];
+        if (n) LINA_NCCL_CHECK(ncclRecv(seg_ptr(recv, src, hh, d), (size_t)n * d, ndt, src, cm->ep_disp, s));
+      }
+    LINA_NCCL_CHECK(ncclGroupEnd());
+  } else {
+    for (int hh = 0; hh < mpd; ++hh) {
+      const int e = hosted[hh];
+      const int n = nrecv[hh];
+      if (e < 0 || n == 0) continue;
+      LINA_CUDA_CHECK(cudaMemcpyAsync(seg_ptr(recv, 0, hh, d), send + (size_t)soff[e] * d * dt,
+                                      (size_t)n * d * dt, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+
+  // ---- expert FFN over the hosted experts (S5; one launch per GEMM for every segment)
+  RowGemm g1{};
+  g1.A = recv;
+  g1.B = w1_all;
+  g1.D = hbuf;
+  g1.vcount = vc;
+  g1.mtp = mtp;
+  g1.seg0 = 0;
+  g1.nseg = P * mpd;
+  g1.El = mpd;
+  g1.Cm = Cm;
+  g1.N = f;
+  g1.K = d;
+  g1.seg_expert = segx;
+  g1.B_experts = E;
+  RowGemm g2 = g1;
+  g2.A = hbuf;
+  g2.B = w2_all;
+  g2.D = obuf;
+  g2.N = d;
+  g2.K = f;
+  prof_begin(cm, s);
+  launch_expert_row_gemm(dtype, g1, true, kEpiRelu, s);
+  launch_expert_row_gemm(dtype, g2, true, kEpiNone, s);
+  prof_end(cm, s, 2);
+
+  // ---- second all-to-all (expert outputs back to their sources) and combine
+  if (P > 1) {
+    LINA_NCCL_CHECK(ncclGroupStart());
+    for (int src = 0; src < P; ++src)
+      for (int hh = 0; hh < mpd; ++hh) {
+        const int n = nrecv[(size_t)src * mpd + hh];
+        if (n) LINA_NCCL_CHECK(ncclSend(seg_ptr(obuf, src, hh, d), (size_t)n * d, ndt, src, cm->ep_comb, s));
+      }
+    for (int dv = 0; dv < P; ++dv)
+      for (int i = 0; i < mpd; ++i) {
+        const int e = hosted[(size_t)dv * mpd + i];
+        if (e < 0 || nsend[(size_t)dv * E + e] == 0) continue;
+        LINA_NCCL_CHECK(ncclRecv(back + (size_t)soff[(size_t)dv * E + e] * d * dt,
+                                 (size_t)nsend[(size_t)dv * E + e] * d, ndt, dv, cm->ep_comb, s));
+      }
+    LINA_NCCL_CHECK(ncclGroupEnd());
+  } else {
+    for (int hh = 0; hh < mpd; ++hh) {
+      const int e = hosted[hh];
+      const int n = nrecv[hh];
+      if (e < 0 || n == 0) continue;
+      LINA_CUDA_CHECK(cudaMemcpyAsync(back + (size_t)soff[e] * d * dt, seg_ptr(obuf, 0, hh, d),
+                                      (size_t)n * d * dt, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  launch_combine_rows(dtype, back, arow, gate, T, k, d, out, s);
+
+  if (plan_out) {
+    plan_out->num_experts = E;
+    plan_out->num_devices = P;
+    plan_out->max_per_device = mpd;
+    for (int e = 0; e < E; ++e) {
+      plan_out->replicas[e] = r[e];
+      for (int i = 0; i < plan_out->max_replicas; ++i)
+        plan_out->replica_device[(size_t)e * plan_out->max_replicas + i] = i < P ? rdev[(size_t)e * P + i] : -1;
+    }
+    for (size_t i = 0; i < (size_t)P * mpd; ++i) plan_out->hosted[i] = hosted[i];
+  }
 }
 
 }  // namespace lina

@@ -72,6 +72,9 @@ struct lina_comm {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_gemm;  // recorded (start, end) pairs
   std::vector<cudaEvent_t> prof_pool;                          // free timing events
   int64_t prof_gemm_launches = 0;
+  // pinned host scratch for the inference control plane (counts D2H, tables H2D)
+  int* pinned = nullptr;
+  size_t pinned_bytes = 0;
 };
 
 namespace lina {

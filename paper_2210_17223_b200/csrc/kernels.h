@@ -17,6 +17,8 @@ struct RowGemm {
   const int* vcount;   // [nseg_total] valid rows per segment
   const int* mtp;      // [nseg+1] prefix of valid 128-row blocks over this launch's segments
   int seg0, nseg, El, Cm, N, K;
+  const int* seg_expert = nullptr;  // [El] weight index of local slot (seg % El); NULL = identity
+  int B_experts = 0;                // expert matrices in B (0 = El)
 };
 
 // Weight-gradient GEMM: D[El][M][N] = Σ_{c,s} Σ_{r < v} A[seg][r][:]ᵀ B[seg][r][:].
@@ -64,6 +66,13 @@ bool tc_row_supported(const RowGemm& g);
 bool tc_wgrad_supported(const WGrad& g);
 void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s);
 void launch_wgrad_tc(const WGrad& g, cudaStream_t s);
+
+// inference replica routing (infer_route.cu); tab = r[E] | rdev[E][N] | send_off[N][E] | cnt[E]
+void launch_infer_permute(int dtype, const void* X, const int* idx, const int* slot, const int* tab,
+                          int T, int k, int d, int E, int N, int s, void* Send, int* arow,
+                          cudaStream_t st);
+void launch_combine_rows(int dtype, const void* Back, const int* arow, const float* gate, int T, int k,
+                         int d, void* Y, cudaStream_t st);
 
 void launch_row_gemm_simt(int dtype, const RowGemm& p, bool b_kmajor, int epi, cudaStream_t s);
 void launch_wgrad_simt(int dtype, const WGrad& p, cudaStream_t s);

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) row_gemm_kernel(RowGemm p) {
   const int v = p.vcount[seg];
   if (m0 >= v) return;
   const int n0 = blockIdx.y * BN;
-  const int el = gi % p.El;
+  const int el = p.seg_expert ? p.seg_expert[gi % p.El] : gi % p.El;
   const T* A = (const T*)p.A + (size_t)seg * p.Cm * p.K;
   const T* B = (const T*)p.B + (size_t)el * p.N * p.K;
   const int ty = tid / 16, tx = tid % 16;

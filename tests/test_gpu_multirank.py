@@ -37,3 +37,23 @@ def test_two_ranks(cfg, tokens, n, extra):
 @pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
 def test_four_ranks():
     _run(4, "--config", "C2", "--tokens", "384", "--n-chunks", "4", "--check-chunks", "1", port=29612)
+
+
+def _run_infer(nproc, *args, port=29621):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "mp_infer.py"), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "MP_INFER OK" in out, out[-4000:]
+    return out
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("zipf,experts", [(1.0, 8), (1.2, 32), (0.5, 32)])
+def test_infer_replication_two_ranks(zipf, experts):
+    _run_infer(2, "--tokens", "512", "--zipf", str(zipf), "--experts", str(experts))
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
+def test_infer_replication_four_ranks():
+    _run_infer(4, "--tokens", "512", "--zipf", "1.0", "--experts", "32", port=29622)
