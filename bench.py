@@ -261,6 +261,51 @@ def main():
         total_ms_max, kept_total = total_ms, float(kept_local)
     value = world * T * args.steps / (total_ms_max / 1e3)
 
+    # ---------------- exposed communication (N>1): compute-only and all-to-all-only passes
+    a2a = None
+    if world > 1:
+        def timed(flags):
+            lina.lina_profile_enable(comm, flags)
+            barrier()
+            torch.cuda.synchronize()
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)]
+            for i in range(args.steps):
+                flush.zero_()
+                ev[i][0].record(stream)
+                step(x, dy)
+                ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            lina.lina_profile_enable(comm, 0)
+            lina.lina_profile_read(comm)
+            t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            return float(t[0])
+        t_comp = timed(2)
+        t_comm = timed(4)
+        t_step = total_ms_max / args.steps
+        exposed = max(0.0, t_step - t_comp)
+        from paper_2210_17223_b200.lina import LINA_BF16  # noqa: F401
+        elt = 2 if tdt == torch.bfloat16 else 4
+        import math
+        cm_rows = C if n_chunks == 1 else None
+        if cm_rows is None:  # chunk pitch (R10)
+            base = math.ceil(C / n_chunks)
+            cm_rows = base
+            for al in (256, 128, 64):
+                cmv = math.ceil(base / al) * al
+                if (n_chunks - 1) * cmv < C:
+                    cm_rows = cmv
+                    break
+        bytes_rank = 4 * n_chunks * E * cm_rows * d * elt   # 4 all-to-alls of the padded send buffer
+        algbw = bytes_rank / (t_comm / 1e3) / 1e9
+        a2a = {"ms_per_step_isolated": t_comm, "ms_per_step_compute_only": t_comp,
+               "exposed_ms_per_step": exposed,
+               "hidden_frac": (1.0 - exposed / t_comm) if t_comm > 0 else None,
+               "algbw_GBps": algbw, "busbw_GBps": algbw * (world - 1) / world,
+               "bytes_per_rank_per_step": bytes_rank, "nccl_max_ctas": args.nccl_ctas}
+
     # ---------------- end to end through the public API, host buffers (pinned), copies timed
     e2e = None
     if not args.no_e2e:
@@ -327,6 +372,7 @@ def main():
                        "l2": "flushed between timed steps (256 MB write, outside the step events)",
                        "kept_assignments": int(kept_total)},
             "roofline": roof,
+            "a2a": a2a,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(prof["kernel_launches"]),

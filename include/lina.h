@@ -255,8 +255,12 @@ typedef struct {
   int64_t gemm_phases;     /* number of timed phases summed into gemm_ms                  */
 } lina_profile;
 
-/* on != 0: record timing events around the expert-GEMM phases of every forward /
- * backward on this communicator (cheap; off by default). */
+/* Bit flags: 1 = record timing events around the expert-GEMM phases of every forward /
+ * backward on this communicator (cheap; off by default).  For the exposed-
+ * communication measurement only (results are NOT valid while set, world > 1):
+ * 2 = skip the all-to-all collectives (compute-only timing), 4 = run only the
+ * all-to-all collectives of the pass (communication-only timing).  2 and 4 are
+ * exclusive; 0 restores normal operation. */
 lina_status lina_profile_enable(lina_comm* comm, int on);
 /* Synchronises the recorded events, fills *out, and resets the counters. */
 lina_status lina_profile_read(lina_comm* comm, lina_profile* out);

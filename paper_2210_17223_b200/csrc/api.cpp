@@ -442,7 +442,10 @@ lina_status lina_allreduce_wait(lina_comm* cm, lina_stream stream) {
 lina_status lina_profile_enable(lina_comm* cm, int on) {
   return guarded([&] {
     if (!cm) throw ArgError{"comm is NULL"};
-    cm->prof = on != 0;
+    if (on < 0 || on > 7 || ((on & 2) && (on & 4)))
+      throw ArgError{"profile flags: 1 timing | 2 skip collectives | 4 collectives only (2 and 4 exclusive)"};
+    cm->prof = (on & 1) != 0;
+    cm->flags = on;
     return LINA_OK;
   });
 }

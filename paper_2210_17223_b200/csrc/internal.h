@@ -69,6 +69,7 @@ struct lina_comm {
   lina::Scheduler* sched = nullptr;
   // profiling (lina_profile_enable / lina_profile_read)
   bool prof = false;
+  int flags = 0;  // lina_profile_enable bits: 1 timing events, 2 skip collectives, 4 collectives only
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_gemm;  // recorded (start, end) pairs
   std::vector<cudaEvent_t> prof_pool;                          // free timing events
   int64_t prof_gemm_launches = 0;

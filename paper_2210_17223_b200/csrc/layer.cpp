@@ -167,6 +167,24 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   Ptrs q = carve(p, saved, ws);
   const int dtype = p.bf16 ? 1 : 0;
   const bool override_r = route && route->override_routing;
+  // instrumentation (lina_profile_enable): 2 = skip collectives, 4 = collectives only
+  const bool do_comm = !(cm->flags & 2), do_compute = !(cm->flags & 4);
+  if (!do_compute && p.P > 1) {
+    cudaEvent_t* ev = cm->ev.data();
+    LINA_CUDA_CHECK(cudaEventRecord(ev[0], s));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi, ev[0], 0));
+    LINA_NCCL_CHECK(ncclAlltoAll(q.kept, q.recv_kept, (size_t)p.El, ncclInt32, cm->ep_disp, cm->hi));
+    for (int c = 0; c < p.n; ++c) a2a_send_to_recv(p, q.D, q.R, p.d, c, cm->ep_disp, cm->hi);
+    LINA_CUDA_CHECK(cudaEventRecord(ev[1], cm->hi));
+    for (int c = 0; c < p.n; ++c) {
+      LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi2, ev[0], 0));
+      a2a_recv_to_send(p, q.O, q.Cb, p.d, c, cm->ep_comb, cm->hi2);
+    }
+    LINA_CUDA_CHECK(cudaEventRecord(ev[2], cm->hi2));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ev[1], 0));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2], 0));
+    return;
+  }
   if (override_r) {
     LINA_CUDA_CHECK(cudaMemcpyAsync(q.idx, route->idx, 4 * (size_t)p.T * p.k,
                                     cudaMemcpyDeviceToDevice, s));
@@ -214,10 +232,18 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   cudaEvent_t* e_gemm = ev + 3 + n;
   LINA_CUDA_CHECK(cudaEventRecord(e_perm, s));
   LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi, e_perm, 0));
-  LINA_NCCL_CHECK(ncclAlltoAll(q.kept, q.recv_kept, (size_t)p.El, ncclInt32, cm->ep_disp, cm->hi));
+  if (do_comm) {
+    LINA_NCCL_CHECK(ncclAlltoAll(q.kept, q.recv_kept, (size_t)p.El, ncclInt32, cm->ep_disp, cm->hi));
+  } else {  // compute-only timing: pretend every source sent its full kept counts
+    LINA_CUDA_CHECK(cudaMemcpyAsync(q.recv_kept, q.kept, 4 * (size_t)p.El, cudaMemcpyDeviceToDevice,
+                                    cm->hi));
+    for (int r = 1; r < p.P; ++r)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(q.recv_kept + (size_t)r * p.El, q.kept, 4 * (size_t)p.El,
+                                      cudaMemcpyDeviceToDevice, cm->hi));
+  }
   LINA_CUDA_CHECK(cudaEventRecord(e_cnt, cm->hi));
   for (int c = 0; c < n; ++c) {
-    a2a_send_to_recv(p, q.D, q.R, p.d, c, cm->ep_disp, cm->hi);
+    if (do_comm) a2a_send_to_recv(p, q.D, q.R, p.d, c, cm->ep_disp, cm->hi);
     LINA_CUDA_CHECK(cudaEventRecord(e_disp[c], cm->hi));
   }
   LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_cnt, 0));
@@ -233,7 +259,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   }
   for (int c = 0; c < n; ++c) {
     LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi2, e_gemm[c], 0));
-    a2a_recv_to_send(p, q.O, q.Cb, p.d, c, cm->ep_comb, cm->hi2);
+    if (do_comm) a2a_recv_to_send(p, q.O, q.Cb, p.d, c, cm->ep_comb, cm->hi2);
   }
   LINA_CUDA_CHECK(cudaEventRecord(e_end, cm->hi2));
   LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_end, 0));
@@ -246,6 +272,20 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
   Ptrs q = carve(p, const_cast<void*>(saved), ws);
   const int dtype = p.bf16 ? 1 : 0;
   const int n = p.n;
+  const bool do_comm = !(cm->flags & 2), do_compute = !(cm->flags & 4);
+  if (!do_compute && p.P > 1) {  // collectives-only timing
+    cudaEvent_t* ev = cm->ev.data();
+    LINA_CUDA_CHECK(cudaEventRecord(ev[0], s));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi, ev[0], 0));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi2, ev[0], 0));
+    for (int c = 0; c < n; ++c) a2a_send_to_recv(p, q.dS, q.dO, p.d, c, cm->ep_disp, cm->hi);
+    for (int c = 0; c < n; ++c) a2a_recv_to_send(p, q.dXe, q.dXs, p.d, c, cm->ep_comb, cm->hi2);
+    LINA_CUDA_CHECK(cudaEventRecord(ev[1], cm->hi));
+    LINA_CUDA_CHECK(cudaEventRecord(ev[2], cm->hi2));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ev[1], 0));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2], 0));
+    return;
+  }
   // (a) combine backward: dg and g·dY rows into the send layout
   launch_combine_bwd(dtype, dout, q.Cb, q.tok_of, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, q.dS,
                      q.dg, s);
@@ -271,7 +311,7 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
     LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi, e_cb, 0));
     if (cm->sched) sched_a2a_begin(cm, cm->hi);
     for (int c = 0; c < n; ++c) {
-      a2a_send_to_recv(p, q.dS, q.dO, p.d, c, cm->ep_disp, cm->hi);
+      if (do_comm) a2a_send_to_recv(p, q.dS, q.dO, p.d, c, cm->ep_disp, cm->hi);
       LINA_CUDA_CHECK(cudaEventRecord(e_disp[c], cm->hi));
     }
     for (int c = 0; c < n; ++c) {
@@ -284,7 +324,7 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
     }
     for (int c = 0; c < n; ++c) {
       LINA_CUDA_CHECK(cudaStreamWaitEvent(cm->hi2, e_gemm[c], 0));
-      a2a_recv_to_send(p, q.dXe, q.dXs, p.d, c, cm->ep_comb, cm->hi2);
+      if (do_comm) a2a_recv_to_send(p, q.dXe, q.dXs, p.d, c, cm->ep_comb, cm->hi2);
     }
     LINA_CUDA_CHECK(cudaEventRecord(e_end, cm->hi2));
     if (cm->sched) sched_a2a_end(cm, cm->hi2);

@@ -307,8 +307,9 @@ def lina_sched_stats(comm: Comm):
     return a.value, b.value
 
 
-def lina_profile_enable(comm: Comm, on: bool = True):
-    _check(load().lina_profile_enable(comm.handle, 1 if on else 0))
+def lina_profile_enable(comm: Comm, on=True):
+    """on: bool or bit flags (1 timing, 2 skip collectives, 4 collectives only)."""
+    _check(load().lina_profile_enable(comm.handle, int(on)))
 
 
 def lina_profile_read(comm: Comm) -> dict:

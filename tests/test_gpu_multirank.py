@@ -54,6 +54,16 @@ def test_infer_replication_two_ranks(zipf, experts):
     _run_infer(2, "--tokens", "512", "--zipf", str(zipf), "--experts", str(experts))
 
 
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_scheduler_allreduce_two_ranks():
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port=29631", os.path.join(ROOT, "tests", "mp_sched.py"),
+           "--config", "C3", "--tokens", "1024", "--reps", "2"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "MP_SCHED OK" in out, out[-4000:]
+
+
 @pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
 def test_infer_replication_four_ranks():
     _run_infer(4, "--tokens", "512", "--zipf", "1.0", "--experts", "32", port=29622)
