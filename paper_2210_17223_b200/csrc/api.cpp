@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "ce.h"
 #include "layer.h"
 
 #include <atomic>
@@ -177,8 +178,12 @@ lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned 
       if (nccl_max_ctas > 0) cfg3.maxCTAs = nccl_max_ctas;
       LINA_NCCL_CHECK(ncclCommSplit(cm->ep_disp, 0, rank, &cm->dp, &cfg3));
       cm->sched = sched_create(cm);
-      // dispatch + combine all-to-all kernels may run beside the expert GEMM at once
-      tc_set_reserved_sms(nccl_max_ctas > 0 ? 2 * nccl_max_ctas : 16);
+      // Training all-to-all transport: copy engines over NVLink (zero SMs, ce.cpp) unless
+      // LINA_TRANSPORT=nccl; NCCL kernels running beside the persistent expert GEMM need
+      // SMs left free for them.
+      const char* tr = getenv("LINA_TRANSPORT");
+      if (!(tr && std::string(tr) == "nccl")) cm->ce = new CeTransport(cm);
+      tc_set_reserved_sms(cm->ce ? 0 : (nccl_max_ctas > 0 ? 2 * nccl_max_ctas : 16));
     }
     *out = cm;
     return LINA_OK;
@@ -191,6 +196,8 @@ lina_status lina_comm_destroy(lina_comm* cm) {
     cudaSetDevice(cm->device);
     if (cm->sched) sched_destroy(cm->sched);
     cm->sched = nullptr;
+    delete cm->ce;
+    cm->ce = nullptr;
     if (cm->dp) ncclCommDestroy(cm->dp);
     if (cm->ep_comb) ncclCommDestroy(cm->ep_comb);
     if (cm->ep_disp) ncclCommDestroy(cm->ep_disp);

@@ -1,0 +1,48 @@
+// Copy-engine all-to-all transport (ce.cpp).
+#pragma once
+#include <vector>
+
+#include "internal.h"
+
+namespace lina {
+
+class CeTransport {
+ public:
+  // flag kinds: READY (at the receiver) and PULLED (at the sender) per exchange
+  enum { kReadyFwdD = 0, kReadyFwdC = 1, kReadyBwdD = 2, kReadyBwdC = 3,
+         kPulledFwdD = 4, kPulledFwdC = 5, kPulledBwdD = 6, kPulledBwdC = 7, kKinds = 8 };
+  static constexpr int kMaxChunks = 32;
+
+  explicit CeTransport(lina_comm* cm);  // collective (allgathers the flag-array handles)
+  ~CeTransport();
+  // Every rank's copy of `local` (same offset in its own buffer), mapped into this
+  // process; collective on the first call for a pointer, cached afterwards.
+  const std::vector<char*>& peers(const void* local, cudaStream_t s);
+  // Stream `s` waits until my flag (kind, peer, chunk) >= value.
+  void wait_flag(cudaStream_t s, int kind, int peer, int chunk, uint32_t value);
+  // Stream `s` writes `value` into rank `rank`'s flag (kind, peer, chunk).
+  void post_flag(cudaStream_t s, int rank, int kind, int peer, int chunk, uint32_t value);
+  cudaStream_t disp_stream(int peer) const { return disp_[peer]; }
+  cudaStream_t comb_stream(int peer) const { return comb_[peer]; }
+  // event pool: [which (0..3)][peer][chunk or kMaxChunks(+1)]
+  cudaEvent_t ev(int which, int peer, int chunk) const {
+    return events_[((size_t)which * cm_->world + peer) * (kMaxChunks + 2) + chunk];
+  }
+  uint32_t seq_fwd = 0, seq_bwd = 0;
+
+ private:
+  size_t slot(int kind, int peer, int chunk) const {
+    return ((size_t)kind * cm_->world + peer) * kMaxChunks + chunk;
+  }
+  std::vector<char*> map_collective(const void* local, cudaStream_t s);
+  lina_comm* cm_;
+  struct Impl;
+  Impl* impl_;
+  uint32_t* flags_ = nullptr;
+  size_t nflags_ = 0;
+  std::vector<char*> peer_flags_;
+  std::vector<cudaStream_t> disp_, comb_;
+  std::vector<cudaEvent_t> events_;
+};
+
+}  // namespace lina

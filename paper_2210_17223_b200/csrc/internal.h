@@ -36,7 +36,8 @@ struct StatusError {
                               __FILE__ + ":" + std::to_string(__LINE__) + ")"};                \
   } while (0)
 
-class Scheduler;  // sched.cpp
+class Scheduler;    // sched.cpp
+class CeTransport;  // ce.cpp
 
 // Buffer plan for one descriptor on one communicator (layer.cpp).
 struct Plan {
@@ -67,6 +68,7 @@ struct lina_comm {
   cudaStream_t lo = nullptr;     // allreduce micro-ops (least priority)
   std::vector<cudaEvent_t> ev;   // event pool (timing disabled)
   lina::Scheduler* sched = nullptr;
+  lina::CeTransport* ce = nullptr;  // copy-engine all-to-all (NULL = NCCL all-to-all)
   // profiling (lina_profile_enable / lina_profile_read)
   bool prof = false;
   int flags = 0;  // lina_profile_enable bits: 1 timing events, 2 skip collectives, 4 collectives only

@@ -21,6 +21,7 @@
 
 #include "internal.h"
 #include "kernels.h"
+#include "ce.h"
 #include "layer.h"
 
 namespace lina {
@@ -159,6 +160,132 @@ void row_gemm(const Plan& p, const void* A, const void* B, void* D, const void* 
   launch_expert_row_gemm(p.bf16 ? 1 : 0, g, b_kmajor, epi, st);
 }
 
+// ------------------------------------------------------------------ copy-engine transport
+// (ce.cpp).  Byte offsets of the chunk blocks:
+//   send layout [n][E][Cm][w]:        block of peer r in chunk c  = (c*E + r*El)*Cm*w
+//   recv layout [n][P][El][Cm][w]:    segment of source s in chunk c = (c*P + s)*El*Cm*w
+size_t send_block(const Plan& p, int c, int r, int w) { return ((size_t)c * p.E + (size_t)r * p.El) * p.Cm * w * p.dt; }
+size_t recv_block(const Plan& p, int c, int s, int w) { return ((size_t)c * p.P + s) * p.El * p.Cm * w * p.dt; }
+size_t block_bytes(const Plan& p, int w) { return (size_t)p.El * p.Cm * w * p.dt; }
+
+// Forward micro-ops on the copy engines: dispatch pulls (peer D -> my R) per (source,
+// chunk) on per-source streams, GEMMs per chunk as soon as every source's chunk is in,
+// combine pulls (peer O -> my Cb) per chunk as soon as the expert rank posts it.
+void forward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, const void* w2,
+                void* saved, void* ws, cudaEvent_t e_perm, uint32_t seq, bool compute, cudaStream_t s) {
+  CeTransport& ce = *cm->ce;
+  const int P = p.P, me = cm->rank, n = p.n, d = p.d;
+  const auto& peer_ws = ce.peers(ws, s);
+  const auto& peer_saved = ce.peers(saved, s);
+  for (int src = 0; src < P; ++src) {
+    cudaStream_t st = ce.disp_stream(src);
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(st, e_perm, 0));
+    if (src != me) ce.wait_flag(st, CeTransport::kReadyFwdD, src, 0, seq);
+    LINA_CUDA_CHECK(cudaMemcpyAsync(q.recv_kept + (size_t)src * p.El,
+                                    peer_saved[src] + p.s_kept + 4 * (size_t)me * p.El, 4 * (size_t)p.El,
+                                    cudaMemcpyDeviceToDevice, st));
+    LINA_CUDA_CHECK(cudaEventRecord(ce.ev(0, src, CeTransport::kMaxChunks), st));
+    for (int c = 0; c < n; ++c) {
+      LINA_CUDA_CHECK(cudaMemcpyAsync(q.R + recv_block(p, c, src, d), peer_ws[src] + p.w_D + send_block(p, c, me, d),
+                                      block_bytes(p, d), cudaMemcpyDeviceToDevice, st));
+      LINA_CUDA_CHECK(cudaEventRecord(ce.ev(0, src, c), st));
+    }
+    if (src != me) ce.post_flag(st, src, CeTransport::kPulledFwdD, me, 0, seq);
+  }
+  for (int src = 0; src < P; ++src)
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ce.ev(0, src, CeTransport::kMaxChunks), 0));
+  if (compute) {
+    launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
+    launch_mtile_prefix(q.vcount, n, P * p.El, tc_tile_rows(), q.mtp, s);
+  }
+  for (int r = 0; r < P; ++r)  // every peer has pulled my previous O
+    if (r != me) ce.wait_flag(s, CeTransport::kPulledFwdC, r, 0, seq - 1);
+  for (int c = 0; c < n; ++c) {
+    for (int src = 0; src < P; ++src) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ce.ev(0, src, c), 0));
+    if (compute) {
+      prof_begin(cm, s);
+      row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s);
+      row_gemm(p, q.H, w2, q.O, nullptr, q.vcount, q.mtp, c, p.d, p.f, true, kEpiNone, s);
+      prof_end(cm, s, 2);
+    }
+    for (int r = 0; r < P; ++r)
+      if (r != me) ce.post_flag(s, r, CeTransport::kReadyFwdC, me, c, seq);
+    LINA_CUDA_CHECK(cudaEventRecord(ce.ev(1, me, c), s));
+  }
+  for (int src = 0; src < P; ++src) {
+    cudaStream_t st = ce.comb_stream(src);
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(st, e_perm, 0));
+    for (int c = 0; c < n; ++c) {
+      if (src == me) LINA_CUDA_CHECK(cudaStreamWaitEvent(st, ce.ev(1, me, c), 0));
+      else ce.wait_flag(st, CeTransport::kReadyFwdC, src, c, seq);
+      LINA_CUDA_CHECK(cudaMemcpyAsync(q.Cb + send_block(p, c, src, d), peer_ws[src] + p.w_O + recv_block(p, c, me, d),
+                                      block_bytes(p, d), cudaMemcpyDeviceToDevice, st));
+    }
+    if (src != me) ce.post_flag(st, src, CeTransport::kPulledFwdC, me, 0, seq);
+    LINA_CUDA_CHECK(cudaEventRecord(ce.ev(2, src, CeTransport::kMaxChunks), st));
+  }
+  for (int src = 0; src < P; ++src)
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ce.ev(2, src, CeTransport::kMaxChunks), 0));
+}
+
+void backward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, const void* w2, void* dw1,
+                 void* dw2, void* ws, cudaEvent_t e_cb, uint32_t seq, int dtype, bool compute,
+                 cudaStream_t s) {
+  CeTransport& ce = *cm->ce;
+  const int P = p.P, me = cm->rank, n = p.n, d = p.d;
+  const auto& peer_ws = ce.peers(ws, s);
+  if (cm->sched) sched_a2a_begin(cm, s);
+  for (int src = 0; src < P; ++src) {
+    cudaStream_t st = ce.disp_stream(src);
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(st, e_cb, 0));
+    if (src != me) ce.wait_flag(st, CeTransport::kReadyBwdD, src, 0, seq);
+    for (int c = 0; c < n; ++c) {
+      LINA_CUDA_CHECK(cudaMemcpyAsync(q.dO + recv_block(p, c, src, d), peer_ws[src] + p.w_dS + send_block(p, c, me, d),
+                                      block_bytes(p, d), cudaMemcpyDeviceToDevice, st));
+      LINA_CUDA_CHECK(cudaEventRecord(ce.ev(0, src, c), st));
+    }
+    if (src != me) ce.post_flag(st, src, CeTransport::kPulledBwdD, me, 0, seq);
+  }
+  for (int r = 0; r < P; ++r)  // every peer has pulled my previous dXe
+    if (r != me) ce.wait_flag(s, CeTransport::kPulledBwdC, r, 0, seq - 1);
+  for (int c = 0; c < n; ++c) {
+    for (int src = 0; src < P; ++src) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ce.ev(0, src, c), 0));
+    if (compute) {
+      prof_begin(cm, s);
+      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s);
+      row_gemm(p, q.dH, w1, q.dXe, nullptr, q.vcount, q.mtp, c, p.d, p.f, false, kEpiNone, s);
+      prof_end(cm, s, 2);
+    }
+    for (int r = 0; r < P; ++r)
+      if (r != me) ce.post_flag(s, r, CeTransport::kReadyBwdC, me, c, seq);
+    LINA_CUDA_CHECK(cudaEventRecord(ce.ev(1, me, c), s));
+  }
+  for (int src = 0; src < P; ++src) {
+    cudaStream_t st = ce.comb_stream(src);
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(st, e_cb, 0));
+    for (int c = 0; c < n; ++c) {
+      if (src == me) LINA_CUDA_CHECK(cudaStreamWaitEvent(st, ce.ev(1, me, c), 0));
+      else ce.wait_flag(st, CeTransport::kReadyBwdC, src, c, seq);
+      LINA_CUDA_CHECK(cudaMemcpyAsync(q.dXs + send_block(p, c, src, d), peer_ws[src] + p.w_dXe + recv_block(p, c, me, d),
+                                      block_bytes(p, d), cudaMemcpyDeviceToDevice, st));
+    }
+    if (src != me) ce.post_flag(st, src, CeTransport::kPulledBwdC, me, 0, seq);
+    LINA_CUDA_CHECK(cudaEventRecord(ce.ev(2, src, CeTransport::kMaxChunks), st));
+    if (cm->sched) sched_a2a_end(cm, st);
+  }
+  // weight gradients overlap the last combine pulls
+  WGrad wg2{q.dO, q.H, dw2, q.vcount, n, P, p.El, p.Cm, p.d, p.f};
+  WGrad wg1{q.dH, q.R, dw1, q.vcount, n, P, p.El, p.Cm, p.f, p.d};
+  if (compute) {
+    prof_begin(cm, s);
+    launch_expert_wgrad(dtype, wg2, s);
+    launch_expert_wgrad(dtype, wg1, s);
+    prof_end(cm, s, 2);
+  }
+  for (int src = 0; src < P; ++src)
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ce.ev(2, src, CeTransport::kMaxChunks), 0));
+}
+
 }  // namespace
 
 void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* gate_w,
@@ -169,6 +296,21 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   const bool override_r = route && route->override_routing;
   // instrumentation (lina_profile_enable): 2 = skip collectives, 4 = collectives only
   const bool do_comm = !(cm->flags & 2), do_compute = !(cm->flags & 4);
+  const bool ce = cm->ce && p.P > 1 && do_comm;
+  uint32_t seq = 0;
+  if (ce) {  // every peer has pulled my previous send buffer and counts before I rewrite them
+    seq = ++cm->ce->seq_fwd;
+    for (int r = 0; r < p.P; ++r)
+      if (r != cm->rank) cm->ce->wait_flag(s, CeTransport::kPulledFwdD, r, 0, seq - 1);
+  }
+  if (ce && !do_compute) {  // copy-engine collectives only (exposed-communication timing)
+    cudaEvent_t e0 = cm->ev[0];
+    for (int r = 0; r < p.P; ++r)
+      if (r != cm->rank) cm->ce->post_flag(s, r, CeTransport::kReadyFwdD, cm->rank, 0, seq);
+    LINA_CUDA_CHECK(cudaEventRecord(e0, s));
+    forward_ce(cm, p, q, w1, w2, saved, ws, e0, seq, false, s);
+    return;
+  }
   if (!do_compute && p.P > 1) {
     cudaEvent_t* ev = cm->ev.data();
     LINA_CUDA_CHECK(cudaEventRecord(ev[0], s));
@@ -228,6 +370,14 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   cudaEvent_t* ev = cm->ev.data();
   const int n = p.n;
   cudaEvent_t e_perm = ev[0], e_cnt = ev[1], e_end = ev[2];
+  if (ce) {
+    for (int r = 0; r < p.P; ++r)
+      if (r != cm->rank) cm->ce->post_flag(s, r, CeTransport::kReadyFwdD, cm->rank, 0, seq);
+    LINA_CUDA_CHECK(cudaEventRecord(e_perm, s));
+    forward_ce(cm, p, q, w1, w2, saved, ws, e_perm, seq, true, s);
+    launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, p.n, p.Cm, out, s);
+    return;
+  }
   cudaEvent_t* e_disp = ev + 3;
   cudaEvent_t* e_gemm = ev + 3 + n;
   LINA_CUDA_CHECK(cudaEventRecord(e_perm, s));
@@ -273,6 +423,21 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
   const int dtype = p.bf16 ? 1 : 0;
   const int n = p.n;
   const bool do_comm = !(cm->flags & 2), do_compute = !(cm->flags & 4);
+  const bool ce = cm->ce && p.P > 1 && do_comm;
+  uint32_t seq = 0;
+  if (ce) {  // every peer has pulled my previous g·dY rows before combine-bwd rewrites them
+    seq = ++cm->ce->seq_bwd;
+    for (int r = 0; r < p.P; ++r)
+      if (r != cm->rank) cm->ce->wait_flag(s, CeTransport::kPulledBwdD, r, 0, seq - 1);
+  }
+  if (ce && !do_compute) {
+    cudaEvent_t e0 = cm->ev[0];
+    for (int r = 0; r < p.P; ++r)
+      if (r != cm->rank) cm->ce->post_flag(s, r, CeTransport::kReadyBwdD, cm->rank, 0, seq);
+    LINA_CUDA_CHECK(cudaEventRecord(e0, s));
+    backward_ce(cm, p, q, w1, w2, dw1, dw2, ws, e0, seq, dtype, false, s);
+    return;
+  }
   if (!do_compute && p.P > 1) {  // collectives-only timing
     cudaEvent_t* ev = cm->ev.data();
     LINA_CUDA_CHECK(cudaEventRecord(ev[0], s));
@@ -293,7 +458,13 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
   if (cm->sched) sched_a2a_imminent(cm);
   WGrad wg2{q.dO, q.H, dw2, q.vcount, n, p.P, p.El, p.Cm, p.d, p.f};
   WGrad wg1{q.dH, q.R, dw1, q.vcount, n, p.P, p.El, p.Cm, p.f, p.d};
-  if (p.P == 1) {
+  if (ce) {
+    for (int r = 0; r < p.P; ++r)
+      if (r != cm->rank) cm->ce->post_flag(s, r, CeTransport::kReadyBwdD, cm->rank, 0, seq);
+    cudaEvent_t e_cb = cm->ev[0];
+    LINA_CUDA_CHECK(cudaEventRecord(e_cb, s));
+    backward_ce(cm, p, q, w1, w2, dw1, dw2, ws, e_cb, seq, dtype, true, s);
+  } else if (p.P == 1) {
     prof_begin(cm, s);
     for (int c = 0; c < n; ++c) {
       row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s);
