@@ -182,7 +182,9 @@ lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned 
       // LINA_TRANSPORT=nccl; NCCL kernels running beside the persistent expert GEMM need
       // SMs left free for them.
       const char* tr = getenv("LINA_TRANSPORT");
-      if (!(tr && std::string(tr) == "nccl")) cm->ce = new CeTransport(cm);
+      const std::string t = tr ? tr : "fused";
+      cm->transport = t == "nccl" ? 0 : (t == "ce" ? 1 : 2);
+      if (cm->transport > 0) cm->ce = new CeTransport(cm);
       tc_set_reserved_sms(cm->ce ? 0 : (nccl_max_ctas > 0 ? 2 * nccl_max_ctas : 16));
     }
     *out = cm;

@@ -1,5 +1,6 @@
 // Copy-engine all-to-all transport (ce.cpp).
 #pragma once
+#include <string>
 #include <vector>
 
 #include "internal.h"
@@ -10,7 +11,8 @@ class CeTransport {
  public:
   // flag kinds: READY (at the receiver) and PULLED (at the sender) per exchange
   enum { kReadyFwdD = 0, kReadyFwdC = 1, kReadyBwdD = 2, kReadyBwdC = 3,
-         kPulledFwdD = 4, kPulledFwdC = 5, kPulledBwdD = 6, kPulledBwdC = 7, kKinds = 8 };
+         kPulledFwdD = 4, kPulledFwdC = 5, kPulledBwdD = 6, kPulledBwdC = 7,
+         kFreeFwd = 8, kFreeBwd = 9, kKinds = 10 };
   static constexpr int kMaxChunks = 32;
 
   explicit CeTransport(lina_comm* cm);  // collective (allgathers the flag-array handles)
@@ -22,6 +24,11 @@ class CeTransport {
   void wait_flag(cudaStream_t s, int kind, int peer, int chunk, uint32_t value);
   // Stream `s` writes `value` into rank `rank`'s flag (kind, peer, chunk).
   void post_flag(cudaStream_t s, int rank, int kind, int peer, int chunk, uint32_t value);
+  // Device array of the P pointers peers(local)[r] + offset (cached; uploaded once).
+  void* const* dev_ptrs(const void* local, size_t offset, cudaStream_t s);
+  // Device array of P tensor maps, one per rank's buffer (cached by key; built by
+  // `build` on first use, uploaded once).
+  const void* dev_blob(const std::string& key, const std::vector<unsigned char>& bytes, cudaStream_t s);
   cudaStream_t disp_stream(int peer) const { return disp_[peer]; }
   cudaStream_t comb_stream(int peer) const { return comb_[peer]; }
   // event pool: [which (0..3)][peer][chunk or kMaxChunks(+1)]
@@ -29,6 +36,8 @@ class CeTransport {
     return events_[((size_t)which * cm_->world + peer) * (kMaxChunks + 2) + chunk];
   }
   uint32_t seq_fwd = 0, seq_bwd = 0;
+  // rounds that ran the copy-engine pipeline (its PULLED flags carry these values)
+  uint32_t last_ce_fwd = 0, last_ce_bwd = 0, prev_ce_fwd = 0, prev_ce_bwd = 0;
 
  private:
   size_t slot(int kind, int peer, int chunk) const {

@@ -68,7 +68,8 @@ struct lina_comm {
   cudaStream_t lo = nullptr;     // allreduce micro-ops (least priority)
   std::vector<cudaEvent_t> ev;   // event pool (timing disabled)
   lina::Scheduler* sched = nullptr;
-  lina::CeTransport* ce = nullptr;  // copy-engine all-to-all (NULL = NCCL all-to-all)
+  lina::CeTransport* ce = nullptr;  // peer mappings + flags (NULL = NCCL all-to-all only)
+  int transport = 0;                // 0 NCCL, 1 copy engines, 2 fused into the kernels (default)
   // profiling (lina_profile_enable / lina_profile_read)
   bool prof = false;
   int flags = 0;  // lina_profile_enable bits: 1 timing events, 2 skip collectives, 4 collectives only

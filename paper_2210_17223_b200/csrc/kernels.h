@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include <vector>
+
 namespace lina {
 
 enum { kEpiNone = 0, kEpiRelu = 1, kEpiMask = 2 };
@@ -66,6 +68,24 @@ bool tc_row_supported(const RowGemm& g);
 bool tc_wgrad_supported(const WGrad& g);
 void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s);
 void launch_wgrad_tc(const WGrad& g, cudaStream_t s);
+
+// fused dispatch over NVLink peer stores (permute.cu): rows go straight into the owners'
+// receive buffers (peer_rows[o]) and the counts into their recv_kept (peer_counts[o]).
+void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d,
+                         int E, int C, int n, int Cm, int El, int P, int me, void* const* peer_rows,
+                         void* const* peer_counts, cudaStream_t s);
+void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of,
+                             const float* gate, int T, int k, int d, int E, int C, int n, int Cm, int El,
+                             int P, int me, void* const* peer_rows, float* dg, cudaStream_t s);
+// Output tiles of a row GEMM stored through per-owner tensor maps (peer memory):
+// segment (c, s, el) of the receive layout goes to dmaps[s] at segment c*E + me*El + el.
+struct PeerStore {
+  const void* dmaps = nullptr;  // device array [P] of CUtensorMap (64-byte aligned)
+  int P = 0, me = 0, E = 0;
+};
+void launch_row_gemm_tc_peer(const RowGemm& g, bool b_kmajor, int epi, const PeerStore& ps, cudaStream_t s);
+// Host bytes of the P tensor maps of `bases[r]` viewed as [nseg][Cm][N] bf16 (box 64 x 32).
+std::vector<unsigned char> tc_peer_dmaps(const std::vector<char*>& bases, int N, int Cm, int nseg);
 
 // inference replica routing (infer_route.cu); tab = r[E] | rdev[E][N] | send_off[N][E] | cnt[E]
 void launch_infer_permute(int dtype, const void* X, const int* idx, const int* slot, const int* tab,

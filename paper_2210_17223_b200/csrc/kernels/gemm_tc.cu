@@ -32,6 +32,8 @@
 // are enumerated from a per-chunk prefix of valid row blocks (launch_mtile_prefix).
 #include <cuda.h>
 
+#include <cstring>
+
 #include "../common.h"
 #include "../kernels.h"
 
@@ -258,6 +260,11 @@ struct TcParams {
   __nv_bfloat16* D;
   const __nv_bfloat16* aux;
   int nchunks, P;      // WGRAD
+  // ROW with peer stores: output tile of segment (c, s, el) goes through dmaps[s] to
+  // segment c*dE + dme*El + el of rank s's buffer (the combine all-to-all fused into
+  // the epilogue); NULL = local store through tmD
+  const CUtensorMap* dmaps;
+  int dP, dme, dE;
 };
 
 template <int CG, bool WGRAD, bool B_MN, int EPI>
@@ -534,7 +541,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) {
           int x0, x1, x2;
           box_of(t, c0, x0, x1, x2);
-          tma_store_3d(&tmD, buf, x0, x1, x2);
+          if (!WGRAD && p.dmaps) {  // fused combine all-to-all: store into the owner's buffer
+            const int seg = x2;
+            const int el = seg % p.El, sidx = (seg / p.El) % p.dP, c = seg / (p.El * p.dP);
+            tma_store_3d(p.dmaps + sidx, buf, x0, x1, c * p.dE + p.dme * p.El + el);
+          } else {
+            tma_store_3d(&tmD, buf, x0, x1, x2);
+          }
           bulk_commit();
         }
         __syncwarp();
@@ -666,7 +679,31 @@ int tc_tile_rows() { return 128 * kTcCtaGroup; }
 bool tc_row_supported(const RowGemm& g) { return g.N % tc::BN == 0 && g.K % tc::BK == 0 && g.mtp; }
 bool tc_wgrad_supported(const WGrad& g) { return g.M % tc_tile_rows() == 0 && g.N % tc::BN == 0; }
 
+static void row_gemm_tc_impl(const RowGemm& g, bool b_kmajor, int epi, const PeerStore* ps,
+                             cudaStream_t s);
+
 void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s) {
+  row_gemm_tc_impl(g, b_kmajor, epi, nullptr, s);
+}
+
+void launch_row_gemm_tc_peer(const RowGemm& g, bool b_kmajor, int epi, const PeerStore& ps, cudaStream_t s) {
+  row_gemm_tc_impl(g, b_kmajor, epi, &ps, s);
+}
+
+std::vector<unsigned char> tc_peer_dmaps(const std::vector<char*>& bases, int N, int Cm, int nseg) {
+  std::vector<unsigned char> out(bases.size() * sizeof(CUtensorMap));
+  const uint64_t dims[3] = {(uint64_t)N, (uint64_t)Cm, (uint64_t)nseg};
+  const uint64_t str[2] = {(uint64_t)N * 2, (uint64_t)Cm * N * 2};
+  const uint32_t box[3] = {64, 32, 1};
+  for (size_t r = 0; r < bases.size(); ++r) {
+    CUtensorMap m = tc::make_map(bases[r], 3, dims, str, box);
+    std::memcpy(out.data() + r * sizeof(CUtensorMap), &m, sizeof(CUtensorMap));
+  }
+  return out;
+}
+
+static void row_gemm_tc_impl(const RowGemm& g, bool b_kmajor, int epi, const PeerStore* ps,
+                             cudaStream_t s) {
   using namespace tc;
   constexpr int CG = kTcCtaGroup;
   const int nseg_total = g.seg0 + g.nseg;  // the map spans every segment up to this launch's last
@@ -703,6 +740,12 @@ void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s
   const uint32_t dbox[3] = {64, 32, 1};
   CUtensorMap md = make_map(g.D, 3, ddims, dstr, dbox);
   CUtensorMap mx = (epi == kEpiMask) ? make_map(g.aux, 3, ddims, dstr, dbox) : md;
+  if (ps) {
+    p.dmaps = (const CUtensorMap*)ps->dmaps;
+    p.dP = ps->P;
+    p.dme = ps->me;
+    p.dE = ps->E;
+  }
   const int grid = num_sms() / CG * CG;
   row_dispatch<CG>(ma, mb, md, mx, p, b_kmajor, epi, grid, s);
   LINA_LAUNCH_CHECK();

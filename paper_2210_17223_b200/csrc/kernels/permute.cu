@@ -157,6 +157,88 @@ __global__ void gate_bwd_kernel(const float* __restrict__ probs, const int* __re
   if (lane + 32 < E) dL[t * E + lane + 32] = p1 * (dp1 - dot);
 }
 
+// ---- fused dispatch: the same row loops, but each row is stored straight into the
+// owner's receive buffer over NVLink (peer[o] = rank o's buffer mapped here).  Row
+// (c, e, r) of the send layout lands at recv row ((c*P + me)*El + e%El)*Cm + r of
+// owner o = e / El: the permute IS the dispatch all-to-all.
+__device__ __forceinline__ size_t peer_row(int c, int e, int r, int El, int P, int me, int Cm) {
+  return (((size_t)c * P + me) * El + (e % El)) * Cm + r;
+}
+
+template <typename T>
+__global__ void permute_peer_kernel(const T* __restrict__ X, const int* __restrict__ tok_of, int k,
+                                    int d, int E, int C, int n, int Cm, int El, int P, int me,
+                                    T* const* __restrict__ peer) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long rows = (long long)n * E * Cm;
+  if (gw >= rows) return;
+  const int r = (int)(gw % Cm);
+  const int ce = (int)(gw / Cm);
+  const int e = ce % E, c = ce / E;
+  const int b = chunk_begin(c, C, n), Cc = chunk_begin(c + 1, C, n) - b;
+  const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
+  constexpr int V = 16 / sizeof(T);
+  uint4* dst = reinterpret_cast<uint4*>(peer[e / El] + peer_row(c, e, r, El, P, me, Cm) * d);
+  const int nv = d / V;
+  if (a >= 0) {
+    const uint4* src = reinterpret_cast<const uint4*>(X + (size_t)(a / k) * d);
+    for (int v = lane; v < nv; v += 32) dst[v] = src[v];
+  } else {
+    for (int v = lane; v < nv; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
+  }
+}
+
+template <typename T>
+__global__ void combine_bwd_peer_kernel(const T* __restrict__ dY, const T* __restrict__ Recv,
+                                        const int* __restrict__ tok_of, const float* __restrict__ gate,
+                                        int k, int d, int E, int C, int n, int Cm, int El, int P, int me,
+                                        T* const* __restrict__ peer, float* __restrict__ dg) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long rows = (long long)n * E * Cm;
+  if (gw >= rows) return;
+  const int r = (int)(gw % Cm);
+  const int ce = (int)(gw / Cm);
+  const int e = ce % E, c = ce / E;
+  const int b = chunk_begin(c, C, n), Cc = chunk_begin(c + 1, C, n) - b;
+  const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
+  constexpr int V = 16 / sizeof(T);
+  const int nv = d / V;
+  T* dst = peer[e / El] + peer_row(c, e, r, El, P, me, Cm) * d;
+  if (a < 0) {
+    for (int v = lane; v < nv; v += 32) reinterpret_cast<uint4*>(dst)[v] = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  const float g = gate[a];
+  const T* dy = dY + (size_t)(a / k) * d;
+  const T* o = Recv + (size_t)gw * d;
+  float dot = 0.f;
+  for (int v = lane; v < nv; v += 32) {
+    float x[V], w[V];
+    load16(dy + v * V, x, (const T*)nullptr);
+    load16(o + v * V, w, (const T*)nullptr);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      dot = fmaf(x[i], w[i], dot);
+      x[i] *= g;
+    }
+    store16(dst + v * V, x, (T*)nullptr);
+  }
+#pragma unroll
+  for (int o2 = 16; o2; o2 >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o2);
+  if (lane == 0) dg[a] = dot;
+}
+
+// kept[o*El + el] (this source's counts for owner o's experts) -> owner's recv_kept[me*El + el]
+__global__ void counts_peer_kernel(const int* __restrict__ kept, int El, int P, int me,
+                                   int* const* __restrict__ peer) {
+  for (int i = threadIdx.x; i < P * El; i += blockDim.x) {
+    const int o = i / El, el = i % El;
+    peer[o][me * El + el] = kept[i];
+  }
+}
+
 inline int blocks_for_warps(long long warps, int threads = 256) {
   return (int)((warps * 32 + threads - 1) / threads);
 }
@@ -207,6 +289,30 @@ void launch_gate_bwd(const float* probs, const int* idx, const float* gate, cons
                      int k, int E, float* dL, cudaStream_t s) {
   if (T <= 0) return;
   gate_bwd_kernel<<<blocks_for_warps(T), 256, 0, s>>>(probs, idx, gate, dg, T, k, E, dL);
+  LINA_LAUNCH_CHECK();
+}
+
+void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d,
+                         int E, int C, int n, int Cm, int El, int P, int me, void* const* peer_rows,
+                         void* const* peer_counts, cudaStream_t s) {
+  counts_peer_kernel<<<1, 128, 0, s>>>(kept, El, P, me, (int* const*)peer_counts);
+  LINA_LAUNCH_CHECK();
+  const long long rows = (long long)n * E * Cm;
+  if (rows == 0) return;
+  LINA_DISPATCH_T(dtype, permute_peer_kernel<ET><<<blocks_for_warps(rows), 256, 0, s>>>(
+                             (const ET*)X, tok_of, k, d, E, C, n, Cm, El, P, me, (ET* const*)peer_rows));
+  LINA_LAUNCH_CHECK();
+}
+
+void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of,
+                             const float* gate, int T, int k, int d, int E, int C, int n, int Cm, int El,
+                             int P, int me, void* const* peer_rows, float* dg, cudaStream_t s) {
+  if (T > 0) LINA_CUDA_CHECK(cudaMemsetAsync(dg, 0, sizeof(float) * (size_t)T * k, s));
+  const long long rows = (long long)n * E * Cm;
+  if (rows == 0) return;
+  LINA_DISPATCH_T(dtype, combine_bwd_peer_kernel<ET><<<blocks_for_warps(rows), 256, 0, s>>>(
+                             (const ET*)dY, (const ET*)Recv, tok_of, gate, k, d, E, C, n, Cm, El, P, me,
+                             (ET* const*)peer_rows, dg));
   LINA_LAUNCH_CHECK();
 }
 

@@ -199,7 +199,7 @@ void forward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, con
     launch_mtile_prefix(q.vcount, n, P * p.El, tc_tile_rows(), q.mtp, s);
   }
   for (int r = 0; r < P; ++r)  // every peer has pulled my previous O
-    if (r != me) ce.wait_flag(s, CeTransport::kPulledFwdC, r, 0, seq - 1);
+    if (r != me) ce.wait_flag(s, CeTransport::kPulledFwdC, r, 0, ce.prev_ce_fwd);
   for (int c = 0; c < n; ++c) {
     for (int src = 0; src < P; ++src) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ce.ev(0, src, c), 0));
     if (compute) {
@@ -247,7 +247,7 @@ void backward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, co
     if (src != me) ce.post_flag(st, src, CeTransport::kPulledBwdD, me, 0, seq);
   }
   for (int r = 0; r < P; ++r)  // every peer has pulled my previous dXe
-    if (r != me) ce.wait_flag(s, CeTransport::kPulledBwdC, r, 0, seq - 1);
+    if (r != me) ce.wait_flag(s, CeTransport::kPulledBwdC, r, 0, ce.prev_ce_bwd);
   for (int c = 0; c < n; ++c) {
     for (int src = 0; src < P; ++src) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ce.ev(0, src, c), 0));
     if (compute) {
@@ -286,6 +286,150 @@ void backward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, co
     LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ce.ev(2, src, CeTransport::kMaxChunks), 0));
 }
 
+// ------------------------------------------------------------------ fused transport
+// The all-to-alls disappear into the kernels that produce their data (NVLink 5 peer
+// stores through IPC-mapped buffers): permute / combine-backward store each row into
+// its owner's receive buffer; the GEMM2 / dgrad2 epilogues TMA-store each output tile
+// into the owner's send-layout buffer while the tensor cores work on the next tile.
+// Cross-rank ordering: FREE (the receive buffers of this round may be written) and
+// READY (this rank's stores of the round are complete) flags, written with stream
+// memory operations after the producing kernel, waited on with stream memory
+// operations before the consuming kernel — no SM ever waits on another GPU.
+void post_all(lina_comm* cm, cudaStream_t s, int kind, uint32_t seq) {
+  for (int r = 0; r < cm->world; ++r)
+    if (r != cm->rank) cm->ce->post_flag(s, r, kind, cm->rank, 0, seq);
+}
+void wait_all(lina_comm* cm, cudaStream_t s, int kind, uint32_t seq) {
+  for (int r = 0; r < cm->world; ++r)
+    if (r != cm->rank) cm->ce->wait_flag(s, kind, r, 0, seq);
+}
+
+bool fused_ok(const lina_comm* cm, const Plan& p) {
+  return cm->transport == 2 && cm->ce && p.P > 1 && p.bf16 && p.d % 256 == 0 && p.f % 256 == 0 &&
+         p.d % 64 == 0 && p.f % 64 == 0;
+}
+
+void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* tokens, const float* gate_w,
+                   const void* w1, const void* w2, void* out, void* saved, void* ws, lina_route* route,
+                   cudaStream_t s) {
+  CeTransport& ce = *cm->ce;
+  const int dtype = 1, P = p.P, me = cm->rank, n = p.n;
+  const uint32_t seq = ++ce.seq_fwd;
+  const bool override_r = route && route->override_routing;
+  post_all(cm, s, CeTransport::kFreeFwd, seq);  // my R, recv counts and Cb may be overwritten
+  if (override_r) {
+    LINA_CUDA_CHECK(cudaMemcpyAsync(q.idx, route->idx, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
+    LINA_CUDA_CHECK(cudaMemcpyAsync(q.gate, route->gate, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
+  }
+  launch_gate_topk(dtype, tokens, gate_w, p.T, p.d, p.E, p.k, override_r ? 0 : 1, q.probs, q.idx, q.gate, s);
+  launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr, q.kept,
+               q.tok_of, s);
+  void* const* peer_R = ce.dev_ptrs(saved, p.s_R, s);
+  void* const* peer_cnt = ce.dev_ptrs(saved, p.s_recvkept, s);
+  wait_all(cm, s, CeTransport::kFreeFwd, seq);
+  launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me, peer_R,
+                      peer_cnt, s);
+  post_all(cm, s, CeTransport::kReadyFwdD, seq);
+  if (route) {
+    if (route->idx && !override_r)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->idx, q.idx, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
+    if (route->gate && !override_r)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->gate, q.gate, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
+    if (route->slot)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->slot, q.slot, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
+    if (route->probs)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->probs, q.probs, 4 * (size_t)p.T * p.E, cudaMemcpyDeviceToDevice, s));
+  }
+  wait_all(cm, s, CeTransport::kReadyFwdD, seq);
+  launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
+  launch_mtile_prefix(q.vcount, n, P * p.El, tc_tile_rows(), q.mtp, s);
+  const auto& ps_saved = ce.peers(saved, s);
+  std::vector<char*> cb(P);
+  for (int r = 0; r < P; ++r) cb[r] = ps_saved[r] + p.s_C;
+  PeerStore st;
+  st.dmaps = ce.dev_blob("fwdC:" + std::to_string((uintptr_t)saved) + ":" + std::to_string(p.s_C) + ":" +
+                             std::to_string(p.Cm) + ":" + std::to_string(n * p.E),
+                         tc_peer_dmaps(cb, p.d, p.Cm, n * p.E), s);
+  st.P = P;
+  st.me = me;
+  st.E = p.E;
+  prof_begin(cm, s);
+  for (int c = 0; c < n; ++c) {
+    row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s);
+    RowGemm g{};
+    g.mtp = q.mtp + (size_t)c * (P * p.El + 1);
+    g.A = q.H;
+    g.B = w2;
+    g.D = q.O;
+    g.vcount = q.vcount;
+    g.seg0 = c * P * p.El;
+    g.nseg = P * p.El;
+    g.El = p.El;
+    g.Cm = p.Cm;
+    g.N = p.d;
+    g.K = p.f;
+    launch_row_gemm_tc_peer(g, true, kEpiNone, st, s);  // combine all-to-all in the epilogue
+  }
+  prof_end(cm, s, 2 * n);
+  post_all(cm, s, CeTransport::kReadyFwdC, seq);
+  wait_all(cm, s, CeTransport::kReadyFwdC, seq);
+  launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, out, s);
+}
+
+void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dout, const void* tokens,
+                    const float* gate_w, const void* w1, const void* w2, void* dtokens, float* dgate_w,
+                    void* dw1, void* dw2, void* ws, cudaStream_t s) {
+  CeTransport& ce = *cm->ce;
+  const int dtype = 1, P = p.P, me = cm->rank, n = p.n;
+  const uint32_t seq = ++ce.seq_bwd;
+  post_all(cm, s, CeTransport::kFreeBwd, seq);  // my dO and dXs may be overwritten
+  void* const* peer_dO = ce.dev_ptrs(ws, p.w_dO, s);
+  if (cm->sched) sched_a2a_imminent(cm);
+  wait_all(cm, s, CeTransport::kFreeBwd, seq);
+  launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me,
+                          peer_dO, q.dg, s);
+  post_all(cm, s, CeTransport::kReadyBwdD, seq);
+  wait_all(cm, s, CeTransport::kReadyBwdD, seq);
+  const auto& ps_ws = ce.peers(ws, s);
+  std::vector<char*> dxs(P);
+  for (int r = 0; r < P; ++r) dxs[r] = ps_ws[r] + p.w_dXs;
+  PeerStore st;
+  st.dmaps = ce.dev_blob("bwdC:" + std::to_string((uintptr_t)ws) + ":" + std::to_string(p.w_dXs) + ":" +
+                             std::to_string(p.Cm) + ":" + std::to_string(n * p.E),
+                         tc_peer_dmaps(dxs, p.d, p.Cm, n * p.E), s);
+  st.P = P;
+  st.me = me;
+  st.E = p.E;
+  prof_begin(cm, s);
+  for (int c = 0; c < n; ++c) {
+    row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s);
+    RowGemm g{};
+    g.mtp = q.mtp + (size_t)c * (P * p.El + 1);
+    g.A = q.dH;
+    g.B = w1;
+    g.D = q.dXe;
+    g.vcount = q.vcount;
+    g.seg0 = c * P * p.El;
+    g.nseg = P * p.El;
+    g.El = p.El;
+    g.Cm = p.Cm;
+    g.N = p.d;
+    g.K = p.f;
+    launch_row_gemm_tc_peer(g, false, kEpiNone, st, s);  // combine all-to-all in the epilogue
+  }
+  post_all(cm, s, CeTransport::kReadyBwdC, seq);
+  WGrad wg2{q.dO, q.H, dw2, q.vcount, n, P, p.El, p.Cm, p.d, p.f};
+  WGrad wg1{q.dH, q.R, dw1, q.vcount, n, P, p.El, p.Cm, p.f, p.d};
+  launch_expert_wgrad(dtype, wg2, s);
+  launch_expert_wgrad(dtype, wg1, s);
+  prof_end(cm, s, 2 * n + 2);
+  wait_all(cm, s, CeTransport::kReadyBwdC, seq);
+  if (cm->sched) sched_a2a_end(cm, s);
+  launch_gate_bwd(q.probs, q.idx, q.gate, q.dg, p.T, p.k, p.E, q.dL, s);
+  launch_dx(dtype, q.dXs, q.idx, q.slot, q.dL, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm, dtokens, s);
+  launch_dwg(dtype, tokens, q.dL, p.T, p.d, p.E, q.dwg, dgate_w, s);
+}
+
 }  // namespace
 
 void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* gate_w,
@@ -296,12 +440,18 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   const bool override_r = route && route->override_routing;
   // instrumentation (lina_profile_enable): 2 = skip collectives, 4 = collectives only
   const bool do_comm = !(cm->flags & 2), do_compute = !(cm->flags & 4);
+  if (do_comm && do_compute && fused_ok(cm, p)) {
+    forward_fused(cm, p, q, tokens, gate_w, w1, w2, out, saved, ws, route, s);
+    return;
+  }
   const bool ce = cm->ce && p.P > 1 && do_comm;
   uint32_t seq = 0;
   if (ce) {  // every peer has pulled my previous send buffer and counts before I rewrite them
     seq = ++cm->ce->seq_fwd;
+    cm->ce->prev_ce_fwd = cm->ce->last_ce_fwd;  // the previous round that used the copy engines
+    cm->ce->last_ce_fwd = seq;
     for (int r = 0; r < p.P; ++r)
-      if (r != cm->rank) cm->ce->wait_flag(s, CeTransport::kPulledFwdD, r, 0, seq - 1);
+      if (r != cm->rank) cm->ce->wait_flag(s, CeTransport::kPulledFwdD, r, 0, cm->ce->prev_ce_fwd);
   }
   if (ce && !do_compute) {  // copy-engine collectives only (exposed-communication timing)
     cudaEvent_t e0 = cm->ev[0];
@@ -423,12 +573,18 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
   const int dtype = p.bf16 ? 1 : 0;
   const int n = p.n;
   const bool do_comm = !(cm->flags & 2), do_compute = !(cm->flags & 4);
+  if (do_comm && do_compute && fused_ok(cm, p)) {
+    backward_fused(cm, p, q, dout, tokens, gate_w, w1, w2, dtokens, dgate_w, dw1, dw2, ws, s);
+    return;
+  }
   const bool ce = cm->ce && p.P > 1 && do_comm;
   uint32_t seq = 0;
   if (ce) {  // every peer has pulled my previous g·dY rows before combine-bwd rewrites them
     seq = ++cm->ce->seq_bwd;
+    cm->ce->prev_ce_bwd = cm->ce->last_ce_bwd;
+    cm->ce->last_ce_bwd = seq;
     for (int r = 0; r < p.P; ++r)
-      if (r != cm->rank) cm->ce->wait_flag(s, CeTransport::kPulledBwdD, r, 0, seq - 1);
+      if (r != cm->rank) cm->ce->wait_flag(s, CeTransport::kPulledBwdD, r, 0, cm->ce->prev_ce_bwd);
   }
   if (ce && !do_compute) {
     cudaEvent_t e0 = cm->ev[0];
