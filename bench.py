@@ -38,7 +38,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="lina", choices=["lina", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(li.CONFIGS))
-    ap.add_argument("--n-chunks", type=int, default=0, help="0 = 1 at N=1, 4 otherwise")
+    ap.add_argument("--n-chunks", type=int, default=0,
+                    help="0 = 1 (the fused transport needs no micro-op chunking; see DESIGN.md §7)")
     ap.add_argument("--nccl-ctas", type=int, default=8, help="ncclConfig_t.maxCTAs per communicator (N>1)")
     ap.add_argument("--family", default="balanced", choices=["balanced", "grid"])
     ap.add_argument("--seed", type=int, default=1234)
@@ -199,7 +200,8 @@ def main():
     T, d, f, E, k = cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, cfg.num_experts, cfg.k
     C = cfg.capacity()
     El = E // world
-    n_chunks = args.n_chunks or (1 if world == 1 else 4)
+    n_chunks = args.n_chunks or 1
+    transport = os.environ.get("LINA_TRANSPORT", "fused") if world > 1 else "none"
     tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
     Wg_np, W1_np, W2_np = li.layer_weights(cfg, args.seed, args.family, experts=range(rank * El, (rank + 1) * El))
     X_np, dY_np = li.layer_tokens(cfg, args.seed, rank, args.family)
@@ -368,7 +370,7 @@ def main():
             "data": f"synthetic ({args.family} family, seeded random-init weights)",
             "config": {"workload": f"{cfg.name}: E={E} top-{k} d={d} f={f} T/rank={T} cf={cfg.cf} C={C} "
                                    f"n_chunks={n_chunks} {cfg.dtype}",
-                       "global_batch": world * T, "parallelism": f"ep{world}",
+                       "global_batch": world * T, "parallelism": f"ep{world}", "a2a_transport": transport,
                        "l2": "flushed between timed steps (256 MB write, outside the step events)",
                        "kept_assignments": int(kept_total)},
             "roofline": roof,
