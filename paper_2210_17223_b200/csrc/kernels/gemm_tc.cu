@@ -45,16 +45,14 @@ constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;  // 2 accumulators x BN
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the pair leader
 
-// MASK: the dgrad epilogue stages the whole 32 x 256 H box of each warp (4 boxes)
-// and gives up one pipeline stage for it.
 template <int CG, bool MASK = false> struct Geo {
   static constexpr int ROWS = 128 * CG;                  // tile rows per cluster
   static constexpr int A_BYTES = 128 * BK * 2;           // 16 KB per CTA
   static constexpr int B_ROWS = BN / CG;                 // B rows (N) staged per CTA
   static constexpr int B_BYTES = B_ROWS * BK * 2;        // 32 KB (CG=1) / 16 KB (CG=2)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (CG == 2 ? 6 : 4) - (MASK ? 1 : 0);
-  static constexpr int EPI_BUFS = MASK ? 4 : 2;          // 32 rows x 128 B boxes per epilogue warp
+  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  static constexpr int EPI_BUFS = 2;                     // 32 rows x 128 B boxes per epilogue warp
   static constexpr int EPI_BYTES = 4 * EPI_BUFS * 4096;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
@@ -265,6 +263,8 @@ struct TcParams {
   // the epilogue); NULL = local store through tmD
   const CUtensorMap* dmaps;
   int dP, dme, dE;
+  uint64_t* mask_out;       // ROW + ReLU: ReLU' bits of the stored output, [rows][N/64]
+  const uint64_t* mask_in;  // ROW + mask epilogue: the bits written by GEMM1
 };
 
 template <int CG, bool WGRAD, bool B_MN, int EPI>
@@ -380,15 +380,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (!WGRAD) {
           const int seg = p.seg0 + se;
           const int el = p.seg_expert ? p.seg_expert[se % p.El] : se % p.El;
-          if (EPI == kEpiMask) {
-            // Warm L2 with this CTA's 128 x 256 box of the mask operand H about one
-            // tile before the epilogue TMA-loads it into shared memory.
-            for (int yb = 0; yb < 128; yb += 32)
-              for (int xb = 0; xb < BN; xb += 64)
-                asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(&tmX),
-                             "r"(n0 + xb), "r"(m0 + arow + yb), "r"(seg)
-                             : "memory");
-          }
           for (int kb = 0; kb < p.K / BK; ++kb) {
             const int k0 = kb * BK;
             if (!B_MN) issue(k0, m0 + arow, seg, k0, el * p.N + n0 + brow, 0);
@@ -451,17 +442,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // Each warp owns 32 rows: TMEM -> registers -> epi -> bf16 -> a 128B-swizzled
     // 32 x 64 smem box -> TMA store (rows past the segment end are clipped by the
     // tensor map).  Two boxes per warp alternate so the store of one overlaps the
-    // fill of the next.  The ReLU'-mask epilogue (dgrad) instead owns four boxes:
-    // before waiting for the accumulator it TMA-loads the warp's whole 32 x 256 box
-    // of H (the loads overlap the tile's MMAs), then overwrites each box in place
-    // with the output and stores it.
+    // fill of the next.  The ReLU epilogue (GEMM1) also emits the ReLU' bit mask of
+    // the bf16 H it stores (1 bit per element, [rows][N/64] words); the dgrad
+    // epilogue multiplies by that mask instead of re-reading H (6 MB instead of
+    // 100 MB at configs[1]).
     const int quarter = warp & 3;
     uint8_t* my_epi = epi_smem + quarter * G::EPI_BUFS * 4096;
-    uint64_t* abar = tempty + 2 + 1 + quarter * 4;   // 4 aux barriers per warp (after the TMEM slot)
-    uint32_t abph = 0;                               // phase of this tile's aux boxes
     int acc = 0;
     uint32_t aph = 0;
-    int sub = 0;  // sub-tile counter (buffer = sub & 1 without mask)
+    int sub = 0;  // sub-tile counter (buffer = sub & 1)
+    const int mwords = p.N / 64;
     auto box_of = [&](int t, int c0, int& x0, int& x1, int& x2) {
       int se, m0, n0;
       decode(t, se, m0, n0);
@@ -473,21 +463,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int se, m0, n0;
       decode(t, se, m0, n0);
       const int nkb = kblocks_of(se);
-      if (EPI == kEpiMask && lane == 0) {
-        bulk_wait_all();  // the previous tile's stores have left the boxes
-        for (int j = 0; j < 4; ++j) {
-          int x0, x1, x2;
-          box_of(t, j * 64, x0, x1, x2);
-          mbar_expect_tx(&abar[j], 4096);
-          tma_load_3d<1>(my_epi + j * 4096, &tmX, &abar[j], x0, x1, x2);
-        }
+      const int row = m0 + 128 * rank + quarter * 32 + lane;  // row within the segment
+      const bool row_ok = !WGRAD && row < p.Cm;
+      const size_t mrow = row_ok ? ((size_t)(p.seg0 + se) * p.Cm + row) * mwords : 0;
+      uint64_t mk[4] = {0, 0, 0, 0};
+      if (EPI == kEpiMask && row_ok) {  // before the accumulator wait: latency hidden
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mk[j] = p.mask_in[mrow + (n0 >> 6) + j];
       }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 64, ++sub) {
-        const int b = EPI == kEpiMask ? (c0 >> 6) : (sub & 1);
+        const int b = sub & 1;
         uint8_t* buf = my_epi + b * 4096;
         const uint32_t rowaddr = smem_u32(buf) + lane * 128;
         uint32_t v[64];
@@ -499,43 +488,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 64; ++i) v[i] = 0u;
         }
-        if (EPI == kEpiMask) {
-          mbar_wait(&abar[b], abph);
-        } else {
-          if (lane == 0 && sub >= 2) bulk_wait_read1();  // the store that last used `buf` has read it
-          __syncwarp();
-        }
+        if (lane == 0 && sub >= 2) bulk_wait_read1();  // the store that last used `buf` has read it
+        __syncwarp();
+        uint64_t mword = 0;
+        const uint64_t min = EPI == kEpiMask ? mk[c0 >> 6] : 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const uint32_t qa = rowaddr + ((q ^ (lane & 7)) << 4);
-          float hx[8];
-          if (EPI == kEpiMask) {
-            uint4 hv;
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(hv.x), "=r"(hv.y), "=r"(hv.z), "=r"(hv.w)
-                         : "r"(qa));
-            const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&hv);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float2 f = __bfloat1622float2(hh[i]);
-              hx[2 * i] = f.x;
-              hx[2 * i + 1] = f.y;
-            }
-          }
           float x[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             float y = __uint_as_float(v[q * 8 + i]);
             if (EPI == kEpiRelu) y = fmaxf(y, 0.f);
-            if (EPI == kEpiMask) y = hx[i] > 0.f ? y : 0.f;
+            if (EPI == kEpiMask) y = ((min >> (q * 8 + i)) & 1) ? y : 0.f;
             x[i] = y;
           }
           uint4 pk;
           __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&pk);
 #pragma unroll
           for (int i = 0; i < 4; ++i) hp[i] = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+          if (EPI == kEpiRelu) {  // ReLU' of the stored (rounded, non-negative) value: bits != 0
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(&pk);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              mword |= (uint64_t)((w[i] & 0xFFFFu) != 0) << (q * 8 + 2 * i);
+              mword |= (uint64_t)((w[i] >> 16) != 0) << (q * 8 + 2 * i + 1);
+            }
+          }
           st_shared16(qa, pk);
         }
+        if (EPI == kEpiRelu && p.mask_out && row_ok) p.mask_out[mrow + ((n0 + c0) >> 6)] = mword;
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -552,7 +534,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         __syncwarp();
       }
-      abph ^= 1;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -735,6 +716,9 @@ static void row_gemm_tc_impl(const RowGemm& g, bool b_kmajor, int epi, const Pee
   p.K = g.K;
   p.D = (__nv_bfloat16*)g.D;
   p.aux = (const __nv_bfloat16*)g.aux;
+  p.mask_out = g.mask_out;
+  p.mask_in = g.mask_in;
+  if (epi == kEpiMask && !g.mask_in) throw CudaError{"tcgen05 dgrad needs the ReLU' bit mask"};
   const uint64_t ddims[3] = {(uint64_t)g.N, (uint64_t)g.Cm, (uint64_t)nseg_total};
   const uint64_t dstr[2] = {(uint64_t)g.N * 2, (uint64_t)g.Cm * g.N * 2};
   const uint32_t dbox[3] = {64, 32, 1};

@@ -63,6 +63,7 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
   p.s_R = take(recv_rows * p.d * p.dt);                       // routed tokens (X rows)
   p.s_H = take(recv_rows * (size_t)p.f * p.dt);               // relu(X W1ᵀ)
   p.s_C = take(send_rows * p.d * p.dt);                       // returned expert outputs
+  p.s_mask = take(recv_rows * (size_t)((p.f + 63) / 64) * 8);  // ReLU' bits of H
   p.saved_bytes = o;
   // ---- workspace
   o = 0;
@@ -85,7 +86,7 @@ namespace {
 
 struct Ptrs {
   float* probs; int* idx; float* gate; int* slot; int* kept; int* tok_of; int* recv_kept;
-  int* vcount; int* mtp; char* R; char* H; char* Cb;
+  int* vcount; int* mtp; char* R; char* H; char* Cb; uint64_t* mask;
   int* route; char* D; char* O; float* dg; float* dL; float* dwg; char* dS; char* dO; char* dH;
   char* dXe; char* dXs;
 };
@@ -107,6 +108,7 @@ Ptrs carve(const Plan& p, void* saved, void* ws) {
     q.R = sv + p.s_R;
     q.H = sv + p.s_H;
     q.Cb = sv + p.s_C;
+    q.mask = (uint64_t*)(sv + p.s_mask);
   }
   if (w) {
     q.route = (int*)(w + p.w_route);
@@ -143,8 +145,10 @@ void a2a_recv_to_send(const Plan& p, const char* recv, char* send, int w, int c,
 
 void row_gemm(const Plan& p, const void* A, const void* B, void* D, const void* aux,
               const int* vcount, const int* mtp, int c, int N, int K, bool b_kmajor, int epi,
-              cudaStream_t st) {
+              cudaStream_t st, uint64_t* mask_out = nullptr, const uint64_t* mask_in = nullptr) {
   RowGemm g{};
+  g.mask_out = mask_out;
+  g.mask_in = mask_in;
   g.mtp = mtp + (size_t)c * (p.P * p.El + 1);
   g.A = A;
   g.B = B;
@@ -204,7 +208,7 @@ void forward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, con
     for (int src = 0; src < P; ++src) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ce.ev(0, src, c), 0));
     if (compute) {
       prof_begin(cm, s);
-      row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s);
+      row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask);
       row_gemm(p, q.H, w2, q.O, nullptr, q.vcount, q.mtp, c, p.d, p.f, true, kEpiNone, s);
       prof_end(cm, s, 2);
     }
@@ -252,7 +256,7 @@ void backward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, co
     for (int src = 0; src < P; ++src) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ce.ev(0, src, c), 0));
     if (compute) {
       prof_begin(cm, s);
-      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s);
+      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask);
       row_gemm(p, q.dH, w1, q.dXe, nullptr, q.vcount, q.mtp, c, p.d, p.f, false, kEpiNone, s);
       prof_end(cm, s, 2);
     }
@@ -355,7 +359,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   st.E = p.E;
   prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
-    row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s);
+    row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask);
     RowGemm g{};
     g.mtp = q.mtp + (size_t)c * (P * p.El + 1);
     g.A = q.H;
@@ -402,7 +406,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   st.E = p.E;
   prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
-    row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s);
+    row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask);
     RowGemm g{};
     g.mtp = q.mtp + (size_t)c * (P * p.El + 1);
     g.A = q.dH;
@@ -509,7 +513,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
     launch_mtile_prefix(q.vcount, p.n, p.P * p.El, tc_tile_rows(), q.mtp, s);
     prof_begin(cm, s);
     for (int c = 0; c < p.n; ++c) {
-      row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s);
+      row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask);
       row_gemm(p, q.H, w2, q.O, nullptr, q.vcount, q.mtp, c, p.d, p.f, true, kEpiNone, s);
     }
     prof_end(cm, s, 2 * p.n);
@@ -552,7 +556,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   for (int c = 0; c < n; ++c) {
     LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_disp[c], 0));
     prof_begin(cm, s);
-    row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s);
+    row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask);
     row_gemm(p, q.H, w2, q.O, nullptr, q.vcount, q.mtp, c, p.d, p.f, true, kEpiNone, s);
     prof_end(cm, s, 2);
     LINA_CUDA_CHECK(cudaEventRecord(e_gemm[c], s));
@@ -623,7 +627,7 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
   } else if (p.P == 1) {
     prof_begin(cm, s);
     for (int c = 0; c < n; ++c) {
-      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s);
+      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask);
       row_gemm(p, q.dH, w1, q.dXe, nullptr, q.vcount, q.mtp, c, p.d, p.f, false, kEpiNone, s);
     }
     launch_expert_wgrad(dtype, wg2, s);
@@ -644,7 +648,7 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
     for (int c = 0; c < n; ++c) {
       LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_disp[c], 0));
       prof_begin(cm, s);
-      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s);
+      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask);
       row_gemm(p, q.dH, w1, q.dXe, nullptr, q.vcount, q.mtp, c, p.d, p.f, false, kEpiNone, s);
       prof_end(cm, s, 2);
       LINA_CUDA_CHECK(cudaEventRecord(e_gemm[c], s));
