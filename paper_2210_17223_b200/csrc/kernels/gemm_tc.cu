@@ -263,8 +263,8 @@ struct TcParams {
   // the epilogue); NULL = local store through tmD
   const CUtensorMap* dmaps;
   int dP, dme, dE;
-  uint64_t* mask_out;       // ROW + ReLU: ReLU' bits of the stored output, [rows][N/64]
-  const uint64_t* mask_in;  // ROW + mask epilogue: the bits written by GEMM1
+  uint32_t* mask_out;       // ROW + ReLU: ReLU' bits, [seg][ceil(Cm/32)][N] words (bit = row % 32)
+  const uint32_t* mask_in;  // ROW + mask epilogue: the bits written by GEMM1
 };
 
 template <int CG, bool WGRAD, bool B_MN, int EPI>
@@ -451,7 +451,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int acc = 0;
     uint32_t aph = 0;
     int sub = 0;  // sub-tile counter (buffer = sub & 1)
-    const int mwords = p.N / 64;
     auto box_of = [&](int t, int c0, int& x0, int& x1, int& x2) {
       int se, m0, n0;
       decode(t, se, m0, n0);
@@ -463,13 +462,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int se, m0, n0;
       decode(t, se, m0, n0);
       const int nkb = kblocks_of(se);
-      const int row = m0 + 128 * rank + quarter * 32 + lane;  // row within the segment
-      const bool row_ok = !WGRAD && row < p.Cm;
-      const size_t mrow = row_ok ? ((size_t)(p.seg0 + se) * p.Cm + row) * mwords : 0;
-      uint64_t mk[4] = {0, 0, 0, 0};
-      if (EPI == kEpiMask && row_ok) {  // before the accumulator wait: latency hidden
+      // ReLU' bits, transposed: word [seg][row group of 32][column] holds one bit per row
+      // of the warp's 32-row box (written with one ballot per column, read back with a
+      // coalesced load + one shuffle per column).
+      const int rg = (m0 + 128 * rank + quarter * 32) >> 5;  // row group within the segment
+      const bool grp_ok = !WGRAD && rg * 32 < p.Cm;
+      const size_t mbase = grp_ok ? (((size_t)(p.seg0 + se) * ((p.Cm + 31) >> 5) + rg) * p.N + n0) : 0;
+      uint32_t mk[8];
+      if (EPI == kEpiMask) {  // before the accumulator wait: latency hidden
 #pragma unroll
-        for (int j = 0; j < 4; ++j) mk[j] = p.mask_in[mrow + (n0 >> 6) + j];
+        for (int j = 0; j < 8; ++j) mk[j] = grp_ok ? p.mask_in[mbase + j * 32 + lane] : 0u;
       }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
@@ -490,8 +492,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (lane == 0 && sub >= 2) bulk_wait_read1();  // the store that last used `buf` has read it
         __syncwarp();
-        uint64_t mword = 0;
-        const uint64_t min = EPI == kEpiMask ? mk[c0 >> 6] : 0;
+        // mask words of this sub-tile's columns c0 + j (j < 64): held by lane j%32 in mk[c0/32 + j/32]
+        const uint32_t mlo = EPI == kEpiMask ? (c0 == 0 ? mk[0] : c0 == 64 ? mk[2] : c0 == 128 ? mk[4] : mk[6]) : 0u;
+        const uint32_t mhi = EPI == kEpiMask ? (c0 == 0 ? mk[1] : c0 == 64 ? mk[3] : c0 == 128 ? mk[5] : mk[7]) : 0u;
+        uint32_t wlo = 0, whi = 0;  // ReLU: this lane's ballot words for columns c0+lane, c0+32+lane
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const uint32_t qa = rowaddr + ((q ^ (lane & 7)) << 4);
@@ -500,7 +504,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int i = 0; i < 8; ++i) {
             float y = __uint_as_float(v[q * 8 + i]);
             if (EPI == kEpiRelu) y = fmaxf(y, 0.f);
-            if (EPI == kEpiMask) y = ((min >> (q * 8 + i)) & 1) ? y : 0.f;
+            if (EPI == kEpiMask) {
+              const int j = q * 8 + i;
+              const uint32_t w = __shfl_sync(0xffffffffu, j < 32 ? mlo : mhi, j & 31);
+              y = ((w >> lane) & 1u) ? y : 0.f;
+            }
             x[i] = y;
           }
           uint4 pk;
@@ -511,13 +519,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t* w = reinterpret_cast<const uint32_t*>(&pk);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              mword |= (uint64_t)((w[i] & 0xFFFFu) != 0) << (q * 8 + 2 * i);
-              mword |= (uint64_t)((w[i] >> 16) != 0) << (q * 8 + 2 * i + 1);
+              const int j0 = q * 8 + 2 * i;
+              const uint32_t b0 = __ballot_sync(0xffffffffu, (w[i] & 0xFFFFu) != 0);
+              const uint32_t b1 = __ballot_sync(0xffffffffu, (w[i] >> 16) != 0);
+              if (j0 < 32) {
+                if (lane == j0) wlo = b0;
+                if (lane == j0 + 1) wlo = b1;
+              } else {
+                if (lane == j0 - 32) whi = b0;
+                if (lane == j0 - 31) whi = b1;
+              }
             }
           }
           st_shared16(qa, pk);
         }
-        if (EPI == kEpiRelu && p.mask_out && row_ok) p.mask_out[mrow + ((n0 + c0) >> 6)] = mword;
+        if (EPI == kEpiRelu && p.mask_out && grp_ok) {
+          p.mask_out[mbase + c0 + lane] = wlo;
+          p.mask_out[mbase + c0 + 32 + lane] = whi;
+        }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
