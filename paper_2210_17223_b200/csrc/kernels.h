@@ -21,8 +21,8 @@ struct RowGemm {
   int seg0, nseg, El, Cm, N, K;
   const int* seg_expert = nullptr;  // [El] weight index of local slot (seg % El); NULL = identity
   int B_experts = 0;                // expert matrices in B (0 = El)
-  uint32_t* mask_out = nullptr;       // tcgen05 ReLU epilogue: ReLU' bits [seg][ceil(Cm/32)][N]
-  const uint32_t* mask_in = nullptr;  // tcgen05 mask epilogue: those bits (aux unused)
+  uint64_t* mask_out = nullptr;       // tcgen05 ReLU epilogue: ReLU' bits [nseg_total*Cm][N/64]
+  const uint64_t* mask_in = nullptr;  // tcgen05 mask epilogue: those bits (aux unused)
 };
 
 // Weight-gradient GEMM: D[El][M][N] = Σ_{c,s} Σ_{r < v} A[seg][r][:]ᵀ B[seg][r][:].

@@ -45,15 +45,20 @@ constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;  // 2 accumulators x BN
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the pair leader
 
-template <int CG, bool MASK = false> struct Geo {
+// WIDE: the epilogue-heavy ReLU / ReLU'-mask GEMMs (N = d_ffn outputs per row, short
+// K = d_model) get 8 epilogue warps (two per TMEM lane quarter, each owning half of
+// the 256 columns) and give up one pipeline stage for their staging boxes.
+template <int CG, bool WIDE = false> struct Geo {
   static constexpr int ROWS = 128 * CG;                  // tile rows per cluster
   static constexpr int A_BYTES = 128 * BK * 2;           // 16 KB per CTA
   static constexpr int B_ROWS = BN / CG;                 // B rows (N) staged per CTA
   static constexpr int B_BYTES = B_ROWS * BK * 2;        // 32 KB (CG=1) / 16 KB (CG=2)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  static constexpr int STAGES = (CG == 2 ? 6 : 4) - (WIDE ? 1 : 0);
+  static constexpr int EPW = WIDE ? 8 : 4;               // epilogue warps
+  static constexpr int THREADS = 64 + 32 * EPW;
   static constexpr int EPI_BUFS = 2;                     // 32 rows x 128 B boxes per epilogue warp
-  static constexpr int EPI_BYTES = 4 * EPI_BUFS * 4096;
+  static constexpr int EPI_BYTES = EPW * EPI_BUFS * 4096;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
 
@@ -263,16 +268,16 @@ struct TcParams {
   // the epilogue); NULL = local store through tmD
   const CUtensorMap* dmaps;
   int dP, dme, dE;
-  uint32_t* mask_out;       // ROW + ReLU: ReLU' bits, [seg][ceil(Cm/32)][N] words (bit = row % 32)
-  const uint32_t* mask_in;  // ROW + mask epilogue: the bits written by GEMM1
+  uint64_t* mask_out;       // ROW + ReLU: ReLU' bits of the stored output, [seg*Cm + row][N/64]
+  const uint64_t* mask_in;  // ROW + mask epilogue: the bits written by GEMM1
 };
 
 template <int CG, bool WGRAD, bool B_MN, int EPI>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
                    TcParams p) {
-  using G = Geo<CG, EPI == kEpiMask>;
+  using G = Geo<CG, EPI != kEpiNone>;
   constexpr int STAGES = G::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -305,7 +310,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * CG);
+      mbar_init(&tempty[a], G::EPW * CG);
     }
     for (int a = 0; a < 16; ++a) mbar_init(tempty + 3 + a, 1);  // epilogue aux-box barriers
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -438,19 +443,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
-    // ================= epilogue (warps 2..5): TMEM lane quarter = warp % 4
-    // Each warp owns 32 rows: TMEM -> registers -> epi -> bf16 -> a 128B-swizzled
-    // 32 x 64 smem box -> TMA store (rows past the segment end are clipped by the
-    // tensor map).  Two boxes per warp alternate so the store of one overlaps the
-    // fill of the next.  The ReLU epilogue (GEMM1) also emits the ReLU' bit mask of
-    // the bf16 H it stores (1 bit per element, [rows][N/64] words); the dgrad
-    // epilogue multiplies by that mask instead of re-reading H (6 MB instead of
-    // 100 MB at configs[1]).
+    // ================= epilogue (warps 2..): TMEM lane quarter = warp % 4
+    // Each warp owns 32 rows and BN/(EPW/4) columns: TMEM -> registers -> epi -> bf16 ->
+    // a 128B-swizzled 32 x 64 smem box -> TMA store (rows past the segment end are
+    // clipped by the tensor map).  Two boxes per warp alternate so the store of one
+    // overlaps the fill of the next.  The ReLU epilogue (GEMM1) also emits the ReLU'
+    // bits of the bf16 H it stores (one 64-bit word per row and 64 columns); the dgrad
+    // epilogue multiplies by those bits instead of re-reading H (6 MB instead of 100 MB
+    // at configs[1]).
+    const int ew = warp - 2;                 // epilogue warp index
     const int quarter = warp & 3;
-    uint8_t* my_epi = epi_smem + quarter * G::EPI_BUFS * 4096;
+    constexpr int COLS = BN / (G::EPW / 4);  // columns per warp
+    const int col0 = (ew >> 2) * COLS;
+    uint8_t* my_epi = epi_smem + ew * G::EPI_BUFS * 4096;
     int acc = 0;
     uint32_t aph = 0;
     int sub = 0;  // sub-tile counter (buffer = sub & 1)
+    const int mwords = p.N >> 6;
     auto box_of = [&](int t, int c0, int& x0, int& x1, int& x2) {
       int se, m0, n0;
       decode(t, se, m0, n0);
@@ -462,22 +471,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int se, m0, n0;
       decode(t, se, m0, n0);
       const int nkb = kblocks_of(se);
-      // ReLU' bits, transposed: word [seg][row group of 32][column] holds one bit per row
-      // of the warp's 32-row box (written with one ballot per column, read back with a
-      // coalesced load + one shuffle per column).
-      const int rg = (m0 + 128 * rank + quarter * 32) >> 5;  // row group within the segment
-      const bool grp_ok = !WGRAD && rg * 32 < p.Cm;
-      const size_t mbase = grp_ok ? (((size_t)(p.seg0 + se) * ((p.Cm + 31) >> 5) + rg) * p.N + n0) : 0;
-      uint32_t mk[8];
+      const int row = m0 + 128 * rank + quarter * 32 + lane;  // row within the segment
+      const bool row_ok = !WGRAD && row < p.Cm;
+      const size_t mrow = row_ok ? ((size_t)(p.seg0 + se) * p.Cm + row) * mwords + ((n0 + col0) >> 6) : 0;
+      uint64_t mk[COLS / 64];
       if (EPI == kEpiMask) {  // before the accumulator wait: latency hidden
 #pragma unroll
-        for (int j = 0; j < 8; ++j) mk[j] = grp_ok ? p.mask_in[mbase + j * 32 + lane] : 0u;
+        for (int j = 0; j < COLS / 64; ++j) mk[j] = row_ok ? p.mask_in[mrow + j] : 0ull;
       }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 64, ++sub) {
+#pragma unroll
+      for (int j = 0; j < COLS / 64; ++j, ++sub) {
+        const int c0 = col0 + j * 64;
         const int b = sub & 1;
         uint8_t* buf = my_epi + b * 4096;
         const uint32_t rowaddr = smem_u32(buf) + lane * 128;
@@ -492,10 +499,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (lane == 0 && sub >= 2) bulk_wait_read1();  // the store that last used `buf` has read it
         __syncwarp();
-        // mask words of this sub-tile's columns c0 + j (j < 64): held by lane j%32 in mk[c0/32 + j/32]
-        const uint32_t mlo = EPI == kEpiMask ? (c0 == 0 ? mk[0] : c0 == 64 ? mk[2] : c0 == 128 ? mk[4] : mk[6]) : 0u;
-        const uint32_t mhi = EPI == kEpiMask ? (c0 == 0 ? mk[1] : c0 == 64 ? mk[3] : c0 == 128 ? mk[5] : mk[7]) : 0u;
-        uint32_t wlo = 0, whi = 0;  // ReLU: this lane's ballot words for columns c0+lane, c0+32+lane
+        uint64_t mword = 0;
+        const uint64_t min = EPI == kEpiMask ? mk[j] : 0ull;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const uint32_t qa = rowaddr + ((q ^ (lane & 7)) << 4);
@@ -504,11 +509,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int i = 0; i < 8; ++i) {
             float y = __uint_as_float(v[q * 8 + i]);
             if (EPI == kEpiRelu) y = fmaxf(y, 0.f);
-            if (EPI == kEpiMask) {
-              const int j = q * 8 + i;
-              const uint32_t w = __shfl_sync(0xffffffffu, j < 32 ? mlo : mhi, j & 31);
-              y = ((w >> lane) & 1u) ? y : 0.f;
-            }
+            if (EPI == kEpiMask) y = ((min >> (q * 8 + i)) & 1ull) ? y : 0.f;
             x[i] = y;
           }
           uint4 pk;
@@ -517,26 +518,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int i = 0; i < 4; ++i) hp[i] = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
           if (EPI == kEpiRelu) {  // ReLU' of the stored (rounded, non-negative) value: bits != 0
             const uint32_t* w = reinterpret_cast<const uint32_t*>(&pk);
+            uint32_t byte = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const int j0 = q * 8 + 2 * i;
-              const uint32_t b0 = __ballot_sync(0xffffffffu, (w[i] & 0xFFFFu) != 0);
-              const uint32_t b1 = __ballot_sync(0xffffffffu, (w[i] >> 16) != 0);
-              if (j0 < 32) {
-                if (lane == j0) wlo = b0;
-                if (lane == j0 + 1) wlo = b1;
-              } else {
-                if (lane == j0 - 32) whi = b0;
-                if (lane == j0 - 31) whi = b1;
-              }
+              const uint32_t m = __vcmpne2(w[i], 0u);     // 0xFFFF per nonzero half
+              byte |= ((m & 1u) | ((m >> 15) & 2u)) << (2 * i);
             }
+            mword |= (uint64_t)byte << (q * 8);
           }
           st_shared16(qa, pk);
         }
-        if (EPI == kEpiRelu && p.mask_out && grp_ok) {
-          p.mask_out[mbase + c0 + lane] = wlo;
-          p.mask_out[mbase + c0 + 32 + lane] = whi;
-        }
+        if (EPI == kEpiRelu && p.mask_out && row_ok) p.mask_out[mrow + j] = mword;
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -636,13 +628,13 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   static bool attr_set = false;
   if (!attr_set) {
     LINA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Geo<CG, EPI == kEpiMask>::SMEM_BYTES));
+                                         Geo<CG, EPI != kEpiNone>::SMEM_BYTES));
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = Geo<CG, EPI == kEpiMask>::SMEM_BYTES;
+  cfg.blockDim = dim3(Geo<CG, EPI != kEpiNone>::THREADS);
+  cfg.dynamicSmemBytes = Geo<CG, EPI != kEpiNone>::SMEM_BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -63,7 +63,7 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
   p.s_R = take(recv_rows * p.d * p.dt);                       // routed tokens (X rows)
   p.s_H = take(recv_rows * (size_t)p.f * p.dt);               // relu(X W1ᵀ)
   p.s_C = take(send_rows * p.d * p.dt);                       // returned expert outputs
-  p.s_mask = take((size_t)p.n * p.P * p.El * ((p.Cm + 31) / 32) * p.f * 4);  // ReLU' bits of H
+  p.s_mask = take(recv_rows * (size_t)((p.f + 63) / 64) * 8);  // ReLU' bits of H
   p.saved_bytes = o;
   // ---- workspace
   o = 0;
@@ -86,7 +86,7 @@ namespace {
 
 struct Ptrs {
   float* probs; int* idx; float* gate; int* slot; int* kept; int* tok_of; int* recv_kept;
-  int* vcount; int* mtp; char* R; char* H; char* Cb; uint32_t* mask;
+  int* vcount; int* mtp; char* R; char* H; char* Cb; uint64_t* mask;
   int* route; char* D; char* O; float* dg; float* dL; float* dwg; char* dS; char* dO; char* dH;
   char* dXe; char* dXs;
 };
@@ -108,7 +108,7 @@ Ptrs carve(const Plan& p, void* saved, void* ws) {
     q.R = sv + p.s_R;
     q.H = sv + p.s_H;
     q.Cb = sv + p.s_C;
-    q.mask = (uint32_t*)(sv + p.s_mask);
+    q.mask = (uint64_t*)(sv + p.s_mask);
   }
   if (w) {
     q.route = (int*)(w + p.w_route);
@@ -145,7 +145,7 @@ void a2a_recv_to_send(const Plan& p, const char* recv, char* send, int w, int c,
 
 void row_gemm(const Plan& p, const void* A, const void* B, void* D, const void* aux,
               const int* vcount, const int* mtp, int c, int N, int K, bool b_kmajor, int epi,
-              cudaStream_t st, uint32_t* mask_out = nullptr, const uint32_t* mask_in = nullptr) {
+              cudaStream_t st, uint64_t* mask_out = nullptr, const uint64_t* mask_in = nullptr) {
   RowGemm g{};
   g.mask_out = mask_out;
   g.mask_in = mask_in;
