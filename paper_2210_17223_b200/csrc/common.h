@@ -94,10 +94,18 @@ __host__ __device__ __forceinline__ int chunk_begin(int c, int C, int n) {
 // The chunk holding slot s.
 __host__ __device__ __forceinline__ int chunk_of(int s, int C, int n) { return s / chunk_pitch(C, n); }
 __host__ __device__ __forceinline__ int chunk_rows_max(int C, int n) { return chunk_pitch(C, n); }
-// Row of (expert e, capacity slot s) in the chunk-major send layout [n][E][Cm][w].
+// Row of (expert e, capacity slot s) in the chunk-major send layout [n][E][Cm][w]
+// (Cm = chunk_pitch(C, n), precomputed by the host: one division per call).
 __host__ __device__ __forceinline__ size_t send_row(int e, int s, int E, int C, int n, int Cm) {
-  const int c = chunk_of(s, C, n);
-  return ((size_t)c * E + e) * Cm + (s - chunk_begin(c, C, n));
+  (void)C;
+  (void)n;
+  const int c = s / Cm;
+  return ((size_t)c * E + e) * Cm + (s - c * Cm);
+}
+// First slot of chunk c given the pitch.
+__host__ __device__ __forceinline__ int chunk_begin_p(int c, int C, int Cm) {
+  const long long b = (long long)c * Cm;
+  return b < C ? (int)b : C;
 }
 
 }  // namespace lina

@@ -10,18 +10,20 @@
 // Layout: X [T,d] (bf16|fp32) row-major, Wg [d,E] fp32 row-major.
 //
 // bf16 tokens (gate_mma_kernel): the logits X·Wg are an N = E <= 64 GEMM.  Each warp
-// owns 16 tokens and runs mma.sync m16n8k16 (bf16 in, fp32 accumulate) with the
-// fp32 gate weight split exactly into three bf16 terms (w = hi + mid + lo, 24 =
-// 3 x 8 significand bits), so the product is the fp32 logit up to accumulation
-// order — exact for the grid inputs of DESIGN.md §4.  Tokens are read straight from
-// global memory as 16-byte vectors (16 loads in flight per lane per 256-column
-// slab); K is permuted consistently in A and B so each 16-byte vector feeds two
-// k-steps.  Wg slabs are staged transposed in shared memory (row pitch padded to
-// avoid bank conflicts) and split on the fly.
+// owns 16 tokens and a quarter of d and runs mma.sync m16n8k16 (bf16 in, fp32
+// accumulate) with the fp32 gate weight split exactly into three bf16 terms (w = hi +
+// mid + lo, 24 = 3 x 8 significand bits), so the product is the fp32 logit up to
+// accumulation order — exact for the grid inputs of DESIGN.md §4.  Tokens are read
+// straight from global memory as 16-byte vectors (16 loads in flight per lane); K is
+// permuted consistently in A and B so each 16-byte vector feeds two k-steps.  The
+// split Wg is staged once per CTA in shared memory in B-fragment order.  (Not a
+// tcgen05 GEMM: N = E is 8..64 and the kernel is bound by reading X once.)
 // fp32 tokens (gate_simt_kernel, the C1 path): a register-tiled FMA version.
 // Both end in the same epilogue: logits in shared memory, one warp per token for
 // the softmax (warp-shuffle max/sum) and k rounds of warp arg-max.
 #include <math.h>
+
+#include <algorithm>
 
 #include "../common.h"
 #include "../kernels.h"
@@ -92,9 +94,16 @@ __device__ __forceinline__ void gate_epilogue_rows(const float* lt, int ldl, int
 }
 
 // ------------------------------------------------------------------ tensor-core gate (bf16 X)
-constexpr int kMmaTok = 64;     // tokens per CTA (4 warps x 16)
-constexpr int kSlab = 256;      // d columns per staged Wg slab
-constexpr int kPitch = kSlab + 4;
+// CTA = kGTT token tiles (16 tokens each) x kGKS K-split warps.  Wg is staged once per
+// pass as ready-made B fragments: frag[split][n][kstep][lane] (uint2 = two packed bf16
+// pairs), i.e. the exact hi/mid/lo decomposition computed once per CTA instead of in the
+// inner loop, and read back with one conflict-free 8-byte LDS per fragment.  The K-split
+// partial logits are summed in a fixed order (deterministic).
+constexpr int kGTT = 2;                   // 16-token tiles per CTA
+constexpr int kGKS = 4;                   // K-split warps per tile
+constexpr int kGThreads = 32 * kGTT * kGKS;
+constexpr int kGTok = 16 * kGTT;          // tokens per CTA
+constexpr size_t kGStageBudget = 150 * 1024;
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -114,81 +123,122 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-template <int NT>  // NT = ceil(E/8) n-tiles of 8 experts
-__global__ void __launch_bounds__(128) gate_mma_kernel(const __nv_bfloat16* __restrict__ X,
-                                                       const float* __restrict__ Wg, int T, int d,
-                                                       int E, int k, int write_routing,
-                                                       float* __restrict__ probs,
-                                                       int* __restrict__ idx,
-                                                       float* __restrict__ gate) {
-  extern __shared__ float gsm[];
-  float* wt = gsm;                          // [NT*8][kPitch]  transposed Wg slab
-  float* lt = gsm + NT * 8 * kPitch;        // [kMmaTok][NT*8 + 1] logits
+// NT = ceil(E/8) n-tiles of 8 experts; PB = 32-column blocks staged per pass (runtime).
+template <int NT>
+__global__ void __launch_bounds__(kGThreads) gate_mma_kernel(const __nv_bfloat16* __restrict__ X,
+                                                             const float* __restrict__ Wg, int T, int d,
+                                                             int E, int k, int write_routing, int PB,
+                                                             float* __restrict__ probs,
+                                                             int* __restrict__ idx,
+                                                             float* __restrict__ gate) {
   constexpr int LP = NT * 8 + 1;
+  constexpr int G = NT <= 2 ? 8 : 4;        // 32-column blocks in flight per lane (2 x 16 B each)
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  uint2* frag = reinterpret_cast<uint2*>(gsm_raw);                          // [3][NT][2*PB][32]
+  float* part = reinterpret_cast<float*>(gsm_raw + (size_t)3 * NT * 2 * PB * 32 * sizeof(uint2));
+  // part: [kGKS][kGTok][LP] partial logits
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
-  const int t0 = blockIdx.x * kMmaTok + warp * 16;
+  const int tt = warp % kGTT, kh = warp / kGTT;
+  const int t0 = blockIdx.x * kGTok + tt * 16;
   const int ra = t0 + g, rb = t0 + g + 8;
+  const bool va = ra < T, vb = rb < T;
+  const int nkb = d / 32;
+  const int PB2 = 2 * PB;
+
   float c[NT][4], cm[NT][4], cl[NT][4];  // hi / mid / lo partial products: three independent chains
 #pragma unroll
   for (int n = 0; n < NT; ++n)
 #pragma unroll
     for (int i = 0; i < 4; ++i) c[n][i] = cm[n][i] = cl[n][i] = 0.f;
 
-  for (int s0 = 0; s0 < d; s0 += kSlab) {
-    // X: 8 x 32-column blocks, rows g and g+8, 16 bytes each — all issued before use
-    uint4 xa[8], xb[8];
+  for (int p0 = 0; p0 < nkb; p0 += PB) {
+    const int pb = min(PB, nkb - p0);
+    const int per = (pb + kGKS - 1) / kGKS;
+    const int kb0 = p0 + kh * per, kb1 = min(p0 + pb, kb0 + per);
+    // first group of this warp's X blocks goes out before the staging
+    uint4 xa[G], xb[G];
 #pragma unroll
-    for (int kb = 0; kb < 8; ++kb) {
-      const int col = s0 + kb * 32 + tq * 8;
-      const bool in = col < d;
-      xa[kb] = (in && ra < T) ? *reinterpret_cast<const uint4*>(X + (size_t)ra * d + col) : make_uint4(0, 0, 0, 0);
-      xb[kb] = (in && rb < T) ? *reinterpret_cast<const uint4*>(X + (size_t)rb * d + col) : make_uint4(0, 0, 0, 0);
+    for (int j = 0; j < G; ++j) {
+      const int kb = kb0 + j;
+      const int col = kb * 32 + tq * 8;
+      const bool in = kb < kb1;
+      xa[j] = (in && va) ? *reinterpret_cast<const uint4*>(X + (size_t)ra * d + col) : make_uint4(0, 0, 0, 0);
+      xb[j] = (in && vb) ? *reinterpret_cast<const uint4*>(X + (size_t)rb * d + col) : make_uint4(0, 0, 0, 0);
     }
-    __syncthreads();  // previous slab's B reads are done
-    for (int i = tid; i < NT * 8 * kSlab; i += 128) {
-      const int col = i % kSlab, e = i / kSlab;
-      wt[e * kPitch + col] = (e < E && s0 + col < d) ? __ldg(Wg + (size_t)(s0 + col) * E + e) : 0.f;
+    if (p0) __syncthreads();  // previous pass's fragment reads are done
+    for (int i = tid; i < NT * pb * 2 * 32; i += kGThreads) {
+      const int ln = i & 31, ks = (i >> 5) % (2 * pb), n = (i >> 5) / (2 * pb);
+      const int col = (p0 + (ks >> 1)) * 32 + (ln & 3) * 8 + (ks & 1) * 4;
+      const int e = n * 8 + (ln >> 2);
+      float w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = e < E ? __ldg(Wg + (size_t)(col + q) * E + e) : 0.f;
+      float h[4], m[4], l[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) split3(w[q], h[q], m[q], l[q]);
+      const size_t o = ((size_t)n * PB2 + ks) * 32 + ln;
+      const size_t so = (size_t)NT * PB2 * 32;
+      frag[o] = make_uint2(pack_bf16(h[0], h[1]), pack_bf16(h[2], h[3]));
+      frag[so + o] = make_uint2(pack_bf16(m[0], m[1]), pack_bf16(m[2], m[3]));
+      frag[2 * so + o] = make_uint2(pack_bf16(l[0], l[1]), pack_bf16(l[2], l[3]));
     }
     __syncthreads();
+    for (int kbg = kb0; kbg < kb1; kbg += G) {
+      if (kbg != kb0) {
 #pragma unroll
-    for (int kb = 0; kb < 8; ++kb) {
+        for (int j = 0; j < G; ++j) {
+          const int kb = kbg + j;
+          const int col = kb * 32 + tq * 8;
+          const bool in = kb < kb1;
+          xa[j] = (in && va) ? *reinterpret_cast<const uint4*>(X + (size_t)ra * d + col) : make_uint4(0, 0, 0, 0);
+          xb[j] = (in && vb) ? *reinterpret_cast<const uint4*>(X + (size_t)rb * d + col) : make_uint4(0, 0, 0, 0);
+        }
+      }
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        // logical k (2tq, 2tq+1 | 2tq+8, 2tq+9) <-> physical columns kb*32 + 8tq + 4s + (0,1 | 2,3)
-        const uint32_t a[4] = {s ? xa[kb].z : xa[kb].x, s ? xb[kb].z : xb[kb].x,
-                               s ? xa[kb].w : xa[kb].y, s ? xb[kb].w : xb[kb].y};
+      for (int j = 0; j < G; ++j) {
+        if (kbg + j >= kb1) break;
+        const int kl = kbg + j - p0;
 #pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          const float4 w = *reinterpret_cast<const float4*>(wt + (n * 8 + g) * kPitch + kb * 32 + tq * 8 + s * 4);
-          float h0, m0, l0, h1, m1, l1, h2, m2, l2, h3, m3, l3;
-          split3(w.x, h0, m0, l0);
-          split3(w.y, h1, m1, l1);
-          split3(w.z, h2, m2, l2);
-          split3(w.w, h3, m3, l3);
-          mma16816(c[n], a, pack_bf16(h0, h1), pack_bf16(h2, h3));
-          mma16816(cm[n], a, pack_bf16(m0, m1), pack_bf16(m2, m3));
-          mma16816(cl[n], a, pack_bf16(l0, l1), pack_bf16(l2, l3));
+        for (int s = 0; s < 2; ++s) {
+          // logical k (2tq, 2tq+1 | 2tq+8, 2tq+9) <-> physical columns kb*32 + 8tq + 4s + (0,1 | 2,3)
+          const uint32_t a[4] = {s ? xa[j].z : xa[j].x, s ? xb[j].z : xb[j].x,
+                                 s ? xa[j].w : xa[j].y, s ? xb[j].w : xb[j].y};
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const size_t o = ((size_t)n * PB2 + 2 * kl + s) * 32 + lane;
+            const size_t so = (size_t)NT * PB2 * 32;
+            const uint2 bh = frag[o], bm = frag[so + o], bl = frag[2 * so + o];
+            mma16816(c[n], a, bh.x, bh.y);
+            mma16816(cm[n], a, bm.x, bm.y);
+            mma16816(cl[n], a, bl.x, bl.y);
+          }
         }
       }
     }
   }
-  // fragments -> shared logits: c0,c1 = (row g, cols 2tq, 2tq+1); c2,c3 = (row g+8, ...)
-#pragma unroll
-  for (int n = 0; n < NT; ++n)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) c[n][i] = (c[n][i] + cm[n][i]) + cl[n][i];
+  // fragments -> partial logits: c0,c1 = (row g, cols 2tq, 2tq+1); c2,c3 = (row g+8, ...)
+  float* pw = part + (size_t)kh * kGTok * LP;
 #pragma unroll
   for (int n = 0; n < NT; ++n) {
-    float* r0 = lt + (warp * 16 + g) * LP + n * 8 + 2 * tq;
-    float* r1 = lt + (warp * 16 + g + 8) * LP + n * 8 + 2 * tq;
-    r0[0] = c[n][0];
-    r0[1] = c[n][1];
-    r1[0] = c[n][2];
-    r1[1] = c[n][3];
+    float* r0 = pw + (tt * 16 + g) * LP + n * 8 + 2 * tq;
+    float* r1 = pw + (tt * 16 + g + 8) * LP + n * 8 + 2 * tq;
+    r0[0] = (c[n][0] + cm[n][0]) + cl[n][0];
+    r0[1] = (c[n][1] + cm[n][1]) + cl[n][1];
+    r1[0] = (c[n][2] + cm[n][2]) + cl[n][2];
+    r1[1] = (c[n][3] + cm[n][3]) + cl[n][3];
   }
-  __syncwarp();
-  gate_epilogue_rows(lt + warp * 16 * LP, LP, 16, t0, T, E, k, write_routing, probs, idx, gate);
+  __syncthreads();
+  for (int i = tid; i < kGTok * LP; i += kGThreads) {
+    float v = part[i];
+#pragma unroll
+    for (int q = 1; q < kGKS; ++q) v += part[(size_t)q * kGTok * LP + i];
+    part[i] = v;
+  }
+  __syncthreads();
+  constexpr int RW = kGTok / (kGThreads / 32);  // logit rows per warp in the epilogue
+  gate_epilogue_rows(part + warp * RW * LP, LP, RW, blockIdx.x * kGTok + warp * RW, T, E, k, write_routing,
+                     probs, idx, gate);
 }
 
 // ------------------------------------------------------------------ SIMT gate (fp32 X)
@@ -288,16 +338,19 @@ void launch_gate_simt(const void* X, const float* Wg, int T, int d, int E, int k
 template <int NT>
 void launch_gate_mma(const void* X, const float* Wg, int T, int d, int E, int k, int write_routing,
                      float* probs, int* idx, float* gate, cudaStream_t s) {
-  const size_t smem = sizeof(float) * ((size_t)NT * 8 * kPitch + kMmaTok * (NT * 8 + 1));
-  static bool set = false;
-  if (!set) {
+  const int nkb = d / 32;
+  const size_t per_kb = (size_t)3 * NT * 2 * 32 * sizeof(uint2);
+  const int PB = (int)std::max<size_t>(1, std::min<size_t>(nkb, kGStageBudget / per_kb));
+  const size_t smem = PB * per_kb + sizeof(float) * (size_t)kGKS * kGTok * (NT * 8 + 1);
+  static size_t set = 0;
+  if (smem > set) {
     LINA_CUDA_CHECK(cudaFuncSetAttribute(gate_mma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
-    set = true;
+    set = smem;
   }
-  const int blocks = (T + kMmaTok - 1) / kMmaTok;
-  gate_mma_kernel<NT><<<blocks, 128, smem, s>>>((const __nv_bfloat16*)X, Wg, T, d, E, k, write_routing,
-                                                probs, idx, gate);
+  const int blocks = (T + kGTok - 1) / kGTok;
+  gate_mma_kernel<NT><<<blocks, kGThreads, smem, s>>>((const __nv_bfloat16*)X, Wg, T, d, E, k, write_routing,
+                                                      PB, probs, idx, gate);
 }
 
 }  // namespace

@@ -32,7 +32,7 @@ __global__ void permute_kernel(const T* __restrict__ X, const int* __restrict__ 
   const int r = (int)(gw % Cm);
   const int ce = (int)(gw / Cm);
   const int e = ce % E, c = ce / E;
-  const int b = chunk_begin(c, C, n), Cc = chunk_begin(c + 1, C, n) - b;
+  const int b = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b;
   const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
   constexpr int V = 16 / sizeof(T);
   uint4* dst = reinterpret_cast<uint4*>(Send + (size_t)gw * d);
@@ -92,7 +92,7 @@ __global__ void combine_bwd_kernel(const T* __restrict__ dY, const T* __restrict
   const int r = (int)(gw % Cm);
   const int ce = (int)(gw / Cm);
   const int e = ce % E, c = ce / E;
-  const int b = chunk_begin(c, C, n), Cc = chunk_begin(c + 1, C, n) - b;
+  const int b = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b;
   const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
   constexpr int V = 16 / sizeof(T);
   const int nv = d / V;
@@ -176,7 +176,7 @@ __global__ void permute_peer_kernel(const T* __restrict__ X, const int* __restri
   const int r = (int)(gw % Cm);
   const int ce = (int)(gw / Cm);
   const int e = ce % E, c = ce / E;
-  const int b = chunk_begin(c, C, n), Cc = chunk_begin(c + 1, C, n) - b;
+  const int b = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b;
   const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
   constexpr int V = 16 / sizeof(T);
   uint4* dst = reinterpret_cast<uint4*>(peer[e / El] + peer_row(c, e, r, El, P, me, Cm) * d);
@@ -201,7 +201,7 @@ __global__ void combine_bwd_peer_kernel(const T* __restrict__ dY, const T* __res
   const int r = (int)(gw % Cm);
   const int ce = (int)(gw / Cm);
   const int e = ce % E, c = ce / E;
-  const int b = chunk_begin(c, C, n), Cc = chunk_begin(c + 1, C, n) - b;
+  const int b = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b;
   const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
   constexpr int V = 16 / sizeof(T);
   const int nv = d / V;

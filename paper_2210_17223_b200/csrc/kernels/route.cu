@@ -89,7 +89,8 @@ __global__ void vcount_kernel(const int* __restrict__ recv_kept, int P, int El, 
   if (i >= n * P * El) return;
   const int se = i % (P * El);  // s*El + el
   const int c = i / (P * El);
-  const int b = chunk_begin(c, C, n), Cc = chunk_begin(c + 1, C, n) - b;
+  const int Cm = chunk_pitch(C, n);
+  const int b = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b;
   int v = recv_kept[se] - b;
   vcount[i] = v < 0 ? 0 : (v > Cc ? Cc : v);
 }
