@@ -48,7 +48,7 @@ struct Plan {
       s_C, s_mask;
   size_t saved_bytes;
   // offsets into `workspace`
-  size_t w_route, w_D, w_O, w_dg, w_dL, w_dwg, w_dS, w_dO, w_dH, w_dXe, w_dXs;
+  size_t w_route, w_D, w_O, w_dg, w_dwg, w_dS, w_dO, w_dH, w_dXe, w_dXs;
   size_t ws_bytes;
   size_t rows_send() const { return (size_t)n * E * Cm; }
   size_t rows_recv() const { return (size_t)n * P * El * Cm; }

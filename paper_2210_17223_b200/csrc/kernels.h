@@ -50,14 +50,13 @@ void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot
 void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* tok_of,
                         const float* gate, int T, int k, int d, int E, int C, int n, int Cm,
                         void* dSend, float* dg, cudaStream_t s);
-void launch_gate_bwd(const float* probs, const int* idx, const float* gate, const float* dg, int T,
-                     int k, int E, float* dL, cudaStream_t s);
-void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* dL,
-               const float* Wg, int T, int k, int d, int E, int C, int n, int Cm, void* dX,
-               cudaStream_t s);
+// dX (gather-sum + dL·Wgᵀ) and dWg (Xᵀ dL) with dL recomputed from the forward routing.
+void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* probs,
+               const float* gate, const float* dg, const float* Wg, int T, int k, int d, int E, int C,
+               int n, int Cm, void* dX, cudaStream_t s);
 size_t dwg_scratch_floats(int T, int d, int E);
-void launch_dwg(int dtype, const void* X, const float* dL, int T, int d, int E, float* scratch,
-                float* dWg, cudaStream_t s);
+void launch_dwg(int dtype, const void* X, const float* probs, const int* idx, const float* gate,
+                const float* dg, int T, int d, int E, int k, float* scratch, float* dWg, cudaStream_t s);
 
 // CTAs per tensor-core tile (cta_group::2 pairs -> 256-row tiles).
 constexpr int kTcCtaGroup = 2;

@@ -13,8 +13,7 @@
 // combine       : y_t = sum_{j kept, ascending} g_tj * Recv[row(t,j)]  (fp32 acc, R9)
 //                 ("reshaping the tensors and computing the weighted output" P:172-173).
 // combine_bwd   : dg_tj = <dY_t, O_tj>,  dSend[row] = g_tj * dY_t  (else 0).
-// gate_bwd      : dL_t = p ∘ (dp − <p,dp>),  dp from dg through g (R13).
-// (dX and dWg are in gate_bwd.cu.)
+// (dL, dX and dWg are in gate_bwd.cu.)
 // Rows are moved as 16-byte vectors, one warp per row / token.
 #include "../common.h"
 #include "../kernels.h"
@@ -22,34 +21,166 @@
 namespace lina {
 namespace {
 
-template <typename T>
-__global__ void permute_kernel(const T* __restrict__ X, const int* __restrict__ tok_of, int k,
-                               int d, int E, int C, int n, int Cm, T* __restrict__ Send) {
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long rows = (long long)n * E * Cm;
-  if (gw >= rows) return;
+// Warps move R whole rows at a time: the row indices are resolved by the first R lanes
+// and broadcast, then all R x NVL 16-byte loads of a lane are issued before the first
+// store (NVL = vectors per lane per row, <= kLoadsPerLane loads in flight per lane).
+// NVL = 0 instantiates the plain strided loop for rows wider than 8 x 32 vectors.
+constexpr int kLoadsPerLane = 12;
+
+__device__ __forceinline__ size_t peer_row(int c, int e, int r, int El, int P, int me, int Cm) {
+  return (((size_t)c * P + me) * El + (e % El)) * Cm + r;
+}
+
+// Send-layout row gw = (c*E + e)*Cm + r -> the assignment code in it (-1 = padding) and,
+// for the fused dispatch, its destination (owner e / El, receive row peer_row(...)).
+__device__ __forceinline__ int row_assignment(long long gw, const int* __restrict__ tok_of, int E, int C,
+                                              int Cm, int El, int P, int me, int& owner, size_t& prow) {
   const int r = (int)(gw % Cm);
   const int ce = (int)(gw / Cm);
   const int e = ce % E, c = ce / E;
   const int b = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b;
-  const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
+  owner = El > 0 ? e / El : 0;
+  prow = El > 0 ? peer_row(c, e, r, El, P, me, Cm) : (size_t)gw;
+  return (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
+}
+
+// permute (PEER = false): Send[row] = X[token of row] or 0.
+// fused dispatch (PEER = true): the same rows stored straight into the owners' receive
+// buffers over NVLink (peer[o] = rank o's buffer mapped here): row (c, e, r) lands at
+// recv row ((c*P + me)*El + e%El)*Cm + r of owner o = e / El, so the permute IS the
+// dispatch all-to-all.
+template <typename T, int NVL, bool PEER>
+__global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ X, const int* __restrict__ tok_of,
+                                                      int k, int d, int E, int C, int n, int Cm, int El,
+                                                      int P, int me, T* __restrict__ Send,
+                                                      T* const* __restrict__ peer) {
+  constexpr int R = NVL == 0 ? 1 : (NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / NVL);
+  constexpr int NL = NVL == 0 ? 1 : NVL;
   constexpr int V = 16 / sizeof(T);
-  uint4* dst = reinterpret_cast<uint4*>(Send + (size_t)gw * d);
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long rows = (long long)n * E * Cm;
+  const long long row0 = w * R;
+  if (row0 >= rows) return;
   const int nv = d / V;
-  if (a >= 0) {
-    const uint4* src = reinterpret_cast<const uint4*>(X + (size_t)(a / k) * d);
-    for (int v = lane; v < nv; v += 32) dst[v] = src[v];
+  int a = -1, owner = 0;
+  size_t prow = 0;
+  if (lane < R && row0 + lane < rows)
+    a = row_assignment(row0 + lane, tok_of, E, C, Cm, PEER ? El : 0, P, me, owner, prow);
+  if constexpr (NVL == 0) {
+    uint4* dst = reinterpret_cast<uint4*>(PEER ? peer[owner] + prow * d : Send + (size_t)row0 * d);
+    a = __shfl_sync(0xffffffffu, a, 0);
+    dst = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), 0));
+    const uint4* src = reinterpret_cast<const uint4*>(X + (size_t)(a >= 0 ? a / k : 0) * d);
+    for (int v = lane; v < nv; v += 32) dst[v] = a >= 0 ? src[v] : make_uint4(0, 0, 0, 0);
   } else {
-    for (int v = lane; v < nv; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
+    uint4 buf[R][NL];
+    int ai[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      ai[i] = __shfl_sync(0xffffffffu, a, i);
+      const uint4* src = reinterpret_cast<const uint4*>(X + (size_t)(ai[i] >= 0 ? ai[i] / k : 0) * d);
+#pragma unroll
+      for (int j = 0; j < NL; ++j) {
+        const int v = lane + 32 * j;
+        buf[i][j] = (ai[i] >= 0 && v < nv) ? src[v] : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (row0 + i >= rows) break;
+      uint4* dst;
+      if constexpr (PEER) {
+        const int o = __shfl_sync(0xffffffffu, owner, i);
+        const size_t pr = __shfl_sync(0xffffffffu, (unsigned long long)prow, i);
+        dst = reinterpret_cast<uint4*>(peer[o] + pr * d);
+      } else {
+        dst = reinterpret_cast<uint4*>(Send + (size_t)(row0 + i) * d);
+      }
+#pragma unroll
+      for (int j = 0; j < NL; ++j) {
+        const int v = lane + 32 * j;
+        if (v < nv) dst[v] = buf[i][j];
+      }
+    }
   }
 }
 
+// combine: y_t = Σ_{j kept, ascending} g_tj · Recv[row(t, j)] (fp32 accumulation).  A warp
+// owns TP = U / k tokens (U = kLoadsPerLane / NVL rows in flight); lane q < TP*k resolves
+// pair q, then every row load is issued before the sums.
+template <typename T, int NVL, int KT>
+__global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ Recv, const int* __restrict__ idx,
+                                                      const int* __restrict__ slot,
+                                                      const float* __restrict__ gate, int Tn, int k, int d,
+                                                      int E, int C, int n, int Cm, T* __restrict__ Y) {
+  constexpr int NL = NVL > 0 ? NVL : 1;  // (NVL = 0 is never launched)
+  constexpr int U = kLoadsPerLane / NL;
+  constexpr int TP = U / KT > 0 ? U / KT : 1;
+  static_assert(TP * KT <= 32, "pairs per warp");
+  constexpr int V = 16 / sizeof(T);
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long t0 = w * TP;
+  if (t0 >= Tn) return;
+  const int nv = d / V;
+  // lane q <-> pair (t0 + q / KT, q % KT)
+  size_t rowq = 0;
+  float gq = 0.f;
+  bool kq = false;
+  if (lane < TP * KT && t0 + lane / KT < Tn) {
+    const size_t pi = (size_t)t0 * KT + lane;
+    const int s = slot[pi];
+    kq = s >= 0;
+    if (kq) {
+      rowq = send_row(idx[pi], s, E, C, n, Cm);
+      gq = gate[pi];
+    }
+  }
+  uint4 buf[TP * KT][NL];
+  bool kept[TP * KT];
+  float g[TP * KT];
+#pragma unroll
+  for (int q = 0; q < TP * KT; ++q) {
+    kept[q] = __shfl_sync(0xffffffffu, (int)kq, q);
+    g[q] = __shfl_sync(0xffffffffu, gq, q);
+    const size_t rq = __shfl_sync(0xffffffffu, (unsigned long long)rowq, q);
+    const uint4* src = reinterpret_cast<const uint4*>(Recv + rq * d);
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int v = lane + 32 * j;
+      buf[q][j] = (kept[q] && v < nv) ? src[v] : make_uint4(0, 0, 0, 0);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TP; ++i) {
+    if (t0 + i >= Tn) break;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int v = lane + 32 * j;
+      if (v >= nv) continue;
+      float acc[V];
+#pragma unroll
+      for (int u = 0; u < V; ++u) acc[u] = 0.f;
+#pragma unroll
+      for (int q = i * KT; q < (i + 1) * KT; ++q) {
+        if (!kept[q]) continue;
+        float x[V];
+        load16(&buf[q][j], x, (const T*)nullptr);
+#pragma unroll
+        for (int u = 0; u < V; ++u) acc[u] = fmaf(g[q], x[u], acc[u]);
+      }
+      store16(Y + (size_t)(t0 + i) * d + v * V, acc, (T*)nullptr);
+    }
+  }
+}
+
+// generic k / wide rows: one warp per token, strided loop
 template <typename T>
-__global__ void combine_kernel(const T* __restrict__ Recv, const int* __restrict__ idx,
-                               const int* __restrict__ slot, const float* __restrict__ gate,
-                               int Tn, int k, int d, int E, int C, int n, int Cm,
-                               T* __restrict__ Y) {
+__global__ void combine_loop_kernel(const T* __restrict__ Recv, const int* __restrict__ idx,
+                                    const int* __restrict__ slot, const float* __restrict__ gate,
+                                    int Tn, int k, int d, int E, int C, int n, int Cm,
+                                    T* __restrict__ Y) {
   const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= Tn) return;
@@ -80,154 +211,107 @@ __global__ void combine_kernel(const T* __restrict__ Recv, const int* __restrict
   }
 }
 
-template <typename T>
-__global__ void combine_bwd_kernel(const T* __restrict__ dY, const T* __restrict__ Recv,
-                                   const int* __restrict__ tok_of, const float* __restrict__ gate,
-                                   int k, int d, int E, int C, int n, int Cm,
-                                   T* __restrict__ dSend, float* __restrict__ dg) {
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// combine backward over send-layout rows: dg_a = <dY_t, O_row>, dSend[row] = g_a · dY_t
+// (0 for padding rows).  PEER: dSend rows are stored into the owners' receive buffers.
+template <typename T, int NVL, bool PEER>
+__global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ dY, const T* __restrict__ Recv,
+                                                          const int* __restrict__ tok_of,
+                                                          const float* __restrict__ gate, int k, int d,
+                                                          int E, int C, int n, int Cm, int El, int P,
+                                                          int me, T* __restrict__ dSend,
+                                                          T* const* __restrict__ peer,
+                                                          float* __restrict__ dg) {
+  constexpr int NL = NVL == 0 ? 1 : NVL;
+  constexpr int R = NVL == 0 ? 1 : (2 * NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / (2 * NVL));
+  constexpr int V = 16 / sizeof(T);
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long rows = (long long)n * E * Cm;
-  if (gw >= rows) return;
-  const int r = (int)(gw % Cm);
-  const int ce = (int)(gw / Cm);
-  const int e = ce % E, c = ce / E;
-  const int b = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b;
-  const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
-  constexpr int V = 16 / sizeof(T);
+  const long long row0 = w * R;
+  if (row0 >= rows) return;
   const int nv = d / V;
-  T* dst = dSend + (size_t)gw * d;
-  if (a < 0) {
-    for (int v = lane; v < nv; v += 32) reinterpret_cast<uint4*>(dst)[v] = make_uint4(0, 0, 0, 0);
-    return;
+  int a = -1, owner = 0;
+  size_t prow = 0;
+  float ga = 0.f;
+  if (lane < R && row0 + lane < rows) {
+    a = row_assignment(row0 + lane, tok_of, E, C, Cm, PEER ? El : 0, P, me, owner, prow);
+    if (a >= 0) ga = gate[a];
   }
-  const float g = gate[a];
-  const T* dy = dY + (size_t)(a / k) * d;
-  const T* o = Recv + (size_t)gw * d;
-  float dot = 0.f;
-  for (int v = lane; v < nv; v += 32) {
-    float x[V], w[V];
-    load16(dy + v * V, x, (const T*)nullptr);
-    load16(o + v * V, w, (const T*)nullptr);
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      dot = fmaf(x[i], w[i], dot);
-      x[i] *= g;
+  if constexpr (NVL == 0) {
+    a = __shfl_sync(0xffffffffu, a, 0);
+    ga = __shfl_sync(0xffffffffu, ga, 0);
+    owner = __shfl_sync(0xffffffffu, owner, 0);
+    prow = __shfl_sync(0xffffffffu, (unsigned long long)prow, 0);
+    T* dst = PEER ? peer[owner] + prow * d : dSend + (size_t)row0 * d;
+    if (a < 0) {
+      for (int v = lane; v < nv; v += 32) reinterpret_cast<uint4*>(dst)[v] = make_uint4(0, 0, 0, 0);
+      return;
     }
-    store16(dst + v * V, x, (T*)nullptr);
-  }
+    const T* dy = dY + (size_t)(a / k) * d;
+    const T* o = Recv + (size_t)row0 * d;
+    float dot = 0.f;
+    for (int v = lane; v < nv; v += 32) {
+      float x[V], y[V];
+      load16(dy + v * V, x, (const T*)nullptr);
+      load16(o + v * V, y, (const T*)nullptr);
 #pragma unroll
-  for (int o2 = 16; o2; o2 >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o2);
-  if (lane == 0) dg[a] = dot;
-}
-
-// dL for one token per warp.  k=1: g0 = p_e0  => dp_e0 = dg0.
-// k>=2: g_j = p_ej / S  =>  dp_ei = (dg_i − Σ_j g_j dg_j) / S.   dL = p ∘ (dp − <p,dp>).
-__global__ void gate_bwd_kernel(const float* __restrict__ probs, const int* __restrict__ idx,
-                                const float* __restrict__ gate, const float* __restrict__ dg,
-                                int Tn, int k, int E, float* __restrict__ dL) {
-  const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= Tn) return;
-  const float p0 = lane < E ? probs[t * E + lane] : 0.f;
-  const float p1 = lane + 32 < E ? probs[t * E + lane + 32] : 0.f;
-  float dp0 = 0.f, dp1 = 0.f;
-  if (k == 1) {
-    const int e0 = idx[t];
-    if (e0 == lane) dp0 = dg[t];
-    if (e0 == lane + 32) dp1 = dg[t];
+      for (int i = 0; i < V; ++i) {
+        dot = fmaf(x[i], y[i], dot);
+        x[i] *= ga;
+      }
+      store16(dst + v * V, x, (T*)nullptr);
+    }
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o2);
+    if (lane == 0) dg[a] = dot;
   } else {
-    float S = 0.f, sgd = 0.f;
-    for (int j = 0; j < k; ++j) {
-      const int e = idx[t * k + j];
-      S += probs[t * E + e];
-      sgd = fmaf(gate[t * k + j], dg[t * k + j], sgd);
-    }
-    for (int j = 0; j < k; ++j) {
-      const int e = idx[t * k + j];
-      const float v = (dg[t * k + j] - sgd) / S;
-      if (e == lane) dp0 = v;
-      if (e == lane + 32) dp1 = v;
-    }
-  }
-  float dot = p0 * dp0 + p1 * dp1;
+    uint4 by[R][NL], bo[R][NL];
+    int ai[R];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-  if (lane < E) dL[t * E + lane] = p0 * (dp0 - dot);
-  if (lane + 32 < E) dL[t * E + lane + 32] = p1 * (dp1 - dot);
-}
-
-// ---- fused dispatch: the same row loops, but each row is stored straight into the
-// owner's receive buffer over NVLink (peer[o] = rank o's buffer mapped here).  Row
-// (c, e, r) of the send layout lands at recv row ((c*P + me)*El + e%El)*Cm + r of
-// owner o = e / El: the permute IS the dispatch all-to-all.
-__device__ __forceinline__ size_t peer_row(int c, int e, int r, int El, int P, int me, int Cm) {
-  return (((size_t)c * P + me) * El + (e % El)) * Cm + r;
-}
-
-template <typename T>
-__global__ void permute_peer_kernel(const T* __restrict__ X, const int* __restrict__ tok_of, int k,
-                                    int d, int E, int C, int n, int Cm, int El, int P, int me,
-                                    T* const* __restrict__ peer) {
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long rows = (long long)n * E * Cm;
-  if (gw >= rows) return;
-  const int r = (int)(gw % Cm);
-  const int ce = (int)(gw / Cm);
-  const int e = ce % E, c = ce / E;
-  const int b = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b;
-  const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
-  constexpr int V = 16 / sizeof(T);
-  uint4* dst = reinterpret_cast<uint4*>(peer[e / El] + peer_row(c, e, r, El, P, me, Cm) * d);
-  const int nv = d / V;
-  if (a >= 0) {
-    const uint4* src = reinterpret_cast<const uint4*>(X + (size_t)(a / k) * d);
-    for (int v = lane; v < nv; v += 32) dst[v] = src[v];
-  } else {
-    for (int v = lane; v < nv; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
-  }
-}
-
-template <typename T>
-__global__ void combine_bwd_peer_kernel(const T* __restrict__ dY, const T* __restrict__ Recv,
-                                        const int* __restrict__ tok_of, const float* __restrict__ gate,
-                                        int k, int d, int E, int C, int n, int Cm, int El, int P, int me,
-                                        T* const* __restrict__ peer, float* __restrict__ dg) {
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long rows = (long long)n * E * Cm;
-  if (gw >= rows) return;
-  const int r = (int)(gw % Cm);
-  const int ce = (int)(gw / Cm);
-  const int e = ce % E, c = ce / E;
-  const int b = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b;
-  const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
-  constexpr int V = 16 / sizeof(T);
-  const int nv = d / V;
-  T* dst = peer[e / El] + peer_row(c, e, r, El, P, me, Cm) * d;
-  if (a < 0) {
-    for (int v = lane; v < nv; v += 32) reinterpret_cast<uint4*>(dst)[v] = make_uint4(0, 0, 0, 0);
-    return;
-  }
-  const float g = gate[a];
-  const T* dy = dY + (size_t)(a / k) * d;
-  const T* o = Recv + (size_t)gw * d;
-  float dot = 0.f;
-  for (int v = lane; v < nv; v += 32) {
-    float x[V], w[V];
-    load16(dy + v * V, x, (const T*)nullptr);
-    load16(o + v * V, w, (const T*)nullptr);
+    for (int i = 0; i < R; ++i) {
+      ai[i] = __shfl_sync(0xffffffffu, a, i);
+      const uint4* dy = reinterpret_cast<const uint4*>(dY + (size_t)(ai[i] >= 0 ? ai[i] / k : 0) * d);
+      const uint4* o = reinterpret_cast<const uint4*>(Recv + (size_t)(row0 + i < rows ? row0 + i : 0) * d);
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-      dot = fmaf(x[i], w[i], dot);
-      x[i] *= g;
+      for (int j = 0; j < NL; ++j) {
+        const int v = lane + 32 * j;
+        const bool ok = ai[i] >= 0 && v < nv;
+        by[i][j] = ok ? dy[v] : make_uint4(0, 0, 0, 0);
+        bo[i][j] = ok ? o[v] : make_uint4(0, 0, 0, 0);
+      }
     }
-    store16(dst + v * V, x, (T*)nullptr);
-  }
 #pragma unroll
-  for (int o2 = 16; o2; o2 >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o2);
-  if (lane == 0) dg[a] = dot;
+    for (int i = 0; i < R; ++i) {
+      if (row0 + i >= rows) break;
+      const float g = __shfl_sync(0xffffffffu, ga, i);
+      T* dst;
+      if constexpr (PEER) {
+        const int o = __shfl_sync(0xffffffffu, owner, i);
+        const size_t pr = __shfl_sync(0xffffffffu, (unsigned long long)prow, i);
+        dst = peer[o] + pr * d;
+      } else {
+        dst = dSend + (size_t)(row0 + i) * d;
+      }
+      float dot = 0.f;
+#pragma unroll
+      for (int j = 0; j < NL; ++j) {
+        const int v = lane + 32 * j;
+        if (v >= nv) continue;
+        float x[V], y[V];
+        load16(&by[i][j], x, (const T*)nullptr);
+        load16(&bo[i][j], y, (const T*)nullptr);
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          dot = fmaf(x[u], y[u], dot);
+          x[u] *= g;
+        }
+        store16(dst + v * V, x, (T*)nullptr);
+      }
+#pragma unroll
+      for (int o2 = 16; o2; o2 >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o2);
+      if (lane == 0 && ai[i] >= 0) dg[ai[i]] = dot;
+    }
+  }
 }
 
 // kept[o*El + el] (this source's counts for owner o's experts) -> owner's recv_kept[me*El + el]
@@ -256,40 +340,94 @@ inline int blocks_for_warps(long long warps, int threads = 256) {
     }                                               \
   } while (0)
 
-void launch_permute(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
-                    int Cm, void* Send, cudaStream_t s) {
+// vectors per lane per row, rounded up to an instantiated width (0 = strided loop)
+inline int nvl_of(int d, int dtype) {
+  const int nv = d / (dtype == 0 ? 4 : 8);
+  const int need = (nv + 31) / 32;
+  if (need <= 4) return need < 1 ? 1 : need;
+  if (need <= 6) return 6;
+  if (need <= 8) return 8;
+  return 0;
+}
+
+// rows handled by one warp for a given NVL (must match the kernels' R)
+inline int rows_per_warp(int nvl, int loads_per_row) {
+  if (nvl == 0) return 1;
+  const int per = nvl * loads_per_row;
+  return per >= kLoadsPerLane ? 1 : kLoadsPerLane / per;
+}
+
+#define LINA_DISPATCH_NVL(nvl, ...)             \
+  do {                                          \
+    switch (nvl) {                              \
+      case 1: { constexpr int NV_ = 1; __VA_ARGS__; } break; \
+      case 2: { constexpr int NV_ = 2; __VA_ARGS__; } break; \
+      case 3: { constexpr int NV_ = 3; __VA_ARGS__; } break; \
+      case 4: { constexpr int NV_ = 4; __VA_ARGS__; } break; \
+      case 6: { constexpr int NV_ = 6; __VA_ARGS__; } break; \
+      case 8: { constexpr int NV_ = 8; __VA_ARGS__; } break; \
+      default: { constexpr int NV_ = 0; __VA_ARGS__; } break; \
+    }                                           \
+  } while (0)
+
+template <bool PEER>
+static void permute_any(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
+                        int Cm, int El, int P, int me, void* Send, void* const* peer, cudaStream_t s) {
   const long long rows = (long long)n * E * Cm;
   if (rows == 0) return;
-  LINA_DISPATCH_T(dtype, permute_kernel<ET><<<blocks_for_warps(rows), 256, 0, s>>>(
-                             (const ET*)X, tok_of, k, d, E, C, n, Cm, (ET*)Send));
+  const int nvl = nvl_of(d, dtype);
+  const long long warps = (rows + rows_per_warp(nvl, 1) - 1) / rows_per_warp(nvl, 1);
+  LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (permute_kernel<ET, NV_, PEER><<<blocks_for_warps(warps), 256, 0, s>>>(
+                             (const ET*)X, tok_of, k, d, E, C, n, Cm, El, P, me, (ET*)Send,
+                             (ET* const*)peer))));
   LINA_LAUNCH_CHECK();
+}
+
+void launch_permute(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
+                    int Cm, void* Send, cudaStream_t s) {
+  permute_any<false>(dtype, X, tok_of, k, d, E, C, n, Cm, 0, 1, 0, Send, nullptr, s);
 }
 
 void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot, const float* gate,
                     int T, int k, int d, int E, int C, int n, int Cm, void* Y, cudaStream_t s) {
   if (T <= 0) return;
-  LINA_DISPATCH_T(dtype, combine_kernel<ET><<<blocks_for_warps(T), 256, 0, s>>>(
-                             (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y));
+  const int nvl = nvl_of(d, dtype);
+  const int U = nvl > 0 ? kLoadsPerLane / nvl : 0;
+  if (nvl > 0 && (k == 1 || k == 2) && U >= 1) {
+    const int tp = U / k > 0 ? U / k : 1;
+    const long long warps = (T + tp - 1) / tp;
+    if (k == 1)
+      LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (combine_kernel<ET, NV_, 1><<<blocks_for_warps(warps), 256, 0, s>>>(
+                                 (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y))));
+    else
+      LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (combine_kernel<ET, NV_, 2><<<blocks_for_warps(warps), 256, 0, s>>>(
+                                 (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y))));
+  } else {
+    LINA_DISPATCH_T(dtype, combine_loop_kernel<ET><<<blocks_for_warps(T), 256, 0, s>>>(
+                               (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y));
+  }
+  LINA_LAUNCH_CHECK();
+}
+
+template <bool PEER>
+static void combine_bwd_any(int dtype, const void* dY, const void* Recv, const int* tok_of, const float* gate,
+                            int T, int k, int d, int E, int C, int n, int Cm, int El, int P, int me,
+                            void* dSend, void* const* peer, float* dg, cudaStream_t s) {
+  if (T > 0) LINA_CUDA_CHECK(cudaMemsetAsync(dg, 0, sizeof(float) * (size_t)T * k, s));
+  const long long rows = (long long)n * E * Cm;
+  if (rows == 0) return;
+  const int nvl = nvl_of(d, dtype);
+  const long long warps = (rows + rows_per_warp(nvl, 2) - 1) / rows_per_warp(nvl, 2);
+  LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (combine_bwd_kernel<ET, NV_, PEER><<<blocks_for_warps(warps), 256, 0, s>>>(
+                             (const ET*)dY, (const ET*)Recv, tok_of, gate, k, d, E, C, n, Cm, El, P, me,
+                             (ET*)dSend, (ET* const*)peer, dg))));
   LINA_LAUNCH_CHECK();
 }
 
 void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* tok_of,
                         const float* gate, int T, int k, int d, int E, int C, int n, int Cm,
                         void* dSend, float* dg, cudaStream_t s) {
-  if (T > 0) LINA_CUDA_CHECK(cudaMemsetAsync(dg, 0, sizeof(float) * (size_t)T * k, s));
-  const long long rows = (long long)n * E * Cm;
-  if (rows == 0) return;
-  LINA_DISPATCH_T(dtype, combine_bwd_kernel<ET><<<blocks_for_warps(rows), 256, 0, s>>>(
-                             (const ET*)dY, (const ET*)Recv, tok_of, gate, k, d, E, C, n, Cm,
-                             (ET*)dSend, dg));
-  LINA_LAUNCH_CHECK();
-}
-
-void launch_gate_bwd(const float* probs, const int* idx, const float* gate, const float* dg, int T,
-                     int k, int E, float* dL, cudaStream_t s) {
-  if (T <= 0) return;
-  gate_bwd_kernel<<<blocks_for_warps(T), 256, 0, s>>>(probs, idx, gate, dg, T, k, E, dL);
-  LINA_LAUNCH_CHECK();
+  combine_bwd_any<false>(dtype, dY, Recv, tok_of, gate, T, k, d, E, C, n, Cm, 0, 1, 0, dSend, nullptr, dg, s);
 }
 
 void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d,
@@ -297,23 +435,14 @@ void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int*
                          void* const* peer_counts, cudaStream_t s) {
   counts_peer_kernel<<<1, 128, 0, s>>>(kept, El, P, me, (int* const*)peer_counts);
   LINA_LAUNCH_CHECK();
-  const long long rows = (long long)n * E * Cm;
-  if (rows == 0) return;
-  LINA_DISPATCH_T(dtype, permute_peer_kernel<ET><<<blocks_for_warps(rows), 256, 0, s>>>(
-                             (const ET*)X, tok_of, k, d, E, C, n, Cm, El, P, me, (ET* const*)peer_rows));
-  LINA_LAUNCH_CHECK();
+  permute_any<true>(dtype, X, tok_of, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows, s);
 }
 
 void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of,
                              const float* gate, int T, int k, int d, int E, int C, int n, int Cm, int El,
                              int P, int me, void* const* peer_rows, float* dg, cudaStream_t s) {
-  if (T > 0) LINA_CUDA_CHECK(cudaMemsetAsync(dg, 0, sizeof(float) * (size_t)T * k, s));
-  const long long rows = (long long)n * E * Cm;
-  if (rows == 0) return;
-  LINA_DISPATCH_T(dtype, combine_bwd_peer_kernel<ET><<<blocks_for_warps(rows), 256, 0, s>>>(
-                             (const ET*)dY, (const ET*)Recv, tok_of, gate, k, d, E, C, n, Cm, El, P, me,
-                             (ET* const*)peer_rows, dg));
-  LINA_LAUNCH_CHECK();
+  combine_bwd_any<true>(dtype, dY, Recv, tok_of, gate, T, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows,
+                        dg, s);
 }
 
 }  // namespace lina

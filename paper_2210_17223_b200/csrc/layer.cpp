@@ -71,7 +71,6 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
   p.w_D = (p.P > 1) ? take(send_rows * p.d * p.dt) : 0;       // send buffer (P=1: = R)
   p.w_O = (p.P > 1) ? take(recv_rows * p.d * p.dt) : 0;       // expert outputs (P=1: = C)
   p.w_dg = take(4 * T * k);
-  p.w_dL = take(4 * T * E);
   p.w_dwg = take(4 * dwg_scratch_floats(p.T, p.d, p.E));
   p.w_dS = take(send_rows * p.d * p.dt);                      // g·dY rows, send layout
   p.w_dO = (p.P > 1) ? take(recv_rows * p.d * p.dt) : 0;      // (P=1: = dS)
@@ -87,7 +86,7 @@ namespace {
 struct Ptrs {
   float* probs; int* idx; float* gate; int* slot; int* kept; int* tok_of; int* recv_kept;
   int* vcount; int* mtp; char* R; char* H; char* Cb; uint64_t* mask;
-  int* route; char* D; char* O; float* dg; float* dL; float* dwg; char* dS; char* dO; char* dH;
+  int* route; char* D; char* O; float* dg; float* dwg; char* dS; char* dO; char* dH;
   char* dXe; char* dXs;
 };
 
@@ -115,7 +114,6 @@ Ptrs carve(const Plan& p, void* saved, void* ws) {
     q.D = p.P > 1 ? w + p.w_D : q.R;
     q.O = p.P > 1 ? w + p.w_O : q.Cb;
     q.dg = (float*)(w + p.w_dg);
-    q.dL = (float*)(w + p.w_dL);
     q.dwg = (float*)(w + p.w_dwg);
     q.dS = w + p.w_dS;
     q.dO = p.P > 1 ? w + p.w_dO : q.dS;
@@ -427,11 +425,12 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   launch_expert_wgrad(dtype, wg2, s);
   launch_expert_wgrad(dtype, wg1, s);
   prof_end(cm, s, 2 * n + 2);
+  // dWg needs only this rank's dg: it overlaps the last returning expert gradients
+  launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, p.E, p.k, q.dwg, dgate_w, s);
   wait_all(cm, s, CeTransport::kReadyBwdC, seq);
   if (cm->sched) sched_a2a_end(cm, s);
-  launch_gate_bwd(q.probs, q.idx, q.gate, q.dg, p.T, p.k, p.E, q.dL, s);
-  launch_dx(dtype, q.dXs, q.idx, q.slot, q.dL, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm, dtokens, s);
-  launch_dwg(dtype, tokens, q.dL, p.T, p.d, p.E, q.dwg, dgate_w, s);
+  launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm,
+            dtokens, s);
 }
 
 }  // namespace
@@ -618,6 +617,7 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
   if (cm->sched) sched_a2a_imminent(cm);
   WGrad wg2{q.dO, q.H, dw2, q.vcount, n, p.P, p.El, p.Cm, p.d, p.f};
   WGrad wg1{q.dH, q.R, dw1, q.vcount, n, p.P, p.El, p.Cm, p.f, p.d};
+  bool dwg_done = false;
   if (ce) {
     for (int r = 0; r < p.P; ++r)
       if (r != cm->rank) cm->ce->post_flag(s, r, CeTransport::kReadyBwdD, cm->rank, 0, seq);
@@ -664,13 +664,17 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
     launch_expert_wgrad(dtype, wg2, s);
     launch_expert_wgrad(dtype, wg1, s);
     prof_end(cm, s, 2);
+    // (e)+(f) dWg needs only this rank's dg: it overlaps the last combine all-to-all
+    launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, p.E, p.k, q.dwg, dgate_w, s);
     LINA_CUDA_CHECK(cudaEventRecord(e_wg, s));
     LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_end, 0));
+    dwg_done = true;
   }
-  // (e)+(f): gate backward, gather-sum dX, dWg
-  launch_gate_bwd(q.probs, q.idx, q.gate, q.dg, p.T, p.k, p.E, q.dL, s);
-  launch_dx(dtype, q.dXs, q.idx, q.slot, q.dL, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm, dtokens, s);
-  launch_dwg(dtype, tokens, q.dL, p.T, p.d, p.E, q.dwg, dgate_w, s);
+  if (!dwg_done)
+    launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, p.E, p.k, q.dwg, dgate_w, s);
+  // (e)+(f): gate backward + gather-sum dX
+  launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm,
+            dtokens, s);
 }
 
 }  // namespace lina
