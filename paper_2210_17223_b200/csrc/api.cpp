@@ -178,15 +178,18 @@ lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned 
       if (nccl_max_ctas > 0) cfg3.maxCTAs = nccl_max_ctas;
       LINA_NCCL_CHECK(ncclCommSplit(cm->ep_disp, 0, rank, &cm->dp, &cfg3));
       cm->sched = sched_create(cm);
-      // Training all-to-all transport: copy engines over NVLink (zero SMs, ce.cpp) unless
-      // LINA_TRANSPORT=nccl; NCCL kernels running beside the persistent expert GEMM need
-      // SMs left free for them.
+      // Training all-to-all transport (LINA_TRANSPORT): "fused" (default) = peer stores from
+      // the permute / combine-backward kernels and the GEMM epilogues; "ce" = copy engines
+      // over NVLink (zero SMs, ce.cpp); "nccl" = ncclAlltoAll micro-ops, whose kernels run
+      // beside the persistent expert GEMM and need SMs left free for them.
       const char* tr = getenv("LINA_TRANSPORT");
       const std::string t = tr ? tr : "fused";
       cm->transport = t == "nccl" ? 0 : (t == "ce" ? 1 : 2);
       if (cm->transport > 0) cm->ce = new CeTransport(cm);
       tc_set_reserved_sms(cm->ce ? 0 : (nccl_max_ctas > 0 ? 2 * nccl_max_ctas : 16));
     }
+    const char* trv = getenv("LINA_TRACE");
+    if (trv && atoi(trv) > 0) cm->trace = trace_create();
     *out = cm;
     return LINA_OK;
   });
@@ -196,6 +199,7 @@ lina_status lina_comm_destroy(lina_comm* cm) {
   return guarded([&] {
     if (!cm) return LINA_OK;
     cudaSetDevice(cm->device);
+    trace_destroy(cm);
     if (cm->sched) sched_destroy(cm->sched);
     cm->sched = nullptr;
     delete cm->ce;

@@ -58,6 +58,10 @@ Plan make_plan(const lina_moe_desc& desc, int world);
 
 }  // namespace lina
 
+namespace lina {
+struct Trace;
+}
+
 struct lina_comm {
   int rank = 0, world = 1, device = 0, num_sms = 148;
   ncclComm_t ep_disp = nullptr;  // dispatch-direction all-to-all micro-ops
@@ -76,6 +80,7 @@ struct lina_comm {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_gemm;  // recorded (start, end) pairs
   std::vector<cudaEvent_t> prof_pool;                          // free timing events
   int64_t prof_gemm_launches = 0;
+  lina::Trace* trace = nullptr;  // LINA_TRACE=1 phase trace (trace.cpp), diagnostics only
   // pinned host scratch for the inference control plane (counts D2H, tables H2D)
   int* pinned = nullptr;
   size_t pinned_bytes = 0;
@@ -85,4 +90,9 @@ namespace lina {
 // Profiling helpers (api.cpp): open/close one timed expert-GEMM phase on stream s.
 void prof_begin(lina_comm* cm, cudaStream_t s);
 void prof_end(lina_comm* cm, cudaStream_t s, int gemm_launches);
+// Phase trace (trace.cpp): no-ops unless the comm was created with LINA_TRACE=1.
+Trace* trace_create();
+void trace_mark(lina_comm* cm, cudaStream_t s, const char* label);
+void trace_flush(lina_comm* cm);
+void trace_destroy(lina_comm* cm);
 }  // namespace lina

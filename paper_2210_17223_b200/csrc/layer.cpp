@@ -318,6 +318,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   const int dtype = 1, P = p.P, me = cm->rank, n = p.n;
   const uint32_t seq = ++ce.seq_fwd;
   const bool override_r = route && route->override_routing;
+  trace_mark(cm, s, "fwd:start");
   post_all(cm, s, CeTransport::kFreeFwd, seq);  // my R, recv counts and Cb may be overwritten
   if (override_r) {
     LINA_CUDA_CHECK(cudaMemcpyAsync(q.idx, route->idx, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
@@ -326,11 +327,14 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   launch_gate_topk(dtype, tokens, gate_w, p.T, p.d, p.E, p.k, override_r ? 0 : 1, q.probs, q.idx, q.gate, s);
   launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr, q.kept,
                q.tok_of, s);
+  trace_mark(cm, s, "gate+route");
   void* const* peer_R = ce.dev_ptrs(saved, p.s_R, s);
   void* const* peer_cnt = ce.dev_ptrs(saved, p.s_recvkept, s);
   wait_all(cm, s, CeTransport::kFreeFwd, seq);
+  trace_mark(cm, s, "wait FREE");
   launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me, peer_R,
                       peer_cnt, s);
+  trace_mark(cm, s, "permute(peer)");
   post_all(cm, s, CeTransport::kReadyFwdD, seq);
   if (route) {
     if (route->idx && !override_r)
@@ -343,8 +347,10 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
       LINA_CUDA_CHECK(cudaMemcpyAsync(route->probs, q.probs, 4 * (size_t)p.T * p.E, cudaMemcpyDeviceToDevice, s));
   }
   wait_all(cm, s, CeTransport::kReadyFwdD, seq);
+  trace_mark(cm, s, "wait READY(disp)");
   launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
   launch_mtile_prefix(q.vcount, n, P * p.El, tc_tile_rows(), q.mtp, s);
+  trace_mark(cm, s, "vcount");
   const auto& ps_saved = ce.peers(saved, s);
   std::vector<char*> cb(P);
   for (int r = 0; r < P; ++r) cb[r] = ps_saved[r] + p.s_C;
@@ -358,6 +364,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
     row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask);
+    trace_mark(cm, s, "gemm1");
     RowGemm g{};
     g.mtp = q.mtp + (size_t)c * (P * p.El + 1);
     g.A = q.H;
@@ -371,11 +378,14 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
     g.N = p.d;
     g.K = p.f;
     launch_row_gemm_tc_peer(g, true, kEpiNone, st, s);  // combine all-to-all in the epilogue
+    trace_mark(cm, s, "gemm2(peer)");
   }
   prof_end(cm, s, 2 * n);
   post_all(cm, s, CeTransport::kReadyFwdC, seq);
   wait_all(cm, s, CeTransport::kReadyFwdC, seq);
+  trace_mark(cm, s, "wait READY(comb)");
   launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, out, s);
+  trace_mark(cm, s, "combine");
 }
 
 void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dout, const void* tokens,
@@ -384,14 +394,18 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   CeTransport& ce = *cm->ce;
   const int dtype = 1, P = p.P, me = cm->rank, n = p.n;
   const uint32_t seq = ++ce.seq_bwd;
+  trace_mark(cm, s, "bwd:start");
   post_all(cm, s, CeTransport::kFreeBwd, seq);  // my dO and dXs may be overwritten
   void* const* peer_dO = ce.dev_ptrs(ws, p.w_dO, s);
   if (cm->sched) sched_a2a_imminent(cm);
   wait_all(cm, s, CeTransport::kFreeBwd, seq);
+  trace_mark(cm, s, "wait FREE");
   launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me,
                           peer_dO, q.dg, s);
+  trace_mark(cm, s, "combine_bwd(peer)");
   post_all(cm, s, CeTransport::kReadyBwdD, seq);
   wait_all(cm, s, CeTransport::kReadyBwdD, seq);
+  trace_mark(cm, s, "wait READY(disp)");
   const auto& ps_ws = ce.peers(ws, s);
   std::vector<char*> dxs(P);
   for (int r = 0; r < P; ++r) dxs[r] = ps_ws[r] + p.w_dXs;
@@ -405,6 +419,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
     row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask);
+    trace_mark(cm, s, "dgrad1");
     RowGemm g{};
     g.mtp = q.mtp + (size_t)c * (P * p.El + 1);
     g.A = q.dH;
@@ -418,6 +433,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
     g.N = p.d;
     g.K = p.f;
     launch_row_gemm_tc_peer(g, false, kEpiNone, st, s);  // combine all-to-all in the epilogue
+    trace_mark(cm, s, "dgrad2(peer)");
   }
   post_all(cm, s, CeTransport::kReadyBwdC, seq);
   WGrad wg2{q.dO, q.H, dw2, q.vcount, n, P, p.El, p.Cm, p.d, p.f};
@@ -425,12 +441,16 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   launch_expert_wgrad(dtype, wg2, s);
   launch_expert_wgrad(dtype, wg1, s);
   prof_end(cm, s, 2 * n + 2);
+  trace_mark(cm, s, "wgrad x2");
   // dWg needs only this rank's dg: it overlaps the last returning expert gradients
   launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, p.E, p.k, q.dwg, dgate_w, s);
+  trace_mark(cm, s, "dwg");
   wait_all(cm, s, CeTransport::kReadyBwdC, seq);
+  trace_mark(cm, s, "wait READY(comb)");
   if (cm->sched) sched_a2a_end(cm, s);
   launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm,
             dtokens, s);
+  trace_mark(cm, s, "dx");
 }
 
 }  // namespace
@@ -438,6 +458,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
 void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* gate_w,
                  const void* w1, const void* w2, void* out, void* saved, void* ws,
                  lina_route* route, cudaStream_t s) {
+  trace_flush(cm);
   Ptrs q = carve(p, saved, ws);
   const int dtype = p.bf16 ? 1 : 0;
   const bool override_r = route && route->override_routing;
@@ -572,6 +593,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
 void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* dout,
                   const void* tokens, const float* gate_w, const void* w1, const void* w2,
                   void* dtokens, float* dgate_w, void* dw1, void* dw2, void* ws, cudaStream_t s) {
+  trace_flush(cm);
   Ptrs q = carve(p, const_cast<void*>(saved), ws);
   const int dtype = p.bf16 ? 1 : 0;
   const int n = p.n;
