@@ -72,9 +72,9 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s);
 
 // fused dispatch over NVLink peer stores (permute.cu): rows go straight into the owners'
 // receive buffers (peer_rows[o]) and the counts into their recv_kept (peer_counts[o]).
-void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d,
-                         int E, int C, int n, int Cm, int El, int P, int me, void* const* peer_rows,
-                         void* const* peer_counts, cudaStream_t s);
+void launch_counts_peer(const int* kept, int El, int P, int me, void* const* peer_counts, cudaStream_t s);
+void launch_permute_peer(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
+                         int Cm, int El, int P, int me, void* const* peer_rows, cudaStream_t s);
 void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of,
                              const float* gate, int T, int k, int d, int E, int C, int n, int Cm, int El,
                              int P, int me, void* const* peer_rows, float* dg, cudaStream_t s);

@@ -430,11 +430,13 @@ void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* 
   combine_bwd_any<false>(dtype, dY, Recv, tok_of, gate, T, k, d, E, C, n, Cm, 0, 1, 0, dSend, nullptr, dg, s);
 }
 
-void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d,
-                         int E, int C, int n, int Cm, int El, int P, int me, void* const* peer_rows,
-                         void* const* peer_counts, cudaStream_t s) {
+void launch_counts_peer(const int* kept, int El, int P, int me, void* const* peer_counts, cudaStream_t s) {
   counts_peer_kernel<<<1, 128, 0, s>>>(kept, El, P, me, (int* const*)peer_counts);
   LINA_LAUNCH_CHECK();
+}
+
+void launch_permute_peer(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
+                         int Cm, int El, int P, int me, void* const* peer_rows, cudaStream_t s) {
   permute_any<true>(dtype, X, tok_of, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows, s);
 }
 

@@ -332,8 +332,9 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   void* const* peer_cnt = ce.dev_ptrs(saved, p.s_recvkept, s);
   wait_all(cm, s, CeTransport::kFreeFwd, seq);
   trace_mark(cm, s, "wait FREE");
-  launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me, peer_R,
-                      peer_cnt, s);
+  launch_counts_peer(q.kept, p.El, P, me, peer_cnt, s);
+  trace_mark(cm, s, "counts(peer)");
+  launch_permute_peer(dtype, tokens, q.tok_of, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me, peer_R, s);
   trace_mark(cm, s, "permute(peer)");
   post_all(cm, s, CeTransport::kReadyFwdD, seq);
   if (route) {

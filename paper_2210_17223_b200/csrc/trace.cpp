@@ -2,6 +2,7 @@
 // stream at phase boundaries; the deltas between consecutive marks of one call are
 // accumulated (resolved lazily at the next call) and printed per rank at comm destroy.
 // Off by default; never on a timed path of bench.py.
+#include <algorithm>
 #include <cstdio>
 #include <map>
 #include <string>
@@ -16,7 +17,7 @@ struct Trace {
   using Group = std::vector<std::pair<std::string, cudaEvent_t>>;  // the marks of one call
   std::vector<Group> groups;
   std::vector<cudaEvent_t> pool;
-  std::map<std::string, std::pair<double, long>> acc;
+  std::map<std::string, std::vector<float>> acc;
   std::vector<std::string> order;
 };
 
@@ -45,10 +46,9 @@ static void accumulate(Trace* t, Trace::Group& g) {
     auto it = t->acc.find(key);
     if (it == t->acc.end()) {
       t->order.push_back(key);
-      t->acc[key] = {ms, 1};
+      t->acc[key] = {ms};
     } else {
-      it->second.first += ms;
-      it->second.second += 1;
+      it->second.push_back(ms);
     }
   }
   for (auto& pe : g) t->pool.push_back(pe.second);
@@ -85,9 +85,10 @@ void trace_destroy(lina_comm* cm) {
   } catch (...) {
   }
   for (const auto& k : t->order) {
-    const auto& v = t->acc[k];
-    std::fprintf(stderr, "[lina trace rank %d] %-36s %9.2f us avg over %ld\n", cm->rank, k.c_str(),
-                 1e3 * v.first / v.second, v.second);
+    std::vector<float> v = t->acc[k];
+    std::sort(v.begin(), v.end());
+    std::fprintf(stderr, "[lina trace rank %d] %-36s median %8.2f us  min %8.2f  max %9.2f  (n=%zu)\n", cm->rank,
+                 k.c_str(), 1e3 * v[v.size() / 2], 1e3 * v.front(), 1e3 * v.back(), v.size());
   }
   for (auto e : t->pool) cudaEventDestroy(e);
   delete t;
