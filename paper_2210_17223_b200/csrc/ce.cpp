@@ -88,6 +88,9 @@ CeTransport::CeTransport(lina_comm* cm) : cm_(cm), impl_(new Impl) {
   LINA_CUDA_CHECK(cudaMalloc(&flags_, nflags_ * sizeof(uint32_t)));
   LINA_CUDA_CHECK(cudaMemset(flags_, 0, nflags_ * sizeof(uint32_t)));
   LINA_CUDA_CHECK(cudaMalloc(&impl_->stage, 128 * (size_t)P));
+  LINA_CUDA_CHECK(cudaMalloc(&done_, kDoneSites * sizeof(unsigned int)));
+  LINA_CUDA_CHECK(cudaMemset(done_, 0, kDoneSites * sizeof(unsigned int)));
+  peer_slots_.assign(kKinds, nullptr);
   peer_flags_ = map_collective(flags_, cm->hi);
   for (int r = 0; r < P; ++r) {
     cudaStream_t a, b;
@@ -111,6 +114,9 @@ CeTransport::~CeTransport() {
   for (auto s : comb_) cudaStreamDestroy(s);
   for (auto e : events_) cudaEventDestroy(e);
   if (flags_) cudaFree(flags_);
+  if (done_) cudaFree(done_);
+  for (auto p : peer_slots_)
+    if (p) cudaFree(p);
   if (impl_->stage) cudaFree(impl_->stage);
   delete impl_;
 }
@@ -166,6 +172,18 @@ const std::vector<char*>& CeTransport::peers(const void* local, cudaStream_t s) 
   auto it = impl_->maps.find(local);
   if (it != impl_->maps.end()) return it->second;
   return impl_->maps[local] = map_collective(local, s);
+}
+
+uint32_t* const* CeTransport::peer_slots(int kind) {
+  if (peer_slots_[kind]) return peer_slots_[kind];
+  const int P = cm_->world;
+  std::vector<uint32_t*> v(P);
+  for (int r = 0; r < P; ++r) v[r] = (uint32_t*)peer_flags_[r] + slot(kind, cm_->rank, 0);
+  void* d = nullptr;
+  LINA_CUDA_CHECK(cudaMalloc(&d, sizeof(uint32_t*) * P));
+  LINA_CUDA_CHECK(cudaMemcpy(d, v.data(), sizeof(uint32_t*) * P, cudaMemcpyHostToDevice));
+  peer_slots_[kind] = (uint32_t**)d;
+  return peer_slots_[kind];
 }
 
 void CeTransport::wait_flag(cudaStream_t s, int kind, int peer, int chunk, uint32_t value) {

@@ -1,5 +1,6 @@
 // Copy-engine all-to-all transport (ce.cpp).
 #pragma once
+#include <map>
 #include <string>
 #include <vector>
 
@@ -29,12 +30,21 @@ class CeTransport {
   // Device array of P tensor maps, one per rank's buffer (cached by key; built by
   // `build` on first use, uploaded once).
   const void* dev_blob(const std::string& key, const std::vector<unsigned char>& bytes, cudaStream_t s);
+  // In-kernel signalling (signal.h): my slots of `kind` (peer r at r * kMaxChunks), the
+  // device array [P] of every rank's slot (kind, me) mapped here (uploaded once), and a
+  // zeroed CTA-completion counter per call site (sites < kDoneSites).
+  const uint32_t* slots(int kind) const { return flags_ + slot(kind, 0, 0); }
+  uint32_t* const* peer_slots(int kind);
+  unsigned int* done_counter(int site) const { return done_ + site; }
+  static constexpr int kDoneSites = 16;
   cudaStream_t disp_stream(int peer) const { return disp_[peer]; }
   cudaStream_t comb_stream(int peer) const { return comb_[peer]; }
   // event pool: [which (0..3)][peer][chunk or kMaxChunks(+1)]
   cudaEvent_t ev(int which, int peer, int chunk) const {
     return events_[((size_t)which * cm_->world + peer) * (kMaxChunks + 2) + chunk];
   }
+  // host-side cache of per-rank tensor-map arrays (fused transport epilogue stores)
+  std::map<std::string, std::vector<unsigned char>> host_blobs;
   uint32_t seq_fwd = 0, seq_bwd = 0;
   // rounds that ran the copy-engine pipeline (its PULLED flags carry these values)
   uint32_t last_ce_fwd = 0, last_ce_bwd = 0, prev_ce_fwd = 0, prev_ce_bwd = 0;
@@ -49,6 +59,8 @@ class CeTransport {
   Impl* impl_;
   uint32_t* flags_ = nullptr;
   size_t nflags_ = 0;
+  unsigned int* done_ = nullptr;
+  std::vector<uint32_t**> peer_slots_;
   std::vector<char*> peer_flags_;
   std::vector<cudaStream_t> disp_, comb_;
   std::vector<cudaEvent_t> events_;

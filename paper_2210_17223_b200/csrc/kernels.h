@@ -6,6 +6,8 @@
 
 #include <vector>
 
+#include "signal.h"
+
 namespace lina {
 
 enum { kEpiNone = 0, kEpiRelu = 1, kEpiMask = 2 };
@@ -23,6 +25,7 @@ struct RowGemm {
   int B_experts = 0;                // expert matrices in B (0 = El)
   uint64_t* mask_out = nullptr;       // tcgen05 ReLU epilogue: ReLU' bits [nseg_total*Cm][N/64]
   const uint64_t* mask_in = nullptr;  // tcgen05 mask epilogue: those bits (aux unused)
+  const PeerSignal* sig = nullptr;    // tcgen05: wait before the first A load, post after the last store
 };
 
 // Weight-gradient GEMM: D[El][M][N] = Σ_{c,s} Σ_{r < v} A[seg][r][:]ᵀ B[seg][r][:].
@@ -34,26 +37,33 @@ struct WGrad {
   int nchunks, P, El, Cm, M, N;
 };
 
+// sig (fused transport): block 0 posts sig at kernel start (the FREE of this round).
 void launch_gate_topk(int dtype, const void* X, const float* Wg, int T, int d, int E, int k,
-                      int write_routing, float* probs, int* idx, float* gate, cudaStream_t s);
+                      int write_routing, float* probs, int* idx, float* gate, cudaStream_t s,
+                      const PeerSignal* sig = nullptr);
 
 size_t route_scratch_ints(int T, int k, int E);
 void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int* slot, int* counts,
                   int* kept, int* tok_of, cudaStream_t s);
 // vcount[(c*P + s)*El + el] = clamp(recv_kept[s*El + el] - b_c, 0, Cc)
-void launch_vcount(const int* recv_kept, int P, int El, int C, int n, int* vcount, cudaStream_t s);
+// sig: every CTA first waits for the peers' counts (READY of the dispatch)
+void launch_vcount(const int* recv_kept, int P, int El, int C, int n, int* vcount, cudaStream_t s,
+                   const PeerSignal* sig = nullptr);
 
 void launch_permute(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
                     int Cm, void* Send, cudaStream_t s);
+// sig: block 0 posts sig.post (FREE of the backward buffers) at start; every CTA waits
+// sig.wait (the returned expert outputs) before reading Recv.
 void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot, const float* gate,
-                    int T, int k, int d, int E, int C, int n, int Cm, void* Y, cudaStream_t s);
+                    int T, int k, int d, int E, int C, int n, int Cm, void* Y, cudaStream_t s,
+                    const PeerSignal* sig = nullptr);
 void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* tok_of,
                         const float* gate, int T, int k, int d, int E, int C, int n, int Cm,
                         void* dSend, float* dg, cudaStream_t s);
 // dX (gather-sum + dL·Wgᵀ) and dWg (Xᵀ dL) with dL recomputed from the forward routing.
 void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* probs,
                const float* gate, const float* dg, const float* Wg, int T, int k, int d, int E, int C,
-               int n, int Cm, void* dX, cudaStream_t s);
+               int n, int Cm, void* dX, cudaStream_t s, const PeerSignal* sig = nullptr);
 size_t dwg_scratch_floats(int T, int d, int E);
 void launch_dwg(int dtype, const void* X, const float* probs, const int* idx, const float* gate,
                 const float* dg, int T, int d, int E, int k, float* scratch, float* dWg, cudaStream_t s);
@@ -72,16 +82,19 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s);
 
 // fused dispatch over NVLink peer stores (permute.cu): rows go straight into the owners'
 // receive buffers (peer_rows[o]) and the counts into their recv_kept (peer_counts[o]).
-void launch_counts_peer(const int* kept, int El, int P, int me, void* const* peer_counts, cudaStream_t s);
-void launch_permute_peer(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
-                         int Cm, int El, int P, int me, void* const* peer_rows, cudaStream_t s);
+// sig: every CTA waits for the peers' FREE, block 0 also stores this rank's counts into
+// the owners' recv_kept (peer_counts[o]), and the last CTA posts READY.
+void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d, int E,
+                         int C, int n, int Cm, int El, int P, int me, void* const* peer_rows,
+                         void* const* peer_counts, const PeerSignal& sig, cudaStream_t s);
 void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of,
                              const float* gate, int T, int k, int d, int E, int C, int n, int Cm, int El,
-                             int P, int me, void* const* peer_rows, float* dg, cudaStream_t s);
+                             int P, int me, void* const* peer_rows, float* dg, const PeerSignal& sig,
+                             cudaStream_t s);
 // Output tiles of a row GEMM stored through per-owner tensor maps (peer memory):
-// segment (c, s, el) of the receive layout goes to dmaps[s] at segment c*E + me*El + el.
+// segment (c, s, el) of the receive layout goes to map s at segment c*E + me*El + el.
 struct PeerStore {
-  const void* dmaps = nullptr;  // device array [P] of CUtensorMap (64-byte aligned)
+  const void* host_maps = nullptr;  // host array [P] of CUtensorMap (tc_peer_dmaps), copied into the launch
   int P = 0, me = 0, E = 0;
 };
 void launch_row_gemm_tc_peer(const RowGemm& g, bool b_kmajor, int epi, const PeerStore& ps, cudaStream_t s);

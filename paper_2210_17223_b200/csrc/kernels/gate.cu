@@ -27,6 +27,7 @@
 
 #include "../common.h"
 #include "../kernels.h"
+#include "../signal.h"
 
 namespace lina {
 namespace {
@@ -130,7 +131,10 @@ __global__ void __launch_bounds__(kGThreads) gate_mma_kernel(const __nv_bfloat16
                                                              int E, int k, int write_routing, int PB,
                                                              float* __restrict__ probs,
                                                              int* __restrict__ idx,
-                                                             float* __restrict__ gate) {
+                                                             float* __restrict__ gate, PeerSignal sig) {
+  // fused transport: this rank's receive buffers are free again (the previous backward,
+  // which read them, is complete in stream order)
+  if (blockIdx.x == 0 && threadIdx.x == 0) sig_post(sig);
   constexpr int LP = NT * 8 + 1;
   constexpr int G = NT <= 2 ? 8 : 4;        // 32-column blocks in flight per lane (2 x 16 B each)
   extern __shared__ __align__(16) unsigned char gsm_raw[];
@@ -337,7 +341,7 @@ void launch_gate_simt(const void* X, const float* Wg, int T, int d, int E, int k
 
 template <int NT>
 void launch_gate_mma(const void* X, const float* Wg, int T, int d, int E, int k, int write_routing,
-                     float* probs, int* idx, float* gate, cudaStream_t s) {
+                     float* probs, int* idx, float* gate, const PeerSignal& sig, cudaStream_t s) {
   const int nkb = d / 32;
   const size_t per_kb = (size_t)3 * NT * 2 * 32 * sizeof(uint2);
   const int PB = (int)std::max<size_t>(1, std::min<size_t>(nkb, kGStageBudget / per_kb));
@@ -348,23 +352,27 @@ void launch_gate_mma(const void* X, const float* Wg, int T, int d, int E, int k,
                                          (int)smem));
     set = smem;
   }
-  const int blocks = (T + kGTok - 1) / kGTok;
+  const int blocks = std::max(1, (T + kGTok - 1) / kGTok);  // T = 0: one CTA still posts the signal
   gate_mma_kernel<NT><<<blocks, kGThreads, smem, s>>>((const __nv_bfloat16*)X, Wg, T, d, E, k, write_routing,
-                                                      PB, probs, idx, gate);
+                                                      PB, probs, idx, gate, sig);
 }
 
 }  // namespace
 
 void launch_gate_topk(int dtype, const void* X, const float* Wg, int T, int d, int E, int k,
-                      int write_routing, float* probs, int* idx, float* gate, cudaStream_t s) {
-  if (T <= 0) return;
-  if (dtype == 1 && d % 32 == 0) {
+                      int write_routing, float* probs, int* idx, float* gate, cudaStream_t s,
+                      const PeerSignal* sig) {
+  const PeerSignal none{};
+  const PeerSignal& sg = sig ? *sig : none;
+  if (dtype == 1 && d % 32 == 0 && (T > 0 || sig)) {
     const int nt = (E + 7) / 8;
-    if (nt <= 1) launch_gate_mma<1>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
-    else if (nt <= 2) launch_gate_mma<2>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
-    else if (nt <= 4) launch_gate_mma<4>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
-    else launch_gate_mma<8>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);
+    if (nt <= 1) launch_gate_mma<1>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, sg, s);
+    else if (nt <= 2) launch_gate_mma<2>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, sg, s);
+    else if (nt <= 4) launch_gate_mma<4>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, sg, s);
+    else launch_gate_mma<8>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, sg, s);
   } else {
+    if (sig) throw CudaError{"launch_gate_topk: peer signal needs the bf16 tensor-core gate"};
+    if (T <= 0) return;
     auto go = [&](auto tag) {
       using TIn = decltype(tag);
       if (E <= 8) launch_gate_simt<TIn, 8>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, s);

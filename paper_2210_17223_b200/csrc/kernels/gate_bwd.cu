@@ -24,6 +24,7 @@
 //       float atomics).
 #include "../common.h"
 #include "../kernels.h"
+#include "../signal.h"
 
 namespace lina {
 namespace {
@@ -91,8 +92,11 @@ __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe
                                                        const float* __restrict__ gate,
                                                        const float* __restrict__ dg,
                                                        const float* __restrict__ Wg, int Tn, int k, int d,
-                                                       int E, int C, int n, int Cm, T* __restrict__ dX) {
+                                                       int E, int C, int n, int Cm, T* __restrict__ dX,
+                                                       PeerSignal sig) {
   extern __shared__ float dsm[];
+  if (threadIdx.x == 0) sig_wait(sig);  // fused transport: the expert input-gradients have landed
+  __syncthreads();
   float* sW = dsm;                     // [E][kDxCols]
   float* sL = dsm + E * kDxCols;       // [kDxTok][E]
   constexpr int NV = sizeof(T) == 2 ? 1 : 2;  // 16-byte vectors per 8 columns
@@ -352,7 +356,7 @@ size_t dwg_scratch_floats(int T, int d, int E) {
 template <typename T, int KT>
 static void launch_dx_t(const void* dXe, const int* idx, const int* slot, const float* probs,
                         const float* gate, const float* dg, const float* Wg, int Tn, int k, int d, int E,
-                        int C, int n, int Cm, void* dX, cudaStream_t s) {
+                        int C, int n, int Cm, void* dX, const PeerSignal& sig, cudaStream_t s) {
   dim3 grid((d + kDxCols - 1) / kDxCols, (Tn + kDxTok - 1) / kDxTok);
   const size_t smem = sizeof(float) * ((size_t)E * kDxCols + kDxTok * E);
   static bool set = false;
@@ -362,18 +366,19 @@ static void launch_dx_t(const void* dXe, const int* idx, const int* slot, const 
     set = true;
   }
   dx_tiled_kernel<T, KT><<<grid, 256, smem, s>>>((const T*)dXe, idx, slot, probs, gate, dg, Wg, Tn, k, d, E,
-                                                C, n, Cm, (T*)dX);
+                                                C, n, Cm, (T*)dX, sig);
 }
 
 void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* probs,
                const float* gate, const float* dg, const float* Wg, int T, int k, int d, int E, int C,
-               int n, int Cm, void* dX, cudaStream_t s) {
-  if (T <= 0) return;
+               int n, int Cm, void* dX, cudaStream_t s, const PeerSignal* sig) {
+  if (T <= 0) return;  // (a rank without tokens has nothing to wait for either)
+  const PeerSignal sg = sig ? *sig : PeerSignal{};
   auto go = [&](auto tag) {
     using ET = decltype(tag);
-    if (k == 1) launch_dx_t<ET, 1>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, s);
-    else if (k == 2) launch_dx_t<ET, 2>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, s);
-    else launch_dx_t<ET, 0>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, s);
+    if (k == 1) launch_dx_t<ET, 1>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, sg, s);
+    else if (k == 2) launch_dx_t<ET, 2>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, sg, s);
+    else launch_dx_t<ET, 0>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, sg, s);
   };
   if (dtype == 0) go(float{});
   else go(__nv_bfloat16{});

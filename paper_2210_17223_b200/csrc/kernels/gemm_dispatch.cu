@@ -16,8 +16,12 @@ static bool g_force_simt = [] {
 void set_force_simt(bool on) { g_force_simt = on; }
 
 void launch_expert_row_gemm(int dtype, const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s) {
-  if (dtype == 1 && !g_force_simt && tc_row_supported(g)) launch_row_gemm_tc(g, b_kmajor, epi, s);
-  else launch_row_gemm_simt(dtype, g, b_kmajor, epi, s);
+  if (dtype == 1 && !g_force_simt && tc_row_supported(g)) {
+    launch_row_gemm_tc(g, b_kmajor, epi, s);
+  } else {
+    if (g.sig) throw CudaError{"in-kernel peer signals need the tcgen05 GEMM (unset LINA_FORCE_SIMT)"};
+    launch_row_gemm_simt(dtype, g, b_kmajor, epi, s);
+  }
 }
 
 void launch_expert_wgrad(int dtype, const WGrad& g, cudaStream_t s) {

@@ -36,6 +36,7 @@
 
 #include "../common.h"
 #include "../kernels.h"
+#include "../signal.h"
 
 namespace lina {
 namespace tc {
@@ -146,8 +147,9 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const void* 
       : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -254,6 +256,8 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+constexpr int kMaxPeerMaps = 8;
+
 struct TcParams {
   const int* vcount;   // valid rows per segment (global segment index)
   const int* mtp;      // ROW: [nseg+1] prefix of valid row blocks of this launch's segments
@@ -263,20 +267,22 @@ struct TcParams {
   __nv_bfloat16* D;
   const __nv_bfloat16* aux;
   int nchunks, P;      // WGRAD
-  // ROW with peer stores: output tile of segment (c, s, el) goes through dmaps[s] to
+  // ROW with peer stores: output tile of segment (c, s, el) goes through pmaps[s] to
   // segment c*dE + dme*El + el of rank s's buffer (the combine all-to-all fused into
-  // the epilogue); NULL = local store through tmD
-  const CUtensorMap* dmaps;
+  // the epilogue); has_pmaps = 0: local store through tmD
+  int has_pmaps;
   int dP, dme, dE;
   uint64_t* mask_out;       // ROW + ReLU: ReLU' bits of the stored output, [seg*Cm + row][N/64]
   const uint64_t* mask_in;  // ROW + mask epilogue: the bits written by GEMM1
+  PeerSignal sig;           // fused transport: wait before the first A load / post after the last store
+  CUtensorMap pmaps[kMaxPeerMaps];  // kernel-parameter copies (the TMA unit reads them like tmD)
 };
 
 template <int CG, bool WGRAD, bool B_MN, int EPI>
 __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
-                   TcParams p) {
+                   const __grid_constant__ TcParams p) {
   using G = Geo<CG, EPI != kEpiNone>;
   constexpr int STAGES = G::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -297,7 +303,10 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
   // ---- tile space (per cluster)
   const int n_nblk = p.N / BN;
   const int total_tiles = WGRAD ? p.El * (p.M / G::ROWS) * n_nblk : p.mtp[p.nseg] * n_nblk;
-  if (cluster_id >= total_tiles) return;  // uniform for the whole cluster
+  if (cluster_id >= total_tiles) {  // uniform for the whole cluster
+    if (threadIdx.x == 0) sig_post_last(p.sig);  // still counts towards the grid's completion
+    return;
+  }
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -348,6 +357,10 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
   if (warp == 0) {
     // ================= TMA producer (both CTAs load their own halves)
     if (lane == 0) {
+      if (p.sig.wait) {  // fused transport: the peers' rows of A have landed
+        sig_wait(p.sig);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       int stage = 0;
       uint32_t ph = 0;
       const int arow = 128 * rank;          // this CTA's rows within the tile
@@ -485,7 +498,7 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
 #pragma unroll
       for (int j = 0; j < COLS / 64; ++j, ++sub) {
         const int c0 = col0 + j * 64;
-        const int b = sub & 1;
+        const int b = sub % G::EPI_BUFS;
         uint8_t* buf = my_epi + b * 4096;
         const uint32_t rowaddr = smem_u32(buf) + lane * 128;
         uint32_t v[64];
@@ -497,7 +510,7 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 64; ++i) v[i] = 0u;
         }
-        if (lane == 0 && sub >= 2) bulk_wait_read1();  // the store that last used `buf` has read it
+        if (lane == 0 && sub >= G::EPI_BUFS) bulk_wait_read<G::EPI_BUFS - 1>();  // `buf`'s last store has read it
         __syncwarp();
         uint64_t mword = 0;
         const uint64_t min = EPI == kEpiMask ? mk[j] : 0ull;
@@ -534,10 +547,10 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
         if (lane == 0) {
           int x0, x1, x2;
           box_of(t, c0, x0, x1, x2);
-          if (!WGRAD && p.dmaps) {  // fused combine all-to-all: store into the owner's buffer
+          if (!WGRAD && p.has_pmaps) {  // fused combine all-to-all: store into the owner's buffer
             const int seg = x2;
             const int el = seg % p.El, sidx = (seg / p.El) % p.dP, c = seg / (p.El * p.dP);
-            tma_store_3d(p.dmaps + sidx, buf, x0, x1, c * p.dE + p.dme * p.El + el);
+            tma_store_3d(&p.pmaps[sidx], buf, x0, x1, c * p.dE + p.dme * p.El + el);
           } else {
             tma_store_3d(&tmD, buf, x0, x1, x2);
           }
@@ -556,12 +569,16 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
         aph ^= 1;
       }
     }
-    if (lane == 0) bulk_wait_all();
+    if (lane == 0) {
+      bulk_wait_all();
+      if (p.sig.post) asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
   }
   __syncwarp();
   tc_fence_before();
   if (CG == 2) cluster_sync();
   else __syncthreads();
+  if (threadIdx.x == 0) sig_post_last(p.sig);  // the last CTA: every output tile is stored
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, TMEM_COLS);
@@ -729,6 +746,7 @@ static void row_gemm_tc_impl(const RowGemm& g, bool b_kmajor, int epi, const Pee
   p.aux = (const __nv_bfloat16*)g.aux;
   p.mask_out = g.mask_out;
   p.mask_in = g.mask_in;
+  if (g.sig) p.sig = *g.sig;
   if (epi == kEpiMask && !g.mask_in) throw CudaError{"tcgen05 dgrad needs the ReLU' bit mask"};
   const uint64_t ddims[3] = {(uint64_t)g.N, (uint64_t)g.Cm, (uint64_t)nseg_total};
   const uint64_t dstr[2] = {(uint64_t)g.N * 2, (uint64_t)g.Cm * g.N * 2};
@@ -736,7 +754,9 @@ static void row_gemm_tc_impl(const RowGemm& g, bool b_kmajor, int epi, const Pee
   CUtensorMap md = make_map(g.D, 3, ddims, dstr, dbox);
   CUtensorMap mx = (epi == kEpiMask) ? make_map(g.aux, 3, ddims, dstr, dbox) : md;
   if (ps) {
-    p.dmaps = (const CUtensorMap*)ps->dmaps;
+    if (ps->P > kMaxPeerMaps) throw CudaError{"fused transport supports at most 8 ranks"};
+    std::memcpy(p.pmaps, ps->host_maps, sizeof(CUtensorMap) * ps->P);
+    p.has_pmaps = 1;
     p.dP = ps->P;
     p.dme = ps->me;
     p.dE = ps->E;

@@ -15,8 +15,11 @@
 // combine_bwd   : dg_tj = <dY_t, O_tj>,  dSend[row] = g_tj * dY_t  (else 0).
 // (dL, dX and dWg are in gate_bwd.cu.)
 // Rows are moved as 16-byte vectors, one warp per row / token.
+#include <algorithm>
+
 #include "../common.h"
 #include "../kernels.h"
+#include "../signal.h"
 
 namespace lina {
 namespace {
@@ -50,10 +53,9 @@ __device__ __forceinline__ int row_assignment(long long gw, const int* __restric
 // recv row ((c*P + me)*El + e%El)*Cm + r of owner o = e / El, so the permute IS the
 // dispatch all-to-all.
 template <typename T, int NVL, bool PEER>
-__global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ X, const int* __restrict__ tok_of,
-                                                      int k, int d, int E, int C, int n, int Cm, int El,
-                                                      int P, int me, T* __restrict__ Send,
-                                                      T* const* __restrict__ peer) {
+__device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int* __restrict__ tok_of, int k,
+                                             int d, int E, int C, int n, int Cm, int El, int P, int me,
+                                             T* __restrict__ Send, T* const* __restrict__ peer) {
   constexpr int R = NVL == 0 ? 1 : (NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / NVL);
   constexpr int NL = NVL == 0 ? 1 : NVL;
   constexpr int V = 16 / sizeof(T);
@@ -106,6 +108,27 @@ __global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ X, c
   }
 }
 
+template <typename T, int NVL, bool PEER>
+__global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ X, const int* __restrict__ tok_of,
+                                                      int k, int d, int E, int C, int n, int Cm, int El,
+                                                      int P, int me, T* __restrict__ Send,
+                                                      T* const* __restrict__ peer, const int* __restrict__ kept,
+                                                      int* const* __restrict__ peer_counts, PeerSignal sig) {
+  if constexpr (PEER) {
+    // the owners' receive buffers are free (their FREE of this round), then this rank's
+    // counts go to every owner's recv_kept
+    if (threadIdx.x == 0) sig_wait(sig);
+    __syncthreads();
+    if (blockIdx.x == 0)
+      for (int i = threadIdx.x; i < P * El; i += blockDim.x) peer_counts[i / El][me * El + i % El] = kept[i];
+  }
+  permute_rows<T, NVL, PEER>(X, tok_of, k, d, E, C, n, Cm, El, P, me, Send, peer);
+  if constexpr (PEER) {
+    __syncthreads();
+    if (threadIdx.x == 0) sig_post_last(sig);  // the last CTA: READY of the dispatch
+  }
+}
+
 // combine: y_t = Σ_{j kept, ascending} g_tj · Recv[row(t, j)] (fp32 accumulation).  A warp
 // owns TP = U / k tokens (U = kLoadsPerLane / NVL rows in flight); lane q < TP*k resolves
 // pair q, then every row load is issued before the sums.
@@ -113,7 +136,15 @@ template <typename T, int NVL, int KT>
 __global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ Recv, const int* __restrict__ idx,
                                                       const int* __restrict__ slot,
                                                       const float* __restrict__ gate, int Tn, int k, int d,
-                                                      int E, int C, int n, int Cm, T* __restrict__ Y) {
+                                                      int E, int C, int n, int Cm, T* __restrict__ Y,
+                                                      PeerSignal sig) {
+  // fused transport: this rank's backward receive buffers are free again (block 0 posts);
+  // the peers' returned expert outputs have landed (every CTA waits)
+  if (sig.post && blockIdx.x == 0 && threadIdx.x == 0) sig_post(sig);
+  if (sig.wait) {
+    if (threadIdx.x == 0) sig_wait(sig);
+    __syncthreads();
+  }
   constexpr int NL = NVL > 0 ? NVL : 1;  // (NVL = 0 is never launched)
   constexpr int U = kLoadsPerLane / NL;
   constexpr int TP = U / KT > 0 ? U / KT : 1;
@@ -180,7 +211,12 @@ template <typename T>
 __global__ void combine_loop_kernel(const T* __restrict__ Recv, const int* __restrict__ idx,
                                     const int* __restrict__ slot, const float* __restrict__ gate,
                                     int Tn, int k, int d, int E, int C, int n, int Cm,
-                                    T* __restrict__ Y) {
+                                    T* __restrict__ Y, PeerSignal sig) {
+  if (sig.post && blockIdx.x == 0 && threadIdx.x == 0) sig_post(sig);
+  if (sig.wait) {
+    if (threadIdx.x == 0) sig_wait(sig);
+    __syncthreads();
+  }
   const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= Tn) return;
@@ -214,13 +250,11 @@ __global__ void combine_loop_kernel(const T* __restrict__ Recv, const int* __res
 // combine backward over send-layout rows: dg_a = <dY_t, O_row>, dSend[row] = g_a · dY_t
 // (0 for padding rows).  PEER: dSend rows are stored into the owners' receive buffers.
 template <typename T, int NVL, bool PEER>
-__global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ dY, const T* __restrict__ Recv,
-                                                          const int* __restrict__ tok_of,
-                                                          const float* __restrict__ gate, int k, int d,
-                                                          int E, int C, int n, int Cm, int El, int P,
-                                                          int me, T* __restrict__ dSend,
-                                                          T* const* __restrict__ peer,
-                                                          float* __restrict__ dg) {
+__device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const T* __restrict__ Recv,
+                                                 const int* __restrict__ tok_of, const float* __restrict__ gate,
+                                                 int k, int d, int E, int C, int n, int Cm, int El, int P, int me,
+                                                 T* __restrict__ dSend, T* const* __restrict__ peer,
+                                                 float* __restrict__ dg) {
   constexpr int NL = NVL == 0 ? 1 : NVL;
   constexpr int R = NVL == 0 ? 1 : (2 * NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / (2 * NVL));
   constexpr int V = 16 / sizeof(T);
@@ -314,12 +348,22 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ 
   }
 }
 
-// kept[o*El + el] (this source's counts for owner o's experts) -> owner's recv_kept[me*El + el]
-__global__ void counts_peer_kernel(const int* __restrict__ kept, int El, int P, int me,
-                                   int* const* __restrict__ peer) {
-  for (int i = threadIdx.x; i < P * El; i += blockDim.x) {
-    const int o = i / El, el = i % El;
-    peer[o][me * El + el] = kept[i];
+template <typename T, int NVL, bool PEER>
+__global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ dY, const T* __restrict__ Recv,
+                                                          const int* __restrict__ tok_of,
+                                                          const float* __restrict__ gate, int k, int d,
+                                                          int E, int C, int n, int Cm, int El, int P,
+                                                          int me, T* __restrict__ dSend,
+                                                          T* const* __restrict__ peer,
+                                                          float* __restrict__ dg, PeerSignal sig) {
+  if constexpr (PEER) {  // the owners' backward receive buffers are free (their FREE)
+    if (threadIdx.x == 0) sig_wait(sig);
+    __syncthreads();
+  }
+  combine_bwd_rows<T, NVL, PEER>(dY, Recv, tok_of, gate, k, d, E, C, n, Cm, El, P, me, dSend, peer, dg);
+  if constexpr (PEER) {
+    __syncthreads();
+    if (threadIdx.x == 0) sig_post_last(sig);  // the last CTA: READY of the backward dispatch
   }
 }
 
@@ -372,39 +416,43 @@ inline int rows_per_warp(int nvl, int loads_per_row) {
 
 template <bool PEER>
 static void permute_any(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
-                        int Cm, int El, int P, int me, void* Send, void* const* peer, cudaStream_t s) {
+                        int Cm, int El, int P, int me, void* Send, void* const* peer, const int* kept,
+                        void* const* peer_counts, const PeerSignal& sig, cudaStream_t s) {
   const long long rows = (long long)n * E * Cm;
-  if (rows == 0) return;
+  if (rows == 0 && !PEER) return;
   const int nvl = nvl_of(d, dtype);
-  const long long warps = (rows + rows_per_warp(nvl, 1) - 1) / rows_per_warp(nvl, 1);
+  const long long warps = std::max(1LL, (rows + rows_per_warp(nvl, 1) - 1) / rows_per_warp(nvl, 1));
   LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (permute_kernel<ET, NV_, PEER><<<blocks_for_warps(warps), 256, 0, s>>>(
                              (const ET*)X, tok_of, k, d, E, C, n, Cm, El, P, me, (ET*)Send,
-                             (ET* const*)peer))));
+                             (ET* const*)peer, kept, (int* const*)peer_counts, sig))));
   LINA_LAUNCH_CHECK();
 }
 
 void launch_permute(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
                     int Cm, void* Send, cudaStream_t s) {
-  permute_any<false>(dtype, X, tok_of, k, d, E, C, n, Cm, 0, 1, 0, Send, nullptr, s);
+  permute_any<false>(dtype, X, tok_of, k, d, E, C, n, Cm, 0, 1, 0, Send, nullptr, nullptr, nullptr, PeerSignal{},
+                     s);
 }
 
 void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot, const float* gate,
-                    int T, int k, int d, int E, int C, int n, int Cm, void* Y, cudaStream_t s) {
-  if (T <= 0) return;
+                    int T, int k, int d, int E, int C, int n, int Cm, void* Y, cudaStream_t s,
+                    const PeerSignal* sig) {
+  const PeerSignal sg = sig ? *sig : PeerSignal{};
+  if (T <= 0 && !sig) return;
   const int nvl = nvl_of(d, dtype);
   const int U = nvl > 0 ? kLoadsPerLane / nvl : 0;
   if (nvl > 0 && (k == 1 || k == 2) && U >= 1) {
     const int tp = U / k > 0 ? U / k : 1;
-    const long long warps = (T + tp - 1) / tp;
+    const long long warps = std::max(1LL, ((long long)T + tp - 1) / tp);
     if (k == 1)
       LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (combine_kernel<ET, NV_, 1><<<blocks_for_warps(warps), 256, 0, s>>>(
-                                 (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y))));
+                                 (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg))));
     else
       LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (combine_kernel<ET, NV_, 2><<<blocks_for_warps(warps), 256, 0, s>>>(
-                                 (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y))));
+                                 (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg))));
   } else {
-    LINA_DISPATCH_T(dtype, combine_loop_kernel<ET><<<blocks_for_warps(T), 256, 0, s>>>(
-                               (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y));
+    LINA_DISPATCH_T(dtype, combine_loop_kernel<ET><<<blocks_for_warps(std::max(1, T)), 256, 0, s>>>(
+                               (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg));
   }
   LINA_LAUNCH_CHECK();
 }
@@ -412,39 +460,37 @@ void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot
 template <bool PEER>
 static void combine_bwd_any(int dtype, const void* dY, const void* Recv, const int* tok_of, const float* gate,
                             int T, int k, int d, int E, int C, int n, int Cm, int El, int P, int me,
-                            void* dSend, void* const* peer, float* dg, cudaStream_t s) {
+                            void* dSend, void* const* peer, float* dg, const PeerSignal& sig, cudaStream_t s) {
   if (T > 0) LINA_CUDA_CHECK(cudaMemsetAsync(dg, 0, sizeof(float) * (size_t)T * k, s));
   const long long rows = (long long)n * E * Cm;
-  if (rows == 0) return;
+  if (rows == 0 && !PEER) return;
   const int nvl = nvl_of(d, dtype);
-  const long long warps = (rows + rows_per_warp(nvl, 2) - 1) / rows_per_warp(nvl, 2);
+  const long long warps = std::max(1LL, (rows + rows_per_warp(nvl, 2) - 1) / rows_per_warp(nvl, 2));
   LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (combine_bwd_kernel<ET, NV_, PEER><<<blocks_for_warps(warps), 256, 0, s>>>(
                              (const ET*)dY, (const ET*)Recv, tok_of, gate, k, d, E, C, n, Cm, El, P, me,
-                             (ET*)dSend, (ET* const*)peer, dg))));
+                             (ET*)dSend, (ET* const*)peer, dg, sig))));
   LINA_LAUNCH_CHECK();
 }
 
 void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* tok_of,
                         const float* gate, int T, int k, int d, int E, int C, int n, int Cm,
                         void* dSend, float* dg, cudaStream_t s) {
-  combine_bwd_any<false>(dtype, dY, Recv, tok_of, gate, T, k, d, E, C, n, Cm, 0, 1, 0, dSend, nullptr, dg, s);
+  combine_bwd_any<false>(dtype, dY, Recv, tok_of, gate, T, k, d, E, C, n, Cm, 0, 1, 0, dSend, nullptr, dg,
+                         PeerSignal{}, s);
 }
 
-void launch_counts_peer(const int* kept, int El, int P, int me, void* const* peer_counts, cudaStream_t s) {
-  counts_peer_kernel<<<1, 128, 0, s>>>(kept, El, P, me, (int* const*)peer_counts);
-  LINA_LAUNCH_CHECK();
-}
-
-void launch_permute_peer(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
-                         int Cm, int El, int P, int me, void* const* peer_rows, cudaStream_t s) {
-  permute_any<true>(dtype, X, tok_of, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows, s);
+void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d, int E,
+                         int C, int n, int Cm, int El, int P, int me, void* const* peer_rows,
+                         void* const* peer_counts, const PeerSignal& sig, cudaStream_t s) {
+  permute_any<true>(dtype, X, tok_of, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows, kept, peer_counts, sig, s);
 }
 
 void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of,
                              const float* gate, int T, int k, int d, int E, int C, int n, int Cm, int El,
-                             int P, int me, void* const* peer_rows, float* dg, cudaStream_t s) {
-  combine_bwd_any<true>(dtype, dY, Recv, tok_of, gate, T, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows,
-                        dg, s);
+                             int P, int me, void* const* peer_rows, float* dg, const PeerSignal& sig,
+                             cudaStream_t s) {
+  combine_bwd_any<true>(dtype, dY, Recv, tok_of, gate, T, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows, dg,
+                        sig, s);
 }
 
 }  // namespace lina

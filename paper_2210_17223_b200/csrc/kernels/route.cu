@@ -12,8 +12,11 @@
 //           same-expert lanes below it) + per-warp counts prefix     -> slot[T,k], tok_of[E][C]
 // tok_of[e][s] = t*k + j of the assignment holding slot s (or -1): the inverse
 // map the row-parallel permute / combine-backward kernels gather through.
+#include <algorithm>
+
 #include "../common.h"
 #include "../kernels.h"
+#include "../signal.h"
 
 namespace lina {
 namespace {
@@ -84,7 +87,9 @@ __global__ void __launch_bounds__(kRouteBlock) route_assign_kernel(
 }
 
 __global__ void vcount_kernel(const int* __restrict__ recv_kept, int P, int El, int C, int n,
-                              int* __restrict__ vcount) {
+                              int* __restrict__ vcount, PeerSignal sig) {
+  if (threadIdx.x == 0) sig_wait(sig);  // fused transport: the peers' counts have landed
+  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n * P * El) return;
   const int se = i % (P * El);  // s*El + el
@@ -115,10 +120,12 @@ void launch_mtile_prefix(const int* vcount, int n, int nseg, int rows, int* mtp,
   LINA_LAUNCH_CHECK();
 }
 
-void launch_vcount(const int* recv_kept, int P, int El, int C, int n, int* vcount, cudaStream_t s) {
+void launch_vcount(const int* recv_kept, int P, int El, int C, int n, int* vcount, cudaStream_t s,
+                   const PeerSignal* sig) {
   const int tot = n * P * El;
-  if (tot <= 0) return;
-  vcount_kernel<<<(tot + 255) / 256, 256, 0, s>>>(recv_kept, P, El, C, n, vcount);
+  if (tot <= 0 && !sig) return;
+  vcount_kernel<<<std::max(1, (tot + 255) / 256), 256, 0, s>>>(recv_kept, P, El, C, n, vcount,
+                                                               sig ? *sig : PeerSignal{});
   LINA_LAUNCH_CHECK();
 }
 

@@ -143,8 +143,10 @@ void a2a_recv_to_send(const Plan& p, const char* recv, char* send, int w, int c,
 
 void row_gemm(const Plan& p, const void* A, const void* B, void* D, const void* aux,
               const int* vcount, const int* mtp, int c, int N, int K, bool b_kmajor, int epi,
-              cudaStream_t st, uint64_t* mask_out = nullptr, const uint64_t* mask_in = nullptr) {
+              cudaStream_t st, uint64_t* mask_out = nullptr, const uint64_t* mask_in = nullptr,
+              const PeerSignal* sig = nullptr) {
   RowGemm g{};
+  g.sig = sig;
   g.mask_out = mask_out;
   g.mask_in = mask_in;
   g.mtp = mtp + (size_t)c * (p.P * p.El + 1);
@@ -293,50 +295,64 @@ void backward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, co
 // stores through IPC-mapped buffers): permute / combine-backward store each row into
 // its owner's receive buffer; the GEMM2 / dgrad2 epilogues TMA-store each output tile
 // into the owner's send-layout buffer while the tensor cores work on the next tile.
-// Cross-rank ordering: FREE (the receive buffers of this round may be written) and
-// READY (this rank's stores of the round are complete) flags, written with stream
-// memory operations after the producing kernel, waited on with stream memory
-// operations before the consuming kernel — no SM ever waits on another GPU.
-void post_all(lina_comm* cm, cudaStream_t s, int kind, uint32_t seq) {
-  for (int r = 0; r < cm->world; ++r)
-    if (r != cm->rank) cm->ce->post_flag(s, r, kind, cm->rank, 0, seq);
+// Cross-rank ordering (signal.h): FREE (this rank's receive buffers of the round may be
+// written) and READY (a rank's stores of the round are complete) are release stores of
+// the round number into the peers' flag slots, made by the kernels themselves — FREE
+// by the first kernel after the buffers' last reader, READY by the last CTA of the
+// producing kernel — and acquired by the first consuming kernel (one spinning thread
+// per CTA).  No stream memory operation and no extra launch on the critical path.
+PeerSignal make_sig(lina_comm* cm, int wait_kind, uint32_t wait_value, int post_kind, uint32_t post_value,
+                    int done_site = -1) {
+  CeTransport& ce = *cm->ce;
+  PeerSignal g;
+  g.P = cm->world;
+  g.me = cm->rank;
+  g.stride = CeTransport::kMaxChunks;
+  if (wait_kind >= 0) {
+    g.wait = ce.slots(wait_kind);
+    g.wait_value = wait_value;
+  }
+  if (post_kind >= 0) {
+    g.post = ce.peer_slots(post_kind);
+    g.post_value = post_value;
+    g.done = done_site >= 0 ? ce.done_counter(done_site) : nullptr;
+  }
+  return g;
 }
-void wait_all(lina_comm* cm, cudaStream_t s, int kind, uint32_t seq) {
-  for (int r = 0; r < cm->world; ++r)
-    if (r != cm->rank) cm->ce->wait_flag(s, kind, r, 0, seq);
-}
+enum { kSiteDispFwd = 0, kSiteCombFwd = 1, kSiteDispBwd = 2, kSiteCombBwd = 3 };
 
 bool fused_ok(const lina_comm* cm, const Plan& p) {
   return cm->transport == 2 && cm->ce && p.P > 1 && p.bf16 && p.d % 256 == 0 && p.f % 256 == 0 &&
-         p.d % 64 == 0 && p.f % 64 == 0;
+         p.d % 64 == 0 && p.f % 64 == 0 && p.d % 32 == 0;
 }
 
 void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* tokens, const float* gate_w,
                    const void* w1, const void* w2, void* out, void* saved, void* ws, lina_route* route,
                    cudaStream_t s) {
+  using CT = CeTransport;
   CeTransport& ce = *cm->ce;
   const int dtype = 1, P = p.P, me = cm->rank, n = p.n;
   const uint32_t seq = ++ce.seq_fwd;
   const bool override_r = route && route->override_routing;
   trace_mark(cm, s, "fwd:start");
-  post_all(cm, s, CeTransport::kFreeFwd, seq);  // my R, recv counts and Cb may be overwritten
   if (override_r) {
     LINA_CUDA_CHECK(cudaMemcpyAsync(q.idx, route->idx, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
     LINA_CUDA_CHECK(cudaMemcpyAsync(q.gate, route->gate, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
   }
-  launch_gate_topk(dtype, tokens, gate_w, p.T, p.d, p.E, p.k, override_r ? 0 : 1, q.probs, q.idx, q.gate, s);
+  // gate: block 0 posts FREE (my R, recv counts and Cb were last read by the previous backward)
+  const PeerSignal s_free = make_sig(cm, -1, 0, CT::kFreeFwd, seq);
+  launch_gate_topk(dtype, tokens, gate_w, p.T, p.d, p.E, p.k, override_r ? 0 : 1, q.probs, q.idx, q.gate, s,
+                   &s_free);
   launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr, q.kept,
                q.tok_of, s);
   trace_mark(cm, s, "gate+route");
   void* const* peer_R = ce.dev_ptrs(saved, p.s_R, s);
   void* const* peer_cnt = ce.dev_ptrs(saved, p.s_recvkept, s);
-  wait_all(cm, s, CeTransport::kFreeFwd, seq);
-  trace_mark(cm, s, "wait FREE");
-  launch_counts_peer(q.kept, p.El, P, me, peer_cnt, s);
-  trace_mark(cm, s, "counts(peer)");
-  launch_permute_peer(dtype, tokens, q.tok_of, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me, peer_R, s);
+  // dispatch = permute into the owners' R (waits for their FREE, posts READY)
+  const PeerSignal s_disp = make_sig(cm, CT::kFreeFwd, seq, CT::kReadyFwdD, seq, kSiteDispFwd);
+  launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me, peer_R, peer_cnt,
+                      s_disp, s);
   trace_mark(cm, s, "permute(peer)");
-  post_all(cm, s, CeTransport::kReadyFwdD, seq);
   if (route) {
     if (route->idx && !override_r)
       LINA_CUDA_CHECK(cudaMemcpyAsync(route->idx, q.idx, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
@@ -347,21 +363,25 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
     if (route->probs)
       LINA_CUDA_CHECK(cudaMemcpyAsync(route->probs, q.probs, 4 * (size_t)p.T * p.E, cudaMemcpyDeviceToDevice, s));
   }
-  wait_all(cm, s, CeTransport::kReadyFwdD, seq);
-  trace_mark(cm, s, "wait READY(disp)");
-  launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
+  const PeerSignal s_recv = make_sig(cm, CT::kReadyFwdD, seq, -1, 0);
+  launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s, &s_recv);
   launch_mtile_prefix(q.vcount, n, P * p.El, tc_tile_rows(), q.mtp, s);
   trace_mark(cm, s, "vcount");
   const auto& ps_saved = ce.peers(saved, s);
   std::vector<char*> cb(P);
   for (int r = 0; r < P; ++r) cb[r] = ps_saved[r] + p.s_C;
   PeerStore st;
-  st.dmaps = ce.dev_blob("fwdC:" + std::to_string((uintptr_t)saved) + ":" + std::to_string(p.s_C) + ":" +
-                             std::to_string(p.Cm) + ":" + std::to_string(n * p.E),
-                         tc_peer_dmaps(cb, p.d, p.Cm, n * p.E), s);
+  {
+    const std::string key = "fwdC:" + std::to_string((uintptr_t)saved) + ":" + std::to_string(p.s_C) + ":" +
+                            std::to_string(p.Cm) + ":" + std::to_string(n * p.E);
+    auto it = ce.host_blobs.find(key);
+    if (it == ce.host_blobs.end()) it = ce.host_blobs.emplace(key, tc_peer_dmaps(cb, p.d, p.Cm, n * p.E)).first;
+    st.host_maps = it->second.data();
+  }
   st.P = P;
   st.me = me;
   st.E = p.E;
+  const PeerSignal s_comb = make_sig(cm, -1, 0, CT::kReadyFwdC, seq, kSiteCombFwd);
   prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
     row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask);
@@ -378,48 +398,54 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
     g.Cm = p.Cm;
     g.N = p.d;
     g.K = p.f;
+    if (c == n - 1) g.sig = &s_comb;  // the last CTA of the last chunk posts READY
     launch_row_gemm_tc_peer(g, true, kEpiNone, st, s);  // combine all-to-all in the epilogue
     trace_mark(cm, s, "gemm2(peer)");
   }
   prof_end(cm, s, 2 * n);
-  post_all(cm, s, CeTransport::kReadyFwdC, seq);
-  wait_all(cm, s, CeTransport::kReadyFwdC, seq);
-  trace_mark(cm, s, "wait READY(comb)");
-  launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, out, s);
+  // combine: block 0 posts the backward FREE (my dO / dXs were last read by the previous
+  // backward), every CTA waits for the returned expert outputs
+  const PeerSignal s_out = make_sig(cm, CT::kReadyFwdC, seq, CT::kFreeBwd, seq);
+  launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, out, s, &s_out);
   trace_mark(cm, s, "combine");
 }
 
 void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dout, const void* tokens,
                     const float* gate_w, const void* w1, const void* w2, void* dtokens, float* dgate_w,
                     void* dw1, void* dw2, void* ws, cudaStream_t s) {
+  using CT = CeTransport;
   CeTransport& ce = *cm->ce;
   const int dtype = 1, P = p.P, me = cm->rank, n = p.n;
   const uint32_t seq = ++ce.seq_bwd;
   trace_mark(cm, s, "bwd:start");
-  post_all(cm, s, CeTransport::kFreeBwd, seq);  // my dO and dXs may be overwritten
   void* const* peer_dO = ce.dev_ptrs(ws, p.w_dO, s);
   if (cm->sched) sched_a2a_imminent(cm);
-  wait_all(cm, s, CeTransport::kFreeBwd, seq);
-  trace_mark(cm, s, "wait FREE");
+  // backward dispatch = combine-backward into the owners' dO (waits for the FREE they
+  // posted in their forward's combine, posts READY)
+  const PeerSignal s_disp = make_sig(cm, CT::kFreeBwd, ce.seq_fwd, CT::kReadyBwdD, seq, kSiteDispBwd);
   launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me,
-                          peer_dO, q.dg, s);
+                          peer_dO, q.dg, s_disp, s);
   trace_mark(cm, s, "combine_bwd(peer)");
-  post_all(cm, s, CeTransport::kReadyBwdD, seq);
-  wait_all(cm, s, CeTransport::kReadyBwdD, seq);
-  trace_mark(cm, s, "wait READY(disp)");
   const auto& ps_ws = ce.peers(ws, s);
   std::vector<char*> dxs(P);
   for (int r = 0; r < P; ++r) dxs[r] = ps_ws[r] + p.w_dXs;
   PeerStore st;
-  st.dmaps = ce.dev_blob("bwdC:" + std::to_string((uintptr_t)ws) + ":" + std::to_string(p.w_dXs) + ":" +
-                             std::to_string(p.Cm) + ":" + std::to_string(n * p.E),
-                         tc_peer_dmaps(dxs, p.d, p.Cm, n * p.E), s);
+  {
+    const std::string key = "bwdC:" + std::to_string((uintptr_t)ws) + ":" + std::to_string(p.w_dXs) + ":" +
+                            std::to_string(p.Cm) + ":" + std::to_string(n * p.E);
+    auto it = ce.host_blobs.find(key);
+    if (it == ce.host_blobs.end()) it = ce.host_blobs.emplace(key, tc_peer_dmaps(dxs, p.d, p.Cm, n * p.E)).first;
+    st.host_maps = it->second.data();
+  }
   st.P = P;
   st.me = me;
   st.E = p.E;
+  const PeerSignal s_recv = make_sig(cm, CT::kReadyBwdD, seq, -1, 0);
+  const PeerSignal s_comb = make_sig(cm, -1, 0, CT::kReadyBwdC, seq, kSiteCombBwd);
   prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
-    row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask);
+    row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask,
+             c == 0 ? &s_recv : nullptr);  // the first reader of the peers' dO rows waits
     trace_mark(cm, s, "dgrad1");
     RowGemm g{};
     g.mtp = q.mtp + (size_t)c * (P * p.El + 1);
@@ -433,10 +459,10 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
     g.Cm = p.Cm;
     g.N = p.d;
     g.K = p.f;
+    if (c == n - 1) g.sig = &s_comb;
     launch_row_gemm_tc_peer(g, false, kEpiNone, st, s);  // combine all-to-all in the epilogue
     trace_mark(cm, s, "dgrad2(peer)");
   }
-  post_all(cm, s, CeTransport::kReadyBwdC, seq);
   WGrad wg2{q.dO, q.H, dw2, q.vcount, n, P, p.El, p.Cm, p.d, p.f};
   WGrad wg1{q.dH, q.R, dw1, q.vcount, n, P, p.El, p.Cm, p.f, p.d};
   launch_expert_wgrad(dtype, wg2, s);
@@ -446,11 +472,10 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   // dWg needs only this rank's dg: it overlaps the last returning expert gradients
   launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, p.E, p.k, q.dwg, dgate_w, s);
   trace_mark(cm, s, "dwg");
-  wait_all(cm, s, CeTransport::kReadyBwdC, seq);
-  trace_mark(cm, s, "wait READY(comb)");
-  if (cm->sched) sched_a2a_end(cm, s);
+  const PeerSignal s_back = make_sig(cm, CT::kReadyBwdC, seq, -1, 0);
   launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm,
-            dtokens, s);
+            dtokens, s, &s_back);
+  if (cm->sched) sched_a2a_end(cm, s);  // dx has consumed the last returning rows
   trace_mark(cm, s, "dx");
 }
 
@@ -532,13 +557,17 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
     // All experts local: the "all-to-all" is the identity and chunks only re-slice the GEMMs.
     launch_vcount(q.kept, 1, p.E, p.C, p.n, q.vcount, s);
     launch_mtile_prefix(q.vcount, p.n, p.P * p.El, tc_tile_rows(), q.mtp, s);
+    trace_mark(cm, s, "P1 vcount");
     prof_begin(cm, s);
     for (int c = 0; c < p.n; ++c) {
       row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask);
+      trace_mark(cm, s, "P1 gemm1");
       row_gemm(p, q.H, w2, q.O, nullptr, q.vcount, q.mtp, c, p.d, p.f, true, kEpiNone, s);
+      trace_mark(cm, s, "P1 gemm2");
     }
     prof_end(cm, s, 2 * p.n);
     launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, p.n, p.Cm, out, s);
+    trace_mark(cm, s, "P1 combine");
     return;
   }
   // ---- P > 1: pipelined micro-ops

@@ -1,0 +1,72 @@
+// In-kernel cross-rank ordering for the fused transport (internal header).
+//
+// A rank's flag slot (kind, peer) lives in its IPC-mapped flag array (ce.cpp); rank r
+// publishes "my part of exchange `kind` of round `seq` is done" by a release store of
+// seq into every peer's slot (kind, r), and a consumer kernel acquires it by spinning
+// (one thread per CTA) until every peer's slot reached the round it needs.  This
+// replaces one stream wait / stream write operation per peer and exchange (~6 us of
+// device time each, measured) by a few loads inside kernels that run anyway.
+//
+//   wait side : thread 0 of each CTA calls sig_wait() before the CTA touches data the
+//               peers wrote (then __syncthreads; a TMA consumer adds a proxy fence).
+//   post side : sig_post() by one thread when only it has to publish (nothing written
+//               yet by the kernel), or sig_post_last() by thread 0 of every CTA after
+//               its last write: the last CTA to finish publishes for the whole grid.
+//
+// A peer that never posts must not hang the GPU: a waiter traps after ~10 s.
+#pragma once
+#include <stdint.h>
+
+namespace lina {
+
+struct PeerSignal {
+  const uint32_t* wait = nullptr;   // my slots of the awaited kind: wait[r * stride] written by rank r
+  uint32_t wait_value = 0;          // round to wait for (wrap-safe >=)
+  uint32_t* const* post = nullptr;  // device array [P]: rank r's slot (kind, me), mapped here
+  uint32_t post_value = 0;
+  unsigned int* done = nullptr;     // zeroed CTA-completion counter (sig_post_last)
+  int P = 1, me = 0, stride = 0;
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t sig_ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sig_st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void sig_wait(const PeerSignal& s) {
+  if (!s.wait) return;
+  const long long t0 = clock64();
+  for (int r = 0; r < s.P; ++r) {
+    if (r == s.me) continue;
+    const uint32_t* f = s.wait + (size_t)r * s.stride;
+    while ((int)(sig_ld_acquire(f) - s.wait_value) < 0) {
+      __nanosleep(100);
+      if (clock64() - t0 > 20000000000LL) __trap();  // a peer died: fail loudly, do not hang
+    }
+  }
+}
+
+__device__ __forceinline__ void sig_post(const PeerSignal& s) {
+  if (!s.post) return;
+  __threadfence_system();
+  for (int r = 0; r < s.P; ++r)
+    if (r != s.me) sig_st_release(s.post[r], s.post_value);
+}
+
+__device__ __forceinline__ void sig_post_last(const PeerSignal& s) {
+  if (!s.post) return;
+  __threadfence_system();  // this CTA's writes before its arrival
+  const unsigned int nb = gridDim.x * gridDim.y * gridDim.z;
+  if (atomicAdd(s.done, 1u) == nb - 1) {
+    *s.done = 0u;  // reset for the next launch on this stream
+    sig_post(s);
+  }
+}
+#endif
+
+}  // namespace lina
