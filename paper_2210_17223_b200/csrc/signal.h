@@ -58,11 +58,15 @@ __device__ __forceinline__ void sig_post(const PeerSignal& s) {
     if (r != s.me) sig_st_release(s.post[r], s.post_value);
 }
 
+// The CTA's writes (ordered before thread 0 by the caller's barrier) are released to the
+// last CTA at GPU scope; only that CTA pays the system-scope fence before publishing
+// (release/acquire chains compose: a peer that acquires the flag sees every CTA's writes).
 __device__ __forceinline__ void sig_post_last(const PeerSignal& s) {
   if (!s.post) return;
-  __threadfence_system();  // this CTA's writes before its arrival
   const unsigned int nb = gridDim.x * gridDim.y * gridDim.z;
-  if (atomicAdd(s.done, 1u) == nb - 1) {
+  unsigned int prev;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(s.done) : "memory");
+  if (prev == nb - 1) {
     *s.done = 0u;  // reset for the next launch on this stream
     sig_post(s);
   }
