@@ -50,14 +50,16 @@ void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int*
 void launch_vcount(const int* recv_kept, int P, int El, int C, int n, int* vcount, cudaStream_t s,
                    const PeerSignal* sig = nullptr);
 
-void launch_permute(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
-                    int Cm, void* Send, cudaStream_t s);
+// Rows past the first 64-row boundary after a segment's kept rows are not written (see
+// permute.cu kRowSkip); kept[e] = this rank's kept count of expert e.
+void launch_permute(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d, int E, int C,
+                    int n, int Cm, void* Send, cudaStream_t s);
 // sig: block 0 posts sig.post (FREE of the backward buffers) at start; every CTA waits
 // sig.wait (the returned expert outputs) before reading Recv.
 void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot, const float* gate,
                     int T, int k, int d, int E, int C, int n, int Cm, void* Y, cudaStream_t s,
                     const PeerSignal* sig = nullptr);
-void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* tok_of,
+void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
                         const float* gate, int T, int k, int d, int E, int C, int n, int Cm,
                         void* dSend, float* dg, cudaStream_t s);
 // dX (gather-sum + dL·Wgᵀ) and dWg (Xᵀ dL) with dL recomputed from the forward routing.
@@ -87,7 +89,7 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s);
 void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d, int E,
                          int C, int n, int Cm, int El, int P, int me, void* const* peer_rows,
                          void* const* peer_counts, const PeerSignal& sig, cudaStream_t s);
-void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of,
+void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
                              const float* gate, int T, int k, int d, int E, int C, int n, int Cm, int El,
                              int P, int me, void* const* peer_rows, float* dg, const PeerSignal& sig,
                              cudaStream_t s);

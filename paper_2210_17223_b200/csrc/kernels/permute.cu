@@ -36,15 +36,27 @@ __device__ __forceinline__ size_t peer_row(int c, int e, int r, int El, int P, i
 
 // Send-layout row gw = (c*E + e)*Cm + r -> the assignment code in it (-1 = padding) and,
 // for the fused dispatch, its destination (owner e / El, receive row peer_row(...)).
-__device__ __forceinline__ int row_assignment(long long gw, const int* __restrict__ tok_of, int E, int C,
-                                              int Cm, int El, int P, int me, int& owner, size_t& prow) {
+// kRowSkip: a padding row past the first 64-row block boundary after the segment's valid
+// rows.  Only rows [v, roundup64(v)) of a segment are ever read as padding (the wgrad
+// K-blocks are 64 rows; rows past them only feed output rows nobody reads), so only
+// those are written as zeros — padding is ~20% of the rows at cf = 1.25, and at P > 1
+// it would cross NVLink.
+constexpr int kRowSkip = -2;
+__device__ __forceinline__ int row_assignment(long long gw, const int* __restrict__ tok_of,
+                                              const int* __restrict__ kept, int E, int C, int Cm, int El, int P,
+                                              int me, int& owner, size_t& prow) {
   const int r = (int)(gw % Cm);
   const int ce = (int)(gw / Cm);
   const int e = ce % E, c = ce / E;
   const int b = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b;
   owner = El > 0 ? e / El : 0;
   prow = El > 0 ? peer_row(c, e, r, El, P, me, Cm) : (size_t)gw;
-  return (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
+  const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
+  if (a < 0) {
+    const int v = min(max(kept[e] - b, 0), Cc);
+    if (r >= min(Cm, (v + 63) & ~63)) return kRowSkip;  // (the segment pitch Cm, not Cc, bounds the read)
+  }
+  return a;
 }
 
 // permute (PEER = false): Send[row] = X[token of row] or 0.
@@ -53,9 +65,10 @@ __device__ __forceinline__ int row_assignment(long long gw, const int* __restric
 // recv row ((c*P + me)*El + e%El)*Cm + r of owner o = e / El, so the permute IS the
 // dispatch all-to-all.
 template <typename T, int NVL, bool PEER>
-__device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int* __restrict__ tok_of, int k,
-                                             int d, int E, int C, int n, int Cm, int El, int P, int me,
-                                             T* __restrict__ Send, T* const* __restrict__ peer) {
+__device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int* __restrict__ tok_of,
+                                             const int* __restrict__ kept, int k, int d, int E, int C, int n,
+                                             int Cm, int El, int P, int me, T* __restrict__ Send,
+                                             T* const* __restrict__ peer) {
   constexpr int R = NVL == 0 ? 1 : (NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / NVL);
   constexpr int NL = NVL == 0 ? 1 : NVL;
   constexpr int V = 16 / sizeof(T);
@@ -68,10 +81,11 @@ __device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int*
   int a = -1, owner = 0;
   size_t prow = 0;
   if (lane < R && row0 + lane < rows)
-    a = row_assignment(row0 + lane, tok_of, E, C, Cm, PEER ? El : 0, P, me, owner, prow);
+    a = row_assignment(row0 + lane, tok_of, kept, E, C, Cm, PEER ? El : 0, P, me, owner, prow);
   if constexpr (NVL == 0) {
     uint4* dst = reinterpret_cast<uint4*>(PEER ? peer[owner] + prow * d : Send + (size_t)row0 * d);
     a = __shfl_sync(0xffffffffu, a, 0);
+    if (a == kRowSkip) return;
     dst = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), 0));
     const uint4* src = reinterpret_cast<const uint4*>(X + (size_t)(a >= 0 ? a / k : 0) * d);
     for (int v = lane; v < nv; v += 32) dst[v] = a >= 0 ? src[v] : make_uint4(0, 0, 0, 0);
@@ -91,6 +105,7 @@ __device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int*
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       if (row0 + i >= rows) break;
+      if (ai[i] == kRowSkip) continue;
       uint4* dst;
       if constexpr (PEER) {
         const int o = __shfl_sync(0xffffffffu, owner, i);
@@ -122,7 +137,7 @@ __global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ X, c
     if (blockIdx.x == 0)
       for (int i = threadIdx.x; i < P * El; i += blockDim.x) peer_counts[i / El][me * El + i % El] = kept[i];
   }
-  permute_rows<T, NVL, PEER>(X, tok_of, k, d, E, C, n, Cm, El, P, me, Send, peer);
+  permute_rows<T, NVL, PEER>(X, tok_of, kept, k, d, E, C, n, Cm, El, P, me, Send, peer);
   if constexpr (PEER) {
     __syncthreads();
     if (threadIdx.x == 0) sig_post_last(sig);  // the last CTA: READY of the dispatch
@@ -251,7 +266,8 @@ __global__ void combine_loop_kernel(const T* __restrict__ Recv, const int* __res
 // (0 for padding rows).  PEER: dSend rows are stored into the owners' receive buffers.
 template <typename T, int NVL, bool PEER>
 __device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const T* __restrict__ Recv,
-                                                 const int* __restrict__ tok_of, const float* __restrict__ gate,
+                                                 const int* __restrict__ tok_of, const int* __restrict__ kept,
+                                                 const float* __restrict__ gate,
                                                  int k, int d, int E, int C, int n, int Cm, int El, int P, int me,
                                                  T* __restrict__ dSend, T* const* __restrict__ peer,
                                                  float* __restrict__ dg) {
@@ -268,11 +284,12 @@ __device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const
   size_t prow = 0;
   float ga = 0.f;
   if (lane < R && row0 + lane < rows) {
-    a = row_assignment(row0 + lane, tok_of, E, C, Cm, PEER ? El : 0, P, me, owner, prow);
+    a = row_assignment(row0 + lane, tok_of, kept, E, C, Cm, PEER ? El : 0, P, me, owner, prow);
     if (a >= 0) ga = gate[a];
   }
   if constexpr (NVL == 0) {
     a = __shfl_sync(0xffffffffu, a, 0);
+    if (a == kRowSkip) return;
     ga = __shfl_sync(0xffffffffu, ga, 0);
     owner = __shfl_sync(0xffffffffu, owner, 0);
     prow = __shfl_sync(0xffffffffu, (unsigned long long)prow, 0);
@@ -317,6 +334,7 @@ __device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       if (row0 + i >= rows) break;
+      if (ai[i] == kRowSkip) continue;
       const float g = __shfl_sync(0xffffffffu, ga, i);
       T* dst;
       if constexpr (PEER) {
@@ -351,6 +369,7 @@ __device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const
 template <typename T, int NVL, bool PEER>
 __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ dY, const T* __restrict__ Recv,
                                                           const int* __restrict__ tok_of,
+                                                          const int* __restrict__ kept,
                                                           const float* __restrict__ gate, int k, int d,
                                                           int E, int C, int n, int Cm, int El, int P,
                                                           int me, T* __restrict__ dSend,
@@ -360,7 +379,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ 
     if (threadIdx.x == 0) sig_wait(sig);
     __syncthreads();
   }
-  combine_bwd_rows<T, NVL, PEER>(dY, Recv, tok_of, gate, k, d, E, C, n, Cm, El, P, me, dSend, peer, dg);
+  combine_bwd_rows<T, NVL, PEER>(dY, Recv, tok_of, kept, gate, k, d, E, C, n, Cm, El, P, me, dSend, peer, dg);
   if constexpr (PEER) {
     __syncthreads();
     if (threadIdx.x == 0) sig_post_last(sig);  // the last CTA: READY of the backward dispatch
@@ -428,10 +447,9 @@ static void permute_any(int dtype, const void* X, const int* tok_of, int k, int 
   LINA_LAUNCH_CHECK();
 }
 
-void launch_permute(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
-                    int Cm, void* Send, cudaStream_t s) {
-  permute_any<false>(dtype, X, tok_of, k, d, E, C, n, Cm, 0, 1, 0, Send, nullptr, nullptr, nullptr, PeerSignal{},
-                     s);
+void launch_permute(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d, int E, int C,
+                    int n, int Cm, void* Send, cudaStream_t s) {
+  permute_any<false>(dtype, X, tok_of, k, d, E, C, n, Cm, 0, 1, 0, Send, nullptr, kept, nullptr, PeerSignal{}, s);
 }
 
 void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot, const float* gate,
@@ -458,7 +476,8 @@ void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot
 }
 
 template <bool PEER>
-static void combine_bwd_any(int dtype, const void* dY, const void* Recv, const int* tok_of, const float* gate,
+static void combine_bwd_any(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
+                            const float* gate,
                             int T, int k, int d, int E, int C, int n, int Cm, int El, int P, int me,
                             void* dSend, void* const* peer, float* dg, const PeerSignal& sig, cudaStream_t s) {
   if (T > 0) LINA_CUDA_CHECK(cudaMemsetAsync(dg, 0, sizeof(float) * (size_t)T * k, s));
@@ -467,15 +486,15 @@ static void combine_bwd_any(int dtype, const void* dY, const void* Recv, const i
   const int nvl = nvl_of(d, dtype);
   const long long warps = std::max(1LL, (rows + rows_per_warp(nvl, 2) - 1) / rows_per_warp(nvl, 2));
   LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (combine_bwd_kernel<ET, NV_, PEER><<<blocks_for_warps(warps), 256, 0, s>>>(
-                             (const ET*)dY, (const ET*)Recv, tok_of, gate, k, d, E, C, n, Cm, El, P, me,
-                             (ET*)dSend, (ET* const*)peer, dg, sig))));
+                             (const ET*)dY, (const ET*)Recv, tok_of, kept, gate, k, d, E, C, n, Cm, El, P,
+                             me, (ET*)dSend, (ET* const*)peer, dg, sig))));
   LINA_LAUNCH_CHECK();
 }
 
-void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* tok_of,
+void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
                         const float* gate, int T, int k, int d, int E, int C, int n, int Cm,
                         void* dSend, float* dg, cudaStream_t s) {
-  combine_bwd_any<false>(dtype, dY, Recv, tok_of, gate, T, k, d, E, C, n, Cm, 0, 1, 0, dSend, nullptr, dg,
+  combine_bwd_any<false>(dtype, dY, Recv, tok_of, kept, gate, T, k, d, E, C, n, Cm, 0, 1, 0, dSend, nullptr, dg,
                          PeerSignal{}, s);
 }
 
@@ -485,12 +504,12 @@ void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int*
   permute_any<true>(dtype, X, tok_of, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows, kept, peer_counts, sig, s);
 }
 
-void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of,
+void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
                              const float* gate, int T, int k, int d, int E, int C, int n, int Cm, int El,
                              int P, int me, void* const* peer_rows, float* dg, const PeerSignal& sig,
                              cudaStream_t s) {
-  combine_bwd_any<true>(dtype, dY, Recv, tok_of, gate, T, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows, dg,
-                        sig, s);
+  combine_bwd_any<true>(dtype, dY, Recv, tok_of, kept, gate, T, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows,
+                        dg, sig, s);
 }
 
 }  // namespace lina

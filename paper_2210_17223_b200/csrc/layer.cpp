@@ -423,7 +423,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   // backward dispatch = combine-backward into the owners' dO (waits for the FREE they
   // posted in their forward's combine, posts READY)
   const PeerSignal s_disp = make_sig(cm, CT::kFreeBwd, ce.seq_fwd, CT::kReadyBwdD, seq, kSiteDispBwd);
-  launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me,
+  launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me,
                           peer_dO, q.dg, s_disp, s);
   trace_mark(cm, s, "combine_bwd(peer)");
   const auto& ps_ws = ce.peers(ws, s);
@@ -538,7 +538,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
                    q.gate, s);
   launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr,
                q.kept, q.tok_of, s);
-  launch_permute(dtype, tokens, q.tok_of, p.k, p.d, p.E, p.C, p.n, p.Cm, q.D, s);
+  launch_permute(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, p.n, p.Cm, q.D, s);
   if (route) {
     if (route->idx && !override_r)
       LINA_CUDA_CHECK(cudaMemcpyAsync(route->idx, q.idx, 4 * (size_t)p.T * p.k,
@@ -663,7 +663,7 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
     return;
   }
   // (a) combine backward: dg and g·dY rows into the send layout
-  launch_combine_bwd(dtype, dout, q.Cb, q.tok_of, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, q.dS,
+  launch_combine_bwd(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, q.dS,
                      q.dg, s);
   // the scheduler stops admitting allreduce micro-ops: all-to-all is imminent
   if (cm->sched) sched_a2a_imminent(cm);
