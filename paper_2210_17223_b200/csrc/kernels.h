@@ -97,6 +97,7 @@ void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const 
 // segment (c, s, el) of the receive layout goes to map s at segment c*E + me*El + el.
 struct PeerStore {
   const void* host_maps = nullptr;  // host array [P] of CUtensorMap (tc_peer_dmaps), copied into the launch
+  char* const* bases = nullptr;     // host array [P]: the same buffers (mapped here)
   int P = 0, me = 0, E = 0;
 };
 void launch_row_gemm_tc_peer(const RowGemm& g, bool b_kmajor, int epi, const PeerStore& ps, cudaStream_t s);

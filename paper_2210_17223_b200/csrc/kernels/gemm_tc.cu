@@ -155,6 +155,12 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ uint4 ld_shared16(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_shared16(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
@@ -276,6 +282,7 @@ struct TcParams {
   const uint64_t* mask_in;  // ROW + mask epilogue: the bits written by GEMM1
   PeerSignal sig;           // fused transport: wait before the first A load / post after the last store
   CUtensorMap pmaps[kMaxPeerMaps];  // kernel-parameter copies (the TMA unit reads them like tmD)
+  char* pbase[kMaxPeerMaps];        // the same buffers as plain pointers (remote owners: SM stores)
 };
 
 template <int CG, bool WGRAD, bool B_MN, int EPI>
@@ -331,7 +338,12 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
 
-  auto decode = [&](int t, int& seg_or_el, int& m0, int& n0) {
+  // Fused combine stores: every rank starts at the tiles of source (me + 1) % P, so at any
+  // moment the P ranks write to P different owners (no incast on one rank's links).
+  const int rot = (!WGRAD && p.has_pmaps && p.dP > 1) ? p.mtp[((p.dme + 1) % p.dP) * p.El] * n_nblk : 0;
+  auto decode = [&](int t0, int& seg_or_el, int& m0, int& n0) {
+    int t = t0 + rot;
+    if (t >= total_tiles) t -= total_tiles;
     const int nb = t % n_nblk;
     const int ml = t / n_nblk;
     n0 = nb * BN;
@@ -544,16 +556,29 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
         if (EPI == kEpiRelu && p.mask_out && row_ok) p.mask_out[mrow + j] = mword;
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          int x0, x1, x2;
-          box_of(t, c0, x0, x1, x2);
-          if (!WGRAD && p.has_pmaps) {  // fused combine all-to-all: store into the owner's buffer
-            const int seg = x2;
-            const int el = seg % p.El, sidx = (seg / p.El) % p.dP, c = seg / (p.El * p.dP);
-            tma_store_3d(&p.pmaps[sidx], buf, x0, x1, c * p.dE + p.dme * p.El + el);
-          } else {
-            tma_store_3d(&tmD, buf, x0, x1, x2);
+        int x0, x1, x2;
+        box_of(t, c0, x0, x1, x2);
+        int sidx = 0, dseg = 0;
+        if (!WGRAD && p.has_pmaps) {  // fused combine all-to-all: the owner of this segment
+          const int el = x2 % p.El, c = x2 / (p.El * p.dP);
+          sidx = (x2 / p.El) % p.dP;
+          dseg = c * p.dE + p.dme * p.El + el;
+        }
+        if (!WGRAD && p.has_pmaps && sidx != p.dme) {
+          // remote owner: the warp moves the box with 16-byte stores over NVLink, four
+          // 128-byte row segments per instruction (rows past the segment end skipped);
+          // an empty bulk group keeps the staging-buffer accounting uniform
+          char* base = p.pbase[sidx] + (size_t)dseg * p.Cm * p.N * 2;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + (lane >> 3), q = lane & 7;
+            const uint4 v = ld_shared16(smem_u32(buf) + rr * 128 + ((q ^ (rr & 7)) << 4));
+            if (x1 + rr < p.Cm) *reinterpret_cast<uint4*>(base + ((size_t)(x1 + rr) * p.N + x0 + q * 8) * 2) = v;
           }
+          if (lane == 0) bulk_commit();
+        } else if (lane == 0) {
+          if (!WGRAD && p.has_pmaps) tma_store_3d(&p.pmaps[sidx], buf, x0, x1, dseg);
+          else tma_store_3d(&tmD, buf, x0, x1, x2);
           bulk_commit();
         }
         __syncwarp();
@@ -756,6 +781,7 @@ static void row_gemm_tc_impl(const RowGemm& g, bool b_kmajor, int epi, const Pee
   if (ps) {
     if (ps->P > kMaxPeerMaps) throw CudaError{"fused transport supports at most 8 ranks"};
     std::memcpy(p.pmaps, ps->host_maps, sizeof(CUtensorMap) * ps->P);
+    for (int r = 0; r < ps->P; ++r) p.pbase[r] = ps->bases[r];
     p.has_pmaps = 1;
     p.dP = ps->P;
     p.dme = ps->me;

@@ -59,6 +59,22 @@ __device__ __forceinline__ int row_assignment(long long gw, const int* __restric
   return a;
 }
 
+// First row of this warp's R-row group (-1: none).  Peer stores: warps are rotated so
+// that every rank starts with the rows of owner (me + 1) % P — at any moment the P ranks
+// write to P different owners instead of all to owner 0 (no incast on one rank's links).
+template <bool PEER>
+__device__ __forceinline__ long long rotated_row0(int R, long long rows, int El, int P, int me, int Cm) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (rows + R - 1) / R;
+  if (w >= nw) return -1;
+  long long wr = w;
+  if (PEER && P > 1) {
+    wr += ((long long)((me + 1) % P) * El * Cm) / R;
+    if (wr >= nw) wr -= nw;
+  }
+  return wr * R;
+}
+
 // permute (PEER = false): Send[row] = X[token of row] or 0.
 // fused dispatch (PEER = true): the same rows stored straight into the owners' receive
 // buffers over NVLink (peer[o] = rank o's buffer mapped here): row (c, e, r) lands at
@@ -72,11 +88,10 @@ __device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int*
   constexpr int R = NVL == 0 ? 1 : (NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / NVL);
   constexpr int NL = NVL == 0 ? 1 : NVL;
   constexpr int V = 16 / sizeof(T);
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long rows = (long long)n * E * Cm;
-  const long long row0 = w * R;
-  if (row0 >= rows) return;
+  const long long row0 = rotated_row0<PEER>(R, rows, El, P, me, Cm);
+  if (row0 < 0) return;
   const int nv = d / V;
   int a = -1, owner = 0;
   size_t prow = 0;
@@ -274,11 +289,10 @@ __device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const
   constexpr int NL = NVL == 0 ? 1 : NVL;
   constexpr int R = NVL == 0 ? 1 : (2 * NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / (2 * NVL));
   constexpr int V = 16 / sizeof(T);
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long rows = (long long)n * E * Cm;
-  const long long row0 = w * R;
-  if (row0 >= rows) return;
+  const long long row0 = rotated_row0<PEER>(R, rows, El, P, me, Cm);
+  if (row0 < 0) return;
   const int nv = d / V;
   int a = -1, owner = 0;
   size_t prow = 0;

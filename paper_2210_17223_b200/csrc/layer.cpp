@@ -377,6 +377,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
     auto it = ce.host_blobs.find(key);
     if (it == ce.host_blobs.end()) it = ce.host_blobs.emplace(key, tc_peer_dmaps(cb, p.d, p.Cm, n * p.E)).first;
     st.host_maps = it->second.data();
+    st.bases = cb.data();
   }
   st.P = P;
   st.me = me;
@@ -436,6 +437,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
     auto it = ce.host_blobs.find(key);
     if (it == ce.host_blobs.end()) it = ce.host_blobs.emplace(key, tc_peer_dmaps(dxs, p.d, p.Cm, n * p.E)).first;
     st.host_maps = it->second.data();
+    st.bases = dxs.data();
   }
   st.P = P;
   st.me = me;
