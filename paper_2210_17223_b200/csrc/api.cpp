@@ -174,8 +174,13 @@ lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned 
       ncclConfig_t cfg2 = NCCL_CONFIG_INITIALIZER;
       if (nccl_max_ctas > 0) cfg2.maxCTAs = nccl_max_ctas;
       LINA_NCCL_CHECK(ncclCommSplit(cm->ep_disp, 0, rank, &cm->ep_comb, &cfg2));
+      // DP communicator (allreduce micro-ops): its CTA budget is separate from the EP
+      // ones — under the LINA policy its micro-ops run in the windows without all-to-all
+      // traffic, so it keeps NCCL's default CTA count (LINA_DP_MAX_CTAS overrides).
       ncclConfig_t cfg3 = NCCL_CONFIG_INITIALIZER;
-      if (nccl_max_ctas > 0) cfg3.maxCTAs = nccl_max_ctas;
+      const char* dpc = getenv("LINA_DP_MAX_CTAS");
+      const int dp_ctas = dpc ? atoi(dpc) : 0;
+      if (dp_ctas > 0) cfg3.maxCTAs = dp_ctas;
       LINA_NCCL_CHECK(ncclCommSplit(cm->ep_disp, 0, rank, &cm->dp, &cfg3));
       cm->sched = sched_create(cm);
       // Training all-to-all transport (LINA_TRANSPORT): "fused" (default) = peer stores from

@@ -465,6 +465,9 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
     launch_row_gemm_tc_peer(g, false, kEpiNone, st, s);  // combine all-to-all in the epilogue
     trace_mark(cm, s, "dgrad2(peer)");
   }
+  // the last kernel that moves all-to-all bytes is done: allreduce micro-ops may run
+  // beside the weight gradients, dWg and dX (compute only)
+  if (cm->sched) sched_a2a_end(cm, s);
   WGrad wg2{q.dO, q.H, dw2, q.vcount, n, P, p.El, p.Cm, p.d, p.f};
   WGrad wg1{q.dH, q.R, dw1, q.vcount, n, P, p.El, p.Cm, p.f, p.d};
   launch_expert_wgrad(dtype, wg2, s);
@@ -477,7 +480,6 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   const PeerSignal s_back = make_sig(cm, CT::kReadyBwdC, seq, -1, 0);
   launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm,
             dtokens, s, &s_back);
-  if (cm->sched) sched_a2a_end(cm, s);  // dx has consumed the last returning rows
   trace_mark(cm, s, "dx");
 }
 
