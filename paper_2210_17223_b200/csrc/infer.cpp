@@ -16,9 +16,11 @@
 //   s : gate+softmax+top-k -> dropless slots (C = T) -> per-expert counts
 //   s : allgather counts [P][E] -> D2H -> host plan (Eq. 1 + FFD, replica splits,
 //       send/recv sizes) -> H2D of the routing tables
-//   s : replica-routed permute -> grouped ncclSend/ncclRecv -> grouped expert GEMMs
-//       over the hosted experts (tcgen05, weight index per segment) -> grouped
-//       send/recv back -> row-indexed combine.
+//   s : replica-routed permute -> one ncclSend/ncclRecv per peer (source-major
+//       blocks) -> regroup expert-major (one padded segment per hosted expert) ->
+//       grouped expert GEMMs over the hosted experts (tcgen05, weight index per
+//       segment) -> regroup source-major -> one send/recv per peer back -> row-indexed
+//       combine.
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -35,7 +37,7 @@ struct InferPlan {
   int T, d, f, E, k, P, mpd, dt;
   size_t Cmax;
   size_t o_probs, o_idx, o_gate, o_slot, o_counts, o_kept, o_tokof, o_route, o_all, o_tab, o_vc,
-      o_mtp, o_segx, o_arow, o_send, o_recv, o_h, o_o, o_back, total;
+      o_mtp, o_gvc, o_segx, o_arow, o_send, o_recv, o_gin, o_h, o_o, o_back2, o_back, total;
   size_t tab_ints() const { return (size_t)E + (size_t)E * P + (size_t)P * E + E; }
 };
 
@@ -50,7 +52,8 @@ static InferPlan infer_plan(const lina_moe_desc& dsc, int P, int mpd) {
   q.mpd = mpd;
   q.dt = dsc.dtype == LINA_BF16 ? 2 : 4;
   const size_t Tk = (size_t)q.T * q.k;
-  q.Cmax = std::max<size_t>(128, (Tk + 127) / 128 * 128);  // worst case: a source's tokens to one expert
+  // expert-major segment pitch, worst case: every source's tokens to one expert
+  q.Cmax = std::max<size_t>(128, ((size_t)P * Tk + 127) / 128 * 128);
   const size_t segs = (size_t)P * mpd;
   size_t o = 0;
   auto take = [&](size_t b) {
@@ -68,14 +71,17 @@ static InferPlan infer_plan(const lina_moe_desc& dsc, int P, int mpd) {
   q.o_route = take(4 * route_scratch_ints(q.T, q.k, q.E));
   q.o_all = take(4 * (size_t)P * q.E);
   q.o_tab = take(4 * q.tab_ints());
-  q.o_vc = take(4 * segs);
-  q.o_mtp = take(4 * (segs + 1));
+  q.o_vc = take(4 * segs);                 // rows received per (source, hosted expert)
+  q.o_mtp = take(4 * ((size_t)mpd + 1));   // tile prefix over the hosted experts
+  q.o_gvc = take(4 * (size_t)mpd);         // rows per hosted expert (all sources)
   q.o_segx = take(4 * (size_t)mpd);
   q.o_arow = take(4 * Tk);
   q.o_send = take(Tk * q.d * q.dt);
-  q.o_recv = take(segs * q.Cmax * q.d * q.dt);
-  q.o_h = take(segs * q.Cmax * q.f * q.dt);
-  q.o_o = take(segs * q.Cmax * q.d * q.dt);
+  q.o_recv = take((size_t)P * Tk * q.d * q.dt);          // source-major receive
+  q.o_gin = take((size_t)mpd * q.Cmax * q.d * q.dt);     // expert-major GEMM input
+  q.o_h = take((size_t)mpd * q.Cmax * q.f * q.dt);
+  q.o_o = take((size_t)mpd * q.Cmax * q.d * q.dt);
+  q.o_back2 = take((size_t)P * Tk * q.d * q.dt);         // outputs regrouped source-major
   q.o_back = take(Tk * q.d * q.dt);
   q.total = o;
   return q;
@@ -117,17 +123,22 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   int* tab = (int*)(w + q.o_tab);
   int* vc = (int*)(w + q.o_vc);
   int* mtp = (int*)(w + q.o_mtp);
+  int* gvc = (int*)(w + q.o_gvc);
   int* segx = (int*)(w + q.o_segx);
   int* arow = (int*)(w + q.o_arow);
   char* send = w + q.o_send;
   char* recv = w + q.o_recv;
+  char* gin = w + q.o_gin;
   char* hbuf = w + q.o_h;
   char* obuf = w + q.o_o;
+  char* back2 = w + q.o_back2;
   char* back = w + q.o_back;
   const int T = q.T, E = q.E, k = q.k, d = q.d, f = q.f, dt = q.dt;
   const int dtype = desc.dtype == LINA_BF16 ? 1 : 0;
   const ncclDataType_t ndt = dtype ? ncclBfloat16 : ncclFloat32;
 
+  trace_flush(cm);
+  trace_mark(cm, s, "inf:start");
   // ---- gate, dropless slots, counts (S1, S2 with C = T)
   launch_gate_topk(dtype, tokens, gate_w, T, d, E, k, 1, probs, idx, gate, s);
   launch_route(idx, T, k, E, std::max(T, 1), (int*)(w + q.o_route), slot, counts, kept, tokof, s);
@@ -136,8 +147,9 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   } else {
     LINA_CUDA_CHECK(cudaMemcpyAsync(allc, counts, 4 * (size_t)E, cudaMemcpyDeviceToDevice, s));
   }
-  const size_t ctrl_ints = (size_t)P * E + q.tab_ints() + (size_t)P * mpd + (P * mpd + 1) + mpd;
+  const size_t ctrl_ints = (size_t)P * E + q.tab_ints() + (size_t)P * mpd + (mpd + 1) + 2 * (size_t)mpd;
   int* host = pinned(cm, ctrl_ints);
+  trace_mark(cm, s, "inf:gate+route+counts");
   LINA_CUDA_CHECK(cudaMemcpyAsync(host, allc, 4 * (size_t)P * E, cudaMemcpyDeviceToHost, s));
   LINA_CUDA_CHECK(cudaStreamSynchronize(s));
   std::vector<int> cnt(host, host + (size_t)P * E);  // cnt[src*E + e]
@@ -187,8 +199,10 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
     return split[i];
   };
   std::vector<int> nsend((size_t)P * E, 0), soff((size_t)P * E, 0), nrecv((size_t)P * mpd, 0);
+  std::vector<int> dv_off(P, 0), dv_cnt(P, 0);  // this rank's block for each device (one message)
   int off = 0;
-  for (int dv = 0; dv < P; ++dv)
+  for (int dv = 0; dv < P; ++dv) {
+    dv_off[dv] = off;
     for (int i = 0; i < mpd; ++i) {
       const int e = hosted[(size_t)dv * mpd + i];
       if (e < 0) continue;
@@ -196,18 +210,28 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
       nsend[(size_t)dv * E + e] = tokens_to(rank, e, dv);
       off += nsend[(size_t)dv * E + e];
     }
-  int maxrows = 0;
-  for (int src = 0; src < P; ++src)
+    dv_cnt[dv] = off - dv_off[dv];
+  }
+  std::vector<int> src_off(P, 0), src_cnt(P, 0), tot(mpd, 0);  // source-major receive blocks
+  int roff = 0, maxseg = 0;
+  for (int src = 0; src < P; ++src) {
+    src_off[src] = roff;
     for (int h = 0; h < mpd; ++h) {
       const int e = hosted[(size_t)rank * mpd + h];
       const int n = e < 0 ? 0 : tokens_to(src, e, rank);
       nrecv[(size_t)src * mpd + h] = n;
-      maxrows = std::max(maxrows, n);
+      tot[h] += n;
+      roff += n;
+      maxseg = std::max(maxseg, n);
     }
+    src_cnt[src] = roff - src_off[src];
+  }
+  int maxrows = 0;
+  for (int h = 0; h < mpd; ++h) maxrows = std::max(maxrows, tot[h]);
   const int Cm = std::max(128, (maxrows + 127) / 128 * 128);
   if ((size_t)Cm > q.Cmax) throw StatusError{LINA_ERR_WORKSPACE, "receive segment exceeds workspace"};
 
-  // ---- routing tables to the device (one H2D copy)
+  // ---- routing tables to the device
   int* h = host;
   int* h_tab = h;
   for (int e = 0; e < E; ++e) h_tab[e] = r[e];
@@ -216,61 +240,53 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   for (int e = 0; e < E; ++e) h_tab[E + 2 * (size_t)E * P + e] = cnt[(size_t)rank * E + e];
   int* h_vc = h_tab + q.tab_ints();
   int* h_mtp = h_vc + (size_t)P * mpd;
-  int* h_segx = h_mtp + (P * mpd + 1);
+  int* h_gvc = h_mtp + (mpd + 1);
+  int* h_segx = h_gvc + mpd;
   const int rows = tc_tile_rows();
+  for (int i = 0; i < P * mpd; ++i) h_vc[i] = nrecv[i];
   int run = 0;
-  for (int i = 0; i < P * mpd; ++i) {
-    h_vc[i] = nrecv[i];
+  for (int i = 0; i < mpd; ++i) {
+    h_gvc[i] = tot[i];
     h_mtp[i] = run;
-    run += (nrecv[i] + rows - 1) / rows;
+    run += (tot[i] + rows - 1) / rows;
   }
-  h_mtp[P * mpd] = run;
+  h_mtp[mpd] = run;
   for (int i = 0; i < mpd; ++i) h_segx[i] = std::max(0, hosted[(size_t)rank * mpd + i]);
-  // tab, vc, mtp, segx are adjacent in the workspace in the same order
   LINA_CUDA_CHECK(cudaMemcpyAsync(tab, h_tab, 4 * q.tab_ints(), cudaMemcpyHostToDevice, s));
   LINA_CUDA_CHECK(cudaMemcpyAsync(vc, h_vc, 4 * (size_t)P * mpd, cudaMemcpyHostToDevice, s));
-  LINA_CUDA_CHECK(cudaMemcpyAsync(mtp, h_mtp, 4 * (size_t)(P * mpd + 1), cudaMemcpyHostToDevice, s));
+  LINA_CUDA_CHECK(cudaMemcpyAsync(mtp, h_mtp, 4 * (size_t)(mpd + 1), cudaMemcpyHostToDevice, s));
+  LINA_CUDA_CHECK(cudaMemcpyAsync(gvc, h_gvc, 4 * (size_t)mpd, cudaMemcpyHostToDevice, s));
   LINA_CUDA_CHECK(cudaMemcpyAsync(segx, h_segx, 4 * (size_t)mpd, cudaMemcpyHostToDevice, s));
 
+  trace_mark(cm, s, "inf:plan+tables(host)");
   // ---- replica-routed permute and the unequal-split all-to-all
   launch_infer_permute(dtype, tokens, idx, slot, tab, T, k, d, E, P, rank, send, arow, s);
-  auto seg_ptr = [&](char* base, int src, int hh, int width) {
-    return base + ((size_t)(src * mpd + hh) * Cm) * width * dt;
-  };
+  trace_mark(cm, s, "inf:permute");
+  // one message per peer: my block for device dv -> its source-major receive block
   if (P > 1) {
     LINA_NCCL_CHECK(ncclGroupStart());
     for (int dv = 0; dv < P; ++dv)
-      for (int i = 0; i < mpd; ++i) {
-        const int e = hosted[(size_t)dv * mpd + i];
-        if (e < 0 || nsend[(size_t)dv * E + e] == 0) continue;
-        LINA_NCCL_CHECK(ncclSend(send + (size_t)soff[(size_t)dv * E + e] * d * dt,
-                                 (size_t)nsend[(size_t)dv * E + e] * d, ndt, dv, cm->ep_disp, s));
-      }
+      if (dv_cnt[dv])
+        LINA_NCCL_CHECK(ncclSend(send + (size_t)dv_off[dv] * d * dt, (size_t)dv_cnt[dv] * d, ndt, dv, cm->ep_disp, s));
     for (int src = 0; src < P; ++src)
-      for (int hh = 0; hh < mpd; ++hh) {
-        const int n = nrecv[(size_t)src * mpd + hh];
-        if (n) LINA_NCCL_CHECK(ncclRecv(seg_ptr(recv, src, hh, d), (size_t)n * d, ndt, src, cm->ep_disp, s));
-      }
+      if (src_cnt[src])
+        LINA_NCCL_CHECK(ncclRecv(recv + (size_t)src_off[src] * d * dt, (size_t)src_cnt[src] * d, ndt, src,
+                                 cm->ep_disp, s));
     LINA_NCCL_CHECK(ncclGroupEnd());
-  } else {
-    for (int hh = 0; hh < mpd; ++hh) {
-      const int e = hosted[hh];
-      const int n = nrecv[hh];
-      if (e < 0 || n == 0) continue;
-      LINA_CUDA_CHECK(cudaMemcpyAsync(seg_ptr(recv, 0, hh, d), send + (size_t)soff[e] * d * dt,
-                                      (size_t)n * d * dt, cudaMemcpyDeviceToDevice, s));
-    }
+  } else if (dv_cnt[0]) {
+    LINA_CUDA_CHECK(cudaMemcpyAsync(recv, send, (size_t)dv_cnt[0] * d * dt, cudaMemcpyDeviceToDevice, s));
   }
-
+  launch_regroup(dtype, recv, gin, vc, P, mpd, Cm, d, maxseg, true, s);
+  trace_mark(cm, s, "inf:a2av dispatch");
   // ---- expert FFN over the hosted experts (S5; one launch per GEMM for every segment)
   RowGemm g1{};
-  g1.A = recv;
+  g1.A = gin;
   g1.B = w1_all;
   g1.D = hbuf;
-  g1.vcount = vc;
+  g1.vcount = gvc;
   g1.mtp = mtp;
   g1.seg0 = 0;
-  g1.nseg = P * mpd;
+  g1.nseg = mpd;
   g1.El = mpd;
   g1.Cm = Cm;
   g1.N = f;
@@ -287,33 +303,26 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   launch_expert_row_gemm(dtype, g1, true, kEpiRelu, s);
   launch_expert_row_gemm(dtype, g2, true, kEpiNone, s);
   prof_end(cm, s, 2);
+  trace_mark(cm, s, "inf:expert GEMMs");
 
-  // ---- second all-to-all (expert outputs back to their sources) and combine
+  // ---- second all-to-all (expert outputs back to their sources, one message per peer)
+  launch_regroup(dtype, obuf, back2, vc, P, mpd, Cm, d, maxseg, false, s);
   if (P > 1) {
     LINA_NCCL_CHECK(ncclGroupStart());
     for (int src = 0; src < P; ++src)
-      for (int hh = 0; hh < mpd; ++hh) {
-        const int n = nrecv[(size_t)src * mpd + hh];
-        if (n) LINA_NCCL_CHECK(ncclSend(seg_ptr(obuf, src, hh, d), (size_t)n * d, ndt, src, cm->ep_comb, s));
-      }
+      if (src_cnt[src])
+        LINA_NCCL_CHECK(ncclSend(back2 + (size_t)src_off[src] * d * dt, (size_t)src_cnt[src] * d, ndt, src,
+                                 cm->ep_comb, s));
     for (int dv = 0; dv < P; ++dv)
-      for (int i = 0; i < mpd; ++i) {
-        const int e = hosted[(size_t)dv * mpd + i];
-        if (e < 0 || nsend[(size_t)dv * E + e] == 0) continue;
-        LINA_NCCL_CHECK(ncclRecv(back + (size_t)soff[(size_t)dv * E + e] * d * dt,
-                                 (size_t)nsend[(size_t)dv * E + e] * d, ndt, dv, cm->ep_comb, s));
-      }
+      if (dv_cnt[dv])
+        LINA_NCCL_CHECK(ncclRecv(back + (size_t)dv_off[dv] * d * dt, (size_t)dv_cnt[dv] * d, ndt, dv, cm->ep_comb, s));
     LINA_NCCL_CHECK(ncclGroupEnd());
-  } else {
-    for (int hh = 0; hh < mpd; ++hh) {
-      const int e = hosted[hh];
-      const int n = nrecv[hh];
-      if (e < 0 || n == 0) continue;
-      LINA_CUDA_CHECK(cudaMemcpyAsync(back + (size_t)soff[e] * d * dt, seg_ptr(obuf, 0, hh, d),
-                                      (size_t)n * d * dt, cudaMemcpyDeviceToDevice, s));
-    }
+  } else if (dv_cnt[0]) {
+    LINA_CUDA_CHECK(cudaMemcpyAsync(back, back2, (size_t)dv_cnt[0] * d * dt, cudaMemcpyDeviceToDevice, s));
   }
+  trace_mark(cm, s, "inf:a2av combine");
   launch_combine_rows(dtype, back, arow, gate, T, k, d, out, s);
+  trace_mark(cm, s, "inf:combine");
 
   if (plan_out) {
     plan_out->num_experts = E;

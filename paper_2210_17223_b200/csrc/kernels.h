@@ -110,6 +110,9 @@ void launch_infer_permute(int dtype, const void* X, const int* idx, const int* s
                           cudaStream_t st);
 void launch_combine_rows(int dtype, const void* Back, const int* arow, const float* gate, int T, int k,
                          int d, void* Y, cudaStream_t st);
+// source-major [P][mpd][rows] <-> expert-major [mpd][Cm] rows (nrecv[P][mpd] device table)
+void launch_regroup(int dtype, const void* src, void* dst, const int* nrecv, int P, int mpd, int Cm, int d,
+                    int max_rows, bool to_expert_major, cudaStream_t st);
 
 void launch_row_gemm_simt(int dtype, const RowGemm& p, bool b_kmajor, int epi, cudaStream_t s);
 void launch_wgrad_simt(int dtype, const WGrad& p, cudaStream_t s);

@@ -12,6 +12,13 @@
 //                block; copies the token row (16-byte vectors) and records the row for
 //                the combine.
 // combine_rows : y_t = Σ_j g_tj · Back[arow[t,j]] (fp32 accumulate, j ascending, R9).
+// regroup      : the rows a device receives arrive source-major (one message per peer:
+//                [src][hosted expert][rows]); the expert GEMMs want them expert-major
+//                ([hosted expert][Cm] with every source's rows contiguous), so each
+//                expert is one segment padded once to the tile height instead of once
+//                per source.  The same kernel moves the outputs back.
+#include <algorithm>
+
 #include "../common.h"
 #include "../kernels.h"
 
@@ -83,6 +90,35 @@ __global__ void combine_rows_kernel(const T* __restrict__ Back, const int* __res
 
 inline int blocks_for_warps(long long warps) { return (int)((warps * 32 + 255) / 256); }
 
+
+// rows of segment (src, hh): source-major at off_sm(src, hh) (row-major prefix over
+// [P][mpd]); expert-major at hh*Cm + Σ_{s' < src} nrecv[s'][hh].
+template <typename T>
+__global__ void __launch_bounds__(256) regroup_kernel(const T* __restrict__ src_buf, T* __restrict__ dst_buf,
+                                                      const int* __restrict__ nrecv, int P, int mpd, int Cm,
+                                                      int d, int to_expert_major) {
+  __shared__ long long off_sm, off_em;
+  __shared__ int nrows;
+  const int seg = blockIdx.y, sidx = seg / mpd, hh = seg % mpd;
+  if (threadIdx.x == 0) {
+    long long a = 0, b = 0;
+    for (int i = 0; i < seg; ++i) a += nrecv[i];
+    for (int s2 = 0; s2 < sidx; ++s2) b += nrecv[s2 * mpd + hh];
+    off_sm = a;
+    off_em = (long long)hh * Cm + b;
+    nrows = nrecv[seg];
+  }
+  __syncthreads();
+  constexpr int V = 16 / sizeof(T);
+  const int nv = d / V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * 8 + warp; i < nrows; i += gridDim.x * 8) {
+    const long long rs = off_sm + i, re = off_em + i;
+    const uint4* from = reinterpret_cast<const uint4*>(src_buf + (size_t)(to_expert_major ? rs : re) * d);
+    uint4* to = reinterpret_cast<uint4*>(dst_buf + (size_t)(to_expert_major ? re : rs) * d);
+    for (int v = lane; v < nv; v += 32) to[v] = from[v];
+  }
+}
 }  // namespace
 
 void launch_infer_permute(int dtype, const void* X, const int* idx, const int* slot, const int* tab,
@@ -111,4 +147,19 @@ void launch_combine_rows(int dtype, const void* Back, const int* arow, const flo
   LINA_LAUNCH_CHECK();
 }
 
+}  // namespace lina
+
+namespace lina {
+void launch_regroup(int dtype, const void* src, void* dst, const int* nrecv, int P, int mpd, int Cm, int d,
+                    int max_rows, bool to_expert_major, cudaStream_t st) {
+  if (max_rows <= 0 || P * mpd == 0) return;
+  dim3 grid(std::min(64, (max_rows + 7) / 8), P * mpd);
+  if (dtype == 0)
+    regroup_kernel<float><<<grid, 256, 0, st>>>((const float*)src, (float*)dst, nrecv, P, mpd, Cm, d,
+                                               to_expert_major ? 1 : 0);
+  else
+    regroup_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, nrecv,
+                                                         P, mpd, Cm, d, to_expert_major ? 1 : 0);
+  LINA_LAUNCH_CHECK();
+}
 }  // namespace lina
