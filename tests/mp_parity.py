@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--seed", type=int, default=77)
     ap.add_argument("--check-chunks", type=int, default=0, help="also run with this n_chunks and compare bitwise")
+    ap.add_argument("--poison", action="store_true", help="start from NaN-filled saved/workspace buffers")
     a = ap.parse_args()
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -52,6 +53,11 @@ def main():
     def run(n_chunks):
         layer = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, cfg.capacity(),
                               n_chunks, tdt, dev)
+        if a.poison:  # every byte the layer reads must be one it (or a peer) wrote this step
+            layer.saved.fill_(0xFF)
+            layer.workspace.fill_(0xFF)
+            torch.cuda.synchronize()
+            dist.barrier()
         x = torch.from_numpy(X).to(tdt).to(dev)
         wg = torch.from_numpy(Wg).to(dev)
         w1 = torch.from_numpy(W1).to(tdt).to(dev)

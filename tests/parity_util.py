@@ -23,13 +23,18 @@ def to_dev(a, dtype=None, device="cuda"):
 
 
 def gpu_layer(cfg: li.LayerConfig, n_chunks: int, X, Wg, W1, W2, dY=None, capacity=None,
-              override=None, comm=None):
-    """Run forward (+ backward when dY is given) of one rank at P=1 through the C ABI."""
+              override=None, comm=None, poison=False):
+    """Run forward (+ backward when dY is given) of one rank at P=1 through the C ABI.
+    poison: fill the saved and workspace buffers with 0xFF bytes (NaN in fp32 and bf16)
+    first, so any read of a byte the layer did not write shows up in the results."""
     import paper_2210_17223_b200 as lina
     comm = comm or lina.Comm(1, 0, 0)
     C = cfg.capacity() if capacity is None else capacity
     dt = tdtype(cfg.dtype)
     layer = lina.MoELayer(comm, X.shape[0], cfg.d_model, cfg.d_ffn, cfg.num_experts, cfg.k, C, n_chunks, dt)
+    if poison:
+        layer.saved.fill_(0xFF)
+        layer.workspace.fill_(0xFF)
     x = to_dev(X, dt); wg = to_dev(Wg, torch.float32); w1 = to_dev(W1, dt); w2 = to_dev(W2, dt)
     if override is not None:
         layer.route_t["idx"].copy_(to_dev(override[0].astype(np.int32)))

@@ -66,6 +66,18 @@ def test_c2_reduced_bf16(n_chunks):
     compare(cfg, g, o)
 
 
+@pytest.mark.parametrize("n_chunks", [1, 3])
+def test_c2_poisoned_workspace(n_chunks):
+    """Saved state and workspace start as NaN bytes: the layer must only read what it wrote
+    (padding rows it leaves unwritten, are never read as data)."""
+    cfg, X, Wg, W1, W2, dY = _case("C2", tokens=512)
+    g = gpu_layer(cfg, n_chunks, X, Wg, W1, W2, dY, poison=True)
+    for k in ("y", "dx", "dwg", "dw1", "dw2"):
+        assert np.isfinite(g[k]).all(), f"{k} has non-finite values"
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY)
+    compare(cfg, g, o)
+
+
 def test_c3_reduced_bf16():
     """configs[2] shapes (E=16, top-2, d=1024, f=4096, capacity 1.25) at 256 tokens."""
     cfg, X, Wg, W1, W2, dY = _case("C3", tokens=256)
