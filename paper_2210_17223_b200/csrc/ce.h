@@ -13,7 +13,9 @@ class CeTransport {
   // flag kinds: READY (at the receiver) and PULLED (at the sender) per exchange
   enum { kReadyFwdD = 0, kReadyFwdC = 1, kReadyBwdD = 2, kReadyBwdC = 3,
          kPulledFwdD = 4, kPulledFwdC = 5, kPulledBwdD = 6, kPulledBwdC = 7,
-         kFreeFwd = 8, kFreeBwd = 9, kKinds = 10 };
+         kFreeFwd = 8, kFreeBwd = 9,
+         // fused transport (in-kernel signals; rounds from the device counters below)
+         kFReadyFwdD = 10, kFReadyFwdC = 11, kFReadyBwdD = 12, kFReadyBwdC = 13, kKinds = 14 };
   static constexpr int kMaxChunks = 32;
 
   explicit CeTransport(lina_comm* cm);  // collective (allgathers the flag-array handles)
@@ -36,6 +38,9 @@ class CeTransport {
   const uint32_t* slots(int kind) const { return flags_ + slot(kind, 0, 0); }
   uint32_t* const* peer_slots(int kind);
   unsigned int* done_counter(int site) const { return done_ + site; }
+  // device round counters of the fused transport: [0] forward, [1] backward
+  uint32_t* round_fwd() const { return rounds_; }
+  uint32_t* round_bwd() const { return rounds_ + 1; }
   static constexpr int kDoneSites = 16;
   cudaStream_t disp_stream(int peer) const { return disp_[peer]; }
   cudaStream_t comb_stream(int peer) const { return comb_[peer]; }
@@ -60,6 +65,7 @@ class CeTransport {
   uint32_t* flags_ = nullptr;
   size_t nflags_ = 0;
   unsigned int* done_ = nullptr;
+  uint32_t* rounds_ = nullptr;
   std::vector<uint32_t**> peer_slots_;
   std::vector<char*> peer_flags_;
   std::vector<cudaStream_t> disp_, comb_;

@@ -46,6 +46,8 @@ size_t route_scratch_ints(int T, int k, int E);
 void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int* slot, int* counts,
                   int* kept, int* tok_of, cudaStream_t s);
 // vcount[(c*P + s)*El + el] = clamp(recv_kept[s*El + el] - b_c, 0, Cc)
+// A 1-CTA kernel that waits for sig's flags (sig.post ignored).
+void launch_sig_wait(const PeerSignal& sig, cudaStream_t s);
 // sig: every CTA first waits for the peers' counts (READY of the dispatch)
 void launch_vcount(const int* recv_kept, int P, int El, int C, int n, int* vcount, cudaStream_t s,
                    const PeerSignal* sig = nullptr);

@@ -22,6 +22,8 @@
 //       batches of 4, folded in shared memory in a fixed tree order; each token split
 //       writes one partial, reduced afterwards in a fixed order (deterministic, no
 //       float atomics).
+#include <algorithm>
+
 #include "../common.h"
 #include "../kernels.h"
 #include "../signal.h"
@@ -164,48 +166,53 @@ __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe
     }
   }
   __syncthreads();
-  if (col >= d) return;
-  float acc[4][8];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
-#pragma unroll
-    for (int j = 0; j < KM; ++j) {
-      float x[8];
-      if constexpr (sizeof(T) == 2) {
-        load16(&raw[i][j][0], x, (const __nv_bfloat16*)nullptr);
-      } else {
-        load16(&raw[i][j][0], x, (const float*)nullptr);
-        load16(&raw[i][j][NV - 1], x + 4, (const float*)nullptr);
-      }
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc[i][c] += x[c];
-    }
-  }
-  // + dL · Wgᵀ
-  for (int e = 0; e < E; ++e) {
-    const float4 w0 = *reinterpret_cast<const float4*>(sW + e * kDxCols + cg * 4);
-    const float4 w1 = *reinterpret_cast<const float4*>(sW + e * kDxCols + 128 + cg * 4);
-    const float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
+  if (col < d) {
+    float acc[4][8];
+  #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float l = sL[(tg * 4 + i) * E + e];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc[i][c] = fmaf(l, w[c], acc[i][c]);
+  #pragma unroll
+      for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
+  #pragma unroll
+      for (int j = 0; j < KM; ++j) {
+        float x[8];
+        if constexpr (sizeof(T) == 2) {
+          load16(&raw[i][j][0], x, (const __nv_bfloat16*)nullptr);
+        } else {
+          load16(&raw[i][j][0], x, (const float*)nullptr);
+          load16(&raw[i][j][NV - 1], x + 4, (const float*)nullptr);
+        }
+  #pragma unroll
+        for (int c = 0; c < 8; ++c) acc[i][c] += x[c];
+      }
+    }
+    // + dL · Wgᵀ
+    for (int e = 0; e < E; ++e) {
+      const float4 w0 = *reinterpret_cast<const float4*>(sW + e * kDxCols + cg * 4);
+      const float4 w1 = *reinterpret_cast<const float4*>(sW + e * kDxCols + 128 + cg * 4);
+      const float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+  #pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float l = sL[(tg * 4 + i) * E + e];
+  #pragma unroll
+        for (int c = 0; c < 8; ++c) acc[i][c] = fmaf(l, w[c], acc[i][c]);
+      }
+    }
+  #pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int t = t0 + tg * 4 + i;
+      if (t >= Tn) continue;
+      T* dst = dX + (size_t)t * d + col;
+      if constexpr (sizeof(T) == 2) {
+        store16(dst, acc[i], (__nv_bfloat16*)nullptr);
+      } else {
+        store16(dst, acc[i], (float*)nullptr);
+        store16(dst + 4, acc[i] + 4, (float*)nullptr);
+      }
     }
   }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int t = t0 + tg * 4 + i;
-    if (t >= Tn) continue;
-    T* dst = dX + (size_t)t * d + col;
-    if constexpr (sizeof(T) == 2) {
-      store16(dst, acc[i], (__nv_bfloat16*)nullptr);
-    } else {
-      store16(dst, acc[i], (float*)nullptr);
-      store16(dst + 4, acc[i] + 4, (float*)nullptr);
-    }
+  if (sig.bump) {  // the backward's last kernel closes its round
+    __syncthreads();
+    if (tid == 0) sig_bump_last(sig);
   }
 }
 
@@ -357,7 +364,7 @@ template <typename T, int KT>
 static void launch_dx_t(const void* dXe, const int* idx, const int* slot, const float* probs,
                         const float* gate, const float* dg, const float* Wg, int Tn, int k, int d, int E,
                         int C, int n, int Cm, void* dX, const PeerSignal& sig, cudaStream_t s) {
-  dim3 grid((d + kDxCols - 1) / kDxCols, (Tn + kDxTok - 1) / kDxTok);
+  dim3 grid((d + kDxCols - 1) / kDxCols, std::max(1, (Tn + kDxTok - 1) / kDxTok));
   const size_t smem = sizeof(float) * ((size_t)E * kDxCols + kDxTok * E);
   static bool set = false;
   if (!set) {
@@ -372,7 +379,7 @@ static void launch_dx_t(const void* dXe, const int* idx, const int* slot, const 
 void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* probs,
                const float* gate, const float* dg, const float* Wg, int T, int k, int d, int E, int C,
                int n, int Cm, void* dX, cudaStream_t s, const PeerSignal* sig) {
-  if (T <= 0) return;  // (a rank without tokens has nothing to wait for either)
+  if (T <= 0 && !sig) return;  // (with a signal, one CTA still closes the round)
   const PeerSignal sg = sig ? *sig : PeerSignal{};
   auto go = [&](auto tag) {
     using ET = decltype(tag);

@@ -159,22 +159,11 @@ __global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ X, c
   }
 }
 
-// combine: y_t = Σ_{j kept, ascending} g_tj · Recv[row(t, j)] (fp32 accumulation).  A warp
-// owns TP = U / k tokens (U = kLoadsPerLane / NVL rows in flight); lane q < TP*k resolves
-// pair q, then every row load is issued before the sums.
 template <typename T, int NVL, int KT>
-__global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ Recv, const int* __restrict__ idx,
-                                                      const int* __restrict__ slot,
-                                                      const float* __restrict__ gate, int Tn, int k, int d,
-                                                      int E, int C, int n, int Cm, T* __restrict__ Y,
-                                                      PeerSignal sig) {
-  // fused transport: this rank's backward receive buffers are free again (block 0 posts);
-  // the peers' returned expert outputs have landed (every CTA waits)
-  if (sig.post && blockIdx.x == 0 && threadIdx.x == 0) sig_post(sig);
-  if (sig.wait) {
-    if (threadIdx.x == 0) sig_wait(sig);
-    __syncthreads();
-  }
+__device__ __forceinline__ void combine_tokens(const T* __restrict__ Recv, const int* __restrict__ idx,
+                                               const int* __restrict__ slot, const float* __restrict__ gate,
+                                               int Tn, int k, int d, int E, int C, int n, int Cm,
+                                               T* __restrict__ Y) {
   constexpr int NL = NVL > 0 ? NVL : 1;  // (NVL = 0 is never launched)
   constexpr int U = kLoadsPerLane / NL;
   constexpr int TP = U / KT > 0 ? U / KT : 1;
@@ -236,20 +225,34 @@ __global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ Recv
   }
 }
 
-// generic k / wide rows: one warp per token, strided loop
-template <typename T>
-__global__ void combine_loop_kernel(const T* __restrict__ Recv, const int* __restrict__ idx,
-                                    const int* __restrict__ slot, const float* __restrict__ gate,
-                                    int Tn, int k, int d, int E, int C, int n, int Cm,
-                                    T* __restrict__ Y, PeerSignal sig) {
-  if (sig.post && blockIdx.x == 0 && threadIdx.x == 0) sig_post(sig);
+// combine: y_t = Σ_{j kept, ascending} g_tj · Recv[row(t, j)] (fp32 accumulation).  A warp
+// owns TP = U / k tokens (U = kLoadsPerLane / NVL rows in flight); lane q < TP*k resolves
+// pair q, then every row load is issued before the sums.
+template <typename T, int NVL, int KT>
+__global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ Recv, const int* __restrict__ idx,
+                                                      const int* __restrict__ slot,
+                                                      const float* __restrict__ gate, int Tn, int k, int d,
+                                                      int E, int C, int n, int Cm, T* __restrict__ Y,
+                                                      PeerSignal sig) {
+  // fused transport: this rank's backward receive buffers are free again (block 0 posts);
+  // the peers' returned expert outputs have landed (every CTA waits)
+  if (blockIdx.x == 0 && threadIdx.x == 0) sig_post(sig);
   if (sig.wait) {
     if (threadIdx.x == 0) sig_wait(sig);
     __syncthreads();
   }
-  const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= Tn) return;
+  combine_tokens<T, NVL, KT>(Recv, idx, slot, gate, Tn, k, d, E, C, n, Cm, Y);
+  if (sig.bump) {  // the forward's last kernel closes its round
+    __syncthreads();
+    if (threadIdx.x == 0) sig_bump_last(sig);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void combine_token_loop(const T* __restrict__ Recv, const int* __restrict__ idx,
+                                                   const int* __restrict__ slot, const float* __restrict__ gate,
+                                                   long long t, int lane, int k, int d, int E, int C, int n,
+                                                   int Cm, T* __restrict__ Y) {
   constexpr int V = 16 / sizeof(T);
   const T* rowp[8];
   float g[8];
@@ -274,6 +277,26 @@ __global__ void combine_loop_kernel(const T* __restrict__ Recv, const int* __res
       for (int i = 0; i < V; ++i) acc[i] = fmaf(g[q], x[i], acc[i]);
     }
     store16(Y + t * d + v * V, acc, (T*)nullptr);
+  }
+}
+
+// generic k / wide rows: one warp per token, strided loop
+template <typename T>
+__global__ void combine_loop_kernel(const T* __restrict__ Recv, const int* __restrict__ idx,
+                                    const int* __restrict__ slot, const float* __restrict__ gate,
+                                    int Tn, int k, int d, int E, int C, int n, int Cm,
+                                    T* __restrict__ Y, PeerSignal sig) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) sig_post(sig);
+  if (sig.wait) {
+    if (threadIdx.x == 0) sig_wait(sig);
+    __syncthreads();
+  }
+  const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t < Tn) combine_token_loop<T>(Recv, idx, slot, gate, t, lane, k, d, E, C, n, Cm, Y);
+  if (sig.bump) {
+    __syncthreads();
+    if (threadIdx.x == 0) sig_bump_last(sig);
   }
 }
 

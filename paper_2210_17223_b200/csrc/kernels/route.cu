@@ -100,6 +100,13 @@ __global__ void vcount_kernel(const int* __restrict__ recv_kept, int P, int El, 
   vcount[i] = v < 0 ? 0 : (v > Cc ? Cc : v);
 }
 
+// One thread waits for the peers' flags; the consumer kernel follows in stream order.
+// Waiting in a 1-CTA kernel (not in every CTA of the consumer) keeps the SMs free for
+// kernels the peers' progress may depend on (e.g. an NCCL allreduce on another stream).
+__global__ void sig_wait_kernel(PeerSignal sig) {
+  if (threadIdx.x == 0) sig_wait(sig);
+}
+
 __global__ void mtile_prefix_kernel(const int* __restrict__ vcount, int n, int nseg, int rows,
                                     int* __restrict__ mtp) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -117,6 +124,12 @@ __global__ void mtile_prefix_kernel(const int* __restrict__ vcount, int n, int n
 void launch_mtile_prefix(const int* vcount, int n, int nseg, int rows, int* mtp, cudaStream_t s) {
   if (n <= 0) return;
   mtile_prefix_kernel<<<(n + 63) / 64, 64, 0, s>>>(vcount, n, nseg, rows, mtp);
+  LINA_LAUNCH_CHECK();
+}
+
+void launch_sig_wait(const PeerSignal& sig, cudaStream_t s) {
+  if (!sig.wait) return;
+  sig_wait_kernel<<<1, 32, 0, s>>>(sig);
   LINA_LAUNCH_CHECK();
 }
 

@@ -301,8 +301,10 @@ void backward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, co
 // by the first kernel after the buffers' last reader, READY by the last CTA of the
 // producing kernel — and acquired by the first consuming kernel (one spinning thread
 // per CTA).  No stream memory operation and no extra launch on the critical path.
-PeerSignal make_sig(lina_comm* cm, int wait_kind, uint32_t wait_value, int post_kind, uint32_t post_value,
-                    int done_site = -1) {
+// Signal of one kernel: wait for `wait_kind` at *wait_round + wait_add, publish `post_kind`
+// at *post_round + post_add, optionally close the pass's round (bump) in its last CTA.
+PeerSignal make_sig(lina_comm* cm, int wait_kind, const uint32_t* wait_round, uint32_t wait_add, int post_kind,
+                    const uint32_t* post_round, uint32_t post_add, int done_site = -1, uint32_t* bump = nullptr) {
   CeTransport& ce = *cm->ce;
   PeerSignal g;
   g.P = cm->world;
@@ -310,16 +312,26 @@ PeerSignal make_sig(lina_comm* cm, int wait_kind, uint32_t wait_value, int post_
   g.stride = CeTransport::kMaxChunks;
   if (wait_kind >= 0) {
     g.wait = ce.slots(wait_kind);
-    g.wait_value = wait_value;
+    g.wait_round = wait_round;
+    g.wait_add = wait_add;
   }
   if (post_kind >= 0) {
     g.post = ce.peer_slots(post_kind);
-    g.post_value = post_value;
-    g.done = done_site >= 0 ? ce.done_counter(done_site) : nullptr;
+    g.post_round = post_round;
+    g.post_add = post_add;
   }
+  g.done = done_site >= 0 ? ce.done_counter(done_site) : nullptr;
+  g.bump = bump;
   return g;
 }
-enum { kSiteDispFwd = 0, kSiteCombFwd = 1, kSiteDispBwd = 2, kSiteCombBwd = 3 };
+// The wait part of a signal runs as its own 1-CTA kernel (launch_sig_wait); the consumer
+// gets the rest.
+PeerSignal no_wait(PeerSignal g) {
+  g.wait = nullptr;
+  g.wait_round = nullptr;
+  return g;
+}
+enum { kSiteDispFwd = 0, kSiteCombFwd = 1, kSiteDispBwd = 2, kSiteCombBwd = 3, kSiteFwdEnd = 4, kSiteBwdEnd = 5 };
 
 bool fused_ok(const lina_comm* cm, const Plan& p) {
   return cm->transport == 2 && cm->ce && p.P > 1 && p.bf16 && p.d % 256 == 0 && p.f % 256 == 0 &&
@@ -332,15 +344,15 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   using CT = CeTransport;
   CeTransport& ce = *cm->ce;
   const int dtype = 1, P = p.P, me = cm->rank, n = p.n;
-  const uint32_t seq = ++ce.seq_fwd;
   const bool override_r = route && route->override_routing;
+  uint32_t* rf = ce.round_fwd();  // this forward's round is *rf + 1 (closed by the combine kernel)
   trace_mark(cm, s, "fwd:start");
   if (override_r) {
     LINA_CUDA_CHECK(cudaMemcpyAsync(q.idx, route->idx, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
     LINA_CUDA_CHECK(cudaMemcpyAsync(q.gate, route->gate, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
   }
   // gate: block 0 posts FREE (my R, recv counts and Cb were last read by the previous backward)
-  const PeerSignal s_free = make_sig(cm, -1, 0, CT::kFreeFwd, seq);
+  const PeerSignal s_free = make_sig(cm, -1, nullptr, 0, CT::kFreeFwd, rf, 1);
   launch_gate_topk(dtype, tokens, gate_w, p.T, p.d, p.E, p.k, override_r ? 0 : 1, q.probs, q.idx, q.gate, s,
                    &s_free);
   launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr, q.kept,
@@ -349,9 +361,10 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   void* const* peer_R = ce.dev_ptrs(saved, p.s_R, s);
   void* const* peer_cnt = ce.dev_ptrs(saved, p.s_recvkept, s);
   // dispatch = permute into the owners' R (waits for their FREE, posts READY)
-  const PeerSignal s_disp = make_sig(cm, CT::kFreeFwd, seq, CT::kReadyFwdD, seq, kSiteDispFwd);
+  const PeerSignal s_disp = make_sig(cm, CT::kFreeFwd, rf, 1, CT::kFReadyFwdD, rf, 1, kSiteDispFwd);
+  launch_sig_wait(s_disp, s);
   launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me, peer_R, peer_cnt,
-                      s_disp, s);
+                      no_wait(s_disp), s);
   trace_mark(cm, s, "permute(peer)");
   if (route) {
     if (route->idx && !override_r)
@@ -363,7 +376,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
     if (route->probs)
       LINA_CUDA_CHECK(cudaMemcpyAsync(route->probs, q.probs, 4 * (size_t)p.T * p.E, cudaMemcpyDeviceToDevice, s));
   }
-  const PeerSignal s_recv = make_sig(cm, CT::kReadyFwdD, seq, -1, 0);
+  const PeerSignal s_recv = make_sig(cm, CT::kFReadyFwdD, rf, 1, -1, nullptr, 0);
   launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s, &s_recv);
   launch_mtile_prefix(q.vcount, n, P * p.El, tc_tile_rows(), q.mtp, s);
   trace_mark(cm, s, "vcount");
@@ -382,7 +395,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   st.P = P;
   st.me = me;
   st.E = p.E;
-  const PeerSignal s_comb = make_sig(cm, -1, 0, CT::kReadyFwdC, seq, kSiteCombFwd);
+  const PeerSignal s_comb = make_sig(cm, -1, nullptr, 0, CT::kFReadyFwdC, rf, 1, kSiteCombFwd);
   prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
     row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask);
@@ -406,8 +419,11 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   prof_end(cm, s, 2 * n);
   // combine: block 0 posts the backward FREE (my dO / dXs were last read by the previous
   // backward), every CTA waits for the returned expert outputs
-  const PeerSignal s_out = make_sig(cm, CT::kReadyFwdC, seq, CT::kFreeBwd, seq);
-  launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, out, s, &s_out);
+  // (its last CTA closes the forward's round)
+  const PeerSignal s_out = make_sig(cm, CT::kFReadyFwdC, rf, 1, CT::kFreeBwd, rf, 1, kSiteFwdEnd, rf);
+  launch_sig_wait(s_out, s);
+  const PeerSignal s_out2 = no_wait(s_out);
+  launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, out, s, &s_out2);
   trace_mark(cm, s, "combine");
 }
 
@@ -417,15 +433,17 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   using CT = CeTransport;
   CeTransport& ce = *cm->ce;
   const int dtype = 1, P = p.P, me = cm->rank, n = p.n;
-  const uint32_t seq = ++ce.seq_bwd;
+  uint32_t* rf = ce.round_fwd();  // the last forward's round (closed)
+  uint32_t* rb = ce.round_bwd();  // this backward's round is *rb + 1 (closed by the dX kernel)
   trace_mark(cm, s, "bwd:start");
   void* const* peer_dO = ce.dev_ptrs(ws, p.w_dO, s);
   if (cm->sched) sched_a2a_imminent(cm);
   // backward dispatch = combine-backward into the owners' dO (waits for the FREE they
   // posted in their forward's combine, posts READY)
-  const PeerSignal s_disp = make_sig(cm, CT::kFreeBwd, ce.seq_fwd, CT::kReadyBwdD, seq, kSiteDispBwd);
+  const PeerSignal s_disp = make_sig(cm, CT::kFreeBwd, rf, 0, CT::kFReadyBwdD, rb, 1, kSiteDispBwd);
+  launch_sig_wait(s_disp, s);
   launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me,
-                          peer_dO, q.dg, s_disp, s);
+                          peer_dO, q.dg, no_wait(s_disp), s);
   trace_mark(cm, s, "combine_bwd(peer)");
   const auto& ps_ws = ce.peers(ws, s);
   std::vector<char*> dxs(P);
@@ -442,12 +460,12 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   st.P = P;
   st.me = me;
   st.E = p.E;
-  const PeerSignal s_recv = make_sig(cm, CT::kReadyBwdD, seq, -1, 0);
-  const PeerSignal s_comb = make_sig(cm, -1, 0, CT::kReadyBwdC, seq, kSiteCombBwd);
+  const PeerSignal s_recv = make_sig(cm, CT::kFReadyBwdD, rb, 1, -1, nullptr, 0);
+  const PeerSignal s_comb = make_sig(cm, -1, nullptr, 0, CT::kFReadyBwdC, rb, 1, kSiteCombBwd);
   prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
-    row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask,
-             c == 0 ? &s_recv : nullptr);  // the first reader of the peers' dO rows waits
+    if (c == 0) launch_sig_wait(s_recv, s);  // before the first reader of the peers' dO rows
+    row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask);
     trace_mark(cm, s, "dgrad1");
     RowGemm g{};
     g.mtp = q.mtp + (size_t)c * (P * p.El + 1);
@@ -477,9 +495,11 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   // dWg needs only this rank's dg: it overlaps the last returning expert gradients
   launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, p.E, p.k, q.dwg, dgate_w, s);
   trace_mark(cm, s, "dwg");
-  const PeerSignal s_back = make_sig(cm, CT::kReadyBwdC, seq, -1, 0);
+  const PeerSignal s_back = make_sig(cm, CT::kFReadyBwdC, rb, 1, -1, nullptr, 0, kSiteBwdEnd, rb);
+  launch_sig_wait(s_back, s);
+  const PeerSignal s_back2 = no_wait(s_back);
   launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm,
-            dtokens, s, &s_back);
+            dtokens, s, &s_back2);
   trace_mark(cm, s, "dx");
 }
 

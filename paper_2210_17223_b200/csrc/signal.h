@@ -19,12 +19,20 @@
 
 namespace lina {
 
+// Rounds live in device memory, one forward and one backward counter per rank: during a
+// pass every signal carries counter + 1, and the pass's last kernel bumps the counter
+// (last CTA).  So every pass has its own round (interleaved layers sharing a comm stay
+// ordered), and the kernels — and a CUDA graph captured around them — carry pointers,
+// not round numbers.
 struct PeerSignal {
-  const uint32_t* wait = nullptr;   // my slots of the awaited kind: wait[r * stride] written by rank r
-  uint32_t wait_value = 0;          // round to wait for (wrap-safe >=)
-  uint32_t* const* post = nullptr;  // device array [P]: rank r's slot (kind, me), mapped here
-  uint32_t post_value = 0;
-  unsigned int* done = nullptr;     // zeroed CTA-completion counter (sig_post_last)
+  const uint32_t* wait = nullptr;        // my slots of the awaited kind: wait[r * stride] written by rank r
+  const uint32_t* wait_round = nullptr;  // wait until every peer's slot >= *wait_round + wait_add (wrap-safe)
+  uint32_t wait_add = 0;
+  uint32_t* const* post = nullptr;       // device array [P]: rank r's slot (kind, me), mapped here
+  const uint32_t* post_round = nullptr;  // publish *post_round + post_add
+  uint32_t post_add = 0;
+  uint32_t* bump = nullptr;              // sig_bump_last(): the pass's round counter
+  unsigned int* done = nullptr;          // zeroed CTA-completion counter (sig_post_last / sig_bump_last)
   int P = 1, me = 0, stride = 0;
 };
 
@@ -40,11 +48,12 @@ __device__ __forceinline__ void sig_st_release(uint32_t* p, uint32_t v) {
 
 __device__ __forceinline__ void sig_wait(const PeerSignal& s) {
   if (!s.wait) return;
+  const uint32_t target = *s.wait_round + s.wait_add;
   const long long t0 = clock64();
   for (int r = 0; r < s.P; ++r) {
     if (r == s.me) continue;
     const uint32_t* f = s.wait + (size_t)r * s.stride;
-    while ((int)(sig_ld_acquire(f) - s.wait_value) < 0) {
+    while ((int)(sig_ld_acquire(f) - target) < 0) {
       __nanosleep(100);
       if (clock64() - t0 > 20000000000LL) __trap();  // a peer died: fail loudly, do not hang
     }
@@ -53,9 +62,10 @@ __device__ __forceinline__ void sig_wait(const PeerSignal& s) {
 
 __device__ __forceinline__ void sig_post(const PeerSignal& s) {
   if (!s.post) return;
+  const uint32_t v = *s.post_round + s.post_add;
   __threadfence_system();
   for (int r = 0; r < s.P; ++r)
-    if (r != s.me) sig_st_release(s.post[r], s.post_value);
+    if (r != s.me) sig_st_release(s.post[r], v);
 }
 
 // The CTA's writes (ordered before thread 0 by the caller's barrier) are released to the
@@ -69,6 +79,18 @@ __device__ __forceinline__ void sig_post_last(const PeerSignal& s) {
   if (prev == nb - 1) {
     *s.done = 0u;  // reset for the next launch on this stream
     sig_post(s);
+  }
+}
+
+// Thread 0 of every CTA, after its last use of the round: the last CTA closes the round.
+__device__ __forceinline__ void sig_bump_last(const PeerSignal& s) {
+  if (!s.bump) return;
+  const unsigned int nb = gridDim.x * gridDim.y * gridDim.z;
+  unsigned int prev;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(s.done) : "memory");
+  if (prev == nb - 1) {
+    *s.done = 0u;
+    *s.bump = *s.bump + 1u;
   }
 }
 #endif

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--seed", type=int, default=77)
     ap.add_argument("--check-chunks", type=int, default=0, help="also run with this n_chunks and compare bitwise")
     ap.add_argument("--poison", action="store_true", help="start from NaN-filled saved/workspace buffers")
+    ap.add_argument("--graph", action="store_true",
+                    help="also capture fwd+bwd in a CUDA graph, replay it 3 times, require bitwise equal results")
     a = ap.parse_args()
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -62,18 +64,44 @@ def main():
         wg = torch.from_numpy(Wg).to(dev)
         w1 = torch.from_numpy(W1).to(tdt).to(dev)
         w2 = torch.from_numpy(W2).to(tdt).to(dev)
+        dy = torch.from_numpy(dY).to(tdt).to(dev)
         y = layer.forward(x, wg, w1, w2, want_route=True)
-        dx, dwg, dw1, dw2 = layer.backward(torch.from_numpy(dY).to(tdt).to(dev), x, wg, w1, w2)
+        dx, dwg, dw1, dw2 = layer.backward(dy, x, wg, w1, w2)
         torch.cuda.synchronize()
         comm.check()
-        return {"y": y.float().cpu().numpy(), "dx": dx.float().cpu().numpy(), "dwg": dwg.cpu().numpy(),
-                "dw1": dw1.float().cpu().numpy(), "dw2": dw2.float().cpu().numpy(),
-                "idx": layer.route_t["idx"].cpu().numpy(), "slot": layer.route_t["slot"].cpu().numpy()}
+        out = {"y": y.float().cpu().numpy(), "dx": dx.float().cpu().numpy(), "dwg": dwg.cpu().numpy(),
+               "dw1": dw1.float().cpu().numpy(), "dw2": dw2.float().cpu().numpy(),
+               "idx": layer.route_t["idx"].cpu().numpy(), "slot": layer.route_t["slot"].cpu().numpy()}
+        if a.graph:  # replays must be full steps: the cross-rank rounds live in device memory
+            gy, gdx = torch.empty_like(y), torch.empty_like(dx)
+            gdwg, gdw1, gdw2 = torch.empty_like(dwg), torch.empty_like(dw1), torch.empty_like(dw2)
+            cap = torch.cuda.Stream(dev)
+            cap.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            dist.barrier()
+            with torch.cuda.graph(g, stream=cap):
+                layer.forward(x, wg, w1, w2, out=gy)
+                layer.backward(dy, x, wg, w1, w2, gdx, gdwg, gdw1, gdw2)
+            torch.cuda.synchronize()
+            dist.barrier()
+            for _ in range(3):
+                for t in (gy, gdx, gdw1, gdw2):
+                    t.fill_(float("nan"))
+                g.replay()
+                torch.cuda.synchronize()
+                comm.check()
+                same = all(torch.equal(u, v) for u, v in ((gy, y), (gdx, dx), (gdwg, dwg), (gdw1, dw1), (gdw2, dw2)))
+                if not same:
+                    out["graph_mismatch"] = True
+        return out
 
     res = run(a.n_chunks)
     gathered = [None] * world
     dist.gather_object(res, gathered if rank == 0 else None, dst=0)
     ok = True
+    if rank == 0 and any(g.get("graph_mismatch") for g in gathered):
+        print("CUDA graph replay differs from the eager step", flush=True)
+        ok = False
     if a.check_chunks:
         res2 = run(a.check_chunks)
         # outputs and token gradients are bitwise chunk-invariant (each row's arithmetic is

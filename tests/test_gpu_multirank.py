@@ -27,7 +27,7 @@ def _run(nproc, *args, port=29611):
 @pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("cfg,tokens,n,extra", [
     ("C1", 256, 2, ["--experts", "4"]),
-    ("C2", 512, 2, ["--check-chunks", "1", "--poison"]),
+    ("C2", 512, 2, ["--check-chunks", "1", "--poison", "--graph"]),
     ("C3", 256, 3, []),
 ])
 def test_two_ranks(cfg, tokens, n, extra):
@@ -36,7 +36,7 @@ def test_two_ranks(cfg, tokens, n, extra):
 
 @pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
 def test_four_ranks():
-    _run(4, "--config", "C2", "--tokens", "384", "--n-chunks", "4", "--check-chunks", "1", "--poison", port=29612)
+    _run(4, "--config", "C2", "--tokens", "384", "--n-chunks", "4", "--check-chunks", "1", "--poison", "--graph", port=29612)
 
 
 def _run_infer(nproc, *args, port=29621):

@@ -176,3 +176,35 @@ def test_comm_and_errors():
                               torch.empty(sv, dtype=torch.uint8, device="cuda"), small)
     assert ei.value.status == 6
     comm.close()
+
+
+@pytest.mark.parametrize("n_chunks", [1, 2])
+def test_cuda_graph_replay_bitwise(n_chunks):
+    """The layer is stream-ordered and host-sync free: a captured fwd+bwd replays as a
+    full step (bench.py times replays), bitwise equal to the eager step."""
+    import paper_2210_17223_b200 as lina
+    cfg, X, Wg, W1, W2, dY = _case("C2", tokens=512)
+    dt = tdtype(cfg.dtype)
+    comm = lina.Comm(1, 0, 0)
+    layer = lina.MoELayer(comm, X.shape[0], cfg.d_model, cfg.d_ffn, cfg.num_experts, cfg.k, cfg.capacity(),
+                          n_chunks, dt)
+    x, dy = to_dev(X, dt), to_dev(dY, dt)
+    wg, w1, w2 = to_dev(Wg, torch.float32), to_dev(W1, dt), to_dev(W2, dt)
+    y = layer.forward(x, wg, w1, w2)
+    dx, dwg, dw1, dw2 = layer.backward(dy, x, wg, w1, w2)
+    torch.cuda.synchronize()
+    outs = [torch.empty_like(t) for t in (y, dx, dwg, dw1, dw2)]
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cap):
+        layer.forward(x, wg, w1, w2, out=outs[0])
+        layer.backward(dy, x, wg, w1, w2, *outs[1:])
+    for _ in range(2):
+        for t in outs:
+            t.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        for got, ref in zip(outs, (y, dx, dwg, dw1, dw2)):
+            assert torch.equal(got, ref)
+    comm.close()
