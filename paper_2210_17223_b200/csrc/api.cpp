@@ -8,6 +8,7 @@
 #include "internal.h"
 #include "ce.h"
 #include "layer.h"
+#include "kernels.h"
 
 #include <atomic>
 
@@ -163,6 +164,8 @@ lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned 
     LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->hi, cudaStreamNonBlocking, hi_prio));
     LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->hi2, cudaStreamNonBlocking, hi_prio));
     LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->lo, cudaStreamNonBlocking, lo_prio));
+    LINA_CUDA_CHECK(cudaMalloc(&cm->route_sync, sizeof(unsigned int) * route_sync_words()));
+    LINA_CUDA_CHECK(cudaMemset(cm->route_sync, 0, sizeof(unsigned int) * route_sync_words()));
     cm->ev.resize(128);
     for (auto& e : cm->ev) LINA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (world > 1) {
@@ -218,6 +221,7 @@ lina_status lina_comm_destroy(lina_comm* cm) {
     if (cm->lo) cudaStreamDestroy(cm->lo);
     for (auto e : cm->prof_pool) cudaEventDestroy(e);
     if (cm->pinned) cudaFreeHost(cm->pinned);
+    if (cm->route_sync) cudaFree(cm->route_sync);
     delete cm;
     return LINA_OK;
   });

@@ -141,7 +141,7 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   trace_mark(cm, s, "inf:start");
   // ---- gate, dropless slots, counts (S1, S2 with C = T)
   launch_gate_topk(dtype, tokens, gate_w, T, d, E, k, 1, probs, idx, gate, s);
-  launch_route(idx, T, k, E, std::max(T, 1), (int*)(w + q.o_route), slot, counts, kept, tokof, s);
+  launch_route(idx, T, k, E, std::max(T, 1), (int*)(w + q.o_route), slot, counts, kept, tokof, s, cm->route_sync);
   if (P > 1) {
     LINA_NCCL_CHECK(ncclAllGather(counts, allc, (size_t)E, ncclInt32, cm->ep_disp, s));
   } else {

@@ -81,6 +81,7 @@ struct lina_comm {
   std::vector<cudaEvent_t> prof_pool;                          // free timing events
   int64_t prof_gemm_launches = 0;
   lina::Trace* trace = nullptr;  // LINA_TRACE=1 phase trace (trace.cpp), diagnostics only
+  unsigned int* route_sync = nullptr;  // zeroed words of the fused route kernel (route.cu)
   // pinned host scratch for the inference control plane (counts D2H, tables H2D)
   int* pinned = nullptr;
   size_t pinned_bytes = 0;

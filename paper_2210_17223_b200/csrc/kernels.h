@@ -43,8 +43,11 @@ void launch_gate_topk(int dtype, const void* X, const float* Wg, int T, int d, i
                       const PeerSignal* sig = nullptr);
 
 size_t route_scratch_ints(int T, int k, int E);
+// sync: zeroed device words (route_sync_words(), comm-owned) -> one fused launch;
+// NULL -> the three-launch count / scan / assign path.
+size_t route_sync_words();
 void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int* slot, int* counts,
-                  int* kept, int* tok_of, cudaStream_t s);
+                  int* kept, int* tok_of, cudaStream_t s, unsigned int* sync = nullptr);
 // vcount[(c*P + s)*El + el] = clamp(recv_kept[s*El + el] - b_c, 0, Cc)
 // A 1-CTA kernel that waits for sig's flags (sig.post ignored).
 void launch_sig_wait(const PeerSignal& sig, cudaStream_t s);

@@ -51,9 +51,9 @@ __device__ __forceinline__ int row_assignment(long long gw, const int* __restric
   const int b = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b;
   owner = El > 0 ? e / El : 0;
   prow = El > 0 ? peer_row(c, e, r, El, P, me, Cm) : (size_t)gw;
-  const int a = (r < Cc) ? tok_of[(size_t)e * C + b + r] : -1;
+  const int v = min(max(kept[e] - b, 0), Cc);  // valid rows of this (chunk, expert) segment
+  const int a = (r < v) ? tok_of[(size_t)e * C + b + r] : -1;  // slots >= kept[e] are never read
   if (a < 0) {
-    const int v = min(max(kept[e] - b, 0), Cc);
     if (r >= min(Cm, (v + 63) & ~63)) return kRowSkip;  // (the segment pitch Cm, not Cc, bounds the read)
   }
   return a;

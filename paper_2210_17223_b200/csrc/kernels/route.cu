@@ -10,8 +10,9 @@
 //   scan  : one thread per expert prefix-sums blockcnt over b            -> blockbase, counts, kept
 //   assign: CTA b re-ranks its assignments with __match_any_sync (rank among
 //           same-expert lanes below it) + per-warp counts prefix     -> slot[T,k], tok_of[E][C]
-// tok_of[e][s] = t*k + j of the assignment holding slot s (or -1): the inverse
-// map the row-parallel permute / combine-backward kernels gather through.
+// tok_of[e][s] = t*k + j of the assignment holding slot s < kept[e] (entries past kept[e]
+// are not written and never read): the inverse map the row-parallel permute /
+// combine-backward kernels gather through.
 #include <algorithm>
 
 #include "../common.h"
@@ -100,6 +101,96 @@ __global__ void vcount_kernel(const int* __restrict__ recv_kept, int P, int El, 
   vcount[i] = v < 0 ? 0 : (v > Cc ? Cc : v);
 }
 
+// Fused count + scan + assign (one launch): each CTA ranks its 1024 assignments within
+// the block (warp match + per-warp counts), publishes its per-expert aggregate, sums the
+// aggregates of all earlier CTAs (chained scan with look-back), then assigns slots.  CTAs
+// take their logical index from an atomic ticket, so a CTA only waits on CTAs that have
+// already started (no residency assumption).  sync = [ticket, done, flag[nb]] (zero
+// between launches: the last CTA to finish resets it); agg = [nb][E] scratch.
+constexpr int kRouteMaxBlocks = 4096;
+__global__ void __launch_bounds__(kRouteBlock) route_fused_kernel(
+    const int* __restrict__ idx, int T, int k, int E, int C, int nb, int* __restrict__ agg,
+    unsigned int* __restrict__ sync, int* __restrict__ slot, int* __restrict__ tok_of, int* __restrict__ counts,
+    int* __restrict__ kept) {
+  __shared__ int wc[32][65];
+  __shared__ int pre[64];
+  __shared__ unsigned int bid_s;
+  unsigned int* ticket = sync;
+  unsigned int* done = sync + 1;
+  unsigned int* flag = sync + 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) bid_s = atomicAdd(ticket, 1u);
+  for (int i = tid; i < 32 * 65; i += kRouteBlock) (&wc[0][0])[i] = 0;
+  __syncthreads();
+  const int b = (int)bid_s;
+  const long long a = (long long)b * kRouteBlock + tid;
+  const bool valid = a < (long long)T * k;
+  int j = 0, t = 0, e = -1 - lane;  // distinct negative keys never match
+  if (valid) {
+    j = (int)(a / T);
+    t = (int)(a % T);
+    e = idx[(size_t)t * k + j];
+  }
+  const unsigned mask = __match_any_sync(0xffffffffu, e);
+  const int rank = __popc(mask & ((1u << lane) - 1u));
+  if (valid && lane == __ffs(mask) - 1) wc[warp][e] = __popc(mask);
+  __syncthreads();
+  if (tid < E) {  // this CTA's aggregate, then the exclusive prefix over earlier CTAs
+    int h = 0;
+    for (int w = 0; w < 32; ++w) h += wc[w][tid];
+    agg[(size_t)b * E + tid] = h;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&flag[b]), "r"(1u) : "memory");
+  }
+  if (tid < E) pre[tid] = 0;
+  __syncthreads();
+  // look-back: thread i sums (earlier CTA q = i / E, expert i % E); every flag and
+  // aggregate load of the CTA is in flight at once (integer adds: order-free, exact)
+  for (int i = tid; i < b * E; i += kRouteBlock) {
+    const int q = i / E, ee = i % E;
+    unsigned int f;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(&flag[q]) : "memory");
+      if (f) break;
+      __nanosleep(32);
+    }
+    atomicAdd(&pre[ee], *((volatile const int*)&agg[(size_t)q * E + ee]));
+  }
+  __syncthreads();
+  if (tid < E && b == nb - 1) {  // the last CTA in priority order holds the totals
+    int h = 0;
+    for (int w = 0; w < 32; ++w) h += wc[w][tid];
+    const int tot = pre[tid] + h;
+    if (counts) counts[tid] = tot;
+    kept[tid] = tot < C ? tot : C;
+  }
+  if (valid) {
+    int p2 = pre[e];
+    for (int w = 0; w < warp; ++w) p2 += wc[w][e];
+    const int s2 = p2 + rank;
+    const int code = t * k + j;
+    if (s2 < C) {
+      slot[code] = s2;
+      tok_of[(size_t)e * C + s2] = code;
+    } else {
+      slot[code] = -1;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {  // the last CTA to finish re-arms the sync words for the next launch
+    __threadfence();
+    if (atomicAdd(done, 1u) == (unsigned)nb - 1u) {
+      for (int q = 0; q < nb; ++q) flag[q] = 0u;
+      *ticket = 0u;
+      __threadfence();
+      *done = 0u;
+    }
+  }
+}
+
 // One thread waits for the peers' flags; the consumer kernel follows in stream order.
 // Waiting in a 1-CTA kernel (not in every CTA of the consumer) keeps the SMs free for
 // kernels the peers' progress may depend on (e.g. an NCCL allreduce on another stream).
@@ -142,20 +233,27 @@ void launch_vcount(const int* recv_kept, int P, int El, int C, int n, int* vcoun
   LINA_LAUNCH_CHECK();
 }
 
+size_t route_sync_words() { return 2 + kRouteMaxBlocks; }
+
 size_t route_scratch_ints(int T, int k, int E) {
   const long long nb = ((long long)T * k + kRouteBlock - 1) / kRouteBlock;
   return (size_t)(2 * nb * E);
 }
 
 void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int* slot, int* counts,
-                  int* kept, int* tok_of, cudaStream_t s) {
-  LINA_CUDA_CHECK(cudaMemsetAsync(tok_of, 0xff, sizeof(int) * (size_t)E * C, s));
+                  int* kept, int* tok_of, cudaStream_t s, unsigned int* sync) {
+  // tok_of[e][s] is written for every kept slot s < kept[e]; readers never look past kept[e]
   if (T <= 0) {
     LINA_CUDA_CHECK(cudaMemsetAsync(kept, 0, sizeof(int) * E, s));
     if (counts) LINA_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(int) * E, s));
     return;
   }
   const int nb = (int)(((long long)T * k + kRouteBlock - 1) / kRouteBlock);
+  if (sync && nb <= kRouteMaxBlocks) {
+    route_fused_kernel<<<nb, kRouteBlock, 0, s>>>(idx, T, k, E, C, nb, scratch, sync, slot, tok_of, counts, kept);
+    LINA_LAUNCH_CHECK();
+    return;
+  }
   int* blockcnt = scratch;
   int* blockbase = scratch + (size_t)nb * E;
   route_count_kernel<<<nb, kRouteBlock, 0, s>>>(idx, T, k, E, blockcnt);

@@ -356,7 +356,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   launch_gate_topk(dtype, tokens, gate_w, p.T, p.d, p.E, p.k, override_r ? 0 : 1, q.probs, q.idx, q.gate, s,
                    &s_free);
   launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr, q.kept,
-               q.tok_of, s);
+               q.tok_of, s, cm->route_sync);
   trace_mark(cm, s, "gate+route");
   void* const* peer_R = ce.dev_ptrs(saved, p.s_R, s);
   void* const* peer_cnt = ce.dev_ptrs(saved, p.s_recvkept, s);
@@ -561,7 +561,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   launch_gate_topk(dtype, tokens, gate_w, p.T, p.d, p.E, p.k, override_r ? 0 : 1, q.probs, q.idx,
                    q.gate, s);
   launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr,
-               q.kept, q.tok_of, s);
+               q.kept, q.tok_of, s, cm->route_sync);
   launch_permute(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, p.n, p.Cm, q.D, s);
   if (route) {
     if (route->idx && !override_r)
