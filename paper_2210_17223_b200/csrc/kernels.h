@@ -44,10 +44,12 @@ void launch_gate_topk(int dtype, const void* X, const float* Wg, int T, int d, i
 
 size_t route_scratch_ints(int T, int k, int E);
 // sync: zeroed device words (route_sync_words(), comm-owned) -> one fused launch;
-// NULL -> the three-launch count / scan / assign path.
+// NULL -> the three-launch count / scan / assign path.  vcount/mtp (P = 1 only): also
+// the chunk segments' valid rows [n][E] and m-tile prefix [n][E+1] of `tile_rows` rows.
 size_t route_sync_words();
 void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int* slot, int* counts,
-                  int* kept, int* tok_of, cudaStream_t s, unsigned int* sync = nullptr);
+                  int* kept, int* tok_of, cudaStream_t s, unsigned int* sync = nullptr, int n_chunks = 1,
+                  int* vcount = nullptr, int* mtp = nullptr, int tile_rows = 256);
 // vcount[(c*P + s)*El + el] = clamp(recv_kept[s*El + el] - b_c, 0, Cc)
 // A 1-CTA kernel that waits for sig's flags (sig.post ignored).
 void launch_sig_wait(const PeerSignal& sig, cudaStream_t s);

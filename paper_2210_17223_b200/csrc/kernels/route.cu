@@ -111,9 +111,9 @@ constexpr int kRouteMaxBlocks = 4096;
 __global__ void __launch_bounds__(kRouteBlock) route_fused_kernel(
     const int* __restrict__ idx, int T, int k, int E, int C, int nb, int* __restrict__ agg,
     unsigned int* __restrict__ sync, int* __restrict__ slot, int* __restrict__ tok_of, int* __restrict__ counts,
-    int* __restrict__ kept) {
+    int* __restrict__ kept, int n, int* __restrict__ vcount, int* __restrict__ mtp, int rows) {
   __shared__ int wc[32][65];
-  __shared__ int pre[64];
+  __shared__ int pre[64], kept_s[64];
   __shared__ unsigned int bid_s;
   unsigned int* ticket = sync;
   unsigned int* done = sync + 1;
@@ -166,6 +166,28 @@ __global__ void __launch_bounds__(kRouteBlock) route_fused_kernel(
     const int tot = pre[tid] + h;
     if (counts) counts[tid] = tot;
     kept[tid] = tot < C ? tot : C;
+    kept_s[tid] = tot < C ? tot : C;
+  }
+  // P = 1: the chunk-segment valid rows and the m-tile prefix follow from kept directly
+  // (vcount / mtile_prefix kernels of the P > 1 path)
+  if (vcount && b == nb - 1) {
+    __syncthreads();
+    const int Cm = chunk_pitch(C, n);
+    for (int i = tid; i < n * E; i += kRouteBlock) {
+      const int c = i / E, ee = i % E;
+      const int b0 = chunk_begin_p(c, C, Cm), Cc = chunk_begin_p(c + 1, C, Cm) - b0;
+      const int v = kept_s[ee] - b0;
+      vcount[i] = v < 0 ? 0 : (v > Cc ? Cc : v);
+    }
+    __syncthreads();
+    if (tid < n) {
+      int run = 0;
+      for (int ee = 0; ee < E; ++ee) {
+        mtp[tid * (E + 1) + ee] = run;
+        run += (vcount[tid * E + ee] + rows - 1) / rows;
+      }
+      mtp[tid * (E + 1) + E] = run;
+    }
   }
   if (valid) {
     int p2 = pre[e];
@@ -241,16 +263,22 @@ size_t route_scratch_ints(int T, int k, int E) {
 }
 
 void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int* slot, int* counts,
-                  int* kept, int* tok_of, cudaStream_t s, unsigned int* sync) {
+                  int* kept, int* tok_of, cudaStream_t s, unsigned int* sync, int n_chunks, int* vcount, int* mtp,
+                  int tile_rows) {
   // tok_of[e][s] is written for every kept slot s < kept[e]; readers never look past kept[e]
   if (T <= 0) {
     LINA_CUDA_CHECK(cudaMemsetAsync(kept, 0, sizeof(int) * E, s));
     if (counts) LINA_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(int) * E, s));
+    if (vcount) {
+      launch_vcount(kept, 1, E, C, n_chunks, vcount, s);
+      launch_mtile_prefix(vcount, n_chunks, E, tile_rows, mtp, s);
+    }
     return;
   }
   const int nb = (int)(((long long)T * k + kRouteBlock - 1) / kRouteBlock);
   if (sync && nb <= kRouteMaxBlocks) {
-    route_fused_kernel<<<nb, kRouteBlock, 0, s>>>(idx, T, k, E, C, nb, scratch, sync, slot, tok_of, counts, kept);
+    route_fused_kernel<<<nb, kRouteBlock, 0, s>>>(idx, T, k, E, C, nb, scratch, sync, slot, tok_of, counts, kept,
+                                                  n_chunks, vcount, mtp, tile_rows);
     LINA_LAUNCH_CHECK();
     return;
   }
@@ -262,6 +290,10 @@ void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int*
   LINA_LAUNCH_CHECK();
   route_assign_kernel<<<nb, kRouteBlock, 0, s>>>(idx, T, k, E, C, blockbase, slot, tok_of);
   LINA_LAUNCH_CHECK();
+  if (vcount) {
+    launch_vcount(kept, 1, E, C, n_chunks, vcount, s);
+    launch_mtile_prefix(vcount, n_chunks, E, tile_rows, mtp, s);
+  }
 }
 
 }  // namespace lina

@@ -560,8 +560,10 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   // S1 gate, S2 route, S3 permute
   launch_gate_topk(dtype, tokens, gate_w, p.T, p.d, p.E, p.k, override_r ? 0 : 1, q.probs, q.idx,
                    q.gate, s);
+  // (P = 1: the route launch also yields the chunk segments' valid rows and m-tile prefix)
   launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr,
-               q.kept, q.tok_of, s, cm->route_sync);
+               q.kept, q.tok_of, s, cm->route_sync, p.n, p.P == 1 ? q.vcount : nullptr,
+               p.P == 1 ? q.mtp : nullptr, tc_tile_rows());
   launch_permute(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, p.n, p.Cm, q.D, s);
   if (route) {
     if (route->idx && !override_r)
@@ -579,8 +581,6 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   }
   if (p.P == 1) {
     // All experts local: the "all-to-all" is the identity and chunks only re-slice the GEMMs.
-    launch_vcount(q.kept, 1, p.E, p.C, p.n, q.vcount, s);
-    launch_mtile_prefix(q.vcount, p.n, p.P * p.El, tc_tile_rows(), q.mtp, s);
     trace_mark(cm, s, "P1 vcount");
     prof_begin(cm, s);
     for (int c = 0; c < p.n; ++c) {
