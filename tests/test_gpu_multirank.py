@@ -67,3 +67,22 @@ def test_scheduler_allreduce_two_ranks():
 @pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
 def test_infer_replication_four_ranks():
     _run_infer(4, "--tokens", "512", "--zipf", "1.0", "--experts", "32", port=29622)
+
+
+def _run_full(nproc, port):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "mp_fullsize.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "MP_FULLSIZE OK" in out, out[-4000:]
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_full_size_two_ranks_graph():
+    """configs[1] at full size per rank, fused transport, CUDA-graph replays (the bench launch)."""
+    _run_full(2, 29651)
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
+def test_full_size_four_ranks_graph():
+    _run_full(4, 29652)
