@@ -34,6 +34,16 @@
  *     `stream` reaches that point.  Pointers must stay live until then.  The
  *     calls never synchronise the host, except lina_moe_infer_forward (the
  *     unequal all-to-all needs host-visible counts).
+ *   - lina_moe_forward / lina_moe_backward may be captured in a CUDA graph
+ *     (after one eager call on the same buffers, which sets up the peer
+ *     mappings): the cross-rank ordering of the fused all-to-all keeps its
+ *     rounds in device memory, so every replay is a complete step.  All ranks
+ *     must issue the same sequence of calls.
+ *   - Training all-to-all transport (environment, read at lina_comm_init):
+ *     LINA_TRANSPORT=fused (default: peer stores from the permute / combine-
+ *     backward kernels and the GEMM epilogues over NVLink, in-kernel flags),
+ *     ce (copy engines) or nccl (ncclAlltoAll micro-ops).  LINA_TRACE=1 prints a
+ *     per-phase device-time trace per rank at lina_comm_destroy.
  *   - The library never allocates caller-visible memory in forward/backward:
  *     scratch and saved state are caller-allocated, sized by
  *     lina_moe_workspace_size().
