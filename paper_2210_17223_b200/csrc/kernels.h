@@ -93,11 +93,12 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s);
 // receive buffers (peer_rows[o]) and the counts into their recv_kept (peer_counts[o]).
 // sig: every CTA waits for the peers' FREE, block 0 also stores this rank's counts into
 // the owners' recv_kept (peer_counts[o]), and the last CTA posts READY.
+// [c0, c0 + nc): the micro-op chunks this launch moves (counts are stored with chunk 0).
 void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d, int E,
-                         int C, int n, int Cm, int El, int P, int me, void* const* peer_rows,
+                         int C, int c0, int nc, int Cm, int El, int P, int me, void* const* peer_rows,
                          void* const* peer_counts, const PeerSignal& sig, cudaStream_t s);
 void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
-                             const float* gate, int T, int k, int d, int E, int C, int n, int Cm, int El,
+                             const float* gate, int T, int k, int d, int E, int C, int c0, int nc, int Cm, int El,
                              int P, int me, void* const* peer_rows, float* dg, const PeerSignal& sig,
                              cudaStream_t s);
 // Output tiles of a row GEMM stored through per-owner tensor maps (peer memory):

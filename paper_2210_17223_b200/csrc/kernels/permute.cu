@@ -82,23 +82,24 @@ __device__ __forceinline__ long long rotated_row0(int R, long long rows, int El,
 // dispatch all-to-all.
 template <typename T, int NVL, bool PEER>
 __device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int* __restrict__ tok_of,
-                                             const int* __restrict__ kept, int k, int d, int E, int C, int n,
-                                             int Cm, int El, int P, int me, T* __restrict__ Send,
+                                             const int* __restrict__ kept, int k, int d, int E, int C, int c0,
+                                             int nc, int Cm, int El, int P, int me, T* __restrict__ Send,
                                              T* const* __restrict__ peer) {
   constexpr int R = NVL == 0 ? 1 : (NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / NVL);
   constexpr int NL = NVL == 0 ? 1 : NVL;
   constexpr int V = 16 / sizeof(T);
   const int lane = threadIdx.x & 31;
-  const long long rows = (long long)n * E * Cm;
+  const long long rows = (long long)nc * E * Cm;  // the micro-op chunks [c0, c0 + nc)
+  const long long g0 = (long long)c0 * E * Cm;
   const long long row0 = rotated_row0<PEER>(R, rows, El, P, me, Cm);
   if (row0 < 0) return;
   const int nv = d / V;
   int a = -1, owner = 0;
   size_t prow = 0;
   if (lane < R && row0 + lane < rows)
-    a = row_assignment(row0 + lane, tok_of, kept, E, C, Cm, PEER ? El : 0, P, me, owner, prow);
+    a = row_assignment(g0 + row0 + lane, tok_of, kept, E, C, Cm, PEER ? El : 0, P, me, owner, prow);
   if constexpr (NVL == 0) {
-    uint4* dst = reinterpret_cast<uint4*>(PEER ? peer[owner] + prow * d : Send + (size_t)row0 * d);
+    uint4* dst = reinterpret_cast<uint4*>(PEER ? peer[owner] + prow * d : Send + (size_t)(g0 + row0) * d);
     a = __shfl_sync(0xffffffffu, a, 0);
     if (a == kRowSkip) return;
     dst = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), 0));
@@ -127,7 +128,7 @@ __device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int*
         const size_t pr = __shfl_sync(0xffffffffu, (unsigned long long)prow, i);
         dst = reinterpret_cast<uint4*>(peer[o] + pr * d);
       } else {
-        dst = reinterpret_cast<uint4*>(Send + (size_t)(row0 + i) * d);
+        dst = reinterpret_cast<uint4*>(Send + (size_t)(g0 + row0 + i) * d);
       }
 #pragma unroll
       for (int j = 0; j < NL; ++j) {
@@ -140,8 +141,8 @@ __device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int*
 
 template <typename T, int NVL, bool PEER>
 __global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ X, const int* __restrict__ tok_of,
-                                                      int k, int d, int E, int C, int n, int Cm, int El,
-                                                      int P, int me, T* __restrict__ Send,
+                                                      int k, int d, int E, int C, int c0, int nc, int Cm,
+                                                      int El, int P, int me, T* __restrict__ Send,
                                                       T* const* __restrict__ peer, const int* __restrict__ kept,
                                                       int* const* __restrict__ peer_counts, PeerSignal sig) {
   if constexpr (PEER) {
@@ -149,10 +150,10 @@ __global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ X, c
     // counts go to every owner's recv_kept
     if (threadIdx.x == 0) sig_wait(sig);
     __syncthreads();
-    if (blockIdx.x == 0)
+    if (blockIdx.x == 0 && c0 == 0)
       for (int i = threadIdx.x; i < P * El; i += blockDim.x) peer_counts[i / El][me * El + i % El] = kept[i];
   }
-  permute_rows<T, NVL, PEER>(X, tok_of, kept, k, d, E, C, n, Cm, El, P, me, Send, peer);
+  permute_rows<T, NVL, PEER>(X, tok_of, kept, k, d, E, C, c0, nc, Cm, El, P, me, Send, peer);
   if constexpr (PEER) {
     __syncthreads();
     if (threadIdx.x == 0) sig_post_last(sig);  // the last CTA: READY of the dispatch
@@ -306,14 +307,16 @@ template <typename T, int NVL, bool PEER>
 __device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const T* __restrict__ Recv,
                                                  const int* __restrict__ tok_of, const int* __restrict__ kept,
                                                  const float* __restrict__ gate,
-                                                 int k, int d, int E, int C, int n, int Cm, int El, int P, int me,
+                                                 int k, int d, int E, int C, int c0, int nc, int Cm, int El, int P,
+                                                 int me,
                                                  T* __restrict__ dSend, T* const* __restrict__ peer,
                                                  float* __restrict__ dg) {
   constexpr int NL = NVL == 0 ? 1 : NVL;
   constexpr int R = NVL == 0 ? 1 : (2 * NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / (2 * NVL));
   constexpr int V = 16 / sizeof(T);
   const int lane = threadIdx.x & 31;
-  const long long rows = (long long)n * E * Cm;
+  const long long rows = (long long)nc * E * Cm;  // the micro-op chunks [c0, c0 + nc)
+  const long long g0 = (long long)c0 * E * Cm;
   const long long row0 = rotated_row0<PEER>(R, rows, El, P, me, Cm);
   if (row0 < 0) return;
   const int nv = d / V;
@@ -321,7 +324,7 @@ __device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const
   size_t prow = 0;
   float ga = 0.f;
   if (lane < R && row0 + lane < rows) {
-    a = row_assignment(row0 + lane, tok_of, kept, E, C, Cm, PEER ? El : 0, P, me, owner, prow);
+    a = row_assignment(g0 + row0 + lane, tok_of, kept, E, C, Cm, PEER ? El : 0, P, me, owner, prow);
     if (a >= 0) ga = gate[a];
   }
   if constexpr (NVL == 0) {
@@ -330,13 +333,13 @@ __device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const
     ga = __shfl_sync(0xffffffffu, ga, 0);
     owner = __shfl_sync(0xffffffffu, owner, 0);
     prow = __shfl_sync(0xffffffffu, (unsigned long long)prow, 0);
-    T* dst = PEER ? peer[owner] + prow * d : dSend + (size_t)row0 * d;
+    T* dst = PEER ? peer[owner] + prow * d : dSend + (size_t)(g0 + row0) * d;
     if (a < 0) {
       for (int v = lane; v < nv; v += 32) reinterpret_cast<uint4*>(dst)[v] = make_uint4(0, 0, 0, 0);
       return;
     }
     const T* dy = dY + (size_t)(a / k) * d;
-    const T* o = Recv + (size_t)row0 * d;
+    const T* o = Recv + (size_t)(g0 + row0) * d;
     float dot = 0.f;
     for (int v = lane; v < nv; v += 32) {
       float x[V], y[V];
@@ -359,7 +362,7 @@ __device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const
     for (int i = 0; i < R; ++i) {
       ai[i] = __shfl_sync(0xffffffffu, a, i);
       const uint4* dy = reinterpret_cast<const uint4*>(dY + (size_t)(ai[i] >= 0 ? ai[i] / k : 0) * d);
-      const uint4* o = reinterpret_cast<const uint4*>(Recv + (size_t)(row0 + i < rows ? row0 + i : 0) * d);
+      const uint4* o = reinterpret_cast<const uint4*>(Recv + (size_t)(g0 + (row0 + i < rows ? row0 + i : 0)) * d);
 #pragma unroll
       for (int j = 0; j < NL; ++j) {
         const int v = lane + 32 * j;
@@ -379,7 +382,7 @@ __device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const
         const size_t pr = __shfl_sync(0xffffffffu, (unsigned long long)prow, i);
         dst = peer[o] + pr * d;
       } else {
-        dst = dSend + (size_t)(row0 + i) * d;
+        dst = dSend + (size_t)(g0 + row0 + i) * d;
       }
       float dot = 0.f;
 #pragma unroll
@@ -408,7 +411,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ 
                                                           const int* __restrict__ tok_of,
                                                           const int* __restrict__ kept,
                                                           const float* __restrict__ gate, int k, int d,
-                                                          int E, int C, int n, int Cm, int El, int P,
+                                                          int E, int C, int c0, int nc, int Cm, int El, int P,
                                                           int me, T* __restrict__ dSend,
                                                           T* const* __restrict__ peer,
                                                           float* __restrict__ dg, PeerSignal sig) {
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ 
     if (threadIdx.x == 0) sig_wait(sig);
     __syncthreads();
   }
-  combine_bwd_rows<T, NVL, PEER>(dY, Recv, tok_of, kept, gate, k, d, E, C, n, Cm, El, P, me, dSend, peer, dg);
+  combine_bwd_rows<T, NVL, PEER>(dY, Recv, tok_of, kept, gate, k, d, E, C, c0, nc, Cm, El, P, me, dSend, peer, dg);
   if constexpr (PEER) {
     __syncthreads();
     if (threadIdx.x == 0) sig_post_last(sig);  // the last CTA: READY of the backward dispatch
@@ -471,22 +474,23 @@ inline int rows_per_warp(int nvl, int loads_per_row) {
   } while (0)
 
 template <bool PEER>
-static void permute_any(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int n,
+static void permute_any(int dtype, const void* X, const int* tok_of, int k, int d, int E, int C, int c0, int nc,
                         int Cm, int El, int P, int me, void* Send, void* const* peer, const int* kept,
                         void* const* peer_counts, const PeerSignal& sig, cudaStream_t s) {
-  const long long rows = (long long)n * E * Cm;
+  const long long rows = (long long)nc * E * Cm;
   if (rows == 0 && !PEER) return;
   const int nvl = nvl_of(d, dtype);
   const long long warps = std::max(1LL, (rows + rows_per_warp(nvl, 1) - 1) / rows_per_warp(nvl, 1));
   LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (permute_kernel<ET, NV_, PEER><<<blocks_for_warps(warps), 256, 0, s>>>(
-                             (const ET*)X, tok_of, k, d, E, C, n, Cm, El, P, me, (ET*)Send,
+                             (const ET*)X, tok_of, k, d, E, C, c0, nc, Cm, El, P, me, (ET*)Send,
                              (ET* const*)peer, kept, (int* const*)peer_counts, sig))));
   LINA_LAUNCH_CHECK();
 }
 
 void launch_permute(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d, int E, int C,
                     int n, int Cm, void* Send, cudaStream_t s) {
-  permute_any<false>(dtype, X, tok_of, k, d, E, C, n, Cm, 0, 1, 0, Send, nullptr, kept, nullptr, PeerSignal{}, s);
+  permute_any<false>(dtype, X, tok_of, k, d, E, C, 0, n, Cm, 0, 1, 0, Send, nullptr, kept, nullptr, PeerSignal{},
+                     s);
 }
 
 void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot, const float* gate,
@@ -514,16 +518,17 @@ void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot
 
 template <bool PEER>
 static void combine_bwd_any(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
-                            const float* gate,
-                            int T, int k, int d, int E, int C, int n, int Cm, int El, int P, int me,
-                            void* dSend, void* const* peer, float* dg, const PeerSignal& sig, cudaStream_t s) {
-  if (T > 0) LINA_CUDA_CHECK(cudaMemsetAsync(dg, 0, sizeof(float) * (size_t)T * k, s));
-  const long long rows = (long long)n * E * Cm;
+                            const float* gate, int T, int k, int d, int E, int C, int c0, int nc, int Cm, int El,
+                            int P, int me, void* dSend, void* const* peer, float* dg, const PeerSignal& sig,
+                            cudaStream_t s) {
+  // dg = 0 for dropped assignments: zeroed once, before the first chunk range
+  if (T > 0 && c0 == 0) LINA_CUDA_CHECK(cudaMemsetAsync(dg, 0, sizeof(float) * (size_t)T * k, s));
+  const long long rows = (long long)nc * E * Cm;
   if (rows == 0 && !PEER) return;
   const int nvl = nvl_of(d, dtype);
   const long long warps = std::max(1LL, (rows + rows_per_warp(nvl, 2) - 1) / rows_per_warp(nvl, 2));
   LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (combine_bwd_kernel<ET, NV_, PEER><<<blocks_for_warps(warps), 256, 0, s>>>(
-                             (const ET*)dY, (const ET*)Recv, tok_of, kept, gate, k, d, E, C, n, Cm, El, P,
+                             (const ET*)dY, (const ET*)Recv, tok_of, kept, gate, k, d, E, C, c0, nc, Cm, El, P,
                              me, (ET*)dSend, (ET* const*)peer, dg, sig))));
   LINA_LAUNCH_CHECK();
 }
@@ -531,22 +536,23 @@ static void combine_bwd_any(int dtype, const void* dY, const void* Recv, const i
 void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
                         const float* gate, int T, int k, int d, int E, int C, int n, int Cm,
                         void* dSend, float* dg, cudaStream_t s) {
-  combine_bwd_any<false>(dtype, dY, Recv, tok_of, kept, gate, T, k, d, E, C, n, Cm, 0, 1, 0, dSend, nullptr, dg,
+  combine_bwd_any<false>(dtype, dY, Recv, tok_of, kept, gate, T, k, d, E, C, 0, n, Cm, 0, 1, 0, dSend, nullptr, dg,
                          PeerSignal{}, s);
 }
 
 void launch_permute_peer(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d, int E,
-                         int C, int n, int Cm, int El, int P, int me, void* const* peer_rows,
+                         int C, int c0, int nc, int Cm, int El, int P, int me, void* const* peer_rows,
                          void* const* peer_counts, const PeerSignal& sig, cudaStream_t s) {
-  permute_any<true>(dtype, X, tok_of, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows, kept, peer_counts, sig, s);
+  permute_any<true>(dtype, X, tok_of, k, d, E, C, c0, nc, Cm, El, P, me, nullptr, peer_rows, kept, peer_counts, sig,
+                    s);
 }
 
 void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
-                             const float* gate, int T, int k, int d, int E, int C, int n, int Cm, int El,
+                             const float* gate, int T, int k, int d, int E, int C, int c0, int nc, int Cm, int El,
                              int P, int me, void* const* peer_rows, float* dg, const PeerSignal& sig,
                              cudaStream_t s) {
-  combine_bwd_any<true>(dtype, dY, Recv, tok_of, kept, gate, T, k, d, E, C, n, Cm, El, P, me, nullptr, peer_rows,
-                        dg, sig, s);
+  combine_bwd_any<true>(dtype, dY, Recv, tok_of, kept, gate, T, k, d, E, C, c0, nc, Cm, El, P, me, nullptr,
+                        peer_rows, dg, sig, s);
 }
 
 }  // namespace lina

@@ -338,6 +338,54 @@ bool fused_ok(const lina_comm* cm, const Plan& p) {
          p.d % 64 == 0 && p.f % 64 == 0 && p.d % 32 == 0;
 }
 
+// Micro-op c of a signal: slot c of the kind (wait: chunks [c, c + wait_chunks)).
+PeerSignal chunk_sig(PeerSignal g, int c, int wait_chunks = 1) {
+  if (g.wait) g.wait += c;
+  g.wait_chunks = wait_chunks;
+  g.post_chunk = c;
+  return g;
+}
+
+// Host-side cached per-rank tensor maps of a peer-stored GEMM output.
+PeerStore peer_store(CeTransport& ce, const char* tag, void* buf, size_t off, const Plan& p, int me,
+                     std::vector<char*>& bases, cudaStream_t s) {
+  const auto& ps = ce.peers(buf, s);
+  bases.resize(p.P);
+  for (int r = 0; r < p.P; ++r) bases[r] = ps[r] + off;
+  PeerStore st;
+  const std::string key = std::string(tag) + std::to_string((uintptr_t)buf) + ":" + std::to_string(off) + ":" +
+                          std::to_string(p.Cm) + ":" + std::to_string(p.n * p.E);
+  auto it = ce.host_blobs.find(key);
+  if (it == ce.host_blobs.end()) it = ce.host_blobs.emplace(key, tc_peer_dmaps(bases, p.d, p.Cm, p.n * p.E)).first;
+  st.host_maps = it->second.data();
+  st.bases = bases.data();
+  st.P = p.P;
+  st.me = me;
+  st.E = p.E;
+  return st;
+}
+
+RowGemm peer_gemm(const Plan& p, const void* A, const void* B, void* D, const int* vcount, const int* mtp, int c,
+                  int N, int K) {
+  RowGemm g{};
+  g.mtp = mtp + (size_t)c * (p.P * p.El + 1);
+  g.A = A;
+  g.B = B;
+  g.D = D;
+  g.vcount = vcount;
+  g.seg0 = c * p.P * p.El;
+  g.nseg = p.P * p.El;
+  g.El = p.El;
+  g.Cm = p.Cm;
+  g.N = N;
+  g.K = K;
+  return g;
+}
+
+// n = 1: everything on the caller's stream.  n > 1 (the paper's micro-op pipeline,
+// P:354-376): the data-movement kernels of micro-op c + 1 run on the high-priority
+// stream while the expert GEMMs of micro-op c run on the caller's stream (they share
+// the SMs: the movers need no shared memory), each micro-op with its own flag slot.
 void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* tokens, const float* gate_w,
                    const void* w1, const void* w2, void* out, void* saved, void* ws, lina_route* route,
                    cudaStream_t s) {
@@ -360,11 +408,20 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   trace_mark(cm, s, "gate+route");
   void* const* peer_R = ce.dev_ptrs(saved, p.s_R, s);
   void* const* peer_cnt = ce.dev_ptrs(saved, p.s_recvkept, s);
-  // dispatch = permute into the owners' R (waits for their FREE, posts READY)
+  std::vector<char*> cb;
+  const PeerStore st = peer_store(ce, "fwdC:", saved, p.s_C, p, me, cb, s);
+  // dispatch = permute into the owners' R (after their FREE; READY per micro-op)
   const PeerSignal s_disp = make_sig(cm, CT::kFreeFwd, rf, 1, CT::kFReadyFwdD, rf, 1, kSiteDispFwd);
-  launch_sig_wait(s_disp, s);
-  launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me, peer_R, peer_cnt,
-                      no_wait(s_disp), s);
+  cudaStream_t sm = n > 1 ? cm->hi : s;  // the mover stream
+  if (n > 1) {
+    LINA_CUDA_CHECK(cudaEventRecord(cm->ev[0], s));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(sm, cm->ev[0], 0));
+  }
+  launch_sig_wait(s_disp, sm);
+  for (int c = 0; c < n; ++c)
+    launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, c, 1, p.Cm, p.El, P, me, peer_R,
+                        peer_cnt, chunk_sig(no_wait(s_disp), c), sm);
+  if (n > 1) LINA_CUDA_CHECK(cudaEventRecord(cm->ev[1], sm));
   trace_mark(cm, s, "permute(peer)");
   if (route) {
     if (route->idx && !override_r)
@@ -377,51 +434,30 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
       LINA_CUDA_CHECK(cudaMemcpyAsync(route->probs, q.probs, 4 * (size_t)p.T * p.E, cudaMemcpyDeviceToDevice, s));
   }
   const PeerSignal s_recv = make_sig(cm, CT::kFReadyFwdD, rf, 1, -1, nullptr, 0);
-  launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s, &s_recv);
-  launch_mtile_prefix(q.vcount, n, P * p.El, tc_tile_rows(), q.mtp, s);
-  trace_mark(cm, s, "vcount");
-  const auto& ps_saved = ce.peers(saved, s);
-  std::vector<char*> cb(P);
-  for (int r = 0; r < P; ++r) cb[r] = ps_saved[r] + p.s_C;
-  PeerStore st;
-  {
-    const std::string key = "fwdC:" + std::to_string((uintptr_t)saved) + ":" + std::to_string(p.s_C) + ":" +
-                            std::to_string(p.Cm) + ":" + std::to_string(n * p.E);
-    auto it = ce.host_blobs.find(key);
-    if (it == ce.host_blobs.end()) it = ce.host_blobs.emplace(key, tc_peer_dmaps(cb, p.d, p.Cm, n * p.E)).first;
-    st.host_maps = it->second.data();
-    st.bases = cb.data();
-  }
-  st.P = P;
-  st.me = me;
-  st.E = p.E;
   const PeerSignal s_comb = make_sig(cm, -1, nullptr, 0, CT::kFReadyFwdC, rf, 1, kSiteCombFwd);
-  prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
+    launch_sig_wait(chunk_sig(s_recv, c), s);  // micro-op c (and with c = 0 the counts) has landed
+    if (c == 0) {
+      launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
+      launch_mtile_prefix(q.vcount, n, P * p.El, tc_tile_rows(), q.mtp, s);
+      trace_mark(cm, s, "vcount");
+      prof_begin(cm, s);
+    }
     row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask);
     trace_mark(cm, s, "gemm1");
-    RowGemm g{};
-    g.mtp = q.mtp + (size_t)c * (P * p.El + 1);
-    g.A = q.H;
-    g.B = w2;
-    g.D = q.O;
-    g.vcount = q.vcount;
-    g.seg0 = c * P * p.El;
-    g.nseg = P * p.El;
-    g.El = p.El;
-    g.Cm = p.Cm;
-    g.N = p.d;
-    g.K = p.f;
-    if (c == n - 1) g.sig = &s_comb;  // the last CTA of the last chunk posts READY
+    RowGemm g = peer_gemm(p, q.H, w2, q.O, q.vcount, q.mtp, c, p.d, p.f);
+    const PeerSignal s_c = chunk_sig(s_comb, c);
+    g.sig = &s_c;  // the last CTA posts READY of micro-op c
     launch_row_gemm_tc_peer(g, true, kEpiNone, st, s);  // combine all-to-all in the epilogue
     trace_mark(cm, s, "gemm2(peer)");
   }
   prof_end(cm, s, 2 * n);
+  if (n > 1) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, cm->ev[1], 0));  // join the mover stream
   // combine: block 0 posts the backward FREE (my dO / dXs were last read by the previous
-  // backward), every CTA waits for the returned expert outputs
-  // (its last CTA closes the forward's round)
+  // backward); the returned expert outputs of every micro-op have landed (1-CTA wait);
+  // its last CTA closes the forward's round
   const PeerSignal s_out = make_sig(cm, CT::kFReadyFwdC, rf, 1, CT::kFreeBwd, rf, 1, kSiteFwdEnd, rf);
-  launch_sig_wait(s_out, s);
+  launch_sig_wait(chunk_sig(s_out, 0, n), s);
   const PeerSignal s_out2 = no_wait(s_out);
   launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, out, s, &s_out2);
   trace_mark(cm, s, "combine");
@@ -437,49 +473,33 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   uint32_t* rb = ce.round_bwd();  // this backward's round is *rb + 1 (closed by the dX kernel)
   trace_mark(cm, s, "bwd:start");
   void* const* peer_dO = ce.dev_ptrs(ws, p.w_dO, s);
+  std::vector<char*> dxs;
+  const PeerStore st = peer_store(ce, "bwdC:", ws, p.w_dXs, p, me, dxs, s);
   if (cm->sched) sched_a2a_imminent(cm);
-  // backward dispatch = combine-backward into the owners' dO (waits for the FREE they
-  // posted in their forward's combine, posts READY)
+  // backward dispatch = combine-backward into the owners' dO (after the FREE they posted
+  // in their forward's combine; READY per micro-op)
   const PeerSignal s_disp = make_sig(cm, CT::kFreeBwd, rf, 0, CT::kFReadyBwdD, rb, 1, kSiteDispBwd);
-  launch_sig_wait(s_disp, s);
-  launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, p.El, P, me,
-                          peer_dO, q.dg, no_wait(s_disp), s);
-  trace_mark(cm, s, "combine_bwd(peer)");
-  const auto& ps_ws = ce.peers(ws, s);
-  std::vector<char*> dxs(P);
-  for (int r = 0; r < P; ++r) dxs[r] = ps_ws[r] + p.w_dXs;
-  PeerStore st;
-  {
-    const std::string key = "bwdC:" + std::to_string((uintptr_t)ws) + ":" + std::to_string(p.w_dXs) + ":" +
-                            std::to_string(p.Cm) + ":" + std::to_string(n * p.E);
-    auto it = ce.host_blobs.find(key);
-    if (it == ce.host_blobs.end()) it = ce.host_blobs.emplace(key, tc_peer_dmaps(dxs, p.d, p.Cm, n * p.E)).first;
-    st.host_maps = it->second.data();
-    st.bases = dxs.data();
+  cudaStream_t sm = n > 1 ? cm->hi : s;
+  if (n > 1) {
+    LINA_CUDA_CHECK(cudaEventRecord(cm->ev[2], s));
+    LINA_CUDA_CHECK(cudaStreamWaitEvent(sm, cm->ev[2], 0));
   }
-  st.P = P;
-  st.me = me;
-  st.E = p.E;
+  launch_sig_wait(s_disp, sm);
+  for (int c = 0; c < n; ++c)
+    launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.T, p.k, p.d, p.E, p.C, c, 1, p.Cm, p.El,
+                            P, me, peer_dO, q.dg, chunk_sig(no_wait(s_disp), c), sm);
+  if (n > 1) LINA_CUDA_CHECK(cudaEventRecord(cm->ev[3], sm));
+  trace_mark(cm, s, "combine_bwd(peer)");
   const PeerSignal s_recv = make_sig(cm, CT::kFReadyBwdD, rb, 1, -1, nullptr, 0);
   const PeerSignal s_comb = make_sig(cm, -1, nullptr, 0, CT::kFReadyBwdC, rb, 1, kSiteCombBwd);
   prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
-    if (c == 0) launch_sig_wait(s_recv, s);  // before the first reader of the peers' dO rows
+    launch_sig_wait(chunk_sig(s_recv, c), s);  // micro-op c of the peers' dO rows has landed
     row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask);
     trace_mark(cm, s, "dgrad1");
-    RowGemm g{};
-    g.mtp = q.mtp + (size_t)c * (P * p.El + 1);
-    g.A = q.dH;
-    g.B = w1;
-    g.D = q.dXe;
-    g.vcount = q.vcount;
-    g.seg0 = c * P * p.El;
-    g.nseg = P * p.El;
-    g.El = p.El;
-    g.Cm = p.Cm;
-    g.N = p.d;
-    g.K = p.f;
-    if (c == n - 1) g.sig = &s_comb;
+    RowGemm g = peer_gemm(p, q.dH, w1, q.dXe, q.vcount, q.mtp, c, p.d, p.f);
+    const PeerSignal s_c = chunk_sig(s_comb, c);
+    g.sig = &s_c;
     launch_row_gemm_tc_peer(g, false, kEpiNone, st, s);  // combine all-to-all in the epilogue
     trace_mark(cm, s, "dgrad2(peer)");
   }
@@ -492,11 +512,12 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   launch_expert_wgrad(dtype, wg1, s);
   prof_end(cm, s, 2 * n + 2);
   trace_mark(cm, s, "wgrad x2");
+  if (n > 1) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, cm->ev[3], 0));  // dg of every micro-op
   // dWg needs only this rank's dg: it overlaps the last returning expert gradients
   launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, p.E, p.k, q.dwg, dgate_w, s);
   trace_mark(cm, s, "dwg");
   const PeerSignal s_back = make_sig(cm, CT::kFReadyBwdC, rb, 1, -1, nullptr, 0, kSiteBwdEnd, rb);
-  launch_sig_wait(s_back, s);
+  launch_sig_wait(chunk_sig(s_back, 0, n), s);
   const PeerSignal s_back2 = no_wait(s_back);
   launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm,
             dtokens, s, &s_back2);

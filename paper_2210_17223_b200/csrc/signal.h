@@ -34,6 +34,8 @@ struct PeerSignal {
   uint32_t* bump = nullptr;              // sig_bump_last(): the pass's round counter
   unsigned int* done = nullptr;          // zeroed CTA-completion counter (sig_post_last / sig_bump_last)
   int P = 1, me = 0, stride = 0;
+  int wait_chunks = 1;                   // micro-op slots wait[r*stride + 0 .. wait_chunks-1] per peer
+  int post_chunk = 0;                    // micro-op slot published: post[r] + post_chunk
 };
 
 #ifdef __CUDACC__
@@ -52,10 +54,12 @@ __device__ __forceinline__ void sig_wait(const PeerSignal& s) {
   const long long t0 = clock64();
   for (int r = 0; r < s.P; ++r) {
     if (r == s.me) continue;
-    const uint32_t* f = s.wait + (size_t)r * s.stride;
-    while ((int)(sig_ld_acquire(f) - target) < 0) {
-      __nanosleep(100);
-      if (clock64() - t0 > 20000000000LL) __trap();  // a peer died: fail loudly, do not hang
+    for (int c = 0; c < s.wait_chunks; ++c) {
+      const uint32_t* f = s.wait + (size_t)r * s.stride + c;
+      while ((int)(sig_ld_acquire(f) - target) < 0) {
+        __nanosleep(100);
+        if (clock64() - t0 > 20000000000LL) __trap();  // a peer died: fail loudly, do not hang
+      }
     }
   }
 }
@@ -65,7 +69,7 @@ __device__ __forceinline__ void sig_post(const PeerSignal& s) {
   const uint32_t v = *s.post_round + s.post_add;
   __threadfence_system();
   for (int r = 0; r < s.P; ++r)
-    if (r != s.me) sig_st_release(s.post[r], v);
+    if (r != s.me) sig_st_release(s.post[r] + s.post_chunk, v);
 }
 
 // The CTA's writes (ordered before thread 0 by the caller's barrier) are released to the
