@@ -351,7 +351,11 @@ def main():
                     break
         bytes_rank = 4 * n_chunks * E * cm_rows * d * elt   # 4 all-to-alls of the padded send buffer
         algbw = bytes_rank / (t_comm / 1e3) / 1e9
-        a2a = {"ms_per_step_isolated": t_comm, "ms_per_step_compute_only": t_comp, "ms_per_step_eager": t_step,
+        a2a = {"ms_per_step_isolated": t_comm,
+               # the fused transport has no stand-alone collective: its isolated pass moves the
+               # same bytes with the copy-engine transport
+               "isolated_transport": "ce" if transport == "fused" else transport,
+               "ms_per_step_compute_only": t_comp, "ms_per_step_eager": t_step,
                "exposed_ms_per_step": exposed,
                "hidden_frac": (1.0 - exposed / t_comm) if t_comm > 0 else None,
                "algbw_GBps": algbw, "busbw_GBps": algbw * (world - 1) / world,
