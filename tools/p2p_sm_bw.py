@@ -125,3 +125,40 @@ def rows_case(both, remote=True, reps=20):
 xsrc = {g: torch.empty(8192 * 1536, dtype=torch.uint8, device=f"cuda:{g}") for g in (0, 1)}
 print(json.dumps({"rows_us_local_only": rows_case(False, remote=False), "rows_us_half_remote": rows_case(False),
                   "rows_us_half_remote_both": rows_case(True)}), flush=True)
+
+
+# ---- 4-GPU all-to-all row pattern (when 4 GPUs are visible): every GPU moves 20480 rows
+# of 1536 B, rows of "expert group" g (4 groups) go to GPU g (its own group stays local),
+# groups visited starting at (me + 1) % 4 -- the fused permute's pattern at P = 4.
+if torch.cuda.device_count() >= 4:
+    G = 4
+    for a_ in range(G):
+        for b_ in range(G):
+            if a_ != b_:
+                ext.enable_peer(a_, b_)
+    src4 = {g: torch.empty(8192 * 1536, dtype=torch.uint8, device=f"cuda:{g}") for g in range(G)}
+    dst4 = {g: torch.empty(20480 * 1536, dtype=torch.uint8, device=f"cuda:{g}") for g in range(G)}
+    SRC2 = None
+
+    def run4(reps=20):
+        evs = []
+        for rep in range(2):
+            evs = []
+            for g in range(G):
+                with torch.cuda.device(g):
+                    st = torch.cuda.current_stream()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                    for _ in range(reps if rep else 1):
+                        for j in range(1, G + 1):  # rotated: peers first, own group last
+                            o = (g + j) % G
+                            # 5120 rows for owner o: local dst if o == g
+                            ext.rows(src4[g].data_ptr(), dst4[o].data_ptr(), dst4[o].data_ptr(), 5120, 5120,
+                                     st.cuda_stream)
+                    e1.record(st)
+                    evs.append((g, e0, e1))
+            for g, e0, e1 in evs:
+                torch.cuda.synchronize(g)
+        return [round(e0.elapsed_time(e1) / reps * 1e3, 1) for g, e0, e1 in evs]
+
+    print(json.dumps({"rows4_us_alltoall (4 x 5120 rows of 1536 B per GPU, 3/4 remote)": run4()}), flush=True)
