@@ -23,7 +23,7 @@ import lina_inputs as li  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--zipf", default="0.5,1.0,1.2")
+    ap.add_argument("--zipf", default="0,0.5,1.0,1.2", help="Zipf exponents; 0 = uniform popularity (the balanced ideal)")
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--batches", type=int, default=5, help="distinct seeded batches cycled over the iterations")
     ap.add_argument("--modes", default="static,replicated")
