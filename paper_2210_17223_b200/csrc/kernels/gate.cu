@@ -171,21 +171,35 @@ __global__ void __launch_bounds__(kGThreads) gate_mma_kernel(const __nv_bfloat16
       xb[j] = (in && vb) ? *reinterpret_cast<const uint4*>(X + (size_t)rb * d + col) : make_uint4(0, 0, 0, 0);
     }
     if (p0) __syncthreads();  // previous pass's fragment reads are done
-    for (int i = tid; i < NT * pb * 2 * 32; i += kGThreads) {
-      const int ln = i & 31, ks = (i >> 5) % (2 * pb), n = (i >> 5) / (2 * pb);
-      const int col = (p0 + (ks >> 1)) * 32 + (ln & 3) * 8 + (ks & 1) * 4;
-      const int e = n * 8 + (ln >> 2);
-      float w[4];
+    // staging: kSB entries per thread per batch, every Wg load of a batch issued before
+    // the first split (the loads, not the conversions, are the latency)
+    constexpr int kSB = 4;
+    const int total = NT * pb * 2 * 32;
+    const size_t so = (size_t)NT * PB2 * 32;
+    for (int i0 = 0; i0 < total; i0 += kSB * kGThreads) {
+      float w[kSB][4];
+      int oo[kSB];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) w[q] = e < E ? __ldg(Wg + (size_t)(col + q) * E + e) : 0.f;
-      float h[4], m[4], l[4];
+      for (int u = 0; u < kSB; ++u) {
+        const int i = i0 + u * kGThreads + tid;
+        const int ln = i & 31, ks = (i >> 5) % (2 * pb), n = (i >> 5) / (2 * pb);
+        const int col = (p0 + (ks >> 1)) * 32 + (ln & 3) * 8 + (ks & 1) * 4;
+        const int e = n * 8 + (ln >> 2);
+        const bool ok = i < total && e < E;
+        oo[u] = i < total ? (n * PB2 + ks) * 32 + ln : -1;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) split3(w[q], h[q], m[q], l[q]);
-      const size_t o = ((size_t)n * PB2 + ks) * 32 + ln;
-      const size_t so = (size_t)NT * PB2 * 32;
-      frag[o] = make_uint2(pack_bf16(h[0], h[1]), pack_bf16(h[2], h[3]));
-      frag[so + o] = make_uint2(pack_bf16(m[0], m[1]), pack_bf16(m[2], m[3]));
-      frag[2 * so + o] = make_uint2(pack_bf16(l[0], l[1]), pack_bf16(l[2], l[3]));
+        for (int q = 0; q < 4; ++q) w[u][q] = ok ? __ldg(Wg + (size_t)(col + q) * E + e) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kSB; ++u) {
+        if (oo[u] < 0) continue;
+        float h[4], m[4], l[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) split3(w[u][q], h[q], m[q], l[q]);
+        frag[oo[u]] = make_uint2(pack_bf16(h[0], h[1]), pack_bf16(h[2], h[3]));
+        frag[so + oo[u]] = make_uint2(pack_bf16(m[0], m[1]), pack_bf16(m[2], m[3]));
+        frag[2 * so + oo[u]] = make_uint2(pack_bf16(l[0], l[1]), pack_bf16(l[2], l[3]));
+      }
     }
     __syncthreads();
     for (int kbg = kb0; kbg < kb1; kbg += G) {
