@@ -23,7 +23,7 @@ struct RowGemm {
   int seg0, nseg, El, Cm, N, K;
   const int* seg_expert = nullptr;  // [El] weight index of local slot (seg % El); NULL = identity
   int B_experts = 0;                // expert matrices in B (0 = El)
-  uint64_t* mask_out = nullptr;       // tcgen05 ReLU epilogue: ReLU' bits [nseg_total*Cm][N/64]
+  uint64_t* mask_out = nullptr;       // tcgen05 ReLU epilogue: ReLU' bits [nseg_total][N/64][Cm]
   const uint64_t* mask_in = nullptr;  // tcgen05 mask epilogue: those bits (aux unused)
   const PeerSignal* sig = nullptr;    // tcgen05: wait before the first A load, post after the last store
 };

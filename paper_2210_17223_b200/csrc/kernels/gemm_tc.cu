@@ -278,7 +278,7 @@ struct TcParams {
   // the epilogue); has_pmaps = 0: local store through tmD
   int has_pmaps;
   int dP, dme, dE;
-  uint64_t* mask_out;       // ROW + ReLU: ReLU' bits of the stored output, [seg*Cm + row][N/64]
+  uint64_t* mask_out;       // ROW + ReLU: ReLU' bits of the stored output, [seg][N/64][Cm]
   const uint64_t* mask_in;  // ROW + mask epilogue: the bits written by GEMM1
   PeerSignal sig;           // fused transport: wait before the first A load / post after the last store
   CUtensorMap pmaps[kMaxPeerMaps];  // kernel-parameter copies (the TMA unit reads them like tmD)
@@ -498,11 +498,13 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
       const int nkb = kblocks_of(se);
       const int row = m0 + 128 * rank + quarter * 32 + lane;  // row within the segment
       const bool row_ok = !WGRAD && row < p.Cm;
-      const size_t mrow = row_ok ? ((size_t)(p.seg0 + se) * p.Cm + row) * mwords + ((n0 + col0) >> 6) : 0;
+      // ReLU' words are word-column-major, [seg][N/64][Cm]: the 32 lanes (32 consecutive
+      // rows) of a warp store / load 256 contiguous bytes per word column
+      const size_t mrow = row_ok ? ((size_t)(p.seg0 + se) * mwords + ((n0 + col0) >> 6)) * p.Cm + row : 0;
       uint64_t mk[COLS / 64];
       if (EPI == kEpiMask) {  // before the accumulator wait: latency hidden
 #pragma unroll
-        for (int j = 0; j < COLS / 64; ++j) mk[j] = row_ok ? p.mask_in[mrow + j] : 0ull;
+        for (int j = 0; j < COLS / 64; ++j) mk[j] = row_ok ? p.mask_in[mrow + (size_t)j * p.Cm] : 0ull;
       }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
@@ -553,7 +555,7 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
           }
           st_shared16(qa, pk);
         }
-        if (EPI == kEpiRelu && p.mask_out && row_ok) p.mask_out[mrow + j] = mword;
+        if (EPI == kEpiRelu && p.mask_out && row_ok) p.mask_out[mrow + (size_t)j * p.Cm] = mword;
         fence_proxy_async_smem();
         __syncwarp();
         int x0, x1, x2;
