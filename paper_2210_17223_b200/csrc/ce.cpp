@@ -46,9 +46,8 @@ struct CeTransport::Impl {
   std::map<std::pair<int, std::string>, char*> opened;
   // mapped peer pointers for a local pointer
   std::map<const void*, std::vector<char*>> maps;
-  // device copies: pointer arrays and tensor-map blobs
+  // device copies of peer pointer arrays
   std::map<std::pair<const void*, size_t>, void*> ptr_arrays;
-  std::map<std::string, void*> blobs;
   void* stage = nullptr;  // device staging for handle exchange
 };
 
@@ -64,17 +63,6 @@ void* const* CeTransport::dev_ptrs(const void* local, size_t offset, cudaStream_
   LINA_CUDA_CHECK(cudaMemcpy(d, v.data(), sizeof(char*) * v.size(), cudaMemcpyHostToDevice));
   impl_->ptr_arrays[key] = d;
   return (void* const*)d;
-}
-
-const void* CeTransport::dev_blob(const std::string& key, const std::vector<unsigned char>& bytes,
-                                  cudaStream_t) {
-  auto it = impl_->blobs.find(key);
-  if (it != impl_->blobs.end()) return it->second;
-  void* d = nullptr;
-  LINA_CUDA_CHECK(cudaMalloc(&d, bytes.size()));
-  LINA_CUDA_CHECK(cudaMemcpy(d, bytes.data(), bytes.size(), cudaMemcpyHostToDevice));
-  impl_->blobs[key] = d;
-  return d;
 }
 
 CeTransport::CeTransport(lina_comm* cm) : cm_(cm), impl_(new Impl) {
@@ -111,7 +99,6 @@ CeTransport::~CeTransport() {
   cudaDeviceSynchronize();
   for (auto& kv : impl_->opened) cudaIpcCloseMemHandle(kv.second);
   for (auto& kv : impl_->ptr_arrays) cudaFree(kv.second);
-  for (auto& kv : impl_->blobs) cudaFree(kv.second);
   for (auto s : disp_) cudaStreamDestroy(s);
   for (auto s : comb_) cudaStreamDestroy(s);
   for (auto e : events_) cudaEventDestroy(e);

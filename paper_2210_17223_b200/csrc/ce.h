@@ -29,9 +29,6 @@ class CeTransport {
   void post_flag(cudaStream_t s, int rank, int kind, int peer, int chunk, uint32_t value);
   // Device array of the P pointers peers(local)[r] + offset (cached; uploaded once).
   void* const* dev_ptrs(const void* local, size_t offset, cudaStream_t s);
-  // Device array of P tensor maps, one per rank's buffer (cached by key; built by
-  // `build` on first use, uploaded once).
-  const void* dev_blob(const std::string& key, const std::vector<unsigned char>& bytes, cudaStream_t s);
   // In-kernel signalling (signal.h): my slots of `kind` (peer r at r * kMaxChunks), the
   // device array [P] of every rank's slot (kind, me) mapped here (uploaded once), and a
   // zeroed CTA-completion counter per call site (sites < kDoneSites).
