@@ -17,6 +17,13 @@ static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
 static std::atomic<int64_t> g_launches{0};
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("LINA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static cudaEvent_t prof_event(lina_comm* cm) {

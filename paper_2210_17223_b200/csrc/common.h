@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 namespace lina {
 
@@ -30,6 +31,36 @@ void count_launch();
     ::lina::count_launch();                   \
     LINA_CUDA_CHECK(cudaGetLastError());      \
   } while (0)
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels of the layer are launched with programmatic stream serialization: a kernel may
+// be scheduled while its predecessor on the stream drains.  Every such kernel waits for
+// its predecessor's completion (and memory) before touching global memory
+// (griddepcontrol.wait), then lets its own successor be scheduled (launch_dependents).
+// No-ops when the kernel was launched without the attribute.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif
+bool pdl_enabled();  // LINA_PDL=0 disables (api.cpp)
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  LINA_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 // ---------------------------------------------------------------- dtype traits
 template <typename T> struct Elt;

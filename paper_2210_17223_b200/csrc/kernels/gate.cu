@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kGThreads) gate_mma_kernel(const __nv_bfloat16
                                                              float* __restrict__ probs,
                                                              int* __restrict__ idx,
                                                              float* __restrict__ gate, PeerSignal sig) {
+  pdl_enter();
   // fused transport: this rank's receive buffers are free again (the previous backward,
   // which read them, is complete in stream order)
   if (blockIdx.x == 0 && threadIdx.x == 0) sig_post(sig);
@@ -367,8 +368,8 @@ void launch_gate_mma(const void* X, const float* Wg, int T, int d, int E, int k,
     set = smem;
   }
   const int blocks = std::max(1, (T + kGTok - 1) / kGTok);  // T = 0: one CTA still posts the signal
-  gate_mma_kernel<NT><<<blocks, kGThreads, smem, s>>>((const __nv_bfloat16*)X, Wg, T, d, E, k, write_routing,
-                                                      PB, probs, idx, gate, sig);
+  launch_k(gate_mma_kernel<NT>, dim3(blocks), dim3(kGThreads), smem, s, (const __nv_bfloat16*)X, Wg, T, d, E, k,
+           write_routing, PB, probs, idx, gate, sig);
 }
 
 }  // namespace

@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe
                                                        const float* __restrict__ Wg, int Tn, int k, int d,
                                                        int E, int C, int n, int Cm, T* __restrict__ dX,
                                                        PeerSignal sig) {
+  pdl_enter();
   extern __shared__ float dsm[];
   if (threadIdx.x == 0) sig_wait(sig);  // fused transport: the expert input-gradients have landed
   __syncthreads();
@@ -225,6 +226,7 @@ __global__ void __launch_bounds__(256, 2) dwg_tiled_kernel(const T* __restrict__
                                                            const float* __restrict__ gate,
                                                            const float* __restrict__ dg, int Tn, int d,
                                                            int E, int k, float* __restrict__ part) {
+  pdl_enter();
   __shared__ float red[4][256 * 8];
   __shared__ __align__(16) float sL[kDwgTok][8];
   constexpr int NV = sizeof(T) == 2 ? 1 : 2;
@@ -325,6 +327,7 @@ __global__ void __launch_bounds__(256, 2) dwg_tiled_kernel(const T* __restrict__
 constexpr int kRedG = 8;
 __global__ void __launch_bounds__(256) dwg_reduce_kernel(const float* __restrict__ part, int nparts, int dE,
                                                          float* __restrict__ dWg) {
+  pdl_enter();
   __shared__ float gs[kRedG][32];
   const int lane = threadIdx.x & 31, gq = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
@@ -372,8 +375,8 @@ static void launch_dx_t(const void* dXe, const int* idx, const int* slot, const 
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
     set = true;
   }
-  dx_tiled_kernel<T, KT><<<grid, 256, smem, s>>>((const T*)dXe, idx, slot, probs, gate, dg, Wg, Tn, k, d, E,
-                                                C, n, Cm, (T*)dX, sig);
+  launch_k(dx_tiled_kernel<T, KT>, grid, dim3(256), smem, s, (const T*)dXe, idx, slot, probs, gate, dg, Wg, Tn, k, d,
+           E, C, n, Cm, (T*)dX, sig);
 }
 
 void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* probs,
@@ -401,13 +404,14 @@ void launch_dwg(int dtype, const void* X, const float* probs, const int* idx, co
   const int nsplit = dwg_splits(T);
   dim3 grid((d + 255) / 256, nsplit, (E + 7) / 8);
   if (dtype == 0)
-    dwg_tiled_kernel<float><<<grid, 256, 0, s>>>((const float*)X, probs, idx, gate, dg, T, d, E, k, scratch);
+    launch_k(dwg_tiled_kernel<float>, grid, dim3(256), 0, s, (const float*)X, probs, idx, gate, dg, T, d, E, k,
+             scratch);
   else
-    dwg_tiled_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)X, probs, idx, gate, dg, T, d,
-                                                         E, k, scratch);
+    launch_k(dwg_tiled_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, (const __nv_bfloat16*)X, probs, idx, gate, dg,
+             T, d, E, k, scratch);
   LINA_LAUNCH_CHECK();
   const int dE = d * E;
-  dwg_reduce_kernel<<<(dE + 31) / 32, 256, 0, s>>>(scratch, nsplit, dE, dWg);
+  launch_k(dwg_reduce_kernel, dim3((dE + 31) / 32), dim3(256), 0, s, scratch, nsplit, dE, dWg);
   LINA_LAUNCH_CHECK();
 }
 

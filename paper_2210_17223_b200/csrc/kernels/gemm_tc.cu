@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ TcParams p) {
+  pdl_enter();
   using G = Geo<CG, EPI != kEpiNone>;
   constexpr int STAGES = G::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -680,13 +681,15 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   cfg.blockDim = dim3(Geo<CG, EPI != kEpiNone>::THREADS);
   cfg.dynamicSmemBytes = Geo<CG, EPI != kEpiNone>::SMEM_BYTES;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (common.h: pdl_enter)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   LINA_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, b, d, x, p));
 }
 

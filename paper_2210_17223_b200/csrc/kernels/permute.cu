@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ X, c
                                                       int El, int P, int me, T* __restrict__ Send,
                                                       T* const* __restrict__ peer, const int* __restrict__ kept,
                                                       int* const* __restrict__ peer_counts, PeerSignal sig) {
+  pdl_enter();
   if constexpr (PEER) {
     // the owners' receive buffers are free (their FREE of this round), then this rank's
     // counts go to every owner's recv_kept
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ Recv
                                                       const float* __restrict__ gate, int Tn, int k, int d,
                                                       int E, int C, int n, int Cm, T* __restrict__ Y,
                                                       PeerSignal sig) {
+  pdl_enter();
   // fused transport: this rank's backward receive buffers are free again (block 0 posts);
   // the peers' returned expert outputs have landed (every CTA waits)
   if (blockIdx.x == 0 && threadIdx.x == 0) sig_post(sig);
@@ -287,6 +289,7 @@ __global__ void combine_loop_kernel(const T* __restrict__ Recv, const int* __res
                                     const int* __restrict__ slot, const float* __restrict__ gate,
                                     int Tn, int k, int d, int E, int C, int n, int Cm,
                                     T* __restrict__ Y, PeerSignal sig) {
+  pdl_enter();
   if (blockIdx.x == 0 && threadIdx.x == 0) sig_post(sig);
   if (sig.wait) {
     if (threadIdx.x == 0) sig_wait(sig);
@@ -415,6 +418,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ 
                                                           int me, T* __restrict__ dSend,
                                                           T* const* __restrict__ peer,
                                                           float* __restrict__ dg, PeerSignal sig) {
+  pdl_enter();
   if constexpr (PEER) {  // the owners' backward receive buffers are free (their FREE)
     if (threadIdx.x == 0) sig_wait(sig);
     __syncthreads();
@@ -481,9 +485,9 @@ static void permute_any(int dtype, const void* X, const int* tok_of, int k, int 
   if (rows == 0 && !PEER) return;
   const int nvl = nvl_of(d, dtype);
   const long long warps = std::max(1LL, (rows + rows_per_warp(nvl, 1) - 1) / rows_per_warp(nvl, 1));
-  LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (permute_kernel<ET, NV_, PEER><<<blocks_for_warps(warps), 256, 0, s>>>(
-                             (const ET*)X, tok_of, k, d, E, C, c0, nc, Cm, El, P, me, (ET*)Send,
-                             (ET* const*)peer, kept, (int* const*)peer_counts, sig))));
+  LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, launch_k(permute_kernel<ET, NV_, PEER>, dim3(blocks_for_warps(warps)),
+                             dim3(256), 0, s, (const ET*)X, tok_of, k, d, E, C, c0, nc, Cm, El, P, me, (ET*)Send,
+                             (ET* const*)peer, kept, (int* const*)peer_counts, sig)));
   LINA_LAUNCH_CHECK();
 }
 
@@ -504,14 +508,14 @@ void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot
     const int tp = U / k > 0 ? U / k : 1;
     const long long warps = std::max(1LL, ((long long)T + tp - 1) / tp);
     if (k == 1)
-      LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (combine_kernel<ET, NV_, 1><<<blocks_for_warps(warps), 256, 0, s>>>(
-                                 (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg))));
+      LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, launch_k(combine_kernel<ET, NV_, 1>, dim3(blocks_for_warps(warps)),
+                                 dim3(256), 0, s, (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg)));
     else
-      LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (combine_kernel<ET, NV_, 2><<<blocks_for_warps(warps), 256, 0, s>>>(
-                                 (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg))));
+      LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, launch_k(combine_kernel<ET, NV_, 2>, dim3(blocks_for_warps(warps)),
+                                 dim3(256), 0, s, (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg)));
   } else {
-    LINA_DISPATCH_T(dtype, combine_loop_kernel<ET><<<blocks_for_warps(std::max(1, T)), 256, 0, s>>>(
-                               (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg));
+    LINA_DISPATCH_T(dtype, launch_k(combine_loop_kernel<ET>, dim3(blocks_for_warps(std::max(1, T))), dim3(256), 0, s,
+                                    (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg));
   }
   LINA_LAUNCH_CHECK();
 }
@@ -527,9 +531,9 @@ static void combine_bwd_any(int dtype, const void* dY, const void* Recv, const i
   if (rows == 0 && !PEER) return;
   const int nvl = nvl_of(d, dtype);
   const long long warps = std::max(1LL, (rows + rows_per_warp(nvl, 2) - 1) / rows_per_warp(nvl, 2));
-  LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, (combine_bwd_kernel<ET, NV_, PEER><<<blocks_for_warps(warps), 256, 0, s>>>(
-                             (const ET*)dY, (const ET*)Recv, tok_of, kept, gate, k, d, E, C, c0, nc, Cm, El, P,
-                             me, (ET*)dSend, (ET* const*)peer, dg, sig))));
+  LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, launch_k(combine_bwd_kernel<ET, NV_, PEER>,
+                             dim3(blocks_for_warps(warps)), dim3(256), 0, s, (const ET*)dY, (const ET*)Recv, tok_of,
+                             kept, gate, k, d, E, C, c0, nc, Cm, El, P, me, (ET*)dSend, (ET* const*)peer, dg, sig)));
   LINA_LAUNCH_CHECK();
 }
 

@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kRouteBlock) route_assign_kernel(
 
 __global__ void vcount_kernel(const int* __restrict__ recv_kept, int P, int El, int C, int n,
                               int* __restrict__ vcount, PeerSignal sig) {
+  pdl_enter();
   if (threadIdx.x == 0) sig_wait(sig);  // fused transport: the peers' counts have landed
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(kRouteBlock) route_fused_kernel(
     const int* __restrict__ idx, int T, int k, int E, int C, int nb, int* __restrict__ agg,
     unsigned int* __restrict__ sync, int* __restrict__ slot, int* __restrict__ tok_of, int* __restrict__ counts,
     int* __restrict__ kept, int n, int* __restrict__ vcount, int* __restrict__ mtp, int rows) {
+  pdl_enter();
   __shared__ int wc[32][65];
   __shared__ int pre[64], kept_s[64];
   __shared__ unsigned int bid_s;
@@ -217,11 +219,13 @@ __global__ void __launch_bounds__(kRouteBlock) route_fused_kernel(
 // Waiting in a 1-CTA kernel (not in every CTA of the consumer) keeps the SMs free for
 // kernels the peers' progress may depend on (e.g. an NCCL allreduce on another stream).
 __global__ void sig_wait_kernel(PeerSignal sig) {
+  pdl_enter();
   if (threadIdx.x == 0) sig_wait(sig);
 }
 
 __global__ void mtile_prefix_kernel(const int* __restrict__ vcount, int n, int nseg, int rows,
                                     int* __restrict__ mtp) {
+  pdl_enter();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   int run = 0;
@@ -236,13 +240,13 @@ __global__ void mtile_prefix_kernel(const int* __restrict__ vcount, int n, int n
 
 void launch_mtile_prefix(const int* vcount, int n, int nseg, int rows, int* mtp, cudaStream_t s) {
   if (n <= 0) return;
-  mtile_prefix_kernel<<<(n + 63) / 64, 64, 0, s>>>(vcount, n, nseg, rows, mtp);
+  launch_k(mtile_prefix_kernel, dim3((n + 63) / 64), dim3(64), 0, s, vcount, n, nseg, rows, mtp);
   LINA_LAUNCH_CHECK();
 }
 
 void launch_sig_wait(const PeerSignal& sig, cudaStream_t s) {
   if (!sig.wait) return;
-  sig_wait_kernel<<<1, 32, 0, s>>>(sig);
+  launch_k(sig_wait_kernel, dim3(1), dim3(32), 0, s, sig);
   LINA_LAUNCH_CHECK();
 }
 
@@ -250,8 +254,8 @@ void launch_vcount(const int* recv_kept, int P, int El, int C, int n, int* vcoun
                    const PeerSignal* sig) {
   const int tot = n * P * El;
   if (tot <= 0 && !sig) return;
-  vcount_kernel<<<std::max(1, (tot + 255) / 256), 256, 0, s>>>(recv_kept, P, El, C, n, vcount,
-                                                               sig ? *sig : PeerSignal{});
+  launch_k(vcount_kernel, dim3(std::max(1, (tot + 255) / 256)), dim3(256), 0, s, recv_kept, P, El, C, n, vcount,
+           sig ? *sig : PeerSignal{});
   LINA_LAUNCH_CHECK();
 }
 
@@ -277,8 +281,8 @@ void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int*
   }
   const int nb = (int)(((long long)T * k + kRouteBlock - 1) / kRouteBlock);
   if (sync && nb <= kRouteMaxBlocks) {
-    route_fused_kernel<<<nb, kRouteBlock, 0, s>>>(idx, T, k, E, C, nb, scratch, sync, slot, tok_of, counts, kept,
-                                                  n_chunks, vcount, mtp, tile_rows);
+    launch_k(route_fused_kernel, dim3(nb), dim3(kRouteBlock), 0, s, idx, T, k, E, C, nb, scratch, sync, slot, tok_of,
+             counts, kept, n_chunks, vcount, mtp, tile_rows);
     LINA_LAUNCH_CHECK();
     return;
   }
