@@ -17,7 +17,7 @@
 //       dL tile (8 threads per token);
 //       each e step is 32 FMAs for 6 shared loads.  The expert-gradient rows are
 //       gathered with one 16-byte load per (token, kept j).
-// dwg : CTA = 256 columns x 8 experts x 128 tokens, thread = 8 columns x 8 experts,
+// dwg : CTA = 256 columns x 4 experts x 128 tokens, thread = 8 columns x 4 experts,
 //       8 token lanes (one per warp) each walking every 8th token in double-buffered
 //       batches of 4, folded in shared memory in a fixed tree order; each token split
 //       writes one partial, reduced afterwards in a fixed order (deterministic, no
@@ -33,6 +33,7 @@ namespace {
 
 constexpr int kDxTok = 32, kDxCols = 256;
 constexpr int kDwgTok = 128, kDwgB = 4;  // tokens per dwg CTA; tokens per thread per batch
+constexpr int kDwgE = 4;                  // experts per dwg CTA (grid z covers E)
 
 // Wg slab column c = 8*cg + 4*h + q is kept at 128*h + 4*cg + q so that the float4 reads
 // of one half by the 32 column groups of a warp are contiguous (no bank conflicts).
@@ -220,23 +221,24 @@ __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe
 // part[split][col][e] over tokens t in [split*kDwgTok, +kDwgTok): token lane l (= warp)
 // takes t = ta + l + 8*i, combined over the 8 lanes in shared memory in a fixed order.
 template <typename T>
-__global__ void __launch_bounds__(256, 2) dwg_tiled_kernel(const T* __restrict__ X,
+__global__ void __launch_bounds__(256, 3) dwg_tiled_kernel(const T* __restrict__ X,
                                                            const float* __restrict__ probs,
                                                            const int* __restrict__ idx,
                                                            const float* __restrict__ gate,
                                                            const float* __restrict__ dg, int Tn, int d,
                                                            int E, int k, float* __restrict__ part) {
   pdl_enter();
-  __shared__ float red[4][256 * 8];
-  __shared__ __align__(16) float sL[kDwgTok][8];
+  constexpr int EG = kDwgE;  // experts per CTA (blockIdx.z = expert group)
+  __shared__ float red[4][256 * EG];
+  __shared__ __align__(16) float sL[kDwgTok][EG];
   constexpr int NV = sizeof(T) == 2 ? 1 : 2;
   constexpr int NB = kDwgTok / 8 / kDwgB;  // batches per thread
   const int tid = threadIdx.x;
   const int cg = tid & 31, lane_t = tid >> 5;
   const int col = blockIdx.x * 256 + cg * 8;
   const int split = blockIdx.y;
-  const int e0 = blockIdx.z * 8;
-  const int ne = min(8, E - e0);
+  const int e0 = blockIdx.z * EG;
+  const int ne = min(EG, E - e0);
   const int ta = split * kDwgTok;
   const bool cin = col < d;
   uint4 cur[kDwgB][NV], nxt[kDwgB][NV];
@@ -250,28 +252,29 @@ __global__ void __launch_bounds__(256, 2) dwg_tiled_kernel(const T* __restrict__
     }
   };
   load_batch(0, cur);
-  {  // dL tile: 2 threads per token, 4 of the CTA's 8 experts each
-    const int r = tid >> 1, q0 = (tid & 1) * 4, t = ta + r;
-    float pe[4];
+  {  // dL tile: 2 threads per token, half of the CTA's EG experts each
+    constexpr int EH = EG / 2;
+    const int r = tid >> 1, q0 = (tid & 1) * EH, t = ta + r;
+    float pe[EH];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) pe[q] = (t < Tn && q0 + q < ne) ? probs[(size_t)t * E + e0 + q0 + q] : 0.f;
+    for (int q = 0; q < EH; ++q) pe[q] = (t < Tn && q0 + q < ne) ? probs[(size_t)t * E + e0 + q0 + q] : 0.f;
     if (t < Tn) {
       int es[8];
       float dps[8];
       const float dot = token_dp<8>(probs, idx, gate, dg, t, k, E, es, dps);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) sL[r][q0 + q] = q0 + q < ne ? dl_of<8>(pe[q], e0 + q0 + q, dot, es, dps) : 0.f;
+      for (int q = 0; q < EH; ++q) sL[r][q0 + q] = q0 + q < ne ? dl_of<8>(pe[q], e0 + q0 + q, dot, es, dps) : 0.f;
     } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) sL[r][q0 + q] = 0.f;
+      for (int q = 0; q < EH; ++q) sL[r][q0 + q] = 0.f;
     }
   }
   __syncthreads();
-  float acc[8][8];
+  float acc[8][EG];
 #pragma unroll
   for (int c = 0; c < 8; ++c)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[c][q] = 0.f;
+    for (int q = 0; q < EG; ++q) acc[c][q] = 0.f;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     if (b + 1 < NB) load_batch(b + 1, (b & 1) ? cur : nxt);
@@ -286,13 +289,19 @@ __global__ void __launch_bounds__(256, 2) dwg_tiled_kernel(const T* __restrict__
         load16(&r[i][NV - 1], x + 4, (const float*)nullptr);
       }
       const int tr = lane_t + 8 * (b * kDwgB + i);
-      const float4 la = *reinterpret_cast<const float4*>(&sL[tr][0]);
-      const float4 lb = *reinterpret_cast<const float4*>(&sL[tr][4]);
-      const float l[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+      float l[EG];
+#pragma unroll
+      for (int q = 0; q < EG; q += 4) {
+        const float4 lv = *reinterpret_cast<const float4*>(&sL[tr][q]);
+        l[q] = lv.x;
+        l[q + 1] = lv.y;
+        l[q + 2] = lv.z;
+        l[q + 3] = lv.w;
+      }
 #pragma unroll
       for (int c = 0; c < 8; ++c)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[c][q] = fmaf(x[c], l[q], acc[c][q]);
+        for (int q = 0; q < EG; ++q) acc[c][q] = fmaf(x[c], l[q], acc[c][q]);
     }
   }
   // fixed-order tree over the 8 token lanes: (0+4,1+5,2+6,3+7), (0+2,1+3), (0+1)
@@ -301,14 +310,14 @@ __global__ void __launch_bounds__(256, 2) dwg_tiled_kernel(const T* __restrict__
 #pragma unroll
       for (int c = 0; c < 8; ++c)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) red[lane_t - half][(c * 8 + q) * 32 + cg] = acc[c][q];
+        for (int q = 0; q < EG; ++q) red[lane_t - half][(c * EG + q) * 32 + cg] = acc[c][q];
     }
     __syncthreads();
     if (lane_t < half) {
 #pragma unroll
       for (int c = 0; c < 8; ++c)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[c][q] += red[lane_t][(c * 8 + q) * 32 + cg];
+        for (int q = 0; q < EG; ++q) acc[c][q] += red[lane_t][(c * EG + q) * 32 + cg];
     }
     __syncthreads();
   }
@@ -317,7 +326,7 @@ __global__ void __launch_bounds__(256, 2) dwg_tiled_kernel(const T* __restrict__
 #pragma unroll
     for (int c = 0; c < 8; ++c)
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
+      for (int q = 0; q < EG; ++q)
         if (q < ne) dst[(size_t)c * E + q] = acc[c][q];
   }
 }
@@ -402,7 +411,7 @@ void launch_dwg(int dtype, const void* X, const float* probs, const int* idx, co
     return;
   }
   const int nsplit = dwg_splits(T);
-  dim3 grid((d + 255) / 256, nsplit, (E + 7) / 8);
+  dim3 grid((d + 255) / 256, nsplit, (E + kDwgE - 1) / kDwgE);
   if (dtype == 0)
     launch_k(dwg_tiled_kernel<float>, grid, dim3(256), 0, s, (const float*)X, probs, idx, gate, dg, T, d, E, k,
              scratch);
