@@ -78,8 +78,8 @@ CeTransport::CeTransport(lina_comm* cm) : cm_(cm), impl_(new Impl) {
   LINA_CUDA_CHECK(cudaMalloc(&impl_->stage, 128 * (size_t)P));
   LINA_CUDA_CHECK(cudaMalloc(&done_, kDoneSites * sizeof(unsigned int)));
   LINA_CUDA_CHECK(cudaMemset(done_, 0, kDoneSites * sizeof(unsigned int)));
-  LINA_CUDA_CHECK(cudaMalloc(&rounds_, 2 * sizeof(uint32_t)));
-  LINA_CUDA_CHECK(cudaMemset(rounds_, 0, 2 * sizeof(uint32_t)));
+  LINA_CUDA_CHECK(cudaMalloc(&rounds_, 3 * sizeof(uint32_t)));
+  LINA_CUDA_CHECK(cudaMemset(rounds_, 0, 3 * sizeof(uint32_t)));
   peer_slots_.assign(kKinds, nullptr);
   peer_flags_ = map_collective(flags_, cm->hi);
   for (int r = 0; r < P; ++r) {

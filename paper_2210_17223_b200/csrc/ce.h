@@ -15,7 +15,9 @@ class CeTransport {
          kPulledFwdD = 4, kPulledFwdC = 5, kPulledBwdD = 6, kPulledBwdC = 7,
          kFreeFwd = 8, kFreeBwd = 9,
          // fused transport (in-kernel signals; rounds from the device counters below)
-         kFReadyFwdD = 10, kFReadyFwdC = 11, kFReadyBwdD = 12, kFReadyBwdC = 13, kKinds = 14 };
+         kFReadyFwdD = 10, kFReadyFwdC = 11, kFReadyBwdD = 12, kFReadyBwdC = 13,
+         // inference exchange by peer stores (infer.cpp)
+         kIFreeD = 14, kIReadyD = 15, kIFreeC = 16, kIReadyC = 17, kKinds = 18 };
   static constexpr int kMaxChunks = 32;
 
   explicit CeTransport(lina_comm* cm);  // collective (allgathers the flag-array handles)
@@ -38,6 +40,7 @@ class CeTransport {
   // device round counters of the fused transport: [0] forward, [1] backward
   uint32_t* round_fwd() const { return rounds_; }
   uint32_t* round_bwd() const { return rounds_ + 1; }
+  uint32_t* round_inf() const { return rounds_ + 2; }
   static constexpr int kDoneSites = 16;
   cudaStream_t disp_stream(int peer) const { return disp_[peer]; }
   cudaStream_t comb_stream(int peer) const { return comb_[peer]; }

@@ -25,6 +25,7 @@
 #include <cstring>
 #include <vector>
 
+#include "ce.h"
 #include "internal.h"
 #include "kernels.h"
 #include "layer.h"
@@ -37,7 +38,7 @@ struct InferPlan {
   int T, d, f, E, k, P, mpd, dt;
   size_t Cmax;
   size_t o_probs, o_idx, o_gate, o_slot, o_counts, o_kept, o_tokof, o_route, o_all, o_tab, o_vc,
-      o_mtp, o_gvc, o_segx, o_arow, o_send, o_recv, o_gin, o_h, o_o, o_back2, o_back, total;
+      o_mtp, o_gvc, o_segx, o_blk, o_arow, o_send, o_recv, o_gin, o_h, o_o, o_back2, o_back, total;
   size_t tab_ints() const { return (size_t)E + (size_t)E * P + (size_t)P * E + E; }
 };
 
@@ -75,6 +76,7 @@ static InferPlan infer_plan(const lina_moe_desc& dsc, int P, int mpd) {
   q.o_mtp = take(4 * ((size_t)mpd + 1));   // tile prefix over the hosted experts
   q.o_gvc = take(4 * (size_t)mpd);         // rows per hosted expert (all sources)
   q.o_segx = take(4 * (size_t)mpd);
+  q.o_blk = take(4 * 6 * (size_t)P);        // fused exchange: {src_row, dst_row, rows} per peer, both ways
   q.o_arow = take(4 * Tk);
   q.o_send = take(Tk * q.d * q.dt);
   q.o_recv = take((size_t)P * Tk * q.d * q.dt);          // source-major receive
@@ -125,6 +127,7 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   int* mtp = (int*)(w + q.o_mtp);
   int* gvc = (int*)(w + q.o_gvc);
   int* segx = (int*)(w + q.o_segx);
+  int* blk = (int*)(w + q.o_blk);
   int* arow = (int*)(w + q.o_arow);
   char* send = w + q.o_send;
   char* recv = w + q.o_recv;
@@ -139,6 +142,33 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
 
   trace_flush(cm);
   trace_mark(cm, s, "inf:start");
+  // Fused exchange (peer stores, in-kernel flags) when the comm has the IPC transport;
+  // NCCL send/recv otherwise.  This call's round is *round_inf + 1, closed at its end.
+  CeTransport* ce = (P > 1 && cm->ce && cm->transport == 2) ? cm->ce : nullptr;
+  uint32_t* ri = ce ? ce->round_inf() : nullptr;
+  auto isig = [&](int wait_kind, int post_kind, int site, uint32_t* bump) {
+    PeerSignal g;
+    g.P = P;
+    g.me = rank;
+    g.stride = CeTransport::kMaxChunks;
+    if (wait_kind >= 0) {
+      g.wait = ce->slots(wait_kind);
+      g.wait_round = ri;
+      g.wait_add = 1;
+    }
+    if (post_kind >= 0) {
+      g.post = ce->peer_slots(post_kind);
+      g.post_round = ri;
+      g.post_add = 1;
+    }
+    g.done = site >= 0 ? ce->done_counter(site) : nullptr;
+    g.bump = bump;
+    return g;
+  };
+  if (ce) {  // my receive and return buffers were last read by the previous call
+    launch_sig_wait(isig(-1, CeTransport::kIFreeD, -1, nullptr), s);
+    launch_sig_wait(isig(-1, CeTransport::kIFreeC, -1, nullptr), s);
+  }
   // ---- gate, dropless slots, counts (S1, S2 with C = T)
   launch_gate_topk(dtype, tokens, gate_w, T, d, E, k, 1, probs, idx, gate, s);
   launch_route(idx, T, k, E, std::max(T, 1), (int*)(w + q.o_route), slot, counts, kept, tokof, s, cm->route_sync);
@@ -147,7 +177,7 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   } else {
     LINA_CUDA_CHECK(cudaMemcpyAsync(allc, counts, 4 * (size_t)E, cudaMemcpyDeviceToDevice, s));
   }
-  const size_t ctrl_ints = (size_t)P * E + q.tab_ints() + (size_t)P * mpd + (mpd + 1) + 2 * (size_t)mpd;
+  const size_t ctrl_ints = (size_t)P * E + q.tab_ints() + (size_t)P * mpd + (mpd + 1) + 2 * (size_t)mpd + 6 * (size_t)P;
   int* host = pinned(cm, ctrl_ints);
   trace_mark(cm, s, "inf:gate+route+counts");
   LINA_CUDA_CHECK(cudaMemcpyAsync(host, allc, 4 * (size_t)P * E, cudaMemcpyDeviceToHost, s));
@@ -226,6 +256,14 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
     }
     src_cnt[src] = roff - src_off[src];
   }
+  // rows every source sends every device (identical on all ranks): where my blocks land
+  std::vector<int> cnt_sd((size_t)P * P, 0);
+  for (int src = 0; src < P; ++src)
+    for (int dv = 0; dv < P; ++dv)
+      for (int i = 0; i < mpd; ++i) {
+        const int e = hosted[(size_t)dv * mpd + i];
+        if (e >= 0) cnt_sd[(size_t)src * P + dv] += tokens_to(src, e, dv);
+      }
   int maxrows = 0;
   for (int h = 0; h < mpd; ++h) maxrows = std::max(maxrows, tot[h]);
   const int Cm = std::max(128, (maxrows + 127) / 128 * 128);
@@ -252,18 +290,38 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   }
   h_mtp[mpd] = run;
   for (int i = 0; i < mpd; ++i) h_segx[i] = std::max(0, hosted[(size_t)rank * mpd + i]);
+  int* h_blk = h_segx + mpd;
+  int maxblk = 0;
+  for (int o = 0; o < P; ++o) {
+    int at_o = 0, at_me = 0;  // my block's row in o's receive buffer / o's block's row in my return buffer
+    for (int s2 = 0; s2 < rank; ++s2) at_o += cnt_sd[(size_t)s2 * P + o];
+    for (int dv = 0; dv < rank; ++dv) at_me += cnt_sd[(size_t)o * P + dv];
+    h_blk[3 * o] = dv_off[o];  // dispatch: my send block for device o -> o's receive (source-major)
+    h_blk[3 * o + 1] = at_o;
+    h_blk[3 * o + 2] = dv_cnt[o];
+    h_blk[3 * (P + o)] = src_off[o];  // return: rows source o sent me -> o's return buffer
+    h_blk[3 * (P + o) + 1] = at_me;
+    h_blk[3 * (P + o) + 2] = src_cnt[o];
+    maxblk = std::max(maxblk, std::max(dv_cnt[o], src_cnt[o]));
+  }
   LINA_CUDA_CHECK(cudaMemcpyAsync(tab, h_tab, 4 * q.tab_ints(), cudaMemcpyHostToDevice, s));
   LINA_CUDA_CHECK(cudaMemcpyAsync(vc, h_vc, 4 * (size_t)P * mpd, cudaMemcpyHostToDevice, s));
   LINA_CUDA_CHECK(cudaMemcpyAsync(mtp, h_mtp, 4 * (size_t)(mpd + 1), cudaMemcpyHostToDevice, s));
   LINA_CUDA_CHECK(cudaMemcpyAsync(gvc, h_gvc, 4 * (size_t)mpd, cudaMemcpyHostToDevice, s));
   LINA_CUDA_CHECK(cudaMemcpyAsync(segx, h_segx, 4 * (size_t)mpd, cudaMemcpyHostToDevice, s));
+  if (ce) LINA_CUDA_CHECK(cudaMemcpyAsync(blk, h_blk, 4 * 6 * (size_t)P, cudaMemcpyHostToDevice, s));
 
   trace_mark(cm, s, "inf:plan+tables(host)");
   // ---- replica-routed permute and the unequal-split all-to-all
   launch_infer_permute(dtype, tokens, idx, slot, tab, T, k, d, E, P, rank, send, arow, s);
   trace_mark(cm, s, "inf:permute");
   // one message per peer: my block for device dv -> its source-major receive block
-  if (P > 1) {
+  if (ce) {  // peer stores (after the owners' FREE; READY when every block has landed)
+    void* const* peer_recv = ce->dev_ptrs(ws, q.o_recv, s);
+    launch_sig_wait(isig(CeTransport::kIFreeD, -1, -1, nullptr), s);
+    launch_push_blocks(dtype, send, peer_recv, blk, P, d, maxblk, isig(-1, CeTransport::kIReadyD, 6, nullptr), s);
+    launch_sig_wait(isig(CeTransport::kIReadyD, -1, -1, nullptr), s);
+  } else if (P > 1) {
     LINA_NCCL_CHECK(ncclGroupStart());
     for (int dv = 0; dv < P; ++dv)
       if (dv_cnt[dv])
@@ -307,7 +365,13 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
 
   // ---- second all-to-all (expert outputs back to their sources, one message per peer)
   launch_regroup(dtype, obuf, back2, vc, P, mpd, Cm, d, maxseg, false, s);
-  if (P > 1) {
+  if (ce) {  // the rows go back by peer stores; the last wait also closes this call's round
+    void* const* peer_back = ce->dev_ptrs(ws, q.o_back, s);
+    launch_sig_wait(isig(CeTransport::kIFreeC, -1, -1, nullptr), s);
+    launch_push_blocks(dtype, back2, peer_back, blk + 3 * P, P, d, maxblk, isig(-1, CeTransport::kIReadyC, 7, nullptr),
+                       s);
+    launch_sig_wait(isig(CeTransport::kIReadyC, -1, -1, ri), s);
+  } else if (P > 1) {
     LINA_NCCL_CHECK(ncclGroupStart());
     for (int src = 0; src < P; ++src)
       if (src_cnt[src])

@@ -51,8 +51,13 @@ void launch_route(const int* idx, int T, int k, int E, int C, int* scratch, int*
                   int* kept, int* tok_of, cudaStream_t s, unsigned int* sync = nullptr, int n_chunks = 1,
                   int* vcount = nullptr, int* mtp = nullptr, int tile_rows = 256);
 // vcount[(c*P + s)*El + el] = clamp(recv_kept[s*El + el] - b_c, 0, Cc)
-// A 1-CTA kernel that waits for sig's flags (sig.post ignored).
+// A 1-CTA kernel that waits for sig's flags, then publishes sig.post and bumps sig.bump
+// (each part optional).  Callers pass no_wait()-style signals to the consumer kernel.
 void launch_sig_wait(const PeerSignal& sig, cudaStream_t s);
+// Row blocks to peers over NVLink: block b copies rows [src_row[b], +nrows[b]) of `src`
+// to peer_dst[b] + dst_row[b] (rows of d elements); the last CTA posts sig.
+void launch_push_blocks(int dtype, const void* src, void* const* peer_dst, const int* blocks /*[P][3]*/, int P,
+                        int d, int max_rows, const PeerSignal& sig, cudaStream_t s);
 // sig: every CTA first waits for the peers' counts (READY of the dispatch)
 void launch_vcount(const int* recv_kept, int P, int El, int C, int n, int* vcount, cudaStream_t s,
                    const PeerSignal* sig = nullptr);

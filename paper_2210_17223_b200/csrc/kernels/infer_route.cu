@@ -21,6 +21,7 @@
 
 #include "../common.h"
 #include "../kernels.h"
+#include "../signal.h"
 
 namespace lina {
 namespace {
@@ -119,6 +120,26 @@ __global__ void __launch_bounds__(256) regroup_kernel(const T* __restrict__ src_
     for (int v = lane; v < nv; v += 32) to[v] = from[v];
   }
 }
+
+// blocks[b] = {src_row, dst_row, nrows}: rows of block b go to peer_dst[b] (blockIdx.y = b)
+template <typename T>
+__global__ void __launch_bounds__(256) push_blocks_kernel(const T* __restrict__ src, T* const* __restrict__ peer_dst,
+                                                          const int* __restrict__ blocks, int d, PeerSignal sig) {
+  pdl_enter();
+  const int b = blockIdx.y;
+  const int r0 = blocks[3 * b], d0 = blocks[3 * b + 1], n = blocks[3 * b + 2];
+  constexpr int V = 16 / sizeof(T);
+  const int nv = d / V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* dst = peer_dst[b];
+  for (int i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
+    const uint4* from = reinterpret_cast<const uint4*>(src + (size_t)(r0 + i) * d);
+    uint4* to = reinterpret_cast<uint4*>(dst + (size_t)(d0 + i) * d);
+    for (int v = lane; v < nv; v += 32) to[v] = from[v];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sig_post_last(sig);
+}
 }  // namespace
 
 void launch_infer_permute(int dtype, const void* X, const int* idx, const int* slot, const int* tab,
@@ -160,6 +181,20 @@ void launch_regroup(int dtype, const void* src, void* dst, const int* nrecv, int
   else
     regroup_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, nrecv,
                                                          P, mpd, Cm, d, to_expert_major ? 1 : 0);
+  LINA_LAUNCH_CHECK();
+}
+}  // namespace lina
+
+namespace lina {
+void launch_push_blocks(int dtype, const void* src, void* const* peer_dst, const int* blocks, int P, int d,
+                        int max_rows, const PeerSignal& sig, cudaStream_t st) {
+  dim3 grid(std::max(1, std::min(64, (max_rows + 7) / 8)), P);
+  if (dtype == 0)
+    launch_k(push_blocks_kernel<float>, grid, dim3(256), 0, st, (const float*)src, (float* const*)peer_dst, blocks, d,
+             sig);
+  else
+    launch_k(push_blocks_kernel<__nv_bfloat16>, grid, dim3(256), 0, st, (const __nv_bfloat16*)src,
+             (__nv_bfloat16* const*)peer_dst, blocks, d, sig);
   LINA_LAUNCH_CHECK();
 }
 }  // namespace lina

@@ -220,7 +220,11 @@ __global__ void __launch_bounds__(kRouteBlock) route_fused_kernel(
 // kernels the peers' progress may depend on (e.g. an NCCL allreduce on another stream).
 __global__ void sig_wait_kernel(PeerSignal sig) {
   pdl_enter();
-  if (threadIdx.x == 0) sig_wait(sig);
+  if (threadIdx.x == 0) {
+    sig_wait(sig);
+    sig_post(sig);                      // (a 1-CTA kernel publishes right away)
+    if (sig.bump) *sig.bump = *sig.bump + 1u;
+  }
 }
 
 __global__ void mtile_prefix_kernel(const int* __restrict__ vcount, int n, int nseg, int rows,
@@ -245,7 +249,7 @@ void launch_mtile_prefix(const int* vcount, int n, int nseg, int rows, int* mtp,
 }
 
 void launch_sig_wait(const PeerSignal& sig, cudaStream_t s) {
-  if (!sig.wait) return;
+  if (!sig.wait && !sig.post && !sig.bump) return;
   launch_k(sig_wait_kernel, dim3(1), dim3(32), 0, s, sig);
   LINA_LAUNCH_CHECK();
 }

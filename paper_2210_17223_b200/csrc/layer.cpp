@@ -326,6 +326,12 @@ PeerSignal make_sig(lina_comm* cm, int wait_kind, const uint32_t* wait_round, ui
 }
 // The wait part of a signal runs as its own 1-CTA kernel (launch_sig_wait); the consumer
 // gets the rest.
+PeerSignal wait_only(PeerSignal g) {
+  g.post = nullptr;
+  g.bump = nullptr;
+  g.done = nullptr;
+  return g;
+}
 PeerSignal no_wait(PeerSignal g) {
   g.wait = nullptr;
   g.wait_round = nullptr;
@@ -417,7 +423,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
     LINA_CUDA_CHECK(cudaEventRecord(cm->ev[0], s));
     LINA_CUDA_CHECK(cudaStreamWaitEvent(sm, cm->ev[0], 0));
   }
-  launch_sig_wait(s_disp, sm);
+  launch_sig_wait(wait_only(s_disp), sm);
   for (int c = 0; c < n; ++c)
     launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, c, 1, p.Cm, p.El, P, me, peer_R,
                         peer_cnt, chunk_sig(no_wait(s_disp), c), sm);
@@ -436,7 +442,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   const PeerSignal s_recv = make_sig(cm, CT::kFReadyFwdD, rf, 1, -1, nullptr, 0);
   const PeerSignal s_comb = make_sig(cm, -1, nullptr, 0, CT::kFReadyFwdC, rf, 1, kSiteCombFwd);
   for (int c = 0; c < n; ++c) {
-    launch_sig_wait(chunk_sig(s_recv, c), s);  // micro-op c (and with c = 0 the counts) has landed
+    launch_sig_wait(wait_only(chunk_sig(s_recv, c)), s);  // micro-op c (and with c = 0 the counts) has landed
     if (c == 0) {
       launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
       launch_mtile_prefix(q.vcount, n, P * p.El, tc_tile_rows(), q.mtp, s);
@@ -457,7 +463,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   // backward); the returned expert outputs of every micro-op have landed (1-CTA wait);
   // its last CTA closes the forward's round
   const PeerSignal s_out = make_sig(cm, CT::kFReadyFwdC, rf, 1, CT::kFreeBwd, rf, 1, kSiteFwdEnd, rf);
-  launch_sig_wait(chunk_sig(s_out, 0, n), s);
+  launch_sig_wait(wait_only(chunk_sig(s_out, 0, n)), s);
   const PeerSignal s_out2 = no_wait(s_out);
   launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, out, s, &s_out2);
   trace_mark(cm, s, "combine");
@@ -484,7 +490,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
     LINA_CUDA_CHECK(cudaEventRecord(cm->ev[2], s));
     LINA_CUDA_CHECK(cudaStreamWaitEvent(sm, cm->ev[2], 0));
   }
-  launch_sig_wait(s_disp, sm);
+  launch_sig_wait(wait_only(s_disp), sm);
   for (int c = 0; c < n; ++c)
     launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.T, p.k, p.d, p.E, p.C, c, 1, p.Cm, p.El,
                             P, me, peer_dO, q.dg, chunk_sig(no_wait(s_disp), c), sm);
@@ -494,7 +500,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   const PeerSignal s_comb = make_sig(cm, -1, nullptr, 0, CT::kFReadyBwdC, rb, 1, kSiteCombBwd);
   prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
-    launch_sig_wait(chunk_sig(s_recv, c), s);  // micro-op c of the peers' dO rows has landed
+    launch_sig_wait(wait_only(chunk_sig(s_recv, c)), s);  // micro-op c of the peers' dO rows has landed
     row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask);
     trace_mark(cm, s, "dgrad1");
     RowGemm g = peer_gemm(p, q.dH, w1, q.dXe, q.vcount, q.mtp, c, p.d, p.f);
@@ -517,7 +523,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, p.E, p.k, q.dwg, dgate_w, s);
   trace_mark(cm, s, "dwg");
   const PeerSignal s_back = make_sig(cm, CT::kFReadyBwdC, rb, 1, -1, nullptr, 0, kSiteBwdEnd, rb);
-  launch_sig_wait(chunk_sig(s_back, 0, n), s);
+  launch_sig_wait(wait_only(chunk_sig(s_back, 0, n)), s);
   const PeerSignal s_back2 = no_wait(s_back);
   launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm,
             dtokens, s, &s_back2);
