@@ -86,3 +86,9 @@ def test_full_size_two_ranks_graph():
 @pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
 def test_full_size_four_ranks_graph():
     _run_full(4, 29652)
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
+def test_infer_replication_four_ranks():
+    """S10 at 4 ranks: plan = oracle, replicated = static bitwise, fused peer-store all-to-all."""
+    _run_infer(4, "--tokens", "512", "--zipf", "1.2", "--experts", "32", port=29622)
