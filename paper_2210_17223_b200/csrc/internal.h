@@ -42,6 +42,7 @@ class CeTransport;  // ce.cpp
 // Buffer plan for one descriptor on one communicator (layer.cpp).
 struct Plan {
   int T, d, f, E, k, C, n, P, El, Cm, dt;  // dt = element bytes
+  int tile_rows;                           // expert row-GEMM M tile (128 or 256)
   bool bf16;
   // offsets (bytes) into `saved`
   size_t s_probs, s_idx, s_gate, s_slot, s_kept, s_tokof, s_recvkept, s_vcount, s_mtp, s_R, s_H,

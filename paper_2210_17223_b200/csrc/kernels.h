@@ -26,6 +26,7 @@ struct RowGemm {
   uint64_t* mask_out = nullptr;       // tcgen05 ReLU epilogue: ReLU' bits [nseg_total][N/64][Cm]
   const uint64_t* mask_in = nullptr;  // tcgen05 mask epilogue: those bits (aux unused)
   const PeerSignal* sig = nullptr;    // tcgen05: wait before the first A load, post after the last store
+  int tile_rows = 256;                // tcgen05 M tile (256: CTA pairs, 128: single CTAs); = mtp's rows
 };
 
 // Weight-gradient GEMM: D[El][M][N] = Σ_{c,s} Σ_{r < v} A[seg][r][:]ᵀ B[seg][r][:].
@@ -82,7 +83,8 @@ size_t dwg_scratch_floats(int T, int d, int E);
 void launch_dwg(int dtype, const void* X, const float* probs, const int* idx, const float* gate,
                 const float* dg, int T, int d, int E, int k, float* scratch, float* dWg, cudaStream_t s);
 
-// CTAs per tensor-core tile (cta_group::2 pairs -> 256-row tiles).
+// CTAs per tensor-core tile (cta_group::2 pairs -> 256-row tiles) of the wgrad and the
+// default row GEMM; row GEMMs may also run 128-row single-CTA tiles (RowGemm::tile_rows).
 constexpr int kTcCtaGroup = 2;
 int tc_tile_rows();
 // SMs the persistent GEMM grid leaves free for concurrently running NCCL kernels.

@@ -741,10 +741,21 @@ std::vector<unsigned char> tc_peer_dmaps(const std::vector<char*>& bases, int N,
   return out;
 }
 
+// tile_rows 256: 2-CTA pairs (cta_group::2, M = 256, B halves shared); 128: one CTA per
+// tile (cta_group::1, M = 128) for layers whose expert segments hold few rows.
+template <int CG>
+static void row_gemm_tc_impl_t(const RowGemm& g, bool b_kmajor, int epi, const PeerStore* ps, cudaStream_t s);
+
 static void row_gemm_tc_impl(const RowGemm& g, bool b_kmajor, int epi, const PeerStore* ps,
                              cudaStream_t s) {
+  if (g.tile_rows == 128) row_gemm_tc_impl_t<1>(g, b_kmajor, epi, ps, s);
+  else if (g.tile_rows == 256) row_gemm_tc_impl_t<2>(g, b_kmajor, epi, ps, s);
+  else throw CudaError{"tcgen05 row GEMM: tile_rows must be 128 or 256"};
+}
+
+template <int CG>
+static void row_gemm_tc_impl_t(const RowGemm& g, bool b_kmajor, int epi, const PeerStore* ps, cudaStream_t s) {
   using namespace tc;
-  constexpr int CG = kTcCtaGroup;
   const int nseg_total = g.seg0 + g.nseg;  // the map spans every segment up to this launch's last
   const uint64_t adims[3] = {(uint64_t)g.K, (uint64_t)g.Cm, (uint64_t)nseg_total};
   const uint64_t astr[2] = {(uint64_t)g.K * 2, (uint64_t)g.Cm * g.K * 2};

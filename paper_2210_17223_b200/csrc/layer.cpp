@@ -42,6 +42,14 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
   p.Cm = chunk_rows_max(p.C, p.n);
   p.bf16 = dsc.dtype == LINA_BF16;
   p.dt = p.bf16 ? 2 : 4;
+  // M tile of the expert row GEMMs: 256-row CTA pairs unless a segment (one source's
+  // rows of one expert) averages fewer rows than half a pair tile; LINA_TILE_ROWS=128|256
+  {
+    const long long per_seg = (long long)p.T * p.k / std::max(1, p.E);
+    p.tile_rows = per_seg < 192 ? 128 : 256;
+    const char* tr = getenv("LINA_TILE_ROWS");
+    if (tr && (atoi(tr) == 128 || atoi(tr) == 256)) p.tile_rows = atoi(tr);
+  }
   const size_t T = p.T, k = p.k, E = p.E;
   const size_t send_rows = p.rows_send(), recv_rows = p.rows_recv();
   size_t o = 0;
@@ -146,6 +154,7 @@ void row_gemm(const Plan& p, const void* A, const void* B, void* D, const void* 
               cudaStream_t st, uint64_t* mask_out = nullptr, const uint64_t* mask_in = nullptr,
               const PeerSignal* sig = nullptr) {
   RowGemm g{};
+  g.tile_rows = p.tile_rows;
   g.sig = sig;
   g.mask_out = mask_out;
   g.mask_in = mask_in;
@@ -200,7 +209,7 @@ void forward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, con
     LINA_CUDA_CHECK(cudaStreamWaitEvent(s, ce.ev(0, src, CeTransport::kMaxChunks), 0));
   if (compute) {
     launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
-    launch_mtile_prefix(q.vcount, n, P * p.El, tc_tile_rows(), q.mtp, s);
+    launch_mtile_prefix(q.vcount, n, P * p.El, p.tile_rows, q.mtp, s);
   }
   for (int r = 0; r < P; ++r)  // every peer has pulled my previous O
     if (r != me) ce.wait_flag(s, CeTransport::kPulledFwdC, r, 0, ce.prev_ce_fwd);
@@ -374,6 +383,7 @@ PeerStore peer_store(CeTransport& ce, const char* tag, void* buf, size_t off, co
 RowGemm peer_gemm(const Plan& p, const void* A, const void* B, void* D, const int* vcount, const int* mtp, int c,
                   int N, int K) {
   RowGemm g{};
+  g.tile_rows = p.tile_rows;
   g.mtp = mtp + (size_t)c * (p.P * p.El + 1);
   g.A = A;
   g.B = B;
@@ -445,7 +455,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
     launch_sig_wait(wait_only(chunk_sig(s_recv, c)), s);  // micro-op c (and with c = 0 the counts) has landed
     if (c == 0) {
       launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
-      launch_mtile_prefix(q.vcount, n, P * p.El, tc_tile_rows(), q.mtp, s);
+      launch_mtile_prefix(q.vcount, n, P * p.El, p.tile_rows, q.mtp, s);
       trace_mark(cm, s, "vcount");
       prof_begin(cm, s);
     }
@@ -590,7 +600,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   // (P = 1: the route launch also yields the chunk segments' valid rows and m-tile prefix)
   launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr,
                q.kept, q.tok_of, s, cm->route_sync, p.n, p.P == 1 ? q.vcount : nullptr,
-               p.P == 1 ? q.mtp : nullptr, tc_tile_rows());
+               p.P == 1 ? q.mtp : nullptr, p.tile_rows);
   launch_permute(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, p.n, p.Cm, q.D, s);
   if (route) {
     if (route->idx && !override_r)
@@ -653,7 +663,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   }
   LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_cnt, 0));
   launch_vcount(q.recv_kept, p.P, p.El, p.C, n, q.vcount, s);
-  launch_mtile_prefix(q.vcount, n, p.P * p.El, tc_tile_rows(), q.mtp, s);
+  launch_mtile_prefix(q.vcount, n, p.P * p.El, p.tile_rows, q.mtp, s);
   for (int c = 0; c < n; ++c) {
     LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_disp[c], 0));
     prof_begin(cm, s);
