@@ -39,9 +39,11 @@ void count_launch();
 // (griddepcontrol.wait), then lets its own successor be scheduled (launch_dependents).
 // No-ops when the kernel was launched without the attribute.
 #ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  pdl_wait();
+  pdl_trigger();
 }
 #endif
 bool pdl_enabled();  // LINA_PDL=0 disables (api.cpp)

@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kRouteBlock) route_fused_kernel(
 // Waiting in a 1-CTA kernel (not in every CTA of the consumer) keeps the SMs free for
 // kernels the peers' progress may depend on (e.g. an NCCL allreduce on another stream).
 __global__ void sig_wait_kernel(PeerSignal sig) {
-  pdl_enter();
+  pdl_wait();  // (its successor is released only after the flags: no CTAs parked beside a spin)
   if (threadIdx.x == 0) {
     sig_wait(sig);
     sig_post(sig);                      // (a 1-CTA kernel publishes right away)
