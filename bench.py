@@ -430,11 +430,29 @@ def main():
                "h2d_bytes_per_step": 2 * T * d * elt, "d2h_bytes_per_step": 2 * T * d * elt,
                "copies": "pinned host <-> device on two copy streams, double-buffered, overlapping compute"}
 
-    # ---------------- roofline of the dominant kernel family (expert GEMMs, tensor-bound)
+    # ---------------- roofline of the dominant kernel family (the six expert GEMMs).  Its
+    # bound is whichever floor is higher: tensor = 12·d·f flop per kept
+    # assignment at the sustained bf16 peak; HBM = the algorithmic bytes of the six GEMMs
+    # as separate kernels — the local experts' W1 and W2 read twice (GEMM1/GEMM2, the two
+    # dgrads) and dW1, dW2 written once (6·d·f elements per expert), per kept row 6·d + 6·f
+    # activation elements (X, H, Y, dY, dH, dX in and out, H / dH / X / dY again for the
+    # wgrads) and the ReLU' bits written and read once (2·f/8 bytes) — at the measured copy
+    # bandwidth.  C2 and C5 are tensor-bound; C4's ~128-row experts stream their weights
+    # and are HBM-bound.
     pk = peaks()
+    elt = 2 if tdt == torch.bfloat16 else 4
     flops_per_step_local = 12.0 * kept_local * d * f          # fwd 4df + bwd 8df per kept assignment
+    bytes_per_step_local = (6.0 * (E // world) * d * f * elt + kept_local * (6.0 * (d + f) * elt + 2.0 * f / 8))
     gemm_ms_per_step = gemm_ms / max(args.steps, 1)
-    achieved = flops_per_step_local / (gemm_ms_per_step / 1e3) / 1e12 if gemm_ms > 0 else None
+    t_tensor_ms = flops_per_step_local / (pk["bf16_sustained"] * 1e12) * 1e3
+    t_hbm_ms = bytes_per_step_local / (pk["hbm"] * 1e9) * 1e3
+    hbm_bound = t_hbm_ms > t_tensor_ms
+    if hbm_bound:
+        achieved = bytes_per_step_local / (gemm_ms_per_step / 1e3) / 1e9 if gemm_ms > 0 else None
+        peak, unit, psrc = pk["hbm"], "GB/s", f"{pk['src']} HBM copy bandwidth (MEASURED_PEAKS.json)"
+    else:
+        achieved = flops_per_step_local / (gemm_ms_per_step / 1e3) / 1e12 if gemm_ms > 0 else None
+        peak, unit, psrc = pk["bf16_sustained"], "TFLOP/s", f"{pk['src']} bf16 sustained (MEASURED_PEAKS.json)"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tpath):
@@ -442,13 +460,16 @@ def main():
             traffic = json.load(open(tpath)).get(args.config)
         except Exception:
             traffic = None
-    roof = {"bound": "tensor", "kernel": "expert grouped GEMMs (fwd GEMM1+ReLU, GEMM2; bwd dgrad x2, wgrad x2)",
-            "achieved": achieved, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
-            "frac": (achieved / pk["bf16_sustained"]) if achieved else None, "traffic": traffic,
-            "peak_src": f"{pk['src']} bf16 sustained (MEASURED_PEAKS.json)",
+    roof = {"bound": "hbm" if hbm_bound else "tensor",
+            "kernel": "expert grouped GEMMs (fwd GEMM1+ReLU, GEMM2; bwd dgrad x2, wgrad x2)",
+            "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "peak_src": psrc,
             "gemm_ms_per_step": gemm_ms_per_step,
             "gemm_share_of_step": gemm_ms_per_step / (total_ms / args.steps) if total_ms > 0 else None,
-            "algorithmic_flops_per_step": flops_per_step_local}
+            "algorithmic_flops_per_step": flops_per_step_local,
+            "algorithmic_bytes_per_step": bytes_per_step_local,
+            "floors_ms": {"tensor": t_tensor_ms, "hbm": t_hbm_ms}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -45,7 +45,7 @@
  *     ce (copy engines) or nccl (ncclAlltoAll micro-ops).  LINA_TRACE=1 prints a
  *     per-phase device-time trace per rank at lina_comm_destroy.  LINA_PDL=0 turns
  *     off programmatic dependent launch; LINA_TILE_ROWS=128|256 forces the expert
- *     row-GEMM tile height (default: 128 when segments average < 192 rows).
+ *     row-GEMM tile height (default: 128 when segments average <= 96 rows).
  *   - The library never allocates caller-visible memory in forward/backward:
  *     scratch and saved state are caller-allocated, sized by
  *     lina_moe_workspace_size().

@@ -42,11 +42,14 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
   p.Cm = chunk_rows_max(p.C, p.n);
   p.bf16 = dsc.dtype == LINA_BF16;
   p.dt = p.bf16 ? 2 : 4;
-  // M tile of the expert row GEMMs: 256-row CTA pairs unless a segment (one source's
-  // rows of one expert) averages fewer rows than half a pair tile; LINA_TILE_ROWS=128|256
+  // M tile of the expert row GEMMs: 256-row CTA pairs (the pair splits the weight tile, so
+  // each weight slab is read once per segment up to 256 rows) unless a segment (one source's
+  // rows of one expert) averages <= 96 rows, where 128-row tiles halve the idle MMA rows and
+  // a segment still mostly fits one tile.  At ~128 rows (C4) the pairs measured 2% faster
+  // (profiles/r01_bench_c4_n1.json).  LINA_TILE_ROWS=128|256 overrides.
   {
     const long long per_seg = (long long)p.T * p.k / std::max(1, p.E);
-    p.tile_rows = per_seg < 192 ? 128 : 256;
+    p.tile_rows = per_seg <= 96 ? 128 : 256;
     const char* tr = getenv("LINA_TILE_ROWS");
     if (tr && (atoi(tr) == 128 || atoi(tr) == 256)) p.tile_rows = atoi(tr);
   }
