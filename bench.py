@@ -67,6 +67,23 @@ def peaks():
         return {"bf16_sustained": 1400.0, "bf16_burst": 1590.0, "hbm": 6650.0, "src": "fallback"}
 
 
+def gemm_floors(d, f, experts_local, kept, elt, pk):
+    """Floors of the six expert GEMMs of one step; the bound is the higher.
+
+    tensor: 12·d·f flop per kept assignment (fwd 4df, bwd 8df) at the sustained bf16 peak.
+    HBM: the algorithmic bytes of the six GEMMs as separate kernels at the measured copy
+    bandwidth — each local expert's W1 and W2 read twice (GEMM1/GEMM2, the two dgrads) and
+    dW1, dW2 written once (6·d·f elements per expert); per kept row 6·d + 6·f activation
+    elements (X, H, Y, dY, dH, dX in and out, and the wgrads' two operands each) and the
+    ReLU' bits written and read once (2·f/8 bytes).
+    """
+    flops = 12.0 * kept * d * f
+    nbytes = 6.0 * experts_local * d * f * elt + kept * (6.0 * (d + f) * elt + 2.0 * f / 8)
+    t_tensor = flops / (pk["bf16_sustained"] * 1e12) * 1e3
+    t_hbm = nbytes / (pk["hbm"] * 1e9) * 1e3
+    return {"flops": flops, "bytes": nbytes, "tensor_ms": t_tensor, "hbm_ms": t_hbm, "hbm_bound": t_hbm > t_tensor}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -430,23 +447,12 @@ def main():
                "h2d_bytes_per_step": 2 * T * d * elt, "d2h_bytes_per_step": 2 * T * d * elt,
                "copies": "pinned host <-> device on two copy streams, double-buffered, overlapping compute"}
 
-    # ---------------- roofline of the dominant kernel family (the six expert GEMMs).  Its
-    # bound is whichever floor is higher: tensor = 12·d·f flop per kept
-    # assignment at the sustained bf16 peak; HBM = the algorithmic bytes of the six GEMMs
-    # as separate kernels — the local experts' W1 and W2 read twice (GEMM1/GEMM2, the two
-    # dgrads) and dW1, dW2 written once (6·d·f elements per expert), per kept row 6·d + 6·f
-    # activation elements (X, H, Y, dY, dH, dX in and out, H / dH / X / dY again for the
-    # wgrads) and the ReLU' bits written and read once (2·f/8 bytes) — at the measured copy
-    # bandwidth.  C2 and C5 are tensor-bound; C4's ~128-row experts stream their weights
-    # and are HBM-bound.
+    # ---------------- roofline of the dominant kernel family (the six expert GEMMs)
     pk = peaks()
-    elt = 2 if tdt == torch.bfloat16 else 4
-    flops_per_step_local = 12.0 * kept_local * d * f          # fwd 4df + bwd 8df per kept assignment
-    bytes_per_step_local = (6.0 * (E // world) * d * f * elt + kept_local * (6.0 * (d + f) * elt + 2.0 * f / 8))
+    fl = gemm_floors(d, f, E // world, kept_local, 2 if tdt == torch.bfloat16 else 4, pk)
+    flops_per_step_local, bytes_per_step_local = fl["flops"], fl["bytes"]
+    t_tensor_ms, t_hbm_ms, hbm_bound = fl["tensor_ms"], fl["hbm_ms"], fl["hbm_bound"]
     gemm_ms_per_step = gemm_ms / max(args.steps, 1)
-    t_tensor_ms = flops_per_step_local / (pk["bf16_sustained"] * 1e12) * 1e3
-    t_hbm_ms = bytes_per_step_local / (pk["hbm"] * 1e9) * 1e3
-    hbm_bound = t_hbm_ms > t_tensor_ms
     if hbm_bound:
         achieved = bytes_per_step_local / (gemm_ms_per_step / 1e3) / 1e9 if gemm_ms > 0 else None
         peak, unit, psrc = pk["hbm"], "GB/s", f"{pk['src']} HBM copy bandwidth (MEASURED_PEAKS.json)"
