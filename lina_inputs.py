@@ -90,7 +90,7 @@ def grid(rng: np.random.Generator, shape, scale: float = 1.0) -> np.ndarray:
     return (k.astype(np.float64) / 64.0 * scale).astype(np.float32)
 
 
-TENSOR_IDS = {"X": 1, "Wg": 2, "W1": 3, "W2": 4, "dY": 5, "zipf": 6}
+TENSOR_IDS = {"X": 1, "Wg": 2, "W1": 3, "W2": 4, "dY": 5, "zipf": 6, "trace": 7}
 
 
 def gate_weight(cfg: LayerConfig, seed: int, family: str = "grid") -> np.ndarray:
@@ -175,3 +175,55 @@ def with_tokens(cfg: LayerConfig, tokens: int, **changes) -> LayerConfig:
     fields["tokens_per_rank"] = tokens
     fields.update(changes)
     return LayerConfig(**fields)
+
+
+# ----------------------------------------------------------------------------
+# Expert-selection traces (inputs of the popularity profiler / estimator, §8(f) row 2)
+# ----------------------------------------------------------------------------
+
+
+@dataclass
+class SelectionTrace:
+    """sel[t][i] = the k experts token t selected in MoE layer i (int32 [T, L, k]).
+
+    Generated by a first-order Markov model (SPEC.md's generator idea): each layer i >= 1
+    has a fixed random map ``maps[i-1]`` from the token's previous first expert to a
+    follow-on expert; with probability ``p`` the token's first expert follows the map,
+    else it is drawn from the layer's Zipf(zipf_s) marginal ``marginal`` (expert ids
+    permuted per layer).  The remaining k-1 experts are drawn from the same marginal
+    without replacement.  Layer 0 draws from its marginal.  The maps and marginals are
+    returned so tests can state the ground-truth next-layer distribution in closed form.
+    """
+    sel: np.ndarray
+    maps: np.ndarray       # [L-1, E] follow-on expert of layer i+1 given first expert a in layer i
+    marginal: np.ndarray   # [L, E]   Zipf marginal of each layer (permuted expert ids)
+    p: float
+
+
+def selection_trace(num_tokens: int, num_layers: int, num_experts: int, k: int, p: float,
+                    zipf_s: float, seed: int, stream: int = 0, maps=None, marginal=None) -> SelectionTrace:
+    """Seeded trace; pass ``maps``/``marginal`` of another trace to draw a fresh batch from
+    the same model (a profiling trace and an inference batch share the model)."""
+    T, L, E = num_tokens, num_layers, num_experts
+    if not (0.0 <= p <= 1.0) or not (1 <= k <= E):
+        raise ValueError("need 0 <= p <= 1 and 1 <= k <= E")
+    mrng = _rng(seed, TENSOR_IDS["trace"], 0)
+    if maps is None:
+        maps = np.stack([mrng.integers(0, E, size=E) for _ in range(max(L - 1, 0))]) \
+            if L > 1 else np.zeros((0, E), dtype=np.int64)
+    if marginal is None:
+        z = zipf_probs(E, zipf_s)
+        marginal = np.stack([z[np.argsort(mrng.permutation(E))] for _ in range(L)])
+    rng = _rng(seed, TENSOR_IDS["trace"], 1 + stream)
+    sel = np.empty((T, L, k), dtype=np.int32)
+    for i in range(L):
+        first = rng.choice(E, size=T, p=marginal[i])
+        if i > 0 and p > 0:
+            follow = rng.random(T) < p
+            first = np.where(follow, maps[i - 1][sel[:, i - 1, 0]], first)
+        sel[:, i, 0] = first
+        for t in range(T) if k > 1 else ():
+            w = marginal[i].copy()
+            w[first[t]] = 0.0
+            sel[t, i, 1:] = rng.choice(E, size=k - 1, replace=False, p=w / w.sum())
+    return SelectionTrace(sel, np.asarray(maps), np.asarray(marginal), p)

@@ -18,11 +18,15 @@ moe        : gating, capacity routing, expert FFN,
              combine (PAPER.md:172-173), backward.
 placement  : Eq. (1) replica counts, first-fit-decreasing packing and the
              per-replica token split.
+popularity : sample-path profiles Ψ, phase-one popularity estimation and the
+             phase-two top-2k check.
 
 Parity pins (tests/test_oracle_*.py): every function here is pinned by at
 least one check that does not re-type its formula — integer arithmetic for the
 logits, closed forms for softmax/gates, brute force for top-k and capacity,
 identity/dense special cases for the FFN and combine, central finite
-differences for the backward, hand-evaluated Eq. (1) cases for placement.
+differences for the backward, hand-evaluated Eq. (1) cases for placement,
+the generator's closed-form transition rows and hand-evaluated estimates for
+popularity (tests/test_popularity.py).
 No function is "parity unpinned".
 """
