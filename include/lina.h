@@ -19,7 +19,7 @@
  *   and in inference replicates popular experts by Eq. (1) with first-fit-
  *   decreasing packing (§5.2) and an unequal-split all-to-all.
  *   Readings where the paper is silent (capacity, drop order, gate
- *   normalisation, tie-breaks, rounding points) are R1-R16 in DESIGN.md §3.
+ *   normalisation, tie-breaks, rounding points, sample paths) are R1-R22 in DESIGN.md §3.
  *
  * Conventions for every entry point:
  *   - Every function returns lina_status; nothing throws across the ABI.  On a
@@ -161,6 +161,51 @@ lina_status lina_placement_compute(const double* host_popularity, int32_t num_ex
  * (q + source_rank) mod r_e).  host_out[r_e]. */
 lina_status lina_replica_split(int32_t count, int32_t replicas, int32_t source_rank,
                                int32_t* host_out);
+
+/* ------------------------------------------------------------------------ */
+/* Popularity estimation and two-phase scheduling (§5.2;  */
+/* paper D4: per-layer popularity distributions kept in host DRAM).    */
+/* Pure host functions, no device needed.  Readings R19-R22:   */
+/*  - a sample path of length l ending at layer i = the token's selected      */
+/*    expert SETS at layers i-l+1..i (l >= 1);                                */
+/*  - Psi_j^{m}(e) = tokens of path j selecting e in layer m / (k * |j|);     */
+/*  - an unseen path backs off to its suffixes l-1..1, then layer m's         */
+/*    marginal;                                                               */
+/*  - top-k ties go to the lower expert id.                                   */
+/* Layers are 0-indexed.                                                      */
+/* ------------------------------------------------------------------------ */
+typedef struct lina_pop_profile lina_pop_profile;
+
+/* An empty profile.  num_layers >= 2, num_experts >= 1, 1 <= k <= num_experts,
+ * 1 <= path_len < num_layers.  Errors: INVALID_ARGUMENT (all violations listed). */
+lina_status lina_popprof_create(int32_t num_layers, int32_t num_experts, int32_t k, int32_t path_len,
+                                lina_pop_profile** out);
+/* Frees the profile.  NULL is a no-op. */
+lina_status lina_popprof_destroy(lina_pop_profile* prof);
+/* "collect the expert selection results of all tokens" and group them by
+ * sample path: host_sel [num_tokens][num_layers][k] int32 expert ids
+ * (host memory, read only during the call).  Counts accumulate over calls.
+ * Errors: INVALID_ARGUMENT (NULL, num_tokens < 0, an id outside [0, E), or a token
+ * selecting one expert twice in a layer); the profile is unchanged on error. */
+lina_status lina_popprof_add(lina_pop_profile* prof, const int32_t* host_sel, int64_t num_tokens);
+/* Phase-one estimate of layer `layer`'s expert popularity for a batch, before any of
+ * its computation: each token t takes the top-k experts of its path's
+ * Psi and contributes their probabilities P_j(e); host_popularity[e] =
+ * (sum_t P_{j(t)}(e)) / num_tokens in fp64, summed in token order (Eq. (1)'s overall
+ * popularity).  host_history [num_tokens][path_len][k] = each token's
+ * selections at layers layer-path_len .. layer-1.  host_topk [num_tokens][k] (may be
+ * NULL) receives each token's chosen experts, -1 for a token with no distribution.
+ * A batch with num_tokens == 0 yields all zeros.  Errors: INVALID_ARGUMENT (layer <
+ * path_len or >= num_layers, bad ids, NULL). */
+lina_status lina_popprof_estimate(const lina_pop_profile* prof, int32_t layer, const int32_t* host_history,
+                                  int64_t num_tokens, double* host_popularity, int32_t* host_topk);
+/* Phase two: *host_identical = 1 when the top-2k experts of the
+ * estimate (host_estimated [E]) and of the actual selection counts
+ * (host_actual_counts [E], e.g. the allgathered gate histogram) are the same set
+ * (ranking by value desc, id asc; 2k capped at E), else 0 — then the caller re-plans
+ * with lina_placement_compute on the actual popularity.  Errors: INVALID_ARGUMENT. */
+lina_status lina_phase_two_check(const double* host_estimated, const int32_t* host_actual_counts,
+                                 int32_t num_experts, int32_t k, int32_t* host_identical);
 
 /* ------------------------------------------------------------------------ */
 /* MoE layer                                                                 */

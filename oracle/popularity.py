@@ -15,17 +15,17 @@ PAPER.md §5.2 (A17, A20, D4):
   fine-tuning is needed ... Otherwise, the scheduler re-computes the resource
   allocation with the actual expert popularity".
 
-Readings (R17-R20):
-  R17 a sample path of length l ending at layer i is the tuple of the token's selected
+Readings (R19-R22):
+  R19 a sample path of length l ending at layer i is the tuple of the token's selected
       expert SETS (sorted ascending) at layers i-l+1 .. i (l >= 1 layers); estimation of
       layer m needs the m >= l layers before it ("starting from the l-th layer").
-  R18 Ψ_j^{m}(e) = (tokens of group j that selected e in layer m) / (k · |group j|), a
+  R20 Ψ_j^{m}(e) = (tokens of group j that selected e in layer m) / (k · |group j|), a
       distribution over experts summing to 1.  A path never seen in profiling backs off to
       its suffixes of length l-1, ..., 1, then to layer m's marginal; a token with none of
       these contributes nothing.
-  R19 top-k of Ψ by (count desc, expert id asc); P_j(e) = Ψ_j(e) for those k experts,
+  R21 top-k of Ψ by (count desc, expert id asc); P_j(e) = Ψ_j(e) for those k experts,
       0 otherwise; popularity(e) = (Σ_t P_{j(t)}(e) in token order) / N_t in fp64.
-  R20 top-2k lists are compared as sets; ranking by (value desc, expert id asc) over
+  R22 top-2k lists are compared as sets; ranking by (value desc, expert id asc) over
       all E experts (estimated popularity for phase one, actual selection counts for
       phase two).
 Layers are 0-indexed here.
@@ -34,7 +34,7 @@ from __future__ import annotations
 
 
 def path_element(sel_t_layer) -> tuple:
-    """The experts one token selected in one layer, as a sorted tuple (R17)."""
+    """The experts one token selected in one layer, as a sorted tuple (R19)."""
     return tuple(sorted(int(e) for e in sel_t_layer))
 
 
@@ -44,7 +44,7 @@ class Profile:
 
     def __init__(self, num_layers: int, num_experts: int, k: int, path_len: int):
         if path_len < 1:
-            raise ValueError("path length l >= 1 (R17)")
+            raise ValueError("path length l >= 1 (R19)")
         self.L, self.E, self.k, self.l = num_layers, num_experts, k, path_len
         self.psi: dict = {}
         self.marg: dict = {}
@@ -64,7 +64,7 @@ class Profile:
                         c[e] += 1
 
     def distribution(self, m: int, history) -> list | None:
-        """Counts of Ψ for a token whose selections at layers m-l..m-1 are `history` (R18)."""
+        """Counts of Ψ for a token whose selections at layers m-l..m-1 are `history` (R20)."""
         elems = [path_element(h) for h in history]
         for s in range(self.l, 0, -1):
             key = (m, s, tuple(elems[len(elems) - s:]))
@@ -74,7 +74,7 @@ class Profile:
 
 
 def top_k(counts, k: int) -> list:
-    """The k experts with the largest counts, ties to the lower id (R19)."""
+    """The k experts with the largest counts, ties to the lower id (R21)."""
     return sorted(range(len(counts)), key=lambda e: (-counts[e], e))[:k]
 
 
@@ -84,7 +84,7 @@ def estimate(profile: Profile, m: int, histories):
     histories[t] = token t's selections at layers m-l .. m-1.  Returns (popularity[E],
     per-token top-k lists; [] for a token with no distribution)."""
     if m < profile.l:
-        raise ValueError(f"layer {m} < path length {profile.l}: no sample path yet (R17)")
+        raise ValueError(f"layer {m} < path length {profile.l}: no sample path yet (R19)")
     E, k = profile.E, profile.k
     acc = [0.0] * E
     picks = []
@@ -103,7 +103,7 @@ def estimate(profile: Profile, m: int, histories):
 
 
 def top2k_set(values, k: int) -> frozenset:
-    """'the overall top-2k experts', ranked by (value desc, id asc) (R20)."""
+    """'the overall top-2k experts', ranked by (value desc, id asc) (R22)."""
     return frozenset(sorted(range(len(values)), key=lambda e: (-values[e], e))[:2 * k])
 
 

@@ -302,6 +302,78 @@ lina_status lina_replica_split(int32_t count, int32_t replicas, int32_t source_r
   });
 }
 
+lina_status lina_popprof_create(int32_t L, int32_t E, int32_t k, int32_t l, lina_pop_profile** out) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    need(v, out, "out");
+    if (L < 2) v.push_back("num_layers < 2");
+    if (E < 1) v.push_back("num_experts < 1");
+    if (k < 1 || k > E) v.push_back("k outside [1, num_experts]");
+    if (l < 1 || l >= L) v.push_back("path_len outside [1, num_layers)");
+    raise_if(v, "lina_popprof_create");
+    *out = popprof_create(L, E, k, l);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_popprof_destroy(lina_pop_profile* prof) {
+  delete prof;
+  return LINA_OK;
+}
+
+lina_status lina_popprof_add(lina_pop_profile* prof, const int32_t* sel, int64_t T) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    need(v, prof, "prof");
+    if (T < 0) v.push_back("num_tokens < 0");
+    if (T > 0) need(v, sel, "host_sel");
+    if (prof && sel && T > 0) {
+      const std::string bad = popprof_check_ids(prof, sel, T, prof->L);
+      if (!bad.empty()) v.push_back(bad);
+    }
+    raise_if(v, "lina_popprof_add");
+    popprof_add(prof, sel, T);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_popprof_estimate(const lina_pop_profile* prof, int32_t layer, const int32_t* hist,
+                                  int64_t T, double* pop, int32_t* topk) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    need(v, prof, "prof");
+    need(v, pop, "host_popularity");
+    if (T < 0) v.push_back("num_tokens < 0");
+    if (T > 0) need(v, hist, "host_history");
+    if (prof) {
+      if (layer < prof->l) v.push_back("layer < path_len (no sample path yet)");
+      if (layer >= prof->L) v.push_back("layer >= num_layers");
+      if (hist && T > 0) {
+        const std::string bad = popprof_check_ids(prof, hist, T, prof->l);
+        if (!bad.empty()) v.push_back(bad);
+      }
+    }
+    raise_if(v, "lina_popprof_estimate");
+    popprof_estimate(prof, layer, hist, T, pop, topk);
+    return LINA_OK;
+  });
+}
+
+lina_status lina_phase_two_check(const double* est, const int32_t* actual, int32_t E, int32_t k,
+                                 int32_t* identical) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    need(v, est, "host_estimated");
+    need(v, actual, "host_actual_counts");
+    need(v, identical, "host_identical");
+    if (E < 1) v.push_back("num_experts < 1");
+    if (k < 1) v.push_back("k < 1");
+    raise_if(v, "lina_phase_two_check");
+    *identical = phase_two_identical(est, actual, E, k) ? 1 : 0;
+    return LINA_OK;
+  });
+}
+
 lina_status lina_moe_workspace_size(const lina_comm* cm, const lina_moe_desc* desc,
                                     size_t* workspace_bytes, size_t* saved_bytes) {
   return guarded([&] {

@@ -3,6 +3,19 @@
 #include "internal.h"
 #include "kernels.h"
 
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+// Sample-path popularity profile (popularity.cpp; paper D4: host DRAM).
+struct lina_pop_profile {
+  int L = 0, E = 0, k = 0, l = 0;
+  // maps[m * (l + 1) + s] for 1 <= s <= min(l, m): packed path (s sorted expert sets)
+  // -> per-expert selection counts in layer m
+  std::vector<std::unordered_map<std::string, std::vector<int64_t>>> maps;
+  std::vector<std::vector<int64_t>> marg;  // [L][E] layer marginals (backoff)
+};
+
 namespace lina {
 
 void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* gate_w,
@@ -34,5 +47,13 @@ void sched_stats(Scheduler* s, int64_t* issued, int64_t* deferred);
 lina_status placement_compute(const double* pop, int E, int N, int mpd, lina_placement* out,
                               std::string* err);
 void replica_split(int count, int replicas, int source_rank, int* out);
+
+// Popularity estimation / two-phase scheduling (popularity.cpp).
+lina_pop_profile* popprof_create(int L, int E, int k, int l);
+std::string popprof_check_ids(const lina_pop_profile* p, const int32_t* sel, int64_t rows, int layers);
+void popprof_add(lina_pop_profile* p, const int32_t* sel, int64_t T);
+void popprof_estimate(const lina_pop_profile* p, int m, const int32_t* hist, int64_t T, double* pop,
+                      int32_t* topk);
+bool phase_two_identical(const double* est, const int32_t* actual, int E, int k);
 
 }  // namespace lina

@@ -1,0 +1,171 @@
+// Popularity estimation and two-phase scheduling (§5.2).
+//
+// "We then group tokens that select the same experts from layer i-l to layer i, which
+// represent a unique sample path of experts used.  For each sample path j, we compute
+// the expert popularity distribution Ψ_j^{i+1} for layer i+1".  "For a
+// sample path j, we pick the top-k expert(s) of the subsequent layer from Ψ_j^{i+1}
+// and use their probabilities {P_j^{i+1}(e)}"; Eq. (1) aggregates
+// Σ_t P_{j(t)}(e) / N_t.  Phase two compares "the overall top-2k experts"
+// (P:482-484).  Profiles live in host DRAM as hash maps per layer (paper D4).
+// Readings R19-R22.
+//
+// Layout: per target layer m and path length s, one hash map keyed by the path's
+// packed expert sets (s·k int32, each set sorted ascending) -> per-expert counts.
+// Estimation is O(N_t · l) hash lookups plus one top-k per distinct path; counts are
+// integers, so the distribution chosen and the per-token P are exact functions of the trace.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "layer.h"
+
+namespace lina {
+
+namespace {
+
+// One token's selections in one layer as a sorted set, appended to a key (R19).
+void append_set(std::string* key, const int32_t* sel, int k) {
+  int32_t tmp[64];
+  std::vector<int32_t> big;
+  int32_t* v = tmp;
+  if (k > 64) {
+    big.resize(k);
+    v = big.data();
+  }
+  std::memcpy(v, sel, sizeof(int32_t) * k);
+  std::sort(v, v + k);
+  key->append(reinterpret_cast<const char*>(v), sizeof(int32_t) * k);
+}
+
+// k experts with the largest counts, ties to the lower id (R21).
+void top_k(const std::vector<int64_t>& c, int k, std::vector<int>* out) {
+  const int E = (int)c.size();
+  out->resize(E);
+  for (int e = 0; e < E; ++e) (*out)[e] = e;
+  std::partial_sort(out->begin(), out->begin() + k, out->end(), [&](int a, int b) {
+    return c[a] != c[b] ? c[a] > c[b] : a < b;
+  });
+  out->resize(k);
+}
+
+}  // namespace
+
+std::string popprof_check_ids(const lina_pop_profile* p, const int32_t* sel, int64_t rows, int layers) {
+  for (int64_t t = 0; t < rows; ++t)
+    for (int i = 0; i < layers; ++i) {
+      const int32_t* s = sel + (t * layers + i) * p->k;
+      for (int q = 0; q < p->k; ++q) {
+        if (s[q] < 0 || s[q] >= p->E)
+          return "token " + std::to_string(t) + " layer slot " + std::to_string(i) + ": expert id " +
+                 std::to_string(s[q]) + " outside [0, " + std::to_string(p->E) + ")";
+        for (int r = 0; r < q; ++r)
+          if (s[r] == s[q])
+            return "token " + std::to_string(t) + " layer slot " + std::to_string(i) +
+                   " selects expert " + std::to_string(s[q]) + " twice";
+      }
+    }
+  return "";
+}
+
+lina_pop_profile* popprof_create(int L, int E, int k, int l) {
+  auto* p = new lina_pop_profile;
+  p->L = L;
+  p->E = E;
+  p->k = k;
+  p->l = l;
+  p->maps.resize((size_t)L * (l + 1));
+  p->marg.assign(L, std::vector<int64_t>(E, 0));
+  return p;
+}
+
+void popprof_add(lina_pop_profile* p, const int32_t* sel, int64_t T) {
+  const int L = p->L, k = p->k, l = p->l;
+  std::string key;
+  for (int64_t t = 0; t < T; ++t) {
+    const int32_t* st = sel + t * (int64_t)L * k;
+    for (int m = 0; m < L; ++m) {
+      const int32_t* next = st + (int64_t)m * k;
+      for (int q = 0; q < k; ++q) p->marg[m][next[q]] += 1;
+      for (int s = 1; s <= std::min(l, m); ++s) {
+        key.clear();
+        for (int i = m - s; i < m; ++i) append_set(&key, st + (int64_t)i * k, k);
+        auto& c = p->maps[(size_t)m * (l + 1) + s][key];
+        if (c.empty()) c.assign(p->E, 0);
+        for (int q = 0; q < k; ++q) c[next[q]] += 1;
+      }
+    }
+  }
+}
+
+// The counts Ψ is read from for one token's history (R20): the longest seen suffix,
+// else the layer marginal; nullptr when neither has any selection.
+static const std::vector<int64_t>* distribution(const lina_pop_profile* p, int m, const int32_t* hist,
+                                                std::string* key) {
+  const int k = p->k, l = p->l;
+  for (int s = l; s >= 1; --s) {
+    key->clear();
+    for (int i = l - s; i < l; ++i) append_set(key, hist + (int64_t)i * k, k);
+    const auto& mp = p->maps[(size_t)m * (l + 1) + s];
+    auto it = mp.find(*key);
+    if (it != mp.end()) return &it->second;
+  }
+  const auto& mg = p->marg[m];
+  for (int64_t c : mg)
+    if (c) return &mg;
+  return nullptr;
+}
+
+void popprof_estimate(const lina_pop_profile* p, int m, const int32_t* hist, int64_t T, double* pop,
+                      int32_t* topk) {
+  const int E = p->E, k = p->k, l = p->l;
+  std::vector<double> acc(E, 0.0);
+  // Tokens sharing a path share its top-k and P: computed once per distribution per call.
+  std::unordered_map<const std::vector<int64_t>*, size_t> memo;
+  std::vector<int> picks;     // [entries][k]
+  std::vector<double> probs;  // [entries][k]
+  std::vector<int> chosen;
+  std::string key;
+  for (int64_t t = 0; t < T; ++t) {
+    const std::vector<int64_t>* c = distribution(p, m, hist + t * (int64_t)l * k, &key);
+    if (!c) {
+      if (topk)
+        for (int q = 0; q < k; ++q) topk[t * k + q] = -1;
+      continue;
+    }
+    auto it = memo.find(c);
+    if (it == memo.end()) {
+      int64_t total = 0;
+      for (int64_t x : *c) total += x;
+      top_k(*c, k, &chosen);
+      it = memo.emplace(c, picks.size() / k).first;
+      for (int q = 0; q < k; ++q) {
+        picks.push_back(chosen[q]);
+        probs.push_back((double)(*c)[chosen[q]] / (double)total);  // P_j(e) = Ψ_j(e)
+      }
+    }
+    const size_t base = it->second * k;
+    for (int q = 0; q < k; ++q) {
+      acc[picks[base + q]] += probs[base + q];  // token order, as Σ_t in Eq. (1)
+      if (topk) topk[t * k + q] = picks[base + q];
+    }
+  }
+  for (int e = 0; e < E; ++e) pop[e] = T ? acc[e] / (double)T : 0.0;
+}
+
+bool phase_two_identical(const double* est, const int32_t* actual, int E, int k) {
+  const int n = std::min(E, 2 * k);
+  std::vector<int> a(E), b(E);
+  for (int e = 0; e < E; ++e) a[e] = b[e] = e;
+  std::partial_sort(a.begin(), a.begin() + n, a.end(),
+                    [&](int x, int y) { return est[x] != est[y] ? est[x] > est[y] : x < y; });
+  std::partial_sort(b.begin(), b.begin() + n, b.end(),
+                    [&](int x, int y) { return actual[x] != actual[y] ? actual[x] > actual[y] : x < y; });
+  std::sort(a.begin(), a.begin() + n);
+  std::sort(b.begin(), b.begin() + n);
+  return std::equal(a.begin(), a.begin() + n, b.begin());
+}
+
+}  // namespace lina

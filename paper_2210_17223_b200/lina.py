@@ -30,6 +30,8 @@ ABI_SYMBOLS = [
     "lina_moe_workspace_size", "lina_moe_forward", "lina_moe_backward", "lina_moe_infer_forward",
     "lina_moe_infer_workspace_size", "lina_sched_config", "lina_allreduce_submit",
     "lina_allreduce_wait", "lina_sched_stats", "lina_profile_enable", "lina_profile_read",
+    "lina_popprof_create", "lina_popprof_destroy", "lina_popprof_add", "lina_popprof_estimate",
+    "lina_phase_two_check",
 ]
 
 
@@ -87,6 +89,11 @@ def load() -> ctypes.CDLL:
         "lina_comm_info": ([vp, P(ctypes.c_int), P(ctypes.c_int)], i32),
         "lina_placement_compute": ([P(ctypes.c_double), i32, i32, i32, P(Placement)], i32),
         "lina_replica_split": ([i32, i32, i32, P(i32)], i32),
+        "lina_popprof_create": ([i32, i32, i32, i32, P(vp)], i32),
+        "lina_popprof_destroy": ([vp], i32),
+        "lina_popprof_add": ([vp, P(i32), ctypes.c_int64], i32),
+        "lina_popprof_estimate": ([vp, i32, P(i32), ctypes.c_int64, P(ctypes.c_double), P(i32)], i32),
+        "lina_phase_two_check": ([P(ctypes.c_double), P(i32), i32, i32, P(i32)], i32),
         "lina_moe_workspace_size": ([vp, P(MoEDesc), P(sz), P(sz)], i32),
         "lina_moe_forward": ([vp, P(MoEDesc), vp, vp, vp, vp, vp, vp, vp, sz, P(Route), vp], i32),
         "lina_moe_backward": ([vp, P(MoEDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
@@ -267,6 +274,61 @@ def lina_replica_split(count: int, replicas: int, source_rank: int) -> list:
     out = (ctypes.c_int32 * replicas)()
     _check(load().lina_replica_split(count, replicas, source_rank, out))
     return list(out)
+
+
+class PopProfile:
+    """Sample-path popularity profile (lina_popprof_*; §5.2).
+
+    Host-only: arrays are numpy int32 ([T, L, k] traces, [T, l, k] histories)."""
+
+    def __init__(self, num_layers: int, num_experts: int, k: int, path_len: int):
+        import numpy as np  # noqa: F401  (callers pass numpy arrays)
+        h = ctypes.c_void_p()
+        _check(load().lina_popprof_create(num_layers, num_experts, k, path_len, ctypes.byref(h)))
+        self._h, self.L, self.E, self.k, self.l = h, num_layers, num_experts, k, path_len
+
+    def close(self):
+        if self._h:
+            load().lina_popprof_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _i32(a, shape_tail):
+        import numpy as np
+        a = np.ascontiguousarray(a, dtype=np.int32)
+        if a.ndim != 3 or tuple(a.shape[1:]) != shape_tail:
+            raise ValueError(f"expected [T, {shape_tail[0]}, {shape_tail[1]}] int32, got {a.shape}")
+        return a
+
+    def add(self, sel):
+        a = self._i32(sel, (self.L, self.k))
+        _check(load().lina_popprof_add(self._h, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), a.shape[0]))
+
+    def estimate(self, layer: int, history):
+        """Phase-one popularity of `layer` (list of E floats) and each token's top-k ([T, k], -1 = none)."""
+        import numpy as np
+        a = self._i32(history, (self.l, self.k))
+        pop = (ctypes.c_double * self.E)()
+        topk = np.empty((a.shape[0], self.k), dtype=np.int32)
+        _check(load().lina_popprof_estimate(self._h, layer, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                            a.shape[0], pop, topk.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
+        return list(pop), topk
+
+
+def lina_phase_two_check(estimated, actual_counts, k: int) -> bool:
+    """True when the estimated and actual top-2k expert sets are identical."""
+    E = len(estimated)
+    est = (ctypes.c_double * E)(*[float(x) for x in estimated])
+    act = (ctypes.c_int32 * E)(*[int(x) for x in actual_counts])
+    out = ctypes.c_int32()
+    _check(load().lina_phase_two_check(est, act, E, k, ctypes.byref(out)))
+    return bool(out.value)
 
 
 def lina_moe_infer_forward(comm: Comm, desc: MoEDesc, tokens, gate_w, w1_all, w2_all, out, workspace,

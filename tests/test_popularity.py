@@ -82,7 +82,7 @@ def test_hand_evaluated_two_token_estimate():
 
 
 def test_backoff_to_suffix_then_marginal():
-    """R18: an unseen length-2 path uses its seen length-1 suffix; a token whose last
+    """R20: an unseen length-2 path uses its seen length-1 suffix; a token whose last
     expert was never seen before layer m uses layer m's marginal."""
     E = 4
     sel = np.array([[[0], [1], [2]], [[1], [1], [3]], [[2], [2], [0]]], dtype=np.int32)
@@ -122,7 +122,7 @@ def test_profile_brute_force_regrouping():
 
 
 def test_k2_distribution_sums_to_one_and_popularity_bounded():
-    """With top-2 gating Ψ sums to 1 (R18) and each token contributes at most 1 in total,
+    """With top-2 gating Ψ sums to 1 (R20) and each token contributes at most 1 in total,
     so Σ_e popularity(e) <= 1 and N·popularity gives at most N devices (Eq. (1))."""
     tr = li.selection_trace(3000, 4, 8, 2, 0.6, 1.2, seed=4)
     pf = _profile(tr, 2)
@@ -141,9 +141,80 @@ def test_layer_too_early_rejected():
 
 def test_phase_two_set_comparison():
     """identical top-2k lists -> no fine-tuning; order inside the list does not
-    matter (R20); ties at rank 2k resolve to the lower expert id, deterministically."""
+    matter (R22); ties at rank 2k resolve to the lower expert id, deterministically."""
     k = 1
     assert pop.phase_two([0.5, 0.3, 0.1, 0.1], [10, 40, 0, 0], k)      # {0,1} vs {1,0}
     assert not pop.phase_two([0.5, 0.3, 0.1, 0.1], [10, 0, 40, 0], k)  # {0,1} vs {2,0}
     assert pop.top2k_set([0, 5, 5, 5], k) == frozenset({1, 2})           # tie at rank 2 -> id 2 < 3
     assert pop.top2k_set([0.25] * 4, 2) == frozenset({0, 1, 2, 3})
+
+
+# ---------------------------------------------------------------------------------------
+# The native implementation (liblina.so host functions, no GPU) against the oracle:
+# bit-exact popularity (same fp64 operations in token order), identical top-k picks.
+# ---------------------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def lina():
+    import paper_2210_17223_b200 as pkg
+    return pkg
+
+
+@pytest.mark.parametrize("k,l,p,s", [(1, 1, 0.6, 1.0), (1, 3, 0.6, 1.2), (2, 2, 0.4, 0.8), (2, 3, 1.0, 0.0)])
+def test_native_estimate_bit_exact(lina, k, l, p, s):
+    E, L = 16, 6
+    tr = li.selection_trace(3000, L, E, k, p, s, seed=21)
+    pf = _profile(tr, l)
+    nat = lina.PopProfile(L, E, k, l)
+    nat.add(tr.sel[:1000])
+    nat.add(tr.sel[1000:])                     # counts accumulate over calls
+    fresh = li.selection_trace(700, L, E, k, p, s, seed=21, stream=5, maps=tr.maps, marginal=tr.marginal)
+    for m in range(l, L):
+        hist = fresh.sel[:, m - l:m, :]
+        want, picks = pop.estimate(pf, m, hist)
+        got, topk = nat.estimate(m, hist)
+        assert got == want                      # bit-exact
+        assert [list(r) for r in topk] == [list(q) if q else [-1] * k for q in picks]
+
+
+def test_native_unseen_paths_and_empty_batch(lina):
+    E = 4
+    sel = np.array([[[0], [1], [2]], [[1], [1], [3]], [[2], [2], [0]]], dtype=np.int32)
+    nat = lina.PopProfile(3, E, 1, 2)
+    nat.add(sel)
+    got, topk = nat.estimate(2, np.array([[[3], [1]], [[0], [0]]], dtype=np.int32))
+    pf = pop.Profile(3, E, 1, 2)
+    pf.add_trace(sel)
+    want, _ = pop.estimate(pf, 2, [[[3], [1]], [[0], [0]]])
+    assert got == want
+    got0, _ = nat.estimate(2, np.zeros((0, 2, 1), dtype=np.int32))
+    assert got0 == [0.0] * E
+    empty = lina.PopProfile(3, E, 1, 2)           # nothing profiled: no distribution at all
+    g, t = empty.estimate(2, np.array([[[0], [1]]], dtype=np.int32))
+    assert g == [0.0] * E and t.tolist() == [[-1]]
+
+
+def test_native_rejects_bad_arguments(lina):
+    with pytest.raises(lina.LinaError) as ei:
+        lina.PopProfile(1, 4, 5, 0)
+    msg = str(ei.value)
+    assert "num_layers" in msg and "k outside" in msg and "path_len" in msg
+    nat = lina.PopProfile(3, 4, 1, 2)
+    with pytest.raises(lina.LinaError):
+        nat.add(np.array([[[0], [4], [1]]], dtype=np.int32))          # id outside [0, E)
+    with pytest.raises(lina.LinaError):
+        nat.estimate(1, np.zeros((1, 2, 1), dtype=np.int32))           # layer < path_len
+    nat2 = lina.PopProfile(3, 4, 2, 1)
+    with pytest.raises(lina.LinaError):
+        nat2.add(np.array([[[0, 0], [1, 2], [1, 3]]], dtype=np.int32))  # expert twice in a layer
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_native_phase_two_matches_oracle(lina, seed):
+    rng = np.random.default_rng(seed)
+    E, k = 16, 1 + seed % 3
+    for _ in range(50):
+        est = rng.integers(0, 5, size=E) / 8.0           # many ties
+        act = rng.integers(0, 6, size=E)
+        assert lina.lina_phase_two_check(est, act, k) == pop.phase_two(list(est), list(act), k)
+    assert lina.lina_phase_two_check([0.25] * 4, [1, 2, 3, 4], 2)   # 2k >= E: both lists are all experts
