@@ -277,6 +277,23 @@ lina_status lina_moe_infer_forward(lina_comm* comm, const lina_moe_desc* desc, c
                                    void* out, const lina_placement* placement,
                                    int32_t max_per_device, lina_placement* plan_out,
                                    void* workspace, size_t workspace_bytes, lina_stream stream);
+/* Two-phase scheduling: as lina_moe_infer_forward with the phase-one
+ * `placement` (built before gating from host_estimated [E], e.g. by
+ * lina_popprof_estimate + lina_placement_compute), then, once the gate's global
+ * per-expert counts are known, the phase-two check of lina_phase_two_check: the
+ * top-2k experts of host_estimated and of the actual counts are compared as sets
+ * and, if they differ, the plan is re-computed from the actual popularity ("following
+ * the same logic in phase 1") before any token moves.  *host_replanned (may be
+ * NULL) = 1 when phase two re-planned, else 0.  Identical on every rank (the counts
+ * are allgathered).  Errors: as lina_moe_infer_forward, plus INVALID_ARGUMENT for a
+ * NULL placement or host_estimated. */
+lina_status lina_moe_infer_forward_two_phase(lina_comm* comm, const lina_moe_desc* desc,
+                                             const void* tokens, const float* gate_w,
+                                             const void* w1_all, const void* w2_all, void* out,
+                                             const lina_placement* placement,
+                                             const double* host_estimated, lina_placement* plan_out,
+                                             int32_t* host_replanned, void* workspace,
+                                             size_t workspace_bytes, lina_stream stream);
 /* Workspace for lina_moe_infer_forward with at most max_per_device hosted experts per
  * device (sized for the worst case: all of a source's tokens routed to one replica). */
 lina_status lina_moe_infer_workspace_size(const lina_comm* comm, const lina_moe_desc* desc,

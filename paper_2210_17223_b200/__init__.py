@@ -8,7 +8,8 @@ fallback.
 from . import lina  # noqa: F401
 from .lina import (ABI_SYMBOLS, Comm, LinaError, MoELayer, PopProfile, lina_allreduce_submit,  # noqa: F401
                    lina_allreduce_wait, lina_comm_init, lina_get_unique_id, lina_moe_backward,
-                   lina_moe_forward, lina_moe_infer_forward, lina_moe_infer_workspace_size,
+                   lina_moe_forward, lina_moe_infer_forward, lina_moe_infer_forward_two_phase,
+                   lina_moe_infer_workspace_size,
                    lina_moe_workspace_size, lina_placement_compute, lina_profile_enable,
                    lina_phase_two_check, lina_profile_read, lina_replica_split,
                    lina_sched_config, lina_sched_stats, lina_version, load, make_desc)

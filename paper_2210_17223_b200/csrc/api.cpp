@@ -53,7 +53,8 @@ void prof_end(lina_comm* cm, cudaStream_t s, int gemm_launches) {
 void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
                    const float* gate_w, const void* w1_all, const void* w2_all, void* out,
                    const lina_placement* placement, int mpd, lina_placement* plan_out, void* ws,
-                   size_t ws_bytes, cudaStream_t s);
+                   size_t ws_bytes, cudaStream_t s, const double* estimated = nullptr,
+                   int32_t* replanned = nullptr);
 size_t infer_workspace_bytes(const lina_moe_desc& desc, int world, int mpd);
 }  // namespace lina
 
@@ -463,11 +464,14 @@ lina_status lina_moe_infer_workspace_size(const lina_comm* cm, const lina_moe_de
   });
 }
 
-lina_status lina_moe_infer_forward(lina_comm* cm, const lina_moe_desc* desc, const void* tokens,
-                                   const float* gate_w, const void* w1_all, const void* w2_all,
-                                   void* out, const lina_placement* placement,
-                                   int32_t max_per_device, lina_placement* plan_out,
-                                   void* workspace, size_t workspace_bytes, lina_stream stream) {
+// Validation and dispatch shared by lina_moe_infer_forward and its two-phase variant
+// (estimated != NULL: phase-two check against the phase-one `placement`).
+static lina_status infer_entry(lina_comm* cm, const lina_moe_desc* desc, const void* tokens,
+                               const float* gate_w, const void* w1_all, const void* w2_all, void* out,
+                               const lina_placement* placement, int32_t max_per_device,
+                               lina_placement* plan_out, void* workspace, size_t workspace_bytes,
+                               lina_stream stream, const double* estimated, int32_t* replanned,
+                               const char* what) {
   return guarded([&] {
     if (!cm) throw ArgError{"comm is NULL"};
     validate_desc(desc, cm->world, false);
@@ -496,15 +500,48 @@ lina_status lina_moe_infer_forward(lina_comm* cm, const lina_moe_desc* desc, con
       need(v, plan_out->hosted, "plan_out->hosted");
       if (plan_out->max_replicas < cm->world) v.push_back("plan_out->max_replicas < world");
     }
-    raise_if(v, "lina_moe_infer_forward");
+    raise_if(v, what);
     const int mpd = placement ? placement->max_per_device : max_per_device;
     if (workspace_bytes < infer_workspace_bytes(*desc, cm->world, mpd))
       throw StatusError{LINA_ERR_WORKSPACE, "workspace_bytes < lina_moe_infer_workspace_size"};
     LINA_CUDA_CHECK(cudaSetDevice(cm->device));
     infer_forward(cm, *desc, tokens, gate_w, w1_all, w2_all, out, placement, max_per_device,
-                  plan_out, workspace, workspace_bytes, (cudaStream_t)stream);
+                  plan_out, workspace, workspace_bytes, (cudaStream_t)stream, estimated, replanned);
     return LINA_OK;
   });
+}
+
+lina_status lina_moe_infer_forward(lina_comm* cm, const lina_moe_desc* desc, const void* tokens,
+                                   const float* gate_w, const void* w1_all, const void* w2_all,
+                                   void* out, const lina_placement* placement,
+                                   int32_t max_per_device, lina_placement* plan_out,
+                                   void* workspace, size_t workspace_bytes, lina_stream stream) {
+  return infer_entry(cm, desc, tokens, gate_w, w1_all, w2_all, out, placement, max_per_device, plan_out,
+                     workspace, workspace_bytes, stream, nullptr, nullptr, "lina_moe_infer_forward");
+}
+
+lina_status lina_moe_infer_forward_two_phase(lina_comm* cm, const lina_moe_desc* desc,
+                                             const void* tokens, const float* gate_w,
+                                             const void* w1_all, const void* w2_all, void* out,
+                                             const lina_placement* placement,
+                                             const double* estimated, lina_placement* plan_out,
+                                             int32_t* replanned, void* workspace,
+                                             size_t workspace_bytes, lina_stream stream) {
+  if (!placement || !estimated) {
+    set_error(std::string("lina_moe_infer_forward_two_phase:") +
+              (placement ? "" : " placement (the phase-one plan) is NULL;") +
+              (estimated ? "" : " host_estimated is NULL;"));
+    return LINA_ERR_INVALID_ARGUMENT;
+  }
+  if (desc)
+    for (int e = 0; e < desc->num_experts; ++e)
+      if (!(estimated[e] >= 0.0)) {
+        set_error("lina_moe_infer_forward_two_phase: host_estimated[" + std::to_string(e) + "] < 0 or NaN");
+        return LINA_ERR_INVALID_ARGUMENT;
+      }
+  return infer_entry(cm, desc, tokens, gate_w, w1_all, w2_all, out, placement, placement->max_per_device,
+                     plan_out, workspace, workspace_bytes, stream, estimated, replanned,
+                     "lina_moe_infer_forward_two_phase");
 }
 
 lina_status lina_sched_config(lina_comm* cm, lina_policy policy, size_t partition_bytes) {

@@ -106,7 +106,8 @@ static int* pinned(lina_comm* cm, size_t ints) {
 
 void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens, const float* gate_w,
                    const void* w1_all, const void* w2_all, void* out, const lina_placement* placement,
-                   int mpd_arg, lina_placement* plan_out, void* ws, size_t ws_bytes, cudaStream_t s) {
+                   int mpd_arg, lina_placement* plan_out, void* ws, size_t ws_bytes, cudaStream_t s,
+                   const double* estimated, int32_t* replanned) {
   const int P = cm->world, rank = cm->rank;
   const int mpd = placement ? placement->max_per_device : mpd_arg;
   InferPlan q = infer_plan(desc, P, mpd);
@@ -184,9 +185,18 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   LINA_CUDA_CHECK(cudaStreamSynchronize(s));
   std::vector<int> cnt(host, host + (size_t)P * E);  // cnt[src*E + e]
 
-  // ---- the plan (identical on every rank)
+  // ---- the plan (identical on every rank).  Phase two: a phase-one plan
+  // whose estimated top-2k experts differ from the actual ones is re-computed below.
+  bool use_given = placement != nullptr;
+  if (placement && estimated) {
+    std::vector<int32_t> actual(E, 0);
+    for (int src = 0; src < P; ++src)
+      for (int e = 0; e < E; ++e) actual[e] += cnt[(size_t)src * E + e];
+    use_given = phase_two_identical(estimated, actual.data(), E, k);
+  }
+  if (replanned) *replanned = (placement && !use_given) ? 1 : 0;
   std::vector<int> r(E), rdev((size_t)E * P, -1), hosted((size_t)P * mpd, -1);
-  if (placement) {
+  if (use_given) {
     const int mr = placement->max_replicas;
     for (int e = 0; e < E; ++e) {
       r[e] = placement->replicas[e];

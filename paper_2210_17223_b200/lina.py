@@ -31,7 +31,7 @@ ABI_SYMBOLS = [
     "lina_moe_infer_workspace_size", "lina_sched_config", "lina_allreduce_submit",
     "lina_allreduce_wait", "lina_sched_stats", "lina_profile_enable", "lina_profile_read",
     "lina_popprof_create", "lina_popprof_destroy", "lina_popprof_add", "lina_popprof_estimate",
-    "lina_phase_two_check",
+    "lina_phase_two_check", "lina_moe_infer_forward_two_phase",
 ]
 
 
@@ -100,6 +100,8 @@ def load() -> ctypes.CDLL:
         "lina_moe_infer_forward": ([vp, P(MoEDesc), vp, vp, vp, vp, vp, P(Placement), i32, P(Placement),
                                     vp, sz, vp], i32),
         "lina_moe_infer_workspace_size": ([vp, P(MoEDesc), i32, P(sz)], i32),
+        "lina_moe_infer_forward_two_phase": ([vp, P(MoEDesc), vp, vp, vp, vp, vp, P(Placement),
+                                              P(ctypes.c_double), P(Placement), P(i32), vp, sz, vp], i32),
         "lina_sched_config": ([vp, i32, sz], i32),
         "lina_allreduce_submit": ([vp, vp, sz, i32, vp], i32),
         "lina_allreduce_wait": ([vp, vp], i32),
@@ -348,6 +350,25 @@ def lina_moe_infer_forward(comm: Comm, desc: MoEDesc, tokens, gate_w, w1_all, w2
                                          ctypes.byref(pl_out) if pl_out is not None else None,
                                          _ptr(workspace), ws_bytes, _stream(stream)))
     return placement_to_tables(pl_out) if pl_out is not None else None
+
+
+def lina_moe_infer_forward_two_phase(comm: Comm, desc: MoEDesc, tokens, gate_w, w1_all, w2_all, out,
+                                     workspace, placement: PlacementTables, estimated, stream=None):
+    """Phase-one `placement` (from `estimated`, [E] popularity) checked after gating.
+
+    Returns (plan used, replanned: bool).  The workspace must fit the placement's pitch."""
+    N = comm.world
+    mpd = max(len(h) for h in placement.hosted)
+    pl_in = tables_to_placement(placement, N, mpd)
+    pl_out = _alloc_placement(desc.num_experts, N, mpd)
+    est = (ctypes.c_double * desc.num_experts)(*[float(x) for x in estimated])
+    rep = ctypes.c_int32(-1)
+    ws_bytes = workspace.numel() * workspace.element_size()
+    _check(load().lina_moe_infer_forward_two_phase(comm.handle, ctypes.byref(desc), _ptr(tokens), _ptr(gate_w),
+                                                   _ptr(w1_all), _ptr(w2_all), _ptr(out), ctypes.byref(pl_in),
+                                                   est, ctypes.byref(pl_out), ctypes.byref(rep),
+                                                   _ptr(workspace), ws_bytes, _stream(stream)))
+    return placement_to_tables(pl_out), bool(rep.value)
 
 
 def lina_sched_config(comm: Comm, policy: int, partition_bytes: int):

@@ -110,3 +110,19 @@ def test_product_path_does_not_import_oracle():
             if f.endswith((".py", ".cpp", ".cu", ".h")):
                 src = open(os.path.join(dp, f), errors="ignore").read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_two_phase_rejects_missing_phase_one_inputs(lina):
+    """lina_moe_infer_forward_two_phase needs the phase-one plan and the estimate; the
+    check happens before any device work (no GPU needed)."""
+    import ctypes
+    lib = lina.load()
+    E = 4
+    est = (ctypes.c_double * E)(*([0.25] * E))
+    st = lib.lina_moe_infer_forward_two_phase(None, None, None, None, None, None, None, None, est,
+                                              None, None, None, 0, None)
+    assert st == 1 and b"placement" in lib.lina_last_error()
+    pl = lina.lina._alloc_placement(E, 1, E)
+    st = lib.lina_moe_infer_forward_two_phase(None, None, None, None, None, None, None, ctypes.byref(pl), None,
+                                              None, None, None, 0, None)
+    assert st == 1 and b"host_estimated" in lib.lina_last_error()

@@ -44,3 +44,37 @@ def test_infer_single_gpu_matches_oracle_and_static(family):
     if family == "grid":
         g = gpu_layer(cfg, 1, X, Wg, W1, W2, capacity=C)
         assert np.array_equal(g["y"], y)
+
+
+@pytest.mark.parametrize("estimate_matches", [True, False])
+def test_two_phase_keeps_or_replans(estimate_matches):
+    """Phase two: a phase-one plan whose estimated top-2k experts equal the
+    actual ones is used as given; otherwise the plan is re-computed from the actual
+    popularity (= the oracle's placement of the batch histogram).  Output is the oracle's
+    either way (the placement decides where experts run, not what they compute)."""
+    import paper_2210_17223_b200 as lina
+    from oracle import popularity as opop
+    cfg = li.with_tokens(li.CONFIGS["C4"], 512)
+    Wg, W1, W2 = li.layer_weights(cfg, 5, "zipf")
+    X, _ = li.layer_tokens(cfg, 5, 0, "zipf", zipf_s=1.0)
+    C = X.shape[0]
+    fw = moe.moe_forward([X], Wg, W1, W2, cfg.k, C, cfg.dtype)[0]
+    actual = fw.counts / fw.counts.sum()
+    est = list(actual) if estimate_matches else list(actual[::-1])
+    assert opop.phase_two(est, list(fw.counts), cfg.k) == estimate_matches
+    E = cfg.num_experts
+    given = oplace.place(est, 1, E)
+    tables = lina.lina.PlacementTables(given["replicas"], given["replica_device"], given["hosted"])
+    comm = lina.Comm(1, 0, 0)
+    dt = tdtype(cfg.dtype)
+    desc = lina.make_desc(C, cfg.d_model, cfg.d_ffn, E, cfg.k, C, 1, dt)
+    ws = torch.empty(lina.lina_moe_infer_workspace_size(comm, desc, E), dtype=torch.uint8, device="cuda")
+    out = torch.empty((C, cfg.d_model), dtype=dt, device="cuda")
+    plan, replanned = lina.lina_moe_infer_forward_two_phase(
+        comm, desc, to_dev(X, dt), to_dev(Wg, torch.float32), to_dev(W1, dt), to_dev(W2, dt), out, ws,
+        tables, est)
+    torch.cuda.synchronize()
+    assert replanned == (not estimate_matches)
+    ref = given if estimate_matches else oplace.place(list(actual), 1, E)
+    assert plan.replicas == ref["replicas"] and plan.hosted == ref["hosted"]
+    assert moe.normwise_error(out.float().cpu().numpy(), fw.y) <= TOL[cfg.dtype]
