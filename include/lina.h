@@ -89,7 +89,17 @@ typedef enum {
    * all-to-all micro-op is queued or in flight; launching stops
    * once the combine backward starts, "since this implies all-to-all is
    * imminent". */
-  LINA_SCHED_LINA = 1
+  LINA_SCHED_LINA = 1,
+  /* Ablation (fig:schedule_naive P:289): strict priority without
+   * partitioning — a ready gradient is issued WHOLE, and only while no all-to-all
+   * is queued or in flight (the LINA admission rule); once launched it cannot be
+   * preempted (R23). */
+  LINA_SCHED_NAIVE = 2,
+  /* Ablation: "blindly defer allreduce until an even number of
+   * all-to-all finish" — a ready gradient waits only for the backward all-to-all
+   * phase in flight (dispatch + combine, two all-to-alls) to complete, then is
+   * issued WHOLE, without regard to the next all-to-all (R23). */
+  LINA_SCHED_DEFER = 3
 } lina_policy;
 
 typedef void* lina_stream; /* cudaStream_t */

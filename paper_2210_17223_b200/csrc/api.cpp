@@ -547,8 +547,9 @@ lina_status lina_moe_infer_forward_two_phase(lina_comm* cm, const lina_moe_desc*
 lina_status lina_sched_config(lina_comm* cm, lina_policy policy, size_t partition_bytes) {
   return guarded([&] {
     if (!cm) throw ArgError{"comm is NULL"};
-    if (policy != LINA_SCHED_BASELINE && policy != LINA_SCHED_LINA)
-      throw ArgError{"policy not LINA_SCHED_BASELINE/LINA_SCHED_LINA"};
+    if (policy != LINA_SCHED_BASELINE && policy != LINA_SCHED_LINA && policy != LINA_SCHED_NAIVE &&
+        policy != LINA_SCHED_DEFER)
+      throw ArgError{"policy not LINA_SCHED_BASELINE/LINA/NAIVE/DEFER"};
     if (cm->sched) sched_config(cm->sched, policy, partition_bytes);
     return LINA_OK;
   });

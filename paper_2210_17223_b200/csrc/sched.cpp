@@ -20,7 +20,11 @@
 // blocks the device) for (a) gradient readiness and (b) completion of the
 // registered all-to-all phase, and issues ncclAllReduce micro-ops only when the
 // LINA admission rule holds.  BASELINE issues whole gradients immediately, gated
-// on readiness only on the device (fair-sharing the links).
+// on readiness only on the device (fair-sharing the links).  Two
+// ablations of the paper's design discussion: NAIVE = the LINA admission rule with
+// whole gradients (strict priority, no partitioning) and DEFER = whole
+// gradients issued once the backward all-to-all phase in flight has completed,
+// blind to the next one; reading R23.
 #include <chrono>
 
 #include "layer.h"
@@ -106,8 +110,8 @@ class Scheduler {
   }
 
  private:
-  // true while an all-to-all is queued or in flight (LINA admission rule)
-  bool a2a_busy_locked() {
+  // true while a registered all-to-all phase has not completed on the device
+  bool a2a_inflight_locked() {
     while (!a2a_events_.empty()) {
       cudaError_t q = cudaEventQuery(a2a_events_.front());
       if (q == cudaErrorNotReady) return true;
@@ -115,8 +119,10 @@ class Scheduler {
       a2a_events_.erase(a2a_events_.begin());
       if (a2a_events_.empty()) imminent_ = false;  // the a2a phase has drained
     }
-    return imminent_;
+    return false;
   }
+  // true while an all-to-all is queued or in flight (LINA / NAIVE admission rule)
+  bool a2a_busy_locked() { return a2a_inflight_locked() || imminent_; }
   void run() {
     std::unique_lock<std::mutex> g(mu_);
     while (true) {
@@ -126,11 +132,12 @@ class Scheduler {
         continue;
       }
       ArJob& j = jobs_.front();
-      const bool lina = policy_ == LINA_SCHED_LINA;
+      const bool gated = policy_ != LINA_SCHED_BASELINE;
+      const bool split = policy_ == LINA_SCHED_LINA;
       bool can_issue = true;
-      if (lina) {
+      if (gated) {
         if (cudaEventQuery(j.ready) == cudaErrorNotReady) can_issue = false;
-        else if (a2a_busy_locked()) {
+        else if (policy_ == LINA_SCHED_DEFER ? a2a_inflight_locked() : a2a_busy_locked()) {
           can_issue = false;
           ++deferred_;
         }
@@ -142,7 +149,7 @@ class Scheduler {
         continue;
       }
       size_t cnt = j.count - j.next;
-      if (lina) cnt = std::min(cnt, std::max<size_t>(1, partition_bytes_ / j.elt));
+      if (split) cnt = std::min(cnt, std::max<size_t>(1, partition_bytes_ / j.elt));
       try {
         if (j.next == 0) LINA_CUDA_CHECK(cudaStreamWaitEvent(cm_->lo, j.ready, 0));
         char* p = j.ptr + j.next * j.elt;

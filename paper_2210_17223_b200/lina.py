@@ -21,7 +21,7 @@ STATUS_NAMES = {0: "LINA_OK", 1: "LINA_ERR_INVALID_ARGUMENT", 2: "LINA_ERR_UNSUP
                 3: "LINA_ERR_INFEASIBLE_PLAN", 4: "LINA_ERR_CUDA", 5: "LINA_ERR_NCCL",
                 6: "LINA_ERR_WORKSPACE"}
 LINA_F32, LINA_BF16 = 0, 1
-LINA_SCHED_BASELINE, LINA_SCHED_LINA = 0, 1
+LINA_SCHED_BASELINE, LINA_SCHED_LINA, LINA_SCHED_NAIVE, LINA_SCHED_DEFER = 0, 1, 2, 3
 
 # Every symbol declared in include/lina.h (tests check the library exports all of them).
 ABI_SYMBOLS = [

@@ -39,7 +39,8 @@ def main():
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     import paper_2210_17223_b200 as lina
-    from paper_2210_17223_b200.lina import LINA_SCHED_BASELINE, LINA_SCHED_LINA
+    from paper_2210_17223_b200.lina import (LINA_SCHED_BASELINE, LINA_SCHED_DEFER, LINA_SCHED_LINA,
+                                             LINA_SCHED_NAIVE)
 
     cfg = li.with_tokens(li.CONFIGS[a.config], a.tokens)
     E, El = cfg.num_experts, cfg.num_experts // world
@@ -65,7 +66,8 @@ def main():
     stream = torch.cuda.current_stream()
     results = {}
     ok = True
-    for name, pol in (("BASELINE", LINA_SCHED_BASELINE), ("LINA", LINA_SCHED_LINA)):
+    for name, pol in (("BASELINE", LINA_SCHED_BASELINE), ("LINA", LINA_SCHED_LINA),
+                      ("NAIVE", LINA_SCHED_NAIVE), ("DEFER", LINA_SCHED_DEFER)):
         lina.lina_sched_config(comm, pol, int(a.partition_mb * 2 ** 20))
         times = []
         for rep in range(a.reps + 1):

@@ -30,13 +30,18 @@ def main():
     ap.add_argument("--partitions", default="4,16,30")
     ap.add_argument("--grad-mb", type=float, default=16.8)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--policies", default="BASELINE,LINA,NAIVE,DEFER",
+                    help="schedulers to compare (NAIVE / DEFER are the paper's ablations, R23)")
     a = ap.parse_args()
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     import paper_2210_17223_b200 as lina
-    from paper_2210_17223_b200.lina import LINA_SCHED_BASELINE, LINA_SCHED_LINA
+    from paper_2210_17223_b200.lina import (LINA_SCHED_BASELINE, LINA_SCHED_DEFER, LINA_SCHED_LINA,
+                                             LINA_SCHED_NAIVE)
+    policies = {"BASELINE": LINA_SCHED_BASELINE, "LINA": LINA_SCHED_LINA, "NAIVE": LINA_SCHED_NAIVE,
+                "DEFER": LINA_SCHED_DEFER}
 
     cfg = li.with_tokens(li.CONFIGS[a.config], a.tokens)
     E, El = cfg.num_experts, cfg.num_experts // world
@@ -90,7 +95,8 @@ def main():
             res = {"world": world, "config": cfg.name, "tokens_per_rank": cfg.tokens_per_rank, "n_chunks": n,
                    "partition_mb": part, "grads": f"4 x {a.grad_mb} MB fp32", "bwd_alone_ms": alone,
                    "transport": os.environ.get("LINA_TRANSPORT", "fused")}
-            for name, pol in (("BASELINE", LINA_SCHED_BASELINE), ("LINA", LINA_SCHED_LINA)):
+            for name in a.policies.split(","):
+                pol = policies[name]
                 lina.lina_sched_config(comm, pol, int(part * 2 ** 20))
                 bwd, done = run(layer, pol)
                 res[name] = {"bwd_ms": bwd, "bwd_slowdown": bwd / alone, "ar_done_ms": done}
