@@ -10,8 +10,11 @@
 // Sample-path popularity profile (popularity.cpp; paper D4: host DRAM).
 struct lina_pop_profile {
   int L = 0, E = 0, k = 0, l = 0;
-  // maps[m * (l + 1) + s] for 1 <= s <= min(l, m): packed path (s sorted expert sets)
-  // -> per-expert selection counts in layer m
+  int bits = 0;         // bits per expert id in a packed key
+  bool packed = false;  // l·k·bits <= 64: paths are uint64 keys, else byte strings
+  // [m * (l + 1) + s] for 1 <= s <= min(l, m): path (s sorted expert sets) -> per-expert
+  // selection counts in layer m
+  std::vector<std::unordered_map<uint64_t, std::vector<int64_t>>> maps64;
   std::vector<std::unordered_map<std::string, std::vector<int64_t>>> maps;
   std::vector<std::vector<int64_t>> marg;  // [L][E] layer marginals (backoff)
 };

@@ -9,8 +9,9 @@
 // (P:482-484).  Profiles live in host DRAM as hash maps per layer (paper D4).
 // Readings R19-R22.
 //
-// Layout: per target layer m and path length s, one hash map keyed by the path's
-// packed expert sets (s·k int32, each set sorted ascending) -> per-expert counts.
+// Layout: per target layer m and path length s, one hash map keyed by the path's expert
+// sets (each sorted ascending) -> per-expert counts.  Keys are the ids bit-packed into a
+// uint64 when l·k·ceil(log2 E) <= 64 (every config here), else s·k int32 byte strings.
 // Estimation is O(N_t · l) hash lookups plus one top-k per distinct path; counts are
 // integers, so the distribution chosen and the per-token P are exact functions of the trace.
 #include <algorithm>
@@ -26,23 +27,66 @@ namespace lina {
 
 namespace {
 
-// One token's selections in one layer as a sorted set, appended to a key (R19).
-void append_set(std::string* key, const int32_t* sel, int k) {
-  int32_t tmp[64];
-  std::vector<int32_t> big;
+// One token's selections in one layer as a sorted set (R19), into v[0..k).
+const int32_t* sorted_set(const int32_t* sel, int k, int32_t* tmp, std::vector<int32_t>* big) {
   int32_t* v = tmp;
   if (k > 64) {
-    big.resize(k);
-    v = big.data();
+    big->resize(k);
+    v = big->data();
   }
   std::memcpy(v, sel, sizeof(int32_t) * k);
   std::sort(v, v + k);
-  key->append(reinterpret_cast<const char*>(v), sizeof(int32_t) * k);
+  return v;
 }
+
+// Key of the path made of the s layer rows rows[0..s) (each k ids): bit-packed or bytes.
+struct PathKey {
+  const lina_pop_profile* p;
+  uint64_t u = 0;
+  std::string str;
+  int32_t tmp[64];
+  std::vector<int32_t> big;
+  void build(const int32_t* rows, int s) {
+    const int k = p->k;
+    u = 0;
+    str.clear();
+    for (int i = 0; i < s; ++i) {
+      const int32_t* v = sorted_set(rows + (int64_t)i * k, k, tmp, &big);
+      if (p->packed)
+        for (int q = 0; q < k; ++q) u = (u << p->bits) | (uint64_t)v[q];
+      else
+        str.append(reinterpret_cast<const char*>(v), sizeof(int32_t) * k);
+    }
+  }
+  std::vector<int64_t>& slot(lina_pop_profile* pp, size_t map) {
+    return pp->packed ? pp->maps64[map][u] : pp->maps[map][str];
+  }
+  const std::vector<int64_t>* find(size_t map) const {
+    if (p->packed) {
+      auto it = p->maps64[map].find(u);
+      return it == p->maps64[map].end() ? nullptr : &it->second;
+    }
+    auto it = p->maps[map].find(str);
+    return it == p->maps[map].end() ? nullptr : &it->second;
+  }
+};
 
 // k experts with the largest counts, ties to the lower id (R21).
 void top_k(const std::vector<int64_t>& c, int k, std::vector<int>* out) {
   const int E = (int)c.size();
+  if (k <= 8) {  // k linear passes: the first strict maximum not yet taken
+    out->clear();
+    for (int q = 0; q < k; ++q) {
+      int best = -1;
+      for (int e = 0; e < E; ++e) {
+        if (best >= 0 && c[e] <= c[best]) continue;
+        if (std::find(out->begin(), out->end(), e) != out->end()) continue;
+        best = e;
+      }
+      out->push_back(best);
+    }
+    return;
+  }
   out->resize(E);
   for (int e = 0; e < E; ++e) (*out)[e] = e;
   std::partial_sort(out->begin(), out->begin() + k, out->end(), [&](int a, int b) {
@@ -76,23 +120,27 @@ lina_pop_profile* popprof_create(int L, int E, int k, int l) {
   p->E = E;
   p->k = k;
   p->l = l;
-  p->maps.resize((size_t)L * (l + 1));
+  int bits = 1;
+  while ((1 << bits) < E) ++bits;
+  p->bits = bits;
+  p->packed = (int64_t)l * k * bits <= 64;
+  if (p->packed) p->maps64.resize((size_t)L * (l + 1));
+  else p->maps.resize((size_t)L * (l + 1));
   p->marg.assign(L, std::vector<int64_t>(E, 0));
   return p;
 }
 
 void popprof_add(lina_pop_profile* p, const int32_t* sel, int64_t T) {
   const int L = p->L, k = p->k, l = p->l;
-  std::string key;
+  PathKey key{p};
   for (int64_t t = 0; t < T; ++t) {
     const int32_t* st = sel + t * (int64_t)L * k;
     for (int m = 0; m < L; ++m) {
       const int32_t* next = st + (int64_t)m * k;
       for (int q = 0; q < k; ++q) p->marg[m][next[q]] += 1;
       for (int s = 1; s <= std::min(l, m); ++s) {
-        key.clear();
-        for (int i = m - s; i < m; ++i) append_set(&key, st + (int64_t)i * k, k);
-        auto& c = p->maps[(size_t)m * (l + 1) + s][key];
+        key.build(st + (int64_t)(m - s) * k, s);
+        auto& c = key.slot(p, (size_t)m * (l + 1) + s);
         if (c.empty()) c.assign(p->E, 0);
         for (int q = 0; q < k; ++q) c[next[q]] += 1;
       }
@@ -103,14 +151,11 @@ void popprof_add(lina_pop_profile* p, const int32_t* sel, int64_t T) {
 // The counts Ψ is read from for one token's history (R20): the longest seen suffix,
 // else the layer marginal; nullptr when neither has any selection.
 static const std::vector<int64_t>* distribution(const lina_pop_profile* p, int m, const int32_t* hist,
-                                                std::string* key) {
+                                                PathKey* key) {
   const int k = p->k, l = p->l;
   for (int s = l; s >= 1; --s) {
-    key->clear();
-    for (int i = l - s; i < l; ++i) append_set(key, hist + (int64_t)i * k, k);
-    const auto& mp = p->maps[(size_t)m * (l + 1) + s];
-    auto it = mp.find(*key);
-    if (it != mp.end()) return &it->second;
+    key->build(hist + (int64_t)(l - s) * k, s);
+    if (const std::vector<int64_t>* c = key->find((size_t)m * (l + 1) + s)) return c;
   }
   const auto& mg = p->marg[m];
   for (int64_t c : mg)
@@ -127,7 +172,7 @@ void popprof_estimate(const lina_pop_profile* p, int m, const int32_t* hist, int
   std::vector<int> picks;     // [entries][k]
   std::vector<double> probs;  // [entries][k]
   std::vector<int> chosen;
-  std::string key;
+  PathKey key{p};
   for (int64_t t = 0; t < T; ++t) {
     const std::vector<int64_t>* c = distribution(p, m, hist + t * (int64_t)l * k, &key);
     if (!c) {

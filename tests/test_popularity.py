@@ -177,6 +177,24 @@ def test_native_estimate_bit_exact(lina, k, l, p, s):
         assert [list(r) for r in topk] == [list(q) if q else [-1] * k for q in picks]
 
 
+@pytest.mark.parametrize("E,k,l", [(64, 2, 3), (64, 4, 3), (1024, 2, 3), (64, 10, 1)])
+def test_native_packed_and_string_keys_agree_with_oracle(lina, E, k, l):
+    """Paths are uint64 bit-packed keys when l·k·ceil(log2 E) <= 64 (E=64, k=2: 36 bits;
+    E=1024, k=2: 60 bits) and byte strings otherwise (E=64, k=4: 72 bits): both layouts
+    give the oracle's values bit-exactly."""
+    L = 5
+    tr = li.selection_trace(1500, L, E, k, 0.7, 1.0, seed=8)
+    pf = _profile(tr, l)
+    nat = lina.PopProfile(L, E, k, l)
+    nat.add(tr.sel)
+    fresh = li.selection_trace(300, L, E, k, 0.7, 1.0, seed=8, stream=2, maps=tr.maps, marginal=tr.marginal)
+    for m in range(l, L):
+        want, picks = pop.estimate(pf, m, fresh.sel[:, m - l:m, :])
+        got, topk = nat.estimate(m, fresh.sel[:, m - l:m, :])
+        assert got == want
+        assert [list(r) for r in topk] == [list(q) if q else [-1] * k for q in picks]
+
+
 def test_native_unseen_paths_and_empty_batch(lina):
     E = 4
     sel = np.array([[[0], [1], [2]], [[1], [1], [3]], [[2], [2], [0]]], dtype=np.int32)
