@@ -79,3 +79,65 @@ def test_two_rank_plan_agreement_gloo(world):
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
     assert all(min(r) >= 1 for _, _, r in res)
+
+
+def _two_phase_worker(rank, world, port, q):
+    """Phase one + phase two across two gloo ranks (§5.2): every rank
+    profiles the same trace, estimates the next layer from ITS OWN tokens' paths,
+    allgathers the estimates and the actual counts, and decides through the C ABI.  The
+    ranks must reach the same phase-one plan, the same phase-two decision and the same
+    final plan with no broadcast, each equal to the oracle's."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import lina_inputs as li
+    import paper_2210_17223_b200 as lina
+    from oracle import placement as oplace
+    from oracle import popularity as opop
+    E, L, k, l, m = 16, 5, 1, 2, 4
+    train = li.selection_trace(20000, L, E, k, 0.8, 1.0, seed=9)          # shared profiling trace
+    batch = li.selection_trace(1024, L, E, k, 0.8, 1.0, seed=9, stream=10 + rank,
+                               maps=train.maps, marginal=train.marginal)  # this rank's tokens
+    prof = lina.PopProfile(L, E, k, l)
+    prof.add(train.sel)
+    est_local, _ = prof.estimate(m, batch.sel[:, m - l:m, :])
+    # phase one: the global estimate is the token-weighted mean of the ranks' estimates
+    ests = [None] * world
+    dist.all_gather_object(ests, est_local)
+    est = [sum(e[x] for e in ests) / world for x in range(E)]
+    mpd = E // world * 2
+    plan1 = lina.lina_placement_compute(est, world, mpd)
+    # phase two: actual counts after gating (here: the trace's layer-m selections)
+    cnt = torch.from_numpy(np.bincount(batch.sel[:, m, :].ravel(), minlength=E).astype(np.int64))
+    allc = [torch.zeros(E, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allc, cnt)
+    actual = sum(c.numpy() for c in allc)
+    same = lina.lina_phase_two_check(est, actual, k)
+    final = plan1 if same else lina.lina_placement_compute(list(actual / actual.sum()), world, mpd)
+    # the oracle, from the same inputs
+    pf = opop.Profile(L, E, k, l)
+    pf.add_trace(train.sel)
+    ok = opop.estimate(pf, m, batch.sel[:, m - l:m, :])[0] == est_local
+    ok &= same == opop.phase_two(est, list(actual), k)
+    ref = oplace.place(est if same else list(actual / actual.sum()), world, mpd)
+    ok &= final.replicas == ref["replicas"] and final.hosted == ref["hosted"]
+    views = [None] * world
+    dist.all_gather_object(views, (same, final.replicas, final.replica_device, final.hosted))
+    ok &= all(v == views[0] for v in views)
+    q.put((rank, bool(ok), bool(same)))
+    dist.destroy_process_group()
+
+
+def test_two_rank_two_phase_agreement_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + os.getpid() % 100
+    procs = [ctx.Process(target=_two_phase_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
