@@ -294,9 +294,11 @@ lina_status lina_moe_infer_forward(lina_comm* comm, const lina_moe_desc* desc, c
  * top-2k experts of host_estimated and of the actual counts are compared as sets
  * and, if they differ, the plan is re-computed from the actual popularity ("following
  * the same logic in phase 1") before any token moves.  *host_replanned (may be
- * NULL) = 1 when phase two re-planned, else 0.  Identical on every rank (the counts
- * are allgathered).  Errors: as lina_moe_infer_forward, plus INVALID_ARGUMENT for a
- * NULL placement or host_estimated. */
+ * NULL) = 1 when phase two re-planned, else 0.  Every rank must pass the same
+ * placement and host_estimated (e.g. the mean of the ranks' estimates, allgathered by
+ * the caller); the decision and the final plan are then identical on every rank (the
+ * counts are allgathered inside).  Errors: as lina_moe_infer_forward, plus
+ * INVALID_ARGUMENT for a NULL placement or host_estimated, or a negative/NaN estimate. */
 lina_status lina_moe_infer_forward_two_phase(lina_comm* comm, const lina_moe_desc* desc,
                                              const void* tokens, const float* gate_w,
                                              const void* w1_all, const void* w2_all, void* out,
