@@ -208,3 +208,33 @@ def test_cuda_graph_replay_bitwise(n_chunks):
         for got, ref in zip(outs, (y, dx, dwg, dw1, dw2)):
             assert torch.equal(got, ref)
     comm.close()
+
+
+def test_two_layers_interleaved_fwd_fwd_bwd_bwd():
+    """Two MoE layers on one communicator run as in a model step — forward A, forward B,
+    backward B, backward A — each with its own saved state and workspace; every output
+    and gradient equals the oracle's single-layer result for that layer's inputs."""
+    import paper_2210_17223_b200 as lina
+    cfg = li.with_tokens(li.CONFIGS["C2"], 512)
+    Wg, W1, W2 = li.layer_weights(cfg, 5, "grid")
+    XA, dYA = li.layer_tokens(cfg, 6, 0, "grid")
+    XB, dYB = li.layer_tokens(cfg, 7, 0, "grid")
+    comm = lina.Comm(1, 0, 0)
+    dt = tdtype(cfg.dtype)
+    wg, w1, w2 = to_dev(Wg, torch.float32), to_dev(W1, dt), to_dev(W2, dt)
+    layers = {n: lina.MoELayer(comm, 512, cfg.d_model, cfg.d_ffn, cfg.num_experts, cfg.k, cfg.capacity(), 1, dt)
+              for n in "AB"}
+    x = {"A": to_dev(XA, dt), "B": to_dev(XB, dt)}
+    dy = {"A": to_dev(dYA, dt), "B": to_dev(dYB, dt)}
+    y = {n: layers[n].forward(x[n], wg, w1, w2) for n in "AB"}
+    grads = {n: layers[n].backward(dy[n], x[n], wg, w1, w2) for n in "BA"}
+    torch.cuda.synchronize()
+    for n, X, dY in (("A", XA, dYA), ("B", XB, dYB)):
+        o = oracle_layer(cfg, X, Wg, W1, W2, dY)
+        tol = TOL[cfg.dtype]
+        assert moe.normwise_error(y[n].float().cpu().numpy(), o["fw"].y) <= tol, n
+        dx, dwg, dw1, dw2 = (t.float().cpu().numpy() for t in grads[n])
+        assert moe.normwise_error(dx, o["bw"].dXs[0]) <= tol, n
+        assert moe.normwise_error(dwg, o["bw"].dWg) <= tol, n
+        assert moe.normwise_error(dw1, o["bw"].dW1) <= tol, n
+        assert moe.normwise_error(dw2, o["bw"].dW2) <= tol, n
