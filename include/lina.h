@@ -184,7 +184,9 @@ lina_status lina_replica_split(int32_t count, int32_t replicas, int32_t source_r
 /*  - top-k ties go to the lower expert id.                                   */
 /* Layers are 0-indexed.                                                      */
 /* ------------------------------------------------------------------------ */
-typedef struct lina_pop_profile lina_pop_profile;
+typedef struct lina_pop_profile lina_pop_profile;  /* lina_popprof_add must not overlap
+                                                      any other call on the same profile;
+                                                      concurrent estimates are safe (read only) */
 
 /* An empty profile.  num_layers >= 2, num_experts >= 1, 1 <= k <= num_experts,
  * 1 <= path_len < num_layers.  Errors: INVALID_ARGUMENT (all violations listed). */
