@@ -211,6 +211,17 @@ lina_status lina_popprof_add(lina_pop_profile* prof, const int32_t* host_sel, in
  * path_len or >= num_layers, bad ids, NULL). */
 lina_status lina_popprof_estimate(const lina_pop_profile* prof, int32_t layer, const int32_t* host_history,
                                   int64_t num_tokens, double* host_popularity, int32_t* host_topk);
+/* Persist a profile built offline from training traces ("In the profiling stage",
+ * P:432) for use at inference: a little-endian binary file (magic "LINAPOP1", the
+ * shape, the layer marginals and every sample-path entry); load returns a new profile
+ * (free it with lina_popprof_destroy) whose estimates equal the saved one's.  Errors:
+ * INVALID_ARGUMENT for a NULL argument or an unwritable, unreadable or malformed file
+ * (the message says which).  Host only. */
+lina_status lina_popprof_save(const lina_pop_profile* prof, const char* path);
+/* Shape of a profile (any output may be NULL). */
+lina_status lina_popprof_info(const lina_pop_profile* prof, int32_t* num_layers, int32_t* num_experts,
+                              int32_t* k, int32_t* path_len);
+lina_status lina_popprof_load(const char* path, lina_pop_profile** out);
 /* Phase two: *host_identical = 1 when the top-2k experts of the
  * estimate (host_estimated [E]) and of the actual selection counts
  * (host_actual_counts [E], e.g. the allgathered gate histogram) are the same set

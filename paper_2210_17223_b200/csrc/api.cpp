@@ -360,6 +360,42 @@ lina_status lina_popprof_estimate(const lina_pop_profile* prof, int32_t layer, c
   });
 }
 
+lina_status lina_popprof_save(const lina_pop_profile* prof, const char* path) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    need(v, prof, "prof");
+    need(v, path, "path");
+    raise_if(v, "lina_popprof_save");
+    const std::string err = popprof_save(prof, path);
+    if (!err.empty()) throw ArgError{"lina_popprof_save: " + err};
+    return LINA_OK;
+  });
+}
+
+lina_status lina_popprof_info(const lina_pop_profile* prof, int32_t* L, int32_t* E, int32_t* k, int32_t* l) {
+  if (!prof) {
+    set_error("lina_popprof_info: prof is NULL");
+    return LINA_ERR_INVALID_ARGUMENT;
+  }
+  if (L) *L = prof->L;
+  if (E) *E = prof->E;
+  if (k) *k = prof->k;
+  if (l) *l = prof->l;
+  return LINA_OK;
+}
+
+lina_status lina_popprof_load(const char* path, lina_pop_profile** out) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    need(v, path, "path");
+    need(v, out, "out");
+    raise_if(v, "lina_popprof_load");
+    const std::string err = popprof_load(path, out);
+    if (!err.empty()) throw ArgError{"lina_popprof_load: " + err};
+    return LINA_OK;
+  });
+}
+
 lina_status lina_phase_two_check(const double* est, const int32_t* actual, int32_t E, int32_t k,
                                  int32_t* identical) {
   return guarded([&] {

@@ -58,5 +58,7 @@ void popprof_add(lina_pop_profile* p, const int32_t* sel, int64_t T);
 void popprof_estimate(const lina_pop_profile* p, int m, const int32_t* hist, int64_t T, double* pop,
                       int32_t* topk);
 bool phase_two_identical(const double* est, const int32_t* actual, int E, int k);
+std::string popprof_save(const lina_pop_profile* p, const char* path);   // "" or the error
+std::string popprof_load(const char* path, lina_pop_profile** out);      // "" or the error
 
 }  // namespace lina

@@ -15,7 +15,9 @@
 // Estimation is O(N_t · l) hash lookups plus one top-k per distinct path; counts are
 // integers, so the distribution chosen and the per-token P are exact functions of the trace.
 #include <algorithm>
+#include <memory>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -198,6 +200,99 @@ void popprof_estimate(const lina_pop_profile* p, int m, const int32_t* hist, int
     }
   }
   for (int e = 0; e < E; ++e) pop[e] = T ? acc[e] / (double)T : 0.0;
+}
+
+// ---- persistence: "LINAPOP1", int32 L E k l, int8 packed, marginals [L][E] int64, then per
+// map (in index order) int64 n_entries and n × (key, counts[E] int64); a packed key is a
+// uint64, a string key an int32 byte length + bytes.
+namespace {
+struct File {
+  FILE* f;
+  explicit File(FILE* x) : f(x) {}
+  ~File() {
+    if (f) fclose(f);
+  }
+};
+template <typename T>
+bool put(FILE* f, const T& v) { return fwrite(&v, sizeof(T), 1, f) == 1; }
+template <typename T>
+bool get(FILE* f, T* v) { return fread(v, sizeof(T), 1, f) == 1; }
+bool put_counts(FILE* f, const std::vector<int64_t>& c) {
+  return fwrite(c.data(), sizeof(int64_t), c.size(), f) == c.size();
+}
+bool get_counts(FILE* f, std::vector<int64_t>* c, int E) {
+  c->resize(E);
+  if (fread(c->data(), sizeof(int64_t), E, f) != (size_t)E) return false;
+  for (int64_t x : *c)
+    if (x < 0) return false;
+  return true;
+}
+}  // namespace
+
+std::string popprof_save(const lina_pop_profile* p, const char* path) {
+  File fh(fopen(path, "wb"));
+  FILE* f = fh.f;
+  if (!f) return std::string("cannot open ") + path + " for writing";
+  bool ok = fwrite("LINAPOP1", 1, 8, f) == 8 && put<int32_t>(f, p->L) && put<int32_t>(f, p->E) &&
+            put<int32_t>(f, p->k) && put<int32_t>(f, p->l) && put<int8_t>(f, p->packed ? 1 : 0);
+  for (int m = 0; ok && m < p->L; ++m) ok = put_counts(f, p->marg[m]);
+  const size_t nmaps = (size_t)p->L * (p->l + 1);
+  for (size_t i = 0; ok && i < nmaps; ++i) {
+    if (p->packed) {
+      ok = put<int64_t>(f, (int64_t)p->maps64[i].size());
+      for (const auto& kv : p->maps64[i]) {
+        if (!ok) break;
+        ok = put<uint64_t>(f, kv.first) && put_counts(f, kv.second);
+      }
+    } else {
+      ok = put<int64_t>(f, (int64_t)p->maps[i].size());
+      for (const auto& kv : p->maps[i]) {
+        if (!ok) break;
+        ok = put<int32_t>(f, (int32_t)kv.first.size()) &&
+             fwrite(kv.first.data(), 1, kv.first.size(), f) == kv.first.size() && put_counts(f, kv.second);
+      }
+    }
+  }
+  if (!ok) return std::string("write to ") + path + " failed";
+  return "";
+}
+
+std::string popprof_load(const char* path, lina_pop_profile** out) {
+  File fh(fopen(path, "rb"));
+  FILE* f = fh.f;
+  if (!f) return std::string("cannot open ") + path;
+  char magic[8];
+  int32_t L, E, k, l;
+  int8_t packed;
+  if (fread(magic, 1, 8, f) != 8 || std::memcmp(magic, "LINAPOP1", 8) != 0) return "not a LINAPOP1 file";
+  if (!get(f, &L) || !get(f, &E) || !get(f, &k) || !get(f, &l) || !get(f, &packed)) return "truncated header";
+  if (L < 2 || E < 1 || k < 1 || k > E || l < 1 || l >= L) return "invalid shape in header";
+  std::unique_ptr<lina_pop_profile> p(popprof_create(L, E, k, l));
+  if ((packed != 0) != p->packed) return "key layout does not match the shape";
+  for (int m = 0; m < L; ++m)
+    if (!get_counts(f, &p->marg[m], E)) return "truncated or negative marginals";
+  const size_t nmaps = (size_t)L * (l + 1);
+  const int32_t key_bytes_max = (int32_t)(sizeof(int32_t) * (size_t)l * k);
+  for (size_t i = 0; i < nmaps; ++i) {
+    int64_t n;
+    if (!get(f, &n) || n < 0) return "truncated map header";
+    for (int64_t j = 0; j < n; ++j) {
+      std::vector<int64_t> c;
+      if (p->packed) {
+        uint64_t key;
+        if (!get(f, &key) || !get_counts(f, &c, E)) return "truncated map entry";
+        p->maps64[i][key] = std::move(c);
+      } else {
+        int32_t len;
+        if (!get(f, &len) || len < 0 || len > key_bytes_max) return "bad key length";
+        std::string key((size_t)len, '\0');
+        if (fread(&key[0], 1, (size_t)len, f) != (size_t)len || !get_counts(f, &c, E)) return "truncated map entry";
+        p->maps[i][key] = std::move(c);
+      }
+    }
+  }
+  *out = p.release();
+  return "";
 }
 
 bool phase_two_identical(const double* est, const int32_t* actual, int E, int k) {

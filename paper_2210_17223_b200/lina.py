@@ -31,7 +31,8 @@ ABI_SYMBOLS = [
     "lina_moe_infer_workspace_size", "lina_sched_config", "lina_allreduce_submit",
     "lina_allreduce_wait", "lina_sched_stats", "lina_profile_enable", "lina_profile_read",
     "lina_popprof_create", "lina_popprof_destroy", "lina_popprof_add", "lina_popprof_estimate",
-    "lina_phase_two_check", "lina_moe_infer_forward_two_phase",
+    "lina_phase_two_check", "lina_moe_infer_forward_two_phase", "lina_popprof_save", "lina_popprof_load",
+    "lina_popprof_info",
 ]
 
 
@@ -94,6 +95,9 @@ def load() -> ctypes.CDLL:
         "lina_popprof_add": ([vp, P(i32), ctypes.c_int64], i32),
         "lina_popprof_estimate": ([vp, i32, P(i32), ctypes.c_int64, P(ctypes.c_double), P(i32)], i32),
         "lina_phase_two_check": ([P(ctypes.c_double), P(i32), i32, i32, P(i32)], i32),
+        "lina_popprof_save": ([vp, ctypes.c_char_p], i32),
+        "lina_popprof_load": ([ctypes.c_char_p, P(vp)], i32),
+        "lina_popprof_info": ([vp, P(i32), P(i32), P(i32), P(i32)], i32),
         "lina_moe_workspace_size": ([vp, P(MoEDesc), P(sz), P(sz)], i32),
         "lina_moe_forward": ([vp, P(MoEDesc), vp, vp, vp, vp, vp, vp, vp, sz, P(Route), vp], i32),
         "lina_moe_backward": ([vp, P(MoEDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
@@ -293,6 +297,21 @@ class PopProfile:
         if self._h:
             load().lina_popprof_destroy(self._h)
             self._h = None
+
+    def save(self, path: str):
+        _check(load().lina_popprof_save(self._h, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path: str) -> "PopProfile":
+        """A profile saved by save() (lina_popprof_load); its shape comes from the file."""
+        h = ctypes.c_void_p()
+        _check(load().lina_popprof_load(os.fsencode(path), ctypes.byref(h)))
+        dims = [ctypes.c_int32() for _ in range(4)]
+        _check(load().lina_popprof_info(h, *[ctypes.byref(x) for x in dims]))
+        obj = cls.__new__(cls)
+        obj._h = h
+        obj.L, obj.E, obj.k, obj.l = (x.value for x in dims)
+        return obj
 
     def __del__(self):
         try:

@@ -236,3 +236,29 @@ def test_native_phase_two_matches_oracle(lina, seed):
         act = rng.integers(0, 6, size=E)
         assert lina.lina_phase_two_check(est, act, k) == pop.phase_two(list(est), list(act), k)
     assert lina.lina_phase_two_check([0.25] * 4, [1, 2, 3, 4], 2)   # 2k >= E: both lists are all experts
+
+
+@pytest.mark.parametrize("E,k,l", [(16, 1, 3), (64, 4, 3)])      # packed keys / byte-string keys
+def test_native_profile_save_load_round_trip(lina, tmp_path, E, k, l):
+    """A profile built offline ("In the profiling stage") and saved gives, once
+    loaded, the same estimates bit for bit; corrupt files are rejected with a reason."""
+    L = 5
+    tr = li.selection_trace(2000, L, E, k, 0.7, 1.0, seed=12)
+    nat = lina.PopProfile(L, E, k, l)
+    nat.add(tr.sel)
+    path = str(tmp_path / "prof.bin")
+    nat.save(path)
+    back = lina.PopProfile.load(path)
+    assert (back.L, back.E, back.k, back.l) == (L, E, k, l)
+    fresh = li.selection_trace(300, L, E, k, 0.7, 1.0, seed=12, stream=4, maps=tr.maps, marginal=tr.marginal)
+    for m in range(l, L):
+        a, ta = nat.estimate(m, fresh.sel[:, m - l:m, :])
+        b, tb = back.estimate(m, fresh.sel[:, m - l:m, :])
+        assert a == b and (ta == tb).all()
+    raw = open(path, "rb").read()
+    for bad in (b"NOTAPROF" + raw[8:], raw[: len(raw) // 2]):
+        open(path, "wb").write(bad)
+        with pytest.raises(lina.LinaError):
+            lina.PopProfile.load(path)
+    with pytest.raises(lina.LinaError):
+        lina.PopProfile.load(str(tmp_path / "missing.bin"))
