@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--copy-streams", type=int, default=1,
+                    help="e2e: split each step's host<->device copies over this many streams per direction")
     ap.add_argument("--eager", action="store_true", help="launch every kernel from the host (no CUDA graph)")
     ap.add_argument("--cpu-sample", type=int, default=256, help="tokens in the oracle sample")
     return ap.parse_args()
@@ -397,14 +399,36 @@ def main():
         in_ready = [torch.cuda.Event() for _ in range(2)]
         comp_done = [torch.cuda.Event() for _ in range(2)]
         out_done = [torch.cuda.Event() for _ in range(2)]
+        nsplit = max(1, args.copy_streams)
+        # extra streams per direction (nsplit > 1): row slices of every copy run on them
+        x_in = [torch.cuda.Stream(dev) for _ in range(nsplit - 1)]
+        x_out = [torch.cuda.Stream(dev) for _ in range(nsplit - 1)]
+
+        def split_copy(main, extra, pairs):
+            """Copy (dst, src) pairs on `main`, or as row slices over main + extra streams."""
+            if not extra:
+                for dst, src in pairs:
+                    dst.copy_(src, non_blocking=True)
+                return
+            ev = torch.cuda.Event()
+            ev.record(main)
+            streams = [main] + extra
+            for st in extra:
+                st.wait_event(ev)
+            rows = -(-T // len(streams))
+            for q, st in enumerate(streams):
+                with torch.cuda.stream(st):
+                    for dst, src in pairs:
+                        dst[q * rows:(q + 1) * rows].copy_(src[q * rows:(q + 1) * rows], non_blocking=True)
+            for st in extra:
+                main.wait_stream(st)
 
         def fetch(i):
             b = i % 2
             with torch.cuda.stream(s_in):
                 if i >= 2:
                     s_in.wait_event(comp_done[b])  # step i-2 is done reading this buffer
-                xd[b].copy_(xp, non_blocking=True)
-                dyd[b].copy_(dyp, non_blocking=True)
+                split_copy(s_in, x_in, [(xd[b], xp), (dyd[b], dyp)])
                 in_ready[b].record(s_in)
 
         e2e_graphs = None
@@ -433,8 +457,7 @@ def main():
             comp_done[b].record(stream)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(comp_done[b])
-                yp[b].copy_(yd[b], non_blocking=True)
-                dxp[b].copy_(dxd[b], non_blocking=True)
+                split_copy(s_out, x_out, [(yp[b], yd[b]), (dxp[b], dxd[b])])
                 out_done[b].record(s_out)
         stream.wait_stream(s_out)
         e1.record(stream)
@@ -445,7 +468,8 @@ def main():
         elt = 2 if tdt == torch.bfloat16 else 4
         e2e = {"value": world * T * args.steps / (float(e2e_ms[0]) / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": 2 * T * d * elt, "d2h_bytes_per_step": 2 * T * d * elt,
-               "copies": "pinned host <-> device on two copy streams, double-buffered, overlapping compute"}
+               "copies": "pinned host <-> device, double-buffered, overlapping compute, "
+                         f"{nsplit} stream(s) per direction"}
 
     # ---------------- roofline of the dominant kernel family (the six expert GEMMs)
     pk = peaks()
