@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--poison", action="store_true", help="start from NaN-filled saved/workspace buffers")
     ap.add_argument("--graph", action="store_true",
                     help="also capture fwd+bwd in a CUDA graph, replay it 3 times, require bitwise equal results")
+    ap.add_argument("--interleave", action="store_true",
+                    help="run a second layer B between A's forward and backward (fwd A, fwd B, bwd B, "
+                         "bwd A) on the same communicator; A must still match the oracle")
     a = ap.parse_args()
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -66,12 +69,22 @@ def main():
         w2 = torch.from_numpy(W2).to(tdt).to(dev)
         dy = torch.from_numpy(dY).to(tdt).to(dev)
         y = layer.forward(x, wg, w1, w2, want_route=True)
+        finite_b = True
+        if a.interleave:  # layer B's exchanges run between A's forward and backward
+            layer_b = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, cfg.capacity(),
+                                    n_chunks, tdt, dev)
+            XB, dYB = li.layer_tokens(cfg, a.seed + 1, rank)
+            xb = torch.from_numpy(XB).to(tdt).to(dev)
+            yb = layer_b.forward(xb, wg, w1, w2)
+            dxb = layer_b.backward(torch.from_numpy(dYB).to(tdt).to(dev), xb, wg, w1, w2)[0]
+            finite_b = bool(torch.isfinite(yb).all()) and bool(torch.isfinite(dxb).all())
         dx, dwg, dw1, dw2 = layer.backward(dy, x, wg, w1, w2)
         torch.cuda.synchronize()
         comm.check()
         out = {"y": y.float().cpu().numpy(), "dx": dx.float().cpu().numpy(), "dwg": dwg.cpu().numpy(),
                "dw1": dw1.float().cpu().numpy(), "dw2": dw2.float().cpu().numpy(),
-               "idx": layer.route_t["idx"].cpu().numpy(), "slot": layer.route_t["slot"].cpu().numpy()}
+               "idx": layer.route_t["idx"].cpu().numpy(), "slot": layer.route_t["slot"].cpu().numpy(),
+               "finite_b": finite_b}
         if a.graph:  # replays must be full steps: the cross-rank rounds live in device memory
             gy, gdx = torch.empty_like(y), torch.empty_like(dx)
             gdwg, gdw1, gdw2 = torch.empty_like(dwg), torch.empty_like(dw1), torch.empty_like(dw2)
@@ -99,6 +112,9 @@ def main():
     gathered = [None] * world
     dist.gather_object(res, gathered if rank == 0 else None, dst=0)
     ok = True
+    if rank == 0 and not all(g["finite_b"] for g in gathered):
+        print("interleaved layer B produced non-finite values", flush=True)
+        ok = False
     if rank == 0 and any(g.get("graph_mismatch") for g in gathered):
         print("CUDA graph replay differs from the eager step", flush=True)
         ok = False
