@@ -37,7 +37,11 @@ def plan_load(plan, actual, N):
 
 
 def main():
-    E, L, k, N, T, MPD = 32, 6, 1, 8, 4096, 8
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--k", type=int, default=1)
+    k = ap.parse_args().k
+    E, L, N, T, MPD = 32, 6, 8, 4096, 8
     print(f"# E={E} experts, L={L} MoE layers, top-{k}, N={N} devices (max {MPD} experts each), "
           f"{T} tokens per inference batch, Zipf s=1.0 marginals, 50k-token profiling trace")
     print("#   p  l  accuracy  finetune  load(est plan)  load(actual plan)  load(static)  estimate ms  plan ms")
