@@ -7,6 +7,15 @@
 #include <unordered_map>
 #include <vector>
 
+// One profiled distribution Ψ: per-expert selection counts, their total, and its top-k
+// experts (count desc, id asc) with P = count / total — refreshed by every add.
+struct PathDist {
+  std::vector<int64_t> c;
+  int64_t total = 0;
+  std::vector<int32_t> top;
+  std::vector<double> prob;
+};
+
 // Sample-path popularity profile (popularity.cpp; paper D4: host DRAM).
 struct lina_pop_profile {
   int L = 0, E = 0, k = 0, l = 0;
@@ -14,9 +23,9 @@ struct lina_pop_profile {
   bool packed = false;  // l·k·bits <= 64: paths are uint64 keys, else byte strings
   // [m * (l + 1) + s] for 1 <= s <= min(l, m): path (s sorted expert sets) -> per-expert
   // selection counts in layer m
-  std::vector<std::unordered_map<uint64_t, std::vector<int64_t>>> maps64;
-  std::vector<std::unordered_map<std::string, std::vector<int64_t>>> maps;
-  std::vector<std::vector<int64_t>> marg;  // [L][E] layer marginals (backoff)
+  std::vector<std::unordered_map<uint64_t, PathDist>> maps64;
+  std::vector<std::unordered_map<std::string, PathDist>> maps;
+  std::vector<PathDist> marg;  // [L] layer marginals (backoff)
 };
 
 namespace lina {

@@ -12,8 +12,9 @@
 // Layout: per target layer m and path length s, one hash map keyed by the path's expert
 // sets (each sorted ascending) -> per-expert counts.  Keys are the ids bit-packed into a
 // uint64 when l·k·ceil(log2 E) <= 64 (every config here), else s·k int32 byte strings.
-// Estimation is O(N_t · l) hash lookups plus one top-k per distinct path; counts are
-// integers, so the distribution chosen and the per-token P are exact functions of the trace.
+// Every entry keeps its top-k and P (refreshed by each add), so an estimate is one hash
+// lookup per backoff level and k additions per token; counts are integers, so the
+// distribution chosen and the per-token P are exact functions of the trace.
 #include <algorithm>
 #include <memory>
 #include <cstdint>
@@ -60,10 +61,10 @@ struct PathKey {
         str.append(reinterpret_cast<const char*>(v), sizeof(int32_t) * k);
     }
   }
-  std::vector<int64_t>& slot(lina_pop_profile* pp, size_t map) {
+  PathDist& slot(lina_pop_profile* pp, size_t map) {
     return pp->packed ? pp->maps64[map][u] : pp->maps[map][str];
   }
-  const std::vector<int64_t>* find(size_t map) const {
+  const PathDist* find(size_t map) const {
     if (p->packed) {
       auto it = p->maps64[map].find(u);
       return it == p->maps64[map].end() ? nullptr : &it->second;
@@ -97,6 +98,17 @@ void top_k(const std::vector<int64_t>& c, int k, std::vector<int>* out) {
   out->resize(k);
 }
 
+// Recompute a distribution's total, top-k and P after its counts changed (R20, R21).
+void refresh(PathDist* d, int k) {
+  d->total = 0;
+  for (int64_t x : d->c) d->total += x;
+  std::vector<int> chosen;
+  top_k(d->c, k, &chosen);
+  d->top.assign(chosen.begin(), chosen.end());
+  d->prob.resize(k);
+  for (int q = 0; q < k; ++q) d->prob[q] = d->total ? (double)d->c[chosen[q]] / (double)d->total : 0.0;
+}
+
 }  // namespace
 
 std::string popprof_check_ids(const lina_pop_profile* p, const int32_t* sel, int64_t rows, int layers) {
@@ -128,75 +140,71 @@ lina_pop_profile* popprof_create(int L, int E, int k, int l) {
   p->packed = (int64_t)l * k * bits <= 64;
   if (p->packed) p->maps64.resize((size_t)L * (l + 1));
   else p->maps.resize((size_t)L * (l + 1));
-  p->marg.assign(L, std::vector<int64_t>(E, 0));
+  p->marg.resize(L);
+  for (auto& d : p->marg) {
+    d.c.assign(E, 0);
+    refresh(&d, k);
+  }
   return p;
 }
 
 void popprof_add(lina_pop_profile* p, const int32_t* sel, int64_t T) {
   const int L = p->L, k = p->k, l = p->l;
   PathKey key{p};
+  std::vector<PathDist*> touched;  // entries whose summary must be refreshed
   for (int64_t t = 0; t < T; ++t) {
     const int32_t* st = sel + t * (int64_t)L * k;
     for (int m = 0; m < L; ++m) {
       const int32_t* next = st + (int64_t)m * k;
-      for (int q = 0; q < k; ++q) p->marg[m][next[q]] += 1;
+      for (int q = 0; q < k; ++q) p->marg[m].c[next[q]] += 1;
       for (int s = 1; s <= std::min(l, m); ++s) {
         key.build(st + (int64_t)(m - s) * k, s);
-        auto& c = key.slot(p, (size_t)m * (l + 1) + s);
-        if (c.empty()) c.assign(p->E, 0);
-        for (int q = 0; q < k; ++q) c[next[q]] += 1;
+        PathDist& d = key.slot(p, (size_t)m * (l + 1) + s);
+        if (d.c.empty()) d.c.assign(p->E, 0);
+        if (d.total >= 0) {  // first touch in this call (refresh sets total >= 0 again)
+          d.total = -1;
+          touched.push_back(&d);
+        }
+        for (int q = 0; q < k; ++q) d.c[next[q]] += 1;
       }
     }
   }
+  for (PathDist* d : touched) refresh(d, k);
+  if (T > 0)
+    for (auto& d : p->marg) refresh(&d, k);
 }
 
-// The counts Ψ is read from for one token's history (R20): the longest seen suffix,
-// else the layer marginal; nullptr when neither has any selection.
-static const std::vector<int64_t>* distribution(const lina_pop_profile* p, int m, const int32_t* hist,
-                                                PathKey* key) {
+// The distribution Ψ is read from for one token's history (R20): the longest seen
+// suffix, else the layer marginal; nullptr when neither has any selection.
+static const PathDist* distribution(const lina_pop_profile* p, int m, const int32_t* hist, PathKey* key) {
   const int k = p->k, l = p->l;
-  for (int s = l; s >= 1; --s) {
-    key->build(hist + (int64_t)(l - s) * k, s);
-    if (const std::vector<int64_t>* c = key->find((size_t)m * (l + 1) + s)) return c;
+  if (p->packed) {  // the length-s suffix of a packed path is its low s·k·bits bits
+    key->build(hist, l);
+    const uint64_t full = key->u;
+    for (int s = l; s >= 1; --s) {
+      const int nb = s * k * p->bits;
+      key->u = nb >= 64 ? full : (full & ((uint64_t(1) << nb) - 1));
+      if (const PathDist* d = key->find((size_t)m * (l + 1) + s)) return d;
+    }
+  } else {
+    for (int s = l; s >= 1; --s) {
+      key->build(hist + (int64_t)(l - s) * k, s);
+      if (const PathDist* d = key->find((size_t)m * (l + 1) + s)) return d;
+    }
   }
-  const auto& mg = p->marg[m];
-  for (int64_t c : mg)
-    if (c) return &mg;
-  return nullptr;
+  return p->marg[m].total > 0 ? &p->marg[m] : nullptr;
 }
 
 void popprof_estimate(const lina_pop_profile* p, int m, const int32_t* hist, int64_t T, double* pop,
                       int32_t* topk) {
   const int E = p->E, k = p->k, l = p->l;
   std::vector<double> acc(E, 0.0);
-  // Tokens sharing a path share its top-k and P: computed once per distribution per call.
-  std::unordered_map<const std::vector<int64_t>*, size_t> memo;
-  std::vector<int> picks;     // [entries][k]
-  std::vector<double> probs;  // [entries][k]
-  std::vector<int> chosen;
   PathKey key{p};
   for (int64_t t = 0; t < T; ++t) {
-    const std::vector<int64_t>* c = distribution(p, m, hist + t * (int64_t)l * k, &key);
-    if (!c) {
-      if (topk)
-        for (int q = 0; q < k; ++q) topk[t * k + q] = -1;
-      continue;
-    }
-    auto it = memo.find(c);
-    if (it == memo.end()) {
-      int64_t total = 0;
-      for (int64_t x : *c) total += x;
-      top_k(*c, k, &chosen);
-      it = memo.emplace(c, picks.size() / k).first;
-      for (int q = 0; q < k; ++q) {
-        picks.push_back(chosen[q]);
-        probs.push_back((double)(*c)[chosen[q]] / (double)total);  // P_j(e) = Ψ_j(e)
-      }
-    }
-    const size_t base = it->second * k;
+    const PathDist* d = distribution(p, m, hist + t * (int64_t)l * k, &key);
     for (int q = 0; q < k; ++q) {
-      acc[picks[base + q]] += probs[base + q];  // token order, as Σ_t in Eq. (1)
-      if (topk) topk[t * k + q] = picks[base + q];
+      if (d) acc[d->top[q]] += d->prob[q];  // P_j(e) = Ψ_j(e), summed in token order (Eq. (1))
+      if (topk) topk[t * k + q] = d ? d->top[q] : -1;
     }
   }
   for (int e = 0; e < E; ++e) pop[e] = T ? acc[e] / (double)T : 0.0;
@@ -235,21 +243,21 @@ std::string popprof_save(const lina_pop_profile* p, const char* path) {
   if (!f) return std::string("cannot open ") + path + " for writing";
   bool ok = fwrite("LINAPOP1", 1, 8, f) == 8 && put<int32_t>(f, p->L) && put<int32_t>(f, p->E) &&
             put<int32_t>(f, p->k) && put<int32_t>(f, p->l) && put<int8_t>(f, p->packed ? 1 : 0);
-  for (int m = 0; ok && m < p->L; ++m) ok = put_counts(f, p->marg[m]);
+  for (int m = 0; ok && m < p->L; ++m) ok = put_counts(f, p->marg[m].c);
   const size_t nmaps = (size_t)p->L * (p->l + 1);
   for (size_t i = 0; ok && i < nmaps; ++i) {
     if (p->packed) {
       ok = put<int64_t>(f, (int64_t)p->maps64[i].size());
       for (const auto& kv : p->maps64[i]) {
         if (!ok) break;
-        ok = put<uint64_t>(f, kv.first) && put_counts(f, kv.second);
+        ok = put<uint64_t>(f, kv.first) && put_counts(f, kv.second.c);
       }
     } else {
       ok = put<int64_t>(f, (int64_t)p->maps[i].size());
       for (const auto& kv : p->maps[i]) {
         if (!ok) break;
         ok = put<int32_t>(f, (int32_t)kv.first.size()) &&
-             fwrite(kv.first.data(), 1, kv.first.size(), f) == kv.first.size() && put_counts(f, kv.second);
+             fwrite(kv.first.data(), 1, kv.first.size(), f) == kv.first.size() && put_counts(f, kv.second.c);
       }
     }
   }
@@ -269,8 +277,10 @@ std::string popprof_load(const char* path, lina_pop_profile** out) {
   if (L < 2 || E < 1 || k < 1 || k > E || l < 1 || l >= L) return "invalid shape in header";
   std::unique_ptr<lina_pop_profile> p(popprof_create(L, E, k, l));
   if ((packed != 0) != p->packed) return "key layout does not match the shape";
-  for (int m = 0; m < L; ++m)
-    if (!get_counts(f, &p->marg[m], E)) return "truncated or negative marginals";
+  for (int m = 0; m < L; ++m) {
+    if (!get_counts(f, &p->marg[m].c, E)) return "truncated or negative marginals";
+    refresh(&p->marg[m], k);
+  }
   const size_t nmaps = (size_t)L * (l + 1);
   const int32_t key_bytes_max = (int32_t)(sizeof(int32_t) * (size_t)l * k);
   for (size_t i = 0; i < nmaps; ++i) {
@@ -281,13 +291,17 @@ std::string popprof_load(const char* path, lina_pop_profile** out) {
       if (p->packed) {
         uint64_t key;
         if (!get(f, &key) || !get_counts(f, &c, E)) return "truncated map entry";
-        p->maps64[i][key] = std::move(c);
+        PathDist& d = p->maps64[i][key];
+        d.c = std::move(c);
+        refresh(&d, k);
       } else {
         int32_t len;
         if (!get(f, &len) || len < 0 || len > key_bytes_max) return "bad key length";
         std::string key((size_t)len, '\0');
         if (fread(&key[0], 1, (size_t)len, f) != (size_t)len || !get_counts(f, &c, E)) return "truncated map entry";
-        p->maps[i][key] = std::move(c);
+        PathDist& d = p->maps[i][key];
+        d.c = std::move(c);
+        refresh(&d, k);
       }
     }
   }
