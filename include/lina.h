@@ -17,7 +17,9 @@
  *   gives all-to-all strict priority over the gradient allreduce, whose tensors
  *   are split into equal micro-ops (§3, §4.2, §6.1),
  *   and in inference replicates popular experts by Eq. (1) with first-fit-
- *   decreasing packing (§5.2) and an unequal-split all-to-all.
+ *   decreasing packing (§5.2) and an unequal-split all-to-all,
+ *   planning from a sample-path popularity estimate before gating and checking it
+ *   against the gate's top-2k after (two-phase scheduling).
  *   Readings where the paper is silent (capacity, drop order, gate
  *   normalisation, tie-breaks, rounding points, sample paths) are R1-R22 in DESIGN.md §3.
  *
