@@ -3,6 +3,7 @@
 #include "internal.h"
 #include "kernels.h"
 
+#include <deque>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -16,6 +17,65 @@ struct PathDist {
   std::vector<double> prob;
 };
 
+// Packed path -> PathDist: open addressing with linear probing over a power-of-two key
+// array (one cache line per probe, instead of a node chase per bucket).  Entries live in
+// a deque, so references stay valid while the table grows.
+class FlatPathMap {
+ public:
+  PathDist& operator[](uint64_t key) {
+    if ((n_ + 1) * 2 > keys_.size()) grow();
+    size_t i = slot_of(key);
+    if (idx_[i] < 0) {
+      idx_[i] = (int32_t)dists_.size();
+      keys_[i] = key;
+      dists_.emplace_back();
+      dist_keys_.push_back(key);
+      ++n_;
+    }
+    return dists_[(size_t)idx_[i]];
+  }
+  const PathDist* find(uint64_t key) const {
+    if (keys_.empty()) return nullptr;
+    const size_t i = slot_of(key);
+    return idx_[i] < 0 ? nullptr : &dists_[(size_t)idx_[i]];
+  }
+  size_t size() const { return n_; }
+  template <typename F>
+  void for_each(F f) const {
+    for (size_t j = 0; j < dists_.size(); ++j) f(dist_keys_[j], dists_[j]);
+  }
+
+ private:
+  static uint64_t mix(uint64_t x) {  // splitmix64 finaliser: packed keys are far from uniform
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+  }
+  size_t slot_of(uint64_t key) const {  // the key's slot, or the empty slot where it belongs
+    const size_t mask = keys_.size() - 1;
+    size_t i = (size_t)mix(key) & mask;
+    while (idx_[i] >= 0 && keys_[i] != key) i = (i + 1) & mask;
+    return i;
+  }
+  void grow() {
+    const size_t cap = keys_.empty() ? 64 : keys_.size() * 2;
+    keys_.assign(cap, 0);
+    idx_.assign(cap, -1);
+    for (size_t j = 0; j < dist_keys_.size(); ++j) {
+      const size_t i = slot_of(dist_keys_[j]);
+      keys_[i] = dist_keys_[j];
+      idx_[i] = (int32_t)j;
+    }
+  }
+  std::vector<uint64_t> keys_;
+  std::vector<int32_t> idx_;
+  std::deque<PathDist> dists_;
+  std::vector<uint64_t> dist_keys_;
+  size_t n_ = 0;
+};
+
 // Sample-path popularity profile (popularity.cpp; paper D4: host DRAM).
 struct lina_pop_profile {
   int L = 0, E = 0, k = 0, l = 0;
@@ -23,7 +83,7 @@ struct lina_pop_profile {
   bool packed = false;  // l·k·bits <= 64: paths are uint64 keys, else byte strings
   // [m * (l + 1) + s] for 1 <= s <= min(l, m): path (s sorted expert sets) -> per-expert
   // selection counts in layer m
-  std::vector<std::unordered_map<uint64_t, PathDist>> maps64;
+  std::vector<FlatPathMap> maps64;
   std::vector<std::unordered_map<std::string, PathDist>> maps;
   std::vector<PathDist> marg;  // [L] layer marginals (backoff)
 };

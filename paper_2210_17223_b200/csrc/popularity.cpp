@@ -66,8 +66,7 @@ struct PathKey {
   }
   const PathDist* find(size_t map) const {
     if (p->packed) {
-      auto it = p->maps64[map].find(u);
-      return it == p->maps64[map].end() ? nullptr : &it->second;
+      return p->maps64[map].find(u);
     }
     auto it = p->maps[map].find(str);
     return it == p->maps[map].end() ? nullptr : &it->second;
@@ -248,10 +247,9 @@ std::string popprof_save(const lina_pop_profile* p, const char* path) {
   for (size_t i = 0; ok && i < nmaps; ++i) {
     if (p->packed) {
       ok = put<int64_t>(f, (int64_t)p->maps64[i].size());
-      for (const auto& kv : p->maps64[i]) {
-        if (!ok) break;
-        ok = put<uint64_t>(f, kv.first) && put_counts(f, kv.second.c);
-      }
+      p->maps64[i].for_each([&](uint64_t key, const PathDist& d) {
+        if (ok) ok = put<uint64_t>(f, key) && put_counts(f, d.c);
+      });
     } else {
       ok = put<int64_t>(f, (int64_t)p->maps[i].size());
       for (const auto& kv : p->maps[i]) {
