@@ -1,11 +1,15 @@
 """Benchmark of the Lina B200 MoE layer: one step = forward + backward of the whole hot
 path (gate, route, permute, dispatch all-to-all, expert FFN, combine all-to-all,
-un-permute, and their backward) on synthetic tokens shaped like BASELINE.json's
-configs[1] (GPT-2-small-shaped MoE layer: 8 experts, top-2, d_model 768, 8K
-tokens per GPU, bf16).  Metric: MoE layer tokens/s fwd+bwd, whole job.
+un-permute, and their backward; at N > 1 also the gate-weight gradient allreduce
+through the micro-op scheduler) on synthetic tokens shaped like BASELINE.json's
+configs[4] (the scale sweep "at 1/2/4/8 B200": 64 experts, top-2, d_model 2048,
+d_ffn 8192, 32K tokens per GPU, bf16) — the largest single-GPU configuration and the
+one the metric's "at 1/2/4/8 B200" names.  Metric: MoE layer tokens/s fwd+bwd,
+whole job.
 
-    python bench.py [--gpus N --steps K --warmup W] [--config C2] [--n-chunks n]
+    python bench.py [--gpus N --steps K --warmup W] [--config C5] [--n-chunks n]
     python bench.py --impl reference ...      # the CPU oracle on a bounded sample
+    torchrun ... bench.py --gpus N --sweep-chunks 1,2,4,8   # H(n) per micro-op count
 
 Multi-GPU: launched by torch.distributed.run, one rank per GPU (weak scaling: each
 rank keeps T tokens; experts are partitioned E/N per rank).  Timing: CUDA events
@@ -37,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="lina", choices=["lina", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(li.CONFIGS))
+    ap.add_argument("--config", default="C5", choices=sorted(li.CONFIGS))
     ap.add_argument("--n-chunks", type=int, default=0,
                     help="0 = 1 (the fused transport needs no micro-op chunking; see DESIGN.md §7)")
     ap.add_argument("--nccl-ctas", type=int, default=8, help="ncclConfig_t.maxCTAs per communicator (N>1)")
@@ -48,8 +52,16 @@ def parse():
     ap.add_argument("--copy-streams", type=int, default=1,
                     help="e2e: split each step's host<->device copies over this many streams per direction")
     ap.add_argument("--eager", action="store_true", help="launch every kernel from the host (no CUDA graph)")
-    ap.add_argument("--cpu-sample", type=int, default=256, help="tokens in the oracle sample")
-    return ap.parse_args()
+    ap.add_argument("--cpu-sample", type=int, default=0,
+                    help="tokens in the oracle sample (0 = 64 for C5, 256 otherwise: ~10-30 s of host work)")
+    ap.add_argument("--sweep-chunks", default="",
+                    help="N > 1: comma list of n_chunks; H(n) and the pipelining efficiency for each (eager passes)")
+    ap.add_argument("--sched-policy", default="lina", choices=["lina", "baseline", "naive", "defer"],
+                    help="N > 1: allreduce scheduler policy for the per-step dWg allreduce")
+    a = ap.parse_args()
+    if a.cpu_sample <= 0:
+        a.cpu_sample = 64 if a.config == "C5" else 256
+    return a
 
 
 def dist_env():
@@ -69,10 +81,43 @@ def peaks():
         return {"bf16_sustained": 1400.0, "bf16_burst": 1590.0, "hbm": 6650.0, "src": "fallback"}
 
 
-def gemm_floors(d, f, experts_local, kept, elt, pk):
+def choose_peak(pk, clk):
+    """Burst bf16 peak unless the timed region ran power-capped or with its median SM clock
+    well below max (then the sustained peak, measured at a loaded clock, is the fair one)."""
+    reasons = clk.get("reasons") or []
+    sm, mx = clk.get("sm_mhz"), clk.get("sm_max_mhz")
+    low = sm is not None and mx and sm < 0.9 * mx
+    if "sw_power_cap" in reasons or low:
+        why = "sw_power_cap" if "sw_power_cap" in reasons else f"median SM clock {sm:.0f} < 0.9 x {mx:.0f} MHz"
+        return pk["bf16_sustained"], "sustained", why
+    why = (f"median SM clock {sm:.0f} of {mx:.0f} MHz, no power cap" if sm is not None
+           else "no clock record (nvidia-smi unavailable)")
+    return pk["bf16_burst"], "burst", why
+
+
+def layer_floor(d, f, E_local, k, T, kept, P, elt, tc_tflops, hbm_gbs, nvlink_gbs=900.0):
+    """SURVEY.md §8(d) layer roofline of one fwd+bwd step on one rank:
+    t_roof = max(F_gemm / TC, B_a2a,offGPU / NVLink) + B_memkernels / HBM.
+
+    F_gemm = 12·k·d·f per kept assignment; B_a2a per direction = the 4 all-to-alls' kept rows
+    (d·elt each) × (P−1)/P leaving the GPU; B_memkernels = the HBM-bound kernels' algorithmic
+    bytes per token: forward d·elt·(3 + 2k) (gate reads X; permute reads X, writes k rows;
+    combine reads k rows, writes y) and backward d·elt·(3 + 3k) (combine-backward reads dY and
+    k output rows, writes k rows; dX reads k rows, writes dX; dWg reads X)."""
+    flops = 12.0 * kept * d * f
+    a2a_dir = 4.0 * kept * d * elt * (P - 1) / P
+    mem = T * d * elt * ((3 + 2 * k) + (3 + 3 * k))
+    t_gemm = flops / (tc_tflops * 1e12) * 1e3
+    t_a2a = a2a_dir / (nvlink_gbs * 1e9) * 1e3
+    t_mem = mem / (hbm_gbs * 1e9) * 1e3
+    return {"t_roof_ms": max(t_gemm, t_a2a) + t_mem, "t_gemm_ms": t_gemm, "t_a2a_ms": t_a2a, "t_mem_ms": t_mem,
+            "gemm_flops": flops, "a2a_bytes_per_direction": a2a_dir, "memkernel_bytes": mem}
+
+
+def gemm_floors(d, f, experts_local, kept, elt, pk, tc_tflops):
     """Floors of the six expert GEMMs of one step; the bound is the higher.
 
-    tensor: 12·d·f flop per kept assignment (fwd 4df, bwd 8df) at the sustained bf16 peak.
+    tensor: 12·d·f flop per kept assignment (fwd 4df, bwd 8df) at the chosen bf16 peak.
     HBM: the algorithmic bytes of the six GEMMs as separate kernels at the measured copy
     bandwidth — each local expert's W1 and W2 read twice (GEMM1/GEMM2, the two dgrads) and
     dW1, dW2 written once (6·d·f elements per expert); per kept row 6·d + 6·f activation
@@ -81,7 +126,7 @@ def gemm_floors(d, f, experts_local, kept, elt, pk):
     """
     flops = 12.0 * kept * d * f
     nbytes = 6.0 * experts_local * d * f * elt + kept * (6.0 * (d + f) * elt + 2.0 * f / 8)
-    t_tensor = flops / (pk["bf16_sustained"] * 1e12) * 1e3
+    t_tensor = flops / (tc_tflops * 1e12) * 1e3
     t_hbm = nbytes / (pk["hbm"] * 1e9) * 1e3
     return {"flops": flops, "bytes": nbytes, "tensor_ms": t_tensor, "hbm_ms": t_hbm, "hbm_bound": t_hbm > t_tensor}
 
@@ -237,9 +282,22 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
+    # N > 1: the gate weights are replicated (data parallel), so every step ends with the
+    # allreduce of dWg (S8(g)) — a non-expert gradient issued through the micro-op scheduler
+    # (S9) on the DP communicator; the stream waits for it on the device.
+    policy = {"baseline": 0, "lina": 1, "naive": 2, "defer": 3}[args.sched_policy]
+    if world > 1:
+        lina.lina_sched_config(comm, policy, 30 << 20)
+
+    def allreduce_dwg():
+        if world > 1:
+            lina.lina_allreduce_submit(comm, outs["dwg"], stream)
+            lina.lina_allreduce_wait(comm, stream)
+
     def step(xx, dyy):
         layer.forward(xx, wg, w1, w2, out=outs["y"])
         layer.backward(dyy, xx, wg, w1, w2, outs["dx"], outs["dwg"], outs["dw1"], outs["dw2"])
+        allreduce_dwg()
 
     # routing of this batch (identical every step): kept assignments for the algorithmic flop count
     layer.forward(x, wg, w1, w2, out=outs["y"], want_route=True)
@@ -280,7 +338,13 @@ def main():
             graph = None
             launch_mode = f"eager (graph capture failed: {type(exc).__name__})"
             torch.cuda.synchronize()
-    run_step = graph.replay if graph is not None else (lambda: step(x, dy))
+    if graph is not None:
+        def run_step():
+            graph.replay()
+            allreduce_dwg()  # (host-issued micro-ops: not part of the captured graph)
+    else:
+        def run_step():
+            step(x, dy)
 
     # ---------------- timed region (device time, per-step events, L2 flushed between steps)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -316,6 +380,7 @@ def main():
     lina.lina_profile_enable(comm, False)
     prof = lina.lina_profile_read(comm)
     gemm_ms = prof["gemm_ms"]
+    step_ms_eager = [a.elapsed_time(b) for a, b in evs_e]
     eager_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in evs_e) / args.steps], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(eager_ms, op=torch.distributed.ReduceOp.MAX)
@@ -331,10 +396,13 @@ def main():
         total_ms_max, kept_total = total_ms, float(kept_local)
     value = world * T * args.steps / (total_ms_max / 1e3)
 
-    # ---------------- exposed communication (N>1): compute-only and all-to-all-only passes
-    a2a = None
-    if world > 1:
-        def timed(flags):
+    # ---------------- exposed communication and H(n) (N > 1): eager passes of
+    # the same steps — full (T_pass, the pipelining efficiency's windows), compute-only
+    # (collectives skipped: T_rest + T_ffn, with T_ffn = the expert-GEMM phases) and
+    # collectives-only (the fused transport's 2n micro-ops per pass alone: T_a2a(n)).
+    # Medians over the K steps.
+    def h_of(lay, nch):
+        def passes(flags):
             lina.lina_profile_enable(comm, flags)
             barrier()
             torch.cuda.synchronize()
@@ -343,42 +411,71 @@ def main():
             for i in range(args.steps):
                 flush.zero_()
                 ev[i][0].record(stream)
-                step(x, dy)
+                lay.forward(x, wg, w1, w2, out=outs["y"])
+                lay.backward(dy, x, wg, w1, w2, outs["dx"], outs["dwg"], outs["dw1"], outs["dw2"])
                 ev[i][1].record(stream)
             torch.cuda.synchronize()
             barrier()
             lina.lina_profile_enable(comm, 0)
-            lina.lina_profile_read(comm)
-            t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], dtype=torch.float64, device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            return float(t[0])
-        t_comp = timed(2)
-        t_comm = timed(4)
-        t_step = eager_step_ms  # the compute-only and collectives-only passes are eager too
-        exposed = max(0.0, t_step - t_comp)
-        from paper_2210_17223_b200.lina import LINA_BF16  # noqa: F401
-        elt = 2 if tdt == torch.bfloat16 else 4
-        import math
-        cm_rows = C if n_chunks == 1 else None
-        if cm_rows is None:  # chunk pitch (R10)
-            base = math.ceil(C / n_chunks)
-            cm_rows = base
-            for al in (256, 128, 64):
-                cmv = math.ceil(base / al) * al
-                if (n_chunks - 1) * cmv < C:
-                    cm_rows = cmv
-                    break
-        bytes_rank = 4 * n_chunks * E * cm_rows * d * elt   # 4 all-to-alls of the padded send buffer
-        algbw = bytes_rank / (t_comm / 1e3) / 1e9
-        a2a = {"ms_per_step_isolated": t_comm,
-               # the fused transport has no stand-alone collective: its isolated pass moves the
-               # same bytes with the copy-engine transport
-               "isolated_transport": "ce" if transport == "fused" else transport,
-               "ms_per_step_compute_only": t_comp, "ms_per_step_eager": t_step,
-               "exposed_ms_per_step": exposed,
-               "hidden_frac": (1.0 - exposed / t_comm) if t_comm > 0 else None,
-               "algbw_GBps": algbw, "busbw_GBps": algbw * (world - 1) / world,
-               "bytes_per_rank_per_step": bytes_rank, "nccl_max_ctas": args.nccl_ctas}
+            pr = lina.lina_profile_read(comm)
+            med = float(np.median([a.elapsed_time(b) for a, b in ev]))
+            v = torch.tensor([med, pr["gemm_ms"] / args.steps, pr["a2a_window_ms"] / args.steps,
+                              pr["gemm_in_a2a_ms"] / args.steps], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(v, op=torch.distributed.ReduceOp.MAX)
+            return [float(t) for t in v]
+        lay.forward(x, wg, w1, w2, out=outs["y"])  # routing in `saved` for the movers-only pass
+        t_pass, _, win, busy = passes(1)
+        t_comp, t_ffn, _, _ = passes(1 | 2)
+        t_a2a = passes(4)[0]
+        lay.forward(x, wg, w1, w2, out=outs["y"])  # (restore real routing / rounds)
+        lay.backward(dy, x, wg, w1, w2, outs["dx"], outs["dwg"], outs["dw1"], outs["dw2"])
+        torch.cuda.synchronize()
+        t_rest = max(0.0, t_comp - t_ffn)
+        X = max(0.0, t_pass - t_comp)
+        O = min(t_a2a * (1.0 - 1.0 / nch), t_ffn)  # fill (first dispatch) and drain (last combine)
+        elt_ = 2 if tdt == torch.bfloat16 else 4
+        a2a_bytes = 4.0 * kept_local * d * elt_ * (world - 1) / world  # algorithmic, off-GPU, per rank
+        return {"n_chunks": nch, "T_pass_ms": t_pass, "T_rest_ms": t_rest, "T_ffn_ms": t_ffn,
+                "T_a2a_ms": t_a2a, "exposed_ms": X,
+                "overlappable_ms": O,
+                "H": (min(1.0, (t_a2a - X) / O) if O > 1e-9 else None),
+                "hidden_vs_isolated": max(0.0, min(1.0, 1.0 - X / t_a2a)) if t_a2a > 0 else None,
+                "pipelining_efficiency": (busy / win) if win > 0 else None,
+                "a2a_window_ms": win, "gemm_in_a2a_window_ms": busy,
+                # nccl-tests convention: algbw = bytes each rank sends (its own experts' rows
+                # included) / T_a2a; busbw = algbw (P-1)/P = the off-GPU bytes / T_a2a
+                "a2a_algbw_GBps": a2a_bytes * world / (world - 1) / (t_a2a / 1e3) / 1e9 if t_a2a > 0 else None,
+                "a2a_busbw_GBps": a2a_bytes / (t_a2a / 1e3) / 1e9 if t_a2a > 0 else None}
+
+    a2a = None
+    sweep = None
+    if world > 1:
+        h = h_of(layer, n_chunks)
+        a2a = dict(h)
+        a2a.update({
+            "transport": transport,
+            "definitions": "SURVEY.md §8(d): X = max(0, T_pass - T_rest - T_ffn); O = min(T_a2a(1 - 1/n), T_ffn) "
+                           "(equal micro-ops: fill = first dispatch, drain = last combine); H = min(1, (T_a2a - X)/O), "
+                           "null when O = 0 (n = 1: nothing overlappable under the paper's model although the fused "
+                           "epilogue stores overlap the GEMM); hidden_vs_isolated = 1 - X/T_a2a; pipelining "
+                           "efficiency = expert-GEMM time inside the all-to-all windows / the windows (P:700); "
+                           "busbw = algorithmic off-GPU bytes (4 all-to-alls of the kept rows x (P-1)/P) / T_a2a",
+            "bytes_per_rank_per_step": 4.0 * kept_local * d * (2 if tdt == torch.bfloat16 else 4) * (world - 1) / world,
+            "dwg_allreduce": f"lina_allreduce_submit/wait every step, policy {args.sched_policy}, 30 MB micro-ops"})
+        if args.sweep_chunks:
+            sweep = []
+            for nch in [int(v) for v in args.sweep_chunks.split(",") if v.strip()]:
+                if nch == n_chunks:
+                    sweep.append(h)
+                    continue
+                lay = lina.MoELayer(comm, T, d, f, E, k, C, nch, tdt, dev)
+                for _ in range(2):
+                    lay.forward(x, wg, w1, w2, out=outs["y"])
+                    lay.backward(dy, x, wg, w1, w2, outs["dx"], outs["dwg"], outs["dw1"], outs["dw2"])
+                torch.cuda.synchronize()
+                sweep.append(h_of(lay, nch))
+                del lay
+                torch.cuda.empty_cache()
 
     # ---------------- end to end through the public API, host buffers (pinned), copies timed
     # Every step copies its inputs (x, dY) from pinned host memory and its results (y, dX)
@@ -454,6 +551,7 @@ def main():
             else:
                 layer.forward(xd[b], wg, w1, w2, out=yd[b])
                 layer.backward(dyd[b], xd[b], wg, w1, w2, dxd[b], outs["dwg"], outs["dw1"], outs["dw2"])
+            allreduce_dwg()
             comp_done[b].record(stream)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(comp_done[b])
@@ -473,16 +571,20 @@ def main():
 
     # ---------------- roofline of the dominant kernel family (the six expert GEMMs)
     pk = peaks()
-    fl = gemm_floors(d, f, E // world, kept_local, 2 if tdt == torch.bfloat16 else 4, pk)
+    clk = clocks.summary()
+    tc_peak, peak_kind, peak_why = choose_peak(pk, clk)
+    elt = 2 if tdt == torch.bfloat16 else 4
+    fl = gemm_floors(d, f, E // world, kept_local, elt, pk, tc_peak)
     flops_per_step_local, bytes_per_step_local = fl["flops"], fl["bytes"]
     t_tensor_ms, t_hbm_ms, hbm_bound = fl["tensor_ms"], fl["hbm_ms"], fl["hbm_bound"]
     gemm_ms_per_step = gemm_ms / max(args.steps, 1)
     if hbm_bound:
         achieved = bytes_per_step_local / (gemm_ms_per_step / 1e3) / 1e9 if gemm_ms > 0 else None
-        peak, unit, psrc = pk["hbm"], "GB/s", f"{pk['src']} HBM copy bandwidth (MEASURED_PEAKS.json)"
+        peak, unit, psrc = pk["hbm"], "GB/s", f"{pk['src']} HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs)"
     else:
         achieved = flops_per_step_local / (gemm_ms_per_step / 1e3) / 1e12 if gemm_ms > 0 else None
-        peak, unit, psrc = pk["bf16_sustained"], "TFLOP/s", f"{pk['src']} bf16 sustained (MEASURED_PEAKS.json)"
+        key = "bf16_tflops" if peak_kind == "burst" else "bf16_tflops_sustained"
+        peak, unit, psrc = tc_peak, "TFLOP/s", f"{pk['src']} bf16 {peak_kind} (MEASURED_PEAKS.json {key}): {peak_why}"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tpath):
@@ -490,16 +592,28 @@ def main():
             traffic = json.load(open(tpath)).get(args.config)
         except Exception:
             traffic = None
+    step_med_ms = float(np.median(step_ms))
+    lf = layer_floor(d, f, E // world, k, T, kept_local, world, elt, tc_peak, pk["hbm"])
     roof = {"bound": "hbm" if hbm_bound else "tensor",
             "kernel": "expert grouped GEMMs (fwd GEMM1+ReLU, GEMM2; bwd dgrad x2, wgrad x2)",
             "achieved": achieved, "peak": peak, "unit": unit,
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "peak_src": psrc,
+            "peak_kind": peak_kind, "peak_src": psrc,
+            "how": "achieved = algorithmic flops per step (12*k*d*f per kept assignment) / the expert-GEMM phase "
+                   "time per step (CUDA events on the compute stream around every GEMM phase, eager pass)",
             "gemm_ms_per_step": gemm_ms_per_step,
-            "gemm_share_of_step": gemm_ms_per_step / (total_ms / args.steps) if total_ms > 0 else None,
+            "gemm_share_of_step": gemm_ms_per_step / (sum(step_ms_eager) / args.steps) if step_ms_eager else None,
             "algorithmic_flops_per_step": flops_per_step_local,
             "algorithmic_bytes_per_step": bytes_per_step_local,
-            "floors_ms": {"tensor": t_tensor_ms, "hbm": t_hbm_ms}}
+            "floors_ms": {"tensor": t_tensor_ms, "hbm": t_hbm_ms},
+            # the whole layer against max(GEMM/TC, a2a/NVLink) + memory-bound/HBM
+            "layer": {"t_roof_ms": lf["t_roof_ms"], "t_measured_ms": step_med_ms,
+                      "frac": lf["t_roof_ms"] / step_med_ms if step_med_ms > 0 else None,
+                      "terms_ms": {"gemm_tensor": lf["t_gemm_ms"], "a2a_nvlink": lf["t_a2a_ms"],
+                                   "memory_bound_kernels_hbm": lf["t_mem_ms"]},
+                      "bytes": {"a2a_per_direction": lf["a2a_bytes_per_direction"],
+                                "memory_bound_kernels": lf["memkernel_bytes"]},
+                      "peaks": {"tensor_TFLOPs": tc_peak, "hbm_GBps": pk["hbm"], "nvlink_GBps_per_direction": 900.0}}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -522,10 +636,11 @@ def main():
                        "kept_assignments": int(kept_total)},
             "roofline": roof,
             "a2a": a2a,
+            "a2a_sweep": sweep,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(prof["kernel_launches"]),  # this library's kernels per K steps (eager count)
-            "clocks": clocks.summary(),
+            "clocks": clk,
             "step_ms": {"min": min(step_ms), "median": float(np.median(step_ms)), "max": max(step_ms)},
             "host_enqueue_ms_per_step": host_ms,
         }

@@ -19,7 +19,7 @@
  *   and in inference replicates popular experts by Eq. (1) with first-fit-
  *   decreasing packing (§5.2) and an unequal-split all-to-all,
  *   planning from a sample-path popularity estimate before gating and checking it
- *   against the gate's top-2k after (two-phase scheduling, P:432-485).
+ *   against the gate's top-2k after (two-phase scheduling, P:428-485).
  *   Readings where the paper is silent (capacity, drop order, gate
  *   normalisation, tie-breaks, rounding points, sample paths) are R1-R22 in DESIGN.md §3.
  *
@@ -175,7 +175,7 @@ lina_status lina_replica_split(int32_t count, int32_t replicas, int32_t source_r
                                int32_t* host_out);
 
 /* ------------------------------------------------------------------------ */
-/* Popularity estimation and two-phase scheduling (PAPER.md §5.2, P:432-484;  */
+/* Popularity estimation and two-phase scheduling (PAPER.md §5.2, P:428-484;  */
 /* paper D4: per-layer popularity distributions kept in host DRAM).    */
 /* Pure host functions, no device needed.  Readings R19-R22:   */
 /*  - a sample path of length l ending at layer i = the token's selected      */
@@ -196,17 +196,17 @@ lina_status lina_popprof_create(int32_t num_layers, int32_t num_experts, int32_t
                                 lina_pop_profile** out);
 /* Frees the profile.  NULL is a no-op. */
 lina_status lina_popprof_destroy(lina_pop_profile* prof);
-/* "collect the expert selection results of all tokens" (P:432-433) and group them by
- * sample path (P:434-436): host_sel [num_tokens][num_layers][k] int32 expert ids
+/* "collect the expert selection results of all tokens" (P:428) and group them by
+ * sample path (P:429-430): host_sel [num_tokens][num_layers][k] int32 expert ids
  * (host memory, read only during the call).  Counts accumulate over calls.
  * Errors: INVALID_ARGUMENT (NULL, num_tokens < 0, an id outside [0, E), or a token
  * selecting one expert twice in a layer); the profile is unchanged on error. */
 lina_status lina_popprof_add(lina_pop_profile* prof, const int32_t* host_sel, int64_t num_tokens);
 /* Phase-one estimate of layer `layer`'s expert popularity for a batch, before any of
- * its computation (P:455-458): each token t takes the top-k experts of its path's
+ * its computation (P:461-463): each token t takes the top-k experts of its path's
  * Psi and contributes their probabilities P_j(e); host_popularity[e] =
  * (sum_t P_{j(t)}(e)) / num_tokens in fp64, summed in token order (Eq. (1)'s overall
- * popularity, P:466-471).  host_history [num_tokens][path_len][k] = each token's
+ * popularity, P:473-476).  host_history [num_tokens][path_len][k] = each token's
  * selections at layers layer-path_len .. layer-1.  host_topk [num_tokens][k] (may be
  * NULL) receives each token's chosen experts, -1 for a token with no distribution.
  * A batch with num_tokens == 0 yields all zeros.  Errors: INVALID_ARGUMENT (layer <
@@ -214,7 +214,7 @@ lina_status lina_popprof_add(lina_pop_profile* prof, const int32_t* host_sel, in
 lina_status lina_popprof_estimate(const lina_pop_profile* prof, int32_t layer, const int32_t* host_history,
                                   int64_t num_tokens, double* host_popularity, int32_t* host_topk);
 /* Persist a profile built offline from training traces ("In the profiling stage",
- * P:432) for use at inference: a little-endian binary file (magic "LINAPOP1", the
+ * P:428) for use at inference: a little-endian binary file (magic "LINAPOP1", the
  * shape, the layer marginals and every sample-path entry); load returns a new profile
  * (free it with lina_popprof_destroy) whose estimates equal the saved one's.  Errors:
  * INVALID_ARGUMENT for a NULL argument or an unwritable, unreadable or malformed file
@@ -260,7 +260,18 @@ typedef struct {
 
 /* Bytes of scratch (`workspace`) and of state kept from forward to backward
  * (`saved`) for this descriptor on this communicator.  saved may be 0-sized
- * pointer-wise for inference-only forward (pass saved = NULL). */
+ * pointer-wise for inference-only forward (pass saved = NULL).
+ * Multi-rank rules (fused / copy-engine transports, where ranks store into and read
+ * from each other's saved and workspace buffers):
+ *   - capacity, n_chunks, num_experts, d_model, d_ffn and dtype must be equal on every
+ *     rank; num_tokens may differ (every peer-visible region sits at an offset that does
+ *     not depend on it).  The first call with a buffer checks this collectively and
+ *     fails with INVALID_ARGUMENT on every rank otherwise.
+ *   - saved and workspace are bound to the peers on their first use (a collective
+ *     inside that call); a buffer freed and re-allocated is bound again, so all ranks
+ *     must switch to new buffers in the same call (as an SPMD program does).
+ *   - workspace is scratch: several layers on one communicator may share it (their
+ *     calls are ordered by the per-communicator rounds); saved is per layer. */
 lina_status lina_moe_workspace_size(const lina_comm* comm, const lina_moe_desc* desc,
                                     size_t* workspace_bytes, size_t* saved_bytes);
 
@@ -296,12 +307,24 @@ lina_status lina_moe_backward(lina_comm* comm, const lina_moe_desc* desc, const 
  *   P:905) with max_per_device; else used as given (e.g. an estimate-based
  *   plan, phase one).  plan_out (nullable, host arrays caller-allocated) gets the
  *   plan used.  Dropless top-k (capacity ignored, R5).  Synchronises the host
- *   once (H9).  Output equals lina_moe_forward's with a static placement (P9). */
+ *   once (H9).  Output equals lina_moe_forward's with a static placement (P9).
+ *   A caller-supplied placement is checked entry by entry before use (its tables
+ *   index device buffers): 1 <= replicas[e] <= min(world, max_replicas); replica
+ *   devices in [0, world), distinct per expert, each hosting that expert; hosted ids
+ *   in [-1, E), none twice on a device, each listed among its expert's replica
+ *   devices.  INVALID_ARGUMENT lists every violation. */
 lina_status lina_moe_infer_forward(lina_comm* comm, const lina_moe_desc* desc, const void* tokens,
                                    const float* gate_w, const void* w1_all, const void* w2_all,
                                    void* out, const lina_placement* placement,
                                    int32_t max_per_device, lina_placement* plan_out,
                                    void* workspace, size_t workspace_bytes, lina_stream stream);
+/* Rows moved by the last lina_moe_infer_forward(_two_phase) call on this comm, as the
+ * call's plan computed them (host copies; diagnostics and tests of the replica split,
+ * R14): host_recv_rows[src] = rows this rank received from source rank src over all
+ * its hosted experts; host_sent_rows[dv] = rows this rank sent to device dv.  Arrays
+ * [world], host, caller-allocated, either may be NULL.  Before any inference call both
+ * are zero.  Errors: INVALID_ARGUMENT for a NULL comm. */
+lina_status lina_infer_last_rows(const lina_comm* comm, int32_t* host_recv_rows, int32_t* host_sent_rows);
 /* Two-phase scheduling: as lina_moe_infer_forward with the phase-one
  * `placement` (built before gating from host_estimated [E], e.g. by
  * lina_popprof_estimate + lina_placement_compute), then, once the gate's global
@@ -338,7 +361,13 @@ lina_status lina_sched_config(lina_comm* comm, lina_policy policy, size_t partit
  * micro-op.  Non-blocking. */
 lina_status lina_allreduce_submit(lina_comm* comm, void* grad, size_t count, lina_dtype dtype,
                                   lina_stream ready_stream);
-/* Make `stream` wait until every submitted allreduce has completed. */
+/* Make `stream` wait, on the device, until every allreduce submitted so far has
+ * completed.  Does not block the host: the scheduler thread publishes the wait
+ * point on its stream after the last micro-op (a stream memory write) and `stream`
+ * waits for it (a stream memory wait), so the caller may enqueue further work at
+ * once.  Not capturable in a CUDA graph (the micro-ops are issued later by the
+ * scheduler thread).  An error of the scheduler thread surfaces here or at
+ * lina_comm_check. */
 lina_status lina_allreduce_wait(lina_comm* comm, lina_stream stream);
 /* Scheduler statistics since the last call: micro-ops issued, micro-ops that
  * were deferred because an all-to-all was queued/in flight. */
@@ -354,6 +383,11 @@ typedef struct {
   double gemm_ms;          /* device time of the expert-GEMM phases (CUDA events recorded on the
                               compute stream around each phase, after its all-to-all waits) */
   int64_t gemm_phases;     /* number of timed phases summed into gemm_ms                  */
+  double a2a_window_ms;    /* fused transport: summed all-to-all windows of the passes (first
+                              mover launched on its stream .. last micro-op of the pass landed) */
+  double gemm_in_a2a_ms;   /* expert-GEMM phase time inside those windows: / a2a_window_ms = the
+                              paper's pipelining efficiency                            */
+  int64_t a2a_windows;     /* number of windows summed                                      */
 } lina_profile;
 
 /* Bit flags: 1 = record timing events around the expert-GEMM phases of every forward /

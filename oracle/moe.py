@@ -160,12 +160,13 @@ def moe_forward(Xs, Wg, W1, W2, k: int, capacity: int, dtype: str):
         outs.append(RankForward(L=L, p=p, idx=idx, gate=g, slot=slot, counts=counts,
                                 y=np.zeros_like(X)))
     # Experts: each kept (rank, t, j) row goes to expert idx[t,j] (the dispatch all-to-all).
+    X64 = [np.asarray(X, np.float64) for X in Xs]   # (once: a row of a per-row copy pins the copy)
     for e in range(E):
         rows = [(r, t, j) for r, fw in enumerate(outs)
                 for t, j in zip(*np.nonzero((fw.idx == e) & (fw.slot >= 0)))]
         if not rows:
             continue
-        x = np.stack([np.asarray(Xs[r], np.float64)[t] for r, t, _ in rows])
+        x = np.stack([X64[r][t] for r, t, _ in rows])
         h, o = expert_ffn(x, W1[e], W2[e], dtype)
         for n, (r, t, j) in enumerate(rows):
             outs[r].h[(int(t), int(j))] = h[n]
@@ -222,6 +223,7 @@ def moe_backward(fw_outs, Xs, dYs, Wg, W1, W2, k: int, dtype: str) -> Backward:
             dO[r][(t, j)] = round_to(fw.gate[t, j] * dY[t], dtype)
         dgs.append(round_to(dg, "f64" if dtype == "f64" else "f32"))
     # (c) experts: dH = (dO · W2e) ∘ 1[h > 0], dXe = dH · W1e, dW2e = Σ dOᵀ h, dW1e = Σ dHᵀ x
+    X64 = [np.asarray(X, np.float64) for X in Xs]
     for e in range(E):
         keys = [(r, t, j) for r, fw in enumerate(fw_outs) for (t, j) in fw.o
                 if fw.idx[t, j] == e]
@@ -229,7 +231,7 @@ def moe_backward(fw_outs, Xs, dYs, Wg, W1, W2, k: int, dtype: str) -> Backward:
             continue
         do = np.stack([dO[r][(t, j)] for r, t, j in keys])
         h = np.stack([fw_outs[r].h[(t, j)] for r, t, j in keys])
-        x = np.stack([np.asarray(Xs[r], np.float64)[t] for r, t, _ in keys])
+        x = np.stack([X64[r][t] for r, t, _ in keys])
         dh = round_to((do @ W2[e]) * (h > 0), dtype)          # relu'(0) = 0 (R8)
         dxe = round_to(dh @ W1[e], dtype)
         dW2[e] += do.T @ h

@@ -6,11 +6,11 @@ PAPER.md §5.2 (A17, A20, D4):
   "In the profiling stage, we collect the expert selection results of all tokens ...
   We then group tokens that select the same experts from layer i-l to layer i, which
   represent a unique sample path of experts used.  For each sample path j, we compute
-  the expert popularity distribution Ψ_j^{i+1} for layer i+1" (P:433-436).
+  the expert popularity distribution Ψ_j^{i+1} for layer i+1" (P:429-430).
   "In each layer i, for a sample path j, we pick the top-k expert(s) of the subsequent
   layer from Ψ_j^{i+1} and use their probabilities {P_j^{i+1}(e)} to represent expert
-  popularity" (P:455-456); Eq. (1) then uses "Σ_{t=1}^{N_t} P^{i+1}_{j(t)}(e)/N_t"
-  as the overall popularity of expert e (P:466-471).
+  popularity" (P:462-463); Eq. (1) then uses "Σ_{t=1}^{N_t} P^{i+1}_{j(t)}(e)/N_t"
+  as the overall popularity of expert e (P:473-476).
   Phase two: "comparing the overall top-2k experts.  If the two lists are identical, no
   fine-tuning is needed ... Otherwise, the scheduler re-computes the resource
   allocation with the actual expert popularity".
@@ -50,7 +50,7 @@ class Profile:
         self.marg: dict = {}
 
     def add_trace(self, sel):
-        """'collect the expert selection results of all tokens' (P:432-433): sel[t][i][:k]."""
+        """'collect the expert selection results of all tokens' (P:428): sel[t][i][:k]."""
         for t in range(len(sel)):
             elems = [path_element(sel[t][i]) for i in range(self.L)]
             for m in range(self.L):
@@ -79,7 +79,7 @@ def top_k(counts, k: int) -> list:
 
 
 def estimate(profile: Profile, m: int, histories):
-    """Phase-one estimate of layer m's expert popularity for a batch (P:455-471).
+    """Phase-one estimate of layer m's expert popularity for a batch (P:461-476).
 
     histories[t] = token t's selections at layers m-l .. m-1.  Returns (popularity[E],
     per-token top-k lists; [] for a token with no distribution)."""

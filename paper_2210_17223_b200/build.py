@@ -31,16 +31,6 @@ def nccl_dir() -> str:
     return base
 
 
-def _cutlass_include() -> str | None:
-    try:
-        import flashinfer  # noqa: F401  (header tree only; no flashinfer code is linked)
-        base = os.path.dirname(flashinfer.__file__)
-        inc = os.path.join(base, "data", "cutlass", "include")
-        return inc if os.path.isdir(inc) else None
-    except Exception:
-        return None
-
-
 def _flags():
     nd = nccl_dir()
     inc = ["-I" + os.path.join(nd, "include"), "-I" + CSRC, "-I" + os.path.join(ROOT, "include")]

@@ -42,6 +42,18 @@ void prof_begin(lina_comm* cm, cudaStream_t s) {
   LINA_CUDA_CHECK(cudaEventRecord(a, s));
   cm->prof_gemm.push_back({a, nullptr});
 }
+void prof_a2a_begin(lina_comm* cm, cudaStream_t s) {
+  if (!cm->prof) return;
+  cudaEvent_t a = prof_event(cm);
+  LINA_CUDA_CHECK(cudaEventRecord(a, s));
+  cm->prof_a2a.push_back({a, nullptr});
+}
+void prof_a2a_end(lina_comm* cm, cudaStream_t s) {
+  if (!cm->prof || cm->prof_a2a.empty() || cm->prof_a2a.back().second) return;
+  cudaEvent_t b = prof_event(cm);
+  LINA_CUDA_CHECK(cudaEventRecord(b, s));
+  cm->prof_a2a.back().second = b;
+}
 void prof_end(lina_comm* cm, cudaStream_t s, int gemm_launches) {
   if (!cm->prof || cm->prof_gemm.empty() || cm->prof_gemm.back().second) return;
   cudaEvent_t b = prof_event(cm);
@@ -109,6 +121,58 @@ void validate_desc(const lina_moe_desc* d, int world, bool static_placement) {
     os << "invalid lina_moe_desc:";
     for (auto& s : v) os << " [" << s << "]";
     throw ArgError{os.str()};
+  }
+}
+
+// Contents of a caller-supplied placement (the tables index device buffers, so every
+// entry is checked): 1 <= r_e <= min(N, max_replicas); replica devices in [0, N), distinct
+// per expert, each hosting that expert; hosted ids in [-1, E), no expert twice per device,
+// and every hosted expert listed among its replicas.
+void validate_placement_tables(const lina_placement& pl, int E, int N, std::vector<std::string>& v) {
+  const int mr = pl.max_replicas, mpd = pl.max_per_device;
+  auto hosts = [&](int dv, int e) {
+    for (int i = 0; i < mpd; ++i)
+      if (pl.hosted[(size_t)dv * mpd + i] == e) return true;
+    return false;
+  };
+  for (int e = 0; e < E; ++e) {
+    const int r = pl.replicas[e];
+    const std::string ex = "expert " + std::to_string(e);
+    if (r < 1 || r > N || r > mr) {
+      v.push_back(ex + ": replicas " + std::to_string(r) + " not in [1, min(num_devices, max_replicas)]");
+      continue;
+    }
+    for (int i = 0; i < r; ++i) {
+      const int dv = pl.replica_device[(size_t)e * mr + i];
+      if (dv < 0 || dv >= N) {
+        v.push_back(ex + ": replica device " + std::to_string(dv) + " not in [0, num_devices)");
+        continue;
+      }
+      for (int j = 0; j < i; ++j)
+        if (pl.replica_device[(size_t)e * mr + j] == dv) v.push_back(ex + ": device " + std::to_string(dv) + " listed twice");
+      if (!hosts(dv, e)) v.push_back(ex + ": replica device " + std::to_string(dv) + " does not host it");
+    }
+  }
+  for (int dv = 0; dv < N; ++dv)
+    for (int i = 0; i < mpd; ++i) {
+      const int e = pl.hosted[(size_t)dv * mpd + i];
+      const std::string at = "hosted[" + std::to_string(dv) + "][" + std::to_string(i) + "]";
+      if (e < -1 || e >= E) {
+        v.push_back(at + " = " + std::to_string(e) + " not in [-1, num_experts)");
+        continue;
+      }
+      if (e < 0) continue;
+      for (int j = 0; j < i; ++j)
+        if (pl.hosted[(size_t)dv * mpd + j] == e) v.push_back(at + ": expert " + std::to_string(e) + " twice");
+      bool listed = false;
+      const int r = std::max(0, std::min(pl.replicas[e], mr));
+      for (int q = 0; q < r; ++q) listed |= pl.replica_device[(size_t)e * mr + q] == dv;
+      if (!listed) v.push_back(at + ": expert " + std::to_string(e) + " not among its replica devices");
+    }
+  if (v.size() > 16) {  // keep the message readable; the count says how many there were
+    const size_t n = v.size();
+    v.resize(16);
+    v.push_back("... " + std::to_string(n - 16) + " more");
   }
 }
 
@@ -239,6 +303,7 @@ lina_status lina_comm_check(lina_comm* cm) {
   return guarded([&] {
     if (!cm) throw ArgError{"comm is NULL"};
     LINA_CUDA_CHECK(cudaPeekAtLastError());
+    if (cm->sched) sched_check(cm->sched);
     for (ncclComm_t c : {cm->ep_disp, cm->ep_comb, cm->dp}) {
       if (!c) continue;
       ncclResult_t r = ncclSuccess;
@@ -529,6 +594,7 @@ static lina_status infer_entry(lina_comm* cm, const lina_moe_desc* desc, const v
       need(v, placement->replicas, "placement->replicas");
       need(v, placement->replica_device, "placement->replica_device");
       need(v, placement->hosted, "placement->hosted");
+      if (v.empty()) validate_placement_tables(*placement, desc->num_experts, cm->world, v);
     }
     if (plan_out) {
       need(v, plan_out->replicas, "plan_out->replicas");
@@ -578,6 +644,17 @@ lina_status lina_moe_infer_forward_two_phase(lina_comm* cm, const lina_moe_desc*
   return infer_entry(cm, desc, tokens, gate_w, w1_all, w2_all, out, placement, placement->max_per_device,
                      plan_out, workspace, workspace_bytes, stream, estimated, replanned,
                      "lina_moe_infer_forward_two_phase");
+}
+
+lina_status lina_infer_last_rows(const lina_comm* cm, int32_t* recv_rows, int32_t* sent_rows) {
+  return guarded([&] {
+    if (!cm) throw ArgError{"comm is NULL"};
+    for (int r = 0; r < cm->world; ++r) {
+      if (recv_rows) recv_rows[r] = r < (int)cm->inf_recv_rows.size() ? cm->inf_recv_rows[r] : 0;
+      if (sent_rows) sent_rows[r] = r < (int)cm->inf_sent_rows.size() ? cm->inf_sent_rows[r] : 0;
+    }
+    return LINA_OK;
+  });
 }
 
 lina_status lina_sched_config(lina_comm* cm, lina_policy policy, size_t partition_bytes) {
@@ -631,22 +708,50 @@ lina_status lina_profile_read(lina_comm* cm, lina_profile* out) {
     if (!out) throw ArgError{"out is NULL"};
     double ms = 0.0;
     int64_t phases = 0;
+    // timestamps relative to one reference event (all events are on this device)
+    cudaEvent_t ref = !cm->prof_gemm.empty() ? cm->prof_gemm.front().first
+                                             : (!cm->prof_a2a.empty() ? cm->prof_a2a.front().first : nullptr);
+    auto at = [&](cudaEvent_t e) {
+      float t = 0.f;
+      LINA_CUDA_CHECK(cudaEventSynchronize(e));
+      LINA_CUDA_CHECK(cudaEventElapsedTime(&t, ref, e));
+      return (double)t;
+    };
+    std::vector<std::pair<double, double>> gemm_iv;
     for (auto& pr : cm->prof_gemm) {
       if (pr.second) {
-        LINA_CUDA_CHECK(cudaEventSynchronize(pr.second));
-        float t = 0.f;
-        LINA_CUDA_CHECK(cudaEventElapsedTime(&t, pr.first, pr.second));
-        ms += t;
+        const double a = at(pr.first), b = at(pr.second);
+        ms += b - a;
+        gemm_iv.push_back({a, b});
         ++phases;
-        cm->prof_pool.push_back(pr.second);
       }
-      cm->prof_pool.push_back(pr.first);
     }
-    cm->prof_gemm.clear();
+    // all-to-all windows of the fused passes and the expert-GEMM time inside them (the
+    // paper's pipelining efficiency: non-idle time of the computation stream
+    // during the all-to-all)
+    double win = 0.0, busy = 0.0;
+    int64_t nwin = 0;
+    for (auto& pr : cm->prof_a2a) {
+      if (!pr.second) continue;
+      const double a = at(pr.first), b = at(pr.second);
+      win += b - a;
+      ++nwin;
+      for (auto& g : gemm_iv) busy += std::max(0.0, std::min(b, g.second) - std::max(a, g.first));
+    }
+    for (auto* v : {&cm->prof_gemm, &cm->prof_a2a}) {
+      for (auto& pr : *v) {
+        if (pr.second) cm->prof_pool.push_back(pr.second);
+        cm->prof_pool.push_back(pr.first);
+      }
+      v->clear();
+    }
     out->kernel_launches = g_launches.exchange(0);
     out->gemm_launches = cm->prof_gemm_launches;
     out->gemm_ms = ms;
     out->gemm_phases = phases;
+    out->a2a_window_ms = win;
+    out->gemm_in_a2a_ms = busy;
+    out->a2a_windows = nwin;
     cm->prof_gemm_launches = 0;
     return LINA_OK;
   });

@@ -28,6 +28,7 @@ namespace lina {
 typedef CUresult (*WaitValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*WriteValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+typedef CUresult (*PtrAttrFn)(void*, CUpointer_attribute, CUdeviceptr);
 
 static void* entry(const char* name) {
   void* f = nullptr;
@@ -42,26 +43,45 @@ struct CeTransport::Impl {
   WaitValueFn wait_fn = nullptr;
   WriteValueFn write_fn = nullptr;
   AddrRangeFn range_fn = nullptr;
+  PtrAttrFn attr_fn = nullptr;
   // IPC-opened peer allocation bases, keyed by (rank, handle bytes)
   std::map<std::pair<int, std::string>, char*> opened;
-  // mapped peer pointers for a local pointer
-  std::map<const void*, std::vector<char*>> maps;
-  // device copies of peer pointer arrays
-  std::map<std::pair<const void*, size_t>, void*> ptr_arrays;
+  // mapped peer pointers for a local pointer, with the allocation's buffer id and the
+  // mapping generation
+  struct Mapping {
+    unsigned long long buffer_id = 0;
+    uint64_t gen = 0;
+    std::vector<char*> ptrs;
+  };
+  std::map<const void*, Mapping> maps;
+  uint64_t next_gen = 0;
+  // device copies of peer pointer arrays (with the generation they were built from)
+  std::map<std::pair<const void*, size_t>, std::pair<void*, uint64_t>> ptr_arrays;
+  unsigned long long buffer_id(const void* p) const {
+    unsigned long long id = 0;
+    if (attr_fn(&id, CU_POINTER_ATTRIBUTE_BUFFER_ID, (CUdeviceptr)p) != CUDA_SUCCESS)
+      throw CudaError{"cuPointerGetAttribute(BUFFER_ID) failed: not a device allocation"};
+    return id;
+  }
   void* stage = nullptr;  // device staging for handle exchange
 };
 
-void* const* CeTransport::dev_ptrs(const void* local, size_t offset, cudaStream_t s) {
+void* const* CeTransport::dev_ptrs(const void* local, size_t offset, cudaStream_t s, uint64_t layout_key) {
+  const auto& pr = peers(local, s, layout_key);  // (re-)maps first if the allocation changed
+  const uint64_t gen = generation(local);
   auto key = std::make_pair(local, offset);
   auto it = impl_->ptr_arrays.find(key);
-  if (it != impl_->ptr_arrays.end()) return (void* const*)it->second;
-  const auto& pr = peers(local, s);
+  if (it != impl_->ptr_arrays.end()) {
+    if (it->second.second == gen) return (void* const*)it->second.first;
+    LINA_CUDA_CHECK(cudaFree(it->second.first));  // built from a stale mapping
+    impl_->ptr_arrays.erase(it);
+  }
   std::vector<char*> v(pr.size());
   for (size_t i = 0; i < pr.size(); ++i) v[i] = pr[i] + offset;
   void* d = nullptr;
   LINA_CUDA_CHECK(cudaMalloc(&d, sizeof(char*) * v.size()));
   LINA_CUDA_CHECK(cudaMemcpy(d, v.data(), sizeof(char*) * v.size(), cudaMemcpyHostToDevice));
-  impl_->ptr_arrays[key] = d;
+  impl_->ptr_arrays[key] = {d, gen};
   return (void* const*)d;
 }
 
@@ -69,7 +89,8 @@ CeTransport::CeTransport(lina_comm* cm) : cm_(cm), impl_(new Impl) {
   impl_->wait_fn = (WaitValueFn)entry("cuStreamWaitValue32");
   impl_->write_fn = (WriteValueFn)entry("cuStreamWriteValue32");
   impl_->range_fn = (AddrRangeFn)entry("cuMemGetAddressRange");
-  if (!impl_->wait_fn || !impl_->write_fn || !impl_->range_fn)
+  impl_->attr_fn = (PtrAttrFn)entry("cuPointerGetAttribute");
+  if (!impl_->wait_fn || !impl_->write_fn || !impl_->range_fn || !impl_->attr_fn)
     throw StatusError{LINA_ERR_UNSUPPORTED, "stream memory operations not available"};
   const int P = cm->world;
   nflags_ = (size_t)kKinds * P * kMaxChunks;
@@ -81,7 +102,7 @@ CeTransport::CeTransport(lina_comm* cm) : cm_(cm), impl_(new Impl) {
   LINA_CUDA_CHECK(cudaMalloc(&rounds_, 3 * sizeof(uint32_t)));
   LINA_CUDA_CHECK(cudaMemset(rounds_, 0, 3 * sizeof(uint32_t)));
   peer_slots_.assign(kKinds, nullptr);
-  peer_flags_ = map_collective(flags_, cm->hi);
+  peer_flags_ = map_collective(flags_, cm->hi, 0);
   for (int r = 0; r < P; ++r) {
     cudaStream_t a, b;
     int lo_prio = 0, hi_prio = 0;
@@ -98,7 +119,7 @@ CeTransport::CeTransport(lina_comm* cm) : cm_(cm), impl_(new Impl) {
 CeTransport::~CeTransport() {
   cudaDeviceSynchronize();
   for (auto& kv : impl_->opened) cudaIpcCloseMemHandle(kv.second);
-  for (auto& kv : impl_->ptr_arrays) cudaFree(kv.second);
+  for (auto& kv : impl_->ptr_arrays) cudaFree(kv.second.first);
   for (auto s : disp_) cudaStreamDestroy(s);
   for (auto s : comb_) cudaStreamDestroy(s);
   for (auto e : events_) cudaEventDestroy(e);
@@ -111,9 +132,9 @@ CeTransport::~CeTransport() {
   delete impl_;
 }
 
-// Exchange (IPC handle, offset) of `local` with every rank (NCCL allgather on the
-// dispatch communicator, blocking) and return each rank's pointer mapped here.
-std::vector<char*> CeTransport::map_collective(const void* local, cudaStream_t s) {
+// Exchange (IPC handle, offset, layout key) of `local` with every rank (NCCL allgather on
+// the dispatch communicator, blocking) and return each rank's pointer mapped here.
+std::vector<char*> CeTransport::map_collective(const void* local, cudaStream_t s, uint64_t layout_key) {
   const int P = cm_->world;
   CUdeviceptr base = 0;
   size_t size = 0;
@@ -126,12 +147,25 @@ std::vector<char*> CeTransport::map_collective(const void* local, cudaStream_t s
   std::memcpy(rec, &h, sizeof(h));
   const uint64_t off = (uint64_t)((const char*)local - (const char*)base);
   std::memcpy(rec + 64, &off, 8);
+  std::memcpy(rec + 72, &layout_key, 8);
   char* st = (char*)impl_->stage;
   LINA_CUDA_CHECK(cudaMemcpyAsync(st + 128 * (size_t)cm_->rank, rec, 128, cudaMemcpyHostToDevice, s));
   LINA_NCCL_CHECK(ncclAllGather(st + 128 * (size_t)cm_->rank, st, 128, ncclUint8, cm_->ep_disp, s));
   std::vector<unsigned char> all((size_t)128 * P);
   LINA_CUDA_CHECK(cudaMemcpyAsync(all.data(), st, all.size(), cudaMemcpyDeviceToHost, s));
   LINA_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (layout_key) {  // every rank sees the same records, so every rank throws or none does
+    std::string bad;
+    for (int r = 0; r < P; ++r) {
+      uint64_t kr = 0;
+      std::memcpy(&kr, all.data() + 128 * (size_t)r + 72, 8);
+      if (kr != layout_key) bad += " " + std::to_string(r);
+    }
+    if (!bad.empty())
+      throw ArgError{"peer-visible buffer layout differs on rank(s)" + bad +
+                     ": capacity, n_chunks, num_experts, d_model, d_ffn, k and dtype must be equal on every "
+                     "rank (inference: num_tokens too)"};
+  }
   std::vector<char*> out(P, nullptr);
   for (int r = 0; r < P; ++r) {
     if (r == cm_->rank) {
@@ -158,10 +192,20 @@ std::vector<char*> CeTransport::map_collective(const void* local, cudaStream_t s
   return out;
 }
 
-const std::vector<char*>& CeTransport::peers(const void* local, cudaStream_t s) {
+const std::vector<char*>& CeTransport::peers(const void* local, cudaStream_t s, uint64_t layout_key) {
+  const unsigned long long id = impl_->buffer_id(local);
   auto it = impl_->maps.find(local);
-  if (it != impl_->maps.end()) return it->second;
-  return impl_->maps[local] = map_collective(local, s);
+  if (it != impl_->maps.end() && it->second.buffer_id == id) return it->second.ptrs;
+  Impl::Mapping m;
+  m.ptrs = map_collective(local, s, layout_key);
+  m.buffer_id = id;
+  m.gen = ++impl_->next_gen;
+  return (impl_->maps[local] = std::move(m)).ptrs;
+}
+
+uint64_t CeTransport::generation(const void* local) const {
+  auto it = impl_->maps.find(local);
+  return it == impl_->maps.end() ? 0 : it->second.gen;
 }
 
 uint32_t* const* CeTransport::peer_slots(int kind) {

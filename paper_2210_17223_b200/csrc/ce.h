@@ -23,14 +23,21 @@ class CeTransport {
   explicit CeTransport(lina_comm* cm);  // collective (allgathers the flag-array handles)
   ~CeTransport();
   // Every rank's copy of `local` (same offset in its own buffer), mapped into this
-  // process; collective on the first call for a pointer, cached afterwards.
-  const std::vector<char*>& peers(const void* local, cudaStream_t s);
+  // process; collective on the first call for an allocation, cached afterwards.  The
+  // cache is keyed by the pointer AND the allocation's process-wide buffer id, so a
+  // buffer freed and re-allocated at the same address is mapped again (collectively:
+  // every rank passes its new buffers in the same call, as an SPMD program does) instead
+  // of reusing a stale peer mapping.  layout_key != 0: every rank must map this buffer
+  // with the same key (a hash of the peer-visible layout), else ArgError on every rank.
+  const std::vector<char*>& peers(const void* local, cudaStream_t s, uint64_t layout_key = 0);
+  // Mapping generation of `local` (changes whenever peers() re-maps it; 0 = unmapped).
+  uint64_t generation(const void* local) const;
   // Stream `s` waits until my flag (kind, peer, chunk) >= value.
   void wait_flag(cudaStream_t s, int kind, int peer, int chunk, uint32_t value);
   // Stream `s` writes `value` into rank `rank`'s flag (kind, peer, chunk).
   void post_flag(cudaStream_t s, int rank, int kind, int peer, int chunk, uint32_t value);
   // Device array of the P pointers peers(local)[r] + offset (cached; uploaded once).
-  void* const* dev_ptrs(const void* local, size_t offset, cudaStream_t s);
+  void* const* dev_ptrs(const void* local, size_t offset, cudaStream_t s, uint64_t layout_key = 0);
   // In-kernel signalling (signal.h): my slots of `kind` (peer r at r * kMaxChunks), the
   // device array [P] of every rank's slot (kind, me) mapped here (uploaded once), and a
   // zeroed CTA-completion counter per call site (sites < kDoneSites).
@@ -58,7 +65,7 @@ class CeTransport {
   size_t slot(int kind, int peer, int chunk) const {
     return ((size_t)kind * cm_->world + peer) * kMaxChunks + chunk;
   }
-  std::vector<char*> map_collective(const void* local, cudaStream_t s);
+  std::vector<char*> map_collective(const void* local, cudaStream_t s, uint64_t layout_key);
   lina_comm* cm_;
   struct Impl;
   Impl* impl_;

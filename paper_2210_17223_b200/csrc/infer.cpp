@@ -39,6 +39,7 @@ struct InferPlan {
   size_t Cmax;
   size_t o_probs, o_idx, o_gate, o_slot, o_counts, o_kept, o_tokof, o_route, o_all, o_tab, o_vc,
       o_mtp, o_gvc, o_segx, o_blk, o_arow, o_send, o_recv, o_gin, o_h, o_o, o_back2, o_back, total;
+  uint64_t peer_key;
   size_t tab_ints() const { return (size_t)E + (size_t)E * P + (size_t)P * E + E; }
 };
 
@@ -62,6 +63,9 @@ static InferPlan infer_plan(const lina_moe_desc& dsc, int P, int mpd) {
     o = al(o + b);
     return at;
   };
+  // peer-written regions first (a rank stores into a peer's workspace at its own offsets)
+  q.o_recv = take((size_t)P * Tk * q.d * q.dt);          // source-major receive       [peer-written]
+  q.o_back = take(Tk * q.d * q.dt);                      // returned rows               [peer-written]
   q.o_probs = take(4 * (size_t)q.T * q.E);
   q.o_idx = take(4 * Tk);
   q.o_gate = take(4 * Tk);
@@ -79,13 +83,16 @@ static InferPlan infer_plan(const lina_moe_desc& dsc, int P, int mpd) {
   q.o_blk = take(4 * 6 * (size_t)P);        // fused exchange: {src_row, dst_row, rows} per peer, both ways
   q.o_arow = take(4 * Tk);
   q.o_send = take(Tk * q.d * q.dt);
-  q.o_recv = take((size_t)P * Tk * q.d * q.dt);          // source-major receive
   q.o_gin = take((size_t)mpd * q.Cmax * q.d * q.dt);     // expert-major GEMM input
   q.o_h = take((size_t)mpd * q.Cmax * q.f * q.dt);
   q.o_o = take((size_t)mpd * q.Cmax * q.d * q.dt);
   q.o_back2 = take((size_t)P * Tk * q.d * q.dt);         // outputs regrouped source-major
-  q.o_back = take(Tk * q.d * q.dt);
   q.total = o;
+  uint64_t h = 1469598103934665603ull;  // FNV-1a of the peer-visible geometry
+  for (uint64_t v : {(uint64_t)q.T, (uint64_t)q.k, (uint64_t)q.E, (uint64_t)q.d, (uint64_t)q.dt, (uint64_t)P,
+                     (uint64_t)q.o_recv, (uint64_t)q.o_back, (uint64_t)0x1f})
+    for (int b = 0; b < 8; ++b) h = (h ^ ((v >> (8 * b)) & 0xff)) * 1099511628211ull;
+  q.peer_key = h | 1;
   return q;
 }
 
@@ -184,6 +191,16 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   LINA_CUDA_CHECK(cudaMemcpyAsync(host, allc, 4 * (size_t)P * E, cudaMemcpyDeviceToHost, s));
   LINA_CUDA_CHECK(cudaStreamSynchronize(s));
   std::vector<int> cnt(host, host + (size_t)P * E);  // cnt[src*E + e]
+  {  // dropless: every source sends T·k rows; the receive regions are sized for equal T
+    std::string bad;
+    for (int src = 0; src < P; ++src) {
+      long long tot = 0;
+      for (int e = 0; e < E; ++e) tot += cnt[(size_t)src * E + e];
+      if (tot != (long long)T * k) bad += " " + std::to_string(src);
+    }
+    if (!bad.empty())  // every rank sees the same counts: all of them raise
+      throw ArgError{"inference needs num_tokens equal on every rank; rank(s)" + bad + " differ"};
+  }
 
   // ---- the plan (identical on every rank).  Phase two: a phase-one plan
   // whose estimated top-2k experts differ from the actual ones is re-computed below.
@@ -274,6 +291,8 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
         const int e = hosted[(size_t)dv * mpd + i];
         if (e >= 0) cnt_sd[(size_t)src * P + dv] += tokens_to(src, e, dv);
       }
+  cm->inf_recv_rows.assign(src_cnt.begin(), src_cnt.end());
+  cm->inf_sent_rows.assign(dv_cnt.begin(), dv_cnt.end());
   int maxrows = 0;
   for (int h = 0; h < mpd; ++h) maxrows = std::max(maxrows, tot[h]);
   const int Cm = std::max(128, (maxrows + 127) / 128 * 128);
@@ -327,7 +346,7 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   trace_mark(cm, s, "inf:permute");
   // one message per peer: my block for device dv -> its source-major receive block
   if (ce) {  // peer stores (after the owners' FREE; READY when every block has landed)
-    void* const* peer_recv = ce->dev_ptrs(ws, q.o_recv, s);
+    void* const* peer_recv = ce->dev_ptrs(ws, q.o_recv, s, q.peer_key);
     launch_sig_wait(isig(CeTransport::kIFreeD, -1, -1, nullptr), s);
     launch_push_blocks(dtype, send, peer_recv, blk, P, d, maxblk, isig(-1, CeTransport::kIReadyD, 6, nullptr), s);
     launch_sig_wait(isig(CeTransport::kIReadyD, -1, -1, nullptr), s);
@@ -376,7 +395,7 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   // ---- second all-to-all (expert outputs back to their sources, one message per peer)
   launch_regroup(dtype, obuf, back2, vc, P, mpd, Cm, d, maxseg, false, s);
   if (ce) {  // the rows go back by peer stores; the last wait also closes this call's round
-    void* const* peer_back = ce->dev_ptrs(ws, q.o_back, s);
+    void* const* peer_back = ce->dev_ptrs(ws, q.o_back, s, q.peer_key);
     launch_sig_wait(isig(CeTransport::kIFreeC, -1, -1, nullptr), s);
     launch_push_blocks(dtype, back2, peer_back, blk + 3 * P, P, d, maxblk, isig(-1, CeTransport::kIReadyC, 7, nullptr),
                        s);

@@ -51,6 +51,7 @@ struct Plan {
   // offsets into `workspace`
   size_t w_route, w_D, w_O, w_dg, w_dwg, w_dS, w_dO, w_dH, w_dXe, w_dXs;
   size_t ws_bytes;
+  uint64_t peer_key;  // hash of the peer-visible geometry (checked across ranks on first mapping)
   size_t rows_send() const { return (size_t)n * E * Cm; }
   size_t rows_recv() const { return (size_t)n * P * El * Cm; }
 };
@@ -79,6 +80,7 @@ struct lina_comm {
   bool prof = false;
   int flags = 0;  // lina_profile_enable bits: 1 timing events, 2 skip collectives, 4 collectives only
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_gemm;  // recorded (start, end) pairs
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_a2a;   // all-to-all windows of fused passes
   std::vector<cudaEvent_t> prof_pool;                          // free timing events
   int64_t prof_gemm_launches = 0;
   lina::Trace* trace = nullptr;  // LINA_TRACE=1 phase trace (trace.cpp), diagnostics only
@@ -86,12 +88,17 @@ struct lina_comm {
   // pinned host scratch for the inference control plane (counts D2H, tables H2D)
   int* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // rows of the last inference call (lina_infer_last_rows): [world] each
+  std::vector<int32_t> inf_recv_rows, inf_sent_rows;
 };
 
 namespace lina {
 // Profiling helpers (api.cpp): open/close one timed expert-GEMM phase on stream s.
 void prof_begin(lina_comm* cm, cudaStream_t s);
 void prof_end(lina_comm* cm, cudaStream_t s, int gemm_launches);
+// open/close one all-to-all window of a fused pass (first mover launched .. last micro-op landed)
+void prof_a2a_begin(lina_comm* cm, cudaStream_t s);
+void prof_a2a_end(lina_comm* cm, cudaStream_t s);
 // Phase trace (trace.cpp): no-ops unless the comm was created with LINA_TRACE=1.
 Trace* trace_create();
 void trace_mark(lina_comm* cm, cudaStream_t s, const char* label);

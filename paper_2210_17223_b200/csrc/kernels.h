@@ -108,6 +108,11 @@ void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const 
                              const float* gate, int T, int k, int d, int E, int C, int c0, int nc, int Cm, int El,
                              int P, int me, void* const* peer_rows, float* dg, const PeerSignal& sig,
                              cudaStream_t s);
+// Collectives-only timing (movers.cu): the valid rows of micro-op c's segments of a
+// receive-layout buffer to each owner's send-layout buffer (peer_send_layout[s]), as the
+// peer-storing GEMM epilogue moves them; the last CTA posts sig (READY of micro-op c).
+void launch_push_segments(int dtype, const void* recv_layout, void* const* peer_send_layout, const int* vcount,
+                          int c, int P, int El, int E, int Cm, int me, int d, const PeerSignal& sig, cudaStream_t s);
 // Output tiles of a row GEMM stored through per-owner tensor maps (peer memory):
 // segment (c, s, el) of the receive layout goes to map s at segment c*E + me*El + el.
 struct PeerStore {

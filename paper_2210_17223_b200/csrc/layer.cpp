@@ -61,34 +61,46 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
     o = align_up(o + bytes);
     return at;
   };
+  // Every region a peer writes or reads at this rank's offsets (fused / copy-engine
+  // transports: a rank finds a peer's buffer as the peer's base + ITS OWN offset) comes
+  // first, sized by (C, n_chunks, E, d, dtype, world) only, so ranks may pass different
+  // num_tokens; the peer mapping checks every rank's peer_key (ce.cpp) on first use.
   // ---- saved (forward -> backward)
+  p.s_R = take(recv_rows * p.d * p.dt);                       // routed tokens (X rows)     [peer-written]
+  p.s_C = take(send_rows * p.d * p.dt);                       // returned expert outputs    [peer-written]
+  p.s_recvkept = take(4 * (size_t)p.P * p.El);                // kept counts of each source [peer-written]
+  p.s_kept = take(4 * E);                                     //                            [peer-read, ce]
   p.s_probs = take(4 * T * E);
   p.s_idx = take(4 * T * k);
   p.s_gate = take(4 * T * k);
   p.s_slot = take(4 * T * k);
-  p.s_kept = take(4 * E);
   p.s_tokof = take(4 * E * (size_t)p.C);
-  p.s_recvkept = take(4 * (size_t)p.P * p.El);
   p.s_vcount = take(4 * (size_t)p.n * p.P * p.El);
   p.s_mtp = take(4 * (size_t)p.n * (p.P * p.El + 1));
-  p.s_R = take(recv_rows * p.d * p.dt);                       // routed tokens (X rows)
   p.s_H = take(recv_rows * (size_t)p.f * p.dt);               // relu(X W1ᵀ)
-  p.s_C = take(send_rows * p.d * p.dt);                       // returned expert outputs
   p.s_mask = take(recv_rows * (size_t)((p.f + 63) / 64) * 8);  // ReLU' bits of H
   p.saved_bytes = o;
   // ---- workspace
   o = 0;
+  p.w_dO = (p.P > 1) ? take(recv_rows * p.d * p.dt) : 0;      // (P=1: = dS)                [peer-written]
+  p.w_dXs = (p.P > 1) ? take(send_rows * p.d * p.dt) : 0;     // (P=1: = dXe)               [peer-written]
+  p.w_D = (p.P > 1) ? take(send_rows * p.d * p.dt) : 0;       // send buffer (P=1: = R)     [peer-read, ce]
+  p.w_O = (p.P > 1) ? take(recv_rows * p.d * p.dt) : 0;       // expert outputs (P=1: = C)  [peer-read, ce]
+  p.w_dS = take(send_rows * p.d * p.dt);                      // g·dY rows, send layout     [peer-read, ce]
+  p.w_dXe = take(recv_rows * p.d * p.dt);                     //                            [peer-read, ce]
   p.w_route = take(4 * route_scratch_ints(p.T, p.k, p.E));
-  p.w_D = (p.P > 1) ? take(send_rows * p.d * p.dt) : 0;       // send buffer (P=1: = R)
-  p.w_O = (p.P > 1) ? take(recv_rows * p.d * p.dt) : 0;       // expert outputs (P=1: = C)
   p.w_dg = take(4 * T * k);
   p.w_dwg = take(4 * dwg_scratch_floats(p.T, p.d, p.E));
-  p.w_dS = take(send_rows * p.d * p.dt);                      // g·dY rows, send layout
-  p.w_dO = (p.P > 1) ? take(recv_rows * p.d * p.dt) : 0;      // (P=1: = dS)
   p.w_dH = take(recv_rows * (size_t)p.f * p.dt);
-  p.w_dXe = take(recv_rows * p.d * p.dt);
-  p.w_dXs = (p.P > 1) ? take(send_rows * p.d * p.dt) : 0;     // (P=1: = dXe)
   p.ws_bytes = o;
+  // FNV-1a over the peer-visible geometry (equal on every rank or the mapping fails)
+  uint64_t h = 1469598103934665603ull;
+  for (uint64_t v : {(uint64_t)p.C, (uint64_t)p.n, (uint64_t)p.Cm, (uint64_t)p.E, (uint64_t)p.P, (uint64_t)p.d,
+                     (uint64_t)p.f, (uint64_t)p.dt, (uint64_t)p.s_R, (uint64_t)p.s_C, (uint64_t)p.s_recvkept,
+                     (uint64_t)p.s_kept, (uint64_t)p.w_dO, (uint64_t)p.w_dXs, (uint64_t)p.w_D, (uint64_t)p.w_O,
+                     (uint64_t)p.w_dS, (uint64_t)p.w_dXe})
+    for (int b = 0; b < 8; ++b) h = (h ^ ((v >> (8 * b)) & 0xff)) * 1099511628211ull;
+  p.peer_key = h | 1;
   return p;
 }
 
@@ -191,8 +203,8 @@ void forward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, con
                 void* saved, void* ws, cudaEvent_t e_perm, uint32_t seq, bool compute, cudaStream_t s) {
   CeTransport& ce = *cm->ce;
   const int P = p.P, me = cm->rank, n = p.n, d = p.d;
-  const auto& peer_ws = ce.peers(ws, s);
-  const auto& peer_saved = ce.peers(saved, s);
+  const auto& peer_ws = ce.peers(ws, s, p.peer_key);
+  const auto& peer_saved = ce.peers(saved, s, p.peer_key);
   for (int src = 0; src < P; ++src) {
     cudaStream_t st = ce.disp_stream(src);
     LINA_CUDA_CHECK(cudaStreamWaitEvent(st, e_perm, 0));
@@ -249,7 +261,7 @@ void backward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, co
                  cudaStream_t s) {
   CeTransport& ce = *cm->ce;
   const int P = p.P, me = cm->rank, n = p.n, d = p.d;
-  const auto& peer_ws = ce.peers(ws, s);
+  const auto& peer_ws = ce.peers(ws, s, p.peer_key);
   if (cm->sched) sched_a2a_begin(cm, s);
   for (int src = 0; src < P; ++src) {
     cudaStream_t st = ce.disp_stream(src);
@@ -367,11 +379,12 @@ PeerSignal chunk_sig(PeerSignal g, int c, int wait_chunks = 1) {
 // Host-side cached per-rank tensor maps of a peer-stored GEMM output.
 PeerStore peer_store(CeTransport& ce, const char* tag, void* buf, size_t off, const Plan& p, int me,
                      std::vector<char*>& bases, cudaStream_t s) {
-  const auto& ps = ce.peers(buf, s);
+  const auto& ps = ce.peers(buf, s, p.peer_key);
   bases.resize(p.P);
   for (int r = 0; r < p.P; ++r) bases[r] = ps[r] + off;
   PeerStore st;
-  const std::string key = std::string(tag) + std::to_string((uintptr_t)buf) + ":" + std::to_string(off) + ":" +
+  const std::string key = std::string(tag) + std::to_string((uintptr_t)buf) + "@" +
+                          std::to_string(ce.generation(buf)) + ":" + std::to_string(off) + ":" +
                           std::to_string(p.Cm) + ":" + std::to_string(p.n * p.E);
   auto it = ce.host_blobs.find(key);
   if (it == ce.host_blobs.end()) it = ce.host_blobs.emplace(key, tc_peer_dmaps(bases, p.d, p.Cm, p.n * p.E)).first;
@@ -425,8 +438,8 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr, q.kept,
                q.tok_of, s, cm->route_sync);
   trace_mark(cm, s, "gate+route");
-  void* const* peer_R = ce.dev_ptrs(saved, p.s_R, s);
-  void* const* peer_cnt = ce.dev_ptrs(saved, p.s_recvkept, s);
+  void* const* peer_R = ce.dev_ptrs(saved, p.s_R, s, p.peer_key);
+  void* const* peer_cnt = ce.dev_ptrs(saved, p.s_recvkept, s, p.peer_key);
   std::vector<char*> cb;
   const PeerStore st = peer_store(ce, "fwdC:", saved, p.s_C, p, me, cb, s);
   // dispatch = permute into the owners' R (after their FREE; READY per micro-op)
@@ -436,6 +449,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
     LINA_CUDA_CHECK(cudaEventRecord(cm->ev[0], s));
     LINA_CUDA_CHECK(cudaStreamWaitEvent(sm, cm->ev[0], 0));
   }
+  prof_a2a_begin(cm, sm);
   launch_sig_wait(wait_only(s_disp), sm);
   for (int c = 0; c < n; ++c)
     launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, c, 1, p.Cm, p.El, P, me, peer_R,
@@ -472,11 +486,11 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   }
   prof_end(cm, s, 2 * n);
   if (n > 1) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, cm->ev[1], 0));  // join the mover stream
-  // combine: block 0 posts the backward FREE (my dO / dXs were last read by the previous
-  // backward); the returned expert outputs of every micro-op have landed (1-CTA wait);
-  // its last CTA closes the forward's round
-  const PeerSignal s_out = make_sig(cm, CT::kFReadyFwdC, rf, 1, CT::kFreeBwd, rf, 1, kSiteFwdEnd, rf);
+  // combine: the returned expert outputs of every micro-op have landed (1-CTA wait); its
+  // last CTA closes the forward's round
+  const PeerSignal s_out = make_sig(cm, CT::kFReadyFwdC, rf, 1, -1, nullptr, 0, kSiteFwdEnd, rf);
   launch_sig_wait(wait_only(chunk_sig(s_out, 0, n)), s);
+  prof_a2a_end(cm, s);
   const PeerSignal s_out2 = no_wait(s_out);
   launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, out, s, &s_out2);
   trace_mark(cm, s, "combine");
@@ -491,18 +505,20 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   uint32_t* rf = ce.round_fwd();  // the last forward's round (closed)
   uint32_t* rb = ce.round_bwd();  // this backward's round is *rb + 1 (closed by the dX kernel)
   trace_mark(cm, s, "bwd:start");
-  void* const* peer_dO = ce.dev_ptrs(ws, p.w_dO, s);
+  void* const* peer_dO = ce.dev_ptrs(ws, p.w_dO, s, p.peer_key);
   std::vector<char*> dxs;
   const PeerStore st = peer_store(ce, "bwdC:", ws, p.w_dXs, p, me, dxs, s);
   if (cm->sched) sched_a2a_imminent(cm);
-  // backward dispatch = combine-backward into the owners' dO (after the FREE they posted
-  // in their forward's combine; READY per micro-op)
-  const PeerSignal s_disp = make_sig(cm, CT::kFreeBwd, rf, 0, CT::kFReadyBwdD, rb, 1, kSiteDispBwd);
+  // backward dispatch = combine-backward into the owners' dO (after the backward FREE they
+  // posted at the end of their previous backward, once its wgrad and dX had read dO and
+  // dXs — so layers sharing one workspace on a comm stay ordered; READY per micro-op)
+  const PeerSignal s_disp = make_sig(cm, CT::kFreeBwd, rb, 0, CT::kFReadyBwdD, rb, 1, kSiteDispBwd);
   cudaStream_t sm = n > 1 ? cm->hi : s;
   if (n > 1) {
     LINA_CUDA_CHECK(cudaEventRecord(cm->ev[2], s));
     LINA_CUDA_CHECK(cudaStreamWaitEvent(sm, cm->ev[2], 0));
   }
+  prof_a2a_begin(cm, sm);
   launch_sig_wait(wait_only(s_disp), sm);
   for (int c = 0; c < n; ++c)
     launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.T, p.k, p.d, p.E, p.C, c, 1, p.Cm, p.El,
@@ -537,10 +553,68 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   trace_mark(cm, s, "dwg");
   const PeerSignal s_back = make_sig(cm, CT::kFReadyBwdC, rb, 1, -1, nullptr, 0, kSiteBwdEnd, rb);
   launch_sig_wait(wait_only(chunk_sig(s_back, 0, n)), s);
+  prof_a2a_end(cm, s);
   const PeerSignal s_back2 = no_wait(s_back);
   launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm,
             dtokens, s, &s_back2);
+  // backward FREE: my dO and dXs have been read (wgrad, dX) — publish the round just closed
+  launch_sig_wait(make_sig(cm, -1, nullptr, 0, CT::kFreeBwd, rb, 0), s);
   trace_mark(cm, s, "dx");
+}
+
+// Collectives-only passes of the fused transport (lina_profile_enable flag 4; SURVEY.md
+// §8(d) T_a2a(n)): the 2n all-to-all micro-ops of a pass with their in-kernel signals and
+// nothing else — the dispatch kernel (permute / combine-backward peer stores, as in the
+// real pass) and, for the return all-to-all that the real pass folds into the GEMM2 /
+// dgrad2 epilogues, a stand-alone mover of the same rows.  Routing (tok_of, kept, gate)
+// is the last real forward's, from `saved`.  All on the caller's stream, in order.
+void forward_fused_movers(lina_comm* cm, const Plan& p, const Ptrs& q, const void* tokens, void* saved,
+                          cudaStream_t s) {
+  using CT = CeTransport;
+  CeTransport& ce = *cm->ce;
+  const int dtype = 1, P = p.P, me = cm->rank, n = p.n;
+  uint32_t* rf = ce.round_fwd();
+  launch_sig_wait(make_sig(cm, -1, nullptr, 0, CT::kFreeFwd, rf, 1), s);  // (the gate kernel posts it normally)
+  void* const* peer_R = ce.dev_ptrs(saved, p.s_R, s, p.peer_key);
+  void* const* peer_cnt = ce.dev_ptrs(saved, p.s_recvkept, s, p.peer_key);
+  void* const* peer_C = ce.dev_ptrs(saved, p.s_C, s, p.peer_key);
+  const PeerSignal s_disp = make_sig(cm, CT::kFreeFwd, rf, 1, CT::kFReadyFwdD, rf, 1, kSiteDispFwd);
+  launch_sig_wait(wait_only(s_disp), s);
+  for (int c = 0; c < n; ++c)
+    launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, c, 1, p.Cm, p.El, P, me, peer_R,
+                        peer_cnt, chunk_sig(no_wait(s_disp), c), s);
+  const PeerSignal s_recv = make_sig(cm, CT::kFReadyFwdD, rf, 1, -1, nullptr, 0);
+  const PeerSignal s_comb = make_sig(cm, -1, nullptr, 0, CT::kFReadyFwdC, rf, 1, kSiteCombFwd);
+  for (int c = 0; c < n; ++c) {
+    launch_sig_wait(wait_only(chunk_sig(s_recv, c)), s);
+    if (c == 0) launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
+    launch_push_segments(dtype, q.O, peer_C, q.vcount, c, P, p.El, p.E, p.Cm, me, p.d, chunk_sig(s_comb, c), s);
+  }
+  // every returned micro-op has landed; close the forward's round
+  launch_sig_wait(chunk_sig(make_sig(cm, CT::kFReadyFwdC, rf, 1, -1, nullptr, 0, -1, rf), 0, n), s);
+}
+
+void backward_fused_movers(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dout, void* ws,
+                           cudaStream_t s) {
+  using CT = CeTransport;
+  CeTransport& ce = *cm->ce;
+  const int dtype = 1, P = p.P, me = cm->rank, n = p.n;
+  uint32_t* rb = ce.round_bwd();
+  void* const* peer_dO = ce.dev_ptrs(ws, p.w_dO, s, p.peer_key);
+  void* const* peer_dXs = ce.dev_ptrs(ws, p.w_dXs, s, p.peer_key);
+  const PeerSignal s_disp = make_sig(cm, CT::kFreeBwd, rb, 0, CT::kFReadyBwdD, rb, 1, kSiteDispBwd);
+  launch_sig_wait(wait_only(s_disp), s);
+  for (int c = 0; c < n; ++c)
+    launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.T, p.k, p.d, p.E, p.C, c, 1, p.Cm, p.El,
+                            P, me, peer_dO, q.dg, chunk_sig(no_wait(s_disp), c), s);
+  const PeerSignal s_recv = make_sig(cm, CT::kFReadyBwdD, rb, 1, -1, nullptr, 0);
+  const PeerSignal s_comb = make_sig(cm, -1, nullptr, 0, CT::kFReadyBwdC, rb, 1, kSiteCombBwd);
+  for (int c = 0; c < n; ++c) {
+    launch_sig_wait(wait_only(chunk_sig(s_recv, c)), s);
+    launch_push_segments(dtype, q.dXe, peer_dXs, q.vcount, c, P, p.El, p.E, p.Cm, me, p.d, chunk_sig(s_comb, c), s);
+  }
+  launch_sig_wait(chunk_sig(make_sig(cm, CT::kFReadyBwdC, rb, 1, -1, nullptr, 0, -1, rb), 0, n), s);
+  launch_sig_wait(make_sig(cm, -1, nullptr, 0, CT::kFreeBwd, rb, 0), s);  // backward FREE
 }
 
 }  // namespace
@@ -556,6 +630,10 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   const bool do_comm = !(cm->flags & 2), do_compute = !(cm->flags & 4);
   if (do_comm && do_compute && fused_ok(cm, p)) {
     forward_fused(cm, p, q, tokens, gate_w, w1, w2, out, saved, ws, route, s);
+    return;
+  }
+  if (!do_compute && fused_ok(cm, p)) {  // collectives only (timing): the fused micro-ops alone
+    forward_fused_movers(cm, p, q, tokens, saved, s);
     return;
   }
   const bool ce = cm->ce && p.P > 1 && do_comm;
@@ -694,6 +772,10 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
   const bool do_comm = !(cm->flags & 2), do_compute = !(cm->flags & 4);
   if (do_comm && do_compute && fused_ok(cm, p)) {
     backward_fused(cm, p, q, dout, tokens, gate_w, w1, w2, dtokens, dgate_w, dw1, dw2, ws, s);
+    return;
+  }
+  if (!do_compute && fused_ok(cm, p)) {
+    backward_fused_movers(cm, p, q, dout, ws, s);
     return;
   }
   const bool ce = cm->ce && p.P > 1 && do_comm;

@@ -112,7 +112,8 @@ Scheduler* sched_create(lina_comm* cm);
 void sched_destroy(Scheduler* s);
 void sched_config(Scheduler* s, lina_policy p, size_t partition_bytes);
 void sched_submit(Scheduler* s, void* grad, size_t count, lina_dtype dt, cudaStream_t ready);
-void sched_wait(Scheduler* s, cudaStream_t st);
+void sched_wait(Scheduler* s, cudaStream_t st);  // device-side wait point, host never blocks
+void sched_check(Scheduler* s);                  // rethrows an error of the scheduler thread
 void sched_stats(Scheduler* s, int64_t* issued, int64_t* deferred);
 
 // Placement (placement.cpp).

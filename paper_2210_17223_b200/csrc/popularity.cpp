@@ -2,10 +2,10 @@
 //
 // "We then group tokens that select the same experts from layer i-l to layer i, which
 // represent a unique sample path of experts used.  For each sample path j, we compute
-// the expert popularity distribution Ψ_j^{i+1} for layer i+1" (P:434-436).  "For a
+// the expert popularity distribution Ψ_j^{i+1} for layer i+1" (P:429-430).  "For a
 // sample path j, we pick the top-k expert(s) of the subsequent layer from Ψ_j^{i+1}
-// and use their probabilities {P_j^{i+1}(e)}" (P:455-456); Eq. (1) aggregates
-// Σ_t P_{j(t)}(e) / N_t (P:466-471).  Phase two compares "the overall top-2k experts"
+// and use their probabilities {P_j^{i+1}(e)}" (P:462-463); Eq. (1) aggregates
+// Σ_t P_{j(t)}(e) / N_t (P:473-476).  Phase two compares "the overall top-2k experts"
 // (P:482-484).  Profiles live in host DRAM as hash maps per layer (paper D4).
 // Readings R19-R22.
 //

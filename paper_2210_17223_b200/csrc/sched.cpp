@@ -25,6 +25,8 @@
 // whole gradients (strict priority, no partitioning) and DEFER = whole
 // gradients issued once the backward all-to-all phase in flight has completed,
 // blind to the next one; reading R23.
+#include <cuda.h>
+
 #include <chrono>
 
 #include "layer.h"
@@ -38,11 +40,29 @@ struct ArJob {
   ncclDataType_t dt;
   cudaEvent_t ready;
   size_t next = 0;   // next element offset to issue
+  uint32_t marker = 0;  // != 0: a lina_allreduce_wait point (no data): publish it on `lo`
 };
+
+typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+static void* driver_fn(const char* name) {
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return f;
+}
 
 class Scheduler {
  public:
-  explicit Scheduler(lina_comm* cm) : cm_(cm) { thread_ = std::thread([this] { run(); }); }
+  explicit Scheduler(lina_comm* cm) : cm_(cm) {
+    wait_fn_ = (StreamValueFn)driver_fn("cuStreamWaitValue32");
+    write_fn_ = (StreamValueFn)driver_fn("cuStreamWriteValue32");
+    if (!wait_fn_ || !write_fn_) throw StatusError{LINA_ERR_UNSUPPORTED, "stream memory operations not available"};
+    LINA_CUDA_CHECK(cudaMalloc(&done_flag_, sizeof(uint32_t)));
+    LINA_CUDA_CHECK(cudaMemset(done_flag_, 0, sizeof(uint32_t)));
+    thread_ = std::thread([this] { run(); });
+  }
   ~Scheduler() {
     {
       std::lock_guard<std::mutex> g(mu_);
@@ -50,8 +70,10 @@ class Scheduler {
     }
     cv_.notify_all();
     thread_.join();
-    for (auto& j : jobs_) cudaEventDestroy(j.ready);
+    for (auto& j : jobs_)
+      if (j.ready) cudaEventDestroy(j.ready);
     for (auto e : a2a_events_) cudaEventDestroy(e);
+    cudaFree(done_flag_);
   }
   void config(lina_policy pol, size_t bytes) {
     std::lock_guard<std::mutex> g(mu_);
@@ -86,21 +108,39 @@ class Scheduler {
     a2a_events_.push_back(e);
     cv_.notify_all();
   }
-  // Block the host until every submitted job is fully issued, then make `s` wait.
+  // Make `s` wait, on the device, for every job submitted so far: a marker job goes
+  // behind them in the queue; when the thread reaches it (every earlier micro-op issued on
+  // `lo`) it writes the marker's value into a device word on `lo` (a stream memory
+  // operation, ordered after those allreduces), and `s` waits for that value.  The host
+  // never blocks, so the caller keeps enqueueing the next step while the allreduce
+  // micro-ops wait for their admission window.
   void wait(cudaStream_t s) {
-    std::unique_lock<std::mutex> g(mu_);
-    cv_.wait(g, [&] { return outstanding_ == 0 || !err_.empty(); });
+    uint32_t target;
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      if (!err_.empty()) {
+        std::string e = err_;
+        err_.clear();
+        throw NcclError{e};
+      }
+      if (outstanding_ == 0) return;  // nothing submitted since the last wait point
+      target = ++wait_target_;
+      ArJob m{};
+      m.marker = target;
+      jobs_.push_back(m);
+    }
+    cv_.notify_all();
+    if (wait_fn_((CUstream)s, (CUdeviceptr)done_flag_, target, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      throw CudaError{"cuStreamWaitValue32 failed"};
+  }
+  // Surface an error of the scheduler thread (lina_comm_check).
+  void check() {
+    std::lock_guard<std::mutex> g(mu_);
     if (!err_.empty()) {
       std::string e = err_;
       err_.clear();
       throw NcclError{e};
     }
-    g.unlock();
-    cudaEvent_t e;
-    LINA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    LINA_CUDA_CHECK(cudaEventRecord(e, cm_->lo));
-    LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e, 0));
-    LINA_CUDA_CHECK(cudaEventDestroy(e));
   }
   void stats(int64_t* issued, int64_t* deferred) {
     std::lock_guard<std::mutex> g(mu_);
@@ -124,7 +164,10 @@ class Scheduler {
   // true while an all-to-all is queued or in flight (LINA / NAIVE admission rule)
   bool a2a_busy_locked() { return a2a_inflight_locked() || imminent_; }
   void run() {
+    // this thread's runtime calls must target the comm's device (not device 0)
+    const cudaError_t de = cudaSetDevice(cm_->device);
     std::unique_lock<std::mutex> g(mu_);
+    if (de != cudaSuccess) err_ = std::string("scheduler thread: cudaSetDevice -> ") + cudaGetErrorString(de);
     while (true) {
       if (stop_) return;
       if (jobs_.empty()) {
@@ -132,6 +175,16 @@ class Scheduler {
         continue;
       }
       ArJob& j = jobs_.front();
+      if (j.marker) {  // every earlier micro-op is on `lo`: publish the wait point after them
+        // (also after an error, so the waiting stream is never left hanging; the error
+        // surfaces at the next wait / lina_comm_check)
+        if (write_fn_((CUstream)cm_->lo, (CUdeviceptr)done_flag_, j.marker, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+            CUDA_SUCCESS)
+          err_ = "cuStreamWriteValue32 failed";
+        jobs_.pop_front();
+        cv_.notify_all();
+        continue;
+      }
       const bool gated = policy_ != LINA_SCHED_BASELINE;
       const bool split = policy_ == LINA_SCHED_LINA;
       bool can_issue = true;
@@ -180,6 +233,9 @@ class Scheduler {
   size_t partition_bytes_ = (size_t)30 << 20;
   bool imminent_ = false, stop_ = false;
   int outstanding_ = 0;
+  uint32_t wait_target_ = 0;
+  uint32_t* done_flag_ = nullptr;  // device word: the last wait point published on `lo`
+  StreamValueFn wait_fn_ = nullptr, write_fn_ = nullptr;
   int64_t issued_ = 0, deferred_ = 0;
   std::string err_;
 };
@@ -191,6 +247,7 @@ void sched_submit(Scheduler* s, void* g, size_t c, lina_dtype dt, cudaStream_t r
   s->submit(g, c, dt, rs);
 }
 void sched_wait(Scheduler* s, cudaStream_t st) { s->wait(st); }
+void sched_check(Scheduler* s) { s->check(); }
 void sched_stats(Scheduler* s, int64_t* i, int64_t* d) { s->stats(i, d); }
 
 void sched_a2a_imminent(lina_comm* cm) {

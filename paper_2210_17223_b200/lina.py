@@ -32,7 +32,7 @@ ABI_SYMBOLS = [
     "lina_allreduce_wait", "lina_sched_stats", "lina_profile_enable", "lina_profile_read",
     "lina_popprof_create", "lina_popprof_destroy", "lina_popprof_add", "lina_popprof_estimate",
     "lina_phase_two_check", "lina_moe_infer_forward_two_phase", "lina_popprof_save", "lina_popprof_load",
-    "lina_popprof_info",
+    "lina_popprof_info", "lina_infer_last_rows",
 ]
 
 
@@ -56,7 +56,9 @@ class Route(ctypes.Structure):
 
 class Profile(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_int64), ("gemm_launches", ctypes.c_int64),
-                ("gemm_ms", ctypes.c_double), ("gemm_phases", ctypes.c_int64)]
+                ("gemm_ms", ctypes.c_double), ("gemm_phases", ctypes.c_int64),
+                ("a2a_window_ms", ctypes.c_double), ("gemm_in_a2a_ms", ctypes.c_double),
+                ("a2a_windows", ctypes.c_int64)]
 
 
 class Placement(ctypes.Structure):
@@ -110,6 +112,7 @@ def load() -> ctypes.CDLL:
         "lina_allreduce_submit": ([vp, vp, sz, i32, vp], i32),
         "lina_allreduce_wait": ([vp, vp], i32),
         "lina_sched_stats": ([vp, P(ctypes.c_int64), P(ctypes.c_int64)], i32),
+        "lina_infer_last_rows": ([vp, P(i32), P(i32)], i32),
         "lina_profile_enable": ([vp, ctypes.c_int], i32),
         "lina_profile_read": ([vp, P(Profile)], i32),
     }
@@ -283,7 +286,7 @@ def lina_replica_split(count: int, replicas: int, source_rank: int) -> list:
 
 
 class PopProfile:
-    """Sample-path popularity profile (lina_popprof_*; PAPER.md §5.2, P:432-458).
+    """Sample-path popularity profile (lina_popprof_*; PAPER.md §5.2, P:428-463).
 
     Host-only: arrays are numpy int32 ([T, L, k] traces, [T, l, k] histories)."""
 
@@ -390,6 +393,14 @@ def lina_moe_infer_forward_two_phase(comm: Comm, desc: MoEDesc, tokens, gate_w, 
     return placement_to_tables(pl_out), bool(rep.value)
 
 
+def lina_infer_last_rows(comm: Comm):
+    """(rows received from each source, rows sent to each device) of the last inference call."""
+    recv = (ctypes.c_int32 * comm.world)()
+    sent = (ctypes.c_int32 * comm.world)()
+    _check(load().lina_infer_last_rows(comm.handle, recv, sent))
+    return list(recv), list(sent)
+
+
 def lina_sched_config(comm: Comm, policy: int, partition_bytes: int):
     _check(load().lina_sched_config(comm.handle, policy, partition_bytes))
 
@@ -418,7 +429,8 @@ def lina_profile_read(comm: Comm) -> dict:
     p = Profile()
     _check(load().lina_profile_read(comm.handle, ctypes.byref(p)))
     return {"kernel_launches": p.kernel_launches, "gemm_launches": p.gemm_launches,
-            "gemm_ms": p.gemm_ms, "gemm_phases": p.gemm_phases}
+            "gemm_ms": p.gemm_ms, "gemm_phases": p.gemm_phases, "a2a_window_ms": p.a2a_window_ms,
+            "gemm_in_a2a_ms": p.gemm_in_a2a_ms, "a2a_windows": p.a2a_windows}
 
 
 # ----------------------------------------------------------------------------- convenience layer

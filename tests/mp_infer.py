@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--experts", type=int, default=0)
     ap.add_argument("--mpd", type=int, default=0, help="max experts per device (0 = 2 E/N)")
     ap.add_argument("--seed", type=int, default=11)
+    ap.add_argument("--min-replicas", type=int, default=1,
+                    help="fail unless the plan replicates some expert at least this many times")
     a = ap.parse_args()
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -61,11 +63,14 @@ def main():
         return out.float().cpu().numpy(), plan
 
     y_rep, plan = run(None)
+    rows_rep = lina.lina_infer_last_rows(comm)  # (received per source, sent per device) under the plan
     El = E // world
     static = PlacementTables([1] * E, [[e // El] for e in range(E)],
                              [list(range(dv * El, (dv + 1) * El)) for dv in range(world)])
     y_sta, _ = run(static)
-    res = {"y_rep": y_rep, "y_sta": y_sta, "plan": (plan.replicas, plan.replica_device, plan.hosted)}
+    rows_sta = lina.lina_infer_last_rows(comm)
+    res = {"y_rep": y_rep, "y_sta": y_sta, "plan": (plan.replicas, plan.replica_device, plan.hosted),
+           "rows_rep": rows_rep, "rows_sta": rows_sta}
     gathered = [None] * world
     dist.gather_object(res, gathered if rank == 0 else None, dst=0)
     ok = True
@@ -84,9 +89,24 @@ def main():
         send = oplace.route_counts(counts, ref, world)
         per_dev = np.array(send).sum(axis=(0, 2))
         static_dev = counts.sum(0).reshape(world, El).sum(1)
-        ok = plan_ok and bitwise and max(errs) <= 2e-2
+        # rows each device received from each source = the oracle's replica split (R14), under
+        # the replicated plan and under the static placement; and what each rank sent
+        sta_ref = {"replicas": [1] * E, "replica_device": [[e // El] for e in range(E)]}
+        send_sta = oplace.route_counts(counts, sta_ref, world)
+        rows_ok = True
+        for dv in range(world):
+            for key, snd in (("rows_rep", send), ("rows_sta", send_sta)):
+                recv, sent = gathered[dv][key]
+                rows_ok &= recv == [int(sum(snd[s][dv])) for s in range(world)]
+                rows_ok &= sent == [int(sum(snd[dv][o])) for o in range(world)]
+        max_r = max(ref["replicas"])
+        repl_ok = max_r >= a.min_replicas
+        ok = plan_ok and bitwise and max(errs) <= 2e-2 and rows_ok and repl_ok
         print("MP_INFER", "OK" if ok else "FAIL", f"world={world} E={E} T={T} zipf={a.zipf} mpd={mpd}",
-              f"plan_ok={plan_ok} bitwise={bitwise} err={max(errs):.2e} replicas={ref['replicas']}",
+              f"plan_ok={plan_ok} bitwise={bitwise} rows_ok={rows_ok} max_replicas={max_r} "
+              f"(need >= {a.min_replicas}) err={max(errs):.2e} replicas={ref['replicas']}",
+              f"rows received by each device from each source: "
+              f"{[gathered[dv]['rows_rep'][0] for dv in range(world)]}",
               f"max/mean tokens per device: replicated {per_dev.max() / per_dev.mean():.2f} "
               f"static {static_dev.max() / static_dev.mean():.2f}", flush=True)
     flag = torch.tensor([1 if ok else 0], device=dev)

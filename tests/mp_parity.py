@@ -34,6 +34,9 @@ def main():
     ap.add_argument("--interleave", action="store_true",
                     help="run a second layer B between A's forward and backward (fwd A, fwd B, bwd B, "
                          "bwd A) on the same communicator; A must still match the oracle")
+    ap.add_argument("--shared-ws", action="store_true",
+                    help="with --interleave: layer B uses layer A's workspace (scratch may be shared between "
+                         "layers on one communicator; lina.h)")
     a = ap.parse_args()
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -73,6 +76,8 @@ def main():
         if a.interleave:  # layer B's exchanges run between A's forward and backward
             layer_b = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, cfg.capacity(),
                                     n_chunks, tdt, dev)
+            if a.shared_ws:
+                layer_b.workspace = layer.workspace
             XB, dYB = li.layer_tokens(cfg, a.seed + 1, rank)
             xb = torch.from_numpy(XB).to(tdt).to(dev)
             yb = layer_b.forward(xb, wg, w1, w2)

@@ -34,6 +34,13 @@ def test_two_ranks(cfg, tokens, n, extra):
     _run(2, "--config", cfg, "--tokens", str(tokens), "--n-chunks", str(n), *extra)
 
 
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_two_ranks_interleaved_layers_shared_workspace():
+    """fwd A, fwd B, bwd B, bwd A on one comm, B using A's workspace: the backward FREE is
+    posted after each backward's last read of dO / dXs, so A's gradients stay exact."""
+    _run(2, "--config", "C2", "--tokens", "512", "--n-chunks", "2", "--interleave", "--shared-ws", port=29613)
+
+
 @pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
 def test_four_ranks():
     _run(4, "--config", "C2", "--tokens", "384", "--n-chunks", "4", "--check-chunks", "1", "--poison", "--graph", port=29612)
@@ -64,9 +71,18 @@ def test_scheduler_allreduce_two_ranks():
     assert r.returncode == 0 and "MP_SCHED OK" in out, out[-4000:]
 
 
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_infer_replicas_two_ranks():
+    """Eq. (1) gives r_0 = 2 (E=8, Zipf 3: n_0 ~ 1.67): the replica token split runs."""
+    _run_infer(2, "--tokens", "512", "--zipf", "3.0", "--experts", "8", "--min-replicas", "2", port=29623)
+
+
 @pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
-def test_infer_replication_four_ranks():
-    _run_infer(4, "--tokens", "512", "--zipf", "1.0", "--experts", "32", port=29622)
+@pytest.mark.parametrize("zipf,experts,min_r", [(1.5, 32, 2), (2.0, 8, 3)])
+def test_infer_replicas_four_ranks(zipf, experts, min_r):
+    """r_e >= 2 at 4 ranks (E=32 Zipf 1.5: n_0 ~ 1.8; E=8 Zipf 2: n_0 ~ 2.6)."""
+    _run_infer(4, "--tokens", "512", "--zipf", str(zipf), "--experts", str(experts), "--min-replicas", str(min_r),
+               port=29624)
 
 
 def _run_full(nproc, port):
@@ -89,6 +105,7 @@ def test_full_size_four_ranks_graph():
 
 
 @pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
-def test_infer_replication_four_ranks():
+@pytest.mark.parametrize("zipf", [1.0, 1.2])
+def test_infer_replication_four_ranks(zipf):
     """S10 at 4 ranks: plan = oracle, replicated = static bitwise, fused peer-store all-to-all."""
-    _run_infer(4, "--tokens", "512", "--zipf", "1.2", "--experts", "32", port=29622)
+    _run_infer(4, "--tokens", "512", "--zipf", str(zipf), "--experts", "32", port=29622)

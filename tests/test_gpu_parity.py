@@ -238,3 +238,40 @@ def test_two_layers_interleaved_fwd_fwd_bwd_bwd():
         assert moe.normwise_error(dwg, o["bw"].dWg) <= tol, n
         assert moe.normwise_error(dw1, o["bw"].dW1) <= tol, n
         assert moe.normwise_error(dw2, o["bw"].dW2) <= tol, n
+
+
+def test_c5_shapes_fwd_bwd_two_cta_tiles():
+    """configs[4] layer dims (d=2048, f=8192, top-2, capacity 1.25) with 16 experts at 1024
+    tokens: 128 rows per expert segment (> 96), so the expert GEMMs run the 2-CTA 256-row
+    tiles the C5 bench runs, with K = 8192 in GEMM2 / dgrad2 and M = 2048 / 8192 in the
+    wgrads; forward and backward against the oracle.  (All 64 experts at full C5 would need
+    the oracle's fp64 weight gradients, 34 GB; the forward at E = 64 is the test above.)"""
+    cfg, X, Wg, W1, W2, dY = _case("C5", tokens=1024, num_experts=16)
+    assert cfg.tokens_per_rank * cfg.k / cfg.num_experts > 96
+    g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY)
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY)
+    compare(cfg, g, o)
+
+
+def test_c2_full_size_weight_gradients():
+    """configs[1] at full size (8192 tokens, ~2048 rows per expert, the bench shape at N=1):
+    y, dX, dWg and the expert weight gradients dW1, dW2 (K = 2048+ rows per wgrad) against
+    the oracle over every element."""
+    cfg, X, Wg, W1, W2, dY = _case("C2")
+    g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY)
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY)
+    compare(cfg, g, o)
+
+
+def test_c2_chunk_invariance_bf16():
+    """P8 on the bf16 tensor-core path: y and dX are bitwise equal for every n_chunks (each
+    row's arithmetic is fixed); dW1 / dW2 reduce rows in 64-row K blocks that follow the chunk
+    boundaries, so they agree to accumulation rounding only."""
+    cfg, X, Wg, W1, W2, dY = _case("C2", tokens=2048)
+    a = gpu_layer(cfg, 1, X, Wg, W1, W2, dY)
+    for n in (2, 4):
+        b = gpu_layer(cfg, n, X, Wg, W1, W2, dY)
+        for key in ("y", "dx", "dwg", "idx", "slot"):
+            assert np.array_equal(a[key], b[key]), (n, key)
+        for key in ("dw1", "dw2"):
+            assert moe.normwise_error(b[key], a[key]) <= 1e-2, (n, key)

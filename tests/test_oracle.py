@@ -320,3 +320,57 @@ def test_ffd_within_known_bound_of_brute_force_optimum(seed):
     plan = placement.place(list(pop), N, E)
     used = sum(1 for h in plan["hosted"] if h)
     assert used <= 11 / 9 * _opt_bins(list(sizes)) + 6 / 9 + 1e-9
+
+
+# ---------------------------------------------------------------------------
+# Pins of the comparison metric and of the replica token split (unpinned)
+# ---------------------------------------------------------------------------
+
+
+def test_normwise_error_hand_cases():
+    """north_star's metric (SURVEY.md §8(c) "Tolerances"): max_i |got_i − ref_i| / max_i |ref_i|.
+    The cases are chosen so a mean for a max, |got| in the denominator or an element-wise
+    relative error each give a different value."""
+    assert moe.normwise_error([1.0, 2.0, 3.0], [1.0, 2.0, 4.0]) == 0.25
+    # diffs (1, 1, 10), max|ref| = 20: 0.5 (mean of diffs 4/20 = 0.2; max|got| denominator
+    # 10/10 = 1; element-wise max |d|/|r| = 1)
+    assert moe.normwise_error([0.0, 0.0, 10.0], [1.0, 1.0, 20.0]) == 0.5
+    assert moe.normwise_error([0.0, -3.0], [1.0, -2.0]) == 0.5           # signs: |−3 − (−2)| = 1
+    assert moe.normwise_error(np.array([[1.0, 5.0], [2.0, 2.0]]), np.array([[1.0, 4.0], [2.0, 8.0]])) == 0.75
+    assert moe.normwise_error([0.5, 0.0], [0.0, 0.0]) == 0.5             # zero reference: absolute
+    assert moe.normwise_error([], []) == 0.0
+
+
+@pytest.mark.parametrize("count,r,s,expect", [
+    (7, 3, 0, [3, 2, 2]),      # blocks (3, 2, 2) in slot order, block q -> replica q
+    (7, 3, 1, [2, 3, 2]),      # block q -> replica (q + 1) mod 3
+    (7, 3, 2, [2, 2, 3]),
+    (7, 3, 4, [2, 3, 2]),      # s = 4 rotates like s = 1
+    (5, 2, 1, [2, 3]),
+    (1, 4, 3, [0, 0, 0, 1]),
+    (0, 3, 1, [0, 0, 0]),
+    (8, 4, 2, [2, 2, 2, 2]),
+])
+def test_replica_split_rotation_hand_table(count, r, s, expect):
+    """R14 (P:516 "how many tokens each replica should handle to balance the load"):
+    contiguous blocks differing by <= 1, block q to replica (q + s) mod r_e."""
+    assert placement.replica_split(count, r, s) == expect
+
+
+def test_replica_split_rotation_balances_remainders_across_sources():
+    """With one token per source and r_e sources, the rotation gives every replica exactly one
+    token; any split without the rotation puts all of them on replica 0."""
+    for r in (2, 3, 5):
+        tot = np.zeros(r, int)
+        for s in range(r):
+            tot += placement.replica_split(1, r, s)
+        assert tot.tolist() == [1] * r
+
+
+def test_route_counts_hand_case():
+    """send[s][dv][e] for two sources, expert 0 replicated on devices {0, 1}, expert 1 on {1}."""
+    plan = {"replicas": [2, 1], "replica_device": [[0, 1], [1]]}
+    send = placement.route_counts([[5, 3], [4, 2]], plan, 2)
+    # source 0: e0 5 tokens -> blocks (3, 2) to replicas (0, 1); e1 -> device 1
+    # source 1: e0 4 tokens -> blocks (2, 2) to replicas (1, 0); e1 -> device 1
+    assert send == [[[3, 0], [2, 3]], [[2, 0], [2, 2]]]

@@ -1,5 +1,5 @@
 """Pins of oracle/popularity.py (sample-path profiles, phase-one estimate, phase-two check;
-PAPER.md §5.2, P:432-484) — CPU only.
+PAPER.md §5.2, P:428-484) — CPU only.
 
 Each pin checks the oracle against something other than itself: the closed-form
 next-layer distribution of the seeded Markov generator, analytic expectations,
@@ -22,7 +22,7 @@ def _profile(tr, l):
 
 
 def test_deterministic_map_gives_point_masses_and_exact_estimate():
-    """p = 1, top-1: every Ψ is a point mass on the mapped expert (P:433-436), so the
+    """p = 1, top-1: every Ψ is a point mass on the mapped expert (P:429-430), so the
     phase-one estimate of a fresh batch equals its actual next-layer histogram / N_t."""
     E, L = 8, 5
     tr = li.selection_trace(4000, L, E, 1, 1.0, 1.0, seed=3)
@@ -71,7 +71,7 @@ def test_markov_trace_reproduces_ground_truth_rows():
 def test_hand_evaluated_two_token_estimate():
     """Two tokens: A's path has Ψ = {e1: 0.5, e2: 0.5} (top-1 picks e1 by the id tie-break,
     P = 0.5), B's path has Ψ = {e1: 1.0} -> popularity(e1) = (0.5 + 1.0) / 2 = 0.75
-    (the Σ_t P/N_t aggregation of Eq. (1), P:466-471)."""
+    (the Σ_t P/N_t aggregation of Eq. (1), P:473-476)."""
     E = 4
     sel = np.array([[[0], [1]], [[0], [2]], [[3], [1]], [[3], [1]]], dtype=np.int32)   # [T=4, L=2, k=1]
     pf = pop.Profile(2, E, 1, 1)
@@ -240,7 +240,7 @@ def test_native_phase_two_matches_oracle(lina, seed):
 
 @pytest.mark.parametrize("E,k,l", [(16, 1, 3), (64, 4, 3)])      # packed keys / byte-string keys
 def test_native_profile_save_load_round_trip(lina, tmp_path, E, k, l):
-    """A profile built offline ("In the profiling stage", P:432) and saved gives, once
+    """A profile built offline ("In the profiling stage", P:428) and saved gives, once
     loaded, the same estimates bit for bit; corrupt files are rejected with a reason."""
     L = 5
     tr = li.selection_trace(2000, L, E, k, 0.7, 1.0, seed=12)
