@@ -241,7 +241,14 @@ typedef struct {
   int32_t d_ffn;       /* f  (f*elt % 16 == 0; bf16 also f % 128 == 0)                  */
   int32_t num_experts; /* E global; static placement needs E % world == 0 (E_l = E/world) */
   int32_t k;           /* top-k, 1 <= k <= min(E, 8)  (k=2 training, k=1 inference) */
-  int32_t capacity;    /* C >= 1 slots per expert per SOURCE rank (R5); C >= T => dropless */
+  int32_t capacity;    /* C >= 1 slots per expert per SOURCE rank (R5); C >= T => no drops, with
+                          buffers padded to E·C rows per source.  0 = DROPLESS layout (§8(f) row 4):
+                          no capacity bound; the per-expert counts are exchanged on the device and
+                          the all-to-alls use an unequal split (P:525 applied to training), so the
+                          receive buffers hold P·T·min(k, E_l) rows (plus one M tile per expert and
+                          source) instead of E·T, and the source buffers T·k.  Needs n_chunks == 1;
+                          across ranks: the fused transport, bf16, d and f multiples of 256, equal
+                          num_tokens on every rank, world*E <= 512 (else UNSUPPORTED). */
   int32_t n_chunks;    /* all-to-all micro-ops per direction, 1 <= n <= C (R10) */
   lina_dtype dtype;    /* tokens, expert weights, outputs and their gradients            */
 } lina_moe_desc;

@@ -108,9 +108,11 @@ void validate_desc(const lina_moe_desc* d, int world, bool static_placement) {
   if (d->d_ffn <= 0) v.push_back("d_ffn <= 0");
   if (d->num_experts < 1 || d->num_experts > 64) v.push_back("num_experts not in [1, 64]");
   if (d->k < 1 || d->k > 8 || d->k > d->num_experts) v.push_back("k not in [1, min(E, 8)]");
-  if (d->capacity < 1) v.push_back("capacity < 1");
+  if (d->capacity < 0) v.push_back("capacity < 0 (0 = dropless)");
   if (d->n_chunks < 1 || d->n_chunks > 32 || (d->capacity >= 1 && d->n_chunks > d->capacity))
     v.push_back("n_chunks not in [1, min(C, 32)]");
+  if (static_placement && d->capacity == 0 && d->n_chunks != 1)
+    v.push_back("dropless (capacity 0) needs n_chunks == 1");
   if (d->d_model > 0 && (d->d_model * elt) % 16 != 0) v.push_back("d_model*elt % 16 != 0");
   if (d->d_ffn > 0 && (d->d_ffn * elt) % 16 != 0) v.push_back("d_ffn*elt % 16 != 0");
   if (d->d_model > 0 && d->d_model % 16 != 0) v.push_back("d_model % 16 != 0");
@@ -174,6 +176,21 @@ void validate_placement_tables(const lina_placement& pl, int E, int N, std::vect
     v.resize(16);
     v.push_back("... " + std::to_string(n - 16) + " more");
   }
+}
+
+// Dropless training across ranks runs on the fused transport only (its exchanges are peer
+// stores with in-kernel flags); one GPU runs both dtypes.
+void check_dropless(const lina_comm* cm, const lina_moe_desc* d) {
+  if (d->capacity != 0 || cm->world == 1) return;
+  std::vector<std::string> v;
+  if (cm->transport != 2 || !cm->ce) v.push_back("LINA_TRANSPORT must be fused");
+  if (d->dtype != LINA_BF16) v.push_back("dtype must be bf16");
+  if (d->d_model % 256 != 0 || d->d_ffn % 256 != 0) v.push_back("d_model and d_ffn must be multiples of 256");
+  if (cm->world > 8 || cm->world * d->num_experts > 512) v.push_back("world <= 8 and world*E <= 512");
+  if (v.empty()) return;
+  std::string m = "dropless training (capacity 0) across ranks:";
+  for (auto& x : v) m += " [" + x + "]";
+  throw StatusError{LINA_ERR_UNSUPPORTED, m};
 }
 
 void need(std::vector<std::string>& v, const void* p, const char* name) {
@@ -481,6 +498,7 @@ lina_status lina_moe_workspace_size(const lina_comm* cm, const lina_moe_desc* de
   return guarded([&] {
     if (!cm) throw ArgError{"comm is NULL"};
     validate_desc(desc, cm->world, true);
+    check_dropless(cm, desc);
     Plan p = make_plan(*desc, cm->world);
     if (workspace_bytes) *workspace_bytes = p.ws_bytes;
     if (saved_bytes) *saved_bytes = p.saved_bytes;
@@ -495,6 +513,7 @@ lina_status lina_moe_forward(lina_comm* cm, const lina_moe_desc* desc, const voi
   return guarded([&] {
     if (!cm) throw ArgError{"comm is NULL"};
     validate_desc(desc, cm->world, true);
+    check_dropless(cm, desc);
     std::vector<std::string> v;
     const bool any = desc->num_tokens > 0;
     if (any) need(v, tokens, "tokens");
@@ -527,6 +546,7 @@ lina_status lina_moe_backward(lina_comm* cm, const lina_moe_desc* desc, const vo
   return guarded([&] {
     if (!cm) throw ArgError{"comm is NULL"};
     validate_desc(desc, cm->world, true);
+    check_dropless(cm, desc);
     std::vector<std::string> v;
     const bool any = desc->num_tokens > 0;
     need(v, saved, "saved");

@@ -17,7 +17,9 @@ class CeTransport {
          // fused transport (in-kernel signals; rounds from the device counters below)
          kFReadyFwdD = 10, kFReadyFwdC = 11, kFReadyBwdD = 12, kFReadyBwdC = 13,
          // inference exchange by peer stores (infer.cpp)
-         kIFreeD = 14, kIReadyD = 15, kIFreeC = 16, kIReadyC = 17, kKinds = 18 };
+         kIFreeD = 14, kIReadyD = 15, kIFreeC = 16, kIReadyC = 17,
+         // dropless training: the per-expert counts of a forward have landed
+         kFCountFwd = 18, kKinds = 19 };
   static constexpr int kMaxChunks = 32;
 
   explicit CeTransport(lina_comm* cm);  // collective (allgathers the flag-array handles)

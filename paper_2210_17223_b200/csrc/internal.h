@@ -52,6 +52,11 @@ struct Plan {
   size_t w_route, w_D, w_O, w_dg, w_dwg, w_dS, w_dO, w_dH, w_dXe, w_dXs;
   size_t ws_bytes;
   uint64_t peer_key;  // hash of the peer-visible geometry (checked across ranks on first mapping)
+  // dropless layout (capacity == 0; §8(f) row 4): V virtual segments of tile_rows rows per
+  // receive buffer, T·k compact rows per source buffer, the count table and the layout tables
+  bool dropless = false;
+  int V = 0;
+  size_t s_allc = 0, s_tab = 0;
   size_t rows_send() const { return (size_t)n * E * Cm; }
   size_t rows_recv() const { return (size_t)n * P * El * Cm; }
 };

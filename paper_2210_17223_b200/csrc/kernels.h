@@ -36,6 +36,10 @@ struct WGrad {
   void* D;             // [El][M][N]
   const int* vcount;
   int nchunks, P, El, Cm, M, N;
+  // dropless layout: expert el sums segments [seg_range[2el], seg_range[2el+1]) of
+  // nseg_total (instead of segments (c*P + s)*El + el)
+  const int* seg_range = nullptr;
+  int nseg_total = 0;
 };
 
 // sig (fused transport): block 0 posts sig at kernel start (the FREE of this round).
@@ -69,16 +73,18 @@ void launch_permute(int dtype, const void* X, const int* tok_of, const int* kept
                     int n, int Cm, void* Send, cudaStream_t s);
 // sig: block 0 posts sig.post (FREE of the backward buffers) at start; every CTA waits
 // sig.wait (the returned expert outputs) before reading Recv.
+// ebase (dropless layout): row of (t, j) = ebase[idx] + slot instead of the send-layout row.
 void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot, const float* gate,
                     int T, int k, int d, int E, int C, int n, int Cm, void* Y, cudaStream_t s,
-                    const PeerSignal* sig = nullptr);
+                    const PeerSignal* sig = nullptr, const int* ebase = nullptr);
 void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
                         const float* gate, int T, int k, int d, int E, int C, int n, int Cm,
                         void* dSend, float* dg, cudaStream_t s);
 // dX (gather-sum + dL·Wgᵀ) and dWg (Xᵀ dL) with dL recomputed from the forward routing.
 void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* probs,
                const float* gate, const float* dg, const float* Wg, int T, int k, int d, int E, int C,
-               int n, int Cm, void* dX, cudaStream_t s, const PeerSignal* sig = nullptr);
+               int n, int Cm, void* dX, cudaStream_t s, const PeerSignal* sig = nullptr,
+               const int* ebase = nullptr);
 size_t dwg_scratch_floats(int T, int d, int E);
 void launch_dwg(int dtype, const void* X, const float* probs, const int* idx, const float* gate,
                 const float* dg, int T, int d, int E, int k, float* scratch, float* dWg, cudaStream_t s);
@@ -113,6 +119,32 @@ void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const 
 // peer-storing GEMM epilogue moves them; the last CTA posts sig (READY of micro-op c).
 void launch_push_segments(int dtype, const void* recv_layout, void* const* peer_send_layout, const int* vcount,
                           int c, int P, int El, int E, int Cm, int me, int d, const PeerSignal& sig, cudaStream_t s);
+// Dropless training (dropless.cu; §8(f) row 4): tables computed on the device from the
+// exchanged per-expert counts allc [P][E] (identical on every rank).
+struct DlTables {
+  int* dbase;      // [E]   first row of this rank's block for expert e at its owner (dispatch target)
+  int* ebase;      // [E]   first row of this rank's expert-e rows where the combine reads them
+  int* soff;       // [P][E] compact source offsets: Σ_{e'<e} allc[s][e']
+  int* src_total;  // [P]   rows each source sends in total (= T_s·k)
+  int* vcount;     // [V]   valid rows of each virtual segment of this rank (0 past the used ones)
+  int* vexp;       // [V]   local expert (weight index) of the segment
+  int* vsrc;       // [V]   source rank of the segment's rows
+  int* vq0;        // [V]   first slot (within the source's expert block) of the segment
+  int* mtp;        // [V+1] m-tile prefix (one tile per used segment)
+  int* vrange;     // [E_l][2] segment range of each local expert (wgrad)
+};
+void launch_dl_counts(const int* kept, int* const* peer_allc, int P, int me, int E, const PeerSignal& sig,
+                      cudaStream_t s);
+void launch_dl_layout(const int* allc, int P, int E, int El, int me, int R, int V, const DlTables& t, cudaStream_t s);
+// peer_dst: device array [P] of the owners' buffers (fused transport), or NULL and local_dst
+void launch_dl_permute(int dtype, const void* X, const int* tok_of, const int* kept, const DlTables& t, int me,
+                       int T, int k, int E, int El, int d, void* const* peer_dst, void* local_dst,
+                       const PeerSignal& sig, cudaStream_t s);
+void launch_dl_combine_bwd(int dtype, const void* dY, const void* O, const int* tok_of, const int* kept,
+                           const float* gate, const DlTables& t, int me, int T, int k, int E, int El, int d,
+                           void* const* peer_dst, void* local_dst, float* dg, const PeerSignal& sig, cudaStream_t s);
+void launch_dl_push_vsegs(int dtype, const void* src, void* const* peer, const DlTables& t, int V, int R, int E,
+                          int El, int me, int d, const PeerSignal& sig, cudaStream_t s);
 // Output tiles of a row GEMM stored through per-owner tensor maps (peer memory):
 // segment (c, s, el) of the receive layout goes to map s at segment c*E + me*El + el.
 struct PeerStore {

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe
                                                        const float* __restrict__ dg,
                                                        const float* __restrict__ Wg, int Tn, int k, int d,
                                                        int E, int C, int n, int Cm, T* __restrict__ dX,
-                                                       PeerSignal sig) {
+                                                       PeerSignal sig, const int* __restrict__ ebase) {
   pdl_enter();
   extern __shared__ float dsm[];
   if (threadIdx.x == 0) sig_wait(sig);  // fused transport: the expert input-gradients have landed
@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(256) dx_tiled_kernel(const T* __restrict__ dXe
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
       const uint4* src = reinterpret_cast<const uint4*>(
-          dXe + send_row(ex[i][j], sl[i][j] < 0 ? 0 : sl[i][j], E, C, n, Cm) * d + col);
+          dXe + (ebase ? (size_t)(ebase[ex[i][j]] + (sl[i][j] < 0 ? 0 : sl[i][j]))   // dropless: compact rows
+                       : send_row(ex[i][j], sl[i][j] < 0 ? 0 : sl[i][j], E, C, n, Cm)) * d + col);
 #pragma unroll
       for (int v = 0; v < NV; ++v) raw[i][j][v] = sl[i][j] >= 0 ? src[v] : make_uint4(0, 0, 0, 0);
     }
@@ -375,7 +376,8 @@ size_t dwg_scratch_floats(int T, int d, int E) {
 template <typename T, int KT>
 static void launch_dx_t(const void* dXe, const int* idx, const int* slot, const float* probs,
                         const float* gate, const float* dg, const float* Wg, int Tn, int k, int d, int E,
-                        int C, int n, int Cm, void* dX, const PeerSignal& sig, cudaStream_t s) {
+                        int C, int n, int Cm, void* dX, const PeerSignal& sig, cudaStream_t s,
+                        const int* ebase) {
   dim3 grid((d + kDxCols - 1) / kDxCols, std::max(1, (Tn + kDxTok - 1) / kDxTok));
   const size_t smem = sizeof(float) * ((size_t)E * kDxCols + kDxTok * E);
   static bool set = false;
@@ -385,19 +387,19 @@ static void launch_dx_t(const void* dXe, const int* idx, const int* slot, const 
     set = true;
   }
   launch_k(dx_tiled_kernel<T, KT>, grid, dim3(256), smem, s, (const T*)dXe, idx, slot, probs, gate, dg, Wg, Tn, k, d,
-           E, C, n, Cm, (T*)dX, sig);
+           E, C, n, Cm, (T*)dX, sig, ebase);
 }
 
 void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* probs,
                const float* gate, const float* dg, const float* Wg, int T, int k, int d, int E, int C,
-               int n, int Cm, void* dX, cudaStream_t s, const PeerSignal* sig) {
+               int n, int Cm, void* dX, cudaStream_t s, const PeerSignal* sig, const int* ebase) {
   if (T <= 0 && !sig) return;  // (with a signal, one CTA still closes the round)
   const PeerSignal sg = sig ? *sig : PeerSignal{};
   auto go = [&](auto tag) {
     using ET = decltype(tag);
-    if (k == 1) launch_dx_t<ET, 1>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, sg, s);
-    else if (k == 2) launch_dx_t<ET, 2>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, sg, s);
-    else launch_dx_t<ET, 0>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, sg, s);
+    if (k == 1) launch_dx_t<ET, 1>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, sg, s, ebase);
+    else if (k == 2) launch_dx_t<ET, 2>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, sg, s, ebase);
+    else launch_dx_t<ET, 0>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, sg, s, ebase);
   };
   if (dtype == 0) go(float{});
   else go(__nv_bfloat16{});

@@ -114,9 +114,11 @@ __global__ void __launch_bounds__(256) wgrad_kernel(WGrad p) {
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  for (int c = 0; c < p.nchunks; ++c) {
-    for (int s = 0; s < p.P; ++s) {
-      const int seg = (c * p.P + s) * p.El + el;
+  // segments of expert el: (c*P + s)*El + el, or the dropless range
+  const int nlist = p.seg_range ? p.seg_range[2 * el + 1] - p.seg_range[2 * el] : p.nchunks * p.P;
+  for (int li = 0; li < nlist; ++li) {
+    {
+      const int seg = p.seg_range ? p.seg_range[2 * el] + li : li * p.El + el;
       const int v = p.vcount[seg];
       const T* A = (const T*)p.A + (size_t)seg * p.Cm * p.M;
       const T* B = (const T*)p.B + (size_t)seg * p.Cm * p.N;

@@ -273,6 +273,7 @@ struct TcParams {
   __nv_bfloat16* D;
   const __nv_bfloat16* aux;
   int nchunks, P;      // WGRAD
+  const int* seg_range;  // WGRAD, dropless layout: expert el's segments [seg_range[2el], seg_range[2el+1])
   // ROW with peer stores: output tile of segment (c, s, el) goes through pmaps[s] to
   // segment c*dE + dme*El + el of rank s's buffer (the combine all-to-all fused into
   // the epilogue); has_pmaps = 0: local store through tmD
@@ -353,8 +354,14 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
       seg_or_el = ml / mblks;
       m0 = (ml % mblks) * G::ROWS;
     } else {
-      int i = 0;
-      while (i + 1 < p.nseg && p.mtp[i + 1] <= ml) ++i;
+      // the last segment whose first m-tile is <= ml (binary search over the prefix; an
+      // empty segment shares its start with the next one, so the last such is non-empty)
+      int i = 0, hi = p.nseg - 1;
+      while (i < hi) {
+        const int mid = (i + hi + 1) >> 1;
+        if (__ldg(p.mtp + mid) <= ml) i = mid;
+        else hi = mid - 1;
+      }
       seg_or_el = i;  // local segment index within this launch
       m0 = (ml - p.mtp[i]) * G::ROWS;
     }
@@ -362,6 +369,11 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
   auto kblocks_of = [&](int seg_or_el) {
     if (!WGRAD) return p.K / BK;
     int kb = 0;
+    if (p.seg_range) {
+      for (int seg = p.seg_range[2 * seg_or_el]; seg < p.seg_range[2 * seg_or_el + 1]; ++seg)
+        kb += (p.vcount[seg] + BK - 1) / BK;
+      return kb;
+    }
     for (int c = 0; c < p.nchunks; ++c)
       for (int s = 0; s < p.P; ++s) kb += (p.vcount[(c * p.P + s) * p.El + seg_or_el] + BK - 1) / BK;
     return kb;
@@ -418,12 +430,19 @@ __global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
           }
         } else {
           const int el = se;
-          for (int c = 0; c < p.nchunks; ++c)
-            for (int s = 0; s < p.P; ++s) {
-              const int seg = (c * p.P + s) * p.El + el;
+          if (p.seg_range) {
+            for (int seg = p.seg_range[2 * el]; seg < p.seg_range[2 * el + 1]; ++seg) {
               const int v = p.vcount[seg];
               for (int r0 = 0; r0 < v; r0 += BK) issue(m0 + arow, r0, seg, n0 + brow, r0, seg);
             }
+          } else {
+            for (int c = 0; c < p.nchunks; ++c)
+              for (int s = 0; s < p.P; ++s) {
+                const int seg = (c * p.P + s) * p.El + el;
+                const int v = p.vcount[seg];
+                for (int r0 = 0; r0 < v; r0 += BK) issue(m0 + arow, r0, seg, n0 + brow, r0, seg);
+              }
+          }
         }
       }
     }
@@ -811,7 +830,7 @@ static void row_gemm_tc_impl_t(const RowGemm& g, bool b_kmajor, int epi, const P
 void launch_wgrad_tc(const WGrad& g, cudaStream_t s) {
   using namespace tc;
   constexpr int CG = kTcCtaGroup;
-  const uint64_t nseg_total = (uint64_t)g.nchunks * g.P * g.El;
+  const uint64_t nseg_total = g.nseg_total ? (uint64_t)g.nseg_total : (uint64_t)g.nchunks * g.P * g.El;
   const uint64_t ad[3] = {(uint64_t)g.M, (uint64_t)g.Cm, nseg_total};
   const uint64_t as[2] = {(uint64_t)g.M * 2, (uint64_t)g.Cm * g.M * 2};
   const uint32_t ab[3] = {64, BK, 1};
@@ -828,6 +847,7 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s) {
   p.N = g.N;
   p.nchunks = g.nchunks;
   p.P = g.P;
+  p.seg_range = g.seg_range;
   p.D = (__nv_bfloat16*)g.D;
   const int tiles = g.El * (g.M / Geo<CG>::ROWS) * (g.N / BN);
   const int maxc = num_sms() / CG;

@@ -165,7 +165,7 @@ template <typename T, int NVL, int KT>
 __device__ __forceinline__ void combine_tokens(const T* __restrict__ Recv, const int* __restrict__ idx,
                                                const int* __restrict__ slot, const float* __restrict__ gate,
                                                int Tn, int k, int d, int E, int C, int n, int Cm,
-                                               T* __restrict__ Y) {
+                                               T* __restrict__ Y, const int* __restrict__ ebase) {
   constexpr int NL = NVL > 0 ? NVL : 1;  // (NVL = 0 is never launched)
   constexpr int U = kLoadsPerLane / NL;
   constexpr int TP = U / KT > 0 ? U / KT : 1;
@@ -185,7 +185,7 @@ __device__ __forceinline__ void combine_tokens(const T* __restrict__ Recv, const
     const int s = slot[pi];
     kq = s >= 0;
     if (kq) {
-      rowq = send_row(idx[pi], s, E, C, n, Cm);
+      rowq = ebase ? (size_t)(ebase[idx[pi]] + s) : send_row(idx[pi], s, E, C, n, Cm);  // (dropless: compact)
       gq = gate[pi];
     }
   }
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ Recv
                                                       const int* __restrict__ slot,
                                                       const float* __restrict__ gate, int Tn, int k, int d,
                                                       int E, int C, int n, int Cm, T* __restrict__ Y,
-                                                      PeerSignal sig) {
+                                                      PeerSignal sig, const int* __restrict__ ebase) {
   pdl_enter();
   // fused transport: this rank's backward receive buffers are free again (block 0 posts);
   // the peers' returned expert outputs have landed (every CTA waits)
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ Recv
     if (threadIdx.x == 0) sig_wait(sig);
     __syncthreads();
   }
-  combine_tokens<T, NVL, KT>(Recv, idx, slot, gate, Tn, k, d, E, C, n, Cm, Y);
+  combine_tokens<T, NVL, KT>(Recv, idx, slot, gate, Tn, k, d, E, C, n, Cm, Y, ebase);
   if (sig.bump) {  // the forward's last kernel closes its round
     __syncthreads();
     if (threadIdx.x == 0) sig_bump_last(sig);
@@ -255,7 +255,7 @@ template <typename T>
 __device__ __forceinline__ void combine_token_loop(const T* __restrict__ Recv, const int* __restrict__ idx,
                                                    const int* __restrict__ slot, const float* __restrict__ gate,
                                                    long long t, int lane, int k, int d, int E, int C, int n,
-                                                   int Cm, T* __restrict__ Y) {
+                                                   int Cm, T* __restrict__ Y, const int* __restrict__ ebase) {
   constexpr int V = 16 / sizeof(T);
   const T* rowp[8];
   float g[8];
@@ -263,7 +263,7 @@ __device__ __forceinline__ void combine_token_loop(const T* __restrict__ Recv, c
   for (int j = 0; j < k; ++j) {
     const int s = slot[t * k + j];
     if (s >= 0) {
-      rowp[kk] = Recv + send_row(idx[t * k + j], s, E, C, n, Cm) * d;
+      rowp[kk] = Recv + (ebase ? (size_t)(ebase[idx[t * k + j]] + s) : send_row(idx[t * k + j], s, E, C, n, Cm)) * d;
       g[kk] = gate[t * k + j];
       ++kk;
     }
@@ -288,7 +288,7 @@ template <typename T>
 __global__ void combine_loop_kernel(const T* __restrict__ Recv, const int* __restrict__ idx,
                                     const int* __restrict__ slot, const float* __restrict__ gate,
                                     int Tn, int k, int d, int E, int C, int n, int Cm,
-                                    T* __restrict__ Y, PeerSignal sig) {
+                                    T* __restrict__ Y, PeerSignal sig, const int* __restrict__ ebase) {
   pdl_enter();
   if (blockIdx.x == 0 && threadIdx.x == 0) sig_post(sig);
   if (sig.wait) {
@@ -297,7 +297,7 @@ __global__ void combine_loop_kernel(const T* __restrict__ Recv, const int* __res
   }
   const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (t < Tn) combine_token_loop<T>(Recv, idx, slot, gate, t, lane, k, d, E, C, n, Cm, Y);
+  if (t < Tn) combine_token_loop<T>(Recv, idx, slot, gate, t, lane, k, d, E, C, n, Cm, Y, ebase);
   if (sig.bump) {
     __syncthreads();
     if (threadIdx.x == 0) sig_bump_last(sig);
@@ -499,7 +499,7 @@ void launch_permute(int dtype, const void* X, const int* tok_of, const int* kept
 
 void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot, const float* gate,
                     int T, int k, int d, int E, int C, int n, int Cm, void* Y, cudaStream_t s,
-                    const PeerSignal* sig) {
+                    const PeerSignal* sig, const int* ebase) {
   const PeerSignal sg = sig ? *sig : PeerSignal{};
   if (T <= 0 && !sig) return;
   const int nvl = nvl_of(d, dtype);
@@ -509,13 +509,13 @@ void launch_combine(int dtype, const void* Recv, const int* idx, const int* slot
     const long long warps = std::max(1LL, ((long long)T + tp - 1) / tp);
     if (k == 1)
       LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, launch_k(combine_kernel<ET, NV_, 1>, dim3(blocks_for_warps(warps)),
-                                 dim3(256), 0, s, (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg)));
+                                 dim3(256), 0, s, (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg, ebase)));
     else
       LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, launch_k(combine_kernel<ET, NV_, 2>, dim3(blocks_for_warps(warps)),
-                                 dim3(256), 0, s, (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg)));
+                                 dim3(256), 0, s, (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg, ebase)));
   } else {
     LINA_DISPATCH_T(dtype, launch_k(combine_loop_kernel<ET>, dim3(blocks_for_warps(std::max(1, T))), dim3(256), 0, s,
-                                    (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg));
+                                    (const ET*)Recv, idx, slot, gate, T, k, d, E, C, n, Cm, (ET*)Y, sg, ebase));
   }
   LINA_LAUNCH_CHECK();
 }

@@ -54,13 +54,57 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
     if (tr && (atoi(tr) == 128 || atoi(tr) == 256)) p.tile_rows = atoi(tr);
   }
   const size_t T = p.T, k = p.k, E = p.E;
-  const size_t send_rows = p.rows_send(), recv_rows = p.rows_recv();
   size_t o = 0;
   auto take = [&](size_t bytes) {
     size_t at = o;
     o = align_up(o + bytes);
     return at;
   };
+  if (dsc.capacity == 0) {  // dropless (§8(f) row 4): count exchange + unequal split
+    p.dropless = true;
+    p.C = std::max(p.T, 1);  // route slots within (source, expert): never dropped
+    p.n = 1;
+    const int R = p.tile_rows;
+    p.Cm = R;
+    // virtual segments: Σ_{(el, s)} ceil(c / R) <= rows / R + P·E_l, rows <= P·T·min(k, E_l)
+    const long long rows = (long long)p.P * p.T * std::min(p.k, p.El);
+    p.V = (int)(rows / R + (long long)p.P * p.El + 1);
+    const size_t vrows = (size_t)p.V * R, srows = (size_t)p.T * p.k;
+    const size_t tab_ints = 2 * E + (size_t)p.P * E + p.P + 4 * (size_t)p.V + (p.V + 1) + 2 * (size_t)p.El;
+    // peer-visible regions first (T-independent offsets are not possible here: the
+    // source-compact buffers hold T·k rows, so dropless needs equal T on every rank)
+    p.s_R = take(vrows * p.d * p.dt);                                    // [peer-written]
+    p.s_C = take((p.P > 1 ? srows : vrows) * p.d * p.dt);                // [peer-written] (P=1: O itself)
+    p.s_allc = take(4 * (size_t)p.P * E);                                // [peer-written]
+    p.s_kept = take(4 * E);
+    p.s_probs = take(4 * T * E);
+    p.s_idx = take(4 * T * k);
+    p.s_gate = take(4 * T * k);
+    p.s_slot = take(4 * T * k);
+    p.s_tokof = take(4 * E * (size_t)p.C);
+    p.s_tab = take(4 * tab_ints);
+    p.s_H = take(vrows * (size_t)p.f * p.dt);
+    p.s_mask = take(vrows * (size_t)((p.f + 63) / 64) * 8);
+    p.saved_bytes = o;
+    o = 0;
+    p.w_dO = take(vrows * p.d * p.dt);                                   // [peer-written]
+    p.w_dXs = (p.P > 1) ? take(srows * p.d * p.dt) : 0;                  // [peer-written]
+    p.w_O = (p.P > 1) ? take(vrows * p.d * p.dt) : 0;
+    p.w_dXe = take(vrows * p.d * p.dt);
+    p.w_route = take(4 * route_scratch_ints(p.T, p.k, p.E));
+    p.w_dg = take(4 * T * k);
+    p.w_dwg = take(4 * dwg_scratch_floats(p.T, p.d, p.E));
+    p.w_dH = take(vrows * (size_t)p.f * p.dt);
+    p.ws_bytes = o;
+    uint64_t h = 1469598103934665603ull;
+    for (uint64_t v : {(uint64_t)0xd1, (uint64_t)p.T, (uint64_t)p.k, (uint64_t)p.V, (uint64_t)R, (uint64_t)p.E,
+                       (uint64_t)p.P, (uint64_t)p.d, (uint64_t)p.f, (uint64_t)p.dt, (uint64_t)p.s_R, (uint64_t)p.s_C,
+                       (uint64_t)p.s_allc, (uint64_t)p.w_dO, (uint64_t)p.w_dXs})
+      for (int b = 0; b < 8; ++b) h = (h ^ ((v >> (8 * b)) & 0xff)) * 1099511628211ull;
+    p.peer_key = h | 1;
+    return p;
+  }
+  const size_t send_rows = p.rows_send(), recv_rows = p.rows_recv();
   // Every region a peer writes or reads at this rank's offsets (fused / copy-engine
   // transports: a rank finds a peer's buffer as the peer's base + ITS OWN offset) comes
   // first, sized by (C, n_chunks, E, d, dtype, world) only, so ranks may pass different
@@ -111,9 +155,56 @@ struct Ptrs {
   int* vcount; int* mtp; char* R; char* H; char* Cb; uint64_t* mask;
   int* route; char* D; char* O; float* dg; float* dwg; char* dS; char* dO; char* dH;
   char* dXe; char* dXs;
+  int* allc;    // dropless: [P][E] exchanged counts
+  DlTables dl;  // dropless: layout tables
 };
 
+Ptrs carve_dropless(const Plan& p, void* saved, void* ws) {
+  char* sv = (char*)saved;
+  char* w = (char*)ws;
+  Ptrs q{};
+  if (sv) {
+    q.probs = (float*)(sv + p.s_probs);
+    q.idx = (int*)(sv + p.s_idx);
+    q.gate = (float*)(sv + p.s_gate);
+    q.slot = (int*)(sv + p.s_slot);
+    q.kept = (int*)(sv + p.s_kept);
+    q.tok_of = (int*)(sv + p.s_tokof);
+    q.allc = (int*)(sv + p.s_allc);
+    q.R = sv + p.s_R;
+    q.H = sv + p.s_H;
+    q.Cb = sv + p.s_C;
+    q.mask = (uint64_t*)(sv + p.s_mask);
+    int* t = (int*)(sv + p.s_tab);
+    const int E = p.E, P = p.P, V = p.V;
+    q.dl.dbase = t;
+    q.dl.ebase = t + E;
+    q.dl.soff = t + 2 * E;
+    q.dl.src_total = q.dl.soff + (size_t)P * E;
+    q.dl.vcount = q.dl.src_total + P;
+    q.dl.vexp = q.dl.vcount + V;
+    q.dl.vsrc = q.dl.vexp + V;
+    q.dl.vq0 = q.dl.vsrc + V;
+    q.dl.mtp = q.dl.vq0 + V;
+    q.dl.vrange = q.dl.mtp + V + 1;
+    q.vcount = q.dl.vcount;
+    q.mtp = q.dl.mtp;
+  }
+  if (w) {
+    q.route = (int*)(w + p.w_route);
+    q.O = p.P > 1 ? w + p.w_O : q.Cb;  // P = 1: the expert outputs stay in `saved` (read back by backward)
+    q.dg = (float*)(w + p.w_dg);
+    q.dwg = (float*)(w + p.w_dwg);
+    q.dO = w + p.w_dO;
+    q.dH = w + p.w_dH;
+    q.dXe = w + p.w_dXe;
+    q.dXs = p.P > 1 ? w + p.w_dXs : q.dXe;
+  }
+  return q;
+}
+
 Ptrs carve(const Plan& p, void* saved, void* ws) {
+  if (p.dropless) return carve_dropless(p, saved, ws);
   char* sv = (char*)saved;
   char* w = (char*)ws;
   Ptrs q{};
@@ -617,6 +708,160 @@ void backward_fused_movers(lina_comm* cm, const Plan& p, const Ptrs& q, const vo
   launch_sig_wait(make_sig(cm, -1, nullptr, 0, CT::kFreeBwd, rb, 0), s);  // backward FREE
 }
 
+// ------------------------------------------------------------------ dropless layout
+// (§8(f) row 4; kernels/dropless.cu): no capacity bound, a count exchange, unequal-split
+// dispatch / return by peer stores, the expert GEMMs over virtual segments.  n_chunks = 1.
+RowGemm dl_gemm(const Plan& p, const Ptrs& q, const void* A, const void* B, void* D, int N, int K) {
+  RowGemm g{};
+  g.tile_rows = p.tile_rows;
+  g.A = A;
+  g.B = B;
+  g.D = D;
+  g.vcount = q.dl.vcount;
+  g.mtp = q.dl.mtp;
+  g.seg0 = 0;
+  g.nseg = p.V;
+  g.El = p.V;               // segment v's weight index = seg_expert[v % V] = vexp[v]
+  g.seg_expert = q.dl.vexp;
+  g.B_experts = p.El;
+  g.Cm = p.tile_rows;
+  g.N = N;
+  g.K = K;
+  return g;
+}
+
+void forward_dropless(lina_comm* cm, const Plan& p, const Ptrs& q, const void* tokens, const float* gate_w,
+                      const void* w1, const void* w2, void* out, void* saved, lina_route* route, cudaStream_t s) {
+  using CT = CeTransport;
+  const int dtype = p.bf16 ? 1 : 0, P = p.P, me = cm->rank, E = p.E, El = p.El, R = p.tile_rows;
+  const bool peer = P > 1;
+  CeTransport* ce = peer ? cm->ce : nullptr;
+  uint32_t* rf = peer ? ce->round_fwd() : nullptr;
+  const bool override_r = route && route->override_routing;
+  trace_mark(cm, s, "dl fwd:start");
+  if (override_r) {
+    LINA_CUDA_CHECK(cudaMemcpyAsync(q.idx, route->idx, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
+    LINA_CUDA_CHECK(cudaMemcpyAsync(q.gate, route->gate, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
+  }
+  // gate (block 0 posts FREE: my R, counts and returned rows were last read by the previous backward)
+  const PeerSignal s_free = peer ? make_sig(cm, -1, nullptr, 0, CT::kFreeFwd, rf, 1) : PeerSignal{};
+  launch_gate_topk(dtype, tokens, gate_w, p.T, p.d, E, p.k, override_r ? 0 : 1, q.probs, q.idx, q.gate, s,
+                   peer ? &s_free : nullptr);
+  launch_route(q.idx, p.T, p.k, E, p.C, q.route, q.slot, route ? route->counts : nullptr, q.kept, q.tok_of, s,
+               cm->route_sync);
+  const int* allc = q.kept;
+  if (peer) {  // the count exchange, then every rank derives the same layout
+    prof_a2a_begin(cm, s);
+    int* const* peer_allc = (int* const*)ce->dev_ptrs(saved, p.s_allc, s, p.peer_key);
+    launch_dl_counts(q.kept, peer_allc, P, me, E, make_sig(cm, CT::kFreeFwd, rf, 1, CT::kFCountFwd, rf, 1), s);
+    launch_sig_wait(make_sig(cm, CT::kFCountFwd, rf, 1, -1, nullptr, 0), s);
+    allc = q.allc;
+  }
+  launch_dl_layout(allc, P, E, El, me, R, p.V, q.dl, s);
+  trace_mark(cm, s, "dl gate+route+layout");
+  if (peer) {
+    void* const* peer_R = ce->dev_ptrs(saved, p.s_R, s, p.peer_key);
+    launch_dl_permute(dtype, tokens, q.tok_of, q.kept, q.dl, me, p.T, p.k, E, El, p.d, peer_R, nullptr,
+                      make_sig(cm, -1, nullptr, 0, CT::kFReadyFwdD, rf, 1, kSiteDispFwd), s);
+    launch_sig_wait(make_sig(cm, CT::kFReadyFwdD, rf, 1, -1, nullptr, 0), s);  // every source's rows landed
+  } else {
+    launch_dl_permute(dtype, tokens, q.tok_of, q.kept, q.dl, me, p.T, p.k, E, El, p.d, nullptr, q.R, PeerSignal{}, s);
+  }
+  if (route) {
+    if (route->idx && !override_r)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->idx, q.idx, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
+    if (route->gate && !override_r)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->gate, q.gate, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
+    if (route->slot)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->slot, q.slot, 4 * (size_t)p.T * p.k, cudaMemcpyDeviceToDevice, s));
+    if (route->probs)
+      LINA_CUDA_CHECK(cudaMemcpyAsync(route->probs, q.probs, 4 * (size_t)p.T * E, cudaMemcpyDeviceToDevice, s));
+  }
+  trace_mark(cm, s, "dl dispatch");
+  prof_begin(cm, s);
+  RowGemm g1 = dl_gemm(p, q, q.R, w1, q.H, p.f, p.d);
+  g1.mask_out = q.mask;
+  launch_expert_row_gemm(dtype, g1, true, kEpiRelu, s);
+  launch_expert_row_gemm(dtype, dl_gemm(p, q, q.H, w2, q.O, p.d, p.f), true, kEpiNone, s);
+  prof_end(cm, s, 2);
+  trace_mark(cm, s, "dl gemm1+gemm2");
+  if (peer) {  // return all-to-all: each segment's rows to its source's compact buffer
+    void* const* peer_C = ce->dev_ptrs(saved, p.s_C, s, p.peer_key);
+    launch_dl_push_vsegs(dtype, q.O, peer_C, q.dl, p.V, R, E, El, me, p.d,
+                         make_sig(cm, -1, nullptr, 0, CT::kFReadyFwdC, rf, 1, kSiteCombFwd), s);
+    const PeerSignal s_out = make_sig(cm, CT::kFReadyFwdC, rf, 1, -1, nullptr, 0, kSiteFwdEnd, rf);
+    launch_sig_wait(wait_only(s_out), s);
+    prof_a2a_end(cm, s);
+    const PeerSignal s_out2 = no_wait(s_out);
+    launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, E, p.C, 1, p.C, out, s, &s_out2, q.dl.ebase);
+  } else {
+    launch_combine(dtype, q.O, q.idx, q.slot, q.gate, p.T, p.k, p.d, E, p.C, 1, p.C, out, s, nullptr, q.dl.ebase);
+  }
+  trace_mark(cm, s, "dl combine");
+}
+
+void backward_dropless(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dout, const void* tokens,
+                       const float* gate_w, const void* w1, const void* w2, void* dtokens, float* dgate_w, void* dw1,
+                       void* dw2, void* ws, cudaStream_t s) {
+  using CT = CeTransport;
+  const int dtype = p.bf16 ? 1 : 0, P = p.P, me = cm->rank, E = p.E, El = p.El, R = p.tile_rows;
+  const bool peer = P > 1;
+  CeTransport* ce = peer ? cm->ce : nullptr;
+  uint32_t* rb = peer ? ce->round_bwd() : nullptr;
+  trace_mark(cm, s, "dl bwd:start");
+  if (cm->sched) sched_a2a_imminent(cm);
+  const void* O = peer ? (const void*)q.Cb : (const void*)q.O;  // the returned expert outputs
+  if (peer) {
+    prof_a2a_begin(cm, s);
+    const PeerSignal s_disp = make_sig(cm, CT::kFreeBwd, rb, 0, CT::kFReadyBwdD, rb, 1, kSiteDispBwd);
+    launch_sig_wait(wait_only(s_disp), s);
+    void* const* peer_dO = ce->dev_ptrs(ws, p.w_dO, s, p.peer_key);
+    launch_dl_combine_bwd(dtype, dout, O, q.tok_of, q.kept, q.gate, q.dl, me, p.T, p.k, E, El, p.d, peer_dO, nullptr,
+                          q.dg, no_wait(s_disp), s);
+    launch_sig_wait(make_sig(cm, CT::kFReadyBwdD, rb, 1, -1, nullptr, 0), s);
+  } else {
+    launch_dl_combine_bwd(dtype, dout, O, q.tok_of, q.kept, q.gate, q.dl, me, p.T, p.k, E, El, p.d, nullptr, q.dO,
+                          q.dg, PeerSignal{}, s);
+  }
+  trace_mark(cm, s, "dl combine_bwd");
+  prof_begin(cm, s);
+  RowGemm d1 = dl_gemm(p, q, q.dO, w2, q.dH, p.f, p.d);
+  d1.aux = q.H;
+  d1.mask_in = q.mask;
+  launch_expert_row_gemm(dtype, d1, false, kEpiMask, s);
+  launch_expert_row_gemm(dtype, dl_gemm(p, q, q.dH, w1, q.dXe, p.d, p.f), false, kEpiNone, s);
+  if (peer) {
+    void* const* peer_dXs = ce->dev_ptrs(ws, p.w_dXs, s, p.peer_key);
+    launch_dl_push_vsegs(dtype, q.dXe, peer_dXs, q.dl, p.V, R, E, El, me, p.d,
+                         make_sig(cm, -1, nullptr, 0, CT::kFReadyBwdC, rb, 1, kSiteCombBwd), s);
+    if (cm->sched) sched_a2a_end(cm, s);
+  }
+  WGrad wg2{q.dO, q.H, dw2, q.dl.vcount, 1, 1, El, R, p.d, p.f};
+  wg2.seg_range = q.dl.vrange;
+  wg2.nseg_total = p.V;
+  WGrad wg1{q.dH, q.R, dw1, q.dl.vcount, 1, 1, El, R, p.f, p.d};
+  wg1.seg_range = q.dl.vrange;
+  wg1.nseg_total = p.V;
+  launch_expert_wgrad(dtype, wg2, s);
+  launch_expert_wgrad(dtype, wg1, s);
+  prof_end(cm, s, 4);
+  trace_mark(cm, s, "dl dgrad x2 + wgrad x2");
+  launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, E, p.k, q.dwg, dgate_w, s);
+  if (peer) {
+    const PeerSignal s_back = make_sig(cm, CT::kFReadyBwdC, rb, 1, -1, nullptr, 0, kSiteBwdEnd, rb);
+    launch_sig_wait(wait_only(s_back), s);
+    prof_a2a_end(cm, s);
+    const PeerSignal s_back2 = no_wait(s_back);
+    launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, E, p.C, 1, p.C, dtokens, s,
+              &s_back2, q.dl.ebase);
+    launch_sig_wait(make_sig(cm, -1, nullptr, 0, CT::kFreeBwd, rb, 0), s);  // backward FREE
+  } else {
+    launch_dx(dtype, q.dXe, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, E, p.C, 1, p.C, dtokens, s,
+              nullptr, q.dl.ebase);
+  }
+  trace_mark(cm, s, "dl dx");
+}
+
 }  // namespace
 
 void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* gate_w,
@@ -624,6 +869,10 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
                  lina_route* route, cudaStream_t s) {
   trace_flush(cm);
   Ptrs q = carve(p, saved, ws);
+  if (p.dropless) {  // (instrumentation flags 2 / 4 do not apply: always the full pass)
+    forward_dropless(cm, p, q, tokens, gate_w, w1, w2, out, saved, route, s);
+    return;
+  }
   const int dtype = p.bf16 ? 1 : 0;
   const bool override_r = route && route->override_routing;
   // instrumentation (lina_profile_enable): 2 = skip collectives, 4 = collectives only
@@ -767,6 +1016,10 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
                   void* dtokens, float* dgate_w, void* dw1, void* dw2, void* ws, cudaStream_t s) {
   trace_flush(cm);
   Ptrs q = carve(p, const_cast<void*>(saved), ws);
+  if (p.dropless) {
+    backward_dropless(cm, p, q, dout, tokens, gate_w, w1, w2, dtokens, dgate_w, dw1, dw2, ws, s);
+    return;
+  }
   const int dtype = p.bf16 ? 1 : 0;
   const int n = p.n;
   const bool do_comm = !(cm->flags & 2), do_compute = !(cm->flags & 4);

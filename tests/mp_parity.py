@@ -37,6 +37,9 @@ def main():
     ap.add_argument("--shared-ws", action="store_true",
                     help="with --interleave: layer B uses layer A's workspace (scratch may be shared between "
                          "layers on one communicator; lina.h)")
+    ap.add_argument("--dropless", action="store_true",
+                    help="capacity 0: the dropless layout (count exchange + unequal split, §8(f) row 4); "
+                         "the oracle runs with C = T (no drops)")
     a = ap.parse_args()
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -58,8 +61,10 @@ def main():
     X, dY = li.layer_tokens(cfg, a.seed, rank)
     tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
 
+    C_layer = 0 if a.dropless else cfg.capacity()
+
     def run(n_chunks):
-        layer = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, cfg.capacity(),
+        layer = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, C_layer,
                               n_chunks, tdt, dev)
         if a.poison:  # every byte the layer reads must be one it (or a peer) wrote this step
             layer.saved.fill_(0xFF)
@@ -74,7 +79,7 @@ def main():
         y = layer.forward(x, wg, w1, w2, want_route=True)
         finite_b = True
         if a.interleave:  # layer B's exchanges run between A's forward and backward
-            layer_b = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, cfg.capacity(),
+            layer_b = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, C_layer,
                                     n_chunks, tdt, dev)
             if a.shared_ws:
                 layer_b.workspace = layer.workspace
@@ -141,7 +146,8 @@ def main():
         Wg_all, W1_all, W2_all = li.layer_weights(cfg, a.seed)
         Xs = [li.layer_tokens(cfg, a.seed, r)[0] for r in range(world)]
         dYs = [li.layer_tokens(cfg, a.seed, r)[1] for r in range(world)]
-        fw = moe.moe_forward(Xs, Wg_all, W1_all, W2_all, cfg.k, cfg.capacity(), cfg.dtype)
+        C_ref = cfg.tokens_per_rank if a.dropless else cfg.capacity()
+        fw = moe.moe_forward(Xs, Wg_all, W1_all, W2_all, cfg.k, C_ref, cfg.dtype)
         bw = moe.moe_backward(fw, Xs, dYs, Wg_all, W1_all, W2_all, cfg.k, cfg.dtype)
         tol = 1e-5 if cfg.dtype == "f32" else 2e-2
         dwg_sum = sum(g["dwg"] for g in gathered)   # the DP allreduce of R12
@@ -156,7 +162,7 @@ def main():
         errs["dwg"] = moe.normwise_error(dwg_sum, bw.dWg)
         ok &= all(v <= tol for v in errs.values())
         print("MP_PARITY", "OK" if ok else "FAIL", f"world={world} cfg={cfg.name} T={cfg.tokens_per_rank} "
-              f"n={a.n_chunks}", " ".join(f"{k}={v:.2e}" for k, v in errs.items()), flush=True)
+              f"n={a.n_chunks}" + (" dropless" if a.dropless else ""), " ".join(f"{k}={v:.2e}" for k, v in errs.items()), flush=True)
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.broadcast(flag, 0)
     comm.close()

@@ -41,6 +41,22 @@ def test_two_ranks_interleaved_layers_shared_workspace():
     _run(2, "--config", "C2", "--tokens", "512", "--n-chunks", "2", "--interleave", "--shared-ws", port=29613)
 
 
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("cfg,tokens,extra", [
+    ("C2", 512, ["--poison", "--graph"]),
+    ("C3", 256, ["--interleave", "--shared-ws"]),
+])
+def test_two_ranks_dropless(cfg, tokens, extra):
+    """§8(f) row 4: capacity 0 — count exchange, unequal-split dispatch / return by peer stores,
+    expert GEMMs over virtual segments — against the oracle with C = T."""
+    _run(2, "--config", cfg, "--tokens", str(tokens), "--n-chunks", "1", "--dropless", *extra, port=29614)
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
+def test_four_ranks_dropless():
+    _run(4, "--config", "C2", "--tokens", "384", "--n-chunks", "1", "--dropless", "--poison", "--graph", port=29615)
+
+
 @pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
 def test_four_ranks():
     _run(4, "--config", "C2", "--tokens", "384", "--n-chunks", "4", "--check-chunks", "1", "--poison", "--graph", port=29612)

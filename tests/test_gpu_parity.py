@@ -275,3 +275,52 @@ def test_c2_chunk_invariance_bf16():
             assert np.array_equal(a[key], b[key]), (n, key)
         for key in ("dw1", "dw2"):
             assert moe.normwise_error(b[key], a[key]) <= 1e-2, (n, key)
+
+
+# ---------------------------------------------------------------- dropless layout (§8(f) row 4)
+
+
+@pytest.mark.parametrize("name,tokens,k,dtype", [("C1", 512, 1, "f32"), ("C1", 333, 2, "f32"),
+                                                 ("C2", 512, 2, "bf16"), ("C2", 63, 2, "bf16")])
+def test_dropless_single_gpu(name, tokens, k, dtype):
+    """capacity 0: no token is dropped; outputs and gradients equal the oracle with C = T."""
+    cfg, X, Wg, W1, W2, dY = _case(name, tokens=tokens, k=k, dtype=dtype)
+    g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY, capacity=0, poison=True)
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY, capacity=tokens)
+    assert (g["slot"] >= 0).all()
+    compare(cfg, g, o)
+
+
+def test_dropless_c5_shapes_two_cta():
+    """configs[4] dims at 16 experts / 1024 tokens through the dropless layout (256-row tiles)."""
+    cfg, X, Wg, W1, W2, dY = _case("C5", tokens=1024, num_experts=16)
+    g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY, capacity=0)
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY, capacity=1024)
+    compare(cfg, g, o)
+
+
+def test_dropless_skewed_routing():
+    """Zipf-skewed routing (most tokens on a few experts, some experts empty): every row of the
+    hot experts' long blocks is processed — the case capacity padding handles worst."""
+    cfg = li.with_tokens(li.CONFIGS["C4"], 512, num_experts=8, k=2, d_model=256, d_ffn=512)
+    Wg, W1, W2 = li.layer_weights(cfg, 5, "zipf")
+    X, dY = li.layer_tokens(cfg, 5, 0, "zipf", zipf_s=1.5)
+    g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY, capacity=0)
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY, capacity=512)
+    assert np.bincount(g["idx"][:, 0], minlength=8).max() > 512 * 0.3
+    compare(cfg, g, o)
+
+
+def test_dropless_footprint_against_padded_layout():
+    """The point of the dropless layout: saved + workspace bytes well below the C = T padding."""
+    import paper_2210_17223_b200 as lina
+    comm = lina.Comm(1, 0, 0)
+    cfg = li.CONFIGS["C5"]
+    T, E = cfg.tokens_per_rank, cfg.num_experts
+    dl = lina.lina_moe_workspace_size(comm, lina.make_desc(T, cfg.d_model, cfg.d_ffn, E, cfg.k, 0, 1, torch.bfloat16))
+    pad = lina.lina_moe_workspace_size(comm, lina.make_desc(T, cfg.d_model, cfg.d_ffn, E, cfg.k, T, 1, torch.bfloat16))
+    cap = lina.lina_moe_workspace_size(comm, lina.make_desc(T, cfg.d_model, cfg.d_ffn, E, cfg.k, cfg.capacity(), 1,
+                                                            torch.bfloat16))
+    print(f"C5 saved+workspace GB: dropless {sum(dl) / 1e9:.2f}, C=T {sum(pad) / 1e9:.2f}, "
+          f"C=1.25 {sum(cap) / 1e9:.2f}")
+    assert sum(dl) * 8 < sum(pad)
