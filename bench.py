@@ -71,6 +71,12 @@ def dist_env():
     return world, rank, local
 
 
+def progress(msg):
+    """Phase markers on stderr (rank 0) — a hung multi-rank run shows where it stopped."""
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -303,9 +309,11 @@ def main():
     layer.forward(x, wg, w1, w2, out=outs["y"], want_route=True)
     counts = layer.route_t["counts"].cpu().numpy()
     kept_local = int(np.minimum(counts, C).sum())
+    progress(f"{cfg.name} N={world}: layer built, {args.warmup} warm-up steps")
     for _ in range(args.warmup):
         step(x, dy)
     torch.cuda.synchronize()
+    progress("warm-up done")
 
     def barrier():
         if world > 1:
@@ -346,6 +354,7 @@ def main():
         def run_step():
             step(x, dy)
 
+    progress(f"launch mode: {launch_mode}")
     # ---------------- timed region (device time, per-step events, L2 flushed between steps)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
@@ -362,6 +371,7 @@ def main():
         barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = float(sum(step_ms))
+    progress(f"timed region done: median {np.median(step_ms):.3f} ms/step")
 
     # ---------------- the same steps launched eagerly with the library's GEMM-phase events
     # (roofline numerator) and launch counter (gpu_launches); not part of `value`
@@ -450,6 +460,7 @@ def main():
     a2a = None
     sweep = None
     if world > 1:
+        progress("exposed-communication passes")
         h = h_of(layer, n_chunks)
         a2a = dict(h)
         a2a.update({
@@ -473,6 +484,7 @@ def main():
                     lay.forward(x, wg, w1, w2, out=outs["y"])
                     lay.backward(dy, x, wg, w1, w2, outs["dx"], outs["dwg"], outs["dw1"], outs["dw2"])
                 torch.cuda.synchronize()
+                progress(f"sweep n_chunks={nch}")
                 sweep.append(h_of(lay, nch))
                 del lay
                 torch.cuda.empty_cache()
@@ -484,6 +496,7 @@ def main():
     # step i computes (the way a training input pipeline feeds the layer).
     e2e = None
     if not args.no_e2e:
+        progress("end-to-end pass")
         xp = torch.from_numpy(X_np).to(tdt).pin_memory()
         dyp = torch.from_numpy(dY_np).to(tdt).pin_memory()
         yp = [torch.empty((T, d), dtype=tdt).pin_memory() for _ in range(2)]

@@ -251,6 +251,15 @@ typedef struct {
                           num_tokens on every rank, world*E <= 512 (else UNSUPPORTED). */
   int32_t n_chunks;    /* all-to-all micro-ops per direction, 1 <= n <= C (R10) */
   lina_dtype dtype;    /* tokens, expert weights, outputs and their gradients            */
+  int32_t pack;        /* expert packing factor m (0 or 1 = none): ranks form groups
+                          of m consecutive ranks, every rank of group G hosts the same m·E/world
+                          experts [G·m·E_l, (G+1)·m·E_l) (w1/w2/dw1/dw2 hold those m·E_l experts,
+                          E_l = E/world), source rank s sends its rows of those experts to the
+                          group member with rank % m == s % m (so a group's own rows stay on the
+                          device), and the expert gradients are summed over the group (an NCCL
+                          allreduce on a group communicator split off on first use).  m must
+                          divide world; m > 1 runs on the variable layout (as capacity 0, with
+                          or without a capacity bound) and has its requirements. */
 } lina_moe_desc;
 
 /* Optional routing tensors (device, caller-owned; NULL fields are skipped).
@@ -382,6 +391,37 @@ lina_status lina_sched_stats(lina_comm* comm, int64_t* issued, int64_t* deferred
 
 
 /* ------------------------------------------------------------------------ */
+/* Expert packing (§4.2; §6.1; §7.1; §8(f) row 3)          */
+/* ------------------------------------------------------------------------ */
+/* The packing rule: "starting with one expert per device, it iteratively increases the
+ * number of experts per device in powers of two, until the FFN computation exceeds that
+ * of the all-to-all micro-op": *pack_next = 2·pack when ffn_ms < a2a_ms and 2·pack
+ * divides world, else pack.  Host only.  INVALID_ARGUMENT for pack not a power of two
+ * dividing world, negative/NaN times or a NULL output. */
+lina_status lina_pack_decide(int32_t world, int32_t pack, double ffn_ms, double a2a_ms, int32_t* pack_next);
+/* The packing controller (host state): "adjusted after 10 training steps ...
+ * every four steps".  Feed every training step's FFN and all-to-all micro-op times (e.g.
+ * lina_profile gemm_ms / a2a_op_ms per step, the max over ranks so that every rank decides
+ * the same); at step start_step and every `every` steps after, the means since the last
+ * decision go through lina_pack_decide.  *pack = the factor to run with from the next step;
+ * *changed (nullable) = 1 when it just changed (then re-pack the weights with
+ * lina_pack_weights and run the layer with desc.pack = *pack). */
+typedef struct lina_pack_ctl lina_pack_ctl;
+lina_status lina_pack_ctl_create(int32_t world, int32_t start_step, int32_t every, lina_pack_ctl** out);
+lina_status lina_pack_ctl_step(lina_pack_ctl* ctl, double ffn_ms, double a2a_ms, int32_t* pack, int32_t* changed);
+lina_status lina_pack_ctl_destroy(lina_pack_ctl* ctl);
+/* The one-time synchronous parameter exchange between packed devices: w_from
+ * holds this rank's experts under pack_from ([m0·E_l][expert_elems], experts
+ * [(rank/m0)·m0·E_l, ...)), w_to receives those under pack_to ([m1·E_l][expert_elems]);
+ * each expert is copied from a rank hosting it under pack_from (itself when it can) over
+ * peer memory.  Collective: every rank calls it with the same factors; the host blocks
+ * (barrier before and after, so no rank changes w_from while another reads it).  Call
+ * once per weight tensor (w1, w2).  Needs the fused or ce transport at world > 1. */
+lina_status lina_pack_weights(lina_comm* comm, int32_t num_experts, int32_t pack_from, int32_t pack_to,
+                              size_t expert_elems, lina_dtype dtype, const void* w_from, void* w_to,
+                              lina_stream stream);
+
+/* ------------------------------------------------------------------------ */
 /* Instrumentation (bench.py / tests): counters since the last read.          */
 /* ------------------------------------------------------------------------ */
 typedef struct {
@@ -395,6 +435,11 @@ typedef struct {
   double gemm_in_a2a_ms;   /* expert-GEMM phase time inside those windows: / a2a_window_ms = the
                               paper's pipelining efficiency                            */
   int64_t a2a_windows;     /* number of windows summed                                      */
+  double a2a_op_ms;        /* variable layout (capacity 0 / pack > 1): summed device time of the
+                              all-to-all micro-ops themselves (count exchange + dispatch rows, and
+                              the return rows, each up to the peers' READY) — the packing
+                              controller's a2a micro-op time                         */
+  int64_t a2a_ops;         /* number of micro-op intervals summed into a2a_op_ms             */
 } lina_profile;
 
 /* Bit flags: 1 = record timing events around the expert-GEMM phases of every forward /

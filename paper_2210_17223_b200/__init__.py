@@ -12,6 +12,7 @@ from .lina import (ABI_SYMBOLS, Comm, LinaError, MoELayer, PopProfile, lina_allr
                    lina_moe_infer_workspace_size,
                    lina_moe_workspace_size, lina_placement_compute, lina_profile_enable,
                    lina_phase_two_check, lina_profile_read, lina_replica_split,
-                   lina_sched_config, lina_sched_stats, lina_version, load, make_desc)
+                   lina_sched_config, lina_sched_stats, lina_version, load, make_desc,
+                   lina_infer_last_rows, lina_pack_decide, lina_pack_weights, PackController)
 
 load()

@@ -54,6 +54,18 @@ void prof_a2a_end(lina_comm* cm, cudaStream_t s) {
   LINA_CUDA_CHECK(cudaEventRecord(b, s));
   cm->prof_a2a.back().second = b;
 }
+void prof_comm_begin(lina_comm* cm, cudaStream_t s) {
+  if (!cm->prof) return;
+  cudaEvent_t a = prof_event(cm);
+  LINA_CUDA_CHECK(cudaEventRecord(a, s));
+  cm->prof_comm.push_back({a, nullptr});
+}
+void prof_comm_end(lina_comm* cm, cudaStream_t s) {
+  if (!cm->prof || cm->prof_comm.empty() || cm->prof_comm.back().second) return;
+  cudaEvent_t b = prof_event(cm);
+  LINA_CUDA_CHECK(cudaEventRecord(b, s));
+  cm->prof_comm.back().second = b;
+}
 void prof_end(lina_comm* cm, cudaStream_t s, int gemm_launches) {
   if (!cm->prof || cm->prof_gemm.empty() || cm->prof_gemm.back().second) return;
   cudaEvent_t b = prof_event(cm);
@@ -111,8 +123,11 @@ void validate_desc(const lina_moe_desc* d, int world, bool static_placement) {
   if (d->capacity < 0) v.push_back("capacity < 0 (0 = dropless)");
   if (d->n_chunks < 1 || d->n_chunks > 32 || (d->capacity >= 1 && d->n_chunks > d->capacity))
     v.push_back("n_chunks not in [1, min(C, 32)]");
-  if (static_placement && d->capacity == 0 && d->n_chunks != 1)
-    v.push_back("dropless (capacity 0) needs n_chunks == 1");
+  const int pack = d->pack > 1 ? d->pack : 1;
+  if (d->pack < 0 || (pack & (pack - 1)) != 0 || world % pack != 0)
+    v.push_back("pack not a power of two dividing world (0/1 = no packing)");
+  if (static_placement && (d->capacity == 0 || pack > 1) && d->n_chunks != 1)
+    v.push_back("the variable layout (capacity 0 or pack > 1) needs n_chunks == 1");
   if (d->d_model > 0 && (d->d_model * elt) % 16 != 0) v.push_back("d_model*elt % 16 != 0");
   if (d->d_ffn > 0 && (d->d_ffn * elt) % 16 != 0) v.push_back("d_ffn*elt % 16 != 0");
   if (d->d_model > 0 && d->d_model % 16 != 0) v.push_back("d_model % 16 != 0");
@@ -181,14 +196,14 @@ void validate_placement_tables(const lina_placement& pl, int E, int N, std::vect
 // Dropless training across ranks runs on the fused transport only (its exchanges are peer
 // stores with in-kernel flags); one GPU runs both dtypes.
 void check_dropless(const lina_comm* cm, const lina_moe_desc* d) {
-  if (d->capacity != 0 || cm->world == 1) return;
+  if ((d->capacity != 0 && d->pack <= 1) || cm->world == 1) return;
   std::vector<std::string> v;
   if (cm->transport != 2 || !cm->ce) v.push_back("LINA_TRANSPORT must be fused");
   if (d->dtype != LINA_BF16) v.push_back("dtype must be bf16");
   if (d->d_model % 256 != 0 || d->d_ffn % 256 != 0) v.push_back("d_model and d_ffn must be multiples of 256");
   if (cm->world > 8 || cm->world * d->num_experts > 512) v.push_back("world <= 8 and world*E <= 512");
   if (v.empty()) return;
-  std::string m = "dropless training (capacity 0) across ranks:";
+  std::string m = "the variable layout (capacity 0 / pack > 1) across ranks:";
   for (auto& x : v) m += " [" + x + "]";
   throw StatusError{LINA_ERR_UNSUPPORTED, m};
 }
@@ -301,6 +316,8 @@ lina_status lina_comm_destroy(lina_comm* cm) {
     cm->sched = nullptr;
     delete cm->ce;
     cm->ce = nullptr;
+    for (auto& kv : cm->group_comms) ncclCommDestroy(kv.second);
+    cm->group_comms.clear();
     if (cm->dp) ncclCommDestroy(cm->dp);
     if (cm->ep_comb) ncclCommDestroy(cm->ep_comb);
     if (cm->ep_disp) ncclCommDestroy(cm->ep_disp);
@@ -666,6 +683,30 @@ lina_status lina_moe_infer_forward_two_phase(lina_comm* cm, const lina_moe_desc*
                      "lina_moe_infer_forward_two_phase");
 }
 
+lina_status lina_pack_weights(lina_comm* cm, int32_t num_experts, int32_t pack_from, int32_t pack_to,
+                              size_t expert_elems, lina_dtype dtype, const void* w_from, void* w_to,
+                              lina_stream stream) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    if (!cm) throw ArgError{"comm is NULL"};
+    const int P = cm->world;
+    auto pow2_div = [&](int m) { return m >= 1 && (m & (m - 1)) == 0 && P % m == 0; };
+    if (num_experts < 1 || num_experts % P != 0) v.push_back("num_experts not a positive multiple of world");
+    if (!pow2_div(pack_from)) v.push_back("pack_from not a power of two dividing world");
+    if (!pow2_div(pack_to)) v.push_back("pack_to not a power of two dividing world");
+    if (dtype != LINA_F32 && dtype != LINA_BF16) v.push_back("dtype not LINA_F32/LINA_BF16");
+    if (expert_elems == 0) v.push_back("expert_elems == 0");
+    need(v, w_from, "w_from");
+    need(v, w_to, "w_to");
+    if (P > 1 && !cm->ce) v.push_back("world > 1 needs the fused or ce transport (peer mappings)");
+    raise_if(v, "lina_pack_weights");
+    LINA_CUDA_CHECK(cudaSetDevice(cm->device));
+    pack_weights(cm, num_experts, pack_from, pack_to, expert_elems * (dtype == LINA_BF16 ? 2 : 4), w_from, w_to,
+                 (cudaStream_t)stream);
+    return LINA_OK;
+  });
+}
+
 lina_status lina_infer_last_rows(const lina_comm* cm, int32_t* recv_rows, int32_t* sent_rows) {
   return guarded([&] {
     if (!cm) throw ArgError{"comm is NULL"};
@@ -729,8 +770,10 @@ lina_status lina_profile_read(lina_comm* cm, lina_profile* out) {
     double ms = 0.0;
     int64_t phases = 0;
     // timestamps relative to one reference event (all events are on this device)
-    cudaEvent_t ref = !cm->prof_gemm.empty() ? cm->prof_gemm.front().first
-                                             : (!cm->prof_a2a.empty() ? cm->prof_a2a.front().first : nullptr);
+    cudaEvent_t ref = !cm->prof_gemm.empty()  ? cm->prof_gemm.front().first
+                      : !cm->prof_a2a.empty() ? cm->prof_a2a.front().first
+                      : !cm->prof_comm.empty() ? cm->prof_comm.front().first
+                                               : nullptr;
     auto at = [&](cudaEvent_t e) {
       float t = 0.f;
       LINA_CUDA_CHECK(cudaEventSynchronize(e));
@@ -758,7 +801,14 @@ lina_status lina_profile_read(lina_comm* cm, lina_profile* out) {
       ++nwin;
       for (auto& g : gemm_iv) busy += std::max(0.0, std::min(b, g.second) - std::max(a, g.first));
     }
-    for (auto* v : {&cm->prof_gemm, &cm->prof_a2a}) {
+    double comm = 0.0;
+    int64_t ncomm = 0;
+    for (auto& pr : cm->prof_comm) {
+      if (!pr.second) continue;
+      comm += at(pr.second) - at(pr.first);
+      ++ncomm;
+    }
+    for (auto* v : {&cm->prof_gemm, &cm->prof_a2a, &cm->prof_comm}) {
       for (auto& pr : *v) {
         if (pr.second) cm->prof_pool.push_back(pr.second);
         cm->prof_pool.push_back(pr.first);
@@ -772,6 +822,8 @@ lina_status lina_profile_read(lina_comm* cm, lina_profile* out) {
     out->a2a_window_ms = win;
     out->gemm_in_a2a_ms = busy;
     out->a2a_windows = nwin;
+    out->a2a_op_ms = comm;
+    out->a2a_ops = ncomm;
     cm->prof_gemm_launches = 0;
     return LINA_OK;
   });

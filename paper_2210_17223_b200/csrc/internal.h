@@ -6,6 +6,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <deque>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -54,7 +55,8 @@ struct Plan {
   uint64_t peer_key;  // hash of the peer-visible geometry (checked across ranks on first mapping)
   // dropless layout (capacity == 0; §8(f) row 4): V virtual segments of tile_rows rows per
   // receive buffer, T·k compact rows per source buffer, the count table and the layout tables
-  bool dropless = false;
+  bool dropless = false;  // the variable layout (capacity 0 and / or pack > 1)
+  int pack = 1;           // expert packing factor m (El = m·E/P experts hosted per rank)
   int V = 0;
   size_t s_allc = 0, s_tab = 0;
   size_t rows_send() const { return (size_t)n * E * Cm; }
@@ -86,6 +88,7 @@ struct lina_comm {
   int flags = 0;  // lina_profile_enable bits: 1 timing events, 2 skip collectives, 4 collectives only
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_gemm;  // recorded (start, end) pairs
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_a2a;   // all-to-all windows of fused passes
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_comm;  // all-to-all micro-op intervals (variable layout)
   std::vector<cudaEvent_t> prof_pool;                          // free timing events
   int64_t prof_gemm_launches = 0;
   lina::Trace* trace = nullptr;  // LINA_TRACE=1 phase trace (trace.cpp), diagnostics only
@@ -95,6 +98,8 @@ struct lina_comm {
   size_t pinned_bytes = 0;
   // rows of the last inference call (lina_infer_last_rows): [world] each
   std::vector<int32_t> inf_recv_rows, inf_sent_rows;
+  // expert packing: one NCCL communicator per packing factor m (the rank's group of m)
+  std::map<int, ncclComm_t> group_comms;
 };
 
 namespace lina {
@@ -104,6 +109,9 @@ void prof_end(lina_comm* cm, cudaStream_t s, int gemm_launches);
 // open/close one all-to-all window of a fused pass (first mover launched .. last micro-op landed)
 void prof_a2a_begin(lina_comm* cm, cudaStream_t s);
 void prof_a2a_end(lina_comm* cm, cudaStream_t s);
+// open/close one all-to-all micro-op (its kernels and the wait for the peers' READY)
+void prof_comm_begin(lina_comm* cm, cudaStream_t s);
+void prof_comm_end(lina_comm* cm, cudaStream_t s);
 // Phase trace (trace.cpp): no-ops unless the comm was created with LINA_TRACE=1.
 Trace* trace_create();
 void trace_mark(lina_comm* cm, cudaStream_t s, const char* label);

@@ -135,16 +135,18 @@ struct DlTables {
 };
 void launch_dl_counts(const int* kept, int* const* peer_allc, int P, int me, int E, const PeerSignal& sig,
                       cudaStream_t s);
-void launch_dl_layout(const int* allc, int P, int E, int El, int me, int R, int V, const DlTables& t, cudaStream_t s);
-// peer_dst: device array [P] of the owners' buffers (fused transport), or NULL and local_dst
+void launch_dl_layout(const int* allc, int P, int E, int El, int m, int me, int R, int V, const DlTables& t,
+                      cudaStream_t s);
+// peer_dst: device array [P] of the owners' buffers (fused transport), or NULL and local_dst.
+// El = experts hosted per rank, m = packing factor (owner of my rows of e: (e/El)*m + me%m).
 void launch_dl_permute(int dtype, const void* X, const int* tok_of, const int* kept, const DlTables& t, int me,
-                       int T, int k, int E, int El, int d, void* const* peer_dst, void* local_dst,
+                       int T, int C, int k, int E, int El, int m, int d, void* const* peer_dst, void* local_dst,
                        const PeerSignal& sig, cudaStream_t s);
 void launch_dl_combine_bwd(int dtype, const void* dY, const void* O, const int* tok_of, const int* kept,
-                           const float* gate, const DlTables& t, int me, int T, int k, int E, int El, int d,
+                           const float* gate, const DlTables& t, int me, int T, int C, int k, int E, int El, int m, int d,
                            void* const* peer_dst, void* local_dst, float* dg, const PeerSignal& sig, cudaStream_t s);
 void launch_dl_push_vsegs(int dtype, const void* src, void* const* peer, const DlTables& t, int V, int R, int E,
-                          int El, int me, int d, const PeerSignal& sig, cudaStream_t s);
+                          int El, int m, int me, int d, const PeerSignal& sig, cudaStream_t s);
 // Output tiles of a row GEMM stored through per-owner tensor maps (peer memory):
 // segment (c, s, el) of the receive layout goes to map s at segment c*E + me*El + el.
 struct PeerStore {

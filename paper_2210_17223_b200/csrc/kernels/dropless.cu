@@ -47,27 +47,31 @@ __global__ void dl_counts_kernel(const int* __restrict__ kept, int* const* __res
 }
 
 // 1 CTA (256 threads): the layout tables from allc [P][E].  kMaxPE = P·E <= 8·64.
+// Expert packing m (pack): rank o hosts the El = m·E/P experts of group o / m and receives
+// from the Q = P/m sources s with s % m == o % m; its blocks are (el, j), j = s / m, so
+// every owner has El·Q = E blocks.
 constexpr int kMaxPE = 512;
-__global__ void __launch_bounds__(256) dl_layout_kernel(const int* __restrict__ allc, int P, int E, int El, int me,
-                                                        int R, int V, DlTables t) {
+__global__ void __launch_bounds__(256) dl_layout_kernel(const int* __restrict__ allc, int P, int E, int El, int m,
+                                                        int me, int R, int V, DlTables t) {
   pdl_enter();
   __shared__ int cnt[kMaxPE];
-  __shared__ int vb[kMaxPE];     // [o][el][s]: first virtual segment of block (el, s) at owner o
+  __shared__ int vb[kMaxPE];     // [o][el][j]: first virtual segment of block (el, j) at owner o
   __shared__ int soff[kMaxPE];   // [s][e]: compact source offsets
   __shared__ int used[8];        // segments used per owner
+  const int Q = P / m;
   for (int i = threadIdx.x; i < P * E; i += blockDim.x) cnt[i] = allc[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int w = warp; w < 2 * P; w += blockDim.x >> 5) {
-    if (w < P) {  // owner o = w: exclusive prefix over (el, s) of ceil(count / R)
-      const int o = w, n = El * P;
+    if (w < P) {  // owner o = w: exclusive prefix over its blocks (el, j) of ceil(count / R)
+      const int o = w;
       int run = 0;
-      for (int b = 0; b < n; b += 32) {
+      for (int b = 0; b < E; b += 32) {
         const int i = b + lane;
         int v = 0;
-        if (i < n) {
-          const int el = i / P, s = i % P;
-          v = (cnt[s * E + o * El + el] + R - 1) / R;
+        if (i < E) {
+          const int el = i / Q, s = (i % Q) * m + o % m;
+          v = (cnt[s * E + (o / m) * El + el] + R - 1) / R;
         }
         int x = v;  // inclusive warp scan
 #pragma unroll
@@ -75,7 +79,7 @@ __global__ void __launch_bounds__(256) dl_layout_kernel(const int* __restrict__ 
           const int y = __shfl_up_sync(0xffffffffu, x, dd);
           if (lane >= dd) x += y;
         }
-        if (i < n) vb[o * n + i] = run + x - v;
+        if (i < E) vb[o * E + i] = run + x - v;
         run += __shfl_sync(0xffffffffu, x, 31);
       }
       if (lane == 0) used[o] = run;
@@ -98,19 +102,18 @@ __global__ void __launch_bounds__(256) dl_layout_kernel(const int* __restrict__ 
     }
   }
   __syncthreads();
-  const int n = El * P;
   for (int i = threadIdx.x; i < P * E; i += blockDim.x) t.soff[i] = soff[i];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    const int o = e / El, el = e % El;
-    t.dbase[e] = vb[o * n + el * P + me] * R;
-    t.ebase[e] = P > 1 ? soff[me * E + e] : vb[el * P] * R;  // (P = 1: o = 0, s = 0)
+    const int o = (e / El) * m + me % m, el = e % El;  // the group member that takes my rows of e
+    t.dbase[e] = vb[o * E + el * Q + me / m] * R;
+    t.ebase[e] = P > 1 ? soff[me * E + e] : vb[el] * R;  // (P = 1: m = Q = 1, o = 0)
   }
   const int U = used[me];
-  // this rank's segments: block (el, s) -> ceil(c / R) segments of R rows
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int el = i / P, s = i % P;
-    const int c = cnt[s * E + me * El + el];
-    const int b = vb[me * n + i];
+  // this rank's segments: block (el, j) -> ceil(c / R) segments of R rows
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {
+    const int el = i / Q, s = (i % Q) * m + me % m;
+    const int c = cnt[s * E + (me / m) * El + el];
+    const int b = vb[me * E + i];
     for (int j = 0; j * R < c; ++j) {
       t.vcount[b + j] = min(R, c - j * R);
       t.vexp[b + j] = el;
@@ -126,8 +129,8 @@ __global__ void __launch_bounds__(256) dl_layout_kernel(const int* __restrict__ 
   }
   for (int v = threadIdx.x; v <= V; v += blockDim.x) t.mtp[v] = min(v, U);  // one M tile per used segment
   for (int el = threadIdx.x; el < El; el += blockDim.x) {
-    t.vrange[2 * el] = vb[me * n + el * P];
-    t.vrange[2 * el + 1] = el + 1 < El ? vb[me * n + (el + 1) * P] : U;
+    t.vrange[2 * el] = vb[me * E + el * Q];
+    t.vrange[2 * el + 1] = el + 1 < El ? vb[me * E + (el + 1) * Q] : U;
   }
 }
 
@@ -147,8 +150,9 @@ __device__ __forceinline__ int expert_of_row(const int* __restrict__ off, int E,
 template <bool BWD>
 __global__ void __launch_bounds__(256) dl_rows_kernel(const uint4* __restrict__ X, const int* __restrict__ tok_of,
                                                       const int* __restrict__ kept, const int* __restrict__ soff_me,
-                                                      const int* __restrict__ dbase, int total, int T, int k, int E,
-                                                      int El, int nv, uint4* const* __restrict__ dst,
+                                                      const int* __restrict__ dbase, const int* __restrict__ total_p,
+                                                      int C, int k, int E, int El, int m, int me, int nv,
+                                                      uint4* const* __restrict__ dst,
                                                       uint4* __restrict__ dst_local,  // when dst == NULL
                                                       // BWD: dY = X, rows of O at ebase, gate, dg out
                                                       const uint4* __restrict__ O, const int* __restrict__ ebase,
@@ -164,6 +168,7 @@ __global__ void __launch_bounds__(256) dl_rows_kernel(const uint4* __restrict__ 
   // peer stores: every rank starts with the rows of owner (me + 1) % P (its first expert
   // rot_expert), so at any moment the ranks write to different owners (no incast)
   const int rot = rot_expert >= 0 ? off[rot_expert] : 0;
+  const int total = *total_p;  // this rank's kept rows (T·k when nothing is dropped)
   const int lane = threadIdx.x & 31;
   const long long items = (long long)total + (long long)E * 64;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
@@ -176,9 +181,9 @@ __global__ void __launch_bounds__(256) dl_rows_kernel(const uint4* __restrict__ 
       const int r = (int)it;
       const int e = expert_of_row(off, E, total, r);
       const int q = r - off[e];
-      const int a = tok_of[(size_t)e * T + q];
+      const int a = tok_of[(size_t)e * C + q];  // (tok_of pitch: the capacity C)
       const int t = a / k;
-      uint4* to = (dst ? dst[e / El] : dst_local) + (size_t)(dbase[e] + q) * nv;
+      uint4* to = (dst ? dst[(e / El) * m + me % m] : dst_local) + (size_t)(dbase[e] + q) * nv;
       const uint4* xr = X + (size_t)t * nv;
       if constexpr (!BWD) {
         for (int v = lane; v < nv; v += 32) to[v] = xr[v];
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(256) dl_rows_kernel(const uint4* __restrict__ 
       const int e = (int)(p / 64), i = (int)(p % 64);
       const int c = kept[e], q = c + i;
       if (q >= ((c + 63) & ~63)) continue;
-      uint4* to = (dst ? dst[e / El] : dst_local) + (size_t)(dbase[e] + q) * nv;
+      uint4* to = (dst ? dst[(e / El) * m + me % m] : dst_local) + (size_t)(dbase[e] + q) * nv;
       for (int v = lane; v < nv; v += 32) to[v] = make_uint4(0, 0, 0, 0);
     }
   }
@@ -223,7 +228,8 @@ __global__ void __launch_bounds__(256) dl_combine_bwd_f32_kernel(const float4* _
                                                                  const int* __restrict__ tok_of,
                                                                  const int* __restrict__ kept,
                                                                  const int* __restrict__ soff_me,
-                                                                 const int* __restrict__ dbase, int total, int T,
+                                                                 const int* __restrict__ dbase,
+                                                                 const int* __restrict__ total_p, int C,
                                                                  int k, int E, int nv, float4* __restrict__ dO,
                                                                  const float4* __restrict__ O,
                                                                  const int* __restrict__ ebase,
@@ -233,6 +239,7 @@ __global__ void __launch_bounds__(256) dl_combine_bwd_f32_kernel(const float4* _
   __shared__ int off[65];
   for (int e = threadIdx.x; e < E; e += blockDim.x) off[e] = soff_me[e];
   __syncthreads();
+  const int total = *total_p;
   const int lane = threadIdx.x & 31;
   const long long items = (long long)total + (long long)E * 64;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
@@ -241,7 +248,7 @@ __global__ void __launch_bounds__(256) dl_combine_bwd_f32_kernel(const float4* _
       const int r = (int)w;
       const int e = expert_of_row(off, E, total, r);
       const int q = r - off[e];
-      const int a = tok_of[(size_t)e * T + q];
+      const int a = tok_of[(size_t)e * C + q];  // (tok_of pitch: the capacity C)
       const float4* yr = dY + (size_t)(a / k) * nv;
       const float4* orow = O + (size_t)(ebase[e] + q) * nv;
       float4* to = dO + (size_t)(dbase[e] + q) * nv;
@@ -272,12 +279,12 @@ __global__ void __launch_bounds__(256) dl_combine_bwd_f32_kernel(const float4* _
 // grid (x, V): the valid rows of segment v to source vsrc[v] at soff[s][me*El + el] + q0.
 __global__ void __launch_bounds__(256) dl_push_vsegs_kernel(const uint4* __restrict__ src,
                                                             uint4* const* __restrict__ peer, DlTables t, int R,
-                                                            int E, int El, int me, int nv, PeerSignal sig) {
+                                                            int E, int El, int m, int me, int nv, PeerSignal sig) {
   pdl_enter();
   const int v = blockIdx.y;
   const int rows = t.vcount[v];
   if (rows > 0) {
-    const int s = t.vsrc[v], e = me * El + t.vexp[v];
+    const int s = t.vsrc[v], e = (me / m) * El + t.vexp[v];  // (my group's expert)
     const uint4* from = src + (size_t)v * R * nv;
     uint4* to = peer[s] + (size_t)(t.soff[s * E + e] + t.vq0[v]) * nv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -288,8 +295,12 @@ __global__ void __launch_bounds__(256) dl_push_vsegs_kernel(const uint4* __restr
   if (threadIdx.x == 0) sig_post_last(sig);
 }
 
-int P_of(int E, int El) { return E / El; }
-int rot_expert(void* const* peer, int me, int P, int El) { return (peer && P > 1) ? ((me + 1) % P) * El : -1; }
+// first expert whose rows go to rank (me + 1) % P: the group of that rank (packing m)
+int rot_expert(void* const* peer, int me, int P, int El, int m) {
+  if (!peer || P <= 1) return -1;
+  const int o = (me + 1) % P;
+  return (o % m == me % m) ? (o / m) * El : ((me / m + 1) % (P / m)) * El;
+}
 
 int row_blocks(long long items) {
   const long long warps = std::max(1LL, items);
@@ -304,46 +315,48 @@ void launch_dl_counts(const int* kept, int* const* peer_allc, int P, int me, int
   LINA_LAUNCH_CHECK();
 }
 
-void launch_dl_layout(const int* allc, int P, int E, int El, int me, int R, int V, const DlTables& t, cudaStream_t s) {
+void launch_dl_layout(const int* allc, int P, int E, int El, int m, int me, int R, int V, const DlTables& t,
+                      cudaStream_t s) {
   if (P * E > kMaxPE || P > 8) throw CudaError{"dropless layout: P*E > 512 or P > 8"};
-  launch_k(dl_layout_kernel, dim3(1), dim3(256), 0, s, allc, P, E, El, me, R, V, t);
+  launch_k(dl_layout_kernel, dim3(1), dim3(256), 0, s, allc, P, E, El, m, me, R, V, t);
   LINA_LAUNCH_CHECK();
 }
 
 void launch_dl_permute(int dtype, const void* X, const int* tok_of, const int* kept, const DlTables& t, int me,
-                       int T, int k, int E, int El, int d, void* const* peer_dst, void* local_dst,
+                       int T, int C, int k, int E, int El, int m, int d, void* const* peer_dst, void* local_dst,
                        const PeerSignal& sig, cudaStream_t s) {
   const int elt = dtype == 1 ? 2 : 4;
-  const int total = T * k;  // dropless: every assignment is kept
-  launch_k(dl_rows_kernel<false>, dim3(row_blocks(total + 64LL * E)), dim3(256), 0, s, (const uint4*)X, tok_of, kept,
-           t.soff + (size_t)me * E, t.dbase, total, T, k, E, El, d * elt / 16, (uint4* const*)peer_dst,
-           (uint4*)local_dst, (const uint4*)nullptr, (const int*)nullptr, (const float*)nullptr, (float*)nullptr, sig,
-           rot_expert(peer_dst, me, P_of(E, El), El));
+  const int P = E / El * m;
+  launch_k(dl_rows_kernel<false>, dim3(row_blocks((long long)T * k + 64LL * E)), dim3(256), 0, s, (const uint4*)X,
+           tok_of, kept, t.soff + (size_t)me * E, t.dbase, t.src_total + me, C, k, E, El, m, me, d * elt / 16,
+           (uint4* const*)peer_dst, (uint4*)local_dst, (const uint4*)nullptr, (const int*)nullptr,
+           (const float*)nullptr, (float*)nullptr, sig, rot_expert(peer_dst, me, P, El, m));
   LINA_LAUNCH_CHECK();
 }
 
 void launch_dl_combine_bwd(int dtype, const void* dY, const void* O, const int* tok_of, const int* kept,
-                           const float* gate, const DlTables& t, int me, int T, int k, int E, int El, int d,
+                           const float* gate, const DlTables& t, int me, int T, int C, int k, int E, int El, int m, int d,
                            void* const* peer_dst, void* local_dst, float* dg, const PeerSignal& sig, cudaStream_t s) {
-  const int total = T * k;
+  const int P = E / El * m;
+  const dim3 grid(row_blocks((long long)T * k + 64LL * E));
   if (dtype == 1) {
-    launch_k(dl_rows_kernel<true>, dim3(row_blocks(total + 64LL * E)), dim3(256), 0, s, (const uint4*)dY, tok_of,
-             kept, t.soff + (size_t)me * E, t.dbase, total, T, k, E, El, d * 2 / 16, (uint4* const*)peer_dst,
-             (uint4*)local_dst, (const uint4*)O, t.ebase, gate, dg, sig, rot_expert(peer_dst, me, P_of(E, El), El));
+    launch_k(dl_rows_kernel<true>, grid, dim3(256), 0, s, (const uint4*)dY, tok_of, kept, t.soff + (size_t)me * E,
+             t.dbase, t.src_total + me, C, k, E, El, m, me, d * 2 / 16, (uint4* const*)peer_dst, (uint4*)local_dst,
+             (const uint4*)O, t.ebase, gate, dg, sig, rot_expert(peer_dst, me, P, El, m));
   } else {
     if (peer_dst) throw CudaError{"dropless fp32 path is single-GPU"};
-    launch_k(dl_combine_bwd_f32_kernel, dim3(row_blocks(total + 64LL * E)), dim3(256), 0, s, (const float4*)dY,
-             tok_of, kept, t.soff + (size_t)me * E, t.dbase, total, T, k, E, d / 4, (float4*)local_dst,
+    launch_k(dl_combine_bwd_f32_kernel, grid, dim3(256), 0, s, (const float4*)dY, tok_of, kept,
+             t.soff + (size_t)me * E, t.dbase, t.src_total + me, C, k, E, d / 4, (float4*)local_dst,
              (const float4*)O, t.ebase, gate, dg);
   }
   LINA_LAUNCH_CHECK();
 }
 
 void launch_dl_push_vsegs(int dtype, const void* src, void* const* peer, const DlTables& t, int V, int R, int E,
-                          int El, int me, int d, const PeerSignal& sig, cudaStream_t s) {
+                          int El, int m, int me, int d, const PeerSignal& sig, cudaStream_t s) {
   const int elt = dtype == 1 ? 2 : 4;
   dim3 grid(std::max(1, std::min(8, R / 32)), std::max(1, V));
-  launch_k(dl_push_vsegs_kernel, grid, dim3(256), 0, s, (const uint4*)src, (uint4* const*)peer, t, R, E, El, me,
+  launch_k(dl_push_vsegs_kernel, grid, dim3(256), 0, s, (const uint4*)src, (uint4* const*)peer, t, R, E, El, m, me,
            d * elt / 16, sig);
   LINA_LAUNCH_CHECK();
 }

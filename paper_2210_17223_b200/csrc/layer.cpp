@@ -60,15 +60,22 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
     o = align_up(o + bytes);
     return at;
   };
-  if (dsc.capacity == 0) {  // dropless (§8(f) row 4): count exchange + unequal split
+  const int pack = dsc.pack > 1 ? dsc.pack : 1;
+  if (dsc.capacity == 0 || pack > 1) {
+    // variable layout: dropless (capacity 0, §8(f) row 4: count exchange + unequal split)
+    // and/or expert packing (pack > 1: m·E_l experts per rank, groups of m ranks)
     p.dropless = true;
-    p.C = std::max(p.T, 1);  // route slots within (source, expert): never dropped
+    p.pack = pack;
+    p.El = pack * p.E / p.P;  // experts hosted per rank
+    p.C = dsc.capacity > 0 ? dsc.capacity : std::max(p.T, 1);  // capacity 0: slots never run out
     p.n = 1;
     const int R = p.tile_rows;
     p.Cm = R;
-    // virtual segments: Σ_{(el, s)} ceil(c / R) <= rows / R + P·E_l, rows <= P·T·min(k, E_l)
-    const long long rows = (long long)p.P * p.T * std::min(p.k, p.El);
-    p.V = (int)(rows / R + (long long)p.P * p.El + 1);
+    // virtual segments: Σ_{(el, source)} ceil(c / R) <= rows / R + (P/m)·m·E_l, with the
+    // P/m sources of a rank sending it rows <= (P/m)·T·min(k, hosted experts)
+    const long long rows =
+        (long long)(p.P / pack) * std::min((long long)p.T * std::min(p.k, p.El), (long long)p.C * p.El);
+    p.V = (int)(rows / R + (long long)p.E + 1);
     const size_t vrows = (size_t)p.V * R, srows = (size_t)p.T * p.k;
     const size_t tab_ints = 2 * E + (size_t)p.P * E + p.P + 4 * (size_t)p.V + (p.V + 1) + 2 * (size_t)p.El;
     // peer-visible regions first (T-independent offsets are not possible here: the
@@ -98,6 +105,7 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
     p.ws_bytes = o;
     uint64_t h = 1469598103934665603ull;
     for (uint64_t v : {(uint64_t)0xd1, (uint64_t)p.T, (uint64_t)p.k, (uint64_t)p.V, (uint64_t)R, (uint64_t)p.E,
+                       (uint64_t)p.pack, (uint64_t)p.C,
                        (uint64_t)p.P, (uint64_t)p.d, (uint64_t)p.f, (uint64_t)p.dt, (uint64_t)p.s_R, (uint64_t)p.s_C,
                        (uint64_t)p.s_allc, (uint64_t)p.w_dO, (uint64_t)p.w_dXs})
       for (int b = 0; b < 8; ++b) h = (h ^ ((v >> (8 * b)) & 0xff)) * 1099511628211ull;
@@ -599,7 +607,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   void* const* peer_dO = ce.dev_ptrs(ws, p.w_dO, s, p.peer_key);
   std::vector<char*> dxs;
   const PeerStore st = peer_store(ce, "bwdC:", ws, p.w_dXs, p, me, dxs, s);
-  if (cm->sched) sched_a2a_imminent(cm);
+  if (cm->sched) sched_a2a_imminent(cm, s);
   // backward dispatch = combine-backward into the owners' dO (after the backward FREE they
   // posted at the end of their previous backward, once its wgrad and dX had read dO and
   // dXs — so layers sharing one workspace on a comm stay ordered; READY per micro-op)
@@ -711,6 +719,18 @@ void backward_fused_movers(lina_comm* cm, const Plan& p, const Ptrs& q, const vo
 // ------------------------------------------------------------------ dropless layout
 // (§8(f) row 4; kernels/dropless.cu): no capacity bound, a count exchange, unequal-split
 // dispatch / return by peer stores, the expert GEMMs over virtual segments.  n_chunks = 1.
+// Communicator of this rank's packing group (ranks [G·m, (G+1)·m)), split off the dispatch
+// communicator on first use (collective: every rank reaches it in the same call).
+ncclComm_t group_comm(lina_comm* cm, int m) {
+  auto it = cm->group_comms.find(m);
+  if (it != cm->group_comms.end()) return it->second;
+  ncclComm_t g = nullptr;
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  LINA_NCCL_CHECK(ncclCommSplit(cm->ep_disp, cm->rank / m, cm->rank, &g, &cfg));
+  cm->group_comms[m] = g;
+  return g;
+}
+
 RowGemm dl_gemm(const Plan& p, const Ptrs& q, const void* A, const void* B, void* D, int N, int K) {
   RowGemm g{};
   g.tile_rows = p.tile_rows;
@@ -749,23 +769,27 @@ void forward_dropless(lina_comm* cm, const Plan& p, const Ptrs& q, const void* t
                    peer ? &s_free : nullptr);
   launch_route(q.idx, p.T, p.k, E, p.C, q.route, q.slot, route ? route->counts : nullptr, q.kept, q.tok_of, s,
                cm->route_sync);
+  if (p.pack > 1) group_comm(cm, p.pack);  // (created by the first, eager call)
   const int* allc = q.kept;
   if (peer) {  // the count exchange, then every rank derives the same layout
     prof_a2a_begin(cm, s);
+    prof_comm_begin(cm, s);
     int* const* peer_allc = (int* const*)ce->dev_ptrs(saved, p.s_allc, s, p.peer_key);
     launch_dl_counts(q.kept, peer_allc, P, me, E, make_sig(cm, CT::kFreeFwd, rf, 1, CT::kFCountFwd, rf, 1), s);
     launch_sig_wait(make_sig(cm, CT::kFCountFwd, rf, 1, -1, nullptr, 0), s);
     allc = q.allc;
   }
-  launch_dl_layout(allc, P, E, El, me, R, p.V, q.dl, s);
+  launch_dl_layout(allc, P, E, El, p.pack, me, R, p.V, q.dl, s);
   trace_mark(cm, s, "dl gate+route+layout");
   if (peer) {
     void* const* peer_R = ce->dev_ptrs(saved, p.s_R, s, p.peer_key);
-    launch_dl_permute(dtype, tokens, q.tok_of, q.kept, q.dl, me, p.T, p.k, E, El, p.d, peer_R, nullptr,
+    launch_dl_permute(dtype, tokens, q.tok_of, q.kept, q.dl, me, p.T, p.C, p.k, E, El, p.pack, p.d, peer_R, nullptr,
                       make_sig(cm, -1, nullptr, 0, CT::kFReadyFwdD, rf, 1, kSiteDispFwd), s);
     launch_sig_wait(make_sig(cm, CT::kFReadyFwdD, rf, 1, -1, nullptr, 0), s);  // every source's rows landed
+    prof_comm_end(cm, s);
   } else {
-    launch_dl_permute(dtype, tokens, q.tok_of, q.kept, q.dl, me, p.T, p.k, E, El, p.d, nullptr, q.R, PeerSignal{}, s);
+    launch_dl_permute(dtype, tokens, q.tok_of, q.kept, q.dl, me, p.T, p.C, p.k, E, El, 1, p.d, nullptr, q.R, PeerSignal{},
+                      s);
   }
   if (route) {
     if (route->idx && !override_r)
@@ -787,10 +811,12 @@ void forward_dropless(lina_comm* cm, const Plan& p, const Ptrs& q, const void* t
   trace_mark(cm, s, "dl gemm1+gemm2");
   if (peer) {  // return all-to-all: each segment's rows to its source's compact buffer
     void* const* peer_C = ce->dev_ptrs(saved, p.s_C, s, p.peer_key);
-    launch_dl_push_vsegs(dtype, q.O, peer_C, q.dl, p.V, R, E, El, me, p.d,
+    prof_comm_begin(cm, s);
+    launch_dl_push_vsegs(dtype, q.O, peer_C, q.dl, p.V, R, E, El, p.pack, me, p.d,
                          make_sig(cm, -1, nullptr, 0, CT::kFReadyFwdC, rf, 1, kSiteCombFwd), s);
     const PeerSignal s_out = make_sig(cm, CT::kFReadyFwdC, rf, 1, -1, nullptr, 0, kSiteFwdEnd, rf);
     launch_sig_wait(wait_only(s_out), s);
+    prof_comm_end(cm, s);
     prof_a2a_end(cm, s);
     const PeerSignal s_out2 = no_wait(s_out);
     launch_combine(dtype, q.Cb, q.idx, q.slot, q.gate, p.T, p.k, p.d, E, p.C, 1, p.C, out, s, &s_out2, q.dl.ebase);
@@ -809,19 +835,23 @@ void backward_dropless(lina_comm* cm, const Plan& p, const Ptrs& q, const void* 
   CeTransport* ce = peer ? cm->ce : nullptr;
   uint32_t* rb = peer ? ce->round_bwd() : nullptr;
   trace_mark(cm, s, "dl bwd:start");
-  if (cm->sched) sched_a2a_imminent(cm);
+  if (cm->sched) sched_a2a_imminent(cm, s);
   const void* O = peer ? (const void*)q.Cb : (const void*)q.O;  // the returned expert outputs
+  // dg = 0 for assignments a capacity bound dropped (the row kernel writes the kept ones)
+  if (p.C < p.T && p.T > 0) LINA_CUDA_CHECK(cudaMemsetAsync(q.dg, 0, sizeof(float) * (size_t)p.T * p.k, s));
   if (peer) {
     prof_a2a_begin(cm, s);
     const PeerSignal s_disp = make_sig(cm, CT::kFreeBwd, rb, 0, CT::kFReadyBwdD, rb, 1, kSiteDispBwd);
     launch_sig_wait(wait_only(s_disp), s);
+    prof_comm_begin(cm, s);
     void* const* peer_dO = ce->dev_ptrs(ws, p.w_dO, s, p.peer_key);
-    launch_dl_combine_bwd(dtype, dout, O, q.tok_of, q.kept, q.gate, q.dl, me, p.T, p.k, E, El, p.d, peer_dO, nullptr,
-                          q.dg, no_wait(s_disp), s);
+    launch_dl_combine_bwd(dtype, dout, O, q.tok_of, q.kept, q.gate, q.dl, me, p.T, p.C, p.k, E, El, p.pack, p.d, peer_dO,
+                          nullptr, q.dg, no_wait(s_disp), s);
     launch_sig_wait(make_sig(cm, CT::kFReadyBwdD, rb, 1, -1, nullptr, 0), s);
+    prof_comm_end(cm, s);
   } else {
-    launch_dl_combine_bwd(dtype, dout, O, q.tok_of, q.kept, q.gate, q.dl, me, p.T, p.k, E, El, p.d, nullptr, q.dO,
-                          q.dg, PeerSignal{}, s);
+    launch_dl_combine_bwd(dtype, dout, O, q.tok_of, q.kept, q.gate, q.dl, me, p.T, p.C, p.k, E, El, 1, p.d, nullptr,
+                          q.dO, q.dg, PeerSignal{}, s);
   }
   trace_mark(cm, s, "dl combine_bwd");
   prof_begin(cm, s);
@@ -832,8 +862,10 @@ void backward_dropless(lina_comm* cm, const Plan& p, const Ptrs& q, const void* 
   launch_expert_row_gemm(dtype, dl_gemm(p, q, q.dH, w1, q.dXe, p.d, p.f), false, kEpiNone, s);
   if (peer) {
     void* const* peer_dXs = ce->dev_ptrs(ws, p.w_dXs, s, p.peer_key);
-    launch_dl_push_vsegs(dtype, q.dXe, peer_dXs, q.dl, p.V, R, E, El, me, p.d,
+    prof_comm_begin(cm, s);
+    launch_dl_push_vsegs(dtype, q.dXe, peer_dXs, q.dl, p.V, R, E, El, p.pack, me, p.d,
                          make_sig(cm, -1, nullptr, 0, CT::kFReadyBwdC, rb, 1, kSiteCombBwd), s);
+    prof_comm_end(cm, s);  // (the return rows are pushed; the wgrads overlap their arrival)
     if (cm->sched) sched_a2a_end(cm, s);
   }
   WGrad wg2{q.dO, q.H, dw2, q.dl.vcount, 1, 1, El, R, p.d, p.f};
@@ -846,6 +878,12 @@ void backward_dropless(lina_comm* cm, const Plan& p, const Ptrs& q, const void* 
   launch_expert_wgrad(dtype, wg1, s);
   prof_end(cm, s, 4);
   trace_mark(cm, s, "dl dgrad x2 + wgrad x2");
+  if (p.pack > 1) {  // packed experts: each replica summed its share of the rows; sum over the group
+    ncclComm_t g = group_comm(cm, p.pack);
+    const size_t nel = (size_t)El * p.d * p.f;
+    LINA_NCCL_CHECK(ncclAllReduce(dw2, dw2, nel, nccl_dt(p), ncclSum, g, s));
+    LINA_NCCL_CHECK(ncclAllReduce(dw1, dw1, nel, nccl_dt(p), ncclSum, g, s));
+  }
   launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, E, p.k, q.dwg, dgate_w, s);
   if (peer) {
     const PeerSignal s_back = make_sig(cm, CT::kFReadyBwdC, rb, 1, -1, nullptr, 0, kSiteBwdEnd, rb);
@@ -1065,7 +1103,7 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
   launch_combine_bwd(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.T, p.k, p.d, p.E, p.C, n, p.Cm, q.dS,
                      q.dg, s);
   // the scheduler stops admitting allreduce micro-ops: all-to-all is imminent
-  if (cm->sched) sched_a2a_imminent(cm);
+  if (cm->sched) sched_a2a_imminent(cm, s);
   WGrad wg2{q.dO, q.H, dw2, q.vcount, n, p.P, p.El, p.Cm, p.d, p.f};
   WGrad wg1{q.dH, q.R, dw1, q.vcount, n, p.P, p.El, p.Cm, p.f, p.d};
   bool dwg_done = false;

@@ -104,7 +104,9 @@ void launch_expert_wgrad(int dtype, const WGrad& g, cudaStream_t s);
 void set_force_simt(bool on);
 
 // Scheduler hooks called by the layer (sched.cpp).
-void sched_a2a_imminent(lina_comm* cm);                   // combine-bwd started
+// (all three are no-ops while `s` is being captured into a CUDA graph: the scheduler tracks
+// eagerly launched all-to-all phases; a captured event would never be recorded)
+void sched_a2a_imminent(lina_comm* cm, cudaStream_t s);   // combine-bwd started
 void sched_a2a_begin(lina_comm* cm, cudaStream_t a2a_stream);
 void sched_a2a_end(lina_comm* cm, cudaStream_t a2a_stream);  // phase ends there
 
@@ -115,6 +117,11 @@ void sched_submit(Scheduler* s, void* grad, size_t count, lina_dtype dt, cudaStr
 void sched_wait(Scheduler* s, cudaStream_t st);  // device-side wait point, host never blocks
 void sched_check(Scheduler* s);                  // rethrows an error of the scheduler thread
 void sched_stats(Scheduler* s, int64_t* issued, int64_t* deferred);
+
+// Expert packing (packing.cpp).
+int pack_decide(int world, int pack, double ffn_ms, double a2a_ms);
+void pack_weights(lina_comm* cm, int E, int m0, int m1, size_t expert_bytes, const void* w_from, void* w_to,
+                  cudaStream_t s);
 
 // Placement (placement.cpp).
 lina_status placement_compute(const double* pop, int E, int N, int mpd, lina_placement* out,

@@ -250,14 +250,19 @@ void sched_wait(Scheduler* s, cudaStream_t st) { s->wait(st); }
 void sched_check(Scheduler* s) { s->check(); }
 void sched_stats(Scheduler* s, int64_t* i, int64_t* d) { s->stats(i, d); }
 
-void sched_a2a_imminent(lina_comm* cm) {
-  if (cm->sched) cm->sched->a2a_imminent();
+static bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  LINA_CUDA_CHECK(cudaStreamIsCapturing(s, &st));
+  return st != cudaStreamCaptureStatusNone;
 }
-void sched_a2a_begin(lina_comm* cm, cudaStream_t) {
-  if (cm->sched) cm->sched->a2a_imminent();
+void sched_a2a_imminent(lina_comm* cm, cudaStream_t s) {
+  if (cm->sched && !capturing(s)) cm->sched->a2a_imminent();
+}
+void sched_a2a_begin(lina_comm* cm, cudaStream_t s) {
+  if (cm->sched && !capturing(s)) cm->sched->a2a_imminent();
 }
 void sched_a2a_end(lina_comm* cm, cudaStream_t a2a_stream) {
-  if (cm->sched) cm->sched->a2a_end(a2a_stream);
+  if (cm->sched && !capturing(a2a_stream)) cm->sched->a2a_end(a2a_stream);
 }
 
 }  // namespace lina

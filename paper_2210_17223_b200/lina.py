@@ -32,7 +32,8 @@ ABI_SYMBOLS = [
     "lina_allreduce_wait", "lina_sched_stats", "lina_profile_enable", "lina_profile_read",
     "lina_popprof_create", "lina_popprof_destroy", "lina_popprof_add", "lina_popprof_estimate",
     "lina_phase_two_check", "lina_moe_infer_forward_two_phase", "lina_popprof_save", "lina_popprof_load",
-    "lina_popprof_info", "lina_infer_last_rows",
+    "lina_popprof_info", "lina_infer_last_rows", "lina_pack_decide", "lina_pack_ctl_create", "lina_pack_ctl_step",
+    "lina_pack_ctl_destroy", "lina_pack_weights",
 ]
 
 
@@ -45,7 +46,7 @@ class LinaError(RuntimeError):
 class MoEDesc(ctypes.Structure):
     _fields_ = [("num_tokens", ctypes.c_int32), ("d_model", ctypes.c_int32), ("d_ffn", ctypes.c_int32),
                 ("num_experts", ctypes.c_int32), ("k", ctypes.c_int32), ("capacity", ctypes.c_int32),
-                ("n_chunks", ctypes.c_int32), ("dtype", ctypes.c_int32)]
+                ("n_chunks", ctypes.c_int32), ("dtype", ctypes.c_int32), ("pack", ctypes.c_int32)]
 
 
 class Route(ctypes.Structure):
@@ -58,7 +59,7 @@ class Profile(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_int64), ("gemm_launches", ctypes.c_int64),
                 ("gemm_ms", ctypes.c_double), ("gemm_phases", ctypes.c_int64),
                 ("a2a_window_ms", ctypes.c_double), ("gemm_in_a2a_ms", ctypes.c_double),
-                ("a2a_windows", ctypes.c_int64)]
+                ("a2a_windows", ctypes.c_int64), ("a2a_op_ms", ctypes.c_double), ("a2a_ops", ctypes.c_int64)]
 
 
 class Placement(ctypes.Structure):
@@ -113,6 +114,11 @@ def load() -> ctypes.CDLL:
         "lina_allreduce_wait": ([vp, vp], i32),
         "lina_sched_stats": ([vp, P(ctypes.c_int64), P(ctypes.c_int64)], i32),
         "lina_infer_last_rows": ([vp, P(i32), P(i32)], i32),
+        "lina_pack_decide": ([i32, i32, ctypes.c_double, ctypes.c_double, P(i32)], i32),
+        "lina_pack_ctl_create": ([i32, i32, i32, P(vp)], i32),
+        "lina_pack_ctl_step": ([vp, ctypes.c_double, ctypes.c_double, P(i32), P(i32)], i32),
+        "lina_pack_ctl_destroy": ([vp], i32),
+        "lina_pack_weights": ([vp, i32, i32, i32, sz, i32, vp, vp, vp], i32),
         "lina_profile_enable": ([vp, ctypes.c_int], i32),
         "lina_profile_read": ([vp, P(Profile)], i32),
     }
@@ -199,8 +205,8 @@ def lina_comm_init(world=1, rank=0, device=0, unique_id=None, nccl_max_ctas=0) -
     return Comm(world, rank, device, unique_id, nccl_max_ctas)
 
 
-def make_desc(num_tokens, d_model, d_ffn, num_experts, k, capacity, n_chunks, dtype) -> MoEDesc:
-    return MoEDesc(num_tokens, d_model, d_ffn, num_experts, k, capacity, n_chunks, _dtype_code(dtype))
+def make_desc(num_tokens, d_model, d_ffn, num_experts, k, capacity, n_chunks, dtype, pack=1) -> MoEDesc:
+    return MoEDesc(num_tokens, d_model, d_ffn, num_experts, k, capacity, n_chunks, _dtype_code(dtype), pack)
 
 
 def lina_moe_workspace_size(comm: Comm, desc: MoEDesc):
@@ -401,6 +407,43 @@ def lina_infer_last_rows(comm: Comm):
     return list(recv), list(sent)
 
 
+def lina_pack_decide(world: int, pack: int, ffn_ms: float, a2a_ms: float) -> int:
+    out = ctypes.c_int32()
+    _check(load().lina_pack_decide(world, pack, ffn_ms, a2a_ms, ctypes.byref(out)))
+    return out.value
+
+
+class PackController:
+    """lina_pack_ctl_create / _step / _destroy (host state of the packing controller)."""
+
+    def __init__(self, world: int, start_step: int = 10, every: int = 4):
+        self.handle = ctypes.c_void_p()
+        _check(load().lina_pack_ctl_create(world, start_step, every, ctypes.byref(self.handle)))
+
+    def step(self, ffn_ms: float, a2a_ms: float):
+        pack, changed = ctypes.c_int32(), ctypes.c_int32()
+        _check(load().lina_pack_ctl_step(self.handle, ffn_ms, a2a_ms, ctypes.byref(pack), ctypes.byref(changed)))
+        return pack.value, bool(changed.value)
+
+    def close(self):
+        if self.handle:
+            load().lina_pack_ctl_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def lina_pack_weights(comm: Comm, num_experts: int, pack_from: int, pack_to: int, w_from, w_to, stream=None):
+    """w_from [m0*E_l, ...] -> w_to [m1*E_l, ...] (same per-expert shape and dtype)."""
+    per = w_from[0].numel() if w_from.dim() > 0 else 0
+    _check(load().lina_pack_weights(comm.handle, num_experts, pack_from, pack_to, per, _dtype_code(w_from.dtype),
+                                    _ptr(w_from), _ptr(w_to), _stream(stream)))
+
+
 def lina_sched_config(comm: Comm, policy: int, partition_bytes: int):
     _check(load().lina_sched_config(comm.handle, policy, partition_bytes))
 
@@ -430,7 +473,8 @@ def lina_profile_read(comm: Comm) -> dict:
     _check(load().lina_profile_read(comm.handle, ctypes.byref(p)))
     return {"kernel_launches": p.kernel_launches, "gemm_launches": p.gemm_launches,
             "gemm_ms": p.gemm_ms, "gemm_phases": p.gemm_phases, "a2a_window_ms": p.a2a_window_ms,
-            "gemm_in_a2a_ms": p.gemm_in_a2a_ms, "a2a_windows": p.a2a_windows}
+            "gemm_in_a2a_ms": p.gemm_in_a2a_ms, "a2a_windows": p.a2a_windows, "a2a_op_ms": p.a2a_op_ms,
+            "a2a_ops": p.a2a_ops}
 
 
 # ----------------------------------------------------------------------------- convenience layer
@@ -442,9 +486,9 @@ class MoELayer:
     Pure marshalling: buffers are torch allocations, the compute is liblina.so."""
 
     def __init__(self, comm: Comm, num_tokens, d_model, d_ffn, num_experts, k, capacity, n_chunks=1,
-                 dtype=torch.bfloat16, device=None):
+                 dtype=torch.bfloat16, device=None, pack=1):
         self.comm = comm
-        self.desc = make_desc(num_tokens, d_model, d_ffn, num_experts, k, capacity, n_chunks, dtype)
+        self.desc = make_desc(num_tokens, d_model, d_ffn, num_experts, k, capacity, n_chunks, dtype, pack)
         self.dtype = torch_dtype(self.desc.dtype)
         self.device = device or torch.device("cuda", comm.device)
         ws, sv = lina_moe_workspace_size(comm, self.desc)

@@ -40,6 +40,10 @@ def main():
     ap.add_argument("--dropless", action="store_true",
                     help="capacity 0: the dropless layout (count exchange + unequal split, §8(f) row 4); "
                          "the oracle runs with C = T (no drops)")
+    ap.add_argument("--pack", type=int, default=1,
+                    help="expert packing factor m (P:376): groups of m ranks host the same m*E/world experts")
+    ap.add_argument("--pack-exchange", action="store_true",
+                    help="build the packed weights with lina_pack_weights from the unpacked ones (P:505)")
     a = ap.parse_args()
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -57,7 +61,22 @@ def main():
     uid = [lina.lina_get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = lina.Comm(world, rank, local, uid[0])
-    Wg, W1, W2 = li.layer_weights(cfg, a.seed, experts=range(rank * El, (rank + 1) * El))
+    m = max(1, a.pack)
+    G = rank // m                    # packing group; its experts [G*m*El, (G+1)*m*El)
+    hosted = range(G * m * El, (G + 1) * m * El)
+    Wg, W1, W2 = li.layer_weights(cfg, a.seed, experts=hosted)
+    exchange_ok = True
+    if a.pack_exchange and m > 1:
+        _, W1u, W2u = li.layer_weights(cfg, a.seed, experts=range(rank * El, (rank + 1) * El))
+        tdt_ = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+        got = []
+        for Wu in (W1u, W2u):
+            src = torch.from_numpy(Wu).to(tdt_).to(dev)
+            dst = torch.full((m * El,) + tuple(Wu.shape[1:]), float("nan"), dtype=tdt_, device=dev)
+            lina.lina_pack_weights(comm, E, 1, m, src, dst)
+            got.append(dst.float().cpu().numpy())
+        exchange_ok = np.array_equal(got[0], torch.from_numpy(W1).to(tdt_).float().numpy()) and \
+            np.array_equal(got[1], torch.from_numpy(W2).to(tdt_).float().numpy())
     X, dY = li.layer_tokens(cfg, a.seed, rank)
     tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
 
@@ -65,7 +84,7 @@ def main():
 
     def run(n_chunks):
         layer = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, C_layer,
-                              n_chunks, tdt, dev)
+                              n_chunks, tdt, dev, pack=m)
         if a.poison:  # every byte the layer reads must be one it (or a peer) wrote this step
             layer.saved.fill_(0xFF)
             layer.workspace.fill_(0xFF)
@@ -80,7 +99,7 @@ def main():
         finite_b = True
         if a.interleave:  # layer B's exchanges run between A's forward and backward
             layer_b = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, C_layer,
-                                    n_chunks, tdt, dev)
+                                    n_chunks, tdt, dev, pack=m)
             if a.shared_ws:
                 layer_b.workspace = layer.workspace
             XB, dYB = li.layer_tokens(cfg, a.seed + 1, rank)
@@ -94,7 +113,7 @@ def main():
         out = {"y": y.float().cpu().numpy(), "dx": dx.float().cpu().numpy(), "dwg": dwg.cpu().numpy(),
                "dw1": dw1.float().cpu().numpy(), "dw2": dw2.float().cpu().numpy(),
                "idx": layer.route_t["idx"].cpu().numpy(), "slot": layer.route_t["slot"].cpu().numpy(),
-               "finite_b": finite_b}
+               "finite_b": finite_b, "exchange_ok": exchange_ok}
         if a.graph:  # replays must be full steps: the cross-rank rounds live in device memory
             gy, gdx = torch.empty_like(y), torch.empty_like(dx)
             gdwg, gdw1, gdw2 = torch.empty_like(dwg), torch.empty_like(dw1), torch.empty_like(dw2)
@@ -157,12 +176,14 @@ def main():
             ok &= np.array_equal(g["idx"], fw[r].idx) and np.array_equal(g["slot"], fw[r].slot)
             errs[f"y{r}"] = moe.normwise_error(g["y"], fw[r].y)
             errs[f"dx{r}"] = moe.normwise_error(g["dx"], bw.dXs[r])
-            errs[f"dw1_{r}"] = moe.normwise_error(g["dw1"], bw.dW1[r * El:(r + 1) * El])
-            errs[f"dw2_{r}"] = moe.normwise_error(g["dw2"], bw.dW2[r * El:(r + 1) * El])
+            lo, hi = (r // m) * m * El, (r // m + 1) * m * El   # the experts rank r hosts
+            errs[f"dw1_{r}"] = moe.normwise_error(g["dw1"], bw.dW1[lo:hi])
+            errs[f"dw2_{r}"] = moe.normwise_error(g["dw2"], bw.dW2[lo:hi])
         errs["dwg"] = moe.normwise_error(dwg_sum, bw.dWg)
         ok &= all(v <= tol for v in errs.values())
+        ok &= all(g["exchange_ok"] for g in gathered)
         print("MP_PARITY", "OK" if ok else "FAIL", f"world={world} cfg={cfg.name} T={cfg.tokens_per_rank} "
-              f"n={a.n_chunks}" + (" dropless" if a.dropless else ""), " ".join(f"{k}={v:.2e}" for k, v in errs.items()), flush=True)
+              f"n={a.n_chunks}" + (" dropless" if a.dropless else "") + (f" pack={m}" if m > 1 else ""), " ".join(f"{k}={v:.2e}" for k, v in errs.items()), flush=True)
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.broadcast(flag, 0)
     comm.close()

@@ -52,6 +52,22 @@ def test_two_ranks_dropless(cfg, tokens, extra):
     _run(2, "--config", cfg, "--tokens", str(tokens), "--n-chunks", "1", "--dropless", *extra, port=29614)
 
 
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("extra", [["--dropless", "--pack-exchange"], ["--poison", "--graph"]])
+def test_two_ranks_packed(extra):
+    """Expert packing m = 2 at 2 ranks: both ranks host all experts, each takes the rows
+    of the sources with its residue (its own rows stay local), dW summed over the group; the
+    packed weights built by lina_pack_weights; with and without a capacity bound."""
+    _run(2, "--config", "C2", "--tokens", "512", "--n-chunks", "1", "--pack", "2", *extra, port=29616)
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
+@pytest.mark.parametrize("pack", [2, 4])
+def test_four_ranks_packed(pack):
+    _run(4, "--config", "C3", "--tokens", "256", "--n-chunks", "1", "--pack", str(pack), "--dropless",
+         "--pack-exchange", port=29617)
+
+
 @pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
 def test_four_ranks_dropless():
     _run(4, "--config", "C2", "--tokens", "384", "--n-chunks", "1", "--dropless", "--poison", "--graph", port=29615)
