@@ -47,6 +47,11 @@ void launch_gate_topk(int dtype, const void* X, const float* Wg, int T, int d, i
                       int write_routing, float* probs, int* idx, float* gate, cudaStream_t s,
                       const PeerSignal* sig = nullptr);
 
+// tcgen05 gate (gate_tc.cu): logits on the tensor cores, softmax / top-k in the epilogue.
+bool gate_tc_supported(int d, int E, int k);
+void launch_gate_tc(const void* X, const float* Wg, int T, int d, int E, int k, int write_routing, float* probs,
+                    int* idx, float* gate, const PeerSignal& sig, cudaStream_t s);
+
 size_t route_scratch_ints(int T, int k, int E);
 // sync: zeroed device words (route_sync_words(), comm-owned) -> one fused launch;
 // NULL -> the three-launch count / scan / assign path.  vcount/mtp (P = 1 only): also
@@ -81,10 +86,21 @@ void launch_combine_bwd(int dtype, const void* dY, const void* Recv, const int* 
                         const float* gate, int T, int k, int d, int E, int C, int n, int Cm,
                         void* dSend, float* dg, cudaStream_t s);
 // dX (gather-sum + dL·Wgᵀ) and dWg (Xᵀ dL) with dL recomputed from the forward routing.
+// tc_scratch: the dWg scratch of the same backward (its launch_dwg ran first): the
+// tensor-core path reads the dL split from it; NULL = the CUDA-core kernel.
 void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* probs,
                const float* gate, const float* dg, const float* Wg, int T, int k, int d, int E, int C,
                int n, int Cm, void* dX, cudaStream_t s, const PeerSignal* sig = nullptr,
-               const int* ebase = nullptr);
+               const int* ebase = nullptr, const void* tc_scratch = nullptr);
+// tensor-core gate backward (gate_bwd_tc.cu)
+bool gate_bwd_tc_supported(int dtype, int d, int E, int k);
+size_t gate_bwd_tc_scratch_bytes(int T, int d, int E);
+void launch_dwg_tc(const void* X, const float* probs, const int* idx, const float* gate, const float* dg, int T,
+                   int d, int E, int k, void* scratch, float* dWg, cudaStream_t s);
+void launch_dx_tc(const void* dXe, const int* idx, const int* slot, const float* Wg, int T, int k, int d, int E,
+                  int C, int n, int Cm, const int* ebase, void* dX, const void* scratch, const PeerSignal& sig,
+                  cudaStream_t s);
+void launch_dwg_reduce(const float* part, int nparts, int dE, float* dWg, cudaStream_t s);
 size_t dwg_scratch_floats(int T, int d, int E);
 void launch_dwg(int dtype, const void* X, const float* probs, const int* idx, const float* gate,
                 const float* dg, int T, int d, int E, int k, float* scratch, float* dWg, cudaStream_t s);

@@ -22,6 +22,7 @@
 // Both end in the same epilogue: logits in shared memory, one warp per token for
 // the softmax (warp-shuffle max/sum) and k rounds of warp arg-max.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -379,6 +380,15 @@ void launch_gate_topk(int dtype, const void* X, const float* Wg, int T, int d, i
                       const PeerSignal* sig) {
   const PeerSignal none{};
   const PeerSignal& sg = sig ? *sig : none;
+  // bf16 tokens: the tcgen05 gate (gate_tc.cu); LINA_GATE_MMA=1 keeps the mma.sync one
+  static const bool force_mma = [] {
+    const char* e = getenv("LINA_GATE_MMA");
+    return e && e[0] == '1';
+  }();
+  if (dtype == 1 && !force_mma && gate_tc_supported(d, E, k) && (T > 0 || sig)) {
+    launch_gate_tc(X, Wg, T, d, E, k, write_routing, probs, idx, gate, sg, s);
+    return;
+  }
   if (dtype == 1 && d % 32 == 0 && (T > 0 || sig)) {
     const int nt = (E + 7) / 8;
     if (nt <= 1) launch_gate_mma<1>(X, Wg, T, d, E, k, write_routing, probs, idx, gate, sg, s);

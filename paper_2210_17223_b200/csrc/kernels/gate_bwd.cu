@@ -22,6 +22,8 @@
 //       batches of 4, folded in shared memory in a fixed tree order; each token split
 //       writes one partial, reduced afterwards in a fixed order (deterministic, no
 //       float atomics).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "../common.h"
@@ -370,7 +372,22 @@ int dwg_splits(int T) { return (T + kDwgTok - 1) / kDwgTok; }
 }  // namespace
 
 size_t dwg_scratch_floats(int T, int d, int E) {
-  return (size_t)dwg_splits(T) * d * E;
+  // (also the tensor-core path's dL split and partials, gate_bwd_tc.cu)
+  return std::max((size_t)dwg_splits(T) * d * E, (gate_bwd_tc_scratch_bytes(T, d, E) + 3) / 4);
+}
+
+void launch_dwg_reduce(const float* part, int nparts, int dE, float* dWg, cudaStream_t s) {
+  launch_k(dwg_reduce_kernel, dim3((dE + 31) / 32), dim3(256), 0, s, part, nparts, dE, dWg);
+  LINA_LAUNCH_CHECK();
+}
+
+// LINA_GATE_BWD_SIMT=1 keeps the CUDA-core dX / dWg (A/B comparisons)
+static bool gate_bwd_tc_on(int dtype, int d, int E, int k) {
+  static const bool simt = [] {
+    const char* e = getenv("LINA_GATE_BWD_SIMT");
+    return e && e[0] == '1';
+  }();
+  return !simt && gate_bwd_tc_supported(dtype, d, E, k);
 }
 
 template <typename T, int KT>
@@ -392,9 +409,14 @@ static void launch_dx_t(const void* dXe, const int* idx, const int* slot, const 
 
 void launch_dx(int dtype, const void* dXe, const int* idx, const int* slot, const float* probs,
                const float* gate, const float* dg, const float* Wg, int T, int k, int d, int E, int C,
-               int n, int Cm, void* dX, cudaStream_t s, const PeerSignal* sig, const int* ebase) {
+               int n, int Cm, void* dX, cudaStream_t s, const PeerSignal* sig, const int* ebase,
+               const void* tc_scratch) {
   if (T <= 0 && !sig) return;  // (with a signal, one CTA still closes the round)
   const PeerSignal sg = sig ? *sig : PeerSignal{};
+  if (tc_scratch && gate_bwd_tc_on(dtype, d, E, k)) {  // dL split by the preceding launch_dwg
+    launch_dx_tc(dXe, idx, slot, Wg, T, k, d, E, C, n, Cm, ebase, dX, tc_scratch, sg, s);
+    return;
+  }
   auto go = [&](auto tag) {
     using ET = decltype(tag);
     if (k == 1) launch_dx_t<ET, 1>(dXe, idx, slot, probs, gate, dg, Wg, T, k, d, E, C, n, Cm, dX, sg, s, ebase);
@@ -410,6 +432,10 @@ void launch_dwg(int dtype, const void* X, const float* probs, const int* idx, co
                 const float* dg, int T, int d, int E, int k, float* scratch, float* dWg, cudaStream_t s) {
   if (T <= 0) {
     LINA_CUDA_CHECK(cudaMemsetAsync(dWg, 0, sizeof(float) * (size_t)d * E, s));
+    return;
+  }
+  if (gate_bwd_tc_on(dtype, d, E, k)) {
+    launch_dwg_tc(X, probs, idx, gate, dg, T, d, E, k, scratch, dWg, s);
     return;
   }
   const int nsplit = dwg_splits(T);

@@ -655,7 +655,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   prof_a2a_end(cm, s);
   const PeerSignal s_back2 = no_wait(s_back);
   launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm,
-            dtokens, s, &s_back2);
+            dtokens, s, &s_back2, nullptr, q.dwg);
   // backward FREE: my dO and dXs have been read (wgrad, dX) — publish the round just closed
   launch_sig_wait(make_sig(cm, -1, nullptr, 0, CT::kFreeBwd, rb, 0), s);
   trace_mark(cm, s, "dx");
@@ -891,11 +891,11 @@ void backward_dropless(lina_comm* cm, const Plan& p, const Ptrs& q, const void* 
     prof_a2a_end(cm, s);
     const PeerSignal s_back2 = no_wait(s_back);
     launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, E, p.C, 1, p.C, dtokens, s,
-              &s_back2, q.dl.ebase);
+              &s_back2, q.dl.ebase, q.dwg);
     launch_sig_wait(make_sig(cm, -1, nullptr, 0, CT::kFreeBwd, rb, 0), s);  // backward FREE
   } else {
     launch_dx(dtype, q.dXe, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, E, p.C, 1, p.C, dtokens, s,
-              nullptr, q.dl.ebase);
+              nullptr, q.dl.ebase, q.dwg);
   }
   trace_mark(cm, s, "dl dx");
 }
@@ -1163,7 +1163,7 @@ void moe_backward(lina_comm* cm, const Plan& p, const void* saved, const void* d
     launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, p.E, p.k, q.dwg, dgate_w, s);
   // (e)+(f): gate backward + gather-sum dX
   launch_dx(dtype, q.dXs, q.idx, q.slot, q.probs, q.gate, q.dg, gate_w, p.T, p.k, p.d, p.E, p.C, n, p.Cm,
-            dtokens, s);
+            dtokens, s, nullptr, nullptr, q.dwg);
 }
 
 }  // namespace lina
