@@ -32,6 +32,8 @@
 // are enumerated from a per-chunk prefix of valid row blocks (launch_mtile_prefix).
 #include <cuda.h>
 
+#include <stdlib.h>
+
 #include <cstring>
 
 #include "../common.h"
@@ -87,13 +89,13 @@ struct TcParams {
   char* pbase[kMaxPeerMaps];        // the same buffers as plain pointers (remote owners: SM stores)
 };
 
-template <int CG, bool WGRAD, bool B_MN, int EPI>
-__global__ void __launch_bounds__(Geo<CG, EPI != kEpiNone>::THREADS, 1)
+template <int CG, bool WGRAD, bool B_MN, int EPI, bool WIDE = (EPI != kEpiNone)>
+__global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ TcParams p) {
   pdl_enter();
-  using G = Geo<CG, EPI != kEpiNone>;
+  using G = Geo<CG, WIDE>;
   constexpr int STAGES = G::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -450,20 +452,20 @@ static int num_sms() {
   return m < 2 ? 2 : m;
 }
 
-template <int CG, bool WGRAD, bool B_MN, int EPI>
+template <int CG, bool WGRAD, bool B_MN, int EPI, bool WIDE = (EPI != kEpiNone)>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const CUtensorMap& x,
                    const TcParams& p, int grid, cudaStream_t s) {
-  auto kern = tc_gemm_kernel<CG, WGRAD, B_MN, EPI>;
+  auto kern = tc_gemm_kernel<CG, WGRAD, B_MN, EPI, WIDE>;
   static bool attr_set = false;
   if (!attr_set) {
     LINA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Geo<CG, EPI != kEpiNone>::SMEM_BYTES));
+                                         Geo<CG, WIDE>::SMEM_BYTES));
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(Geo<CG, EPI != kEpiNone>::THREADS);
-  cfg.dynamicSmemBytes = Geo<CG, EPI != kEpiNone>::SMEM_BYTES;
+  cfg.blockDim = dim3(Geo<CG, WIDE>::THREADS);
+  cfg.dynamicSmemBytes = Geo<CG, WIDE>::SMEM_BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -481,12 +483,20 @@ template <int CG>
 static void row_dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                          const CUtensorMap& mx, const TcParams& p, bool b_kmajor, int epi, int grid,
                          cudaStream_t s) {
+  // LINA_GEMM_NARROW=1: the ReLU / mask epilogues on 4 warps with the 6-stage ring (A/B
+  // measurement of the wide-epilogue geometry)
+  static const bool narrow = [] {
+    const char* e = getenv("LINA_GEMM_NARROW");
+    return e && e[0] == '1';
+  }();
   if (b_kmajor) {
-    if (epi == kEpiRelu) launch<CG, false, false, kEpiRelu>(ma, mb, md, mx, p, grid, s);
+    if (epi == kEpiRelu && narrow) launch<CG, false, false, kEpiRelu, false>(ma, mb, md, mx, p, grid, s);
+    else if (epi == kEpiRelu) launch<CG, false, false, kEpiRelu>(ma, mb, md, mx, p, grid, s);
     else if (epi == kEpiMask) launch<CG, false, false, kEpiMask>(ma, mb, md, mx, p, grid, s);
     else launch<CG, false, false, kEpiNone>(ma, mb, md, mx, p, grid, s);
   } else {
     if (epi == kEpiRelu) launch<CG, false, true, kEpiRelu>(ma, mb, md, mx, p, grid, s);
+    else if (epi == kEpiMask && narrow) launch<CG, false, true, kEpiMask, false>(ma, mb, md, mx, p, grid, s);
     else if (epi == kEpiMask) launch<CG, false, true, kEpiMask>(ma, mb, md, mx, p, grid, s);
     else launch<CG, false, true, kEpiNone>(ma, mb, md, mx, p, grid, s);
   }

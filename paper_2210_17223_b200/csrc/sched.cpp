@@ -41,6 +41,10 @@ struct ArJob {
   cudaEvent_t ready;
   size_t next = 0;   // next element offset to issue
   uint32_t marker = 0;  // != 0: a lina_allreduce_wait point (no data): publish it on `lo`
+  // all-to-all phases this job may be held back by: those registered before the wait
+  // point behind it (a phase enqueued after a stream wait on this job can only run after
+  // the job, so counting it as "queued" would deadlock); ~0 = every phase
+  uint64_t a2a_limit = ~0ull;
 };
 
 typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
@@ -72,7 +76,7 @@ class Scheduler {
     thread_.join();
     for (auto& j : jobs_)
       if (j.ready) cudaEventDestroy(j.ready);
-    for (auto e : a2a_events_) cudaEventDestroy(e);
+    for (auto& e : a2a_events_) cudaEventDestroy(e.second);
     cudaFree(done_flag_);
   }
   void config(lina_policy pol, size_t bytes) {
@@ -95,8 +99,10 @@ class Scheduler {
     }
     cv_.notify_all();
   }
+  // The next all-to-all phase (sequence number reg_seq_) is imminent.
   void a2a_imminent() {
     std::lock_guard<std::mutex> g(mu_);
+    imminent_seq_ = reg_seq_;
     imminent_ = true;
   }
   // The all-to-all phase ends when `a2a_stream` reaches this point.
@@ -105,7 +111,7 @@ class Scheduler {
     LINA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     LINA_CUDA_CHECK(cudaEventRecord(e, a2a_stream));
     std::lock_guard<std::mutex> g(mu_);
-    a2a_events_.push_back(e);
+    a2a_events_.push_back({reg_seq_++, e});
     cv_.notify_all();
   }
   // Make `s` wait, on the device, for every job submitted so far: a marker job goes
@@ -125,6 +131,8 @@ class Scheduler {
       }
       if (outstanding_ == 0) return;  // nothing submitted since the last wait point
       target = ++wait_target_;
+      for (auto& j : jobs_)  // phases registered from now on run after these jobs
+        if (!j.marker && j.a2a_limit == ~0ull) j.a2a_limit = reg_seq_;
       ArJob m{};
       m.marker = target;
       jobs_.push_back(m);
@@ -150,19 +158,21 @@ class Scheduler {
   }
 
  private:
-  // true while a registered all-to-all phase has not completed on the device
-  bool a2a_inflight_locked() {
+  // true while a registered all-to-all phase (sequence < limit) has not completed on the device
+  bool a2a_inflight_locked(uint64_t limit) {
     while (!a2a_events_.empty()) {
-      cudaError_t q = cudaEventQuery(a2a_events_.front());
-      if (q == cudaErrorNotReady) return true;
-      cudaEventDestroy(a2a_events_.front());
-      a2a_events_.erase(a2a_events_.begin());
-      if (a2a_events_.empty()) imminent_ = false;  // the a2a phase has drained
+      cudaError_t q = cudaEventQuery(a2a_events_.front().second);
+      if (q == cudaErrorNotReady) return a2a_events_.front().first < limit;
+      cudaEventDestroy(a2a_events_.front().second);
+      a2a_events_.pop_front();
+      if (a2a_events_.empty() && imminent_seq_ < reg_seq_) imminent_ = false;  // the a2a phase has drained
     }
     return false;
   }
   // true while an all-to-all is queued or in flight (LINA / NAIVE admission rule)
-  bool a2a_busy_locked() { return a2a_inflight_locked() || imminent_; }
+  bool a2a_busy_locked(uint64_t limit) {
+    return a2a_inflight_locked(limit) || (imminent_ && imminent_seq_ < limit);
+  }
   void run() {
     // this thread's runtime calls must target the comm's device (not device 0)
     const cudaError_t de = cudaSetDevice(cm_->device);
@@ -190,7 +200,7 @@ class Scheduler {
       bool can_issue = true;
       if (gated) {
         if (cudaEventQuery(j.ready) == cudaErrorNotReady) can_issue = false;
-        else if (policy_ == LINA_SCHED_DEFER ? a2a_inflight_locked() : a2a_busy_locked()) {
+        else if (policy_ == LINA_SCHED_DEFER ? a2a_inflight_locked(j.a2a_limit) : a2a_busy_locked(j.a2a_limit)) {
           can_issue = false;
           ++deferred_;
         }
@@ -228,7 +238,8 @@ class Scheduler {
   std::mutex mu_;
   std::condition_variable cv_;
   std::deque<ArJob> jobs_;
-  std::vector<cudaEvent_t> a2a_events_;
+  std::deque<std::pair<uint64_t, cudaEvent_t>> a2a_events_;  // (phase sequence, end event)
+  uint64_t reg_seq_ = 0, imminent_seq_ = 0;
   lina_policy policy_ = LINA_SCHED_LINA;
   size_t partition_bytes_ = (size_t)30 << 20;
   bool imminent_ = false, stop_ = false;
