@@ -134,6 +134,20 @@ lina_status lina_get_unique_id(unsigned char host_id[128]);
  * Errors: INVALID_ARGUMENT, UNSUPPORTED (device is not sm_100), CUDA, NCCL. */
 lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned char* host_id,
                            int nccl_max_ctas, lina_comm** out);
+/* A communicator without NCCL: the ranks' bootstrap exchanges (the peer-memory handles,
+ * the inference counts, barriers) go through a caller-supplied HOST allgather —
+ * fn(send, recv, bytes, ctx) gathers `bytes` from every rank into recv [world][bytes] in
+ * rank order and returns 0 on success (e.g. a torch gloo all_gather).  All-to-alls use the
+ * fused transport (NVLink peer stores, in-kernel flags); what needs an NCCL collective is
+ * UNSUPPORTED on it: the allreduce scheduler (lina_allreduce_submit with world > 1), the
+ * nccl / ce transports and expert packing's group sum.  Several ranks may share one GPU
+ * (NCCL refuses that): their kernels time-slice and the in-kernel flag waits still order
+ * them — slow, but it lets one GPU run the multi-rank data path (tests).  fn is called
+ * from the calling thread only, inside lina calls.
+ * Errors: INVALID_ARGUMENT, UNSUPPORTED (device is not sm_100), CUDA. */
+typedef int (*lina_host_allgather_fn)(const void* send, void* recv, size_t bytes, void* ctx);
+lina_status lina_comm_init_host(int world, int rank, int cuda_device, lina_host_allgather_fn fn, void* ctx,
+                                lina_comm** out);
 /* Waits for the scheduler thread, destroys comms/streams/events.  NULL is a no-op. */
 lina_status lina_comm_destroy(lina_comm* comm);
 /* Surfaces asynchronous NCCL/CUDA errors (ncclCommGetAsyncError, cudaPeekAtLastError). */

@@ -195,7 +195,17 @@ void validate_placement_tables(const lina_placement& pl, int E, int N, std::vect
 
 // Dropless training across ranks runs on the fused transport only (its exchanges are peer
 // stores with in-kernel flags); one GPU runs both dtypes.
+// A host-bootstrap communicator has no NCCL: only the fused transport's shapes run on it.
+void check_host_comm(const lina_comm* cm, const lina_moe_desc* d) {
+  if (!cm->host_allgather || cm->world == 1) return;
+  if (d->dtype != LINA_BF16 || d->d_model % 256 != 0 || d->d_ffn % 256 != 0)
+    throw StatusError{LINA_ERR_UNSUPPORTED,
+                      "a host-bootstrap communicator runs the fused transport only: bf16, d_model and d_ffn "
+                      "multiples of 256"};
+}
+
 void check_dropless(const lina_comm* cm, const lina_moe_desc* d) {
+  check_host_comm(cm, d);
   if ((d->capacity != 0 && d->pack <= 1) || cm->world == 1) return;
   std::vector<std::string> v;
   if (cm->transport != 2 || !cm->ce) v.push_back("LINA_TRANSPORT must be fused");
@@ -237,6 +247,70 @@ lina_status lina_get_unique_id(unsigned char host_id[128]) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+// The device side of a communicator (streams, events, route words); rank / world set.
+lina_comm* comm_base(int world, int rank, int cuda_device) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw StatusError{LINA_ERR_UNSUPPORTED, "no CUDA device visible (there is no CPU fallback)"};
+  if (cuda_device < 0 || cuda_device >= ndev) throw ArgError{"cuda_device out of range"};
+  LINA_CUDA_CHECK(cudaSetDevice(cuda_device));
+  cudaDeviceProp prop;
+  LINA_CUDA_CHECK(cudaGetDeviceProperties(&prop, cuda_device));
+  if (prop.major != 10)
+    throw StatusError{LINA_ERR_UNSUPPORTED, "device is sm_" + std::to_string(prop.major) +
+                                                std::to_string(prop.minor) + "; this library is built for sm_100a only"};
+  auto* cm = new lina_comm();
+  cm->rank = rank;
+  cm->world = world;
+  cm->device = cuda_device;
+  cm->num_sms = prop.multiProcessorCount;
+  int lo_prio = 0, hi_prio = 0;
+  LINA_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->hi, cudaStreamNonBlocking, hi_prio));
+  LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->hi2, cudaStreamNonBlocking, hi_prio));
+  LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->lo, cudaStreamNonBlocking, lo_prio));
+  LINA_CUDA_CHECK(cudaMalloc(&cm->route_sync, sizeof(unsigned int) * route_sync_words()));
+  LINA_CUDA_CHECK(cudaMemset(cm->route_sync, 0, sizeof(unsigned int) * route_sync_words()));
+  cm->ev.resize(128);
+  for (auto& e : cm->ev) LINA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const char* trv = getenv("LINA_TRACE");
+  if (trv && atoi(trv) > 0) cm->trace = trace_create();
+  return cm;
+}
+}  // namespace
+
+namespace lina {
+void host_allgather(lina_comm* cm, const void* send, void* recv, size_t bytes) {
+  if (!cm->host_allgather) throw StatusError{LINA_ERR_UNSUPPORTED, "host allgather on an NCCL communicator"};
+  if (cm->host_allgather(send, recv, bytes, cm->host_ctx) != 0)
+    throw StatusError{LINA_ERR_CUDA, "host allgather callback failed"};
+}
+void comm_barrier(lina_comm* cm, cudaStream_t s) {
+  if (cm->world == 1) {
+    LINA_CUDA_CHECK(cudaStreamSynchronize(s));
+    return;
+  }
+  if (cm->host_allgather) {
+    LINA_CUDA_CHECK(cudaStreamSynchronize(s));
+    std::vector<int> all((size_t)cm->world);
+    const int one = 1;
+    host_allgather(cm, &one, all.data(), sizeof(int));
+    return;
+  }
+  int* one = nullptr;
+  LINA_CUDA_CHECK(cudaMallocAsync((void**)&one, sizeof(int), s));
+  LINA_CUDA_CHECK(cudaMemsetAsync(one, 0, sizeof(int), s));
+  LINA_NCCL_CHECK(ncclAllReduce(one, one, 1, ncclInt32, ncclSum, cm->ep_disp, s));
+  LINA_CUDA_CHECK(cudaFreeAsync(one, s));
+  LINA_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+}  // namespace lina
+
+extern "C" {
+
 lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned char* host_id,
                            int nccl_max_ctas, lina_comm** out) {
   return guarded([&] {
@@ -247,31 +321,7 @@ lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned 
     if (world > 1 && !host_id) v.push_back("host_id is NULL with world > 1");
     if (nccl_max_ctas < 0) v.push_back("nccl_max_ctas < 0");
     raise_if(v, "lina_comm_init");
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-      throw StatusError{LINA_ERR_UNSUPPORTED, "no CUDA device visible (there is no CPU fallback)"};
-    if (cuda_device < 0 || cuda_device >= ndev) throw ArgError{"cuda_device out of range"};
-    LINA_CUDA_CHECK(cudaSetDevice(cuda_device));
-    cudaDeviceProp prop;
-    LINA_CUDA_CHECK(cudaGetDeviceProperties(&prop, cuda_device));
-    if (prop.major != 10)
-      throw StatusError{LINA_ERR_UNSUPPORTED, "device is sm_" + std::to_string(prop.major) +
-                                                  std::to_string(prop.minor) +
-                                                  "; this library is built for sm_100a only"};
-    auto* cm = new lina_comm();
-    cm->rank = rank;
-    cm->world = world;
-    cm->device = cuda_device;
-    cm->num_sms = prop.multiProcessorCount;
-    int lo_prio = 0, hi_prio = 0;
-    LINA_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-    LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->hi, cudaStreamNonBlocking, hi_prio));
-    LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->hi2, cudaStreamNonBlocking, hi_prio));
-    LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->lo, cudaStreamNonBlocking, lo_prio));
-    LINA_CUDA_CHECK(cudaMalloc(&cm->route_sync, sizeof(unsigned int) * route_sync_words()));
-    LINA_CUDA_CHECK(cudaMemset(cm->route_sync, 0, sizeof(unsigned int) * route_sync_words()));
-    cm->ev.resize(128);
-    for (auto& e : cm->ev) LINA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    lina_comm* cm = comm_base(world, rank, cuda_device);
     if (world > 1) {
       ncclUniqueId id;
       std::memcpy(&id, host_id, 128);
@@ -300,8 +350,28 @@ lina_status lina_comm_init(int world, int rank, int cuda_device, const unsigned 
       if (cm->transport > 0) cm->ce = new CeTransport(cm);
       tc_set_reserved_sms(cm->ce ? 0 : (nccl_max_ctas > 0 ? 2 * nccl_max_ctas : 16));
     }
-    const char* trv = getenv("LINA_TRACE");
-    if (trv && atoi(trv) > 0) cm->trace = trace_create();
+    *out = cm;
+    return LINA_OK;
+  });
+}
+
+lina_status lina_comm_init_host(int world, int rank, int cuda_device, lina_host_allgather_fn fn, void* ctx,
+                                lina_comm** out) {
+  return guarded([&] {
+    std::vector<std::string> v;
+    if (!out) v.push_back("out is NULL");
+    if (world < 1) v.push_back("world < 1");
+    if (rank < 0 || rank >= world) v.push_back("rank not in [0, world)");
+    if (!fn) v.push_back("fn is NULL");
+    raise_if(v, "lina_comm_init_host");
+    lina_comm* cm = comm_base(world, rank, cuda_device);
+    cm->host_allgather = fn;
+    cm->host_ctx = ctx;
+    if (world > 1) {
+      cm->transport = 2;  // fused: its exchanges are peer stores, its bootstrap host-side
+      cm->ce = new CeTransport(cm);
+      tc_set_reserved_sms(0);
+    }
     *out = cm;
     return LINA_OK;
   });
@@ -737,6 +807,8 @@ lina_status lina_allreduce_submit(lina_comm* cm, void* grad, size_t count, lina_
     need(v, grad, "grad");
     if (dtype != LINA_F32 && dtype != LINA_BF16) v.push_back("dtype not LINA_F32/LINA_BF16");
     raise_if(v, "lina_allreduce_submit");
+    if (!cm->sched && cm->world > 1)
+      throw StatusError{LINA_ERR_UNSUPPORTED, "allreduce needs an NCCL communicator (lina_comm_init)"};
     if (count == 0 || !cm->sched) return LINA_OK;  // world == 1: the sum over one rank is itself
     LINA_CUDA_CHECK(cudaSetDevice(cm->device));
     sched_submit(cm->sched, grad, count, dtype, (cudaStream_t)ready_stream);

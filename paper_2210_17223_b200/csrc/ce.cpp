@@ -148,12 +148,17 @@ std::vector<char*> CeTransport::map_collective(const void* local, cudaStream_t s
   const uint64_t off = (uint64_t)((const char*)local - (const char*)base);
   std::memcpy(rec + 64, &off, 8);
   std::memcpy(rec + 72, &layout_key, 8);
-  char* st = (char*)impl_->stage;
-  LINA_CUDA_CHECK(cudaMemcpyAsync(st + 128 * (size_t)cm_->rank, rec, 128, cudaMemcpyHostToDevice, s));
-  LINA_NCCL_CHECK(ncclAllGather(st + 128 * (size_t)cm_->rank, st, 128, ncclUint8, cm_->ep_disp, s));
   std::vector<unsigned char> all((size_t)128 * P);
-  LINA_CUDA_CHECK(cudaMemcpyAsync(all.data(), st, all.size(), cudaMemcpyDeviceToHost, s));
-  LINA_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (cm_->host_allgather) {  // host-bootstrap communicator: the caller's allgather
+    LINA_CUDA_CHECK(cudaStreamSynchronize(s));
+    host_allgather(cm_, rec, all.data(), 128);
+  } else {
+    char* st = (char*)impl_->stage;
+    LINA_CUDA_CHECK(cudaMemcpyAsync(st + 128 * (size_t)cm_->rank, rec, 128, cudaMemcpyHostToDevice, s));
+    LINA_NCCL_CHECK(ncclAllGather(st + 128 * (size_t)cm_->rank, st, 128, ncclUint8, cm_->ep_disp, s));
+    LINA_CUDA_CHECK(cudaMemcpyAsync(all.data(), st, all.size(), cudaMemcpyDeviceToHost, s));
+    LINA_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
   if (layout_key) {  // every rank sees the same records, so every rank throws or none does
     std::string bad;
     for (int r = 0; r < P; ++r) {

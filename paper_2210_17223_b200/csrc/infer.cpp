@@ -180,16 +180,24 @@ void infer_forward(lina_comm* cm, const lina_moe_desc& desc, const void* tokens,
   // ---- gate, dropless slots, counts (S1, S2 with C = T)
   launch_gate_topk(dtype, tokens, gate_w, T, d, E, k, 1, probs, idx, gate, s);
   launch_route(idx, T, k, E, std::max(T, 1), (int*)(w + q.o_route), slot, counts, kept, tokof, s, cm->route_sync);
-  if (P > 1) {
-    LINA_NCCL_CHECK(ncclAllGather(counts, allc, (size_t)E, ncclInt32, cm->ep_disp, s));
-  } else {
-    LINA_CUDA_CHECK(cudaMemcpyAsync(allc, counts, 4 * (size_t)E, cudaMemcpyDeviceToDevice, s));
-  }
   const size_t ctrl_ints = (size_t)P * E + q.tab_ints() + (size_t)P * mpd + (mpd + 1) + 2 * (size_t)mpd + 6 * (size_t)P;
   int* host = pinned(cm, ctrl_ints);
-  trace_mark(cm, s, "inf:gate+route+counts");
-  LINA_CUDA_CHECK(cudaMemcpyAsync(host, allc, 4 * (size_t)P * E, cudaMemcpyDeviceToHost, s));
-  LINA_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (P > 1 && cm->host_allgather) {  // host-bootstrap communicator: counts through the host
+    std::vector<int> mine((size_t)E);
+    LINA_CUDA_CHECK(cudaMemcpyAsync(mine.data(), counts, 4 * (size_t)E, cudaMemcpyDeviceToHost, s));
+    LINA_CUDA_CHECK(cudaStreamSynchronize(s));
+    host_allgather(cm, mine.data(), host, 4 * (size_t)E);
+    trace_mark(cm, s, "inf:gate+route+counts");
+  } else {
+    if (P > 1) {
+      LINA_NCCL_CHECK(ncclAllGather(counts, allc, (size_t)E, ncclInt32, cm->ep_disp, s));
+    } else {
+      LINA_CUDA_CHECK(cudaMemcpyAsync(allc, counts, 4 * (size_t)E, cudaMemcpyDeviceToDevice, s));
+    }
+    trace_mark(cm, s, "inf:gate+route+counts");
+    LINA_CUDA_CHECK(cudaMemcpyAsync(host, allc, 4 * (size_t)P * E, cudaMemcpyDeviceToHost, s));
+    LINA_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
   std::vector<int> cnt(host, host + (size_t)P * E);  // cnt[src*E + e]
   {  // dropless: every source sends T·k rows; the receive regions are sized for equal T
     std::string bad;

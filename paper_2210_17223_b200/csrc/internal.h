@@ -100,7 +100,19 @@ struct lina_comm {
   std::vector<int32_t> inf_recv_rows, inf_sent_rows;
   // expert packing: one NCCL communicator per packing factor m (the rank's group of m)
   std::map<int, ncclComm_t> group_comms;
+  // host-bootstrap communicator (lina_comm_init_host): no NCCL; exchanges go through this
+  lina_host_allgather_fn host_allgather = nullptr;
+  void* host_ctx = nullptr;
 };
+
+namespace lina {
+// Host allgather of `bytes` per rank through the comm's bootstrap (the caller's callback);
+// throws on failure.  Only for host-bootstrap communicators.
+void host_allgather(lina_comm* cm, const void* send, void* recv, size_t bytes);
+// Barrier of every rank: NCCL allreduce on the dispatch communicator, or the host
+// allgather of a host-bootstrap communicator (after synchronising `s`).
+void comm_barrier(lina_comm* cm, cudaStream_t s);
+}  // namespace lina
 
 namespace lina {
 // Profiling helpers (api.cpp): open/close one timed expert-GEMM phase on stream s.

@@ -724,6 +724,8 @@ void backward_fused_movers(lina_comm* cm, const Plan& p, const Ptrs& q, const vo
 ncclComm_t group_comm(lina_comm* cm, int m) {
   auto it = cm->group_comms.find(m);
   if (it != cm->group_comms.end()) return it->second;
+  if (!cm->ep_disp)
+    throw StatusError{LINA_ERR_UNSUPPORTED, "expert packing needs an NCCL communicator (lina_comm_init)"};
   ncclComm_t g = nullptr;
   ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
   LINA_NCCL_CHECK(ncclCommSplit(cm->ep_disp, cm->rank / m, cm->rank, &g, &cfg));

@@ -42,23 +42,13 @@ int pack_decide(int world, int pack, double ffn_ms, double a2a_ms) {
   return pack;
 }
 
-// A barrier of every rank on the device stream, then the host waits for it.
-static void barrier(lina_comm* cm, cudaStream_t s) {
-  int* one = nullptr;
-  LINA_CUDA_CHECK(cudaMallocAsync((void**)&one, sizeof(int), s));
-  LINA_CUDA_CHECK(cudaMemsetAsync(one, 0, sizeof(int), s));
-  LINA_NCCL_CHECK(ncclAllReduce(one, one, 1, ncclInt32, ncclSum, cm->ep_disp, s));
-  LINA_CUDA_CHECK(cudaFreeAsync(one, s));
-  LINA_CUDA_CHECK(cudaStreamSynchronize(s));
-}
-
 void pack_weights(lina_comm* cm, int E, int m0, int m1, size_t expert_bytes, const void* w_from, void* w_to,
                   cudaStream_t s) {
   const int P = cm->world, me = cm->rank;
   const int Elb = E / P, El0 = m0 * Elb, El1 = m1 * Elb;
   std::vector<char*> src(P, nullptr);
   if (P > 1) {
-    barrier(cm, s);  // every rank's w_from is complete
+    comm_barrier(cm, s);  // every rank's w_from is complete
     src = cm->ce->peers(w_from, s);
   } else {
     src[0] = (char*)w_from;
@@ -71,7 +61,7 @@ void pack_weights(lina_comm* cm, int E, int m0, int m1, size_t expert_bytes, con
                                     src[r] + (size_t)(e - g0 * El0) * expert_bytes, expert_bytes,
                                     cudaMemcpyDeviceToDevice, s));
   }
-  if (P > 1) barrier(cm, s);  // nobody changes w_from before every rank has copied
+  if (P > 1) comm_barrier(cm, s);  // nobody changes w_from before every rank has copied
 }
 
 }  // namespace lina

@@ -33,7 +33,7 @@ ABI_SYMBOLS = [
     "lina_popprof_create", "lina_popprof_destroy", "lina_popprof_add", "lina_popprof_estimate",
     "lina_phase_two_check", "lina_moe_infer_forward_two_phase", "lina_popprof_save", "lina_popprof_load",
     "lina_popprof_info", "lina_infer_last_rows", "lina_pack_decide", "lina_pack_ctl_create", "lina_pack_ctl_step",
-    "lina_pack_ctl_destroy", "lina_pack_weights",
+    "lina_pack_ctl_destroy", "lina_pack_weights", "lina_comm_init_host",
 ]
 
 
@@ -88,6 +88,7 @@ def load() -> ctypes.CDLL:
         "lina_version": ([], ctypes.c_char_p),
         "lina_get_unique_id": ([ctypes.c_char_p], i32),
         "lina_comm_init": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, P(vp)], i32),
+        "lina_comm_init_host": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, HostAllgather, vp, P(vp)], i32),
         "lina_comm_destroy": ([vp], i32),
         "lina_comm_check": ([vp], i32),
         "lina_comm_info": ([vp, P(ctypes.c_int), P(ctypes.c_int)], i32),
@@ -176,8 +177,35 @@ def lina_get_unique_id() -> bytes:
     return buf.raw
 
 
+# lina_host_allgather_fn: int (*)(const void* send, void* recv, size_t bytes, void* ctx)
+HostAllgather = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+
+
 class Comm:
-    """One lina_comm per rank (lina_comm_init / lina_comm_destroy)."""
+    """One lina_comm per rank (lina_comm_init / lina_comm_init_host / lina_comm_destroy)."""
+
+    @classmethod
+    def host(cls, world: int, rank: int, device: int, allgather):
+        """lina_comm_init_host: no NCCL; `allgather(data: bytes) -> list[bytes]` (one entry per
+        rank, rank order) carries the bootstrap exchanges, e.g. over a torch gloo group."""
+        obj = cls.__new__(cls)
+        obj.handle = ctypes.c_void_p()
+
+        def cb(send, recv, nbytes, _ctx):
+            try:
+                parts = allgather(ctypes.string_at(send, nbytes))
+                buf = b"".join(parts)
+                if len(buf) != nbytes * world:
+                    return 1
+                ctypes.memmove(recv, buf, len(buf))
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a failed exchange by the library
+                return 1
+
+        obj._cb = HostAllgather(cb)  # kept alive with the communicator
+        _check(load().lina_comm_init_host(world, rank, device, obj._cb, None, ctypes.byref(obj.handle)))
+        obj.world, obj.rank, obj.device = world, rank, device
+        return obj
 
     def __init__(self, world: int = 1, rank: int = 0, device: int = 0, unique_id: bytes | None = None,
                  nccl_max_ctas: int = 0):

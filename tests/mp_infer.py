@@ -29,11 +29,11 @@ def main():
     ap.add_argument("--seed", type=int, default=11)
     ap.add_argument("--min-replicas", type=int, default=1,
                     help="fail unless the plan replicates some expert at least this many times")
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="every rank on GPU 0 with a host-bootstrap communicator (no NCCL; tests/mp_util.py)")
     a = ap.parse_args()
-    world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    from tests.mp_util import setup
+    world, rank, dev, comm, flag_dev = setup(a.shared_gpu, 8)
     import paper_2210_17223_b200 as lina
     from paper_2210_17223_b200.lina import PlacementTables
 
@@ -41,9 +41,6 @@ def main():
     cfg = li.with_tokens(li.CONFIGS["C4"], a.tokens, **changes)
     E, T = cfg.num_experts, cfg.tokens_per_rank
     mpd = a.mpd or 2 * E // world
-    uid = [lina.lina_get_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    comm = lina.Comm(world, rank, local, uid[0], 8)
     Wg, W1, W2 = li.layer_weights(cfg, a.seed, "zipf")
     X, _ = li.layer_tokens(cfg, a.seed, rank, "zipf", zipf_s=a.zipf)
     dt = torch.bfloat16
@@ -109,7 +106,7 @@ def main():
               f"{[gathered[dv]['rows_rep'][0] for dv in range(world)]}",
               f"max/mean tokens per device: replicated {per_dev.max() / per_dev.mean():.2f} "
               f"static {static_dev.max() / static_dev.mean():.2f}", flush=True)
-    flag = torch.tensor([1 if ok else 0], device=dev)
+    flag = torch.tensor([1 if ok else 0], device=flag_dev)
     dist.broadcast(flag, 0)
     comm.close()
     dist.destroy_process_group()

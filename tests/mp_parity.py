@@ -44,11 +44,14 @@ def main():
                     help="expert packing factor m (P:376): groups of m ranks host the same m*E/world experts")
     ap.add_argument("--pack-exchange", action="store_true",
                     help="build the packed weights with lina_pack_weights from the unpacked ones (P:505)")
+    ap.add_argument("--ragged-ranks", type=int, default=0,
+                    help="rank r holds T - r*R tokens (same capacity C on every rank): the peer-visible buffer "
+                         "regions must not depend on num_tokens")
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="every rank on GPU 0 with a host-bootstrap communicator (no NCCL; tests/mp_util.py)")
     a = ap.parse_args()
-    world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    from tests.mp_util import setup
+    world, rank, dev, comm, flag_dev = setup(a.shared_gpu, 0)
     import paper_2210_17223_b200 as lina
 
     changes = {}
@@ -58,9 +61,6 @@ def main():
         changes["k"] = a.k
     cfg = li.with_tokens(li.CONFIGS[a.config], a.tokens, **changes)
     E, El = cfg.num_experts, cfg.num_experts // world
-    uid = [lina.lina_get_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    comm = lina.Comm(world, rank, local, uid[0])
     m = max(1, a.pack)
     G = rank // m                    # packing group; its experts [G*m*El, (G+1)*m*El)
     hosted = range(G * m * El, (G + 1) * m * El)
@@ -77,13 +77,16 @@ def main():
             got.append(dst.float().cpu().numpy())
         exchange_ok = np.array_equal(got[0], torch.from_numpy(W1).to(tdt_).float().numpy()) and \
             np.array_equal(got[1], torch.from_numpy(W2).to(tdt_).float().numpy())
-    X, dY = li.layer_tokens(cfg, a.seed, rank)
+    def T_of(r):
+        return cfg.tokens_per_rank - r * a.ragged_ranks
+
+    X, dY = li.layer_tokens(cfg, a.seed, rank, num_tokens=T_of(rank))
     tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
 
     C_layer = 0 if a.dropless else cfg.capacity()
 
     def run(n_chunks):
-        layer = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, C_layer,
+        layer = lina.MoELayer(comm, T_of(rank), cfg.d_model, cfg.d_ffn, E, cfg.k, C_layer,
                               n_chunks, tdt, dev, pack=m)
         if a.poison:  # every byte the layer reads must be one it (or a peer) wrote this step
             layer.saved.fill_(0xFF)
@@ -98,11 +101,11 @@ def main():
         y = layer.forward(x, wg, w1, w2, want_route=True)
         finite_b = True
         if a.interleave:  # layer B's exchanges run between A's forward and backward
-            layer_b = lina.MoELayer(comm, cfg.tokens_per_rank, cfg.d_model, cfg.d_ffn, E, cfg.k, C_layer,
+            layer_b = lina.MoELayer(comm, T_of(rank), cfg.d_model, cfg.d_ffn, E, cfg.k, C_layer,
                                     n_chunks, tdt, dev, pack=m)
             if a.shared_ws:
                 layer_b.workspace = layer.workspace
-            XB, dYB = li.layer_tokens(cfg, a.seed + 1, rank)
+            XB, dYB = li.layer_tokens(cfg, a.seed + 1, rank, num_tokens=T_of(rank))
             xb = torch.from_numpy(XB).to(tdt).to(dev)
             yb = layer_b.forward(xb, wg, w1, w2)
             dxb = layer_b.backward(torch.from_numpy(dYB).to(tdt).to(dev), xb, wg, w1, w2)[0]
@@ -163,8 +166,8 @@ def main():
     if rank == 0:
         from oracle import moe
         Wg_all, W1_all, W2_all = li.layer_weights(cfg, a.seed)
-        Xs = [li.layer_tokens(cfg, a.seed, r)[0] for r in range(world)]
-        dYs = [li.layer_tokens(cfg, a.seed, r)[1] for r in range(world)]
+        Xs = [li.layer_tokens(cfg, a.seed, r, num_tokens=T_of(r))[0] for r in range(world)]
+        dYs = [li.layer_tokens(cfg, a.seed, r, num_tokens=T_of(r))[1] for r in range(world)]
         C_ref = cfg.tokens_per_rank if a.dropless else cfg.capacity()
         fw = moe.moe_forward(Xs, Wg_all, W1_all, W2_all, cfg.k, C_ref, cfg.dtype)
         bw = moe.moe_backward(fw, Xs, dYs, Wg_all, W1_all, W2_all, cfg.k, cfg.dtype)
@@ -184,7 +187,7 @@ def main():
         ok &= all(g["exchange_ok"] for g in gathered)
         print("MP_PARITY", "OK" if ok else "FAIL", f"world={world} cfg={cfg.name} T={cfg.tokens_per_rank} "
               f"n={a.n_chunks}" + (" dropless" if a.dropless else "") + (f" pack={m}" if m > 1 else ""), " ".join(f"{k}={v:.2e}" for k, v in errs.items()), flush=True)
-    flag = torch.tensor([1 if ok else 0], device=dev)
+    flag = torch.tensor([1 if ok else 0], device=flag_dev)
     dist.broadcast(flag, 0)
     comm.close()
     dist.destroy_process_group()

@@ -78,3 +78,26 @@ def test_two_phase_keeps_or_replans(estimate_matches):
     ref = given if estimate_matches else oplace.place(list(actual), 1, E)
     assert plan.replicas == ref["replicas"] and plan.hosted == ref["hosted"]
     assert moe.normwise_error(out.float().cpu().numpy(), fw.y) <= TOL[cfg.dtype]
+
+
+@pytest.mark.parametrize("bad,needle", [
+    ({"replicas": [2, 1, 1, 1]}, "replicas 2 not in"),            # r_e > world (1)
+    ({"replica_device": [[0], [5], [0], [0]]}, "not in [0, num_devices)"),
+    ({"hosted": [[0, 1, 2, 7]]}, "not in [-1, num_experts)"),
+    ({"hosted": [[0, 1, 2, -1]]}, "does not host it"),            # expert 3's device does not list it
+    ({"hosted": [[0, 1, 2, 2]]}, "twice"),
+])
+def test_infer_rejects_inconsistent_placement(bad, needle):
+    """A caller-supplied placement is checked entry by entry before its tables index device
+    buffers: INVALID_ARGUMENT naming the violation, nothing launched."""
+    import paper_2210_17223_b200 as lina
+    from paper_2210_17223_b200.lina import LinaError, PlacementTables
+    cfg = li.with_tokens(li.CONFIGS["C4"], 64, num_experts=4)
+    Wg, W1, W2 = li.layer_weights(cfg, 5, "grid")
+    X, _ = li.layer_tokens(cfg, 5, 0, "grid")
+    tables = {"replicas": [1, 1, 1, 1], "replica_device": [[0], [0], [0], [0]], "hosted": [[0, 1, 2, 3]]}
+    tables.update(bad)
+    pl = PlacementTables(tables["replicas"], tables["replica_device"], tables["hosted"])
+    with pytest.raises(LinaError) as ei:
+        _run_infer(cfg, X, Wg, W1, W2, mpd=4, placement=pl)
+    assert needle in str(ei.value) and ei.value.status == 1

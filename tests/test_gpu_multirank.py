@@ -42,6 +42,13 @@ def test_two_ranks_interleaved_layers_shared_workspace():
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_two_ranks_unequal_token_counts():
+    """Ranks with different num_tokens (512 and 475) and one capacity: every peer-visible
+    buffer region sits at a T-independent offset, so the peer stores land right."""
+    _run(2, "--config", "C2", "--tokens", "512", "--n-chunks", "2", "--ragged-ranks", "37", "--poison", port=29618)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("cfg,tokens,extra", [
     ("C2", 512, ["--poison", "--graph"]),
     ("C3", 256, ["--interleave", "--shared-ws"]),
