@@ -179,20 +179,30 @@ __global__ void __launch_bounds__(192, 1)
         if (s >= 0) rows[j] = ebase ? (size_t)(ebase[e] + s) : send_row(e, s, E, C, n, Cm);
       }
     }
-    mbar_wait(tfull, 0);
-    tc_fence_after();
-    const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16);
-    for (int cb = 0; cb < 256; cb += 32) {
-      float acc[32];
-      tmem_ld32(ta + cb, *reinterpret_cast<uint32_t(*)[32]>(acc));
-      uint4 g[KM][4];
+    // the k rows' 32-column slices of the next block are loaded before the current block is
+    // summed (two blocks in flight per thread; KM = 2 only — KM = 8 would spill)
+    constexpr bool PREF = KM <= 2;
+    uint4 g[PREF ? 2 : 1][KM][4];
+    auto load_rows = [&](int cb, uint4 (&dst)[KM][4]) {
 #pragma unroll
       for (int j = 0; j < KM; ++j)
 #pragma unroll
         for (int v = 0; v < 4; ++v)
-          g[j][v] = rows[j] != ~(size_t)0
-                        ? *reinterpret_cast<const uint4*>(dXe + rows[j] * d + n0 + cb + 8 * v)
-                        : make_uint4(0, 0, 0, 0);
+          dst[j][v] = rows[j] != ~(size_t)0 ? *reinterpret_cast<const uint4*>(dXe + rows[j] * d + n0 + cb + 8 * v)
+                                            : make_uint4(0, 0, 0, 0);
+    };
+    load_rows(0, g[0]);
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int cb = 32 * i;
+      float acc[32];
+      tmem_ld32(ta + cb, *reinterpret_cast<uint32_t(*)[32]>(acc));
+      if (PREF && i + 1 < 8) load_rows(cb + 32, g[(i + 1) & 1]);
+      if (!PREF && i > 0) load_rows(cb, g[0]);
+      uint4 (&cur)[KM][4] = g[PREF ? (i & 1) : 0];
       tmem_wait_ld();
       if (t < T) {
 #pragma unroll
@@ -200,7 +210,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
             float x[8];
-            load16(&g[j][v], x, (const __nv_bfloat16*)nullptr);
+            load16(&cur[j][v], x, (const __nv_bfloat16*)nullptr);
 #pragma unroll
             for (int u = 0; u < 8; ++u) acc[8 * v + u] += x[u];
           }

@@ -64,13 +64,18 @@ def assert_close(got, ref, tol, what):
     return err
 
 
-def compare(cfg, g, o, check_bwd=True):
+def compare(cfg, g, o, check_bwd=True, p_rtol=2e-6):
+    """p_rtol bounds the fp32 probabilities and gate weights.  On grid inputs the logits are
+    exact on both sides, so 2e-6 (a few ulp of the softmax) holds; on non-grid inputs the
+    GPU's fp32 logits differ from the oracle's fp64-then-rounded ones by accumulation order
+    (|dL| ~ 1e-6 |L|), which a softmax ratio amplifies by |L| — those callers pass 2e-5."""
     fw = o["fw"]
     assert np.array_equal(g["idx"], fw.idx), "routing idx differs"
     assert np.array_equal(g["slot"], fw.slot), "capacity slots differ"
     assert np.array_equal(g["counts"], fw.counts), "per-expert counts differ"
-    assert np.allclose(g["gate"], fw.gate, rtol=2e-6, atol=1e-7), "gate weights differ"
-    assert np.allclose(g["probs"], fw.p, rtol=2e-6, atol=1e-7), "probabilities differ"
+    assert np.allclose(g["gate"], fw.gate, rtol=p_rtol, atol=1e-7), \
+        f"gate weights differ (max rel {np.max(np.abs(g['gate'] - fw.gate) / np.maximum(np.abs(fw.gate), 1e-30)):.2e})"
+    assert np.allclose(g["probs"], fw.p, rtol=p_rtol, atol=1e-7), "probabilities differ"
     tol = TOL[cfg.dtype]
     errs = {"y": assert_close(g["y"], fw.y, tol, "y")}
     if check_bwd and "bw" in o:

@@ -160,11 +160,11 @@ def test_c2_full_size_sampled():
 def test_comm_and_errors():
     import paper_2210_17223_b200 as lina
     comm = lina.Comm(1, 0, 0)
-    bad = lina.make_desc(10, 30, 64, 5, 9, 0, 40, "bf16")
+    bad = lina.make_desc(10, 30, 64, 5, 9, -1, 40, "bf16")
     with pytest.raises(lina.LinaError) as ei:
         lina.lina_moe_workspace_size(comm, bad)
     msg = str(ei.value)
-    for frag in ["k not in", "capacity < 1", "n_chunks", "d_model % 16"]:
+    for frag in ["k not in", "capacity < 0", "n_chunks", "d_model % 16"]:
         assert frag in msg, msg
     good = lina.make_desc(64, 64, 256, 4, 1, 16, 1, "f32")
     ws, sv = lina.lina_moe_workspace_size(comm, good)
@@ -308,7 +308,7 @@ def test_dropless_skewed_routing():
     g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY, capacity=0)
     o = oracle_layer(cfg, X, Wg, W1, W2, dY, capacity=512)
     assert np.bincount(g["idx"][:, 0], minlength=8).max() > 512 * 0.3
-    compare(cfg, g, o)
+    compare(cfg, g, o, p_rtol=2e-5)  # non-grid inputs (parity_util.compare)
 
 
 def test_dropless_footprint_against_padded_layout():
