@@ -342,8 +342,11 @@ size_t al256(size_t b) { return (b + 255) / 256 * 256; }
 
 }  // namespace
 
+// As the gate: the tensor-core dX / dWg win once the E-wide contractions dominate (C5:
+// 170 + 101 vs 522 + 740 us); at E <= 16 the CUDA-core tiles are faster (C2: 16 + 15 vs
+// 28 + 26 us, profiles/r02_launches_c2_n1_*.txt).
 bool gate_bwd_tc_supported(int dtype, int d, int E, int k) {
-  return dtype == 1 && d % 256 == 0 && E >= 1 && E <= kEP && k >= 1 && k <= 8;
+  return dtype == 1 && d % 256 == 0 && E > 16 && E <= kEP && k >= 1 && k <= 8;
 }
 
 // Scratch (bytes) of the tensor-core gate backward inside the dWg workspace region:

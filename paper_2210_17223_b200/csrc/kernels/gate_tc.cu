@@ -256,7 +256,10 @@ void launch_gate_tc_t(const void* X, const float* Wg, int T, int d, int E, int k
 
 }  // namespace
 
-bool gate_tc_supported(int d, int E, int k) { return d % kGBK == 0 && d > 0 && E >= 1 && E <= 64 && k <= 8; }
+// The tensor-core gate pays off once E is large (C5, E = 64: 60 vs 377 us); for E <= 16 the
+// mma.sync kernel's staged split Wg is small and its 32-token CTAs fill the GPU at small T
+// (C2, E = 8, T = 8192: 10.9 vs 18 + 3 us, profiles/r02_launches_c2_n1_*.txt).
+bool gate_tc_supported(int d, int E, int k) { return d % kGBK == 0 && d > 0 && E > 16 && E <= 64 && k <= 8; }
 
 void launch_gate_tc(const void* X, const float* Wg, int T, int d, int E, int k, int write_routing, float* probs,
                     int* idx, float* gate, const PeerSignal& sig, cudaStream_t s) {

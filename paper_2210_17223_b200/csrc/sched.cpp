@@ -199,15 +199,23 @@ class Scheduler {
       const bool split = policy_ == LINA_SCHED_LINA;
       bool can_issue = true;
       if (gated) {
-        if (cudaEventQuery(j.ready) == cudaErrorNotReady) can_issue = false;
-        else if (policy_ == LINA_SCHED_DEFER ? a2a_inflight_locked(j.a2a_limit) : a2a_busy_locked(j.a2a_limit)) {
+        const bool busy =
+            policy_ == LINA_SCHED_DEFER ? a2a_inflight_locked(j.a2a_limit) : a2a_busy_locked(j.a2a_limit);
+        if (cudaEventQuery(j.ready) == cudaErrorNotReady) {
+          // Not ready yet.  A job ahead of a wait point (finite a2a_limit) with every
+          // all-to-all phase before that point already drained can meet no further
+          // all-to-all before it runs (later phases sit behind the wait on the device),
+          // so it is issued now and `lo` waits for its gradient on the device — no host
+          // polling latency between the gradient and its allreduce.
+          can_issue = j.a2a_limit != ~0ull && !busy;
+        } else if (busy) {
           can_issue = false;
           ++deferred_;
         }
       }
       if (!can_issue) {
         g.unlock();
-        std::this_thread::sleep_for(std::chrono::microseconds(10));
+        std::this_thread::sleep_for(std::chrono::microseconds(2));
         g.lock();
         continue;
       }
