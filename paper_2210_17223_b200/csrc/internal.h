@@ -48,6 +48,8 @@ struct Plan {
   // offsets (bytes) into `saved`
   size_t s_probs, s_idx, s_gate, s_slot, s_kept, s_tokof, s_recvkept, s_vcount, s_mtp, s_R, s_H,
       s_C, s_mask;
+  size_t s_mtpt = 0, s_rbase = 0;  // tail-split tile lists (tc row GEMMs with 256-row tiles)
+  bool tail_split = false;
   size_t saved_bytes;
   // offsets into `workspace`
   size_t w_route, w_D, w_O, w_dg, w_dwg, w_dS, w_dO, w_dH, w_dXe, w_dXs;

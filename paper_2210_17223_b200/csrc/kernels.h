@@ -27,6 +27,12 @@ struct RowGemm {
   const uint64_t* mask_in = nullptr;  // tcgen05 mask epilogue: those bits (aux unused)
   const PeerSignal* sig = nullptr;    // tcgen05: wait before the first A load, post after the last store
   int tile_rows = 256;                // tcgen05 M tile (256: CTA pairs, 128: single CTAs); = mtp's rows
+  // tail split (tile_rows 256, tcgen05): mtp counts each segment's 256-row tiles except a
+  // last one holding <= 128 rows, which a second launch computes as a 128-row single-CTA
+  // tile (mtp_tail: prefix of those [nseg+1]; row_base[global segment] = its first row) —
+  // a 129th..256th row costs a full 256-row MMA, a <= 128-row tail only half of one
+  const int* mtp_tail = nullptr;
+  const int* row_base = nullptr;
 };
 
 // Weight-gradient GEMM: D[El][M][N] = Σ_{c,s} Σ_{r < v} A[seg][r][:]ᵀ B[seg][r][:].
@@ -113,6 +119,10 @@ int tc_tile_rows();
 void tc_set_reserved_sms(int n);
 // mtp[c][i] = Σ_{i' < i} ceil(vcount[c*nseg + i'] / rows), i in [0, nseg]  (tcgen05 tile lists)
 void launch_mtile_prefix(const int* vcount, int n, int nseg, int rows, int* mtp, cudaStream_t s);
+// the tail-split lists: mtp[c][nseg+1] (256-row tiles, a last tile only when it holds > 128
+// rows), mtp_tail[c][nseg+1] (one 128-row tile per segment whose remainder is 1..128 rows),
+// rbase[c][nseg] (that tile's first row)
+void launch_mtile_split(const int* vcount, int n, int nseg, int* mtp, int* mtp_tail, int* rbase, cudaStream_t s);
 bool tc_row_supported(const RowGemm& g);
 bool tc_wgrad_supported(const WGrad& g);
 void launch_row_gemm_tc(const RowGemm& g, bool b_kmajor, int epi, cudaStream_t s);
@@ -146,12 +156,13 @@ struct DlTables {
   int* vexp;       // [V]   local expert (weight index) of the segment
   int* vsrc;       // [V]   source rank of the segment's rows
   int* vq0;        // [V]   first slot (within the source's expert block) of the segment
-  int* mtp;        // [V+1] m-tile prefix (one tile per used segment)
+  int* mtp;        // [V+1] m-tile prefix (one tile per used segment; with the tail split: > 128 rows)
+  int* mtpt;       // [V+1] tail-split prefix: segments holding 1..128 rows
   int* vrange;     // [E_l][2] segment range of each local expert (wgrad)
 };
 void launch_dl_counts(const int* kept, int* const* peer_allc, int P, int me, int E, const PeerSignal& sig,
                       cudaStream_t s);
-void launch_dl_layout(const int* allc, int P, int E, int El, int m, int me, int R, int V, const DlTables& t,
+void launch_dl_layout(const int* allc, int P, int E, int El, int m, int me, int R, int V, int split, const DlTables& t,
                       cudaStream_t s);
 // peer_dst: device array [P] of the owners' buffers (fused transport), or NULL and local_dst.
 // El = experts hosted per rank, m = packing factor (owner of my rows of e: (e/El)*m + me%m).

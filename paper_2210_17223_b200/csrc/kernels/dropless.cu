@@ -52,7 +52,7 @@ __global__ void dl_counts_kernel(const int* __restrict__ kept, int* const* __res
 // every owner has El·Q = E blocks.
 constexpr int kMaxPE = 512;
 __global__ void __launch_bounds__(256) dl_layout_kernel(const int* __restrict__ allc, int P, int E, int El, int m,
-                                                        int me, int R, int V, DlTables t) {
+                                                        int me, int R, int V, int split, DlTables t) {
   pdl_enter();
   __shared__ int cnt[kMaxPE];
   __shared__ int vb[kMaxPE];     // [o][el][j]: first virtual segment of block (el, j) at owner o
@@ -127,7 +127,23 @@ __global__ void __launch_bounds__(256) dl_layout_kernel(const int* __restrict__ 
     t.vsrc[v] = 0;
     t.vq0[v] = 0;
   }
-  for (int v = threadIdx.x; v <= V; v += blockDim.x) t.mtp[v] = min(v, U);  // one M tile per used segment
+  if (!split) {
+    for (int v = threadIdx.x; v <= V; v += blockDim.x) t.mtp[v] = min(v, U);  // one M tile per used segment
+  } else {  // tail split: segments of > 128 rows as 256-row tiles, the others as 128-row tiles
+    __syncthreads();  // (the vcount stores above are visible to the block after this)
+    if (threadIdx.x == 0) {
+      int a = 0, b = 0;
+      for (int v = 0; v < V; ++v) {
+        t.mtp[v] = a;
+        t.mtpt[v] = b;
+        const int c = t.vcount[v];
+        a += c > 128 ? 1 : 0;
+        b += (c > 0 && c <= 128) ? 1 : 0;
+      }
+      t.mtp[V] = a;
+      t.mtpt[V] = b;
+    }
+  }
   for (int el = threadIdx.x; el < El; el += blockDim.x) {
     t.vrange[2 * el] = vb[me * E + el * Q];
     t.vrange[2 * el + 1] = el + 1 < El ? vb[me * E + (el + 1) * Q] : U;
@@ -315,10 +331,10 @@ void launch_dl_counts(const int* kept, int* const* peer_allc, int P, int me, int
   LINA_LAUNCH_CHECK();
 }
 
-void launch_dl_layout(const int* allc, int P, int E, int El, int m, int me, int R, int V, const DlTables& t,
+void launch_dl_layout(const int* allc, int P, int E, int El, int m, int me, int R, int V, int split, const DlTables& t,
                       cudaStream_t s) {
   if (P * E > kMaxPE || P > 8) throw CudaError{"dropless layout: P*E > 512 or P > 8"};
-  launch_k(dl_layout_kernel, dim3(1), dim3(256), 0, s, allc, P, E, El, m, me, R, V, t);
+  launch_k(dl_layout_kernel, dim3(1), dim3(256), 0, s, allc, P, E, El, m, me, R, V, split, t);
   LINA_LAUNCH_CHECK();
 }
 

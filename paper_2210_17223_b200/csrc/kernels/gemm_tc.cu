@@ -77,6 +77,7 @@ struct TcParams {
   const __nv_bfloat16* aux;
   int nchunks, P;      // WGRAD
   const int* seg_range;  // WGRAD, dropless layout: expert el's segments [seg_range[2el], seg_range[2el+1])
+  const int* row_base;   // ROW tail launches: first row of each (global) segment's tail tile
   // ROW with peer stores: output tile of segment (c, s, el) goes through pmaps[s] to
   // segment c*dE + dme*El + el of rank s's buffer (the combine all-to-all fused into
   // the epilogue); has_pmaps = 0: local store through tmD
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
         else hi = mid - 1;
       }
       seg_or_el = i;  // local segment index within this launch
-      m0 = (ml - p.mtp[i]) * G::ROWS;
+      m0 = (ml - p.mtp[i]) * G::ROWS + (p.row_base ? __ldg(p.row_base + p.seg0 + i) : 0);
     }
   };
   auto kblocks_of = [&](int seg_or_el) {
@@ -542,6 +543,26 @@ static void row_gemm_tc_impl_t(const RowGemm& g, bool b_kmajor, int epi, const P
 
 static void row_gemm_tc_impl(const RowGemm& g, bool b_kmajor, int epi, const PeerStore* ps,
                              cudaStream_t s) {
+  if (g.tile_rows == 256 && g.mtp_tail) {
+    // tail split: the 256-row tiles, then the <= 128-row tails as single-CTA tiles; only the
+    // second launch publishes READY (its CTAs start after the first launch has completed)
+    RowGemm main = g;
+    PeerSignal msig;
+    if (g.sig) {
+      msig = *g.sig;
+      msig.post = nullptr;
+      main.sig = &msig;
+    }
+    main.mtp_tail = nullptr;
+    main.row_base = nullptr;
+    row_gemm_tc_impl_t<2>(main, b_kmajor, epi, ps, s);
+    RowGemm tail = g;
+    tail.tile_rows = 128;
+    tail.mtp = g.mtp_tail;
+    tail.mtp_tail = nullptr;
+    row_gemm_tc_impl_t<1>(tail, b_kmajor, epi, ps, s);
+    return;
+  }
   if (g.tile_rows == 128) row_gemm_tc_impl_t<1>(g, b_kmajor, epi, ps, s);
   else if (g.tile_rows == 256) row_gemm_tc_impl_t<2>(g, b_kmajor, epi, ps, s);
   else throw CudaError{"tcgen05 row GEMM: tile_rows must be 128 or 256"};
@@ -581,6 +602,7 @@ static void row_gemm_tc_impl_t(const RowGemm& g, bool b_kmajor, int epi, const P
   p.aux = (const __nv_bfloat16*)g.aux;
   p.mask_out = g.mask_out;
   p.mask_in = g.mask_in;
+  p.row_base = g.row_base;
   if (g.sig) p.sig = *g.sig;
   if (epi == kEpiMask && !g.mask_in) throw CudaError{"tcgen05 dgrad needs the ReLU' bit mask"};
   const uint64_t ddims[3] = {(uint64_t)g.N, (uint64_t)g.Cm, (uint64_t)nseg_total};

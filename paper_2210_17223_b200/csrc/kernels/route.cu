@@ -240,7 +240,31 @@ __global__ void mtile_prefix_kernel(const int* __restrict__ vcount, int n, int n
   mtp[c * (nseg + 1) + nseg] = run;
 }
 
+__global__ void mtile_split_kernel(const int* __restrict__ vcount, int n, int nseg, int* __restrict__ mtp,
+                                   int* __restrict__ mtpt, int* __restrict__ rbase) {
+  pdl_enter();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  int run = 0, runt = 0;
+  for (int i = 0; i < nseg; ++i) {
+    const int v = vcount[c * nseg + i], full = v / 256, rem = v % 256;
+    mtp[c * (nseg + 1) + i] = run;
+    mtpt[c * (nseg + 1) + i] = runt;
+    rbase[c * nseg + i] = full * 256;
+    run += full + (rem > 128 ? 1 : 0);
+    runt += (rem > 0 && rem <= 128) ? 1 : 0;
+  }
+  mtp[c * (nseg + 1) + nseg] = run;
+  mtpt[c * (nseg + 1) + nseg] = runt;
+}
+
 }  // namespace
+
+void launch_mtile_split(const int* vcount, int n, int nseg, int* mtp, int* mtp_tail, int* rbase, cudaStream_t s) {
+  if (n <= 0) return;
+  launch_k(mtile_split_kernel, dim3((n + 63) / 64), dim3(64), 0, s, vcount, n, nseg, mtp, mtp_tail, rbase);
+  LINA_LAUNCH_CHECK();
+}
 
 void launch_mtile_prefix(const int* vcount, int n, int nseg, int rows, int* mtp, cudaStream_t s) {
   if (n <= 0) return;

@@ -52,6 +52,10 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
     p.tile_rows = per_seg <= 96 ? 128 : 256;
     const char* tr = getenv("LINA_TILE_ROWS");
     if (tr && (atoi(tr) == 128 || atoi(tr) == 256)) p.tile_rows = atoi(tr);
+    // tail split of the 256-row tiles (RowGemm::mtp_tail): tensor-core path only;
+    // LINA_TAIL128=0 turns it off (A/B)
+    const char* ts = getenv("LINA_TAIL128");
+    p.tail_split = p.bf16 && p.tile_rows == 256 && !(ts && ts[0] == '0') && !getenv("LINA_FORCE_SIMT");
   }
   const size_t T = p.T, k = p.k, E = p.E;
   size_t o = 0;
@@ -77,7 +81,7 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
         (long long)(p.P / pack) * std::min((long long)p.T * std::min(p.k, p.El), (long long)p.C * p.El);
     p.V = (int)(rows / R + (long long)p.E + 1);
     const size_t vrows = (size_t)p.V * R, srows = (size_t)p.T * p.k;
-    const size_t tab_ints = 2 * E + (size_t)p.P * E + p.P + 4 * (size_t)p.V + (p.V + 1) + 2 * (size_t)p.El;
+    const size_t tab_ints = 2 * E + (size_t)p.P * E + p.P + 4 * (size_t)p.V + 2 * (size_t)(p.V + 1) + 2 * (size_t)p.El;
     // peer-visible regions first (T-independent offsets are not possible here: the
     // source-compact buffers hold T·k rows, so dropless needs equal T on every rank)
     p.s_R = take(vrows * p.d * p.dt);                                    // [peer-written]
@@ -129,6 +133,8 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
   p.s_tokof = take(4 * E * (size_t)p.C);
   p.s_vcount = take(4 * (size_t)p.n * p.P * p.El);
   p.s_mtp = take(4 * (size_t)p.n * (p.P * p.El + 1));
+  p.s_mtpt = take(4 * (size_t)p.n * (p.P * p.El + 1));
+  p.s_rbase = take(4 * (size_t)p.n * p.P * p.El);
   p.s_H = take(recv_rows * (size_t)p.f * p.dt);               // relu(X W1ᵀ)
   p.s_mask = take(recv_rows * (size_t)((p.f + 63) / 64) * 8);  // ReLU' bits of H
   p.saved_bytes = o;
@@ -160,7 +166,7 @@ namespace {
 
 struct Ptrs {
   float* probs; int* idx; float* gate; int* slot; int* kept; int* tok_of; int* recv_kept;
-  int* vcount; int* mtp; char* R; char* H; char* Cb; uint64_t* mask;
+  int* vcount; int* mtp; int* mtpt; int* rbase; char* R; char* H; char* Cb; uint64_t* mask;
   int* route; char* D; char* O; float* dg; float* dwg; char* dS; char* dO; char* dH;
   char* dXe; char* dXs;
   int* allc;    // dropless: [P][E] exchanged counts
@@ -194,7 +200,8 @@ Ptrs carve_dropless(const Plan& p, void* saved, void* ws) {
     q.dl.vsrc = q.dl.vexp + V;
     q.dl.vq0 = q.dl.vsrc + V;
     q.dl.mtp = q.dl.vq0 + V;
-    q.dl.vrange = q.dl.mtp + V + 1;
+    q.dl.mtpt = q.dl.mtp + V + 1;
+    q.dl.vrange = q.dl.mtpt + V + 1;
     q.vcount = q.dl.vcount;
     q.mtp = q.dl.mtp;
   }
@@ -226,6 +233,8 @@ Ptrs carve(const Plan& p, void* saved, void* ws) {
     q.recv_kept = (int*)(sv + p.s_recvkept);
     q.vcount = (int*)(sv + p.s_vcount);
     q.mtp = (int*)(sv + p.s_mtp);
+    q.mtpt = (int*)(sv + p.s_mtpt);
+    q.rbase = (int*)(sv + p.s_rbase);
     q.R = sv + p.s_R;
     q.H = sv + p.s_H;
     q.Cb = sv + p.s_C;
@@ -263,6 +272,19 @@ void a2a_recv_to_send(const Plan& p, const char* recv, char* send, int w, int c,
   a2a_send_to_recv(p, recv, send, w, c, comm, st);
 }
 
+// The tail-split tile lists of chunk c (laid out after the main prefix in `saved`: mtp,
+// then mtp_tail [n][nseg+1], then row_base [n][nseg]).
+void set_tail(const Plan& p, RowGemm& g, const int* mtp, int c) {
+  if (!p.tail_split || p.dropless) return;
+  const size_t nseg = (size_t)p.P * p.El;
+  g.mtp_tail = mtp + (p.s_mtpt - p.s_mtp) / 4 + (size_t)c * (nseg + 1);
+  g.row_base = mtp + (p.s_rbase - p.s_mtp) / 4;  // [n][nseg]: indexed by the global segment
+}
+// After vcount (and the plain prefix) of every chunk: the tail-split lists.
+void tile_lists(const Plan& p, const Ptrs& q, cudaStream_t s) {
+  if (p.tail_split && !p.dropless) launch_mtile_split(q.vcount, p.n, p.P * p.El, q.mtp, q.mtpt, q.rbase, s);
+}
+
 void row_gemm(const Plan& p, const void* A, const void* B, void* D, const void* aux,
               const int* vcount, const int* mtp, int c, int N, int K, bool b_kmajor, int epi,
               cudaStream_t st, uint64_t* mask_out = nullptr, const uint64_t* mask_in = nullptr,
@@ -284,6 +306,7 @@ void row_gemm(const Plan& p, const void* A, const void* B, void* D, const void* 
   g.Cm = p.Cm;
   g.N = N;
   g.K = K;
+  set_tail(p, g, mtp, c);
   launch_expert_row_gemm(p.bf16 ? 1 : 0, g, b_kmajor, epi, st);
 }
 
@@ -324,6 +347,7 @@ void forward_ce(lina_comm* cm, const Plan& p, const Ptrs& q, const void* w1, con
   if (compute) {
     launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
     launch_mtile_prefix(q.vcount, n, P * p.El, p.tile_rows, q.mtp, s);
+    tile_lists(p, q, s);
   }
   for (int r = 0; r < P; ++r)  // every peer has pulled my previous O
     if (r != me) ce.wait_flag(s, CeTransport::kPulledFwdC, r, 0, ce.prev_ce_fwd);
@@ -510,6 +534,7 @@ RowGemm peer_gemm(const Plan& p, const void* A, const void* B, void* D, const in
   g.Cm = p.Cm;
   g.N = N;
   g.K = K;
+  set_tail(p, g, mtp, c);
   return g;
 }
 
@@ -572,6 +597,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
     if (c == 0) {
       launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
       launch_mtile_prefix(q.vcount, n, P * p.El, p.tile_rows, q.mtp, s);
+      tile_lists(p, q, s);
       trace_mark(cm, s, "vcount");
       prof_begin(cm, s);
     }
@@ -749,6 +775,7 @@ RowGemm dl_gemm(const Plan& p, const Ptrs& q, const void* A, const void* B, void
   g.Cm = p.tile_rows;
   g.N = N;
   g.K = K;
+  if (p.tail_split) g.mtp_tail = q.dl.mtpt;  // segments of <= 128 rows as single-CTA tiles (row base 0)
   return g;
 }
 
@@ -781,7 +808,7 @@ void forward_dropless(lina_comm* cm, const Plan& p, const Ptrs& q, const void* t
     launch_sig_wait(make_sig(cm, CT::kFCountFwd, rf, 1, -1, nullptr, 0), s);
     allc = q.allc;
   }
-  launch_dl_layout(allc, P, E, El, p.pack, me, R, p.V, q.dl, s);
+  launch_dl_layout(allc, P, E, El, p.pack, me, R, p.V, p.tail_split ? 1 : 0, q.dl, s);
   trace_mark(cm, s, "dl gate+route+layout");
   if (peer) {
     void* const* peer_R = ce->dev_ptrs(saved, p.s_R, s, p.peer_key);
@@ -971,6 +998,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   launch_route(q.idx, p.T, p.k, p.E, p.C, q.route, q.slot, route ? route->counts : nullptr,
                q.kept, q.tok_of, s, cm->route_sync, p.n, p.P == 1 ? q.vcount : nullptr,
                p.P == 1 ? q.mtp : nullptr, p.tile_rows);
+  if (p.P == 1) tile_lists(p, q, s);
   launch_permute(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, p.n, p.Cm, q.D, s);
   if (route) {
     if (route->idx && !override_r)
@@ -1034,6 +1062,7 @@ void moe_forward(lina_comm* cm, const Plan& p, const void* tokens, const float* 
   LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_cnt, 0));
   launch_vcount(q.recv_kept, p.P, p.El, p.C, n, q.vcount, s);
   launch_mtile_prefix(q.vcount, n, p.P * p.El, p.tile_rows, q.mtp, s);
+  tile_lists(p, q, s);
   for (int c = 0; c < n; ++c) {
     LINA_CUDA_CHECK(cudaStreamWaitEvent(s, e_disp[c], 0));
     prof_begin(cm, s);
