@@ -207,7 +207,7 @@ class Scheduler {
           // all-to-all before it runs (later phases sit behind the wait on the device),
           // so it is issued now and `lo` waits for its gradient on the device — no host
           // polling latency between the gradient and its allreduce.
-          can_issue = j.a2a_limit != ~0ull && !busy;
+          can_issue = early_issue_ && j.a2a_limit != ~0ull && !busy;
         } else if (busy) {
           can_issue = false;
           ++deferred_;
@@ -253,6 +253,13 @@ class Scheduler {
   bool imminent_ = false, stop_ = false;
   int outstanding_ = 0;
   uint32_t wait_target_ = 0;
+  // LINA_SCHED_EARLY=1: issue a job ahead of a wait point before its gradient is ready (see
+  // run()); off by default — the 2-GPU scheduler test hung with it on (round 2), cause not
+  // yet understood
+  const bool early_issue_ = [] {
+    const char* e = getenv("LINA_SCHED_EARLY");
+    return e && e[0] == '1';
+  }();
   uint32_t* done_flag_ = nullptr;  // device word: the last wait point published on `lo`
   StreamValueFn wait_fn_ = nullptr, write_fn_ = nullptr;
   int64_t issued_ = 0, deferred_ = 0;
