@@ -410,33 +410,38 @@ def main():
     # the same steps — full (T_pass, the pipelining efficiency's windows), compute-only
     # (collectives skipped: T_rest + T_ffn, with T_ffn = the expert-GEMM phases) and
     # collectives-only (the fused transport's 2n micro-ops per pass alone: T_a2a(n)).
-    # Medians over the K steps.
+    # Medians over the K steps; the three kinds are interleaved step by step (full, compute-only,
+    # collectives-only, full, ...) so that clock changes under the power cap hit all three alike
+    # (three back-to-back blocks of K steps disagreed by more than the exposed time at C5).
     def h_of(lay, nch):
-        def passes(flags):
-            lina.lina_profile_enable(comm, flags)
-            barrier()
-            torch.cuda.synchronize()
-            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                  for _ in range(args.steps)]
-            for i in range(args.steps):
+        lay.forward(x, wg, w1, w2, out=outs["y"])  # routing in `saved` for the movers-only pass
+        kinds = (1, 1 | 2, 4)
+        got = {f: [] for f in kinds}
+        for i in range(args.steps):
+            for flags in kinds:
+                lina.lina_profile_enable(comm, flags)
+                barrier()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 flush.zero_()
-                ev[i][0].record(stream)
+                e0.record(stream)
                 lay.forward(x, wg, w1, w2, out=outs["y"])
                 lay.backward(dy, x, wg, w1, w2, outs["dx"], outs["dwg"], outs["dw1"], outs["dw2"])
-                ev[i][1].record(stream)
-            torch.cuda.synchronize()
-            barrier()
-            lina.lina_profile_enable(comm, 0)
-            pr = lina.lina_profile_read(comm)
-            med = float(np.median([a.elapsed_time(b) for a, b in ev]))
-            v = torch.tensor([med, pr["gemm_ms"] / args.steps, pr["a2a_window_ms"] / args.steps,
-                              pr["gemm_in_a2a_ms"] / args.steps], dtype=torch.float64, device=dev)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                lina.lina_profile_enable(comm, 0)
+                pr = lina.lina_profile_read(comm)
+                got[flags].append((e0.elapsed_time(e1), pr["gemm_ms"], pr["a2a_window_ms"], pr["gemm_in_a2a_ms"]))
+        barrier()
+
+        def med(flags):
+            v = torch.tensor(np.median(np.array(got[flags], dtype=np.float64), axis=0), dtype=torch.float64,
+                             device=dev)
             torch.distributed.all_reduce(v, op=torch.distributed.ReduceOp.MAX)
             return [float(t) for t in v]
-        lay.forward(x, wg, w1, w2, out=outs["y"])  # routing in `saved` for the movers-only pass
-        t_pass, _, win, busy = passes(1)
-        t_comp, t_ffn, _, _ = passes(1 | 2)
-        t_a2a = passes(4)[0]
+        t_pass, _, win, busy = med(1)
+        t_comp, t_ffn, _, _ = med(1 | 2)
+        t_a2a = med(4)[0]
         lay.forward(x, wg, w1, w2, out=outs["y"])  # (restore real routing / rounds)
         lay.backward(dy, x, wg, w1, w2, outs["dx"], outs["dwg"], outs["dw1"], outs["dw2"])
         torch.cuda.synchronize()

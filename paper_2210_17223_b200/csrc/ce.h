@@ -19,7 +19,9 @@ class CeTransport {
          // inference exchange by peer stores (infer.cpp)
          kIFreeD = 14, kIReadyD = 15, kIFreeC = 16, kIReadyC = 17,
          // dropless training: the per-expert counts of a forward have landed
-         kFCountFwd = 18, kKinds = 19 };
+         kFCountFwd = 18,
+         // split dispatch (n = 1): a forward's per-expert counts have landed (before the rows)
+         kFCountFwdS = 19, kKinds = 20 };
   static constexpr int kMaxChunks = 32;
 
   explicit CeTransport(lina_comm* cm);  // collective (allgathers the flag-array handles)
@@ -50,7 +52,7 @@ class CeTransport {
   uint32_t* round_fwd() const { return rounds_; }
   uint32_t* round_bwd() const { return rounds_ + 1; }
   uint32_t* round_inf() const { return rounds_ + 2; }
-  static constexpr int kDoneSites = 16;
+  static constexpr int kDoneSites = 32;  // 16..23 / 24..31: split dispatch, per owner block
   cudaStream_t disp_stream(int peer) const { return disp_[peer]; }
   cudaStream_t comb_stream(int peer) const { return comb_[peer]; }
   // event pool: [which (0..3)][peer][chunk or kMaxChunks(+1)]

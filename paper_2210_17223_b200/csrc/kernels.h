@@ -33,6 +33,10 @@ struct RowGemm {
   // a 129th..256th row costs a full 256-row MMA, a <= 128-row tail only half of one
   const int* mtp_tail = nullptr;
   const int* row_base = nullptr;
+  // split dispatch (tcgen05, n = 1): sig.wait is per source — the TMA producer waits for
+  // source s's slot before its first A load of a segment of s, and tiles are walked from
+  // source src_me upwards (the order the sources' rows arrive in, permute.cu)
+  int src_wait = 0, src_P = 1, src_me = 0;
 };
 
 // Weight-gradient GEMM: D[El][M][N] = Σ_{c,s} Σ_{r < v} A[seg][r][:]ᵀ B[seg][r][:].
@@ -140,6 +144,20 @@ void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const 
                              const float* gate, int T, int k, int d, int E, int C, int c0, int nc, int Cm, int El,
                              int P, int me, void* const* peer_rows, float* dg, const PeerSignal& sig,
                              cudaStream_t s);
+// Split dispatch (n = 1; permute.cu split_rows_kernel): the owner blocks j0 .. j0+nj-1 in
+// the order owner(j) = (me - j) mod P (j = 0: this rank's own block), grid CTAs (0 = one
+// pass), the last CTA done with block j > 0 posts sig's READY to owner(j) (done[j] = its
+// zeroed counter); sig.wait (if set) is awaited by every CTA first.  The combine-backward
+// variant also writes dg of its rows (dg zeroed by the caller).
+void launch_dispatch_counts(const int* kept, int P, int El, int me, void* const* peer_counts,
+                            const PeerSignal& free_sig, const PeerSignal& count_sig, cudaStream_t s);
+void launch_permute_split(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d, int E, int C,
+                          int Cm, int El, int P, int me, void* const* peer_rows, int j0, int nj, int grid,
+                          const PeerSignal& sig, unsigned int* done, cudaStream_t s);
+void launch_combine_bwd_split(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
+                              const float* gate, int k, int d, int E, int C, int Cm, int El, int P, int me,
+                              void* const* peer_rows, float* dg, int j0, int nj, int grid, const PeerSignal& sig,
+                              unsigned int* done, cudaStream_t s);
 // Collectives-only timing (movers.cu): the valid rows of micro-op c's segments of a
 // receive-layout buffer to each owner's send-layout buffer (peer_send_layout[s]), as the
 // peer-storing GEMM epilogue moves them; the last CTA posts sig (READY of micro-op c).

@@ -66,32 +66,38 @@ __device__ __forceinline__ float token_dot_dp(const float* __restrict__ probs, c
   return dot;
 }
 
+// one thread per (token, 8 padded experts): the token's <p, dp> once, three 16-byte stores
 __global__ void __launch_bounds__(256) dl_split_kernel(const float* __restrict__ probs, const int* __restrict__ idx,
                                                        const float* __restrict__ gate, const float* __restrict__ dg,
                                                        int T, int E, int k, __nv_bfloat16* __restrict__ dls) {
   pdl_enter();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (long long)T * kEP) return;
-  const int t = (int)(i / kEP), e = (int)(i % kEP);
-  float dl = 0.f;
-  if (e < E) {
-    int es[8];
-    float dps[8];
-    const float dot = token_dot_dp<8>(probs, idx, gate, dg, t, k, E, es, dps);
-    float dp = 0.f;
+  if (i >= (long long)T * (kEP / 8)) return;
+  const int t = (int)(i / (kEP / 8)), e0 = (int)(i % (kEP / 8)) * 8;
+  int es[8];
+  float dps[8];
+  const float dot = token_dot_dp<8>(probs, idx, gate, dg, t, k, E, es, dps);
+  __align__(16) __nv_bfloat16 h[8], m[8], l[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (es[j] == e) dp = dps[j];
-    dl = probs[(size_t)t * E + e] * (dp - dot);
+  for (int u = 0; u < 8; ++u) {
+    const int e = e0 + u;
+    float dl = 0.f;
+    if (e < E) {
+      float dp = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (es[j] == e) dp = dps[j];
+      dl = probs[(size_t)t * E + e] * (dp - dot);
+    }
+    h[u] = __float2bfloat16_rn(dl);
+    const float r1 = dl - __bfloat162float(h[u]);
+    m[u] = __float2bfloat16_rn(r1);
+    l[u] = __float2bfloat16_rn(r1 - __bfloat162float(m[u]));
   }
-  const __nv_bfloat16 hi = __float2bfloat16_rn(dl);
-  const float r1 = dl - __bfloat162float(hi);
-  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-  const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-  const size_t plane = (size_t)T * kEP;
-  dls[i] = hi;
-  dls[plane + i] = mid;
-  dls[2 * plane + i] = lo;
+  const size_t plane = (size_t)T * kEP, o = (size_t)t * kEP + e0;
+  *reinterpret_cast<uint4*>(dls + o) = *reinterpret_cast<const uint4*>(h);
+  *reinterpret_cast<uint4*>(dls + plane + o) = *reinterpret_cast<const uint4*>(m);
+  *reinterpret_cast<uint4*>(dls + 2 * plane + o) = *reinterpret_cast<const uint4*>(l);
 }
 
 // WgS [3][d][64]: the terms of Wg[c][e] as rows c (K-major B of the dX contraction)
@@ -111,13 +117,22 @@ __global__ void wgt_split_kernel(const float* __restrict__ Wg, int d, int E, __n
   ws[2 * plane + i] = lo;
 }
 
-// ---- dX: CTA = 128 tokens x 256 columns; K = 64 (padded experts) x 3 term pairs
+// ---- dX: a persistent grid; CTA c owns the 256-column block c % nblk of dX (its Wg terms,
+// 64 KB, loaded once) and walks the 128-token blocks c / nblk, + G / nblk, ...  Warp 0: TMA
+// of the dL terms (3-stage ring); warp 1: 12 MMAs per token block (K = 64 padded experts x
+// 3 term pairs) into one of two TMEM accumulators; warps 2..9: the epilogue (thread = token
+// row, warps w and w + 4 split the 256 columns), which adds the k returned expert rows and
+// stores bf16 dX while the tensor cores work on the next token block — the kernel is bound
+// by the epilogue's HBM traffic (read k·d, write d elements per token).
 constexpr int kDxA = 128 * kEP * 2;  // 16 KB per dL term
 constexpr int kDxB = 256 * kEP * 2;  // 32 KB per Wg term
-constexpr int kDxSmem = 2 * kDxA + 2 * kDxB + 1024 + 256;
+constexpr int kDxStages = 3;
+constexpr int kDxEpw = 8;
+constexpr int kDxThreads = 64 + 32 * kDxEpw;
+constexpr int kDxSmem = 2 * kDxB + kDxStages * 2 * kDxA + 1024 + 256;
 
 template <int KM>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kDxThreads, 1)
     dx_tc_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmW,
                  const __nv_bfloat16* __restrict__ dXe, const int* __restrict__ idx, const int* __restrict__ slot,
                  int T, int k, int d, int E, int C, int n, int Cm, const int* __restrict__ ebase,
@@ -125,97 +140,158 @@ __global__ void __launch_bounds__(192, 1)
   pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + 2 * kDxA + 2 * kDxB);
-  uint64_t* tfull = full + 1;
-  uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+  uint8_t* sw = smem;                 // Wg hi | Wg mid (resident)
+  uint8_t* sl = smem + 2 * kDxB;      // [stage] dL hi | dL mid
+  uint64_t* wfull = (uint64_t*)(sl + kDxStages * 2 * kDxA);
+  uint64_t* full = wfull + 1;
+  uint64_t* empty = full + kDxStages;
+  uint64_t* tfull = empty + kDxStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = blockIdx.x * 128, n0 = blockIdx.y * 256;
+  const int nblk = d / 256;
+  const int per = gridDim.x / nblk;  // CTAs per column block (the launcher sizes the grid so)
+  const int n0 = (blockIdx.x % nblk) * 256;
+  const int tb0 = blockIdx.x / nblk;
+  const int ntb = (T + 127) / 128;
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmL);
     prefetch_tmap(&tmW);
-    mbar_init(full, 1);
-    mbar_init(tfull, 1);
+    mbar_init(wfull, 1);
+    for (int i = 0; i < kDxStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kDxEpw);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc<1>(tmem_slot, 256);
+  if (warp == 1) tmem_alloc<1>(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(full, 2 * kDxA + 2 * kDxB);
-      tma_load_3d<1>(smem, &tmL, full, 0, t0, 0);                          // dL hi
-      tma_load_3d<1>(smem + kDxA, &tmL, full, 0, t0, 1);                   // dL mid
-      tma_load_3d<1>(smem + 2 * kDxA, &tmW, full, 0, n0, 0);               // Wg hi
-      tma_load_3d<1>(smem + 2 * kDxA + kDxB, &tmW, full, 0, n0, 1);        // Wg mid
+      mbar_expect_tx(wfull, 2 * kDxB);
+      tma_load_3d<1>(sw, &tmW, wfull, 0, n0, 0);          // Wg hi
+      tma_load_3d<1>(sw + kDxB, &tmW, wfull, 0, n0, 1);   // Wg mid
+      int st = 0;
+      uint32_t ph = 0;
+      for (int tb = tb0; tb < ntb; tb += per) {
+        mbar_wait(&empty[st], ph ^ 1);
+        uint8_t* dst = sl + st * 2 * kDxA;
+        mbar_expect_tx(&full[st], 2 * kDxA);
+        tma_load_3d<1>(dst, &tmL, &full[st], 0, tb * 128, 0);          // dL hi
+        tma_load_3d<1>(dst + kDxA, &tmL, &full[st], 0, tb * 128, 1);   // dL mid
+        if (++st == kDxStages) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(128, 256, false, false);
-      mbar_wait(full, 0);
-      tc_fence_after();
-      const uint32_t la = smem_u32(smem), lm = la + kDxA, wa = la + 2 * kDxA, wm = wa + kDxB;
+      mbar_wait(wfull, 0);
+      const uint32_t wa = smem_u32(sw), wm = wa + kDxB;
+      int st = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int tb = tb0; tb < ntb; tb += per) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        mbar_wait(&full[st], ph);
+        tc_fence_after();
+        const uint32_t la = smem_u32(sl + st * 2 * kDxA), lm = la + kDxA;
+        const uint32_t dt = tmem + acc * 256;
 #pragma unroll
-      for (int kk = 0; kk < kEP / 16; ++kk) {
-        mma_bf16<1>(tmem, sdesc(la + kk * 32, 16, 1024), sdesc(wa + kk * 32, 16, 1024), idesc, kk ? 1u : 0u);
-        mma_bf16<1>(tmem, sdesc(la + kk * 32, 16, 1024), sdesc(wm + kk * 32, 16, 1024), idesc, 1u);
-        mma_bf16<1>(tmem, sdesc(lm + kk * 32, 16, 1024), sdesc(wa + kk * 32, 16, 1024), idesc, 1u);
+        for (int kk = 0; kk < kEP / 16; ++kk) {
+          mma_bf16<1>(dt, sdesc(la + kk * 32, 16, 1024), sdesc(wa + kk * 32, 16, 1024), idesc, kk ? 1u : 0u);
+          mma_bf16<1>(dt, sdesc(la + kk * 32, 16, 1024), sdesc(wm + kk * 32, 16, 1024), idesc, 1u);
+          mma_bf16<1>(dt, sdesc(lm + kk * 32, 16, 1024), sdesc(wa + kk * 32, 16, 1024), idesc, 1u);
+        }
+        mma_commit<1>(&empty[st]);
+        mma_commit<1>(&tfull[acc]);
+        if (++st == kDxStages) {
+          st = 0;
+          ph ^= 1;
+        }
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
       }
-      mma_commit<1>(tfull);
     }
   } else {  // epilogue: thread = token row; + the k returned expert input-gradient rows
+    const int ew = warp - 2;
     const int quarter = warp & 3;
-    const int t = t0 + quarter * 32 + lane;
-    if (lane == 0) sig_wait(sig);  // fused transport: the returned rows have landed
+    const int c0 = (ew >> 2) * 128;  // this warp's 128 of the block's 256 columns
+    if (lane == 0) sig_wait(sig);    // fused transport: the returned rows have landed
     __syncwarp();
-    size_t rows[KM];
-#pragma unroll
-    for (int j = 0; j < KM; ++j) {
-      rows[j] = ~(size_t)0;
-      if (t < T && j < k) {
-        const int s = slot[(size_t)t * k + j];
-        const int e = idx[(size_t)t * k + j];
-        if (s >= 0) rows[j] = ebase ? (size_t)(ebase[e] + s) : send_row(e, s, E, C, n, Cm);
-      }
-    }
-    // the k rows' 32-column slices of the next block are loaded before the current block is
-    // summed (two blocks in flight per thread; KM = 2 only — KM = 8 would spill)
+    // the k rows' 32-column slices of the next chunk are loaded before the current chunk is
+    // summed (two chunks in flight per thread; KM = 2 only — KM = 8 would spill)
     constexpr bool PREF = KM <= 2;
-    uint4 g[PREF ? 2 : 1][KM][4];
-    auto load_rows = [&](int cb, uint4 (&dst)[KM][4]) {
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int tb = tb0; tb < ntb; tb += per) {
+      const int t = tb * 128 + quarter * 32 + lane;
+      size_t rows[KM];
 #pragma unroll
-      for (int j = 0; j < KM; ++j)
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-          dst[j][v] = rows[j] != ~(size_t)0 ? *reinterpret_cast<const uint4*>(dXe + rows[j] * d + n0 + cb + 8 * v)
-                                            : make_uint4(0, 0, 0, 0);
-    };
-    load_rows(0, g[0]);
-    mbar_wait(tfull, 0);
-    tc_fence_after();
-    const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int cb = 32 * i;
-      float acc[32];
-      tmem_ld32(ta + cb, *reinterpret_cast<uint32_t(*)[32]>(acc));
-      if (PREF && i + 1 < 8) load_rows(cb + 32, g[(i + 1) & 1]);
-      if (!PREF && i > 0) load_rows(cb, g[0]);
-      uint4 (&cur)[KM][4] = g[PREF ? (i & 1) : 0];
-      tmem_wait_ld();
-      if (t < T) {
+      for (int j = 0; j < KM; ++j) {
+        rows[j] = ~(size_t)0;
+        if (t < T && j < k) {
+          const int s = slot[(size_t)t * k + j];
+          const int e = idx[(size_t)t * k + j];
+          if (s >= 0) rows[j] = ebase ? (size_t)(ebase[e] + s) : send_row(e, s, E, C, n, Cm);
+        }
+      }
+      uint4 g[PREF ? 2 : 1][KM][4];
+      auto load_rows = [&](int cb, uint4 (&dst)[KM][4]) {
 #pragma unroll
         for (int j = 0; j < KM; ++j)
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            float x[8];
-            load16(&cur[j][v], x, (const __nv_bfloat16*)nullptr);
+          for (int v = 0; v < 4; ++v)
+            dst[j][v] = rows[j] != ~(size_t)0
+                            ? *reinterpret_cast<const uint4*>(dXe + rows[j] * d + n0 + cb + 8 * v)
+                            : make_uint4(0, 0, 0, 0);
+      };
+      load_rows(c0, g[0]);
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + acc * 256;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc[8 * v + u] += x[u];
-          }
+      for (int i = 0; i < 4; ++i) {
+        const int cb = c0 + 32 * i;
+        float a[32];
+        tmem_ld32(ta + cb, *reinterpret_cast<uint32_t(*)[32]>(a));
+        if (PREF && i + 1 < 4) load_rows(cb + 32, g[(i + 1) & 1]);
+        if (!PREF && i > 0) load_rows(cb, g[0]);
+        uint4 (&cur)[KM][4] = g[PREF ? (i & 1) : 0];
+        tmem_wait_ld();
+        if (i == 3) {  // the accumulator is read: the MMA warp may reuse it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
+        }
+        if (t < T) {
 #pragma unroll
-        for (int v = 0; v < 4; ++v) store16(dX + (size_t)t * d + n0 + cb + 8 * v, acc + 8 * v, (__nv_bfloat16*)nullptr);
+          for (int j = 0; j < KM; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              float x[8];
+              load16(&cur[j][v], x, (const __nv_bfloat16*)nullptr);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) a[8 * v + u] += x[u];
+            }
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            store16(dX + (size_t)t * d + n0 + cb + 8 * v, a + 8 * v, (__nv_bfloat16*)nullptr);
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
       }
     }
   }
@@ -223,7 +299,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<1>(tmem, 256);
+    tmem_dealloc<1>(tmem, 512);
   }
   if (sig.bump && threadIdx.x == 0) sig_bump_last(sig);  // the backward's last kernel closes its round
 }
@@ -332,10 +408,19 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// Token splits of dWg: one wave of (d / 128) x S CTAs (one per SM: 160 KB of shared memory
+// each) — 2 x 148 / (d / 128) splits ran 2.05 waves at C5 (a third wave of 8 CTAs).
 int dwg_tc_splits(int T, int d) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+  }
   const int mt = std::max(1, d / 128);
   const int kbs = std::max(1, (T + 63) / 64);
-  return std::max(1, std::min(kbs, (2 * 148 + mt - 1) / mt));
+  return std::max(1, std::min(kbs, sms / mt));
 }
 
 size_t al256(size_t b) { return (b + 255) / 256 * 256; }
@@ -362,8 +447,8 @@ void launch_dwg_tc(const void* X, const float* probs, const int* idx, const floa
   char* sc = (char*)scratch;
   float* part = (float*)sc;
   __nv_bfloat16* dls = (__nv_bfloat16*)(sc + al256(sizeof(float) * (size_t)S * d * E));
-  launch_k(dl_split_kernel, dim3((unsigned)(((long long)T * kEP + 255) / 256)), dim3(256), 0, s, probs, idx, gate, dg,
-           T, E, k, dls);
+  launch_k(dl_split_kernel, dim3((unsigned)std::max(1LL, ((long long)T * (kEP / 8) + 255) / 256)), dim3(256), 0, s,
+           probs, idx, gate, dg, T, E, k, dls);
   LINA_LAUNCH_CHECK();
   const uint64_t xd[2] = {(uint64_t)d, (uint64_t)T};
   const uint64_t xs[1] = {(uint64_t)d * 2};
@@ -407,13 +492,19 @@ void launch_dx_tc(const void* dXe, const int* idx, const int* slot, const float*
     LINA_CUDA_CHECK(cudaFuncSetAttribute(dx_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDxSmem));
     attr = true;
   }
-  const dim3 grid(std::max(1, (T + 127) / 128), d / 256);
+  // persistent: a multiple of the column blocks, at most one CTA per SM and per tile
+  int dev = 0, sms = 148;
+  LINA_CUDA_CHECK(cudaGetDevice(&dev));
+  LINA_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int nblk = d / 256, ntb = std::max(1, (T + 127) / 128);
+  const int per = std::max(1, std::min(sms / nblk, ntb));
+  const dim3 grid(per * nblk);
   if (k <= 2)
-    launch_k(dx_tc_kernel<2>, grid, dim3(192), kDxSmem, s, ml, mw, (const __nv_bfloat16*)dXe, idx, slot, T, k, d, E,
-             C, n, Cm, ebase, (__nv_bfloat16*)dX, sig);
+    launch_k(dx_tc_kernel<2>, grid, dim3(kDxThreads), kDxSmem, s, ml, mw, (const __nv_bfloat16*)dXe, idx, slot, T, k,
+             d, E, C, n, Cm, ebase, (__nv_bfloat16*)dX, sig);
   else
-    launch_k(dx_tc_kernel<8>, grid, dim3(192), kDxSmem, s, ml, mw, (const __nv_bfloat16*)dXe, idx, slot, T, k, d, E,
-             C, n, Cm, ebase, (__nv_bfloat16*)dX, sig);
+    launch_k(dx_tc_kernel<8>, grid, dim3(kDxThreads), kDxSmem, s, ml, mw, (const __nv_bfloat16*)dXe, idx, slot, T, k,
+             d, E, C, n, Cm, ebase, (__nv_bfloat16*)dX, sig);
   LINA_LAUNCH_CHECK();
 }
 

@@ -16,7 +16,7 @@
 // order — exact for the grid inputs of DESIGN.md §4.
 //
 // One CTA per 128 tokens, warp-specialised: warp 0 = TMA producer (X tile 128 x 64 and the
-// three Ws slabs EP x 64, 128B-swizzled, 4-stage ring), warp 1 = TMEM allocator + MMA
+// three Ws slabs EP x 64, 128B-swizzled, 2-stage ring, two CTAs per SM), warp 1 = TMEM allocator + MMA
 // issuer, warps 2..5 = epilogue: tcgen05.ld puts one token's EP logits in one thread's
 // registers, which computes the softmax, the top-k and the gate weights without any
 // shuffle and stores its probabilities row (16-byte stores).  X is read once: the kernel
@@ -40,7 +40,9 @@ namespace {
 using namespace tc;
 
 constexpr int kGBK = 64;       // K per stage: 128-byte rows, one swizzle atom wide
-constexpr int kGStages = 4;
+// 2 stages (<= 81 KB of shared memory): two CTAs per SM, so C5's 256 token blocks run in one
+// wave (4 stages, one CTA per SM: 1.73 waves) and one CTA's epilogue overlaps the other's loads
+constexpr int kGStages = 2;
 constexpr int kGThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
 
 template <int EP>
@@ -69,7 +71,7 @@ __global__ void gate_split_kernel(const float* __restrict__ Wg, int d, int E, in
 }
 
 template <int EP>
-__global__ void __launch_bounds__(kGThreads, 1)
+__global__ void __launch_bounds__(kGThreads, 2)
     gate_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, int T, int d,
                    int E, int k, int write_routing, float* __restrict__ probs, int* __restrict__ idx,
                    float* __restrict__ gate, PeerSignal sig) {

@@ -86,6 +86,7 @@ struct TcParams {
   uint64_t* mask_out;       // ROW + ReLU: ReLU' bits of the stored output, [seg][N/64][Cm]
   const uint64_t* mask_in;  // ROW + mask epilogue: the bits written by GEMM1
   PeerSignal sig;           // fused transport: wait before the first A load / post after the last store
+  int src_wait;             // ROW: sig.wait per source (segment (c, s, el) waits for s only), tiles from dme up
   CUtensorMap pmaps[kMaxPeerMaps];  // kernel-parameter copies (the TMA unit reads them like tmD)
   char* pbase[kMaxPeerMaps];        // the same buffers as plain pointers (remote owners: SM stores)
 };
@@ -146,7 +147,11 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
 
   // Fused combine stores: every rank starts at the tiles of source (me + 1) % P, so at any
   // moment the P ranks write to P different owners (no incast on one rank's links).
-  const int rot = (!WGRAD && p.has_pmaps && p.dP > 1) ? p.mtp[((p.dme + 1) % p.dP) * p.El] * n_nblk : 0;
+  // Split dispatch (src_wait): start at this rank's own source, whose rows are local, then
+  // me + 1, me + 2, ... — the order the peers' rows arrive in (permute.cu split_rows_kernel).
+  const int rot = (!WGRAD && p.has_pmaps && p.dP > 1) ? p.mtp[((p.dme + 1) % p.dP) * p.El] * n_nblk
+                  : (!WGRAD && p.src_wait && p.dP > 1) ? p.mtp[p.dme * p.El] * n_nblk
+                                                       : 0;
   auto decode = [&](int t0, int& seg_or_el, int& m0, int& n0) {
     int t = t0 + rot;
     if (t >= total_tiles) t -= total_tiles;
@@ -186,10 +191,11 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
   if (warp == 0) {
     // ================= TMA producer (both CTAs load their own halves)
     if (lane == 0) {
-      if (p.sig.wait) {  // fused transport: the peers' rows of A have landed
+      if (p.sig.wait && !p.src_wait) {  // fused transport: the peers' rows of A have landed
         sig_wait(p.sig);
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
+      uint32_t have = 1u << p.dme;  // split dispatch: sources whose rows are known to be in
       int stage = 0;
       uint32_t ph = 0;
       const int arow = 128 * rank;          // this CTA's rows within the tile
@@ -226,6 +232,14 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
         };
         if (!WGRAD) {
           const int seg = p.seg0 + se;
+          if (p.src_wait) {
+            const int src = (seg / p.El) % p.dP;
+            if (!((have >> src) & 1u)) {
+              sig_wait_one(p.sig, src);
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              have |= 1u << src;
+            }
+          }
           const int el = p.seg_expert ? p.seg_expert[se % p.El] : se % p.El;
           for (int kb = 0; kb < p.K / BK; ++kb) {
             const int k0 = kb * BK;
@@ -604,6 +618,12 @@ static void row_gemm_tc_impl_t(const RowGemm& g, bool b_kmajor, int epi, const P
   p.mask_in = g.mask_in;
   p.row_base = g.row_base;
   if (g.sig) p.sig = *g.sig;
+  if (g.src_wait && !ps) {
+    if (g.src_P > 32) throw CudaError{"split dispatch: at most 32 ranks"};
+    p.src_wait = 1;
+    p.dP = g.src_P;
+    p.dme = g.src_me;
+  }
   if (epi == kEpiMask && !g.mask_in) throw CudaError{"tcgen05 dgrad needs the ReLU' bit mask"};
   const uint64_t ddims[3] = {(uint64_t)g.N, (uint64_t)g.Cm, (uint64_t)nseg_total};
   const uint64_t dstr[2] = {(uint64_t)g.N * 2, (uint64_t)g.Cm * g.N * 2};

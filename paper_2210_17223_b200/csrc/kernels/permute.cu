@@ -80,19 +80,19 @@ __device__ __forceinline__ long long rotated_row0(int R, long long rows, int El,
 // buffers over NVLink (peer[o] = rank o's buffer mapped here): row (c, e, r) lands at
 // recv row ((c*P + me)*El + e%El)*Cm + r of owner o = e / El, so the permute IS the
 // dispatch all-to-all.
+template <int NVL>
+constexpr int permute_R() { return NVL == 0 ? 1 : (NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / NVL); }
+
+// The R rows [g0 + row0, g0 + min(row0 + R, rows)) of one warp.
 template <typename T, int NVL, bool PEER>
-__device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int* __restrict__ tok_of,
-                                             const int* __restrict__ kept, int k, int d, int E, int C, int c0,
-                                             int nc, int Cm, int El, int P, int me, T* __restrict__ Send,
-                                             T* const* __restrict__ peer) {
-  constexpr int R = NVL == 0 ? 1 : (NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / NVL);
+__device__ __forceinline__ void permute_rows_at(const T* __restrict__ X, const int* __restrict__ tok_of,
+                                                const int* __restrict__ kept, int k, int d, int E, int C,
+                                                long long g0, long long row0, long long rows, int Cm, int El,
+                                                int P, int me, T* __restrict__ Send, T* const* __restrict__ peer) {
+  constexpr int R = permute_R<NVL>();
   constexpr int NL = NVL == 0 ? 1 : NVL;
   constexpr int V = 16 / sizeof(T);
   const int lane = threadIdx.x & 31;
-  const long long rows = (long long)nc * E * Cm;  // the micro-op chunks [c0, c0 + nc)
-  const long long g0 = (long long)c0 * E * Cm;
-  const long long row0 = rotated_row0<PEER>(R, rows, El, P, me, Cm);
-  if (row0 < 0) return;
   const int nv = d / V;
   int a = -1, owner = 0;
   size_t prow = 0;
@@ -137,6 +137,18 @@ __device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int*
       }
     }
   }
+}
+
+template <typename T, int NVL, bool PEER>
+__device__ __forceinline__ void permute_rows(const T* __restrict__ X, const int* __restrict__ tok_of,
+                                             const int* __restrict__ kept, int k, int d, int E, int C, int c0,
+                                             int nc, int Cm, int El, int P, int me, T* __restrict__ Send,
+                                             T* const* __restrict__ peer) {
+  const long long rows = (long long)nc * E * Cm;  // the micro-op chunks [c0, c0 + nc)
+  const long long g0 = (long long)c0 * E * Cm;
+  const long long row0 = rotated_row0<PEER>(permute_R<NVL>(), rows, El, P, me, Cm);
+  if (row0 < 0) return;
+  permute_rows_at<T, NVL, PEER>(X, tok_of, kept, k, d, E, C, g0, row0, rows, Cm, El, P, me, Send, peer);
 }
 
 template <typename T, int NVL, bool PEER>
@@ -306,22 +318,20 @@ __global__ void combine_loop_kernel(const T* __restrict__ Recv, const int* __res
 
 // combine backward over send-layout rows: dg_a = <dY_t, O_row>, dSend[row] = g_a · dY_t
 // (0 for padding rows).  PEER: dSend rows are stored into the owners' receive buffers.
+template <int NVL>
+constexpr int combine_bwd_R() { return NVL == 0 ? 1 : (2 * NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / (2 * NVL)); }
+
 template <typename T, int NVL, bool PEER>
-__device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const T* __restrict__ Recv,
-                                                 const int* __restrict__ tok_of, const int* __restrict__ kept,
-                                                 const float* __restrict__ gate,
-                                                 int k, int d, int E, int C, int c0, int nc, int Cm, int El, int P,
-                                                 int me,
-                                                 T* __restrict__ dSend, T* const* __restrict__ peer,
-                                                 float* __restrict__ dg) {
+__device__ __forceinline__ void combine_bwd_rows_at(const T* __restrict__ dY, const T* __restrict__ Recv,
+                                                    const int* __restrict__ tok_of, const int* __restrict__ kept,
+                                                    const float* __restrict__ gate, int k, int d, int E, int C,
+                                                    long long g0, long long row0, long long rows, int Cm, int El,
+                                                    int P, int me, T* __restrict__ dSend,
+                                                    T* const* __restrict__ peer, float* __restrict__ dg) {
   constexpr int NL = NVL == 0 ? 1 : NVL;
-  constexpr int R = NVL == 0 ? 1 : (2 * NVL >= kLoadsPerLane ? 1 : kLoadsPerLane / (2 * NVL));
+  constexpr int R = combine_bwd_R<NVL>();
   constexpr int V = 16 / sizeof(T);
   const int lane = threadIdx.x & 31;
-  const long long rows = (long long)nc * E * Cm;  // the micro-op chunks [c0, c0 + nc)
-  const long long g0 = (long long)c0 * E * Cm;
-  const long long row0 = rotated_row0<PEER>(R, rows, El, P, me, Cm);
-  if (row0 < 0) return;
   const int nv = d / V;
   int a = -1, owner = 0;
   size_t prow = 0;
@@ -410,6 +420,22 @@ __device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const
 }
 
 template <typename T, int NVL, bool PEER>
+__device__ __forceinline__ void combine_bwd_rows(const T* __restrict__ dY, const T* __restrict__ Recv,
+                                                 const int* __restrict__ tok_of, const int* __restrict__ kept,
+                                                 const float* __restrict__ gate,
+                                                 int k, int d, int E, int C, int c0, int nc, int Cm, int El, int P,
+                                                 int me,
+                                                 T* __restrict__ dSend, T* const* __restrict__ peer,
+                                                 float* __restrict__ dg) {
+  const long long rows = (long long)nc * E * Cm;  // the micro-op chunks [c0, c0 + nc)
+  const long long g0 = (long long)c0 * E * Cm;
+  const long long row0 = rotated_row0<PEER>(combine_bwd_R<NVL>(), rows, El, P, me, Cm);
+  if (row0 < 0) return;
+  combine_bwd_rows_at<T, NVL, PEER>(dY, Recv, tok_of, kept, gate, k, d, E, C, g0, row0, rows, Cm, El, P, me, dSend,
+                                    peer, dg);
+}
+
+template <typename T, int NVL, bool PEER>
 __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ dY, const T* __restrict__ Recv,
                                                           const int* __restrict__ tok_of,
                                                           const int* __restrict__ kept,
@@ -428,6 +454,63 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ 
     __syncthreads();
     if (threadIdx.x == 0) sig_post_last(sig);  // the last CTA: READY of the backward dispatch
   }
+}
+
+// Split dispatch (n = 1, fused transport): the owner blocks of the send layout
+// (owner o = experts [o*El, (o+1)*El), El*Cm rows each) in the order j = j0 .. j0+nj-1,
+// owner(j) = (me - j) mod P — j = 0 is this rank's own block (no NVLink), then the peers
+// in descending order, so at step j every rank s writes to s - j (no incast) and rank o
+// receives first from o + 1, then o + 2, ... (the order its expert GEMM consumes them in,
+// gemm_tc.cu `src_wait`).  All CTAs of the (persistent) grid walk the blocks in that
+// order; the last CTA done with block j posts READY to owner(j) alone (done[j]), so an
+// owner's GEMM starts on a source's rows as soon as they are in.
+// BWD = false: the permute (S3 + S4); BWD = true: combine-backward (S8a; dg too).
+template <typename T, int NVL, bool BWD>
+__global__ void __launch_bounds__(256) split_rows_kernel(const T* __restrict__ src, const T* __restrict__ Recv,
+                                                         const int* __restrict__ tok_of,
+                                                         const int* __restrict__ kept,
+                                                         const float* __restrict__ gate, int k, int d, int E, int C,
+                                                         int Cm, int El, int P, int me, int j0, int nj,
+                                                         T* const* __restrict__ peer, float* __restrict__ dg,
+                                                         PeerSignal sig, unsigned int* __restrict__ done) {
+  pdl_enter();
+  if (sig.wait) {  // (backward: the owners' dO is free)
+    if (threadIdx.x == 0) sig_wait(sig);
+    __syncthreads();
+  }
+  constexpr int R = BWD ? combine_bwd_R<NVL>() : permute_R<NVL>();
+  const long long blk = (long long)El * Cm;
+  const long long wpc = blockDim.x >> 5;
+  const long long gw = (long long)blockIdx.x * wpc + (threadIdx.x >> 5);
+  const long long nw = (long long)gridDim.x * wpc;
+  for (int j = j0; j < j0 + nj; ++j) {
+    const int owner = ((me - j) % P + P) % P;
+    const long long base = (long long)owner * blk, end = base + blk;
+    for (long long r0 = base + gw * R; r0 < end; r0 += nw * R) {
+      if constexpr (BWD)
+        combine_bwd_rows_at<T, NVL, true>(src, Recv, tok_of, kept, gate, k, d, E, C, 0, r0, end, Cm, El, P, me,
+                                          nullptr, peer, dg);
+      else
+        permute_rows_at<T, NVL, true>(src, tok_of, kept, k, d, E, C, 0, r0, end, Cm, El, P, me, nullptr, peer);
+    }
+    if (j > 0 && sig.post) {
+      __syncthreads();
+      if (threadIdx.x == 0) sig_post_owner_last(sig, done + j, owner, gridDim.x);
+    }
+  }
+}
+
+// This rank's per-expert counts into every owner's recv_kept (after their FREE), then
+// COUNT posted: the owners' tile lists need every source's counts, the rows may follow.
+__global__ void dispatch_counts_kernel(const int* __restrict__ kept, int P, int El, int me,
+                                       int* const* __restrict__ peer_counts, PeerSignal free_sig,
+                                       PeerSignal count_sig) {
+  pdl_enter();
+  if (threadIdx.x == 0) sig_wait(free_sig);
+  __syncthreads();
+  for (int i = threadIdx.x; i < P * El; i += blockDim.x) peer_counts[i / El][me * El + i % El] = kept[i];
+  __syncthreads();
+  if (threadIdx.x == 0) sig_post(count_sig);
 }
 
 inline int blocks_for_warps(long long warps, int threads = 256) {
@@ -557,6 +640,50 @@ void launch_combine_bwd_peer(int dtype, const void* dY, const void* Recv, const 
                              cudaStream_t s) {
   combine_bwd_any<true>(dtype, dY, Recv, tok_of, kept, gate, T, k, d, E, C, c0, nc, Cm, El, P, me, nullptr,
                         peer_rows, dg, sig, s);
+}
+
+void launch_dispatch_counts(const int* kept, int P, int El, int me, void* const* peer_counts,
+                            const PeerSignal& free_sig, const PeerSignal& count_sig, cudaStream_t s) {
+  launch_k(dispatch_counts_kernel, dim3(1), dim3(256), 0, s, kept, P, El, me, (int* const*)peer_counts, free_sig,
+           count_sig);
+  LINA_LAUNCH_CHECK();
+}
+
+template <bool BWD>
+static void split_any(int dtype, const void* src, const void* Recv, const int* tok_of, const int* kept,
+                      const float* gate, int k, int d, int E, int C, int Cm, int El, int P, int me,
+                      void* const* peer_rows, float* dg, int j0, int nj, int grid, const PeerSignal& sig,
+                      unsigned int* done, cudaStream_t s) {
+  const int nvl = nvl_of(d, dtype);
+  // persistent grids (the peers' rows beside the expert GEMM) use 128-thread CTAs: one fits
+  // next to a GEMM CTA in the SM's registers (<= 64K - 320 x 136) and its 1 KB of reserved
+  // shared memory next to the GEMM's 225.5 KB
+  int threads = 128;
+  if (grid <= 0) {  // one pass over one block
+    const long long rows = (long long)El * Cm * nj;
+    const int r = rows_per_warp(nvl, BWD ? 2 : 1);
+    threads = 256;
+    grid = blocks_for_warps(std::max(1LL, (rows + r - 1) / r));
+  }
+  LINA_DISPATCH_T(dtype, LINA_DISPATCH_NVL(nvl, launch_k(split_rows_kernel<ET, NV_, BWD>, dim3(grid), dim3(threads), 0, s,
+                             (const ET*)src, (const ET*)Recv, tok_of, kept, gate, k, d, E, C, Cm, El, P, me, j0, nj,
+                             (ET* const*)peer_rows, dg, sig, done)));
+  LINA_LAUNCH_CHECK();
+}
+
+void launch_permute_split(int dtype, const void* X, const int* tok_of, const int* kept, int k, int d, int E, int C,
+                          int Cm, int El, int P, int me, void* const* peer_rows, int j0, int nj, int grid,
+                          const PeerSignal& sig, unsigned int* done, cudaStream_t s) {
+  split_any<false>(dtype, X, nullptr, tok_of, kept, nullptr, k, d, E, C, Cm, El, P, me, peer_rows, nullptr, j0, nj,
+                   grid, sig, done, s);
+}
+
+void launch_combine_bwd_split(int dtype, const void* dY, const void* Recv, const int* tok_of, const int* kept,
+                              const float* gate, int k, int d, int E, int C, int Cm, int El, int P, int me,
+                              void* const* peer_rows, float* dg, int j0, int nj, int grid, const PeerSignal& sig,
+                              unsigned int* done, cudaStream_t s) {
+  split_any<true>(dtype, dY, Recv, tok_of, kept, gate, k, d, E, C, Cm, El, P, me, peer_rows, dg, j0, nj, grid, sig,
+                  done, s);
 }
 
 }  // namespace lina

@@ -52,10 +52,13 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
     p.tile_rows = per_seg <= 96 ? 128 : 256;
     const char* tr = getenv("LINA_TILE_ROWS");
     if (tr && (atoi(tr) == 128 || atoi(tr) == 256)) p.tile_rows = atoi(tr);
-    // tail split of the 256-row tiles (RowGemm::mtp_tail): tensor-core path only;
-    // LINA_TAIL128=0 turns it off (A/B)
+    // tail split of the 256-row tiles (RowGemm::mtp_tail): tensor-core path only, opt-in
+    // (LINA_TAIL128=1).  Its second launch has one 128-row tile per segment and N block, each
+    // with the full K: at C2 / C3 that is less than a wave of long tiles, which cost more
+    // than the halved padding saves (C2 N=1: 0.512 vs 0.443 ms per step; C3 N=2: 0.945 vs
+    // 0.890 ms); at C5 the two roughly cancel (profiles/r02_tail_split_ab.txt).
     const char* ts = getenv("LINA_TAIL128");
-    p.tail_split = p.bf16 && p.tile_rows == 256 && !(ts && ts[0] == '0') && !getenv("LINA_FORCE_SIMT");
+    p.tail_split = p.bf16 && p.tile_rows == 256 && (ts && ts[0] == '1') && !getenv("LINA_FORCE_SIMT");
   }
   const size_t T = p.T, k = p.k, E = p.E;
   size_t o = 0;
@@ -288,8 +291,13 @@ void tile_lists(const Plan& p, const Ptrs& q, cudaStream_t s) {
 void row_gemm(const Plan& p, const void* A, const void* B, void* D, const void* aux,
               const int* vcount, const int* mtp, int c, int N, int K, bool b_kmajor, int epi,
               cudaStream_t st, uint64_t* mask_out = nullptr, const uint64_t* mask_in = nullptr,
-              const PeerSignal* sig = nullptr) {
+              const PeerSignal* sig = nullptr, int src_me = -1) {
   RowGemm g{};
+  if (src_me >= 0) {  // split dispatch: sig.wait per source, tiles from source src_me up
+    g.src_wait = 1;
+    g.src_P = p.P;
+    g.src_me = src_me;
+  }
   g.tile_rows = p.tile_rows;
   g.sig = sig;
   g.mask_out = mask_out;
@@ -491,6 +499,32 @@ bool fused_ok(const lina_comm* cm, const Plan& p) {
          p.d % 64 == 0 && p.f % 64 == 0 && p.d % 32 == 0;
 }
 
+// Split dispatch (n = 1; permute.cu split_rows_kernel, gemm_tc.cu src_wait): the counts go
+// first (one 1-CTA kernel), this rank's own rows move on the compute stream, the peers' rows
+// on the high-priority stream by a persistent grid of LINA_DISPATCH_CTAS CTAs (default: one
+// per SM) that shares the SMs with the expert GEMM, posting READY per owner; the owner's
+// GEMM1 / dgrad1 start on its own source's rows and take a peer's rows once that peer has
+// posted them ("the expert can start computing with a subset of the tokens").
+// LINA_SPLIT_DISPATCH=0: the whole dispatch before the GEMMs (round-1 order).
+bool split_dispatch(const Plan& p) {
+  static const bool on = [] {
+    const char* e = getenv("LINA_SPLIT_DISPATCH");
+    return !(e && e[0] == '0');
+  }();
+  return on && p.n == 1 && p.P <= 8;
+}
+int split_ctas() {
+  static const int n = [] {
+    const char* e = getenv("LINA_DISPATCH_CTAS");
+    if (e && atoi(e) > 0) return atoi(e);
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+  }();
+  return n;
+}
+enum { kSiteSplitFwd = 16, kSiteSplitBwd = 24 };
+
 // Micro-op c of a signal: slot c of the kind (wait: chunks [c, c + wait_chunks)).
 PeerSignal chunk_sig(PeerSignal g, int c, int wait_chunks = 1) {
   if (g.wait) g.wait += c;
@@ -568,17 +602,33 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   const PeerStore st = peer_store(ce, "fwdC:", saved, p.s_C, p, me, cb, s);
   // dispatch = permute into the owners' R (after their FREE; READY per micro-op)
   const PeerSignal s_disp = make_sig(cm, CT::kFreeFwd, rf, 1, CT::kFReadyFwdD, rf, 1, kSiteDispFwd);
-  cudaStream_t sm = n > 1 ? cm->hi : s;  // the mover stream
-  if (n > 1) {
+  const bool split = split_dispatch(p);
+  cudaStream_t sm = (n > 1 || split) ? cm->hi : s;  // the mover stream
+  if (split) {
+    // counts first (after the owners' FREE), then the peers' rows on `hi` beside GEMM1
+    launch_dispatch_counts(q.kept, P, p.El, me, peer_cnt, wait_only(s_disp),
+                           make_sig(cm, -1, nullptr, 0, CT::kFCountFwdS, rf, 1), s);
     LINA_CUDA_CHECK(cudaEventRecord(cm->ev[0], s));
     LINA_CUDA_CHECK(cudaStreamWaitEvent(sm, cm->ev[0], 0));
+    prof_a2a_begin(cm, sm);
+    launch_permute_split(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, p.Cm, p.El, P, me, peer_R, 1, P - 1,
+                         split_ctas(), make_sig(cm, -1, nullptr, 0, CT::kFReadyFwdD, rf, 1),
+                         ce.done_counter(kSiteSplitFwd), sm);
+    LINA_CUDA_CHECK(cudaEventRecord(cm->ev[1], sm));
+    launch_permute_split(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, p.Cm, p.El, P, me, peer_R, 0, 1, 0,
+                         PeerSignal{}, nullptr, s);  // this rank's own rows
+  } else {
+    if (n > 1) {
+      LINA_CUDA_CHECK(cudaEventRecord(cm->ev[0], s));
+      LINA_CUDA_CHECK(cudaStreamWaitEvent(sm, cm->ev[0], 0));
+    }
+    prof_a2a_begin(cm, sm);
+    launch_sig_wait(wait_only(s_disp), sm);
+    for (int c = 0; c < n; ++c)
+      launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, c, 1, p.Cm, p.El, P, me, peer_R,
+                          peer_cnt, chunk_sig(no_wait(s_disp), c), sm);
+    if (n > 1) LINA_CUDA_CHECK(cudaEventRecord(cm->ev[1], sm));
   }
-  prof_a2a_begin(cm, sm);
-  launch_sig_wait(wait_only(s_disp), sm);
-  for (int c = 0; c < n; ++c)
-    launch_permute_peer(dtype, tokens, q.tok_of, q.kept, p.k, p.d, p.E, p.C, c, 1, p.Cm, p.El, P, me, peer_R,
-                        peer_cnt, chunk_sig(no_wait(s_disp), c), sm);
-  if (n > 1) LINA_CUDA_CHECK(cudaEventRecord(cm->ev[1], sm));
   trace_mark(cm, s, "permute(peer)");
   if (route) {
     if (route->idx && !override_r)
@@ -593,7 +643,10 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
   const PeerSignal s_recv = make_sig(cm, CT::kFReadyFwdD, rf, 1, -1, nullptr, 0);
   const PeerSignal s_comb = make_sig(cm, -1, nullptr, 0, CT::kFReadyFwdC, rf, 1, kSiteCombFwd);
   for (int c = 0; c < n; ++c) {
-    launch_sig_wait(wait_only(chunk_sig(s_recv, c)), s);  // micro-op c (and with c = 0 the counts) has landed
+    if (split)  // every source's counts have landed (its rows follow: GEMM1 waits per source)
+      launch_sig_wait(wait_only(make_sig(cm, CT::kFCountFwdS, rf, 1, -1, nullptr, 0)), s);
+    else
+      launch_sig_wait(wait_only(chunk_sig(s_recv, c)), s);  // micro-op c (and with c = 0 the counts) has landed
     if (c == 0) {
       launch_vcount(q.recv_kept, P, p.El, p.C, n, q.vcount, s);
       launch_mtile_prefix(q.vcount, n, P * p.El, p.tile_rows, q.mtp, s);
@@ -601,7 +654,11 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
       trace_mark(cm, s, "vcount");
       prof_begin(cm, s);
     }
-    row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask);
+    if (split)
+      row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask, nullptr, &s_recv,
+               me);
+    else
+      row_gemm(p, q.R, w1, q.H, nullptr, q.vcount, q.mtp, c, p.f, p.d, true, kEpiRelu, s, q.mask);
     trace_mark(cm, s, "gemm1");
     RowGemm g = peer_gemm(p, q.H, w2, q.O, q.vcount, q.mtp, c, p.d, p.f);
     const PeerSignal s_c = chunk_sig(s_comb, c);
@@ -610,7 +667,7 @@ void forward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* toke
     trace_mark(cm, s, "gemm2(peer)");
   }
   prof_end(cm, s, 2 * n);
-  if (n > 1) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, cm->ev[1], 0));  // join the mover stream
+  if (n > 1 || split) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, cm->ev[1], 0));  // join the mover stream
   // combine: the returned expert outputs of every micro-op have landed (1-CTA wait); its
   // last CTA closes the forward's round
   const PeerSignal s_out = make_sig(cm, CT::kFReadyFwdC, rf, 1, -1, nullptr, 0, kSiteFwdEnd, rf);
@@ -638,24 +695,45 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   // posted at the end of their previous backward, once its wgrad and dX had read dO and
   // dXs — so layers sharing one workspace on a comm stay ordered; READY per micro-op)
   const PeerSignal s_disp = make_sig(cm, CT::kFreeBwd, rb, 0, CT::kFReadyBwdD, rb, 1, kSiteDispBwd);
-  cudaStream_t sm = n > 1 ? cm->hi : s;
-  if (n > 1) {
+  const bool split = split_dispatch(p);
+  cudaStream_t sm = (n > 1 || split) ? cm->hi : s;
+  if (split) {
+    // the peers' rows on `hi` (every CTA first waits for the owners' backward FREE), this
+    // rank's own rows on `s`; dg of dropped assignments stays 0
+    if (p.T > 0) LINA_CUDA_CHECK(cudaMemsetAsync(q.dg, 0, sizeof(float) * (size_t)p.T * p.k, s));
     LINA_CUDA_CHECK(cudaEventRecord(cm->ev[2], s));
     LINA_CUDA_CHECK(cudaStreamWaitEvent(sm, cm->ev[2], 0));
+    prof_a2a_begin(cm, sm);
+    PeerSignal s_rows = make_sig(cm, CT::kFreeBwd, rb, 0, CT::kFReadyBwdD, rb, 1);
+    launch_combine_bwd_split(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.k, p.d, p.E, p.C, p.Cm, p.El, P, me,
+                             peer_dO, q.dg, 1, P - 1, split_ctas(), s_rows, ce.done_counter(kSiteSplitBwd), sm);
+    LINA_CUDA_CHECK(cudaEventRecord(cm->ev[3], sm));
+    launch_combine_bwd_split(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.k, p.d, p.E, p.C, p.Cm, p.El, P, me,
+                             peer_dO, q.dg, 0, 1, 0, PeerSignal{}, nullptr, s);  // this rank's own rows
+  } else {
+    if (n > 1) {
+      LINA_CUDA_CHECK(cudaEventRecord(cm->ev[2], s));
+      LINA_CUDA_CHECK(cudaStreamWaitEvent(sm, cm->ev[2], 0));
+    }
+    prof_a2a_begin(cm, sm);
+    launch_sig_wait(wait_only(s_disp), sm);
+    for (int c = 0; c < n; ++c)
+      launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.T, p.k, p.d, p.E, p.C, c, 1, p.Cm,
+                              p.El, P, me, peer_dO, q.dg, chunk_sig(no_wait(s_disp), c), sm);
+    if (n > 1) LINA_CUDA_CHECK(cudaEventRecord(cm->ev[3], sm));
   }
-  prof_a2a_begin(cm, sm);
-  launch_sig_wait(wait_only(s_disp), sm);
-  for (int c = 0; c < n; ++c)
-    launch_combine_bwd_peer(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.T, p.k, p.d, p.E, p.C, c, 1, p.Cm, p.El,
-                            P, me, peer_dO, q.dg, chunk_sig(no_wait(s_disp), c), sm);
-  if (n > 1) LINA_CUDA_CHECK(cudaEventRecord(cm->ev[3], sm));
   trace_mark(cm, s, "combine_bwd(peer)");
   const PeerSignal s_recv = make_sig(cm, CT::kFReadyBwdD, rb, 1, -1, nullptr, 0);
   const PeerSignal s_comb = make_sig(cm, -1, nullptr, 0, CT::kFReadyBwdC, rb, 1, kSiteCombBwd);
   prof_begin(cm, s);
   for (int c = 0; c < n; ++c) {
-    launch_sig_wait(wait_only(chunk_sig(s_recv, c)), s);  // micro-op c of the peers' dO rows has landed
-    row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask);
+    if (split) {  // dgrad1 takes each source's dO rows as soon as that source has posted them
+      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask, &s_recv,
+               me);
+    } else {
+      launch_sig_wait(wait_only(chunk_sig(s_recv, c)), s);  // micro-op c of the peers' dO rows has landed
+      row_gemm(p, q.dO, w2, q.dH, q.H, q.vcount, q.mtp, c, p.f, p.d, false, kEpiMask, s, nullptr, q.mask);
+    }
     trace_mark(cm, s, "dgrad1");
     RowGemm g = peer_gemm(p, q.dH, w1, q.dXe, q.vcount, q.mtp, c, p.d, p.f);
     const PeerSignal s_c = chunk_sig(s_comb, c);
@@ -672,7 +750,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   launch_expert_wgrad(dtype, wg1, s);
   prof_end(cm, s, 2 * n + 2);
   trace_mark(cm, s, "wgrad x2");
-  if (n > 1) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, cm->ev[3], 0));  // dg of every micro-op
+  if (n > 1 || split) LINA_CUDA_CHECK(cudaStreamWaitEvent(s, cm->ev[3], 0));  // dg of every micro-op
   // dWg needs only this rank's dg: it overlaps the last returning expert gradients
   launch_dwg(dtype, tokens, q.probs, q.idx, q.gate, q.dg, p.T, p.d, p.E, p.k, q.dwg, dgate_w, s);
   trace_mark(cm, s, "dwg");

@@ -86,6 +86,36 @@ __device__ __forceinline__ void sig_post_last(const PeerSignal& s) {
   }
 }
 
+// Wait for one peer's slots only (the split dispatch: a consumer takes the rows of source
+// r as soon as r has posted them).
+__device__ __forceinline__ void sig_wait_one(const PeerSignal& s, int r) {
+  if (!s.wait || r == s.me) return;
+  const uint32_t target = *s.wait_round + s.wait_add;
+  const long long t0 = clock64();
+  for (int c = 0; c < s.wait_chunks; ++c) {
+    const uint32_t* f = s.wait + (size_t)r * s.stride + c;
+    while ((int)(sig_ld_acquire(f) - target) < 0) {
+      __nanosleep(64);
+      if (clock64() - t0 > 20000000000LL) __trap();
+    }
+  }
+}
+
+// Thread 0 of every CTA after its last store to `owner`: the last of the `nb` CTAs
+// publishes READY to that owner alone (`done` = that owner's zeroed counter).
+__device__ __forceinline__ void sig_post_owner_last(const PeerSignal& s, unsigned int* done, int owner,
+                                                    unsigned int nb) {
+  if (!s.post) return;
+  unsigned int prev;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(done) : "memory");
+  if (prev == nb - 1) {
+    *done = 0u;
+    const uint32_t v = *s.post_round + s.post_add;
+    __threadfence_system();
+    sig_st_release(s.post[owner] + s.post_chunk, v);
+  }
+}
+
 // Thread 0 of every CTA, after its last use of the round: the last CTA closes the round.
 __device__ __forceinline__ void sig_bump_last(const PeerSignal& s) {
   if (!s.bump) return;

@@ -240,14 +240,31 @@ def test_two_layers_interleaved_fwd_fwd_bwd_bwd():
         assert moe.normwise_error(dw2, o["bw"].dW2) <= tol, n
 
 
-def test_c5_shapes_fwd_bwd_two_cta_tiles():
+@pytest.mark.parametrize("tail", ["0", "1"])
+def test_c5_shapes_fwd_bwd_two_cta_tiles(tail, monkeypatch):
     """configs[4] layer dims (d=2048, f=8192, top-2, capacity 1.25) with 16 experts at 1024
     tokens: 128 rows per expert segment (> 96), so the expert GEMMs run the 2-CTA 256-row
     tiles the C5 bench runs, with K = 8192 in GEMM2 / dgrad2 and M = 2048 / 8192 in the
-    wgrads; forward and backward against the oracle.  (All 64 experts at full C5 would need
-    the oracle's fp64 weight gradients, 34 GB; the forward at E = 64 is the test above.)"""
+    wgrads; forward and backward against the oracle, without and with the opt-in tail split
+    (LINA_TAIL128=1: a segment's last <= 128 rows as single-CTA tiles in a second launch).
+    (All 64 experts at full C5 would need the oracle's fp64 weight gradients, 34 GB; the
+    forward at E = 64 is the test above.)"""
+    monkeypatch.setenv("LINA_TAIL128", tail)
     cfg, X, Wg, W1, W2, dY = _case("C5", tokens=1024, num_experts=16)
     assert cfg.tokens_per_rank * cfg.k / cfg.num_experts > 96
+    g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY)
+    o = oracle_layer(cfg, X, Wg, W1, W2, dY)
+    compare(cfg, g, o)
+
+
+@pytest.mark.parametrize("experts,k,tokens", [(32, 2, 1024), (64, 2, 1000), (64, 3, 777), (24, 1, 640)])
+def test_gate_backward_tensor_core(experts, k, tokens):
+    """E > 16 on the bf16 path: dX and dWg go through the tcgen05 gate-backward kernels
+    (gate_bwd_tc.cu: the persistent dX kernel fused with the gather of the k returned rows,
+    the split-K dWg and the fp32 dL split into bf16 terms) — forward and backward against
+    the oracle at C5's top-k / capacity with d = 512, f = 1024, ragged token counts
+    (777, 1000: a last 128-token block partly empty) and k = 3 (the KM = 8 variant)."""
+    cfg, X, Wg, W1, W2, dY = _case("C5", tokens=tokens, num_experts=experts, k=k, d_model=512, d_ffn=1024)
     g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY)
     o = oracle_layer(cfg, X, Wg, W1, W2, dY)
     compare(cfg, g, o)
