@@ -230,33 +230,40 @@ __global__ void __launch_bounds__(kDxThreads, 1)
     if (lane == 0) sig_wait(sig);    // fused transport: the returned rows have landed
     __syncwarp();
     // the k rows' 32-column slices of the next chunk are loaded before the current chunk is
-    // summed (two chunks in flight per thread; KM = 2 only — KM = 8 would spill)
+    // summed (two chunks in flight per thread; KM = 2 only — KM = 8 would spill), and the
+    // next token block's row indices and first chunk are fetched during the current block's
+    // last chunk (no dependent-load bubble between blocks)
     constexpr bool PREF = KM <= 2;
-    int acc = 0;
-    uint32_t aph = 0;
-    for (int tb = tb0; tb < ntb; tb += per) {
+    auto rows_of = [&](int tb, size_t (&rows)[KM]) {
       const int t = tb * 128 + quarter * 32 + lane;
-      size_t rows[KM];
 #pragma unroll
       for (int j = 0; j < KM; ++j) {
         rows[j] = ~(size_t)0;
-        if (t < T && j < k) {
+        if (tb < ntb && t < T && j < k) {
           const int s = slot[(size_t)t * k + j];
           const int e = idx[(size_t)t * k + j];
           if (s >= 0) rows[j] = ebase ? (size_t)(ebase[e] + s) : send_row(e, s, E, C, n, Cm);
         }
       }
-      uint4 g[PREF ? 2 : 1][KM][4];
-      auto load_rows = [&](int cb, uint4 (&dst)[KM][4]) {
+    };
+    auto load_rows = [&](const size_t (&rows)[KM], int cb, uint4 (&dst)[KM][4]) {
 #pragma unroll
-        for (int j = 0; j < KM; ++j)
+      for (int j = 0; j < KM; ++j)
 #pragma unroll
-          for (int v = 0; v < 4; ++v)
-            dst[j][v] = rows[j] != ~(size_t)0
-                            ? *reinterpret_cast<const uint4*>(dXe + rows[j] * d + n0 + cb + 8 * v)
-                            : make_uint4(0, 0, 0, 0);
-      };
-      load_rows(c0, g[0]);
+        for (int v = 0; v < 4; ++v)
+          dst[j][v] = rows[j] != ~(size_t)0 ? *reinterpret_cast<const uint4*>(dXe + rows[j] * d + n0 + cb + 8 * v)
+                                            : make_uint4(0, 0, 0, 0);
+    };
+    int acc = 0;
+    uint32_t aph = 0;
+    uint4 g[PREF ? 2 : 1][KM][4];
+    size_t rows[KM];
+    rows_of(tb0, rows);
+    load_rows(rows, c0, g[0]);
+    for (int tb = tb0; tb < ntb; tb += per) {
+      const int t = tb * 128 + quarter * 32 + lane;
+      size_t nrows[KM];
+      if (PREF) rows_of(tb + per, nrows);  // (loads in flight while this block is summed)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + acc * 256;
@@ -265,8 +272,9 @@ __global__ void __launch_bounds__(kDxThreads, 1)
         const int cb = c0 + 32 * i;
         float a[32];
         tmem_ld32(ta + cb, *reinterpret_cast<uint32_t(*)[32]>(a));
-        if (PREF && i + 1 < 4) load_rows(cb + 32, g[(i + 1) & 1]);
-        if (!PREF && i > 0) load_rows(cb, g[0]);
+        if (PREF && i + 1 < 4) load_rows(rows, cb + 32, g[(i + 1) & 1]);
+        if (PREF && i == 3) load_rows(nrows, c0, g[0]);  // the next block's first chunk
+        if (!PREF && i > 0) load_rows(rows, cb, g[0]);
         uint4 (&cur)[KM][4] = g[PREF ? (i & 1) : 0];
         tmem_wait_ld();
         if (i == 3) {  // the accumulator is read: the MMA warp may reuse it
@@ -288,6 +296,13 @@ __global__ void __launch_bounds__(kDxThreads, 1)
           for (int v = 0; v < 4; ++v)
             store16(dX + (size_t)t * d + n0 + cb + 8 * v, a + 8 * v, (__nv_bfloat16*)nullptr);
         }
+      }
+      if (PREF) {
+#pragma unroll
+        for (int j = 0; j < KM; ++j) rows[j] = nrows[j];
+      } else {
+        rows_of(tb + per, rows);
+        load_rows(rows, c0, g[0]);
       }
       if (++acc == 2) {
         acc = 0;

@@ -524,6 +524,18 @@ int split_ctas() {
   return n;
 }
 enum { kSiteSplitFwd = 16, kSiteSplitBwd = 24 };
+// LINA_SCHED_WINDOW=dispatch (split dispatch only): the all-to-all phase the allreduce
+// scheduler defers to is the peer-row dispatch kernel alone, not the expert GEMMs whose
+// epilogues return the rows (a B200 reading of "no all-to-all in flight": there the
+// link traffic is the dispatch; the return is spread over dgrad2's tiles).  Default: the
+// whole window from combine-backward to the last returned tile.
+bool sched_window_dispatch() {
+  static const bool on = [] {
+    const char* e = getenv("LINA_SCHED_WINDOW");
+    return e && std::string(e) == "dispatch";
+  }();
+  return on;
+}
 
 // Micro-op c of a signal: slot c of the kind (wait: chunks [c, c + wait_chunks)).
 PeerSignal chunk_sig(PeerSignal g, int c, int wait_chunks = 1) {
@@ -707,6 +719,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
     PeerSignal s_rows = make_sig(cm, CT::kFreeBwd, rb, 0, CT::kFReadyBwdD, rb, 1);
     launch_combine_bwd_split(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.k, p.d, p.E, p.C, p.Cm, p.El, P, me,
                              peer_dO, q.dg, 1, P - 1, split_ctas(), s_rows, ce.done_counter(kSiteSplitBwd), sm);
+    if (cm->sched && sched_window_dispatch()) sched_a2a_end(cm, sm);
     LINA_CUDA_CHECK(cudaEventRecord(cm->ev[3], sm));
     launch_combine_bwd_split(dtype, dout, q.Cb, q.tok_of, q.kept, q.gate, p.k, p.d, p.E, p.C, p.Cm, p.El, P, me,
                              peer_dO, q.dg, 0, 1, 0, PeerSignal{}, nullptr, s);  // this rank's own rows
@@ -743,7 +756,7 @@ void backward_fused(lina_comm* cm, const Plan& p, const Ptrs& q, const void* dou
   }
   // the last kernel that moves all-to-all bytes is done: allreduce micro-ops may run
   // beside the weight gradients, dWg and dX (compute only)
-  if (cm->sched) sched_a2a_end(cm, s);
+  if (cm->sched && !(split && sched_window_dispatch())) sched_a2a_end(cm, s);
   WGrad wg2{q.dO, q.H, dw2, q.vcount, n, P, p.El, p.Cm, p.d, p.f};
   WGrad wg1{q.dH, q.R, dw1, q.vcount, n, P, p.El, p.Cm, p.f, p.d};
   launch_expert_wgrad(dtype, wg2, s);
