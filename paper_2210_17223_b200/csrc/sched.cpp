@@ -17,9 +17,11 @@
 // layer never waits on the scheduler).  This thread owns the DP communicator and
 // the low-priority stream.  Micro-ops are pointer offsets into the caller's
 // gradient (no chunk/cat copies).  It polls CUDA events (never
-// blocks the device) for (a) gradient readiness and (b) completion of the
-// registered all-to-all phase, and issues ncclAllReduce micro-ops only when the
-// LINA admission rule holds.  BASELINE issues whole gradients immediately, gated
+// blocks the device) for (a) gradient readiness and (b) the device markers of every
+// registered all-to-all phase (begin = the backward's combining computation starts,
+// end = its last all-to-all byte has moved), and issues ncclAllReduce micro-ops only
+// when the LINA admission rule holds on the DEVICE timeline: no phase the device has
+// reached is unfinished.  BASELINE issues whole gradients immediately, gated
 // on readiness only on the device (fair-sharing the links).  Two
 // ablations of the paper's design discussion: NAIVE = the LINA admission rule with
 // whole gradients (strict priority, no partitioning) and DEFER = whole
@@ -76,7 +78,10 @@ class Scheduler {
     thread_.join();
     for (auto& j : jobs_)
       if (j.ready) cudaEventDestroy(j.ready);
-    for (auto& e : a2a_events_) cudaEventDestroy(e.second);
+    for (auto& ph : phases_) {
+      if (ph.begin) cudaEventDestroy(ph.begin);
+      if (ph.end) cudaEventDestroy(ph.end);
+    }
     cudaFree(done_flag_);
   }
   void config(lina_policy pol, size_t bytes) {
@@ -99,11 +104,20 @@ class Scheduler {
     }
     cv_.notify_all();
   }
-  // The next all-to-all phase (sequence number reg_seq_) is imminent.
-  void a2a_imminent() {
+  // An all-to-all phase is imminent once `s` reaches this point (the combining computation
+  // of the backward starts).  Device time, not host time: the host enqueues a whole
+  // multi-layer backward far ahead of the device, so a host-side flag would hold every
+  // micro-op back until the last layer's phase had ended.
+  void a2a_imminent(cudaStream_t s) {
+    cudaEvent_t e;
+    LINA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    LINA_CUDA_CHECK(cudaEventRecord(e, s));
     std::lock_guard<std::mutex> g(mu_);
-    imminent_seq_ = reg_seq_;
-    imminent_ = true;
+    if (!phases_.empty() && !phases_.back().end) {  // the open phase has begun already
+      cudaEventDestroy(e);
+      return;
+    }
+    phases_.push_back({next_seq_++, e, nullptr});
   }
   // The all-to-all phase ends when `a2a_stream` reaches this point.
   void a2a_end(cudaStream_t a2a_stream) {
@@ -111,7 +125,8 @@ class Scheduler {
     LINA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     LINA_CUDA_CHECK(cudaEventRecord(e, a2a_stream));
     std::lock_guard<std::mutex> g(mu_);
-    a2a_events_.push_back({reg_seq_++, e});
+    if (!phases_.empty() && !phases_.back().end) phases_.back().end = e;
+    else phases_.push_back({next_seq_++, nullptr, e});  // (no begin marker: begun when registered)
     cv_.notify_all();
   }
   // Make `s` wait, on the device, for every job submitted so far: a marker job goes
@@ -132,7 +147,7 @@ class Scheduler {
       if (outstanding_ == 0) return;  // nothing submitted since the last wait point
       target = ++wait_target_;
       for (auto& j : jobs_)  // phases registered from now on run after these jobs
-        if (!j.marker && j.a2a_limit == ~0ull) j.a2a_limit = reg_seq_;
+        if (!j.marker && j.a2a_limit == ~0ull) j.a2a_limit = next_seq_;
       ArJob m{};
       m.marker = target;
       jobs_.push_back(m);
@@ -158,20 +173,25 @@ class Scheduler {
   }
 
  private:
-  // true while a registered all-to-all phase (sequence < limit) has not completed on the device
-  bool a2a_inflight_locked(uint64_t limit) {
-    while (!a2a_events_.empty()) {
-      cudaError_t q = cudaEventQuery(a2a_events_.front().second);
-      if (q == cudaErrorNotReady) return a2a_events_.front().first < limit;
-      cudaEventDestroy(a2a_events_.front().second);
-      a2a_events_.pop_front();
-      if (a2a_events_.empty() && imminent_seq_ < reg_seq_) imminent_ = false;  // the a2a phase has drained
+  static bool done(cudaEvent_t e) { return !e || cudaEventQuery(e) != cudaErrorNotReady; }
+  // Phases (sequence < limit) the device has reached and not finished.  `queued`: a phase
+  // counts from its begin marker (the combining computation has started: the all-to-all is
+  // imminent / waiting, LINA and NAIVE); otherwise from its first all-to-all kernel on —
+  // approximated by the same marker, the fused transport's dispatch follows it at once —
+  // and only while that phase is in flight (DEFER).  Phases not yet reached, and those
+  // behind them, do not count: they cannot start before the device gets there.
+  bool a2a_busy_locked(uint64_t limit) {
+    while (!phases_.empty() && phases_.front().end && done(phases_.front().end)) {
+      if (phases_.front().begin) cudaEventDestroy(phases_.front().begin);
+      cudaEventDestroy(phases_.front().end);
+      phases_.pop_front();
+    }
+    for (const auto& ph : phases_) {
+      if (ph.seq >= limit) break;
+      if (ph.end && done(ph.end)) continue;
+      return done(ph.begin);  // reached and not finished: busy; not reached: nothing later is either
     }
     return false;
-  }
-  // true while an all-to-all is queued or in flight (LINA / NAIVE admission rule)
-  bool a2a_busy_locked(uint64_t limit) {
-    return a2a_inflight_locked(limit) || (imminent_ && imminent_seq_ < limit);
   }
   void run() {
     // this thread's runtime calls must target the comm's device (not device 0)
@@ -199,8 +219,7 @@ class Scheduler {
       const bool split = policy_ == LINA_SCHED_LINA;
       bool can_issue = true;
       if (gated) {
-        const bool busy =
-            policy_ == LINA_SCHED_DEFER ? a2a_inflight_locked(j.a2a_limit) : a2a_busy_locked(j.a2a_limit);
+        const bool busy = a2a_busy_locked(j.a2a_limit);
         if (cudaEventQuery(j.ready) == cudaErrorNotReady) {
           // Not ready yet.  A job ahead of a wait point (finite a2a_limit) with every
           // all-to-all phase before that point already drained can meet no further
@@ -246,11 +265,15 @@ class Scheduler {
   std::mutex mu_;
   std::condition_variable cv_;
   std::deque<ArJob> jobs_;
-  std::deque<std::pair<uint64_t, cudaEvent_t>> a2a_events_;  // (phase sequence, end event)
-  uint64_t reg_seq_ = 0, imminent_seq_ = 0;
+  struct Phase {
+    uint64_t seq;
+    cudaEvent_t begin, end;  // device markers (null begin: begun when registered; null end: open)
+  };
+  std::deque<Phase> phases_;
+  uint64_t next_seq_ = 0;
   lina_policy policy_ = LINA_SCHED_LINA;
   size_t partition_bytes_ = (size_t)30 << 20;
-  bool imminent_ = false, stop_ = false;
+  bool stop_ = false;
   int outstanding_ = 0;
   uint32_t wait_target_ = 0;
   // LINA_SCHED_EARLY=1: issue a job ahead of a wait point before its gradient is ready (see
@@ -282,10 +305,10 @@ static bool capturing(cudaStream_t s) {
   return st != cudaStreamCaptureStatusNone;
 }
 void sched_a2a_imminent(lina_comm* cm, cudaStream_t s) {
-  if (cm->sched && !capturing(s)) cm->sched->a2a_imminent();
+  if (cm->sched && !capturing(s)) cm->sched->a2a_imminent(s);
 }
 void sched_a2a_begin(lina_comm* cm, cudaStream_t s) {
-  if (cm->sched && !capturing(s)) cm->sched->a2a_imminent();
+  if (cm->sched && !capturing(s)) cm->sched->a2a_imminent(s);
 }
 void sched_a2a_end(lina_comm* cm, cudaStream_t a2a_stream) {
   if (cm->sched && !capturing(a2a_stream)) cm->sched->a2a_end(a2a_stream);
