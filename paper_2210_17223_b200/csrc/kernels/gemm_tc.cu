@@ -50,17 +50,19 @@ constexpr int TMEM_COLS = 512;  // 2 accumulators x BN
 
 // WIDE: the epilogue-heavy ReLU / ReLU'-mask GEMMs (N = d_ffn outputs per row, short
 // K = d_model) get 8 epilogue warps (two per TMEM lane quarter, each owning half of
-// the 256 columns) and give up one pipeline stage for their staging boxes.
-template <int CG, bool WIDE = false> struct Geo {
+// the 256 columns).  WIDE = 1 gives up one pipeline stage for their double-buffered
+// staging boxes; WIDE = 2 keeps every stage and single-buffers the boxes (a warp waits
+// for its previous box's TMA store to have read the buffer before refilling it).
+template <int CG, int WIDE = 0> struct Geo {
   static constexpr int ROWS = 128 * CG;                  // tile rows per cluster
   static constexpr int A_BYTES = 128 * BK * 2;           // 16 KB per CTA
   static constexpr int B_ROWS = BN / CG;                 // B rows (N) staged per CTA
   static constexpr int B_BYTES = B_ROWS * BK * 2;        // 32 KB (CG=1) / 16 KB (CG=2)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (CG == 2 ? 6 : 4) - (WIDE ? 1 : 0);
+  static constexpr int STAGES = (CG == 2 ? 6 : 4) - (WIDE == 1 ? 1 : 0);
   static constexpr int EPW = WIDE ? 8 : 4;               // epilogue warps
   static constexpr int THREADS = 64 + 32 * EPW;
-  static constexpr int EPI_BUFS = 2;                     // 32 rows x 128 B boxes per epilogue warp
+  static constexpr int EPI_BUFS = WIDE == 2 ? 1 : 2;     // 32 rows x 128 B boxes per epilogue warp
   static constexpr int EPI_BYTES = EPW * EPI_BUFS * 4096;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
@@ -91,7 +93,7 @@ struct TcParams {
   char* pbase[kMaxPeerMaps];        // the same buffers as plain pointers (remote owners: SM stores)
 };
 
-template <int CG, bool WGRAD, bool B_MN, int EPI, bool WIDE = (EPI != kEpiNone)>
+template <int CG, bool WGRAD, bool B_MN, int EPI, int WIDE = (EPI != kEpiNone)>
 __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
@@ -467,7 +469,7 @@ static int num_sms() {
   return m < 2 ? 2 : m;
 }
 
-template <int CG, bool WGRAD, bool B_MN, int EPI, bool WIDE = (EPI != kEpiNone)>
+template <int CG, bool WGRAD, bool B_MN, int EPI, int WIDE = (EPI != kEpiNone)>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const CUtensorMap& x,
                    const TcParams& p, int grid, cudaStream_t s) {
   auto kern = tc_gemm_kernel<CG, WGRAD, B_MN, EPI, WIDE>;
@@ -498,21 +500,27 @@ template <int CG>
 static void row_dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                          const CUtensorMap& mx, const TcParams& p, bool b_kmajor, int epi, int grid,
                          cudaStream_t s) {
-  // LINA_GEMM_NARROW=1: the ReLU / mask epilogues on 4 warps with the 6-stage ring (A/B
-  // measurement of the wide-epilogue geometry)
-  static const bool narrow = [] {
-    const char* e = getenv("LINA_GEMM_NARROW");
-    return e && e[0] == '1';
+  // The ReLU / mask epilogues: LINA_GEMM_WIDE=0 (4 warps, 6-stage ring), 1 (8 warps,
+  // 5 stages, double-buffered boxes; default), 2 (8 warps, 6 stages, single-buffered boxes).
+  // (LINA_GEMM_NARROW=1 = LINA_GEMM_WIDE=0, kept for the round-2 A/B lines.)
+  static const int wide = [] {
+    const char* n = getenv("LINA_GEMM_NARROW");
+    if (n && n[0] == '1') return 0;
+    const char* e = getenv("LINA_GEMM_WIDE");
+    if (e && (e[0] == '0' || e[0] == '1' || e[0] == '2')) return e[0] - '0';
+    return 1;
   }();
   if (b_kmajor) {
-    if (epi == kEpiRelu && narrow) launch<CG, false, false, kEpiRelu, false>(ma, mb, md, mx, p, grid, s);
-    else if (epi == kEpiRelu) launch<CG, false, false, kEpiRelu>(ma, mb, md, mx, p, grid, s);
-    else if (epi == kEpiMask) launch<CG, false, false, kEpiMask>(ma, mb, md, mx, p, grid, s);
+    if (epi == kEpiRelu && wide == 0) launch<CG, false, false, kEpiRelu, 0>(ma, mb, md, mx, p, grid, s);
+    else if (epi == kEpiRelu && wide == 1) launch<CG, false, false, kEpiRelu, 1>(ma, mb, md, mx, p, grid, s);
+    else if (epi == kEpiRelu) launch<CG, false, false, kEpiRelu, 2>(ma, mb, md, mx, p, grid, s);
+    else if (epi == kEpiMask) launch<CG, false, false, kEpiMask, 1>(ma, mb, md, mx, p, grid, s);
     else launch<CG, false, false, kEpiNone>(ma, mb, md, mx, p, grid, s);
   } else {
-    if (epi == kEpiRelu) launch<CG, false, true, kEpiRelu>(ma, mb, md, mx, p, grid, s);
-    else if (epi == kEpiMask && narrow) launch<CG, false, true, kEpiMask, false>(ma, mb, md, mx, p, grid, s);
-    else if (epi == kEpiMask) launch<CG, false, true, kEpiMask>(ma, mb, md, mx, p, grid, s);
+    if (epi == kEpiRelu) launch<CG, false, true, kEpiRelu, 1>(ma, mb, md, mx, p, grid, s);
+    else if (epi == kEpiMask && wide == 0) launch<CG, false, true, kEpiMask, 0>(ma, mb, md, mx, p, grid, s);
+    else if (epi == kEpiMask && wide == 1) launch<CG, false, true, kEpiMask, 1>(ma, mb, md, mx, p, grid, s);
+    else if (epi == kEpiMask) launch<CG, false, true, kEpiMask, 2>(ma, mb, md, mx, p, grid, s);
     else launch<CG, false, true, kEpiNone>(ma, mb, md, mx, p, grid, s);
   }
 }
@@ -673,7 +681,14 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s) {
   const uint64_t ds[2] = {(uint64_t)g.N * 2, (uint64_t)g.M * g.N * 2};
   const uint32_t db[3] = {64, 32, 1};
   CUtensorMap md = make_map(g.D, 3, dd, ds, db);
-  launch<CG, true, true, kEpiNone>(ma, mb, md, md, p, grid, s);
+  // LINA_WGRAD_WIDE=2: 8 epilogue warps (6 stages, single-buffered boxes) — its tiles are
+  // short in K (one expert's rows), so the epilogue is as heavy per flop as GEMM1's
+  static const bool wide = [] {
+    const char* e = getenv("LINA_WGRAD_WIDE");
+    return e && e[0] == '2';
+  }();
+  if (wide) launch<CG, true, true, kEpiNone, 2>(ma, mb, md, md, p, grid, s);
+  else launch<CG, true, true, kEpiNone>(ma, mb, md, md, p, grid, s);
   LINA_LAUNCH_CHECK();
 }
 
