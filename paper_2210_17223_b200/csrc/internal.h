@@ -50,6 +50,7 @@ struct Plan {
       s_C, s_mask;
   size_t s_mtpt = 0, s_rbase = 0;  // tail-split tile lists (tc row GEMMs with 256-row tiles)
   bool tail_split = false;
+  bool half_tails = false;                 // RowGemm::half_tails (LINA_HALF128, layer.cpp)
   size_t saved_bytes;
   // offsets into `workspace`
   size_t w_route, w_D, w_O, w_dg, w_dwg, w_dS, w_dO, w_dH, w_dXe, w_dXs;

@@ -33,6 +33,10 @@ struct RowGemm {
   // a 129th..256th row costs a full 256-row MMA, a <= 128-row tail only half of one
   const int* mtp_tail = nullptr;
   const int* row_base = nullptr;
+  // half tails (tile_rows 256, tcgen05, no tail split): a segment's last m-tile holding
+  // <= 128 valid rows runs in the same launch as an M = 128 cta_group::2 tile (64 rows per
+  // CTA of the pair) — half the MMA time of the 256-row tile, no second launch
+  int half_tails = 0;
   // split dispatch (tcgen05, n = 1): sig.wait is per source — the TMA producer waits for
   // source s's slot before its first A load of a segment of s, and tiles are walked from
   // source src_me upwards (the order the sources' rows arrive in, permute.cu)

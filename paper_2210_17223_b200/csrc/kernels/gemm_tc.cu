@@ -91,6 +91,12 @@ struct TcParams {
   int src_wait;             // ROW: sig.wait per source (segment (c, s, el) waits for s only), tiles from dme up
   CUtensorMap pmaps[kMaxPeerMaps];  // kernel-parameter copies (the TMA unit reads them like tmD)
   char* pbase[kMaxPeerMaps];        // the same buffers as plain pointers (remote owners: SM stores)
+  // ROW, CG = 2: a segment's last m-tile holding <= 128 valid rows runs as an M = 128
+  // cta_group::2 tile (64 rows per CTA, loaded through tmA64) — half the MMA time of the
+  // M = 256 tile it would otherwise pad to.  Accumulator: the 2x2 data-path layout (per
+  // CTA, columns [0, 128) in TMEM lanes 0-63 and [128, 256) in lanes 64-127, 128 columns).
+  int half;
+  CUtensorMap tmA64;
 };
 
 template <int CG, bool WGRAD, bool B_MN, int EPI, int WIDE = (EPI != kEpiNone)>
@@ -177,6 +183,10 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
       m0 = (ml - p.mtp[i]) * G::ROWS + (p.row_base ? __ldg(p.row_base + p.seg0 + i) : 0);
     }
   };
+  // ROW, CG = 2: does the tile at (local segment se, first row m0) hold <= 128 valid rows?
+  auto half_of = [&](int se, int m0) {
+    return CG == 2 && !WGRAD && p.half && __ldg(p.vcount + p.seg0 + se) - m0 <= 128;
+  };
   auto kblocks_of = [&](int seg_or_el) {
     if (!WGRAD) return p.K / BK;
     int kb = 0;
@@ -205,12 +215,15 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         int se, m0, n0;
         decode(t, se, m0, n0);
+        const bool hf = !WGRAD && half_of(se, m0);
         auto issue = [&](int a0, int a1, int a2, int b0, int b1, int b2) {
           mbar_wait(&empty[stage], ph ^ 1);
           uint8_t* sa = smem + stage * G::STAGE_BYTES;
           uint8_t* sb = sa + G::A_BYTES;
-          if (leader) mbar_expect_tx(&full[stage], CG * G::STAGE_BYTES);
-          if (!A_MN) {
+          if (leader) mbar_expect_tx(&full[stage], CG * (hf ? G::STAGE_BYTES - G::A_BYTES / 2 : G::STAGE_BYTES));
+          if (!A_MN && hf) {
+            tma_load_3d<CG>(sa, &p.tmA64, &full[stage], a0, a1 - 64 * (int)rank, a2);  // rows m0 + 64 * rank
+          } else if (!A_MN) {
             tma_load_3d<CG>(sa, &tmA, &full[stage], a0, a1, a2);
           } else {
 #pragma unroll
@@ -269,7 +282,8 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
   } else if (warp == 1) {
     // ================= MMA issuer (leader CTA only)
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(G::ROWS, BN, A_MN, B_MN);
+      constexpr uint32_t idesc_full = idesc_bf16(G::ROWS, BN, A_MN, B_MN);
+      constexpr uint32_t idesc_half = idesc_bf16(128, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -278,6 +292,7 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
         int se, m0, n0;
         decode(t, se, m0, n0);
         const int nkb = kblocks_of(se);
+        const uint32_t idesc = half_of(se, m0) ? idesc_half : idesc_full;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -319,24 +334,25 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
     const int ew = warp - 2;                 // epilogue warp index
     const int quarter = warp & 3;
     constexpr int COLS = BN / (G::EPW / 4);  // columns per warp
-    const int col0 = (ew >> 2) * COLS;
     uint8_t* my_epi = epi_smem + ew * G::EPI_BUFS * 4096;
     int acc = 0;
     uint32_t aph = 0;
     int sub = 0;  // sub-tile counter (buffer = sub & 1)
     const int mwords = p.N >> 6;
-    auto box_of = [&](int t, int c0, int& x0, int& x1, int& x2) {
-      int se, m0, n0;
-      decode(t, se, m0, n0);
-      x0 = n0 + c0;
-      x1 = m0 + 128 * rank + quarter * 32;
-      x2 = WGRAD ? se : p.seg0 + se;
-    };
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       int se, m0, n0;
       decode(t, se, m0, n0);
       const int nkb = kblocks_of(se);
-      const int row = m0 + 128 * rank + quarter * 32 + lane;  // row within the segment
+      // full tile: this warp's 32 rows = TMEM lanes of its quarter, COLS columns from col0;
+      // half tile (2x2 layout): quarters 0/1 hold rows 0-31 / 32-63 of this CTA's 64 rows
+      // with output columns [0, 128), quarters 2/3 the same rows with columns [128, 256), all
+      // in TMEM columns [0, 128) — COLS / 2 columns per warp
+      const bool hf = half_of(se, m0);
+      const int rbase = hf ? m0 + 64 * rank + (quarter & 1) * 32 : m0 + 128 * rank + quarter * 32;
+      const int col0 = hf ? (quarter >> 1) * 128 + (ew >> 2) * (COLS / 2) : (ew >> 2) * COLS;  // output column
+      const int tcol0 = hf ? (ew >> 2) * (COLS / 2) : col0;                                   // TMEM column
+      const int njs = hf ? COLS / 128 : COLS / 64;  // 64-column boxes of this warp
+      const int row = rbase + lane;  // row within the segment
       const bool row_ok = !WGRAD && row < p.Cm;
       // ReLU' words are word-column-major, [seg][N/64][Cm]: the 32 lanes (32 consecutive
       // rows) of a warp store / load 256 contiguous bytes per word column
@@ -344,27 +360,29 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
       uint64_t mk[COLS / 64];
       if (EPI == kEpiMask) {  // before the accumulator wait: latency hidden
 #pragma unroll
-        for (int j = 0; j < COLS / 64; ++j) mk[j] = row_ok ? p.mask_in[mrow + (size_t)j * p.Cm] : 0ull;
+        for (int j = 0; j < COLS / 64; ++j) mk[j] = row_ok && j < njs ? p.mask_in[mrow + (size_t)j * p.Cm] : 0ull;
       }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
 #pragma unroll
-      for (int j = 0; j < COLS / 64; ++j, ++sub) {
+      for (int j = 0; j < COLS / 64; ++j) {
+        if (j >= njs) break;
         const int c0 = col0 + j * 64;
         const int b = sub % G::EPI_BUFS;
         uint8_t* buf = my_epi + b * 4096;
         const uint32_t rowaddr = smem_u32(buf) + lane * 128;
         uint32_t v[64];
         if (nkb > 0) {
-          tmem_ld32(tbase + c0, *reinterpret_cast<uint32_t(*)[32]>(v));
-          tmem_ld32(tbase + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+          tmem_ld32(tbase + tcol0 + j * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+          tmem_ld32(tbase + tcol0 + j * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
           tmem_wait_ld();
         } else {
 #pragma unroll
           for (int i = 0; i < 64; ++i) v[i] = 0u;
         }
         if (lane == 0 && sub >= G::EPI_BUFS) bulk_wait_read<G::EPI_BUFS - 1>();  // `buf`'s last store has read it
+        ++sub;
         __syncwarp();
         uint64_t mword = 0;
         const uint64_t min = EPI == kEpiMask ? mk[j] : 0ull;
@@ -398,8 +416,7 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
         if (EPI == kEpiRelu && p.mask_out && row_ok) p.mask_out[mrow + (size_t)j * p.Cm] = mword;
         fence_proxy_async_smem();
         __syncwarp();
-        int x0, x1, x2;
-        box_of(t, c0, x0, x1, x2);
+        const int x0 = n0 + c0, x1 = rbase, x2 = WGRAD ? se : p.seg0 + se;
         int sidx = 0, dseg = 0;
         if (!WGRAD && p.has_pmaps) {  // fused combine all-to-all: the owner of this segment
           const int el = x2 % p.El, c = x2 / (p.El * p.dP);
@@ -501,15 +518,19 @@ static void row_dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
                          const CUtensorMap& mx, const TcParams& p, bool b_kmajor, int epi, int grid,
                          cudaStream_t s) {
   // The ReLU / mask epilogues: LINA_GEMM_WIDE=0 (4 warps, 6-stage ring), 1 (8 warps,
-  // 5 stages, double-buffered boxes; default), 2 (8 warps, 6 stages, single-buffered boxes).
-  // (LINA_GEMM_NARROW=1 = LINA_GEMM_WIDE=0, kept for the round-2 A/B lines.)
-  static const int wide = [] {
+  // 5 stages, double-buffered boxes), 2 (8 warps, 6 stages, single-buffered boxes).
+  // Default (profiles/r02_gemm_epilogue_ab.txt, ncu cycles per launch): 4 warps, except the
+  // ReLU GEMM at K < 1536 (C2's K = 768: 12 K-blocks per 256 x 256 tile, the epilogue is
+  // then heavy enough per flop to want 8 warps, WIDE = 2 -3.5%); at C5 (K = 2048) 4 warps
+  // beat 8 by 2-6%.  (LINA_GEMM_NARROW=1 = LINA_GEMM_WIDE=0, kept for the round-2 A/B lines.)
+  static const int wide_env = [] {
     const char* n = getenv("LINA_GEMM_NARROW");
     if (n && n[0] == '1') return 0;
     const char* e = getenv("LINA_GEMM_WIDE");
     if (e && (e[0] == '0' || e[0] == '1' || e[0] == '2')) return e[0] - '0';
-    return 1;
+    return -1;
   }();
+  const int wide = wide_env >= 0 ? wide_env : (epi == kEpiRelu && p.K < 1536) ? 2 : 0;
   if (b_kmajor) {
     if (epi == kEpiRelu && wide == 0) launch<CG, false, false, kEpiRelu, 0>(ma, mb, md, mx, p, grid, s);
     else if (epi == kEpiRelu && wide == 1) launch<CG, false, false, kEpiRelu, 1>(ma, mb, md, mx, p, grid, s);
@@ -625,6 +646,11 @@ static void row_gemm_tc_impl_t(const RowGemm& g, bool b_kmajor, int epi, const P
   p.mask_out = g.mask_out;
   p.mask_in = g.mask_in;
   p.row_base = g.row_base;
+  if (CG == 2 && g.half_tails && !g.row_base) {  // <= 128-row last tiles as M = 128 pair tiles
+    const uint32_t abox64[3] = {BK, 64, 1};
+    p.tmA64 = make_map(g.A, 3, adims, astr, abox64);
+    p.half = 1;
+  }
   if (g.sig) p.sig = *g.sig;
   if (g.src_wait && !ps) {
     if (g.src_P > 32) throw CudaError{"split dispatch: at most 32 ranks"};

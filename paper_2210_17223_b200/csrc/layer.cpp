@@ -59,6 +59,11 @@ Plan make_plan(const lina_moe_desc& dsc, int world) {
     // 0.890 ms); at C5 the two roughly cancel (profiles/r02_tail_split_ab.txt).
     const char* ts = getenv("LINA_TAIL128");
     p.tail_split = p.bf16 && p.tile_rows == 256 && (ts && ts[0] == '1') && !getenv("LINA_FORCE_SIMT");
+    // half tails: the same saving without the second launch — a segment's last <= 128 rows
+    // as an M = 128 cta_group::2 tile inside the 256-row launch (gemm_tc.cu); LINA_HALF128=0|1
+    const char* ht = getenv("LINA_HALF128");
+    p.half_tails = p.bf16 && p.tile_rows == 256 && !p.tail_split && !(ht && ht[0] == '0') &&
+                   !getenv("LINA_FORCE_SIMT");
   }
   const size_t T = p.T, k = p.k, E = p.E;
   size_t o = 0;
@@ -299,6 +304,7 @@ void row_gemm(const Plan& p, const void* A, const void* B, void* D, const void* 
     g.src_me = src_me;
   }
   g.tile_rows = p.tile_rows;
+  g.half_tails = p.half_tails;
   g.sig = sig;
   g.mask_out = mask_out;
   g.mask_in = mask_in;
@@ -569,6 +575,7 @@ RowGemm peer_gemm(const Plan& p, const void* A, const void* B, void* D, const in
                   int N, int K) {
   RowGemm g{};
   g.tile_rows = p.tile_rows;
+  g.half_tails = p.half_tails;
   g.mtp = mtp + (size_t)c * (p.P * p.El + 1);
   g.A = A;
   g.B = B;
@@ -853,6 +860,7 @@ ncclComm_t group_comm(lina_comm* cm, int m) {
 RowGemm dl_gemm(const Plan& p, const Ptrs& q, const void* A, const void* B, void* D, int N, int K) {
   RowGemm g{};
   g.tile_rows = p.tile_rows;
+  g.half_tails = p.half_tails;
   g.A = A;
   g.B = B;
   g.D = D;

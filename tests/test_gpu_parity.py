@@ -240,16 +240,19 @@ def test_two_layers_interleaved_fwd_fwd_bwd_bwd():
         assert moe.normwise_error(dw2, o["bw"].dW2) <= tol, n
 
 
-@pytest.mark.parametrize("tail", ["0", "1"])
-def test_c5_shapes_fwd_bwd_two_cta_tiles(tail, monkeypatch):
+@pytest.mark.parametrize("tail,half", [("0", "1"), ("0", "0"), ("1", "0")])
+def test_c5_shapes_fwd_bwd_two_cta_tiles(tail, half, monkeypatch):
     """configs[4] layer dims (d=2048, f=8192, top-2, capacity 1.25) with 16 experts at 1024
     tokens: 128 rows per expert segment (> 96), so the expert GEMMs run the 2-CTA 256-row
     tiles the C5 bench runs, with K = 8192 in GEMM2 / dgrad2 and M = 2048 / 8192 in the
     wgrads; forward and backward against the oracle, without and with the opt-in tail split
-    (LINA_TAIL128=1: a segment's last <= 128 rows as single-CTA tiles in a second launch).
+    (LINA_TAIL128=1: a segment's last <= 128 rows as single-CTA tiles in a second launch),
+    and with / without the half tails (LINA_HALF128, default on: a segment's last <= 128
+    rows as an M = 128 cta_group::2 tile in the same launch, the 2x2 TMEM layout).
     (All 64 experts at full C5 would need the oracle's fp64 weight gradients, 34 GB; the
     forward at E = 64 is the test above.)"""
     monkeypatch.setenv("LINA_TAIL128", tail)
+    monkeypatch.setenv("LINA_HALF128", half)
     cfg, X, Wg, W1, W2, dY = _case("C5", tokens=1024, num_experts=16)
     assert cfg.tokens_per_rank * cfg.k / cfg.num_experts > 96
     g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY)
