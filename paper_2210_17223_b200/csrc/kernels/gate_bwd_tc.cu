@@ -173,54 +173,62 @@ __global__ void __launch_bounds__(kDxThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // producer and MMA warps walk the token blocks warp-converged; one elected lane issues
   if (warp == 0) {
-    if (lane == 0) {
+    if (elect_one()) {
       mbar_expect_tx(wfull, 2 * kDxB);
       tma_load_3d<1>(sw, &tmW, wfull, 0, n0, 0);          // Wg hi
       tma_load_3d<1>(sw + kDxB, &tmW, wfull, 0, n0, 1);   // Wg mid
-      int st = 0;
-      uint32_t ph = 0;
-      for (int tb = tb0; tb < ntb; tb += per) {
-        mbar_wait(&empty[st], ph ^ 1);
-        uint8_t* dst = sl + st * 2 * kDxA;
+    }
+    __syncwarp();
+    int st = 0;
+    uint32_t ph = 0;
+    for (int tb = tb0; tb < ntb; tb += per) {
+      mbar_wait(&empty[st], ph ^ 1);
+      uint8_t* dst = sl + st * 2 * kDxA;
+      if (elect_one()) {
         mbar_expect_tx(&full[st], 2 * kDxA);
         tma_load_3d<1>(dst, &tmL, &full[st], 0, tb * 128, 0);          // dL hi
         tma_load_3d<1>(dst + kDxA, &tmL, &full[st], 0, tb * 128, 1);   // dL mid
-        if (++st == kDxStages) {
-          st = 0;
-          ph ^= 1;
-        }
+      }
+      __syncwarp();
+      if (++st == kDxStages) {
+        st = 0;
+        ph ^= 1;
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(128, 256, false, false);
-      mbar_wait(wfull, 0);
-      const uint32_t wa = smem_u32(sw), wm = wa + kDxB;
-      int st = 0, acc = 0;
-      uint32_t ph = 0, aph = 0;
-      for (int tb = tb0; tb < ntb; tb += per) {
-        mbar_wait(&tempty[acc], aph ^ 1);
-        mbar_wait(&full[st], ph);
-        tc_fence_after();
-        const uint32_t la = smem_u32(sl + st * 2 * kDxA), lm = la + kDxA;
-        const uint32_t dt = tmem + acc * 256;
+    constexpr uint32_t idesc = idesc_bf16(128, 256, false, false);
+    mbar_wait(wfull, 0);
+    const uint32_t wa = smem_u32(sw), wm = wa + kDxB;
+    const uint64_t wad = sdesc(wa, 16, 1024), wmd = sdesc(wm, 16, 1024);
+    int st = 0, acc = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int tb = tb0; tb < ntb; tb += per) {
+      mbar_wait(&tempty[acc], aph ^ 1);
+      mbar_wait(&full[st], ph);
+      tc_fence_after();
+      const uint32_t la = smem_u32(sl + st * 2 * kDxA), lm = la + kDxA;
+      const uint64_t lad = sdesc(la, 16, 1024), lmd = sdesc(lm, 16, 1024);
+      const uint32_t dt = tmem + acc * 256;
+      if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < kEP / 16; ++kk) {
-          mma_bf16<1>(dt, sdesc(la + kk * 32, 16, 1024), sdesc(wa + kk * 32, 16, 1024), idesc, kk ? 1u : 0u);
-          mma_bf16<1>(dt, sdesc(la + kk * 32, 16, 1024), sdesc(wm + kk * 32, 16, 1024), idesc, 1u);
-          mma_bf16<1>(dt, sdesc(lm + kk * 32, 16, 1024), sdesc(wa + kk * 32, 16, 1024), idesc, 1u);
+        for (int kk = 0; kk < kEP / 16; ++kk) {  // +32 B per K = 16 step
+          mma_bf16<1>(dt, lad + 2 * kk, wad + 2 * kk, idesc, kk ? 1u : 0u);
+          mma_bf16<1>(dt, lad + 2 * kk, wmd + 2 * kk, idesc, 1u);
+          mma_bf16<1>(dt, lmd + 2 * kk, wad + 2 * kk, idesc, 1u);
         }
         mma_commit<1>(&empty[st]);
         mma_commit<1>(&tfull[acc]);
-        if (++st == kDxStages) {
-          st = 0;
-          ph ^= 1;
-        }
-        if (++acc == 2) {
-          acc = 0;
-          aph ^= 1;
-        }
+      }
+      __syncwarp();
+      if (++st == kDxStages) {
+        st = 0;
+        ph ^= 1;
+      }
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
       }
     }
   } else {  // epilogue: thread = token row; + the k returned expert input-gradient rows
@@ -355,49 +363,52 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // producer and MMA warps walk the K blocks warp-converged; one elected lane issues
   if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t ph = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int t = ta + kb * 64;  // (rows past T are zero-filled by the maps)
-        mbar_wait(&empty[stage], ph ^ 1);
-        uint8_t* sa = smem + stage * kDwStage;
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int t = ta + kb * 64;  // (rows past T are zero-filled by the maps)
+      mbar_wait(&empty[stage], ph ^ 1);
+      uint8_t* sa = smem + stage * kDwStage;
+      if (elect_one()) {
         mbar_expect_tx(&full[stage], kDwStage);
         tma_load_2d<1>(sa, &tmX, &full[stage], m0, t);
         tma_load_2d<1>(sa + 8192, &tmX, &full[stage], m0 + 64, t);
 #pragma unroll
         for (int q = 0; q < 3; ++q) tma_load_3d<1>(sa + kDwA + q * 8192, &tmL, &full[stage], 0, t, q);
-        if (++stage == kDwStages) {
-          stage = 0;
-          ph ^= 1;
-        }
+      }
+      __syncwarp();
+      if (++stage == kDwStages) {
+        stage = 0;
+        ph ^= 1;
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(128, kEP, true, true);  // both operands MN-major
-      int stage = 0;
-      uint32_t ph = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&full[stage], ph);
-        tc_fence_after();
-        const uint32_t sa = smem_u32(smem + stage * kDwStage);
-        const uint32_t sb = sa + kDwA;
+    constexpr uint32_t idesc = idesc_bf16(128, kEP, true, true);  // both operands MN-major
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      mbar_wait(&full[stage], ph);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + stage * kDwStage);
+      const uint64_t ad = sdesc(sa, 8192, 1024), bd = sdesc(sa + kDwA, 8192, 1024);
+      if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-          for (int q = 0; q < 3; ++q)
-            mma_bf16<1>(tmem, sdesc(sa + kk * 2048, 8192, 1024), sdesc(sb + q * 8192 + kk * 2048, 8192, 1024), idesc,
-                        (kb | kk | q) ? 1u : 0u);
+          for (int q = 0; q < 3; ++q)  // +2 KB per K = 16 step, +8 KB per dL term
+            mma_bf16<1>(tmem, ad + 128 * kk, bd + 512 * q + 128 * kk, idesc, (kb | kk | q) ? 1u : 0u);
         mma_commit<1>(&empty[stage]);
-        if (++stage == kDwStages) {
-          stage = 0;
-          ph ^= 1;
-        }
       }
-      mma_commit<1>(tfull);  // (arrives at once when the split is empty)
+      __syncwarp();
+      if (++stage == kDwStages) {
+        stage = 0;
+        ph ^= 1;
+      }
     }
+    if (elect_one()) mma_commit<1>(tfull);  // (arrives at once when the split is empty)
+    __syncwarp();
   } else {
     const int quarter = warp & 3;
     const int c = m0 + quarter * 32 + lane;  // output row = column of d

@@ -105,46 +105,50 @@ __global__ void __launch_bounds__(kGThreads, 2)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
-      int stage = 0;
-      uint32_t ph = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&empty[stage], ph ^ 1);
-        uint8_t* sa = smem + stage * G::STAGE;
+  // producer and MMA warps walk the K blocks warp-converged (operands in uniform registers);
+  // one elected lane issues the loads / MMAs
+  if (warp == 0) {  // ---- TMA producer
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      mbar_wait(&empty[stage], ph ^ 1);
+      uint8_t* sa = smem + stage * G::STAGE;
+      if (elect_one()) {
         mbar_expect_tx(&full[stage], G::STAGE);
         tma_load_2d<1>(sa, &tmX, &full[stage], kb * kGBK, m0);
         tma_load_2d<1>(sa + G::A_BYTES, &tmW, &full[stage], kb * kGBK, 0);
-        if (++stage == kGStages) {
-          stage = 0;
-          ph ^= 1;
-        }
+      }
+      __syncwarp();
+      if (++stage == kGStages) {
+        stage = 0;
+        ph ^= 1;
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer: hi, mid and lo products into one accumulator
-      constexpr uint32_t idesc = idesc_bf16(128, EP, false, false);
-      int stage = 0;
-      uint32_t ph = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&full[stage], ph);
-        tc_fence_after();
-        const uint32_t sa = smem_u32(smem + stage * G::STAGE);
-        const uint32_t sb = sa + G::A_BYTES;
+  } else if (warp == 1) {  // ---- MMA issuer: hi, mid and lo products into one accumulator
+    constexpr uint32_t idesc = idesc_bf16(128, EP, false, false);
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      mbar_wait(&full[stage], ph);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + stage * G::STAGE);
+      const uint64_t ad = sdesc(sa, 16, 1024), bd = sdesc(sa + G::A_BYTES, 16, 1024);
+      if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < kGBK / 16; ++kk)
 #pragma unroll
-          for (int q = 0; q < 3; ++q)
-            mma_bf16<1>(tmem, sdesc(sa + kk * 32, 16, 1024), sdesc(sb + q * EP * 128 + kk * 32, 16, 1024), idesc,
-                        (kb | kk | q) ? 1u : 0u);
+          for (int q = 0; q < 3; ++q)  // +32 B per K = 16 step, +EP rows x 128 B per term
+            mma_bf16<1>(tmem, ad + 2 * kk, bd + 2 * kk + q * EP * 8, idesc, (kb | kk | q) ? 1u : 0u);
         mma_commit<1>(&empty[stage]);
-        if (++stage == kGStages) {
-          stage = 0;
-          ph ^= 1;
-        }
       }
-      mma_commit<1>(tfull);
+      __syncwarp();
+      if (++stage == kGStages) {
+        stage = 0;
+        ph ^= 1;
+      }
     }
+    if (elect_one()) mma_commit<1>(tfull);
+    __syncwarp();
   } else {  // ---- epilogue: one token per thread
     const int quarter = warp & 3;
     const int t = m0 + quarter * 32 + lane;

@@ -201,11 +201,16 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
   };
 
   if (warp == 0) {
-    // ================= TMA producer (both CTAs load their own halves)
-    if (lane == 0) {
+    // ================= TMA producer (both CTAs load their own halves): the whole warp walks
+    // the tiles and waits (warp-uniform, operands in uniform registers); one elected lane
+    // issues the loads
+    {
       if (p.sig.wait && !p.src_wait) {  // fused transport: the peers' rows of A have landed
-        sig_wait(p.sig);
-        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (elect_one()) {
+          sig_wait(p.sig);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncwarp();
       }
       uint32_t have = 1u << p.dme;  // split dispatch: sources whose rows are known to be in
       int stage = 0;
@@ -220,6 +225,7 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
           mbar_wait(&empty[stage], ph ^ 1);
           uint8_t* sa = smem + stage * G::STAGE_BYTES;
           uint8_t* sb = sa + G::A_BYTES;
+          if (elect_one()) {
           if (leader) mbar_expect_tx(&full[stage], CG * (hf ? G::STAGE_BYTES - G::A_BYTES / 2 : G::STAGE_BYTES));
           if (!A_MN && hf) {
             tma_load_3d<CG>(sa, &p.tmA64, &full[stage], a0, a1 - 64 * (int)rank, a2);  // rows m0 + 64 * rank
@@ -240,6 +246,8 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
             for (int j = 0; j < G::B_ROWS / 64; ++j)
               tma_load_3d<CG>(sb + j * 8192, &tmB, &full[stage], b0 + j * 64, b1, b2);
           }
+          }
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             ph ^= 1;
@@ -250,8 +258,11 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
           if (p.src_wait) {
             const int src = (seg / p.El) % p.dP;
             if (!((have >> src) & 1u)) {
-              sig_wait_one(p.sig, src);
-              asm volatile("fence.proxy.async.global;" ::: "memory");
+              if (elect_one()) {
+                sig_wait_one(p.sig, src);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+              }
+              __syncwarp();
               have |= 1u << src;
             }
           }
@@ -280,10 +291,15 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer (leader CTA only)
-    if (leader && lane == 0) {
+    // ================= MMA issuer (leader CTA only): the whole warp walks the tiles and
+    // waits (warp-uniform control flow, operands in uniform registers); one elected lane
+    // issues the MMAs and commits.  Per 64-deep K block the stage's descriptors are built
+    // once and advanced per K = 16 step by a constant (+32 B K-major, +2 KB MN-major).
+    if (leader) {
       constexpr uint32_t idesc_full = idesc_bf16(G::ROWS, BN, A_MN, B_MN);
       constexpr uint32_t idesc_half = idesc_bf16(128, BN, A_MN, B_MN);
+      constexpr uint64_t a_step = A_MN ? 2048 >> 4 : 32 >> 4, b_step = B_MN ? 2048 >> 4 : 32 >> 4;
+      const uint32_t smem0 = smem_u32(smem);
       int stage = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -299,23 +315,26 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], ph);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * G::STAGE_BYTES);
+          const uint32_t sa = smem0 + stage * G::STAGE_BYTES;
           const uint32_t sb = sa + G::A_BYTES;
+          // K-major SW128: +32 B per K=16 step inside the 128 B atom; SBO = 8 rows * 128 B.
+          // MN-major SW128: +2 x (8 K-rows * 128 B) per K=16 step; LBO = 64-element MN block.
+          const uint64_t ad = A_MN ? sdesc(sa, 8192, 1024) : sdesc(sa, 16, 1024);
+          const uint64_t bd = B_MN ? sdesc(sb, 8192, 1024) : sdesc(sb, 16, 1024);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            // K-major SW128: +32 B per K=16 step inside the 128 B atom; SBO = 8 rows * 128 B.
-            // MN-major SW128: +2 x (8 K-rows * 128 B) per K=16 step; LBO = 64-element MN block.
-            const uint64_t ad = A_MN ? sdesc(sa + kk * 2048, 8192, 1024) : sdesc(sa + kk * 32, 16, 1024);
-            const uint64_t bd = B_MN ? sdesc(sb + kk * 2048, 8192, 1024) : sdesc(sb + kk * 32, 16, 1024);
-            mma_bf16<CG>(d_tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+            for (int kk = 0; kk < BK / 16; ++kk)
+              mma_bf16<CG>(d_tmem, ad + a_step * kk, bd + b_step * kk, idesc, (kb | kk) ? 1u : 0u);
+            mma_commit<CG>(&empty[stage]);  // frees the smem slot (in both CTAs) once read
           }
-          mma_commit<CG>(&empty[stage]);  // frees the smem slot (in both CTAs) once read
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             ph ^= 1;
           }
         }
-        mma_commit<CG>(&tfull[acc]);  // accumulator ready (arrives at once if nkb == 0)
+        if (elect_one()) mma_commit<CG>(&tfull[acc]);  // accumulator ready (arrives at once if nkb == 0)
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           aph ^= 1;
