@@ -274,6 +274,13 @@ lina_comm* comm_base(int world, int rank, int cuda_device) {
   LINA_CUDA_CHECK(cudaStreamCreateWithPriority(&cm->lo, cudaStreamNonBlocking, lo_prio));
   LINA_CUDA_CHECK(cudaMalloc(&cm->route_sync, sizeof(unsigned int) * route_sync_words()));
   LINA_CUDA_CHECK(cudaMemset(cm->route_sync, 0, sizeof(unsigned int) * route_sync_words()));
+  {  // dynamic tile schedule of the expert GEMMs (gemm_tc.cu): LINA_GEMM_DYN=0 keeps the static one
+    const char* dv = getenv("LINA_GEMM_DYN");
+    if (!(dv && dv[0] == '0')) {
+      LINA_CUDA_CHECK(cudaMalloc(&cm->tile_ctr, sizeof(unsigned int)));
+      LINA_CUDA_CHECK(cudaMemset(cm->tile_ctr, 0, sizeof(unsigned int)));
+    }
+  }
   cm->ev.resize(128);
   for (auto& e : cm->ev) LINA_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   const char* trv = getenv("LINA_TRACE");
@@ -398,6 +405,10 @@ lina_status lina_comm_destroy(lina_comm* cm) {
     for (auto e : cm->prof_pool) cudaEventDestroy(e);
     if (cm->pinned) cudaFreeHost(cm->pinned);
     if (cm->route_sync) cudaFree(cm->route_sync);
+    if (cm->tile_ctr) {
+      tc_set_tile_counter(nullptr);
+      cudaFree(cm->tile_ctr);
+    }
     delete cm;
     return LINA_OK;
   });
@@ -620,6 +631,7 @@ lina_status lina_moe_forward(lina_comm* cm, const lina_moe_desc* desc, const voi
       throw StatusError{LINA_ERR_WORKSPACE, "workspace_bytes " + std::to_string(workspace_bytes) +
                                                 " < required " + std::to_string(p.ws_bytes)};
     LINA_CUDA_CHECK(cudaSetDevice(cm->device));
+    tc_set_tile_counter(cm->tile_ctr);
     moe_forward(cm, p, tokens, gate_w, w1, w2, out, saved, workspace, route, (cudaStream_t)stream);
     return LINA_OK;
   });
@@ -655,6 +667,7 @@ lina_status lina_moe_backward(lina_comm* cm, const lina_moe_desc* desc, const vo
       throw StatusError{LINA_ERR_WORKSPACE, "workspace_bytes " + std::to_string(workspace_bytes) +
                                                 " < required " + std::to_string(p.ws_bytes)};
     LINA_CUDA_CHECK(cudaSetDevice(cm->device));
+    tc_set_tile_counter(cm->tile_ctr);
     moe_backward(cm, p, saved, dout, tokens, gate_w, w1, w2, dtokens, dgate_w, dw1, dw2, workspace,
                  (cudaStream_t)stream);
     return LINA_OK;
@@ -714,6 +727,7 @@ static lina_status infer_entry(lina_comm* cm, const lina_moe_desc* desc, const v
     if (workspace_bytes < infer_workspace_bytes(*desc, cm->world, mpd))
       throw StatusError{LINA_ERR_WORKSPACE, "workspace_bytes < lina_moe_infer_workspace_size"};
     LINA_CUDA_CHECK(cudaSetDevice(cm->device));
+    tc_set_tile_counter(cm->tile_ctr);
     infer_forward(cm, *desc, tokens, gate_w, w1_all, w2_all, out, placement, max_per_device,
                   plan_out, workspace, workspace_bytes, (cudaStream_t)stream, estimated, replanned);
     return LINA_OK;
@@ -771,6 +785,7 @@ lina_status lina_pack_weights(lina_comm* cm, int32_t num_experts, int32_t pack_f
     if (P > 1 && !cm->ce) v.push_back("world > 1 needs the fused or ce transport (peer mappings)");
     raise_if(v, "lina_pack_weights");
     LINA_CUDA_CHECK(cudaSetDevice(cm->device));
+    tc_set_tile_counter(cm->tile_ctr);
     pack_weights(cm, num_experts, pack_from, pack_to, expert_elems * (dtype == LINA_BF16 ? 2 : 4), w_from, w_to,
                  (cudaStream_t)stream);
     return LINA_OK;
@@ -811,6 +826,7 @@ lina_status lina_allreduce_submit(lina_comm* cm, void* grad, size_t count, lina_
       throw StatusError{LINA_ERR_UNSUPPORTED, "allreduce needs an NCCL communicator (lina_comm_init)"};
     if (count == 0 || !cm->sched) return LINA_OK;  // world == 1: the sum over one rank is itself
     LINA_CUDA_CHECK(cudaSetDevice(cm->device));
+    tc_set_tile_counter(cm->tile_ctr);
     sched_submit(cm->sched, grad, count, dtype, (cudaStream_t)ready_stream);
     return LINA_OK;
   });

@@ -76,6 +76,7 @@ struct Trace;
 
 struct lina_comm {
   int rank = 0, world = 1, device = 0, num_sms = 148;
+  unsigned int* tile_ctr = nullptr;  // expert-GEMM dynamic tile counter (LINA_GEMM_DYN; self-resetting)
   ncclComm_t ep_disp = nullptr;  // dispatch-direction all-to-all micro-ops
   ncclComm_t ep_comb = nullptr;  // combine-direction all-to-all micro-ops (full-duplex, H8)
   ncclComm_t dp = nullptr;       // non-expert gradient allreduce micro-ops

@@ -125,6 +125,8 @@ constexpr int kTcCtaGroup = 2;
 int tc_tile_rows();
 // SMs the persistent GEMM grid leaves free for concurrently running NCCL kernels.
 void tc_set_reserved_sms(int n);
+// The dynamic tile-schedule counter of the calling communicator (NULL: static schedule).
+void tc_set_tile_counter(unsigned int* ctr);
 // mtp[c][i] = Σ_{i' < i} ceil(vcount[c*nseg + i'] / rows), i in [0, nseg]  (tcgen05 tile lists)
 void launch_mtile_prefix(const int* vcount, int n, int nseg, int rows, int* mtp, cudaStream_t s);
 // the tail-split lists: mtp[c][nseg+1] (256-row tiles, a last tile only when it holds > 128

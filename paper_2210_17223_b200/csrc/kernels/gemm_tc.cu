@@ -97,7 +97,16 @@ struct TcParams {
   // CTA, columns [0, 128) in TMEM lanes 0-63 and [128, 256) in lanes 64-127, 128 columns).
   int half;
   CUtensorMap tmA64;
+  // Dynamic tile schedule (NULL: static, cluster c takes tiles c, c + #clusters, ...): the
+  // leader CTA's producer takes the next tile from this counter and hands it to its MMA and
+  // epilogue warps and to the peer CTA through a 4-deep shared-memory queue, so the tiles in
+  // flight stay a contiguous window whatever their lengths (half tails, unequal wgrad K) and
+  // the clusters reuse each other's operands from L2.  The cluster drawing the last ticket
+  // (#tiles + #clusters - 1) resets the counter to 0 for the next launch (stream order).
+  unsigned int* tile_ctr;
 };
+
+constexpr int kQ = 4;  // tile-queue depth
 
 template <int CG, bool WGRAD, bool B_MN, int EPI, int WIDE = (EPI != kEpiNone)>
 __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
@@ -125,7 +134,8 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
   // ---- tile space (per cluster)
   const int n_nblk = p.N / BN;
   const int total_tiles = WGRAD ? p.El * (p.M / G::ROWS) * n_nblk : p.mtp[p.nseg] * n_nblk;
-  if (cluster_id >= total_tiles) {  // uniform for the whole cluster
+  const bool dyn = p.tile_ctr != nullptr;
+  if (!dyn && cluster_id >= total_tiles) {  // uniform for the whole cluster
     if (threadIdx.x == 0) sig_post_last(p.sig);  // still counts towards the grid's completion
     return;
   }
@@ -144,6 +154,10 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
       mbar_init(&tempty[a], G::EPW * CG);
     }
     for (int a = 0; a < 16; ++a) mbar_init(tempty + 3 + a, 1);  // epilogue aux-box barriers
+    for (int a = 0; a < kQ; ++a) {  // tile queue: one producer; leader MMA + producer of the peer + all epilogue warps
+      mbar_init(tempty + 19 + a, 1);
+      mbar_init(tempty + 19 + kQ + a, (CG == 2 ? 2 : 1) + CG * G::EPW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc<CG>(tmem_base_slot, TMEM_COLS);
@@ -152,6 +166,46 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  uint64_t* qfull = tempty + 19;
+  uint64_t* qempty = qfull + kQ;
+  volatile int* tq = (volatile int*)(qempty + kQ);
+  // the i-th tile of this cluster: static, or from the queue (the leader producer fills it)
+  // leader producer: publish ticket t (drawn earlier, in flight during the previous tile's
+  // loads) to the queue of both CTAs
+  auto q_publish = [&](int& qi, uint32_t& qph, int t) {
+    mbar_wait(&qempty[qi], qph ^ 1);  // (acquire.cta: an acquire.cluster wait invalidates L1 — the tile decode's cached loads)
+    if (lane == 0) {
+      tq[qi] = t;
+      if (CG == 2) st_cluster_s32((const void*)&tq[qi], 1, t);
+      mbar_arrive_local(&qfull[qi]);
+      if (CG == 2) mbar_arrive_cluster_rel(&qfull[qi], 1);
+      if (t == total_tiles + num_clusters - 1) atomicExch(p.tile_ctr, 0u);  // the last ticket
+    }
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (++qi == kQ) {
+      qi = 0;
+      qph ^= 1;
+    }
+    return t;
+  };
+  auto q_draw = [&]() { return lane == 0 ? (int)atomicAdd(p.tile_ctr, 1u) : 0; };
+  auto q_take = [&](int& qi, uint32_t& qph) {
+    mbar_wait(&qfull[qi], qph);  // the ticket sits in this CTA's shared memory (written before the release-arrive)
+    const int t = tq[qi];
+    __syncwarp();
+    if (lane == 0) {
+      if (rank == 0) mbar_arrive_local(&qempty[qi]);
+      else mbar_arrive_cluster_rel(&qempty[qi], 0);
+    }
+    if (++qi == kQ) {
+      qi = 0;
+      qph ^= 1;
+    }
+    return t;
+  };
+  auto next_tile = [&](int it, int& qi, uint32_t& qph) {
+    return dyn ? q_take(qi, qph) : cluster_id + it * num_clusters;
+  };
 
   // Fused combine stores: every rank starts at the tiles of source (me + 1) % P, so at any
   // moment the P ranks write to P different owners (no incast on one rank's links).
@@ -217,7 +271,15 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
       uint32_t ph = 0;
       const int arow = 128 * rank;          // this CTA's rows within the tile
       const int brow = G::B_ROWS * rank;    // this CTA's B (N) rows within the tile
-      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+      int qi = 0;
+      uint32_t qph = 0;
+      // dynamic schedule, leader: the next tile's ticket is drawn when this tile starts and
+      // published when its loads are issued (the atomic's latency hides behind them)
+      int t_next = dyn && leader ? q_publish(qi, qph, q_draw()) : 0;
+      for (int it = 0;; ++it) {
+        const int t = !dyn ? cluster_id + it * num_clusters : leader ? t_next : q_take(qi, qph);
+        if (t >= total_tiles) break;
+        const int drawn = dyn && leader ? q_draw() : 0;
         int se, m0, n0;
         decode(t, se, m0, n0);
         const bool hf = !WGRAD && half_of(se, m0);
@@ -288,6 +350,7 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
               }
           }
         }
+        if (dyn && leader) t_next = q_publish(qi, qph, drawn);
       }
     }
   } else if (warp == 1) {
@@ -304,7 +367,11 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+      int qi = 0;
+      uint32_t qph = 0;
+      for (int it = 0;; ++it) {
+        const int t = next_tile(it, qi, qph);
+        if (t >= total_tiles) break;
         int se, m0, n0;
         decode(t, se, m0, n0);
         const int nkb = kblocks_of(se);
@@ -358,7 +425,11 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
     uint32_t aph = 0;
     int sub = 0;  // sub-tile counter (buffer = sub & 1)
     const int mwords = p.N >> 6;
-    for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+    int qi = 0;
+    uint32_t qph = 0;
+    for (int it = 0;; ++it) {
+      const int t = next_tile(it, qi, qph);
+      if (t >= total_tiles) break;
       int se, m0, n0;
       decode(t, se, m0, n0);
       const int nkb = kblocks_of(se);
@@ -490,6 +561,23 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
 
 // ------------------------------------------------------------------ host side
 static int g_reserved_sms = 0;  // SMs left to concurrent NCCL kernels (H2 in SURVEY.md)
+// The calling communicator's tile counter (dynamic schedule; NULL = static): set by every
+// layer entry point; the GEMMs of one communicator are stream-ordered on its caller's stream.
+static thread_local unsigned int* t_tile_ctr = nullptr;
+// Which GEMMs take the dynamic schedule (K = -1: wgrad).  Measured at C5 / C2 (tools/gpu_r02c_9.sh,
+// profiles/r02_gemm_dyn_ab.txt): the long-K row GEMMs (GEMM2 / dgrad2 at C5, K = 8192, 128
+// K-blocks per tile) gain 13% — the static order lets clusters drift apart (half tails end
+// early) until the tiles in flight span several experts' weights and L2 thrashes (8.4 GB of
+// DRAM reads per launch instead of 3.7) — while the short-K GEMMs (12-32 K-blocks, and the
+// wgrads) lose 2-20% to the per-tile queue hand-off.  LINA_GEMM_DYN=2 forces it everywhere
+// (A/B only), =0 (read at comm init) disables it.
+static bool dyn_schedule(int K) {
+  static const bool all = [] {
+    const char* e = getenv("LINA_GEMM_DYN");
+    return e && e[0] == '2';
+  }();
+  return all || K >= 64 * BK;
+}
 
 // SMs the persistent GEMM grid may occupy.  A persistent grid that takes every SM
 // would leave the all-to-all kernels nothing to run on (they would serialise after
@@ -568,6 +656,7 @@ static void row_dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
 }  // namespace tc
 
 void tc_set_reserved_sms(int n) { tc::g_reserved_sms = n < 0 ? 0 : n; }
+void tc_set_tile_counter(unsigned int* ctr) { tc::t_tile_ctr = ctr; }
 
 // Rows per tensor-core tile (the m-block granularity launch_mtile_prefix must use).
 int tc_tile_rows() { return 128 * kTcCtaGroup; }
@@ -671,6 +760,7 @@ static void row_gemm_tc_impl_t(const RowGemm& g, bool b_kmajor, int epi, const P
     p.half = 1;
   }
   if (g.sig) p.sig = *g.sig;
+  p.tile_ctr = dyn_schedule(g.K) ? t_tile_ctr : nullptr;
   if (g.src_wait && !ps) {
     if (g.src_P > 32) throw CudaError{"split dispatch: at most 32 ranks"};
     p.src_wait = 1;
@@ -719,6 +809,7 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s) {
   p.P = g.P;
   p.seg_range = g.seg_range;
   p.D = (__nv_bfloat16*)g.D;
+  p.tile_ctr = dyn_schedule(-1) ? t_tile_ctr : nullptr;
   const int tiles = g.El * (g.M / Geo<CG>::ROWS) * (g.N / BN);
   const int maxc = num_sms() / CG;
   const int grid = (tiles < maxc ? tiles : maxc) * CG;

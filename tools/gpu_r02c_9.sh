@@ -1,0 +1,13 @@
+# Dynamic GEMM tile schedule with CTA-scope acquire waits: A/B per-GEMM cycles (C5, C2) and benches
+set -x
+M="gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,dram__bytes_write.sum"
+for c in C5 C2; do
+for dy in 1 0; do
+  LINA_GEMM_DYN=$dy timeout 600 ncu --metrics $M --clock-control none -k regex:tc_gemm_kernel --launch-skip 12 -c 12 --csv --log-file gpurun_out/r02c9_${c}_d$dy.csv python bench.py --config $c --eager --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu $c d=$dy rc=$?"
+done
+done
+for dy in 1 0; do LINA_GEMM_DYN=$dy timeout 300 python bench.py --config C2 --no-cpu-baseline --no-e2e > gpurun_out/r02c9_bench_c2_d$dy.json 2>/dev/null; echo "c2 d=$dy rc=$?"; done
+for i in 1 2; do for dy in 1 0; do
+  LINA_GEMM_DYN=$dy timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/r02c9_bench_c5_d$dy.$i.json 2>/dev/null; echo "c5 d=$dy rc=$?"
+done; done
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "c5 or c2_full or dropless or cuda_graph" > gpurun_out/r02c9_pytest.log 2>&1; echo "pytest rc=$?"; tail -n 2 gpurun_out/r02c9_pytest.log
