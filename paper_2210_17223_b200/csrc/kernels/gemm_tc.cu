@@ -104,6 +104,7 @@ struct TcParams {
   // the clusters reuse each other's operands from L2.  The cluster drawing the last ticket
   // (#tiles + #clusters - 1) resets the counter to 0 for the next launch (stream order).
   unsigned int* tile_ctr;
+  int dyn_static;  // A/B only (LINA_GEMM_DYN=3): the queue hand-off with the static tile order
 };
 
 constexpr int kQ = 4;  // tile-queue depth
@@ -176,10 +177,9 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
     mbar_wait(&qempty[qi], qph ^ 1);  // (acquire.cta: an acquire.cluster wait invalidates L1 — the tile decode's cached loads)
     if (lane == 0) {
       tq[qi] = t;
-      if (CG == 2) st_cluster_s32((const void*)&tq[qi], 1, t);
       mbar_arrive_local(&qfull[qi]);
-      if (CG == 2) mbar_arrive_cluster_rel(&qfull[qi], 1);
-      if (t == total_tiles + num_clusters - 1) atomicExch(p.tile_ctr, 0u);  // the last ticket
+      if (CG == 2) st_async_cluster_s32((const void*)&tq[qi], &qfull[qi], 1, t);
+      if (!p.dyn_static && t == total_tiles + num_clusters - 1) atomicExch(p.tile_ctr, 0u);  // the last ticket
     }
     t = __shfl_sync(0xffffffffu, t, 0);
     if (++qi == kQ) {
@@ -188,14 +188,22 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
     }
     return t;
   };
-  auto q_draw = [&]() { return lane == 0 ? (int)atomicAdd(p.tile_ctr, 1u) : 0; };
+  int n_draw = 0;
+  auto q_draw = [&]() {
+    const int i = n_draw++;
+    if (p.dyn_static) return cluster_id + i * num_clusters;
+    return lane == 0 ? (int)atomicAdd(p.tile_ctr, 1u) : 0;
+  };
+  // consumers; in the peer CTA its producer registers the 4 bytes of each ticket's st.async
+  // (with that phase's arrival), the other consumers only wait
   auto q_take = [&](int& qi, uint32_t& qph) {
-    mbar_wait(&qfull[qi], qph);  // the ticket sits in this CTA's shared memory (written before the release-arrive)
+    if (rank != 0 && warp == 0 && lane == 0) mbar_expect_tx(&qfull[qi], 4);
+    mbar_wait(&qfull[qi], qph);
     const int t = tq[qi];
     __syncwarp();
     if (lane == 0) {
       if (rank == 0) mbar_arrive_local(&qempty[qi]);
-      else mbar_arrive_cluster_rel(&qempty[qi], 0);
+      else mbar_arrive_cluster_relaxed(&qempty[qi], 0);
     }
     if (++qi == kQ) {
       qi = 0;
@@ -571,13 +579,14 @@ static thread_local unsigned int* t_tile_ctr = nullptr;
 // DRAM reads per launch instead of 3.7) — while the short-K GEMMs (12-32 K-blocks, and the
 // wgrads) lose 2-20% to the per-tile queue hand-off.  LINA_GEMM_DYN=2 forces it everywhere
 // (A/B only), =0 (read at comm init) disables it.
-static bool dyn_schedule(int K) {
-  static const bool all = [] {
+static int dyn_env() {
+  static const int v = [] {
     const char* e = getenv("LINA_GEMM_DYN");
-    return e && e[0] == '2';
+    return e ? atoi(e) : 1;
   }();
-  return all || K >= 64 * BK;
+  return v;
 }
+static bool dyn_schedule(int K) { return dyn_env() >= 2 || K >= 64 * BK; }
 
 // SMs the persistent GEMM grid may occupy.  A persistent grid that takes every SM
 // would leave the all-to-all kernels nothing to run on (they would serialise after
@@ -761,6 +770,7 @@ static void row_gemm_tc_impl_t(const RowGemm& g, bool b_kmajor, int epi, const P
   }
   if (g.sig) p.sig = *g.sig;
   p.tile_ctr = dyn_schedule(g.K) ? t_tile_ctr : nullptr;
+  p.dyn_static = dyn_env() == 3;
   if (g.src_wait && !ps) {
     if (g.src_P > 32) throw CudaError{"split dispatch: at most 32 ranks"};
     p.src_wait = 1;
@@ -810,6 +820,7 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s) {
   p.seg_range = g.seg_range;
   p.D = (__nv_bfloat16*)g.D;
   p.tile_ctr = dyn_schedule(-1) ? t_tile_ctr : nullptr;
+  p.dyn_static = dyn_env() == 3;
   const int tiles = g.El * (g.M / Geo<CG>::ROWS) * (g.N / BN);
   const int maxc = num_sms() / CG;
   const int grid = (tiles < maxc ? tiles : maxc) * CG;

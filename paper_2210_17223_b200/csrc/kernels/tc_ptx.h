@@ -44,40 +44,35 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
       "r"(rank)
       : "memory");
 }
-// Tile-queue helpers (dynamic GEMM tile scheduler, gemm_tc.cu): cluster-scope acquire wait,
-// local arrive, remote release-arrive and a remote 32-bit shared-memory store.
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
+// Tile-queue helpers (dynamic GEMM tile scheduler, gemm_tc.cu).
 __device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_cluster_rel(uint64_t* bar, uint32_t rank) {
+// Remote arrive without release semantics: a .release.cluster arrive compiles to MEMBAR.ALL.GPU,
+// which waits for every outstanding memory operation of the thread (a producer's TMA loads in
+// flight); a consumer only has to have read its ticket, which precedes the arrive.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint64_t* bar, uint32_t rank) {
   asm volatile(
       "{\n"
       ".reg .b32 ra;\n"
       "mapa.shared::cluster.u32 ra, %0, %1;\n"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(rank)
       : "memory");
 }
-__device__ __forceinline__ void st_cluster_s32(const void* local, uint32_t rank, int v) {
+// 32-bit store into CTA `rank`'s shared memory at the offset of `local`, completing 4 bytes of
+// the transaction count of the barrier at the offset of `bar` there (st.async: no fence; the
+// receiving side registers the 4 bytes with arrive.expect_tx)
+__device__ __forceinline__ void st_async_cluster_s32(const void* local, uint64_t* bar, uint32_t rank, int v) {
   asm volatile(
       "{\n"
-      ".reg .b32 ra;\n"
-      "mapa.shared::cluster.u32 ra, %0, %1;\n"
-      "st.shared::cluster.s32 [ra], %2;\n"
+      ".reg .b32 ra, rb;\n"
+      "mapa.shared::cluster.u32 ra, %0, %2;\n"
+      "mapa.shared::cluster.u32 rb, %1, %2;\n"
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [ra], %3, [rb];\n"
       "}\n" ::"r"(smem_u32(local)),
-      "r"(rank), "r"(v)
+      "r"(smem_u32(bar)), "r"(rank), "r"(v)
       : "memory");
 }
 // One lane of a converged warp (elect.sync): the issuing lane of a warp-uniform loop, so the
