@@ -572,13 +572,15 @@ static int g_reserved_sms = 0;  // SMs left to concurrent NCCL kernels (H2 in SU
 // The calling communicator's tile counter (dynamic schedule; NULL = static): set by every
 // layer entry point; the GEMMs of one communicator are stream-ordered on its caller's stream.
 static thread_local unsigned int* t_tile_ctr = nullptr;
-// Which GEMMs take the dynamic schedule (K = -1: wgrad).  Measured at C5 / C2 (tools/gpu_r02c_9.sh,
-// profiles/r02_gemm_dyn_ab.txt): the long-K row GEMMs (GEMM2 / dgrad2 at C5, K = 8192, 128
-// K-blocks per tile) gain 13% — the static order lets clusters drift apart (half tails end
-// early) until the tiles in flight span several experts' weights and L2 thrashes (8.4 GB of
-// DRAM reads per launch instead of 3.7) — while the short-K GEMMs (12-32 K-blocks, and the
-// wgrads) lose 2-20% to the per-tile queue hand-off.  LINA_GEMM_DYN=2 forces it everywhere
-// (A/B only), =0 (read at comm init) disables it.
+// Which GEMMs take the dynamic schedule (profiles/r02_gemm_dyn_ab.txt, per-GEMM ncu A/B at C5
+// and C2).  The long-K row GEMMs (GEMM2 / dgrad2 at C5, K = 8192, 128 K-blocks per tile) gain
+// 13%: under the static order the clusters drift apart (half tails end early) until the
+// tiles in flight span several experts' weights and L2 thrashes (8.4 GB of DRAM reads per
+// launch instead of 3.7).  GEMMs of many waves (C5's GEMM1 / dgrad1 / wgrads: >= 32 tiles per
+// cluster) gain ~1% (less DRAM under the power cap); GEMMs of a few waves (C2: 3-13 tiles per
+// cluster) lose 1-5% (the ticket drawn a tile ahead worsens the last wave).  LINA_GEMM_DYN=2
+// forces it everywhere, 3 = the hand-off with the static order (A/B only), 0 (read at comm
+// init) disables it.
 static int dyn_env() {
   static const int v = [] {
     const char* e = getenv("LINA_GEMM_DYN");
@@ -586,7 +588,9 @@ static int dyn_env() {
   }();
   return v;
 }
-static bool dyn_schedule(int K) { return dyn_env() >= 2 || K >= 64 * BK; }
+static bool dyn_schedule(int K, long long tiles_max, int clusters) {
+  return dyn_env() >= 2 || K >= 64 * BK || tiles_max >= 32LL * clusters;
+}
 
 // SMs the persistent GEMM grid may occupy.  A persistent grid that takes every SM
 // would leave the all-to-all kernels nothing to run on (they would serialise after
@@ -769,7 +773,10 @@ static void row_gemm_tc_impl_t(const RowGemm& g, bool b_kmajor, int epi, const P
     p.half = 1;
   }
   if (g.sig) p.sig = *g.sig;
-  p.tile_ctr = dyn_schedule(g.K) ? t_tile_ctr : nullptr;
+  {
+    const long long mt = (long long)g.nseg * ((g.Cm + Geo<CG>::ROWS - 1) / Geo<CG>::ROWS);  // m-tiles at most
+    p.tile_ctr = dyn_schedule(g.K, mt * (g.N / BN), num_sms() / CG) ? t_tile_ctr : nullptr;
+  }
   p.dyn_static = dyn_env() == 3;
   if (g.src_wait && !ps) {
     if (g.src_P > 32) throw CudaError{"split dispatch: at most 32 ranks"};
@@ -819,7 +826,8 @@ void launch_wgrad_tc(const WGrad& g, cudaStream_t s) {
   p.P = g.P;
   p.seg_range = g.seg_range;
   p.D = (__nv_bfloat16*)g.D;
-  p.tile_ctr = dyn_schedule(-1) ? t_tile_ctr : nullptr;
+  p.tile_ctr = dyn_schedule(0, (long long)g.El * (g.M / Geo<CG>::ROWS) * (g.N / BN), num_sms() / CG) ? t_tile_ctr
+                                                                                                 : nullptr;
   p.dyn_static = dyn_env() == 3;
   const int tiles = g.El * (g.M / Geo<CG>::ROWS) * (g.N / BN);
   const int maxc = num_sms() / CG;
