@@ -22,6 +22,7 @@ import argparse
 import json
 import os
 import subprocess
+import threading
 import sys
 import time
 
@@ -148,22 +149,40 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        # Returns once nvidia-smi has produced its first sample: its NVML start-up takes driver
+        # locks that stall concurrent CUDA calls for tens of ms (at N > 1 the host-issued dWg
+        # allreduce of a step waited behind it: one 24-28 ms step in a 20-step region), so it
+        # must be done before the timed region starts.
+        self.lines = []
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
                  "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
-        time.sleep(0.25)
+        if self.proc is not None:
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 10 and self.proc.poll() is None:
+                time.sleep(0.02)
+            time.sleep(0.2)
         return self
 
+    def _read(self):
+        for line in self.proc.stdout:
+            if line.strip():
+                self.lines.append(line)
+
     def __exit__(self, *a):
-        self.lines = []
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
-            out, _ = self.proc.communicate(timeout=10)
-            self.lines = [l for l in out.splitlines() if l.strip()]
+            try:
+                self.proc.wait(timeout=10)
+            except Exception:
+                self.proc.kill()
+            self.reader.join(timeout=5)
 
     def summary(self):
         sm, mx, reasons = [], [], set()
@@ -357,9 +376,9 @@ def main():
     progress(f"launch mode: {launch_mode}")
     # ---------------- timed region (device time, per-step events, L2 flushed between steps)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    barrier()
-    torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
+        barrier()
+        torch.cuda.synchronize()
         h0 = time.perf_counter()
         for i in range(args.steps):
             flush.zero_()
