@@ -157,6 +157,44 @@ def test_c2_full_size_sampled():
     assert_close(g["dx"][sample], bw.dXs[0], TOL["bf16"], "dX (sampled)")
 
 
+def test_c5_full_tokens_routing_and_sampled_rows():
+    """configs[4]'s token count and gate (32768 tokens, d = 2048, E = 64, top-2, capacity 1.25)
+    with d_ffn = 256 (the expert FFN shape does not touch routing; full C5 weights in fp64 would
+    not fit the host): routing, slots and counts bit-exact on every token of the bench's
+    gate launch (256 CTAs of 128 tokens, 2 per SM) and y, dX on a
+    sample of tokens computed one by one."""
+    cfg, X, Wg, W1, W2, dY = _case("C5", d_ffn=256)
+    assert cfg.tokens_per_rank == 32768 and cfg.num_experts == 64
+    g = gpu_layer(cfg, 1, X, Wg, W1, W2, dY)
+    L = moe.gate_logits(X, Wg)
+    p = moe.softmax(L)
+    idx = moe.top_k(L, cfg.k)
+    gate = moe.gate_weights(p, idx)
+    slot, counts = moe.capacity_slots(idx, cfg.num_experts, cfg.capacity())
+    assert np.array_equal(g["idx"], idx)
+    assert np.array_equal(g["slot"], slot)
+    assert np.array_equal(g["counts"], counts)
+    assert np.allclose(g["gate"], gate, rtol=2e-6, atol=1e-7)
+    rng = np.random.default_rng(1)
+    T = cfg.tokens_per_rank
+    sample = np.concatenate([[0, 127, 128, 255, 256, T - 1], rng.choice(T - 2, 26, replace=False) + 1])
+    Xs, dYs = X[sample], dY[sample]
+    rf = moe.RankForward(L=L[sample], p=p[sample], idx=idx[sample], gate=gate[sample], slot=slot[sample],
+                         counts=counts, y=np.zeros((len(sample), cfg.d_model)))
+    for n, t in enumerate(sample):
+        for j in range(cfg.k):
+            if slot[t, j] >= 0:
+                e = idx[t, j]
+                h, o = moe.expert_ffn(X[t:t + 1], W1[e], W2[e], "bf16")
+                rf.h[(n, j)] = h[0]
+                rf.o[(n, j)] = o[0]
+    rf.y = moe.combine(rf, cfg.k, "bf16")
+    bw = moe.moe_backward([rf], [Xs], [dYs], Wg, W1, W2, cfg.k, "bf16")
+    from tests.parity_util import assert_close
+    assert_close(g["y"][sample], rf.y, TOL["bf16"], "y (sampled)")
+    assert_close(g["dx"][sample], bw.dXs[0], TOL["bf16"], "dX (sampled)")
+
+
 def test_comm_and_errors():
     import paper_2210_17223_b200 as lina
     comm = lina.Comm(1, 0, 0)
