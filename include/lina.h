@@ -52,7 +52,11 @@
  *     scratch and saved state are caller-allocated, sized by
  *     lina_moe_workspace_size().
  *   - One lina_comm per rank (process/GPU).  Calls on one lina_comm are not
- *     reentrant.  There is NO CPU fallback: on a machine without an sm_100 GPU
+ *     reentrant, and the work of its layer calls must be ordered on one stream
+ *     (its expert GEMMs draw their tiles from one self-resetting device counter
+ *     owned by the comm: the dynamic tile schedule; LINA_GEMM_DYN=0 at
+ *     lina_comm_init selects the static schedule, which has no such state).
+ *     There is NO CPU fallback: on a machine without an sm_100 GPU
  *     lina_comm_init fails with LINA_ERR_UNSUPPORTED.
  */
 #ifndef LINA_H_
