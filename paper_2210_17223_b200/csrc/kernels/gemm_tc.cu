@@ -45,7 +45,6 @@ namespace lina {
 namespace tc {
 
 constexpr int BN = 256, BK = 64;
-constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;  // 2 accumulators x BN
 
 // WIDE: the epilogue-heavy ReLU / ReLU'-mask GEMMs (N = d_ffn outputs per row, short
@@ -170,11 +169,10 @@ __global__ void __launch_bounds__(Geo<CG, WIDE>::THREADS, 1)
   uint64_t* qfull = tempty + 19;
   uint64_t* qempty = qfull + kQ;
   volatile int* tq = (volatile int*)(qempty + kQ);
-  // the i-th tile of this cluster: static, or from the queue (the leader producer fills it)
-  // leader producer: publish ticket t (drawn earlier, in flight during the previous tile's
-  // loads) to the queue of both CTAs
+  // Tile queue of the dynamic schedule.  Leader producer: publish ticket t (drawn a tile
+  // earlier, its atomic in flight during that tile's loads) to the queue of both CTAs
   auto q_publish = [&](int& qi, uint32_t& qph, int t) {
-    mbar_wait(&qempty[qi], qph ^ 1);  // (acquire.cta: an acquire.cluster wait invalidates L1 — the tile decode's cached loads)
+    mbar_wait(&qempty[qi], qph ^ 1);  // (acquire.cta: an acquire.cluster wait would invalidate L1)
     if (lane == 0) {
       tq[qi] = t;
       mbar_arrive_local(&qfull[qi]);
