@@ -208,13 +208,29 @@ class ClockSampler:
 # --------------------------------------------------------------------------- CPU oracle timing
 
 
-def oracle_step_sample(cfg, seed, family, sample_tokens, world):
+def oracle_sample_inputs(cfg, seed, family, sample_tokens):
+    """The gate weight, `sample_tokens` tokens of one rank and the expert weights, fp64, built
+    outside any timing.  The expert weight arrays have all E experts (np.zeros: untouched pages
+    cost no memory) with the experts the sample's tokens select filled in — the layer reads no
+    other expert (C5: 17 GB of fp64 weights for all 64, more than a 62 GB host holds next to
+    the oracle's gradients)."""
+    from oracle import moe
+    sub = li.with_tokens(cfg, sample_tokens)
+    Wg = li.gate_weight(sub, seed, family)
+    X, dY = li.layer_tokens(sub, seed, 0, family)
+    used = sorted(set(int(e) for e in moe.top_k(moe.gate_logits(X, Wg), cfg.k).ravel()))
+    W1 = np.zeros((cfg.num_experts, cfg.d_ffn, cfg.d_model))
+    W2 = np.zeros((cfg.num_experts, cfg.d_model, cfg.d_ffn))
+    for e in used:
+        W1[e], W2[e] = li.expert_weights(sub, seed, e, family)
+    return Wg, W1, W2, X, dY
+
+
+def oracle_step_sample(cfg, seed, family, sample_tokens, world, inputs=None):
     """One oracle fwd+bwd over a bounded sample: `sample_tokens` tokens of one rank, all experts.
     Returns (seconds, tokens)."""
     from oracle import moe
-    sub = li.with_tokens(cfg, sample_tokens)
-    Wg, W1, W2 = li.layer_weights(sub, seed, family)
-    X, dY = li.layer_tokens(sub, seed, 0, family)
+    Wg, W1, W2, X, dY = inputs if inputs is not None else oracle_sample_inputs(cfg, seed, family, sample_tokens)
     C = li.with_tokens(cfg, sample_tokens).capacity()
     t0 = time.perf_counter()
     fw = moe.moe_forward([X], Wg, W1, W2, cfg.k, C, cfg.dtype)
@@ -236,11 +252,16 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = li.CONFIGS[args.config]
+    # the sample's inputs are generated once (C5: up to 17 GB of fp64 expert weights, ~20 s); a
+    # step is the oracle's fwd+bwd over them.  At C5 a step costs ~25-80 s whatever the token
+    # count: the oracle zero-fills and rounds to bf16 the weight gradients of all 64 experts
+    # (2 x 64 x 16.8 M values) — the oracle as it stands is not tuned for this
+    inputs = oracle_sample_inputs(cfg, args.seed, args.family, args.cpu_sample)
     for _ in range(args.warmup):
-        oracle_step_sample(cfg, args.seed, args.family, args.cpu_sample, world)
+        oracle_step_sample(cfg, args.seed, args.family, args.cpu_sample, world, inputs)
     tot, toks = 0.0, 0
     for _ in range(args.steps):
-        s, n = oracle_step_sample(cfg, args.seed, args.family, args.cpu_sample, world)
+        s, n = oracle_step_sample(cfg, args.seed, args.family, args.cpu_sample, world, inputs)
         tot += s
         toks += n
     value = toks / tot
