@@ -4,9 +4,9 @@
 // expert GEMMs are the only dense contraction on the path.
 //
 // One persistent, warp-specialised kernel per (CTA-group, problem, B-major, epilogue):
-//   warp 0      : TMA producer (one elected lane) — A and B tiles into a
+//   warp 0      : TMA producer (one elected lane issues) — A and B tiles into a
 //                 128B-swizzled shared-memory ring, completion on mbarriers;
-//   warp 1      : TMEM allocator + MMA issuer (one elected lane of the leader CTA) —
+//   warp 1      : TMEM allocator + MMA issuer (one elected lane of the leader CTA issues) —
 //                 tcgen05.mma.kind::f16, K=16 per instruction, fp32 accumulators
 //                 in TMEM, double-buffered (2 x 256 columns) so the epilogue of
 //                 tile i overlaps the MMAs of tile i+1;
@@ -28,8 +28,10 @@
 //   WGRAD (backward weight gradients): D_e[M][N] = Σ_segments Σ_rows A_rᵀ B_r with
 //         both operands MN-major views of row buffers; the K loop walks the valid
 //         rows of every (chunk, source) segment of expert e in 64-row blocks.
-// Tiles are handed out statically per cluster over a grid of #SMs CTAs; ROW tiles
-// are enumerated from a per-chunk prefix of valid row blocks (launch_mtile_prefix).
+// Tiles are handed out over a grid of #SMs CTAs, statically per cluster or (long K / many
+// waves) dynamically from a per-communicator ticket counter (TcParams::tile_ctr); ROW tiles
+// are enumerated from a per-chunk prefix of valid row blocks (launch_mtile_prefix).  The
+// producer and MMA warps run warp-converged and issue from one elect.sync lane.
 #include <cuda.h>
 
 #include <stdlib.h>
