@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--copy-streams", type=int, default=1,
+    ap.add_argument("--copy-streams", type=int, default=2,
                     help="e2e: split each step's host<->device copies over this many streams per direction")
     ap.add_argument("--eager", action="store_true", help="launch every kernel from the host (no CUDA graph)")
     ap.add_argument("--cpu-sample", type=int, default=0,
